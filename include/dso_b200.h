@@ -1,0 +1,187 @@
+/*
+ * dso_b200.h — C-ABI of the B200-native DSO hot path (libdso_b200.so).
+ *
+ * The reference (arxiv 2407.13096, /root/reference/proj) has no FFI: its
+ * interface is the C++ API in proj/include/dso/.  Each entry point below
+ * replaces one reference function for a whole batch of GPU kernels; the
+ * replaced interface is cited as  <file>:<line>  (relative to proj/).  The C++
+ * drop-in wrappers with the reference's own signatures and dso::Error
+ * behaviour are in include/dso/batch.hpp; INTEGRATION.md shows the bindings.
+ *
+ * Conventions
+ *   - Plain pointers and sizes only.  Every call returns int32 status:
+ *       0                      ok
+ *       1 + dso::ErrorKind     the reference's error kinds (error.hpp:10-25),
+ *                              e.g. 12 = InvalidArgument, 6 = EtaOutOfRange
+ *       DSO_ERR_CUDA (100)     CUDA runtime failure (mapped to IoError in C++)
+ *     dso_last_error(ctx) returns the message of the last failure on ctx.
+ *   - Device arrays are structure-of-arrays with a leading dimension ld >= n:
+ *     element (row r, kernel k) lives at base[r*ld + k].  A shard [a, b) of a
+ *     larger batch is passed as base + a with the batch's ld — no copy.
+ *       params  float [7][ld]   p0, kappa_pow, gamma, c, t0, alpha, beta
+ *                               (KernelModelParams field order, dvfs_model.hpp:23-31)
+ *       counts  uint32 [126][ld] instr 0..100 | dtype 101..117 | memspace 118..125
+ *                               (category order ptx_features.cpp:18-49)
+ *       dcgm    float [8][ld]   smact smocc tenso drama fp64a fp32a fp16a intac
+ *                               (telemetry.hpp:13-28)
+ *       fused   float [134][ld] FusedFeatures::as_vector order (mlp.cpp:307-314)
+ *     idx = fc_idx * nm + fm_idx (brute_force loop order, optimizer.cpp:99-100).
+ *   - All launches are asynchronous on the context stream; dso_sync() waits.
+ *     Pass DSO_HOST in flags (where offered) for host buffers: the call then
+ *     stages the batch through the device in overlapped chunks and returns
+ *     after the results are back in host memory.
+ *   - One host thread per context at a time (the reference is re-entrant and
+ *     stateless; a context is the per-device state it lacks).
+ */
+#ifndef DSO_B200_H
+#define DSO_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DSO_OK 0
+#define DSO_ERR_CUDA 100
+
+#define DSO_HOST 1u          /* pointers are host memory (pinned for full speed) */
+
+#define DSO_INSTR_SLOTS 101  /* ptx_features.hpp:21 */
+#define DSO_DTYPE_SLOTS 17   /* ptx_features.hpp:22 */
+#define DSO_MEMSPACE_SLOTS 8 /* ptx_features.hpp:23 */
+#define DSO_COUNT_ROWS 126
+#define DSO_FUSED_ROWS 134   /* kFusedFeatureCount, mlp.hpp:15 */
+#define DSO_PARAM_ROWS 7     /* kParamCount, mlp.hpp:16 */
+
+typedef struct dso_ctx dso_ctx;
+
+/* ---- context ------------------------------------------------------------- */
+int32_t dso_ctx_create(int32_t device, dso_ctx** out);
+int32_t dso_ctx_destroy(dso_ctx* ctx);
+/* Use an external cudaStream_t (e.g. torch's current stream); NULL restores
+ * the context's own stream. */
+int32_t dso_ctx_set_stream(dso_ctx* ctx, void* cuda_stream);
+int32_t dso_sync(dso_ctx* ctx);
+const char* dso_last_error(const dso_ctx* ctx);
+/* Name of the dso::ErrorKind a status maps to ("InvalidArgument", ...). */
+const char* dso_status_name(int32_t status);
+/* Number of device kernel launches issued on ctx so far (evidence counter). */
+int64_t dso_launch_count(const dso_ctx* ctx);
+
+/* ---- domain: replaces the DvfsDomain argument + validate(DvfsDomain) ------
+ * optimizer.hpp:14-20, optimizer.cpp:58-88, dvfs_model.hpp:60-70.
+ * dev = [kappa_vf, pmax_w, vmin_v, vmax_v, mhz_per_unit] (dvfs_model.hpp:36-42).
+ * Validates exactly like the reference (same kinds), then uploads the
+ * per-level tables (vc, vc^2*fc, 1/fc; fm, 1/fm) computed in double. */
+int32_t dso_set_domain(dso_ctx* ctx, const double* core_mhz, int32_t nc,
+                       const double* mem_mhz, int32_t nm, const double* dev);
+/* validate(DvfsDomain) alone (host only, no device needed); the message of a
+ * failure is copied into msg (NUL-terminated, at most msg_len bytes). */
+int32_t dso_validate_domain(const double* core_mhz, int32_t nc, const double* mem_mhz,
+                            int32_t nm, const double* dev, char* msg, int32_t msg_len);
+
+/* ---- model: replaces the MlpModel argument + validate(MlpModel) -----------
+ * mlp.hpp:35-42, mlp.cpp:358-375.  weights: per layer l, sizes[l+1] x sizes[l]
+ * row-major, concatenated (model.schema.json order, json_io.cpp:154-160);
+ * biases concatenated; mean/std of size sizes[n_sizes-1], std > 0. */
+int32_t dso_set_model(dso_ctx* ctx, const int32_t* layer_sizes, int32_t n_sizes,
+                      const double* weights, const double* biases,
+                      const double* target_mean, const double* target_std);
+/* Read back the device model (after training) in the same layout. */
+int32_t dso_get_model(dso_ctx* ctx, double* weights, double* biases);
+
+/* ---- host helpers (host C++ inside the library, no device work) ----------- */
+/* init_mlp (mlp.cpp:333-356): Glorot-uniform from Rng(seed), zero biases. */
+int32_t dso_init_mlp(const int32_t* layer_sizes, int32_t n_sizes, uint64_t seed,
+                     double* weights, double* biases);
+/* shuffled_indices (rng.hpp:58-64) from Rng(seed) state; advances *state. */
+int32_t dso_shuffled_indices(uint64_t n, uint64_t* rng_state, uint64_t* out);
+
+/* ---- feature stage ---------------------------------------------------------
+ * featurize (ptx_features.cpp:311-329) + FusedFeatures::as_vector
+ * (mlp.cpp:307-314): per category count/total (all-zero for a zero total),
+ * fused with the already-averaged DCGM vector.  Results equal the reference's
+ * double features rounded once to float. */
+int32_t dso_featurize(dso_ctx* ctx, const uint32_t* counts, const float* dcgm, int64_t n,
+                      int64_t ld, float* fused);
+
+/* load_dcgm_samples mean (telemetry.cpp:73-89) over parsed rows:
+ * samples double [rows][8][ld] -> out float [8][ld].  bad_row[k] = first
+ * 1-based row with a value outside [0,1] (0 if none); status OutOfRange if any. */
+int32_t dso_dcgm_mean(dso_ctx* ctx, const double* samples, int64_t rows, int64_t n,
+                      int64_t ld, float* out, int64_t* bad_row);
+
+/* ---- predictor inference ---------------------------------------------------
+ * predict_params (mlp.cpp:386-402) = forward_raw (mlp.cpp:381-384) + clamp:
+ * negative outputs -> 0, alpha+beta <= 0 -> beta = 1e-12; clamped[k] flags it.
+ * raw (optional, float [7][ld]) receives forward_raw before clamping. */
+int32_t dso_predict(dso_ctx* ctx, const float* fused, int64_t n, int64_t ld, float* params,
+                    uint8_t* clamped, float* raw);
+
+/* ---- grid sweep + eta objective + argmin ------------------------------------
+ * brute_force_config (optimizer.cpp:90-117) for n kernels at one eta.
+ * FP32 evaluation with tables precomputed in double; outputs at the chosen
+ * pair.  kstatus[k] = 0 or 1+InvalidArgument (validate(params),
+ * dvfs_model.hpp:50-58) with idx -1 and NaN outputs.  Returns EtaOutOfRange
+ * for eta outside [0,1] (dvfs_model.hpp:101-102). */
+int32_t dso_sweep(dso_ctx* ctx, const float* params, int64_t n, int64_t ld, double eta,
+                  double pmax_w, int32_t* idx, float* cost, float* energy, float* time,
+                  int32_t* kstatus);
+
+/* Bit-exact variant on the reference's own layout: params is
+ * KernelModelParams[n] (7 doubles each, dvfs_model.hpp:23-31); evaluation in
+ * FP64 in the reference's operation order, so idx/cost/energy/time equal
+ * brute_force_config's exactly. */
+int32_t dso_sweep_f64(dso_ctx* ctx, const double* params_aos, int64_t n, double eta,
+                      double pmax_w, int32_t* idx, double* cost, double* energy,
+                      double* time, int32_t* kstatus, uint32_t flags);
+
+/* eta sweep: brute_force_config at n_eta etas in one pass over the grid.
+ * idx/cost are [n_eta][ld_out]. */
+int32_t dso_eta_sweep(dso_ctx* ctx, const float* params, int64_t n, int64_t ld,
+                      const double* etas, int32_t n_eta, double pmax_w, int32_t* idx,
+                      float* cost, int64_t ld_out);
+
+/* ---- fused pipeline: counts + DCGM -> features -> MLP -> sweep -> argmin ----
+ * One persistent kernel; nothing intermediate touches HBM.  params/clamped
+ * optional (NULL).  flags: DSO_HOST for host buffers (chunked, overlapped
+ * H2D / compute / D2H). */
+int32_t dso_pipeline(dso_ctx* ctx, const uint32_t* counts, const float* dcgm, int64_t n,
+                     int64_t ld, double eta, double pmax_w, float* params, uint8_t* clamped,
+                     int32_t* idx, float* cost, float* energy, float* time, uint32_t flags);
+
+/* ---- synthetic inputs (sim_harness.cpp:118-144 gen_kernel, on device) -------
+ * Kernel k (0 <= k < n) is gen_kernel(Rng(root).fork(salt_base+first+k)
+ * .next_u64()), as run_campaign seeds its corpus (sim_harness.cpp:241-242).
+ * Outputs optional: truth params (float [7][ld]), raw PTX counts, DCGM vector.
+ * Bit-identical to the host generator (counts exact, params/dcgm = double
+ * values rounded once to float). */
+int32_t dso_gen_synthetic(dso_ctx* ctx, uint64_t root, uint64_t salt_base, int64_t first,
+                          int64_t n, int64_t ld, float* params, uint32_t* counts,
+                          float* dcgm);
+
+/* ---- predictor training (data-parallel) ------------------------------------
+ * Mini-batch gradient of mse_loss (mlp.cpp:408-438) on the device model.
+ * x float [in][ld] (fused features), y_std float [out][ld] (standardized
+ * targets).  grad (device, weights then biases, same layout as dso_set_model)
+ * receives the SUM over the batch of per-sample gradients of
+ * 0.5*||out-y||^2 (i.e. analytic_gradients times B*out); loss_sum receives
+ * sum ||out-y||^2 * 0.5.  Scaling by 1/(B_global*out) happens in apply, so a
+ * data-parallel step is: grad -> allreduce(sum) -> apply. */
+int32_t dso_train_grad(dso_ctx* ctx, const float* x, const float* y_std, int64_t n,
+                       int64_t ld, float* grad, double* loss_sum);
+/* W -= lr * scale * grad  (sgd update, mlp.cpp:254-257). */
+int32_t dso_train_apply(dso_ctx* ctx, const float* grad, double lr, double scale);
+/* Number of parameters (weights + biases) of the device model. */
+int64_t dso_model_param_count(const dso_ctx* ctx);
+
+/* ---- diagnostics --------------------------------------------------------------
+ * Measured FP32 FMA-pipe peak of this device (the roofline denominator of the
+ * FP32-bound kernels): mode 0 = scalar FFMA, 1 = packed FFMA2.  TFLOP/s. */
+int32_t dso_probe_fp32_peak(dso_ctx* ctx, int32_t mode, double* tflops);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DSO_B200_H */

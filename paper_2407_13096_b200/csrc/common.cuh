@@ -1,0 +1,157 @@
+// common.cuh — shared definitions for the sm_100a DSO kernels and the C-ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/dso_b200.h"
+
+namespace dso_b200 {
+
+// 1 + dso::ErrorKind (reference proj/include/dso/error.hpp:10-25)
+enum Status : int32_t {
+    kOk = 0,
+    kMalformedPtx = 1,
+    kEmptyTrace = 2,
+    kOutOfRange = 3,
+    kSchemaMismatch = 4,
+    kNonPositivePower = 5,
+    kEtaOutOfRange = 6,
+    kVoltageBelowKappa = 7,
+    kFrequencyBelowKappa = 8,
+    kRankDeficient = 9,
+    kUnderdetermined = 10,
+    kDatasetTooSmall = 11,
+    kInvalidArgument = 12,
+    kInvalidModel = 13,
+    kIoError = 14,
+    kCuda = DSO_ERR_CUDA,
+};
+
+constexpr int kMaxCore = 1024;  // core levels per domain (sweep tables live in smem)
+constexpr int kMaxMem = 64;
+
+// Per-domain tables, precomputed in double on the host (abi.cu) exactly as
+// the reference computes them per evaluation (optimizer.cpp:36,
+// dvfs_model.hpp:117-128), then stored in both precisions.
+struct DomainDev {
+    int nc, nm;
+    // f32 path: per core level {vc, vc*vc*fc, 1/fc, fc}; per mem level {fm, 1/fm}
+    float4* core4;   // [nc]
+    float2* mem2;    // [nm]
+    // f64 exact path: per core level {vc, fc}; per mem level fm
+    double2* core_d;  // [nc]
+    double* mem_d;    // [nm]
+};
+
+// Device model: transposed, zero-padded weights for the FP32 MLP kernels.
+// Only the default topology 134-100-50-25-7 (mlp.cpp:326) runs on the fused
+// kernels; other topologies are rejected by dso_set_model with InvalidModel
+// for the device path (the reference trains probe nets only in unit tests).
+struct ModelDev {
+    int sizes[5];
+    float* wt;       // packed per-layer transposed weights (see mlp.cu layout)
+    float* bias;     // packed biases (padded)
+    float mean[8], std_[8];
+    int64_t wt_floats, bias_floats;
+    // master copy in the reference layout (row-major W, concatenated), f32
+    float* w_master;  // [n_weights + n_biases]
+    int64_t n_weights, n_biases;
+};
+
+struct Ctx {
+    int device = 0;
+    cudaStream_t own_stream = nullptr;
+    cudaStream_t stream = nullptr;
+    std::string last_error;
+    int64_t launches = 0;
+    bool has_domain = false;
+    bool has_model = false;
+    DomainDev dom{};
+    double dom_core[kMaxCore];
+    double dom_mem[kMaxMem];
+    double dom_dev[5];
+    ModelDev model{};
+    // staging for DSO_HOST calls and scratch
+    void* scratch = nullptr;
+    size_t scratch_bytes = 0;
+    cudaStream_t aux[3] = {nullptr, nullptr, nullptr};
+    cudaEvent_t ev[8] = {};
+    int num_sms = 148;
+};
+
+}  // namespace dso_b200
+
+// The opaque handle of the C-ABI.
+struct dso_ctx {
+    dso_b200::Ctx c;
+};
+
+namespace dso_b200 {
+
+// ---- launchers (defined in the kernel .cu files) ------------------------------
+cudaError_t launch_sweep_f32(Ctx& c, const float* params, int64_t n, int64_t ld, float eta,
+                             float K, int32_t* idx, float* cost, float* energy, float* time,
+                             int32_t* kstatus);
+cudaError_t launch_sweep_f64(Ctx& c, const double* params, int64_t n, double eta, double K,
+                             int32_t* idx, double* cost, double* energy, double* time,
+                             int32_t* kstatus);
+cudaError_t launch_eta_sweep(Ctx& c, const float* params, int64_t n, int64_t ld,
+                             const float2* etaK_dev, int n_eta, int32_t* idx, float* cost,
+                             int64_t ld_out);
+cudaError_t launch_gen(Ctx& c, uint64_t root, uint64_t salt_base, int64_t first, int64_t n,
+                       int64_t ld, float* params, uint32_t* counts, float* dcgm);
+cudaError_t launch_featurize(Ctx& c, const uint32_t* counts, const float* dcgm, int64_t n,
+                             int64_t ld, float* fused);
+cudaError_t launch_dcgm_mean(Ctx& c, const double* samples, int64_t rows, int64_t n,
+                             int64_t ld, float* out, int64_t* bad_row, int* any_bad_dev);
+cudaError_t launch_predict(Ctx& c, const float* fused, int64_t n, int64_t ld, float* params,
+                           uint8_t* clamped, float* raw);
+cudaError_t launch_pipeline(Ctx& c, const uint32_t* counts, const float* dcgm, int64_t n,
+                            int64_t ld, float eta, float K, float* params, uint8_t* clamped,
+                            int32_t* idx, float* cost, float* energy, float* time,
+                            int64_t ld_out);
+cudaError_t model_upload(Ctx& c, const double* W, const double* b);
+cudaError_t launch_train_grad(Ctx& c, const float* x, const float* y, int64_t n, int64_t ld,
+                              float* grad, double* loss_sum_dev);
+cudaError_t launch_train_apply(Ctx& c, const float* grad, float lr_scale);
+size_t mlp_smem_bytes();
+
+// ---- device helpers ---------------------------------------------------------
+// Packed FP32x2 FMA (Blackwell FFMA2): d = a * b + c lane-wise.  A scalar
+// broadcast a is expressed as {a, a}; ptxas folds it to the .F32 operand form.
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+    unsigned long long A, B, Cc, D;
+    A = *reinterpret_cast<unsigned long long*>(&a);
+    B = *reinterpret_cast<unsigned long long*>(&b);
+    Cc = *reinterpret_cast<unsigned long long*>(&c);
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(D) : "l"(A), "l"(B), "l"(Cc));
+    return *reinterpret_cast<float2*>(&D);
+}
+
+// FP32 pair evaluation shared by every sweep kernel (sweep, eta sweep, fused
+// pipeline) so all of them round identically.  Explicit _rn intrinsics stop
+// nvcc from re-contracting the expressions differently per kernel.
+//   Pc = p0 + kp*vc + c*(vc^2 fc)         (per core level; t = {vc, vc^2 fc, 1/fc, fc})
+//   P  = Pc + g*fm,  T = t0 + max(a/fm, b/fc),  C = (eta*P + (1-eta)*pmax) * T
+__device__ __forceinline__ float pc_f32(float p0, float kp, float c, float4 t) {
+    return fmaf(c, t.y, fmaf(kp, t.x, p0));
+}
+__device__ __forceinline__ float time_f32(float t0, float ta, float tb) {
+    return __fadd_rn(t0, fmaxf(ta, tb));
+}
+__device__ __forceinline__ float cost_f32(float eta, float K, float P, float T) {
+    return __fmul_rn(fmaf(eta, P, K), T);
+}
+
+inline int grid_for(int64_t n, int block, int num_sms, int per_sm) {
+    int64_t blocks = (n + block - 1) / block;
+    int64_t cap = (int64_t)num_sms * per_sm;
+    if (blocks > cap) blocks = cap;
+    if (blocks < 1) blocks = 1;
+    return (int)blocks;
+}
+
+}  // namespace dso_b200

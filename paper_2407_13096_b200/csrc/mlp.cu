@@ -1,0 +1,604 @@
+// mlp.cu — predictor inference and the fused pipeline (sm_100a).
+//
+// Predictor: the reference MLP 134-100-50-25-7 (proj/src/mlp.cpp:326), sigmoid
+// hidden layers, identity output (forward_trace mlp.cpp:171-181), output
+// de-standardised (forward_raw mlp.cpp:381-384) and clamped (predict_params
+// mlp.cpp:386-402, kBetaFloor mlp.cpp:15).
+//
+// Execution model (one persistent CTA per SM, 256 threads, ~165 KB smem):
+//   * the whole model (19,825 weights + biases) is staged ONCE per CTA into
+//     shared memory, transposed (k-major) and zero-padded per thread group;
+//   * a tile of 128 kernels lives in one k-major activation buffer
+//     act[134][128] (68.6 KB); every layer reads it, keeps its outputs in
+//     registers, syncs, and writes them back in place — nothing between the
+//     input load and the final result touches HBM;
+//   * layers are register-tiled FP32 GEMMs on the FMA pipe using Blackwell's
+//     packed FFMA2 (fma.rn.f32x2 — two FMAs per lane per instruction, with a
+//     scalar-broadcast operand so no duplication MOVs are needed):
+//       L1 134->100 : thread = 2 kernels x 26 neurons (pairs along n)
+//       L2 100->50  : thread = 2 kernels x 13 neurons (pairs along m)
+//       L3  50->25  : thread = 2 kernels x  7 neurons (pairs along m)
+//       L4  25->7   : thread = 2 kernels x  2 neurons (pairs along m)
+//     A warp shares its neuron group, so every weight load is a shared-memory
+//     broadcast; activation loads are 256 B contiguous per warp.
+//   Tensor cores are not used: TF32/BF16 cannot meet the 1e-5 relative
+//   contract on the predicted parameters.
+//
+// The fused pipeline kernel adds the feature stage in front (raw PTX counts ->
+// per-category fractions, fused with DCGM, straight into act) and the grid
+// sweep + eta objective + argmin behind (2 threads per kernel, each half the
+// core levels, merged with one shuffle), so a kernel's 536 input bytes become
+// its 16 result bytes without any intermediate HBM traffic.
+#include <math.h>
+
+#include <vector>
+
+#include "common.cuh"
+
+namespace dso_b200 {
+
+namespace {
+
+constexpr int kTile = 128;     // kernels per CTA tile
+constexpr int kThreads = 256;  // 8 warps
+
+// Packed (transposed, padded) weight layout in floats.  See model_upload.
+constexpr int kW1Stride = 112;  // 4 groups x 28 (26 used)
+constexpr int kW2Stride = 64;   // 4 groups x 16 (13 used)
+constexpr int kW3Stride = 32;   // 4 groups x 8  (7 used)
+constexpr int kW4Stride = 8;    // 7 used
+constexpr int kOffW1 = 0;
+constexpr int kOffW2 = kOffW1 + 134 * kW1Stride;  // 15008
+constexpr int kOffW3 = kOffW2 + 100 * kW2Stride;  // 21408
+constexpr int kOffW4 = kOffW3 + 50 * kW3Stride;   // 23008
+constexpr int kOffB1 = kOffW4 + 25 * kW4Stride;   // 23208
+constexpr int kOffB2 = kOffB1 + 104;
+constexpr int kOffB3 = kOffB2 + 52;
+constexpr int kOffB4 = kOffB3 + 28;
+constexpr int kModelFloats = kOffB4 + 8;          // 23400
+constexpr int kOffAct = kModelFloats;              // act[134][128]
+constexpr int kActFloats = 134 * kTile;
+constexpr int kOffOut = kOffAct + kActFloats;      // out[8][128] + stats
+constexpr int kOutFloats = 8 * kTile;
+constexpr int kOffStats = kOffOut + kOutFloats;    // mean[8], std[8], eta, K
+constexpr int kStatsFloats = 32;
+constexpr int kOffTables = kOffStats + kStatsFloats;  // core4[nc], mem2[nm] (pipeline)
+constexpr int kBaseFloats = kOffTables;
+
+static_assert(kOffW2 % 4 == 0 && kOffW3 % 4 == 0 && kOffW4 % 4 == 0 && kOffB1 % 4 == 0 &&
+                  kModelFloats % 4 == 0 && kOffOut % 4 == 0 && kOffTables % 4 == 0,
+              "16-byte alignment of smem regions");
+
+__device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
+
+// sigmoid (mlp.cpp:166-168) in FP32: 1 / (1 + e^-z) via ex2 + rcp.
+__device__ __forceinline__ float sigmoidf_fast(float z) {
+    return __fdividef(1.0f, 1.0f + __expf(-z));
+}
+
+// ---------------------------------------------------------------------------
+// Stage the packed model into shared memory (once per CTA).
+__device__ __forceinline__ void stage_model(float* smem, const float* __restrict__ packed) {
+    const float4* src = reinterpret_cast<const float4*>(packed);
+    float4* dst = reinterpret_cast<float4*>(smem);
+    for (int i = threadIdx.x; i < kModelFloats / 4; i += kThreads) dst[i] = __ldg(src + i);
+}
+
+// ---------------------------------------------------------------------------
+// The four layers on act[134][128] (k-major, kernels contiguous).
+// Precondition: act rows 0..133 hold the tile's fused features; __syncthreads
+// done.  Postcondition: out[n][m] (n < 7) holds forward_raw outputs
+// (de-standardised, NOT clamped); __syncthreads done.
+__device__ __forceinline__ void mlp_tile(float* smem) {
+    const float* W = smem;
+    float* act = smem + kOffAct;
+    float2* act2 = reinterpret_cast<float2*>(act);  // [row][64] pairs of kernels
+    const int tid = threadIdx.x;
+    const int mp = tid & 63;  // kernel pair: kernels 2mp, 2mp+1
+    const int g = tid >> 6;   // neuron group (uniform per warp)
+
+    // ---- L1: 134 -> 100 (neurons 26g .. 26g+25), pairs along n -------------
+    {
+        float2 acc0[13], acc1[13];
+#pragma unroll
+        for (int p = 0; p < 13; ++p) acc0[p] = acc1[p] = f2(0.f, 0.f);
+        const float* wbase = W + kOffW1 + g * 28;
+#pragma unroll 2
+        for (int k = 0; k < 134; ++k) {
+            const float2 a = act2[k * 64 + mp];
+            const float4* w4 = reinterpret_cast<const float4*>(wbase + k * kW1Stride);
+            float2 w[13];
+#pragma unroll
+            for (int q = 0; q < 6; ++q) {
+                const float4 v = w4[q];
+                w[2 * q] = f2(v.x, v.y);
+                w[2 * q + 1] = f2(v.z, v.w);
+            }
+            w[12] = reinterpret_cast<const float2*>(w4)[12];
+#pragma unroll
+            for (int p = 0; p < 13; ++p) {
+                acc0[p] = ffma2(f2(a.x, a.x), w[p], acc0[p]);
+                acc1[p] = ffma2(f2(a.y, a.y), w[p], acc1[p]);
+            }
+        }
+        __syncthreads();  // all reads of act done
+        const float* b = W + kOffB1 + g * 26;
+#pragma unroll
+        for (int p = 0; p < 13; ++p) {
+            const int n = g * 26 + 2 * p;
+            const float b0 = b[2 * p], b1 = b[2 * p + 1];
+            act2[n * 64 + mp] = f2(sigmoidf_fast(acc0[p].x + b0), sigmoidf_fast(acc1[p].x + b0));
+            act2[(n + 1) * 64 + mp] =
+                f2(sigmoidf_fast(acc0[p].y + b1), sigmoidf_fast(acc1[p].y + b1));
+        }
+        __syncthreads();
+    }
+    // ---- L2: 100 -> 50 (neurons 13g .. 13g+12), pairs along m ----------------
+    {
+        float2 acc[13];
+#pragma unroll
+        for (int t = 0; t < 13; ++t) acc[t] = f2(0.f, 0.f);
+        const float* wbase = W + kOffW2 + g * 16;
+#pragma unroll 2
+        for (int k = 0; k < 100; ++k) {
+            const float2 a = act2[k * 64 + mp];
+            const float4* w4 = reinterpret_cast<const float4*>(wbase + k * kW2Stride);
+            const float4 v0 = w4[0], v1 = w4[1], v2 = w4[2];
+            const float v3 = reinterpret_cast<const float*>(w4)[12];
+            const float w[13] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z,
+                                 v1.w, v2.x, v2.y, v2.z, v2.w, v3};
+#pragma unroll
+            for (int t = 0; t < 13; ++t) acc[t] = ffma2(a, f2(w[t], w[t]), acc[t]);
+        }
+        __syncthreads();
+        const float* b = W + kOffB2 + g * 13;
+#pragma unroll
+        for (int t = 0; t < 13; ++t) {
+            const float bb = b[t];
+            act2[(g * 13 + t) * 64 + mp] =
+                f2(sigmoidf_fast(acc[t].x + bb), sigmoidf_fast(acc[t].y + bb));
+        }
+        __syncthreads();
+    }
+    // ---- L3: 50 -> 25 (neurons 7g .. 7g+6), pairs along m ---------------------
+    {
+        float2 acc[7];
+#pragma unroll
+        for (int t = 0; t < 7; ++t) acc[t] = f2(0.f, 0.f);
+        const float* wbase = W + kOffW3 + g * 8;
+#pragma unroll 2
+        for (int k = 0; k < 50; ++k) {
+            const float2 a = act2[k * 64 + mp];
+            const float4* w4 = reinterpret_cast<const float4*>(wbase + k * kW3Stride);
+            const float4 v0 = w4[0], v1 = w4[1];
+            const float w[7] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z};
+#pragma unroll
+            for (int t = 0; t < 7; ++t) acc[t] = ffma2(a, f2(w[t], w[t]), acc[t]);
+        }
+        __syncthreads();
+        const float* b = W + kOffB3 + g * 7;
+#pragma unroll
+        for (int t = 0; t < 7; ++t) {
+            const float bb = b[t];
+            act2[(g * 7 + t) * 64 + mp] =
+                f2(sigmoidf_fast(acc[t].x + bb), sigmoidf_fast(acc[t].y + bb));
+        }
+        __syncthreads();
+    }
+    // ---- L4: 25 -> 7 (neurons 2g, 2g+1), identity, de-standardise -------------
+    {
+        float2 acc[2] = {f2(0.f, 0.f), f2(0.f, 0.f)};
+        const float* wbase = W + kOffW4 + g * 2;
+#pragma unroll 5
+        for (int k = 0; k < 25; ++k) {
+            const float2 a = act2[k * 64 + mp];
+            const float2 w = *reinterpret_cast<const float2*>(wbase + k * kW4Stride);
+            acc[0] = ffma2(a, f2(w.x, w.x), acc[0]);
+            acc[1] = ffma2(a, f2(w.y, w.y), acc[1]);
+        }
+        const float* st = smem + kOffStats;  // mean[0..7], std[8..15]
+        float2* out2 = reinterpret_cast<float2*>(smem + kOffOut);
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+            const int n = 2 * g + t;
+            if (n < 7) {
+                const float bb = W[kOffB4 + n];
+                const float s = st[8 + n], mu = st[n];
+                // forward_raw: (z * std) + mean, z = (W a) + b
+                out2[n * 64 + mp] = f2(fmaf(acc[t].x + bb, s, mu), fmaf(acc[t].y + bb, s, mu));
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// predict_params clamp (mlp.cpp:390-399) on out[.][m]; returns clamped flag.
+__device__ __forceinline__ bool clamp_params(float p[7]) {
+    bool cl = false;
+#pragma unroll
+    for (int i = 0; i < 7; ++i)
+        if (p[i] < 0.f) {
+            p[i] = 0.f;
+            cl = true;
+        }
+    if (p[5] + p[6] <= 0.f) {
+        p[6] = 1e-12f;
+        cl = true;
+    }
+    return cl;
+}
+
+// ---------------------------------------------------------------------------
+// Feature stage into act: raw counts [126][ld] + DCGM [8][ld] for kernels
+// [t0, t0+128) -> act rows 0..133 (fused order).  Kernels >= n get zeros.
+__device__ __forceinline__ void load_features_from_counts(float* smem,
+                                                          const uint32_t* __restrict__ counts,
+                                                          const float* __restrict__ dcgm,
+                                                          int64_t t0, int64_t n, int64_t ld) {
+    float* act = smem + kOffAct;
+    uint32_t* acti = reinterpret_cast<uint32_t*>(act);
+    const int tid = threadIdx.x;
+    const int m = tid & (kTile - 1);
+    const int h = tid >> 7;  // 0/1
+    const int64_t k = t0 + m;
+    const bool live = k < n;
+    // phase 1: raw counts -> act rows 8.. as integer bits; DCGM -> rows 0..7
+    if (live) {
+#pragma unroll 9
+        for (int r = h; r < DSO_COUNT_ROWS; r += 2)
+            acti[(8 + r) * kTile + m] = __ldg(counts + (int64_t)r * ld + k);
+#pragma unroll
+        for (int r = h; r < 8; r += 2) act[r * kTile + m] = __ldg(dcgm + (int64_t)r * ld + k);
+    } else {
+        for (int r = h; r < DSO_COUNT_ROWS; r += 2) acti[(8 + r) * kTile + m] = 0u;
+        for (int r = h; r < 8; r += 2) act[r * kTile + m] = 0.f;
+    }
+    __syncthreads();
+    // phase 2: category totals (h=0: instr; h=1: dtype + memspace)
+    float* tot = smem + kOffOut;  // scratch [3][128] totals as (float total, float recip)
+    uint32_t* toti = reinterpret_cast<uint32_t*>(tot);
+    if (h == 0) {
+        uint64_t s = 0;
+        for (int r = 0; r < DSO_INSTR_SLOTS; ++r) s += acti[(8 + r) * kTile + m];
+        toti[0 * kTile + m] = s >= (1u << 24) ? 0xffffffffu : (uint32_t)s;
+    } else {
+        uint64_t s1 = 0, s2 = 0;
+        for (int r = 0; r < DSO_DTYPE_SLOTS; ++r)
+            s1 += acti[(8 + DSO_INSTR_SLOTS + r) * kTile + m];
+        for (int r = 0; r < DSO_MEMSPACE_SLOTS; ++r)
+            s2 += acti[(8 + DSO_INSTR_SLOTS + DSO_DTYPE_SLOTS + r) * kTile + m];
+        toti[1 * kTile + m] = s1 >= (1u << 24) ? 0xffffffffu : (uint32_t)s1;
+        toti[2 * kTile + m] = s2 >= (1u << 24) ? 0xffffffffu : (uint32_t)s2;
+    }
+    __syncthreads();
+    // phase 3: normalise in place.  Totals >= 2^24 (never produced by real PTX
+    // or the generator) recompute in FP64 from the exact integer sum.
+    for (int r = h; r < DSO_COUNT_ROWS; r += 2) {
+        const int cat = r < DSO_INSTR_SLOTS ? 0 : (r < DSO_INSTR_SLOTS + DSO_DTYPE_SLOTS ? 1 : 2);
+        const uint32_t t = toti[cat * kTile + m];
+        const uint32_t c = acti[(8 + r) * kTile + m];
+        float v;
+        if (t == 0u) {
+            v = 0.f;
+        } else if (t != 0xffffffffu) {
+            const float tf = __uint2float_rn(t), cf = __uint2float_rn(c);
+            const float rr = __frcp_rn(tf);
+            const float q = __fmul_rn(cf, rr);
+            v = fmaf(fmaf(-q, tf, cf), rr, q);
+        } else {
+            const int base = cat == 0 ? 0 : (cat == 1 ? DSO_INSTR_SLOTS : DSO_INSTR_SLOTS + DSO_DTYPE_SLOTS);
+            const int len = cat == 0 ? DSO_INSTR_SLOTS : (cat == 1 ? DSO_DTYPE_SLOTS : DSO_MEMSPACE_SLOTS);
+            uint64_t s = 0;
+            for (int i = 0; i < len; ++i) s += acti[(8 + base + i) * kTile + m];
+            v = (float)((double)c / (double)s);
+        }
+        act[(8 + r) * kTile + m] = v;
+    }
+    __syncthreads();
+}
+
+// Fused features already in HBM ([134][ld] float) -> act.
+__device__ __forceinline__ void load_features_fused(float* smem, const float* __restrict__ fused,
+                                                    int64_t t0, int64_t n, int64_t ld) {
+    float* act = smem + kOffAct;
+    const int tid = threadIdx.x;
+    const int m = tid & (kTile - 1);
+    const int h = tid >> 7;
+    const int64_t k = t0 + m;
+    const bool live = k < n;
+#pragma unroll 7
+    for (int r = h; r < DSO_FUSED_ROWS; r += 2)
+        act[r * kTile + m] = live ? __ldg(fused + (int64_t)r * ld + k) : 0.f;
+    __syncthreads();
+}
+
+__device__ __forceinline__ void stage_stats(float* smem, const float* mean, const float* std_) {
+    if (threadIdx.x < 8) {
+        smem[kOffStats + threadIdx.x] = mean[threadIdx.x];
+        smem[kOffStats + 8 + threadIdx.x] = std_[threadIdx.x];
+    }
+}
+
+struct Stats {
+    float mean[8];
+    float std_[8];
+};
+
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads, 1) predict_kernel(
+    const float* __restrict__ packed, Stats stats, const float* __restrict__ fused, int64_t n,
+    int64_t ld, float* __restrict__ params, uint8_t* __restrict__ clamped,
+    float* __restrict__ raw) {
+    extern __shared__ __align__(16) float smem[];
+    stage_model(smem, packed);
+    stage_stats(smem, stats.mean, stats.std_);
+    __syncthreads();
+    const int64_t tiles = (n + kTile - 1) / kTile;
+    for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+        const int64_t t0 = tile * kTile;
+        load_features_fused(smem, fused, t0, n, ld);
+        mlp_tile(smem);
+        if (threadIdx.x < kTile) {
+            const int m = threadIdx.x;
+            const int64_t k = t0 + m;
+            if (k < n) {
+                const float* out = smem + kOffOut;
+                float p[7];
+#pragma unroll
+                for (int i = 0; i < 7; ++i) p[i] = out[i * kTile + m];
+                if (raw)
+#pragma unroll
+                    for (int i = 0; i < 7; ++i) raw[i * ld + k] = p[i];
+                const bool cl = clamp_params(p);
+#pragma unroll
+                for (int i = 0; i < 7; ++i) params[i * ld + k] = p[i];
+                if (clamped) clamped[k] = cl ? 1 : 0;
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Fused pipeline: counts + DCGM -> features -> MLP -> clamp -> sweep -> argmin.
+__global__ void __launch_bounds__(kThreads, 1) pipeline_kernel(
+    const float* __restrict__ packed, Stats stats, const float4* __restrict__ core4, int nc,
+    const float2* __restrict__ mem2, int nm, float eta, float K,
+    const uint32_t* __restrict__ counts, const float* __restrict__ dcgm, int64_t n, int64_t ld,
+    float* __restrict__ params_out, uint8_t* __restrict__ clamped_out,
+    int32_t* __restrict__ idx_out, float* __restrict__ cost_out, float* __restrict__ energy_out,
+    float* __restrict__ time_out, int64_t ld_out) {
+    extern __shared__ __align__(16) float smem[];
+    stage_model(smem, packed);
+    stage_stats(smem, stats.mean, stats.std_);
+    float4* s_core = reinterpret_cast<float4*>(smem + kOffTables);
+    float2* s_mem = reinterpret_cast<float2*>(smem + kOffTables + 4 * nc);
+    for (int i = threadIdx.x; i < nc; i += kThreads) s_core[i] = core4[i];
+    for (int j = threadIdx.x; j < nm; j += kThreads) s_mem[j] = mem2[j];
+    __syncthreads();
+
+    const int64_t tiles = (n + kTile - 1) / kTile;
+    const int tid = threadIdx.x;
+    const int m = tid >> 1;    // kernel within tile (2 threads per kernel)
+    const int half = tid & 1;  // which half of the core levels
+    const int i_split = (nc + 1) >> 1;
+    const int i_lo = half ? i_split : 0;
+    const int i_hi = half ? nc : i_split;
+
+    for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+        const int64_t t0 = tile * kTile;
+        load_features_from_counts(smem, counts, dcgm, t0, n, ld);
+        mlp_tile(smem);
+
+        // ---- clamp + sweep + argmin: 2 threads per kernel --------------------
+        const int64_t k = t0 + m;
+        const float* out = smem + kOffOut;
+        float p[7];
+#pragma unroll
+        for (int i = 0; i < 7; ++i) p[i] = out[i * kTile + m];
+        const bool cl = clamp_params(p);
+        const float p0 = p[0], kp = p[1], g = p[2], c = p[3], tt0 = p[4], a = p[5], b = p[6];
+
+        float bc = __int_as_float(0x7fc00000), be = bc;
+        int bi = i_lo * nm;
+        if (i_lo < i_hi) {
+            {  // first candidate of this half taken unconditionally
+                const float4 t = s_core[i_lo];
+                const float P = __fadd_rn(pc_f32(p0, kp, c, t), __fmul_rn(g, s_mem[0].x));
+                const float T = time_f32(tt0, __fmul_rn(a, s_mem[0].y), __fmul_rn(b, t.z));
+                bc = cost_f32(eta, K, P, T);
+                be = __fmul_rn(P, T);
+            }
+            if (nm == 4) {
+                float G[4], Ta[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    G[j] = __fmul_rn(g, s_mem[j].x);
+                    Ta[j] = __fmul_rn(a, s_mem[j].y);
+                }
+#pragma unroll 2
+                for (int i = i_lo; i < i_hi; ++i) {
+                    const float4 t = s_core[i];
+                    const float Pc = pc_f32(p0, kp, c, t);
+                    const float Tb = __fmul_rn(b, t.z);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const float P = __fadd_rn(Pc, G[j]);
+                        const float T = time_f32(tt0, Ta[j], Tb);
+                        const float C = cost_f32(eta, K, P, T);
+                        const float E = __fmul_rn(P, T);
+                        const bool better = (C < bc) | ((C == bc) & (E < be));
+                        bc = better ? C : bc;
+                        be = better ? E : be;
+                        bi = better ? i * 4 + j : bi;
+                    }
+                }
+            } else if (nm == 1) {
+                const float G0 = __fmul_rn(g, s_mem[0].x), Ta0 = __fmul_rn(a, s_mem[0].y);
+#pragma unroll 4
+                for (int i = i_lo; i < i_hi; ++i) {
+                    const float4 t = s_core[i];
+                    const float P = __fadd_rn(pc_f32(p0, kp, c, t), G0);
+                    const float T = time_f32(tt0, Ta0, __fmul_rn(b, t.z));
+                    const float C = cost_f32(eta, K, P, T);
+                    const float E = __fmul_rn(P, T);
+                    const bool better = (C < bc) | ((C == bc) & (E < be));
+                    bc = better ? C : bc;
+                    be = better ? E : be;
+                    bi = better ? i : bi;
+                }
+            } else {
+                for (int i = i_lo; i < i_hi; ++i) {
+                    const float4 t = s_core[i];
+                    const float Pc = pc_f32(p0, kp, c, t);
+                    const float Tb = __fmul_rn(b, t.z);
+                    for (int j = 0; j < nm; ++j) {
+                        const float P = __fadd_rn(Pc, __fmul_rn(g, s_mem[j].x));
+                        const float T = time_f32(tt0, __fmul_rn(a, s_mem[j].y), Tb);
+                        const float C = cost_f32(eta, K, P, T);
+                        const float E = __fmul_rn(P, T);
+                        const bool better = (C < bc) | ((C == bc) & (E < be));
+                        bc = better ? C : bc;
+                        be = better ? E : be;
+                        bi = better ? i * nm + j : bi;
+                    }
+                }
+            }
+        }
+        // merge the two halves: the upper half (higher indices) wins only when
+        // strictly better, exactly as the sequential visit order would decide
+        const float oc = __shfl_xor_sync(0xffffffffu, bc, 1);
+        const float oe = __shfl_xor_sync(0xffffffffu, be, 1);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, 1);
+        if (half == 0 && k < n) {
+            const bool upper_valid = i_split < nc;
+            const bool take = upper_valid && ((oc < bc) | ((oc == bc) & (oe < be)));
+            if (take) {
+                bc = oc;
+                be = oe;
+                bi = oi;
+            }
+            idx_out[k] = bi;
+            if (cost_out) cost_out[k] = bc;
+            if (energy_out) energy_out[k] = be;
+            if (time_out) {
+                const int i = bi / nm, j = bi - i * nm;
+                time_out[k] = time_f32(tt0, __fmul_rn(a, s_mem[j].y), __fmul_rn(b, s_core[i].z));
+            }
+            if (params_out)
+#pragma unroll
+                for (int i = 0; i < 7; ++i) params_out[i * ld_out + k] = p[i];
+            if (clamped_out) clamped_out[k] = cl ? 1 : 0;
+        }
+        __syncthreads();  // out/act reused by the next tile
+    }
+}
+
+}  // namespace
+
+size_t mlp_smem_bytes() { return (size_t)kBaseFloats * sizeof(float); }
+
+static size_t pipeline_smem_bytes(int nc, int nm) {
+    return (size_t)(kBaseFloats + 4 * nc + 2 * nm) * sizeof(float);
+}
+
+// Pack the reference-layout model (W_l row-major [out][in], concatenated, in
+// double) into the transposed zero-padded FP32 layout the kernels expect.
+cudaError_t model_upload(Ctx& cx, const double* W, const double* b) {
+    std::vector<float> pk(kModelFloats, 0.f);
+    const double* W1 = W;
+    const double* W2 = W1 + 100 * 134;
+    const double* W3 = W2 + 50 * 100;
+    const double* W4 = W3 + 25 * 50;
+    for (int k = 0; k < 134; ++k)
+        for (int g = 0; g < 4; ++g)
+            for (int t = 0; t < 26; ++t) {
+                const int nn = 26 * g + t;
+                if (nn < 100) pk[kOffW1 + k * kW1Stride + g * 28 + t] = (float)W1[nn * 134 + k];
+            }
+    for (int k = 0; k < 100; ++k)
+        for (int g = 0; g < 4; ++g)
+            for (int t = 0; t < 13; ++t) {
+                const int nn = 13 * g + t;
+                if (nn < 50) pk[kOffW2 + k * kW2Stride + g * 16 + t] = (float)W2[nn * 100 + k];
+            }
+    for (int k = 0; k < 50; ++k)
+        for (int g = 0; g < 4; ++g)
+            for (int t = 0; t < 7; ++t) {
+                const int nn = 7 * g + t;
+                if (nn < 25) pk[kOffW3 + k * kW3Stride + g * 8 + t] = (float)W3[nn * 50 + k];
+            }
+    for (int k = 0; k < 25; ++k)
+        for (int nn = 0; nn < 7; ++nn) pk[kOffW4 + k * kW4Stride + nn] = (float)W4[nn * 25 + k];
+    const double* b1 = b;
+    const double* b2 = b1 + 100;
+    const double* b3 = b2 + 50;
+    const double* b4 = b3 + 25;
+    for (int i = 0; i < 100; ++i) pk[kOffB1 + i] = (float)b1[i];
+    for (int i = 0; i < 50; ++i) pk[kOffB2 + i] = (float)b2[i];
+    for (int i = 0; i < 25; ++i) pk[kOffB3 + i] = (float)b3[i];
+    for (int i = 0; i < 7; ++i) pk[kOffB4 + i] = (float)b4[i];
+    ModelDev& md = cx.model;
+    if (!md.wt) {
+        cudaError_t e = cudaMalloc(&md.wt, sizeof(float) * kModelFloats);
+        if (e != cudaSuccess) return e;
+    }
+    md.wt_floats = kModelFloats;
+    return cudaMemcpyAsync(md.wt, pk.data(), sizeof(float) * kModelFloats,
+                           cudaMemcpyHostToDevice, cx.stream);
+}
+
+static Stats stats_of(const Ctx& cx) {
+    Stats s;
+    for (int i = 0; i < 8; ++i) {
+        s.mean[i] = cx.model.mean[i];
+        s.std_[i] = cx.model.std_[i];
+    }
+    return s;
+}
+
+cudaError_t launch_predict(Ctx& cx, const float* fused, int64_t n, int64_t ld, float* params,
+                           uint8_t* clamped, float* raw) {
+    if (n <= 0) return cudaSuccess;
+    const size_t smem = mlp_smem_bytes();
+    static bool attr_set = false;  // per process; same value for every device
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(predict_kernel,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)(227 * 1024));
+        if (e != cudaSuccess) return e;
+        attr_set = true;
+    }
+    const int64_t tiles = (n + kTile - 1) / kTile;
+    const int grid = (int)(tiles < cx.num_sms ? tiles : cx.num_sms);
+    predict_kernel<<<grid, kThreads, smem, cx.stream>>>(cx.model.wt, stats_of(cx), fused, n, ld,
+                                                       params, clamped, raw);
+    ++cx.launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pipeline(Ctx& cx, const uint32_t* counts, const float* dcgm, int64_t n,
+                            int64_t ld, float eta, float K, float* params, uint8_t* clamped,
+                            int32_t* idx, float* cost, float* energy, float* time,
+                            int64_t ld_out) {
+    if (n <= 0) return cudaSuccess;
+    const size_t smem = pipeline_smem_bytes(cx.dom.nc, cx.dom.nm);
+    if (smem > 227 * 1024) return cudaErrorInvalidValue;
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(pipeline_kernel,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)(227 * 1024));
+        if (e != cudaSuccess) return e;
+        attr_set = true;
+    }
+    const int64_t tiles = (n + kTile - 1) / kTile;
+    const int grid = (int)(tiles < cx.num_sms ? tiles : cx.num_sms);
+    pipeline_kernel<<<grid, kThreads, smem, cx.stream>>>(
+        cx.model.wt, stats_of(cx), cx.dom.core4, cx.dom.nc, cx.dom.mem2, cx.dom.nm, eta, K,
+        counts, dcgm, n, ld, params, clamped, idx, cost, energy, time, ld_out);
+    ++cx.launches;
+    return cudaGetLastError();
+}
+
+}  // namespace dso_b200

@@ -1,0 +1,360 @@
+// sweep.cu — grid sweep + eta objective + lexicographic argmin (sm_100a).
+//
+// Replaces brute_force_config (reference proj/src/optimizer.cpp:90-117) for a
+// batch of kernels.  Reference semantics kept exactly:
+//   * pairs visited fc-outer / fm-inner (optimizer.cpp:99-100), idx = i*nm + j;
+//   * better() (optimizer.cpp:27-32): cost, then energy, then vc (strictly
+//     increasing in i), then fm — in visit order that is
+//     (C < bc) || (C == bc && E < be), keeping the earlier pair otherwise;
+//   * P = p0 + kp*vc + g*fm + c*vc^2*fc, T = t0 + max(a/fm, b/fc),
+//     C = (eta*P + (1-eta)*pmax)*T, E = P*T (dvfs_model.hpp:81-104);
+//   * validate(params) (dvfs_model.hpp:50-58) per kernel -> kstatus.
+// The first pair seeds the running best unconditionally, as have_best does
+// (optimizer.cpp:96-106), so NaN/inf semantics match too.
+//
+// Work mapping: one thread per kernel, the per-domain tables in shared memory
+// (uniform across the warp -> broadcast LDS), per-kernel terms hoisted out of
+// the pair loop:  per fc level Pc = p0 + kp*vc + c*vc^2*fc and Tb = b/fc; per
+// fm level G = g*fm and Ta = a/fm.  Per pair: FADD, FMNMX, FADD, FFMA, FMUL,
+// FMUL + the comparator.  Issue-bound on the FP32/ALU pipes; no HBM pressure
+// (28 B in, 16 B out per kernel for nc*nm pairs).
+#include <math.h>
+
+#include "common.cuh"
+
+namespace dso_b200 {
+
+namespace {
+
+constexpr int kBlock = 256;
+
+__device__ __forceinline__ bool params_invalid(float p0, float kp, float g, float c, float t0,
+                                               float a, float b) {
+    // dvfs_model.hpp:51-57 (NaN passes the >= 0 tests there too; a NaN in
+    // alpha or beta fails alpha + beta > 0)
+    return p0 < 0.f || kp < 0.f || g < 0.f || c < 0.f || t0 < 0.f || a < 0.f || b < 0.f ||
+           !(a + b > 0.f);
+}
+
+template <int NM>
+__global__ void __launch_bounds__(kBlock) sweep_f32_kernel(
+    const float* __restrict__ params, int64_t n, int64_t ld, const float4* __restrict__ core4,
+    int nc, const float2* __restrict__ mem2, int nm_rt, float eta, float K,
+    int32_t* __restrict__ idx, float* __restrict__ cost, float* __restrict__ energy,
+    float* __restrict__ time, int32_t* __restrict__ kstatus) {
+    __shared__ float4 s_core[kMaxCore];
+    __shared__ float2 s_mem[kMaxMem];
+    const int nm = NM > 0 ? NM : nm_rt;
+    for (int i = threadIdx.x; i < nc; i += blockDim.x) s_core[i] = core4[i];
+    for (int j = threadIdx.x; j < nm; j += blockDim.x) s_mem[j] = mem2[j];
+    __syncthreads();
+
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride) {
+        const float p0 = __ldg(params + k), kp = __ldg(params + ld + k),
+                    g = __ldg(params + 2 * ld + k), c = __ldg(params + 3 * ld + k),
+                    t0 = __ldg(params + 4 * ld + k), a = __ldg(params + 5 * ld + k),
+                    b = __ldg(params + 6 * ld + k);
+        if (params_invalid(p0, kp, g, c, t0, a, b)) {
+            idx[k] = -1;
+            if (cost) cost[k] = __int_as_float(0x7fc00000);
+            if (energy) energy[k] = __int_as_float(0x7fc00000);
+            if (time) time[k] = __int_as_float(0x7fc00000);
+            if (kstatus) kstatus[k] = kInvalidArgument;
+            continue;
+        }
+        // first candidate taken unconditionally (optimizer.cpp:103, have_best)
+        float bc, be;
+        int bi = 0;
+        {
+            const float4 t = s_core[0];
+            const float P = __fadd_rn(pc_f32(p0, kp, c, t), __fmul_rn(g, s_mem[0].x));
+            const float T = time_f32(t0, __fmul_rn(a, s_mem[0].y), __fmul_rn(b, t.z));
+            bc = cost_f32(eta, K, P, T);
+            be = __fmul_rn(P, T);
+        }
+        if constexpr (NM > 0) {
+            float G[NM], Ta[NM];
+#pragma unroll
+            for (int j = 0; j < NM; ++j) {
+                G[j] = __fmul_rn(g, s_mem[j].x);
+                Ta[j] = __fmul_rn(a, s_mem[j].y);
+            }
+#pragma unroll 2
+            for (int i = 0; i < nc; ++i) {
+                const float4 t = s_core[i];
+                const float Pc = pc_f32(p0, kp, c, t);
+                const float Tb = __fmul_rn(b, t.z);
+#pragma unroll
+                for (int j = 0; j < NM; ++j) {
+                    const float P = __fadd_rn(Pc, G[j]);
+                    const float T = time_f32(t0, Ta[j], Tb);
+                    const float C = cost_f32(eta, K, P, T);
+                    const float E = __fmul_rn(P, T);
+                    const bool better = (C < bc) | ((C == bc) & (E < be));
+                    bc = better ? C : bc;
+                    be = better ? E : be;
+                    bi = better ? i * NM + j : bi;
+                }
+            }
+        } else {
+            for (int i = 0; i < nc; ++i) {
+                const float4 t = s_core[i];
+                const float Pc = pc_f32(p0, kp, c, t);
+                const float Tb = __fmul_rn(b, t.z);
+                for (int j = 0; j < nm; ++j) {
+                    const float P = __fadd_rn(Pc, __fmul_rn(g, s_mem[j].x));
+                    const float T = time_f32(t0, __fmul_rn(a, s_mem[j].y), Tb);
+                    const float C = cost_f32(eta, K, P, T);
+                    const float E = __fmul_rn(P, T);
+                    const bool better = (C < bc) | ((C == bc) & (E < be));
+                    bc = better ? C : bc;
+                    be = better ? E : be;
+                    bi = better ? i * nm + j : bi;
+                }
+            }
+        }
+        idx[k] = bi;
+        if (cost) cost[k] = bc;
+        if (energy) energy[k] = be;
+        if (time) {
+            const int i = bi / nm, j = bi - i * nm;
+            time[k] = time_f32(t0, __fmul_rn(a, s_mem[j].y), __fmul_rn(b, s_core[i].z));
+        }
+        if (kstatus) kstatus[k] = 0;
+    }
+}
+
+// ---- exact FP64 variant -------------------------------------------------------
+// Same arithmetic as the reference, operation by operation, with explicit
+// round-to-nearest intrinsics so nothing is contracted into an FMA:
+//   power    ((p0 + kp*vc) + g*fm) + ((c*vc)*vc)*fc      dvfs_model.hpp:82-83
+//   time     t0 + ((a/fm < b/fc) ? b/fc : a/fm)          dvfs_model.hpp:89 (std::max)
+//   cost     (eta*P + (1-eta)*pmax) * T                   dvfs_model.hpp:103
+//   energy   P * T                                        dvfs_model.hpp:94
+// vc per level is computed on the host by required_voltage_mhz's expression.
+// Hoisting (p0 + kp*vc), ((c*vc)*vc)*fc, b/fc and a/fm out of the pair loop
+// does not change any rounding: each is a complete sub-expression.
+__global__ void __launch_bounds__(kBlock) sweep_f64_kernel(
+    const double* __restrict__ params, int64_t n, const double2* __restrict__ core_d, int nc,
+    const double* __restrict__ mem_d, int nm, double eta, double K, int32_t* __restrict__ idx,
+    double* __restrict__ cost, double* __restrict__ energy, double* __restrict__ time,
+    int32_t* __restrict__ kstatus) {
+    __shared__ double2 s_core[kMaxCore];
+    __shared__ double s_mem[kMaxMem];
+    for (int i = threadIdx.x; i < nc; i += blockDim.x) s_core[i] = core_d[i];
+    for (int j = threadIdx.x; j < nm; j += blockDim.x) s_mem[j] = mem_d[j];
+    __syncthreads();
+    const double kNaN = __longlong_as_double(0x7ff8000000000000LL);
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride) {
+        const double* p = params + 7 * k;
+        const double p0 = p[0], kp = p[1], g = p[2], c = p[3], t0 = p[4], a = p[5], b = p[6];
+        if (p0 < 0.0 || kp < 0.0 || g < 0.0 || c < 0.0 || t0 < 0.0 || a < 0.0 || b < 0.0 ||
+            !(__dadd_rn(a, b) > 0.0)) {
+            idx[k] = -1;
+            if (cost) cost[k] = kNaN;
+            if (energy) energy[k] = kNaN;
+            if (time) time[k] = kNaN;
+            if (kstatus) kstatus[k] = kInvalidArgument;
+            continue;
+        }
+        double bc, be, bt;
+        int bi = 0;
+        {  // first candidate taken unconditionally (optimizer.cpp:103)
+            const double vc = s_core[0].x, fc = s_core[0].y, fm = s_mem[0];
+            const double P = __dadd_rn(
+                __dadd_rn(__dadd_rn(p0, __dmul_rn(kp, vc)), __dmul_rn(g, fm)),
+                __dmul_rn(__dmul_rn(__dmul_rn(c, vc), vc), fc));
+            const double Ta = __ddiv_rn(a, fm), Tb = __ddiv_rn(b, fc);
+            bt = __dadd_rn(t0, (Ta < Tb) ? Tb : Ta);
+            bc = __dmul_rn(__dadd_rn(__dmul_rn(eta, P), K), bt);
+            be = __dmul_rn(P, bt);
+        }
+        for (int i = 0; i < nc; ++i) {
+            const double vc = s_core[i].x, fc = s_core[i].y;
+            const double A = __dadd_rn(p0, __dmul_rn(kp, vc));
+            const double W = __dmul_rn(__dmul_rn(__dmul_rn(c, vc), vc), fc);
+            const double Tb = __ddiv_rn(b, fc);
+            for (int j = 0; j < nm; ++j) {
+                const double fm = s_mem[j];
+                const double P = __dadd_rn(__dadd_rn(A, __dmul_rn(g, fm)), W);
+                const double Ta = __ddiv_rn(a, fm);
+                const double T = __dadd_rn(t0, (Ta < Tb) ? Tb : Ta);
+                const double C = __dmul_rn(__dadd_rn(__dmul_rn(eta, P), K), T);
+                const double E = __dmul_rn(P, T);
+                const bool better = (C < bc) | ((C == bc) & (E < be));
+                if (better) {
+                    bc = C;
+                    be = E;
+                    bt = T;
+                    bi = i * nm + j;
+                }
+            }
+        }
+        idx[k] = bi;
+        if (cost) cost[k] = bc;
+        if (energy) energy[k] = be;
+        if (time) time[k] = bt;
+        if (kstatus) kstatus[k] = 0;
+    }
+}
+
+// ---- eta sweep ------------------------------------------------------------------
+// brute_force_config at n_eta objective weights in one pass over the grid.
+// One thread owns one kernel and a chunk of CH etas (state: 3 registers per
+// eta, the eta constants in registers).  P, T and E are computed once per pair
+// and shared by the chunk; per (pair, eta) the objective is one FFMA + FMUL
+// with the same rounding as sweep_f32_kernel, so each eta's argmin equals
+// dso_sweep at that eta bit for bit.
+template <int CH>
+__global__ void __launch_bounds__(128) eta_sweep_kernel(
+    const float* __restrict__ params, int64_t n, int64_t ld, const float4* __restrict__ core4,
+    int nc, const float2* __restrict__ mem2, int nm, const float2* __restrict__ etaK, int n_eta, int32_t* __restrict__ idx, float* __restrict__ cost, int64_t ld_out) {
+    __shared__ float4 s_core[kMaxCore];
+    __shared__ float2 s_mem[kMaxMem];
+    for (int i = threadIdx.x; i < nc; i += blockDim.x) s_core[i] = core4[i];
+    for (int j = threadIdx.x; j < nm; j += blockDim.x) s_mem[j] = mem2[j];
+    __syncthreads();
+    const int chunk = blockIdx.y;
+    const int e0 = chunk * CH;
+    float ev[CH], Kv[CH];
+#pragma unroll
+    for (int e = 0; e < CH; ++e) {
+        const int ee = e0 + e < n_eta ? e0 + e : n_eta - 1;
+        ev[e] = etaK[ee].x;
+        Kv[e] = etaK[ee].y;
+    }
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride) {
+        const float p0 = __ldg(params + k), kp = __ldg(params + ld + k),
+                    g = __ldg(params + 2 * ld + k), c = __ldg(params + 3 * ld + k),
+                    t0 = __ldg(params + 4 * ld + k), a = __ldg(params + 5 * ld + k),
+                    b = __ldg(params + 6 * ld + k);
+        if (params_invalid(p0, kp, g, c, t0, a, b)) {
+#pragma unroll
+            for (int e = 0; e < CH; ++e)
+                if (e0 + e < n_eta) {
+                    idx[(int64_t)(e0 + e) * ld_out + k] = -1;
+                    if (cost) cost[(int64_t)(e0 + e) * ld_out + k] = __int_as_float(0x7fc00000);
+                }
+            continue;
+        }
+        float bc[CH], be[CH];
+        int bi[CH];
+        {  // first candidate taken unconditionally (optimizer.cpp:103)
+            const float4 t = s_core[0];
+            const float P = __fadd_rn(pc_f32(p0, kp, c, t), __fmul_rn(g, s_mem[0].x));
+            const float T = time_f32(t0, __fmul_rn(a, s_mem[0].y), __fmul_rn(b, t.z));
+#pragma unroll
+            for (int e = 0; e < CH; ++e) {
+                bc[e] = cost_f32(ev[e], Kv[e], P, T);
+                be[e] = __fmul_rn(P, T);
+                bi[e] = 0;
+            }
+        }
+        for (int i = 0; i < nc; ++i) {
+            const float4 t = s_core[i];
+            const float Pc = pc_f32(p0, kp, c, t);
+            const float Tb = __fmul_rn(b, t.z);
+            for (int j = 0; j < nm; ++j) {
+                const float2 m = s_mem[j];
+                const float P = __fadd_rn(Pc, __fmul_rn(g, m.x));
+                const float T = time_f32(t0, __fmul_rn(a, m.y), Tb);
+                const float E = __fmul_rn(P, T);
+                const int id = i * nm + j;
+#pragma unroll
+                for (int e = 0; e < CH; ++e) {
+                    const float C = cost_f32(ev[e], Kv[e], P, T);
+                    const bool better = (C < bc[e]) | ((C == bc[e]) & (E < be[e]));
+                    bc[e] = better ? C : bc[e];
+                    be[e] = better ? E : be[e];
+                    bi[e] = better ? id : bi[e];
+                }
+            }
+        }
+#pragma unroll
+        for (int e = 0; e < CH; ++e)
+            if (e0 + e < n_eta) {
+                idx[(int64_t)(e0 + e) * ld_out + k] = bi[e];
+                if (cost) cost[(int64_t)(e0 + e) * ld_out + k] = bc[e];
+            }
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_sweep_f32(Ctx& cx, const float* params, int64_t n, int64_t ld, float eta,
+                             float K, int32_t* idx, float* cost, float* energy, float* time,
+                             int32_t* kstatus) {
+    if (n <= 0) return cudaSuccess;
+    const int grid = grid_for(n, kBlock, cx.num_sms, 8);
+    const DomainDev& d = cx.dom;
+#define DSO_SWEEP_CASE(NMV)                                                                    \
+    sweep_f32_kernel<NMV><<<grid, kBlock, 0, cx.stream>>>(params, n, ld, d.core4, d.nc, d.mem2, \
+                                                          d.nm, eta, K, idx, cost, energy,      \
+                                                          time, kstatus)
+    switch (d.nm) {
+        case 1: DSO_SWEEP_CASE(1); break;
+        case 2: DSO_SWEEP_CASE(2); break;
+        case 3: DSO_SWEEP_CASE(3); break;
+        case 4: DSO_SWEEP_CASE(4); break;
+        default: DSO_SWEEP_CASE(0); break;
+    }
+#undef DSO_SWEEP_CASE
+    ++cx.launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_sweep_f64(Ctx& cx, const double* params, int64_t n, double eta, double K,
+                             int32_t* idx, double* cost, double* energy, double* time,
+                             int32_t* kstatus) {
+    if (n <= 0) return cudaSuccess;
+    const int grid = grid_for(n, kBlock, cx.num_sms, 8);
+    sweep_f64_kernel<<<grid, kBlock, 0, cx.stream>>>(params, n, cx.dom.core_d, cx.dom.nc,
+                                                     cx.dom.mem_d, cx.dom.nm, eta, K, idx, cost,
+                                                     energy, time, kstatus);
+    ++cx.launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_eta_sweep(Ctx& cx, const float* params, int64_t n, int64_t ld,
+                             const float2* etaK_dev, int n_eta, int32_t* idx, float* cost,
+                             int64_t ld_out) {
+    if (n <= 0 || n_eta <= 0) return cudaSuccess;
+    const DomainDev& d = cx.dom;
+    // pick the chunk size with the least padding (ties -> larger chunk)
+    const int cands[3] = {17, 8, 4};
+    int best = 17, best_slots = 1 << 30;
+    for (int ch : cands) {
+        const int slots = ((n_eta + ch - 1) / ch) * ch;
+        if (slots < best_slots) {
+            best_slots = slots;
+            best = ch;
+        }
+    }
+    const int chunks = (n_eta + best - 1) / best;
+    const int gx = grid_for(n, 128, cx.num_sms, 16);
+    dim3 grid(gx, chunks);
+    switch (best) {
+        case 17:
+            eta_sweep_kernel<17><<<grid, 128, 0, cx.stream>>>(params, n, ld, d.core4, d.nc,
+                                                              d.mem2, d.nm, etaK_dev, n_eta,
+                                                              idx, cost, ld_out);
+            break;
+        case 8:
+            eta_sweep_kernel<8><<<grid, 128, 0, cx.stream>>>(params, n, ld, d.core4, d.nc,
+                                                             d.mem2, d.nm, etaK_dev, n_eta,
+                                                             idx, cost, ld_out);
+            break;
+        default:
+            eta_sweep_kernel<4><<<grid, 128, 0, cx.stream>>>(params, n, ld, d.core4, d.nc,
+                                                             d.mem2, d.nm, etaK_dev, n_eta,
+                                                             idx, cost, ld_out);
+            break;
+    }
+    ++cx.launches;
+    return cudaGetLastError();
+}
+
+}  // namespace dso_b200
