@@ -59,8 +59,9 @@ typedef struct dso_ctx dso_ctx;
 /* ---- context ------------------------------------------------------------- */
 int32_t dso_ctx_create(int32_t device, dso_ctx** out);
 int32_t dso_ctx_destroy(dso_ctx* ctx);
-/* Use an external cudaStream_t (e.g. torch's current stream); NULL restores
- * the context's own stream. */
+/* Launch on an external cudaStream_t (e.g. torch's current stream).  NULL is
+ * the legacy default stream (torch's default stream); a context starts on its
+ * own non-blocking stream. */
 int32_t dso_ctx_set_stream(dso_ctx* ctx, void* cuda_stream);
 int32_t dso_sync(dso_ctx* ctx);
 const char* dso_last_error(const dso_ctx* ctx);

@@ -195,7 +195,7 @@ int32_t dso_ctx_destroy(dso_ctx* ctx) {
 
 int32_t dso_ctx_set_stream(dso_ctx* ctx, void* stream) {
     if (!ctx) return kInvalidArgument;
-    ctx->c.stream = stream ? (cudaStream_t)stream : ctx->c.own_stream;
+    ctx->c.stream = (cudaStream_t)stream;  // NULL = legacy default stream
     return kOk;
 }
 

@@ -10,56 +10,56 @@
 // operands are exact in FP32 — see DESIGN.md §4.1), and the quotient is
 // computed with one reciprocal per category plus the Markstein correction
 //   q = c*r;  e = fma(-q, t, c);  q = fma(e, r, q)
-// which is correctly rounded.  Totals >= 2^24 take an FP64 division.
+// which is correctly rounded.  Totals >= 2^24 take an FP64 division
+// (features_core.cuh).
 //
-// Memory-bound: 504 B of counts + 32 B of DCGM in, 536 B out per kernel; all
-// accesses are row-contiguous over kernels (SoA), i.e. fully coalesced.
+// Memory-bound: 504 B of counts + 32 B of DCGM in, 536 B out per kernel
+// (1,072 B); all accesses are 128-bit and row-contiguous over kernels.
+#include <algorithm>
+
 #include "common.cuh"
+#include "features_core.cuh"
 
 namespace dso_b200 {
 
 namespace {
 
-__device__ __forceinline__ float u32_to_f32_exact(uint32_t v) {
-    // exact for v < 2^24 (callers guarantee it); single I2F otherwise
-    return __uint2float_rn(v);
-}
-
-// Correctly rounded c/t for c <= t < 2^24 given r = RN(1/t).
-__device__ __forceinline__ float div_cr(float c, float t, float r) {
-    const float q = __fmul_rn(c, r);
-    const float e = fmaf(-q, t, c);
-    return fmaf(e, r, q);
-}
-
-__device__ __forceinline__ float normalize_one(uint32_t count, uint64_t total, float tf,
-                                               float r) {
-    if (total == 0) return 0.f;
-    if (total < (1u << 24)) return div_cr(u32_to_f32_exact(count), tf, r);
-    return (float)((double)count / (double)total);
-}
-
+// One tile of 128 kernels per iteration: counts + DCGM staged and normalised in
+// shared memory by tile_features (all loads of the tile in flight, 128-bit),
+// then written out row-contiguous with 128-bit stores.  72.7 KB of shared
+// memory per CTA -> 3 CTAs per SM, so one CTA's loads overlap another's math
+// and stores.
 __global__ void __launch_bounds__(256) featurize_kernel(const uint32_t* __restrict__ counts,
                                                         const float* __restrict__ dcgm,
                                                         int64_t n, int64_t ld,
                                                         float* __restrict__ fused) {
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride) {
+    extern __shared__ __align__(16) float smem[];
+    float* act = smem;
+    float* scratch = smem + DSO_FUSED_ROWS * kFeatTile;
+    const bool vec_ok = ((ld & 3) == 0) && ((reinterpret_cast<uintptr_t>(counts) & 15) == 0) &&
+                        ((reinterpret_cast<uintptr_t>(dcgm) & 15) == 0) &&
+                        ((reinterpret_cast<uintptr_t>(fused) & 15) == 0);
+    const int64_t tiles = (n + kFeatTile - 1) / kFeatTile;
+    const int tid = threadIdx.x;
+    for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+        const int64_t t0 = tile * kFeatTile;
+        tile_features(act, scratch, counts, dcgm, t0, n, ld, vec_ok);
+        if (vec_ok && t0 + kFeatTile <= n) {
+            const int q = tid & 31, rp = tid >> 5;
 #pragma unroll
-        for (int m = 0; m < 8; ++m) fused[m * ld + k] = __ldg(dcgm + m * ld + k);
-        const int base[3] = {0, DSO_INSTR_SLOTS, DSO_INSTR_SLOTS + DSO_DTYPE_SLOTS};
-        const int len[3] = {DSO_INSTR_SLOTS, DSO_DTYPE_SLOTS, DSO_MEMSPACE_SLOTS};
-#pragma unroll
-        for (int cat = 0; cat < 3; ++cat) {
-            uint64_t total = 0;
-            for (int i = 0; i < len[cat]; ++i) total += __ldg(counts + (base[cat] + i) * ld + k);
-            const float tf = (float)total;
-            const float r = total ? __frcp_rn(tf) : 0.f;
-            for (int i = 0; i < len[cat]; ++i) {
-                const int row = base[cat] + i;
-                fused[(8 + row) * ld + k] = normalize_one(__ldg(counts + row * ld + k), total, tf, r);
+            for (int j = 0; j < 17; ++j) {
+                const int r = rp + 8 * j;
+                if (r < DSO_FUSED_ROWS)
+                    reinterpret_cast<float4*>(fused + (int64_t)r * ld + t0)[q] =
+                        reinterpret_cast<const float4*>(act + r * kFeatTile)[q];
             }
+        } else {
+            const int m = tid & (kFeatTile - 1), h = tid >> 7;
+            if (t0 + m < n)
+                for (int r = h; r < DSO_FUSED_ROWS; r += 2)
+                    fused[(int64_t)r * ld + t0 + m] = act[r * kFeatTile + m];
         }
+        __syncthreads();
     }
 }
 
@@ -97,8 +97,17 @@ __global__ void __launch_bounds__(256) dcgm_mean_kernel(const double* __restrict
 cudaError_t launch_featurize(Ctx& cx, const uint32_t* counts, const float* dcgm, int64_t n,
                              int64_t ld, float* fused) {
     if (n <= 0) return cudaSuccess;
-    featurize_kernel<<<grid_for(n, 256, cx.num_sms, 8), 256, 0, cx.stream>>>(counts, dcgm, n,
-                                                                              ld, fused);
+    const size_t smem = (size_t)(DSO_FUSED_ROWS * kFeatTile + 1024) * sizeof(float);
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(featurize_kernel,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    const int64_t tiles = (n + kFeatTile - 1) / kFeatTile;
+    const int grid = (int)std::min<int64_t>(tiles, (int64_t)cx.num_sms * 3);
+    featurize_kernel<<<grid, 256, smem, cx.stream>>>(counts, dcgm, n, ld, fused);
     ++cx.launches;
     return cudaGetLastError();
 }

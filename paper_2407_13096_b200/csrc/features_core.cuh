@@ -1,0 +1,143 @@
+// features_core.cuh — the feature stage for one tile of 128 kernels, shared by
+// the standalone featurize kernel and the fused pipeline.
+//
+// featurize (reference proj/src/ptx_features.cpp:311-329) + as_vector
+// (mlp.cpp:307-314): per category (instr 101 | dtype 17 | memspace 8)
+// v[i] = count[i] / total, all-zero for a zero total, DCGM ratios first.  The
+// reference divides in double; for totals < 2^24 the correctly rounded FP32
+// quotient equals that double rounded to float.  Tile layout:
+// act[134][128] floats, k-major (row = feature, 128 kernels contiguous).
+#pragma once
+
+#include "common.cuh"
+
+namespace dso_b200 {
+
+constexpr int kFeatTile = 128;
+
+// ---------------------------------------------------------------------------
+// Feature stage into act: raw counts [126][ld] + DCGM [8][ld] for kernels
+// [t0, t0+128) -> act rows 0..133 (fused order).  Kernels >= n get zeros.
+//   phase 1: every load of the tile in flight at once (16 x 128-bit per
+//            thread; a warp covers one 512-byte row segment) — or a scalar
+//            path for the ragged last tile / unaligned inputs;
+//   phase 2: per (kernel, category) exact integer total and its reciprocal,
+//            once — not per entry;
+//   phase 3: every entry becomes count/total, correctly rounded (Markstein).
+// scratch: 1024 floats: tf[3][128], rr[3][128] and the
+// split instr partial sums (u64 [128]).
+__device__ __forceinline__ void tile_features(float* act, float* scratch,
+                                              const uint32_t* __restrict__ counts,
+                                              const float* __restrict__ dcgm, int64_t t0,
+                                              int64_t n, int64_t ld, bool vec_ok) {
+    uint32_t* acti = reinterpret_cast<uint32_t*>(act);
+    const int tid = threadIdx.x;
+    if (vec_ok && t0 + kFeatTile <= n) {
+        const int q = tid & 31;   // kernels 4q .. 4q+3
+        const int rp = tid >> 5;  // row phase = warp index (0..7)
+        uint4 v[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            const int r = rp + 8 * j;
+            if (r < DSO_COUNT_ROWS)
+                v[j] = __ldg(reinterpret_cast<const uint4*>(counts + (int64_t)r * ld + t0) + q);
+        }
+        const float4 d = __ldg(reinterpret_cast<const float4*>(dcgm + (int64_t)rp * ld + t0) + q);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            const int r = rp + 8 * j;
+            if (r < DSO_COUNT_ROWS) reinterpret_cast<uint4*>(acti + (8 + r) * kFeatTile)[q] = v[j];
+        }
+        reinterpret_cast<float4*>(act + rp * kFeatTile)[q] = d;
+    } else {
+        const int m = tid & (kFeatTile - 1);
+        const int h = tid >> 7;
+        const int64_t k = t0 + m;
+        const bool live = k < n;
+#pragma unroll 9
+        for (int r = h; r < DSO_COUNT_ROWS; r += 2)
+            acti[(8 + r) * kFeatTile + m] = live ? __ldg(counts + (int64_t)r * ld + k) : 0u;
+#pragma unroll
+        for (int r = h; r < 8; r += 2)
+            act[r * kFeatTile + m] = live ? __ldg(dcgm + (int64_t)r * ld + k) : 0.f;
+    }
+    __syncthreads();
+    // phase 2: exact totals (u64), split so both thread halves sum ~63 rows
+    float* tfv = scratch;                     // [3][128]
+    float* rrv = tfv + 3 * kFeatTile;             // [3][128]
+    uint64_t* part = reinterpret_cast<uint64_t*>(rrv + 3 * kFeatTile);  // [128]
+    constexpr int kSplit = 60;
+    const int m = tid & (kFeatTile - 1);
+    uint64_t s_a = 0, s_b = 0, s_c = 0;
+    if (tid < kFeatTile) {
+        for (int r = 0; r < kSplit; ++r) s_a += acti[(8 + r) * kFeatTile + m];
+    } else {
+        for (int r = kSplit; r < DSO_INSTR_SLOTS; ++r) s_a += acti[(8 + r) * kFeatTile + m];
+        for (int r = 0; r < DSO_DTYPE_SLOTS; ++r) s_b += acti[(8 + DSO_INSTR_SLOTS + r) * kFeatTile + m];
+        for (int r = 0; r < DSO_MEMSPACE_SLOTS; ++r)
+            s_c += acti[(8 + DSO_INSTR_SLOTS + DSO_DTYPE_SLOTS + r) * kFeatTile + m];
+        part[m] = s_a;
+    }
+    __syncthreads();
+    // tf = total as float (exact below 2^24), rr = RN(1/tf); tf = 0 marks a zero
+    // total, tf = -1 a total >= 2^24 (FP64 path in phase 3).
+    auto scale = [&](int cat, uint64_t tot) {
+        if (tot == 0) {
+            tfv[cat * kFeatTile + m] = 0.f;
+            rrv[cat * kFeatTile + m] = 0.f;
+        } else if (tot < (1u << 24)) {
+            const float tf = __uint2float_rn((uint32_t)tot);
+            tfv[cat * kFeatTile + m] = tf;
+            rrv[cat * kFeatTile + m] = __frcp_rn(tf);
+        } else {
+            tfv[cat * kFeatTile + m] = -1.f;
+            rrv[cat * kFeatTile + m] = 0.f;
+        }
+    };
+    if (tid < kFeatTile) {
+        scale(0, s_a + part[m]);
+    } else {
+        scale(1, s_b);
+        scale(2, s_c);
+    }
+    __syncthreads();
+    // phase 3: normalise in place, 4 kernels x 16 rows per thread
+    {
+        const int q = tid & 31;
+        const int rp = tid >> 5;
+#pragma unroll 4
+        for (int j = 0; j < 16; ++j) {
+            const int r = rp + 8 * j;
+            if (r >= DSO_COUNT_ROWS) break;
+            const int cat = r < DSO_INSTR_SLOTS ? 0 : (r < DSO_INSTR_SLOTS + DSO_DTYPE_SLOTS ? 1 : 2);
+            uint4* rowp = reinterpret_cast<uint4*>(acti + (8 + r) * kFeatTile) + q;
+            const uint4 c = *rowp;
+            const float4 tf = reinterpret_cast<const float4*>(tfv + cat * kFeatTile)[q];
+            const float4 rr = reinterpret_cast<const float4*>(rrv + cat * kFeatTile)[q];
+            const uint32_t cc[4] = {c.x, c.y, c.z, c.w};
+            const float tt[4] = {tf.x, tf.y, tf.z, tf.w};
+            const float ri[4] = {rr.x, rr.y, rr.z, rr.w};
+            float o[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                if (tt[e] > 0.f) {
+                    const float cf = __uint2float_rn(cc[e]);
+                    const float qq = __fmul_rn(cf, ri[e]);
+                    o[e] = fmaf(fmaf(-qq, tt[e], cf), ri[e], qq);
+                } else if (tt[e] == 0.f) {
+                    o[e] = 0.f;
+                } else {  // total >= 2^24: exact u64 sum, one FP64 division
+                    const int base = cat == 0 ? 0 : (cat == 1 ? DSO_INSTR_SLOTS : DSO_INSTR_SLOTS + DSO_DTYPE_SLOTS);
+                    const int len = cat == 0 ? DSO_INSTR_SLOTS : (cat == 1 ? DSO_DTYPE_SLOTS : DSO_MEMSPACE_SLOTS);
+                    uint64_t s = 0;
+                    for (int i = 0; i < len; ++i) s += acti[(8 + base + i) * kFeatTile + 4 * q + e];
+                    o[e] = (float)((double)cc[e] / (double)s);
+                }
+            }
+            *reinterpret_cast<float4*>(rowp) = make_float4(o[0], o[1], o[2], o[3]);
+        }
+    }
+    __syncthreads();
+}
+
+}  // namespace dso_b200

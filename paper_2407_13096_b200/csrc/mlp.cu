@@ -34,6 +34,8 @@
 #include <vector>
 
 #include "common.cuh"
+#include "features_core.cuh"
+#include "sweep_core.cuh"
 
 namespace dso_b200 {
 
@@ -71,9 +73,13 @@ static_assert(kOffW2 % 4 == 0 && kOffW3 % 4 == 0 && kOffW4 % 4 == 0 && kOffB1 % 
 
 __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
 
-// sigmoid (mlp.cpp:166-168) in FP32: 1 / (1 + e^-z) via ex2 + rcp.
+// sigmoid (mlp.cpp:166-168) in FP32: 1 / (1 + 2^(-z log2 e)) with the
+// approximate MUFU ex2/rcp (rel. error ~2^-22 each; no denormal fix-up code).
 __device__ __forceinline__ float sigmoidf_fast(float z) {
-    return __fdividef(1.0f, 1.0f + __expf(-z));
+    float e, r;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(z * -1.4426950408889634f));
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(1.0f + e));
+    return r;
 }
 
 // ---------------------------------------------------------------------------
@@ -98,23 +104,36 @@ __device__ __forceinline__ void mlp_tile(float* smem) {
     const int g = tid >> 6;   // neuron group (uniform per warp)
 
     // ---- L1: 134 -> 100 (neurons 26g .. 26g+25), pairs along n -------------
+    // Operands of step k+1 are loaded while step k's 26 FFMA2 issue (explicit
+    // register double buffering: only 2 warps per scheduler, so the shared-
+    // memory latency must be covered by ILP, not by other warps).
     {
         float2 acc0[13], acc1[13];
 #pragma unroll
         for (int p = 0; p < 13; ++p) acc0[p] = acc1[p] = f2(0.f, 0.f);
         const float* wbase = W + kOffW1 + g * 28;
-#pragma unroll 2
+        float2 a_n = act2[mp];
+        float4 v_n[6];
+        float2 l_n;
+#pragma unroll
+        for (int q = 0; q < 6; ++q) v_n[q] = reinterpret_cast<const float4*>(wbase)[q];
+        l_n = reinterpret_cast<const float2*>(wbase)[12];
+#pragma unroll 1
         for (int k = 0; k < 134; ++k) {
-            const float2 a = act2[k * 64 + mp];
-            const float4* w4 = reinterpret_cast<const float4*>(wbase + k * kW1Stride);
+            const float2 a = a_n;
             float2 w[13];
 #pragma unroll
             for (int q = 0; q < 6; ++q) {
-                const float4 v = w4[q];
-                w[2 * q] = f2(v.x, v.y);
-                w[2 * q + 1] = f2(v.z, v.w);
+                w[2 * q] = f2(v_n[q].x, v_n[q].y);
+                w[2 * q + 1] = f2(v_n[q].z, v_n[q].w);
             }
-            w[12] = reinterpret_cast<const float2*>(w4)[12];
+            w[12] = l_n;
+            const int kn = k + 1 < 134 ? k + 1 : k;
+            const float* wn = wbase + kn * kW1Stride;
+            a_n = act2[kn * 64 + mp];
+#pragma unroll
+            for (int q = 0; q < 6; ++q) v_n[q] = reinterpret_cast<const float4*>(wn)[q];
+            l_n = reinterpret_cast<const float2*>(wn)[12];
 #pragma unroll
             for (int p = 0; p < 13; ++p) {
                 acc0[p] = ffma2(f2(a.x, a.x), w[p], acc0[p]);
@@ -139,14 +158,23 @@ __device__ __forceinline__ void mlp_tile(float* smem) {
 #pragma unroll
         for (int t = 0; t < 13; ++t) acc[t] = f2(0.f, 0.f);
         const float* wbase = W + kOffW2 + g * 16;
-#pragma unroll 2
+        float2 a_n = act2[mp];
+        float4 v0 = reinterpret_cast<const float4*>(wbase)[0],
+               v1 = reinterpret_cast<const float4*>(wbase)[1],
+               v2 = reinterpret_cast<const float4*>(wbase)[2];
+        float v3 = wbase[12];
+#pragma unroll 1
         for (int k = 0; k < 100; ++k) {
-            const float2 a = act2[k * 64 + mp];
-            const float4* w4 = reinterpret_cast<const float4*>(wbase + k * kW2Stride);
-            const float4 v0 = w4[0], v1 = w4[1], v2 = w4[2];
-            const float v3 = reinterpret_cast<const float*>(w4)[12];
+            const float2 a = a_n;
             const float w[13] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z,
                                  v1.w, v2.x, v2.y, v2.z, v2.w, v3};
+            const int kn = k + 1 < 100 ? k + 1 : k;
+            const float* wn = wbase + kn * kW2Stride;
+            a_n = act2[kn * 64 + mp];
+            v0 = reinterpret_cast<const float4*>(wn)[0];
+            v1 = reinterpret_cast<const float4*>(wn)[1];
+            v2 = reinterpret_cast<const float4*>(wn)[2];
+            v3 = wn[12];
 #pragma unroll
             for (int t = 0; t < 13; ++t) acc[t] = ffma2(a, f2(w[t], w[t]), acc[t]);
         }
@@ -166,12 +194,18 @@ __device__ __forceinline__ void mlp_tile(float* smem) {
 #pragma unroll
         for (int t = 0; t < 7; ++t) acc[t] = f2(0.f, 0.f);
         const float* wbase = W + kOffW3 + g * 8;
-#pragma unroll 2
+        float2 a_n = act2[mp];
+        float4 v0 = reinterpret_cast<const float4*>(wbase)[0],
+               v1 = reinterpret_cast<const float4*>(wbase)[1];
+#pragma unroll 1
         for (int k = 0; k < 50; ++k) {
-            const float2 a = act2[k * 64 + mp];
-            const float4* w4 = reinterpret_cast<const float4*>(wbase + k * kW3Stride);
-            const float4 v0 = w4[0], v1 = w4[1];
+            const float2 a = a_n;
             const float w[7] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z};
+            const int kn = k + 1 < 50 ? k + 1 : k;
+            const float* wn = wbase + kn * kW3Stride;
+            a_n = act2[kn * 64 + mp];
+            v0 = reinterpret_cast<const float4*>(wn)[0];
+            v1 = reinterpret_cast<const float4*>(wn)[1];
 #pragma unroll
             for (int t = 0; t < 7; ++t) acc[t] = ffma2(a, f2(w[t], w[t]), acc[t]);
         }
@@ -228,87 +262,36 @@ __device__ __forceinline__ bool clamp_params(float p[7]) {
     return cl;
 }
 
-// ---------------------------------------------------------------------------
-// Feature stage into act: raw counts [126][ld] + DCGM [8][ld] for kernels
-// [t0, t0+128) -> act rows 0..133 (fused order).  Kernels >= n get zeros.
-__device__ __forceinline__ void load_features_from_counts(float* smem,
-                                                          const uint32_t* __restrict__ counts,
-                                                          const float* __restrict__ dcgm,
-                                                          int64_t t0, int64_t n, int64_t ld) {
-    float* act = smem + kOffAct;
-    uint32_t* acti = reinterpret_cast<uint32_t*>(act);
-    const int tid = threadIdx.x;
-    const int m = tid & (kTile - 1);
-    const int h = tid >> 7;  // 0/1
-    const int64_t k = t0 + m;
-    const bool live = k < n;
-    // phase 1: raw counts -> act rows 8.. as integer bits; DCGM -> rows 0..7
-    if (live) {
-#pragma unroll 9
-        for (int r = h; r < DSO_COUNT_ROWS; r += 2)
-            acti[(8 + r) * kTile + m] = __ldg(counts + (int64_t)r * ld + k);
-#pragma unroll
-        for (int r = h; r < 8; r += 2) act[r * kTile + m] = __ldg(dcgm + (int64_t)r * ld + k);
-    } else {
-        for (int r = h; r < DSO_COUNT_ROWS; r += 2) acti[(8 + r) * kTile + m] = 0u;
-        for (int r = h; r < 8; r += 2) act[r * kTile + m] = 0.f;
-    }
-    __syncthreads();
-    // phase 2: category totals (h=0: instr; h=1: dtype + memspace)
-    float* tot = smem + kOffOut;  // scratch [3][128] totals as (float total, float recip)
-    uint32_t* toti = reinterpret_cast<uint32_t*>(tot);
-    if (h == 0) {
-        uint64_t s = 0;
-        for (int r = 0; r < DSO_INSTR_SLOTS; ++r) s += acti[(8 + r) * kTile + m];
-        toti[0 * kTile + m] = s >= (1u << 24) ? 0xffffffffu : (uint32_t)s;
-    } else {
-        uint64_t s1 = 0, s2 = 0;
-        for (int r = 0; r < DSO_DTYPE_SLOTS; ++r)
-            s1 += acti[(8 + DSO_INSTR_SLOTS + r) * kTile + m];
-        for (int r = 0; r < DSO_MEMSPACE_SLOTS; ++r)
-            s2 += acti[(8 + DSO_INSTR_SLOTS + DSO_DTYPE_SLOTS + r) * kTile + m];
-        toti[1 * kTile + m] = s1 >= (1u << 24) ? 0xffffffffu : (uint32_t)s1;
-        toti[2 * kTile + m] = s2 >= (1u << 24) ? 0xffffffffu : (uint32_t)s2;
-    }
-    __syncthreads();
-    // phase 3: normalise in place.  Totals >= 2^24 (never produced by real PTX
-    // or the generator) recompute in FP64 from the exact integer sum.
-    for (int r = h; r < DSO_COUNT_ROWS; r += 2) {
-        const int cat = r < DSO_INSTR_SLOTS ? 0 : (r < DSO_INSTR_SLOTS + DSO_DTYPE_SLOTS ? 1 : 2);
-        const uint32_t t = toti[cat * kTile + m];
-        const uint32_t c = acti[(8 + r) * kTile + m];
-        float v;
-        if (t == 0u) {
-            v = 0.f;
-        } else if (t != 0xffffffffu) {
-            const float tf = __uint2float_rn(t), cf = __uint2float_rn(c);
-            const float rr = __frcp_rn(tf);
-            const float q = __fmul_rn(cf, rr);
-            v = fmaf(fmaf(-q, tf, cf), rr, q);
-        } else {
-            const int base = cat == 0 ? 0 : (cat == 1 ? DSO_INSTR_SLOTS : DSO_INSTR_SLOTS + DSO_DTYPE_SLOTS);
-            const int len = cat == 0 ? DSO_INSTR_SLOTS : (cat == 1 ? DSO_DTYPE_SLOTS : DSO_MEMSPACE_SLOTS);
-            uint64_t s = 0;
-            for (int i = 0; i < len; ++i) s += acti[(8 + base + i) * kTile + m];
-            v = (float)((double)c / (double)s);
-        }
-        act[(8 + r) * kTile + m] = v;
-    }
-    __syncthreads();
-}
-
-// Fused features already in HBM ([134][ld] float) -> act.
+// Fused features already in HBM ([134][ld] float) -> act.  Full tiles: 17
+// 128-bit loads per thread, all in flight; ragged / unaligned tiles: scalar.
 __device__ __forceinline__ void load_features_fused(float* smem, const float* __restrict__ fused,
-                                                    int64_t t0, int64_t n, int64_t ld) {
+                                                    int64_t t0, int64_t n, int64_t ld,
+                                                    bool vec_ok) {
     float* act = smem + kOffAct;
     const int tid = threadIdx.x;
-    const int m = tid & (kTile - 1);
-    const int h = tid >> 7;
-    const int64_t k = t0 + m;
-    const bool live = k < n;
+    if (vec_ok && t0 + kTile <= n) {
+        const int q = tid & 31, rp = tid >> 5;
+        float4 v[17];
+#pragma unroll
+        for (int j = 0; j < 17; ++j) {
+            const int r = rp + 8 * j;
+            if (r < DSO_FUSED_ROWS)
+                v[j] = __ldg(reinterpret_cast<const float4*>(fused + (int64_t)r * ld + t0) + q);
+        }
+#pragma unroll
+        for (int j = 0; j < 17; ++j) {
+            const int r = rp + 8 * j;
+            if (r < DSO_FUSED_ROWS) reinterpret_cast<float4*>(act + r * kTile)[q] = v[j];
+        }
+    } else {
+        const int m = tid & (kTile - 1);
+        const int h = tid >> 7;
+        const int64_t k = t0 + m;
+        const bool live = k < n;
 #pragma unroll 7
-    for (int r = h; r < DSO_FUSED_ROWS; r += 2)
-        act[r * kTile + m] = live ? __ldg(fused + (int64_t)r * ld + k) : 0.f;
+        for (int r = h; r < DSO_FUSED_ROWS; r += 2)
+            act[r * kTile + m] = live ? __ldg(fused + (int64_t)r * ld + k) : 0.f;
+    }
     __syncthreads();
 }
 
@@ -333,10 +316,11 @@ __global__ void __launch_bounds__(kThreads, 1) predict_kernel(
     stage_model(smem, packed);
     stage_stats(smem, stats.mean, stats.std_);
     __syncthreads();
+    const bool vec_ok = ((ld & 3) == 0) && ((reinterpret_cast<uintptr_t>(fused) & 15) == 0);
     const int64_t tiles = (n + kTile - 1) / kTile;
     for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
         const int64_t t0 = tile * kTile;
-        load_features_fused(smem, fused, t0, n, ld);
+        load_features_fused(smem, fused, t0, n, ld, vec_ok);
         mlp_tile(smem);
         if (threadIdx.x < kTile) {
             const int m = threadIdx.x;
@@ -378,6 +362,8 @@ __global__ void __launch_bounds__(kThreads, 1) pipeline_kernel(
     __syncthreads();
 
     const int64_t tiles = (n + kTile - 1) / kTile;
+    const bool vec_ok = ((ld & 3) == 0) && ((reinterpret_cast<uintptr_t>(counts) & 15) == 0) &&
+                        ((reinterpret_cast<uintptr_t>(dcgm) & 15) == 0);
     const int tid = threadIdx.x;
     const int m = tid >> 1;    // kernel within tile (2 threads per kernel)
     const int half = tid & 1;  // which half of the core levels
@@ -387,107 +373,42 @@ __global__ void __launch_bounds__(kThreads, 1) pipeline_kernel(
 
     for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
         const int64_t t0 = tile * kTile;
-        load_features_from_counts(smem, counts, dcgm, t0, n, ld);
+        tile_features(smem + kOffAct, smem + kOffOut, counts, dcgm, t0, n, ld, vec_ok);
         mlp_tile(smem);
 
         // ---- clamp + sweep + argmin: 2 threads per kernel --------------------
         const int64_t k = t0 + m;
         const float* out = smem + kOffOut;
-        float p[7];
+        float pr[7];
 #pragma unroll
-        for (int i = 0; i < 7; ++i) p[i] = out[i * kTile + m];
-        const bool cl = clamp_params(p);
-        const float p0 = p[0], kp = p[1], g = p[2], c = p[3], tt0 = p[4], a = p[5], b = p[6];
-
-        float bc = __int_as_float(0x7fc00000), be = bc;
-        int bi = i_lo * nm;
+        for (int i = 0; i < 7; ++i) pr[i] = out[i * kTile + m];
+        const bool cl = clamp_params(pr);
+        const KParams p{pr[0], pr[1], pr[2], pr[3], pr[4], pr[5], pr[6]};
+        Best b{__int_as_float(0x7fc00000), __int_as_float(0x7fc00000), i_lo * nm};
         if (i_lo < i_hi) {
-            {  // first candidate of this half taken unconditionally
-                const float4 t = s_core[i_lo];
-                const float P = __fadd_rn(pc_f32(p0, kp, c, t), __fmul_rn(g, s_mem[0].x));
-                const float T = time_f32(tt0, __fmul_rn(a, s_mem[0].y), __fmul_rn(b, t.z));
-                bc = cost_f32(eta, K, P, T);
-                be = __fmul_rn(P, T);
-            }
-            if (nm == 4) {
-                float G[4], Ta[4];
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    G[j] = __fmul_rn(g, s_mem[j].x);
-                    Ta[j] = __fmul_rn(a, s_mem[j].y);
-                }
-#pragma unroll 2
-                for (int i = i_lo; i < i_hi; ++i) {
-                    const float4 t = s_core[i];
-                    const float Pc = pc_f32(p0, kp, c, t);
-                    const float Tb = __fmul_rn(b, t.z);
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        const float P = __fadd_rn(Pc, G[j]);
-                        const float T = time_f32(tt0, Ta[j], Tb);
-                        const float C = cost_f32(eta, K, P, T);
-                        const float E = __fmul_rn(P, T);
-                        const bool better = (C < bc) | ((C == bc) & (E < be));
-                        bc = better ? C : bc;
-                        be = better ? E : be;
-                        bi = better ? i * 4 + j : bi;
-                    }
-                }
-            } else if (nm == 1) {
-                const float G0 = __fmul_rn(g, s_mem[0].x), Ta0 = __fmul_rn(a, s_mem[0].y);
-#pragma unroll 4
-                for (int i = i_lo; i < i_hi; ++i) {
-                    const float4 t = s_core[i];
-                    const float P = __fadd_rn(pc_f32(p0, kp, c, t), G0);
-                    const float T = time_f32(tt0, Ta0, __fmul_rn(b, t.z));
-                    const float C = cost_f32(eta, K, P, T);
-                    const float E = __fmul_rn(P, T);
-                    const bool better = (C < bc) | ((C == bc) & (E < be));
-                    bc = better ? C : bc;
-                    be = better ? E : be;
-                    bi = better ? i : bi;
-                }
-            } else {
-                for (int i = i_lo; i < i_hi; ++i) {
-                    const float4 t = s_core[i];
-                    const float Pc = pc_f32(p0, kp, c, t);
-                    const float Tb = __fmul_rn(b, t.z);
-                    for (int j = 0; j < nm; ++j) {
-                        const float P = __fadd_rn(Pc, __fmul_rn(g, s_mem[j].x));
-                        const float T = time_f32(tt0, __fmul_rn(a, s_mem[j].y), Tb);
-                        const float C = cost_f32(eta, K, P, T);
-                        const float E = __fmul_rn(P, T);
-                        const bool better = (C < bc) | ((C == bc) & (E < be));
-                        bc = better ? C : bc;
-                        be = better ? E : be;
-                        bi = better ? i * nm + j : bi;
-                    }
-                }
-            }
+            if (nm == 4)
+                b = sweep_levels<4>(p, s_core, s_mem, 4, i_lo, i_hi, eta, K);
+            else if (nm == 1)
+                b = sweep_levels<1>(p, s_core, s_mem, 1, i_lo, i_hi, eta, K);
+            else if (nm == 3)
+                b = sweep_levels<3>(p, s_core, s_mem, 3, i_lo, i_hi, eta, K);
+            else
+                b = sweep_levels<0>(p, s_core, s_mem, nm, i_lo, i_hi, eta, K);
         }
-        // merge the two halves: the upper half (higher indices) wins only when
-        // strictly better, exactly as the sequential visit order would decide
-        const float oc = __shfl_xor_sync(0xffffffffu, bc, 1);
-        const float oe = __shfl_xor_sync(0xffffffffu, be, 1);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, 1);
+        // merge the two halves (the upper half holds the later pairs)
+        Best o;
+        o.c = __shfl_xor_sync(0xffffffffu, b.c, 1);
+        o.e = __shfl_xor_sync(0xffffffffu, b.e, 1);
+        o.i = __shfl_xor_sync(0xffffffffu, b.i, 1);
         if (half == 0 && k < n) {
-            const bool upper_valid = i_split < nc;
-            const bool take = upper_valid && ((oc < bc) | ((oc == bc) & (oe < be)));
-            if (take) {
-                bc = oc;
-                be = oe;
-                bi = oi;
-            }
-            idx_out[k] = bi;
-            if (cost_out) cost_out[k] = bc;
-            if (energy_out) energy_out[k] = be;
-            if (time_out) {
-                const int i = bi / nm, j = bi - i * nm;
-                time_out[k] = time_f32(tt0, __fmul_rn(a, s_mem[j].y), __fmul_rn(b, s_core[i].z));
-            }
+            if (i_split < nc) merge_best(b, o);
+            idx_out[k] = b.i;
+            if (cost_out) cost_out[k] = b.c;
+            if (energy_out) energy_out[k] = b.e;
+            if (time_out) time_out[k] = time_at(p, s_core, s_mem, nm, b.i);
             if (params_out)
 #pragma unroll
-                for (int i = 0; i < 7; ++i) params_out[i * ld_out + k] = p[i];
+                for (int i = 0; i < 7; ++i) params_out[i * ld_out + k] = pr[i];
             if (clamped_out) clamped_out[k] = cl ? 1 : 0;
         }
         __syncthreads();  // out/act reused by the next tile

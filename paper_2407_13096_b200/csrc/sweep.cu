@@ -21,6 +21,7 @@
 #include <math.h>
 
 #include "common.cuh"
+#include "sweep_core.cuh"
 
 namespace dso_b200 {
 
@@ -51,11 +52,15 @@ __global__ void __launch_bounds__(kBlock) sweep_f32_kernel(
 
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride) {
-        const float p0 = __ldg(params + k), kp = __ldg(params + ld + k),
-                    g = __ldg(params + 2 * ld + k), c = __ldg(params + 3 * ld + k),
-                    t0 = __ldg(params + 4 * ld + k), a = __ldg(params + 5 * ld + k),
-                    b = __ldg(params + 6 * ld + k);
-        if (params_invalid(p0, kp, g, c, t0, a, b)) {
+        KParams p;
+        p.p0 = __ldg(params + k);
+        p.kp = __ldg(params + ld + k);
+        p.g = __ldg(params + 2 * ld + k);
+        p.c = __ldg(params + 3 * ld + k);
+        p.t0 = __ldg(params + 4 * ld + k);
+        p.a = __ldg(params + 5 * ld + k);
+        p.b = __ldg(params + 6 * ld + k);
+        if (params_invalid(p.p0, p.kp, p.g, p.c, p.t0, p.a, p.b)) {
             idx[k] = -1;
             if (cost) cost[k] = __int_as_float(0x7fc00000);
             if (energy) energy[k] = __int_as_float(0x7fc00000);
@@ -63,64 +68,11 @@ __global__ void __launch_bounds__(kBlock) sweep_f32_kernel(
             if (kstatus) kstatus[k] = kInvalidArgument;
             continue;
         }
-        // first candidate taken unconditionally (optimizer.cpp:103, have_best)
-        float bc, be;
-        int bi = 0;
-        {
-            const float4 t = s_core[0];
-            const float P = __fadd_rn(pc_f32(p0, kp, c, t), __fmul_rn(g, s_mem[0].x));
-            const float T = time_f32(t0, __fmul_rn(a, s_mem[0].y), __fmul_rn(b, t.z));
-            bc = cost_f32(eta, K, P, T);
-            be = __fmul_rn(P, T);
-        }
-        if constexpr (NM > 0) {
-            float G[NM], Ta[NM];
-#pragma unroll
-            for (int j = 0; j < NM; ++j) {
-                G[j] = __fmul_rn(g, s_mem[j].x);
-                Ta[j] = __fmul_rn(a, s_mem[j].y);
-            }
-#pragma unroll 2
-            for (int i = 0; i < nc; ++i) {
-                const float4 t = s_core[i];
-                const float Pc = pc_f32(p0, kp, c, t);
-                const float Tb = __fmul_rn(b, t.z);
-#pragma unroll
-                for (int j = 0; j < NM; ++j) {
-                    const float P = __fadd_rn(Pc, G[j]);
-                    const float T = time_f32(t0, Ta[j], Tb);
-                    const float C = cost_f32(eta, K, P, T);
-                    const float E = __fmul_rn(P, T);
-                    const bool better = (C < bc) | ((C == bc) & (E < be));
-                    bc = better ? C : bc;
-                    be = better ? E : be;
-                    bi = better ? i * NM + j : bi;
-                }
-            }
-        } else {
-            for (int i = 0; i < nc; ++i) {
-                const float4 t = s_core[i];
-                const float Pc = pc_f32(p0, kp, c, t);
-                const float Tb = __fmul_rn(b, t.z);
-                for (int j = 0; j < nm; ++j) {
-                    const float P = __fadd_rn(Pc, __fmul_rn(g, s_mem[j].x));
-                    const float T = time_f32(t0, __fmul_rn(a, s_mem[j].y), Tb);
-                    const float C = cost_f32(eta, K, P, T);
-                    const float E = __fmul_rn(P, T);
-                    const bool better = (C < bc) | ((C == bc) & (E < be));
-                    bc = better ? C : bc;
-                    be = better ? E : be;
-                    bi = better ? i * nm + j : bi;
-                }
-            }
-        }
-        idx[k] = bi;
-        if (cost) cost[k] = bc;
-        if (energy) energy[k] = be;
-        if (time) {
-            const int i = bi / nm, j = bi - i * nm;
-            time[k] = time_f32(t0, __fmul_rn(a, s_mem[j].y), __fmul_rn(b, s_core[i].z));
-        }
+        const Best b = sweep_levels<NM>(p, s_core, s_mem, nm, 0, nc, eta, K);
+        idx[k] = b.i;
+        if (cost) cost[k] = b.c;
+        if (energy) energy[k] = b.e;
+        if (time) time[k] = time_at(p, s_core, s_mem, nm, b.i);
         if (kstatus) kstatus[k] = 0;
     }
 }

@@ -1,0 +1,155 @@
+// sweep_core.cuh — the per-kernel grid sweep shared by every sweep kernel.
+//
+// brute_force_config (reference proj/src/optimizer.cpp:90-117) visits pairs in
+// (fc outer, fm inner) order and keeps the first candidate unless a later one
+// is strictly better (better(), optimizer.cpp:27-32: cost, then energy; vc and
+// fm are the visit order).  Here the visit is split into independent chains
+// (one per memory level, or four interleaved core levels when nm == 1) so the
+// comparator's dependency chain does not serialise the pipe; each chain keeps
+// the reference's sequential rule over its own (increasing) pairs, and
+// merge_best combines chains exactly as the single sequential scan would.
+#pragma once
+
+#include "common.cuh"
+
+namespace dso_b200 {
+
+struct Best {
+    float c, e;
+    int i;
+};
+
+// Sequential visit-order update: a later pair wins only when strictly better.
+__device__ __forceinline__ void upd_best(Best& b, float C, float E, int id) {
+    const bool better = (C < b.c) | ((C == b.c) & (E < b.e));
+    b.c = better ? C : b.c;
+    b.e = better ? E : b.e;
+    b.i = better ? id : b.i;
+}
+
+// Merge two chains' results into what one sequential scan over both would keep.
+// Equal costs: the earlier pair survives unless the later one has strictly
+// lower energy (so unordered/NaN energies keep the earlier one, as better()
+// does).  NaN costs never win (a NaN-cost first pair is never replaced).
+__device__ __forceinline__ void merge_best(Best& a, const Best& o) {
+    bool take = false;
+    if (o.c < a.c) {
+        take = true;
+    } else if (o.c == a.c) {
+        take = (o.i < a.i) ? !(a.e < o.e) : (o.e < a.e);
+    }
+    if (take) a = o;
+}
+
+struct KParams {
+    float p0, kp, g, c, t0, a, b;
+};
+
+__device__ __forceinline__ void eval_pair(const KParams& p, float Pc, float Tb, float G, float Ta,
+                                          float eta, float K, float& C, float& E) {
+    const float P = __fadd_rn(Pc, G);
+    const float T = time_f32(p.t0, Ta, Tb);
+    C = cost_f32(eta, K, P, T);
+    E = __fmul_rn(P, T);
+}
+
+// Sweep core levels [i_lo, i_hi) (non-empty) x all memory levels.
+template <int NM>
+__device__ __forceinline__ Best sweep_levels(const KParams& p, const float4* __restrict__ s_core,
+                                             const float2* __restrict__ s_mem, int nm_rt, int i_lo,
+                                             int i_hi, float eta, float K) {
+    if constexpr (NM >= 2 && NM <= 4) {
+        float G[NM], Ta[NM];
+#pragma unroll
+        for (int j = 0; j < NM; ++j) {
+            G[j] = __fmul_rn(p.g, s_mem[j].x);
+            Ta[j] = __fmul_rn(p.a, s_mem[j].y);
+        }
+        Best ch[NM];
+        {
+            const float4 t = s_core[i_lo];
+            const float Pc = pc_f32(p.p0, p.kp, p.c, t);
+            const float Tb = __fmul_rn(p.b, t.z);
+#pragma unroll
+            for (int j = 0; j < NM; ++j) {
+                eval_pair(p, Pc, Tb, G[j], Ta[j], eta, K, ch[j].c, ch[j].e);
+                ch[j].i = i_lo * NM + j;
+            }
+        }
+#pragma unroll 2
+        for (int i = i_lo + 1; i < i_hi; ++i) {
+            const float4 t = s_core[i];
+            const float Pc = pc_f32(p.p0, p.kp, p.c, t);
+            const float Tb = __fmul_rn(p.b, t.z);
+#pragma unroll
+            for (int j = 0; j < NM; ++j) {
+                float C, E;
+                eval_pair(p, Pc, Tb, G[j], Ta[j], eta, K, C, E);
+                upd_best(ch[j], C, E, i * NM + j);
+            }
+        }
+#pragma unroll
+        for (int j = 1; j < NM; ++j) merge_best(ch[0], ch[j]);
+        return ch[0];
+    } else if constexpr (NM == 1) {
+        const float G = __fmul_rn(p.g, s_mem[0].x);
+        const float Ta = __fmul_rn(p.a, s_mem[0].y);
+        Best ch[4];
+        {
+            const float4 t = s_core[i_lo];
+            eval_pair(p, pc_f32(p.p0, p.kp, p.c, t), __fmul_rn(p.b, t.z), G, Ta, eta, K, ch[0].c,
+                      ch[0].e);
+            ch[0].i = i_lo;
+            ch[1] = ch[2] = ch[3] = ch[0];
+        }
+        int i = i_lo + 1;
+        for (; i + 3 < i_hi; i += 4) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const float4 t = s_core[i + u];
+                float C, E;
+                eval_pair(p, pc_f32(p.p0, p.kp, p.c, t), __fmul_rn(p.b, t.z), G, Ta, eta, K, C, E);
+                upd_best(ch[u], C, E, i + u);
+            }
+        }
+        for (; i < i_hi; ++i) {
+            const float4 t = s_core[i];
+            float C, E;
+            eval_pair(p, pc_f32(p.p0, p.kp, p.c, t), __fmul_rn(p.b, t.z), G, Ta, eta, K, C, E);
+            upd_best(ch[0], C, E, i);
+        }
+        merge_best(ch[0], ch[1]);
+        merge_best(ch[0], ch[2]);
+        merge_best(ch[0], ch[3]);
+        return ch[0];
+    } else {
+        const int nm = nm_rt;
+        Best b;
+        {
+            const float4 t = s_core[i_lo];
+            eval_pair(p, pc_f32(p.p0, p.kp, p.c, t), __fmul_rn(p.b, t.z),
+                      __fmul_rn(p.g, s_mem[0].x), __fmul_rn(p.a, s_mem[0].y), eta, K, b.c, b.e);
+            b.i = i_lo * nm;
+        }
+        for (int i = i_lo; i < i_hi; ++i) {
+            const float4 t = s_core[i];
+            const float Pc = pc_f32(p.p0, p.kp, p.c, t);
+            const float Tb = __fmul_rn(p.b, t.z);
+            for (int j = 0; j < nm; ++j) {
+                float C, E;
+                eval_pair(p, Pc, Tb, __fmul_rn(p.g, s_mem[j].x), __fmul_rn(p.a, s_mem[j].y), eta,
+                          K, C, E);
+                upd_best(b, C, E, i * nm + j);
+            }
+        }
+        return b;
+    }
+}
+
+__device__ __forceinline__ float time_at(const KParams& p, const float4* s_core,
+                                         const float2* s_mem, int nm, int idx) {
+    const int i = idx / nm, j = idx - i * nm;
+    return time_f32(p.t0, __fmul_rn(p.a, s_mem[j].y), __fmul_rn(p.b, s_core[i].z));
+}
+
+}  // namespace dso_b200

@@ -1,0 +1,19 @@
+#!/bin/bash
+# One gpurun session: GPU tests, smoke, short bench, launch list + one full ncu capture.
+# Usage (from the build container):
+#   gpurun --timeout 2400 -- bash scripts/gpu_check.sh [tag]
+set -u
+TAG=${1:-r1}
+OUT=gpurun_out/$TAG
+mkdir -p $OUT
+nvidia-smi > $OUT/nvidia-smi.txt 2>&1
+nvidia-smi -q -d CLOCK >> $OUT/nvidia-smi.txt 2>&1
+nproc > $OUT/nproc.txt; lscpu >> $OUT/nproc.txt 2>&1
+( timeout 1200 python -m pytest tests -q -m gpu --timeout 600 -rf > $OUT/pytest_gpu.log 2>&1; echo "rc=$?" >> $OUT/pytest_gpu.log ) 
+( timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "rc=$?" >> $OUT/smoke.log )
+( timeout 900 python bench.py --steps 10 --warmup 3 > $OUT/bench.log 2>&1; echo "rc=$?" >> $OUT/bench.log )
+( timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv \
+    python bench.py --steps 2 --warmup 1 --kernels 4194304 --no-e2e --no-cpu > $OUT/ncu_launch_bench.log 2>&1; echo "rc=$?" >> $OUT/ncu_launch_bench.log )
+( timeout 900 ncu --set full --clock-control none --import-source on -k regex:pipeline_kernel -s 1 -c 1 \
+    -o $OUT/prof_pipeline python bench.py --steps 1 --warmup 1 --kernels 1048576 --no-e2e --no-cpu --no-stages > $OUT/ncu_full.log 2>&1; echo "rc=$?" >> $OUT/ncu_full.log )
+ls -la $OUT
