@@ -101,17 +101,19 @@ __device__ __forceinline__ void tile_features(float* act, float* scratch,
         scale(2, s_c);
     }
     __syncthreads();
-    // phase 3: normalise in place, 4 kernels x 16 rows per thread
+    // phase 3: normalise, 4 kernels x 16 rows per thread.  All results are
+    // computed before any is stored (the FP64 path for totals >= 2^24 re-reads
+    // raw counts of other rows), then written in place after a barrier.
     {
         const int q = tid & 31;
         const int rp = tid >> 5;
-#pragma unroll 4
+        float4 res[16];
+#pragma unroll
         for (int j = 0; j < 16; ++j) {
             const int r = rp + 8 * j;
             if (r >= DSO_COUNT_ROWS) break;
             const int cat = r < DSO_INSTR_SLOTS ? 0 : (r < DSO_INSTR_SLOTS + DSO_DTYPE_SLOTS ? 1 : 2);
-            uint4* rowp = reinterpret_cast<uint4*>(acti + (8 + r) * kFeatTile) + q;
-            const uint4 c = *rowp;
+            const uint4 c = reinterpret_cast<const uint4*>(acti + (8 + r) * kFeatTile)[q];
             const float4 tf = reinterpret_cast<const float4*>(tfv + cat * kFeatTile)[q];
             const float4 rr = reinterpret_cast<const float4*>(rrv + cat * kFeatTile)[q];
             const uint32_t cc[4] = {c.x, c.y, c.z, c.w};
@@ -134,7 +136,14 @@ __device__ __forceinline__ void tile_features(float* act, float* scratch,
                     o[e] = (float)((double)cc[e] / (double)s);
                 }
             }
-            *reinterpret_cast<float4*>(rowp) = make_float4(o[0], o[1], o[2], o[3]);
+            res[j] = make_float4(o[0], o[1], o[2], o[3]);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            const int r = rp + 8 * j;
+            if (r >= DSO_COUNT_ROWS) break;
+            reinterpret_cast<float4*>(act + (8 + r) * kFeatTile)[q] = res[j];
         }
     }
     __syncthreads();

@@ -103,42 +103,50 @@ __device__ __forceinline__ void mlp_tile(float* smem) {
     const int mp = tid & 63;  // kernel pair: kernels 2mp, 2mp+1
     const int g = tid >> 6;   // neuron group (uniform per warp)
 
+    // Each layer's k-loop is software-pipelined over two register stages (A, B):
+    // the operands of step k+1 are in flight while step k's FFMA2s issue, and
+    // the stages alternate without register copies.  Only 2 warps share a
+    // scheduler, so shared-memory latency is hidden by this ILP, not by TLP.
     // ---- L1: 134 -> 100 (neurons 26g .. 26g+25), pairs along n -------------
-    // Operands of step k+1 are loaded while step k's 26 FFMA2 issue (explicit
-    // register double buffering: only 2 warps per scheduler, so the shared-
-    // memory latency must be covered by ILP, not by other warps).
     {
         float2 acc0[13], acc1[13];
 #pragma unroll
         for (int p = 0; p < 13; ++p) acc0[p] = acc1[p] = f2(0.f, 0.f);
         const float* wbase = W + kOffW1 + g * 28;
-        float2 a_n = act2[mp];
-        float4 v_n[6];
-        float2 l_n;
+        struct Op {
+            float2 a;
+            float4 v[6];
+            float2 l;
+        };
+        auto load = [&](Op& o, int k) {
+            const float* w = wbase + k * kW1Stride;
+            o.a = act2[k * 64 + mp];
 #pragma unroll
-        for (int q = 0; q < 6; ++q) v_n[q] = reinterpret_cast<const float4*>(wbase)[q];
-        l_n = reinterpret_cast<const float2*>(wbase)[12];
-#pragma unroll 1
-        for (int k = 0; k < 134; ++k) {
-            const float2 a = a_n;
+            for (int q = 0; q < 6; ++q) o.v[q] = reinterpret_cast<const float4*>(w)[q];
+            o.l = reinterpret_cast<const float2*>(w)[12];
+        };
+        auto math = [&](const Op& o) {
             float2 w[13];
 #pragma unroll
             for (int q = 0; q < 6; ++q) {
-                w[2 * q] = f2(v_n[q].x, v_n[q].y);
-                w[2 * q + 1] = f2(v_n[q].z, v_n[q].w);
+                w[2 * q] = f2(o.v[q].x, o.v[q].y);
+                w[2 * q + 1] = f2(o.v[q].z, o.v[q].w);
             }
-            w[12] = l_n;
-            const int kn = k + 1 < 134 ? k + 1 : k;
-            const float* wn = wbase + kn * kW1Stride;
-            a_n = act2[kn * 64 + mp];
-#pragma unroll
-            for (int q = 0; q < 6; ++q) v_n[q] = reinterpret_cast<const float4*>(wn)[q];
-            l_n = reinterpret_cast<const float2*>(wn)[12];
+            w[12] = o.l;
 #pragma unroll
             for (int p = 0; p < 13; ++p) {
-                acc0[p] = ffma2(f2(a.x, a.x), w[p], acc0[p]);
-                acc1[p] = ffma2(f2(a.y, a.y), w[p], acc1[p]);
+                acc0[p] = ffma2(f2(o.a.x, o.a.x), w[p], acc0[p]);
+                acc1[p] = ffma2(f2(o.a.y, o.a.y), w[p], acc1[p]);
             }
+        };
+        Op A, B;
+        load(A, 0);
+#pragma unroll 1
+        for (int k = 0; k < 134; k += 2) {
+            load(B, k + 1);
+            math(A);
+            load(A, k + 2 < 134 ? k + 2 : 133);
+            math(B);
         }
         __syncthreads();  // all reads of act done
         const float* b = W + kOffB1 + g * 26;
@@ -158,25 +166,33 @@ __device__ __forceinline__ void mlp_tile(float* smem) {
 #pragma unroll
         for (int t = 0; t < 13; ++t) acc[t] = f2(0.f, 0.f);
         const float* wbase = W + kOffW2 + g * 16;
-        float2 a_n = act2[mp];
-        float4 v0 = reinterpret_cast<const float4*>(wbase)[0],
-               v1 = reinterpret_cast<const float4*>(wbase)[1],
-               v2 = reinterpret_cast<const float4*>(wbase)[2];
-        float v3 = wbase[12];
-#pragma unroll 1
-        for (int k = 0; k < 100; ++k) {
-            const float2 a = a_n;
-            const float w[13] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z,
-                                 v1.w, v2.x, v2.y, v2.z, v2.w, v3};
-            const int kn = k + 1 < 100 ? k + 1 : k;
-            const float* wn = wbase + kn * kW2Stride;
-            a_n = act2[kn * 64 + mp];
-            v0 = reinterpret_cast<const float4*>(wn)[0];
-            v1 = reinterpret_cast<const float4*>(wn)[1];
-            v2 = reinterpret_cast<const float4*>(wn)[2];
-            v3 = wn[12];
+        struct Op {
+            float2 a;
+            float4 v0, v1, v2;
+            float v3;
+        };
+        auto load = [&](Op& o, int k) {
+            const float* w = wbase + k * kW2Stride;
+            o.a = act2[k * 64 + mp];
+            o.v0 = reinterpret_cast<const float4*>(w)[0];
+            o.v1 = reinterpret_cast<const float4*>(w)[1];
+            o.v2 = reinterpret_cast<const float4*>(w)[2];
+            o.v3 = w[12];
+        };
+        auto math = [&](const Op& o) {
+            const float w[13] = {o.v0.x, o.v0.y, o.v0.z, o.v0.w, o.v1.x, o.v1.y, o.v1.z,
+                                 o.v1.w, o.v2.x, o.v2.y, o.v2.z, o.v2.w, o.v3};
 #pragma unroll
-            for (int t = 0; t < 13; ++t) acc[t] = ffma2(a, f2(w[t], w[t]), acc[t]);
+            for (int t = 0; t < 13; ++t) acc[t] = ffma2(o.a, f2(w[t], w[t]), acc[t]);
+        };
+        Op A, B;
+        load(A, 0);
+#pragma unroll 1
+        for (int k = 0; k < 100; k += 2) {
+            load(B, k + 1);
+            math(A);
+            load(A, k + 2 < 100 ? k + 2 : 99);
+            math(B);
         }
         __syncthreads();
         const float* b = W + kOffB2 + g * 13;
@@ -194,20 +210,29 @@ __device__ __forceinline__ void mlp_tile(float* smem) {
 #pragma unroll
         for (int t = 0; t < 7; ++t) acc[t] = f2(0.f, 0.f);
         const float* wbase = W + kOffW3 + g * 8;
-        float2 a_n = act2[mp];
-        float4 v0 = reinterpret_cast<const float4*>(wbase)[0],
-               v1 = reinterpret_cast<const float4*>(wbase)[1];
-#pragma unroll 1
-        for (int k = 0; k < 50; ++k) {
-            const float2 a = a_n;
-            const float w[7] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z};
-            const int kn = k + 1 < 50 ? k + 1 : k;
-            const float* wn = wbase + kn * kW3Stride;
-            a_n = act2[kn * 64 + mp];
-            v0 = reinterpret_cast<const float4*>(wn)[0];
-            v1 = reinterpret_cast<const float4*>(wn)[1];
+        struct Op {
+            float2 a;
+            float4 v0, v1;
+        };
+        auto load = [&](Op& o, int k) {
+            const float* w = wbase + k * kW3Stride;
+            o.a = act2[k * 64 + mp];
+            o.v0 = reinterpret_cast<const float4*>(w)[0];
+            o.v1 = reinterpret_cast<const float4*>(w)[1];
+        };
+        auto math = [&](const Op& o) {
+            const float w[7] = {o.v0.x, o.v0.y, o.v0.z, o.v0.w, o.v1.x, o.v1.y, o.v1.z};
 #pragma unroll
-            for (int t = 0; t < 7; ++t) acc[t] = ffma2(a, f2(w[t], w[t]), acc[t]);
+            for (int t = 0; t < 7; ++t) acc[t] = ffma2(o.a, f2(w[t], w[t]), acc[t]);
+        };
+        Op A, B;
+        load(A, 0);
+#pragma unroll 1
+        for (int k = 0; k < 50; k += 2) {
+            load(B, k + 1);
+            math(A);
+            load(A, k + 2 < 50 ? k + 2 : 49);
+            math(B);
         }
         __syncthreads();
         const float* b = W + kOffB3 + g * 7;

@@ -89,7 +89,7 @@ def test_sweep_large_vs_reference(ctx, ref):
     ctx.set_domain(dom)
     n = 200_000
     gen = ctx.gen_synthetic(n, root=0xD50B203, counts=False, dcgm=False)
-    p32 = gen["params"].cpu().numpy().T.astype(np.float64)
+    p32 = np.ascontiguousarray(gen["params"].cpu().numpy().T.astype(np.float64))
     dev = dom.dev.as_array()
     for eta in (0.0, 0.5, 0.8, 1.0):
         r = ctx.brute_force_config(gen["params"], eta)
@@ -116,7 +116,7 @@ def test_eta_sweep_matches_single_eta(ctx, ref):
     etas = np.arange(101) / 100.0
     idx, cost = ctx.eta_sweep(gen["params"], etas)
     idx, cost = idx.cpu().numpy(), cost.cpu().numpy()
-    p32 = gen["params"].cpu().numpy().T.astype(np.float64)
+    p32 = np.ascontiguousarray(gen["params"].cpu().numpy().T.astype(np.float64))
     for e in (0, 1, 17, 50, 80, 99, 100):
         r = ctx.brute_force_config(gen["params"], float(etas[e]))
         np.testing.assert_array_equal(idx[e], r["idx"].cpu().numpy())
