@@ -44,7 +44,11 @@ CONFIGS = {
                desc="C3: 16M kernels x 128 core x 4 mem freqs per GPU, eta 0.8"),
     "c4": dict(n=1 << 22, nc=128, nm=4, eta=None,
                desc="C4: 101 etas (0.00..1.00) x 4M kernels x 128 core x 4 mem"),
+    "c5": dict(n=10_000_000, nc=128, nm=4, eta=None, batch=65536,
+               desc="C5: predictor training, 10M synthetic samples per GPU, "
+                    "65,536-sample batch per GPU, NCCL grad allreduce"),
 }
+TRAIN_FLOPS = 92_150  # per sample-step, SURVEY.md §8(d)
 
 
 def env_int(name, default):
@@ -239,6 +243,8 @@ def run_ours(args, rank, world, local_rank):
     ctx.set_model(model)
     stream = torch.cuda.current_stream(dev)
 
+    if args.config == "c5":
+        return run_train(args, rank, world, local_rank, ctx, dom, model, n)
     # inputs: this rank's shard [rank*n, (rank+1)*n) of the global synthetic stream
     gen = ctx.gen_synthetic(n, root=ROOT_SEED, first=rank * n, params=(args.config == "c4"))
     counts, dcgm = gen["counts"], gen["dcgm"]
@@ -361,6 +367,92 @@ def run_ours(args, rank, world, local_rank):
     }
     if args.config == "c4":
         line["triples_per_s"] = value * 101
+    print(json.dumps(line), flush=True)
+
+
+def run_train(args, rank, world, local_rank, ctx, dom, model, n):
+    """C5: synchronous data-parallel SGD steps (device grad -> NCCL allreduce ->
+    device update) over a device-resident 10M-sample shard per GPU."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2407_13096_b200.train import DataParallelTrainer
+    cfg = CONFIGS["c5"]
+    dev = torch.device("cuda", local_rank)
+    stream = torch.cuda.current_stream(dev)
+    B = cfg["batch"]
+    gen = ctx.gen_synthetic(n, root=0xACCE5505, first=rank * n)
+    x = ctx.featurize(gen["counts"], gen["dcgm"])
+    del gen["counts"]
+    p = gen["params"].double()
+    mean = torch.tensor(model.target_mean, dtype=torch.float64, device=dev)
+    std = torch.tensor(model.target_std, dtype=torch.float64, device=dev)
+    y = ((p - mean[:, None]) / std[:, None]).float().contiguous()
+    del p, gen
+    tr = DataParallelTrainer(ctx, lr=0.1)
+    nb = n // B
+    grad = torch.empty((ctx.n_model_params,), dtype=torch.float32, device=dev)
+
+    def step(i):
+        s = (i % nb) * B
+        g, loss = ctx.train_grad_slice(x, y, s, B, grad=grad)
+        tr.allreduce(g)
+        tr.allreduce(loss)
+        ctx.train_apply(g, tr.lr, 1.0 / (B * world * 7))
+        return loss
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    barrier()
+    launches0 = ctx.launch_count
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(list(range(world)) if world > 1 else [local_rank]) as clk:
+        e0.record(stream)
+        for i in range(args.steps):
+            step(args.warmup + i)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    ms = e0.elapsed_time(e1) / args.steps
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    # grad kernel alone (share of the step)
+    a = torch.cuda.Event(enable_timing=True)
+    bb = torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for i in range(5):
+        ctx.train_grad_slice(x, y, (i % nb) * B, B, grad=grad)
+    bb.record(stream)
+    torch.cuda.synchronize()
+    grad_ms = a.elapsed_time(bb) / 5
+    if rank != 0:
+        return
+    value = B * world / (ms_max * 1e-3)
+    achieved = B * TRAIN_FLOPS / (grad_ms * 1e-3) / 1e12
+    v = __import__("ctypes").c_double()
+    from paper_2407_13096_b200 import _lib
+    ctx._raise(_lib.lib().dso_probe_fp32_peak(ctx._h, 1, __import__("ctypes").byref(v)))
+    line = {
+        "metric": "predictor training sample-steps/s (C5)", "value": value,
+        "unit": "samples/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (gen_kernel stream generated on device)",
+        "config": {"workload": cfg["desc"], "samples_per_gpu": n, "batch_per_gpu": B,
+                   "global_batch": B * world, "parallelism": f"dp{world} (NCCL allreduce)"},
+        "roofline": {"bound": "fp32", "achieved": achieved, "peak": v.value, "unit": "TFLOP/s",
+                     "frac": achieved / v.value, "traffic": None, "kernel": "train_grad_kernel",
+                     "flops_per_sample": TRAIN_FLOPS, "grad_kernel_ms": grad_ms},
+        "gpu_launches": ctx.launch_count - launches0, "clocks": clk.summary(),
+    }
     print(json.dumps(line), flush=True)
 
 

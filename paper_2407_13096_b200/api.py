@@ -335,6 +335,21 @@ class Context:
                                              _ptr(loss)))
         return grad, loss
 
+    def train_grad_slice(self, x, y_std, start: int, count: int, grad=None):
+        """train_grad on columns [start, start+count) of [134, ld] / [7, ld] tensors
+        (a batch of a device-resident dataset, no copy)."""
+        _check(x, torch.float32, 134, "x")
+        _check(y_std, torch.float32, 7, "y_std")
+        ld = x.shape[1]
+        if y_std.shape[1] != ld or start < 0 or start + count > ld:
+            raise DsoError(ErrorKind.InvalidArgument, "slice outside the dataset")
+        if grad is None:
+            grad = self._empty((self.n_model_params,), torch.float32)
+        loss = self._empty((1,), torch.float64)
+        self._raise(self._lib.dso_train_grad(self._h, _ptr(x) + 4 * start, _ptr(y_std) + 4 * start,
+                                             count, ld, _ptr(grad), _ptr(loss)))
+        return grad, loss
+
     def train_apply(self, grad, lr: float, scale: float) -> None:
         """W -= lr * scale * grad on the device model (mlp.cpp:254-257)."""
         self._raise(self._lib.dso_train_apply(self._h, _ptr(grad), lr, scale))

@@ -184,6 +184,7 @@ int32_t dso_ctx_destroy(dso_ctx* ctx) {
     cudaFree(c.model.wt);
     cudaFree(c.model.w_master);
     cudaFree(c.scratch);
+    cudaFree(c.train_scratch);
     for (auto& s : c.aux)
         if (s) cudaStreamDestroy(s);
     for (auto& ev : c.ev)

@@ -80,6 +80,8 @@ struct Ctx {
     cudaStream_t aux[3] = {nullptr, nullptr, nullptr};
     cudaEvent_t ev[8] = {};
     int num_sms = 148;
+    void* train_scratch = nullptr;  // per-CTA partial gradients
+    size_t train_scratch_bytes = 0;
 };
 
 }  // namespace dso_b200
@@ -117,6 +119,7 @@ cudaError_t model_upload(Ctx& c, const double* W, const double* b);
 cudaError_t launch_train_grad(Ctx& c, const float* x, const float* y, int64_t n, int64_t ld,
                               float* grad, double* loss_sum_dev);
 cudaError_t launch_train_apply(Ctx& c, const float* grad, float lr_scale);
+cudaError_t launch_repack(Ctx& c);  // w_master (f32, reference layout) -> packed wt
 size_t mlp_smem_bytes();
 
 // ---- device helpers ---------------------------------------------------------
@@ -144,6 +147,15 @@ __device__ __forceinline__ float time_f32(float t0, float ta, float tb) {
 }
 __device__ __forceinline__ float cost_f32(float eta, float K, float P, float T) {
     return __fmul_rn(fmaf(eta, P, K), T);
+}
+
+// sigmoid (mlp.cpp:166-168) in FP32: 1 / (1 + 2^(-z log2 e)) with the
+// approximate MUFU ex2/rcp (rel. error ~2^-22 each; no denormal fix-up code).
+__device__ __forceinline__ float sigmoidf_fast(float z) {
+    float e, r;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(z * -1.4426950408889634f));
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(1.0f + e));
+    return r;
 }
 
 inline int grid_for(int64_t n, int block, int num_sms, int per_sm) {

@@ -73,15 +73,6 @@ static_assert(kOffW2 % 4 == 0 && kOffW3 % 4 == 0 && kOffW4 % 4 == 0 && kOffB1 % 
 
 __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
 
-// sigmoid (mlp.cpp:166-168) in FP32: 1 / (1 + 2^(-z log2 e)) with the
-// approximate MUFU ex2/rcp (rel. error ~2^-22 each; no denormal fix-up code).
-__device__ __forceinline__ float sigmoidf_fast(float z) {
-    float e, r;
-    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(z * -1.4426950408889634f));
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(1.0f + e));
-    return r;
-}
-
 // ---------------------------------------------------------------------------
 // Stage the packed model into shared memory (once per CTA).
 __device__ __forceinline__ void stage_model(float* smem, const float* __restrict__ packed) {
@@ -492,6 +483,42 @@ cudaError_t model_upload(Ctx& cx, const double* W, const double* b) {
     md.wt_floats = kModelFloats;
     return cudaMemcpyAsync(md.wt, pk.data(), sizeof(float) * kModelFloats,
                            cudaMemcpyHostToDevice, cx.stream);
+}
+
+// Device-side repack of the master weights (reference layout, f32) into the
+// packed inference layout, after a training update.  Padding stays zero.
+__global__ void repack_kernel(const float* __restrict__ master, float* __restrict__ pk) {
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    constexpr int MW2 = 100 * 134, MW3 = MW2 + 50 * 100, MW4 = MW3 + 25 * 50;
+    constexpr int MB1 = MW4 + 7 * 25, MB2 = MB1 + 100, MB3 = MB2 + 50, MB4 = MB3 + 25;
+    if (e < MW2) {
+        const int nn = e / 134, k = e - nn * 134;
+        pk[kOffW1 + k * kW1Stride + (nn / 26) * 28 + nn % 26] = master[e];
+    } else if (e < MW3) {
+        const int f = e - MW2, nn = f / 100, k = f - nn * 100;
+        pk[kOffW2 + k * kW2Stride + (nn / 13) * 16 + nn % 13] = master[e];
+    } else if (e < MW4) {
+        const int f = e - MW3, nn = f / 50, k = f - nn * 50;
+        pk[kOffW3 + k * kW3Stride + (nn / 7) * 8 + nn % 7] = master[e];
+    } else if (e < MB1) {
+        const int f = e - MW4, nn = f / 25, k = f - nn * 25;
+        pk[kOffW4 + k * kW4Stride + nn] = master[e];
+    } else if (e < MB2) {
+        pk[kOffB1 + e - MB1] = master[e];
+    } else if (e < MB3) {
+        pk[kOffB2 + e - MB2] = master[e];
+    } else if (e < MB4) {
+        pk[kOffB3 + e - MB3] = master[e];
+    } else if (e < MB4 + 7) {
+        pk[kOffB4 + e - MB4] = master[e];
+    }
+}
+
+cudaError_t launch_repack(Ctx& cx) {
+    const int total = 100 * 134 + 50 * 100 + 25 * 50 + 7 * 25 + 182;
+    repack_kernel<<<(total + 255) / 256, 256, 0, cx.stream>>>(cx.model.w_master, cx.model.wt);
+    ++cx.launches;
+    return cudaGetLastError();
 }
 
 static Stats stats_of(const Ctx& cx) {

@@ -1,0 +1,108 @@
+"""GPU parity: predictor training step vs the oracle (analytic_gradients, mse_loss,
+sgd update — reference proj/src/mlp.cpp:233-289, 408-438).
+
+FP32 on the device vs double in the oracle.  Tolerances:
+per-layer max |g_gpu - g_ref| <= 2e-5 * max|g_ref| (entries summed over the
+batch in FP32 per CTA, then in double across CTAs); loss within 1e-5
+relative; 20 SGD steps leave the weights within 1e-4 relative (max-norm)."""
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2407_13096_b200 import init_mlp
+from paper_2407_13096_b200.train import DataParallelTrainer, target_stats
+
+pytestmark = pytest.mark.gpu
+
+
+def batch(port, n, root=0xACCE5505):
+    g = port.gen_stream(root, n, want=("params", "fused"))
+    mean, std, _ = target_stats(g["params"])
+    y = (g["params"] - mean) / std
+    return g["fused"], y, mean, std
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(np.asarray(a, np.float32).T)).cuda()
+
+
+def f32model(m):
+    """The model the device actually holds (weights rounded to float)."""
+    m2 = m.copy()
+    m2.weights = [w.astype(np.float32).astype(np.float64) for w in m.weights]
+    m2.biases = [b.astype(np.float32).astype(np.float64) for b in m.biases]
+    return m2
+
+
+@pytest.mark.parametrize("n", [1, 63, 64, 1000, 20_000])
+def test_gradient_vs_oracle(ctx, port, n):
+    x, y, mean, std = batch(port, n)
+    m = init_mlp(seed=424242)
+    m.target_mean, m.target_std = mean, std
+    ctx.set_model(m)
+    grad, loss = ctx.train_grad(dev(x), dev(y))
+    grad = grad.cpu().numpy().astype(np.float64) / (n * 7)
+    x32 = x.astype(np.float32).astype(np.float64)
+    y32 = y.astype(np.float32).astype(np.float64)
+    mr = f32model(m)
+    gw, gb = port.analytic_gradients(mr, x32, y32)
+    off = 0
+    for w in gw:
+        got = grad[off:off + w.size].reshape(w.shape)
+        off += w.size
+        assert np.abs(got - w).max() <= 2e-5 * np.abs(w).max() + 1e-12
+    for b in gb:
+        got = grad[off:off + b.size]
+        off += b.size
+        assert np.abs(got - b).max() <= 2e-5 * np.abs(b).max() + 1e-12
+    want_loss = port.mse_loss(mr, x32, y32)
+    assert float(loss.item()) / (n * 7) == pytest.approx(want_loss, rel=1e-5)
+
+
+def test_sgd_trajectory_vs_oracle(ctx, port):
+    """20 steps of W -= lr * g on fixed batches (batch 256) vs the oracle in double."""
+    n, B, lr = 256 * 20, 256, 0.3
+    x, y, mean, std = batch(port, n, root=77)
+    m = init_mlp(seed=5)
+    m.target_mean, m.target_std = mean, std
+    ctx.set_model(m)
+    tr = DataParallelTrainer(ctx, lr=lr)
+    ref = f32model(m)
+    for s in range(20):
+        xs, ys = x[s * B:(s + 1) * B], y[s * B:(s + 1) * B]
+        loss = tr.step(dev(xs), dev(ys), B, B)
+        x32 = xs.astype(np.float32).astype(np.float64)
+        y32 = ys.astype(np.float32).astype(np.float64)
+        want = port.mse_loss(ref, x32, y32)
+        assert float(loss.item()) == pytest.approx(want, rel=1e-4)
+        gw, gb = port.analytic_gradients(ref, x32, y32)
+        ref.weights = [w - lr * g for w, g in zip(ref.weights, gw)]
+        ref.biases = [b - lr * g for b, g in zip(ref.biases, gb)]
+    got = ctx.get_model()
+    for a, b in zip(got.weights + got.biases, ref.weights + ref.biases):
+        assert np.abs(a - b).max() <= 1e-4 * np.abs(b).max()
+    # the inference kernels see the trained weights (device repack)
+    p, cl, raw = ctx.predict_params(dev(x[:500]), want_raw=True)
+    want_raw = port.forward_raw(got, x[:500].astype(np.float32).astype(np.float64))
+    assert np.abs(raw.cpu().numpy().T - want_raw).max() <= 1e-5 * np.abs(want_raw).max()
+
+
+def test_training_reduces_loss(ctx, port):
+    """Full-batch-ish SGD on 50k synthetic kernels: the loss must fall steadily
+    (test_mlp.cpp:174-193 analogue at GPU batch sizes)."""
+    n, B = 50_000, 1024
+    x, y, mean, std = batch(port, n, root=99)
+    m = init_mlp(seed=3)
+    m.target_mean, m.target_std = mean, std
+    ctx.set_model(m)
+    tr = DataParallelTrainer(ctx, lr=0.5)
+    X, Y = dev(x), dev(y)
+    losses = []
+    for epoch in range(6):
+        tot = 0.0
+        for s in range(0, n, B):
+            b = min(B, n - s)
+            tot += float(tr.step(X[:, s:s + b].contiguous(), Y[:, s:s + b].contiguous(), b, b))
+        losses.append(tot)
+    assert losses[-1] < 0.7 * losses[0], losses
