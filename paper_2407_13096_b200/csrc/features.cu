@@ -97,7 +97,7 @@ __global__ void __launch_bounds__(256) dcgm_mean_kernel(const double* __restrict
 cudaError_t launch_featurize(Ctx& cx, const uint32_t* counts, const float* dcgm, int64_t n,
                              int64_t ld, float* fused) {
     if (n <= 0) return cudaSuccess;
-    const size_t smem = (size_t)(DSO_FUSED_ROWS * kFeatTile + 1024) * sizeof(float);
+    const size_t smem = (size_t)(DSO_FUSED_ROWS * kFeatTile + 1280) * sizeof(float);
     static bool attr = false;
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(featurize_kernel,

@@ -62,10 +62,12 @@ __device__ __forceinline__ void tile_features(float* act, float* scratch,
             act[r * kFeatTile + m] = live ? __ldg(dcgm + (int64_t)r * ld + k) : 0.f;
     }
     __syncthreads();
-    // phase 2: exact totals (u64), split so both thread halves sum ~63 rows
-    float* tfv = scratch;                     // [3][128]
-    float* rrv = tfv + 3 * kFeatTile;             // [3][128]
-    uint64_t* part = reinterpret_cast<uint64_t*>(rrv + 3 * kFeatTile);  // [128]
+    // phase 2: exact totals (u64), split so both thread halves sum ~63 rows.
+    // scratch (1280 floats): tf[3][128], rr[3][128], totd f64[3][128], part u64[128]
+    float* tfv = scratch;
+    float* rrv = tfv + 3 * kFeatTile;
+    double* totd = reinterpret_cast<double*>(rrv + 3 * kFeatTile);
+    uint64_t* part = reinterpret_cast<uint64_t*>(totd + 3 * kFeatTile);
     constexpr int kSplit = 60;
     const int m = tid & (kFeatTile - 1);
     uint64_t s_a = 0, s_b = 0, s_c = 0;
@@ -80,19 +82,18 @@ __device__ __forceinline__ void tile_features(float* act, float* scratch,
     }
     __syncthreads();
     // tf = total as float (exact below 2^24), rr = RN(1/tf); tf = 0 marks a zero
-    // total, tf = -1 a total >= 2^24 (FP64 path in phase 3).
+    // total, tf = -1 a total >= 2^24 (FP64 division by totd in phase 3).
     auto scale = [&](int cat, uint64_t tot) {
-        if (tot == 0) {
-            tfv[cat * kFeatTile + m] = 0.f;
-            rrv[cat * kFeatTile + m] = 0.f;
-        } else if (tot < (1u << 24)) {
-            const float tf = __uint2float_rn((uint32_t)tot);
-            tfv[cat * kFeatTile + m] = tf;
-            rrv[cat * kFeatTile + m] = __frcp_rn(tf);
-        } else {
-            tfv[cat * kFeatTile + m] = -1.f;
-            rrv[cat * kFeatTile + m] = 0.f;
+        float tf = 0.f, rr = 0.f;
+        if (tot != 0 && tot < (1u << 24)) {
+            tf = __uint2float_rn((uint32_t)tot);
+            rr = __frcp_rn(tf);
+        } else if (tot != 0) {
+            tf = -1.f;
         }
+        tfv[cat * kFeatTile + m] = tf;
+        rrv[cat * kFeatTile + m] = rr;
+        totd[cat * kFeatTile + m] = (double)tot;
     };
     if (tid < kFeatTile) {
         scale(0, s_a + part[m]);
@@ -101,19 +102,17 @@ __device__ __forceinline__ void tile_features(float* act, float* scratch,
         scale(2, s_c);
     }
     __syncthreads();
-    // phase 3: normalise, 4 kernels x 16 rows per thread.  All results are
-    // computed before any is stored (the FP64 path for totals >= 2^24 re-reads
-    // raw counts of other rows), then written in place after a barrier.
+    // phase 3: normalise in place, 4 kernels x 16 rows per thread
     {
         const int q = tid & 31;
         const int rp = tid >> 5;
-        float4 res[16];
-#pragma unroll
+#pragma unroll 4
         for (int j = 0; j < 16; ++j) {
             const int r = rp + 8 * j;
             if (r >= DSO_COUNT_ROWS) break;
             const int cat = r < DSO_INSTR_SLOTS ? 0 : (r < DSO_INSTR_SLOTS + DSO_DTYPE_SLOTS ? 1 : 2);
-            const uint4 c = reinterpret_cast<const uint4*>(acti + (8 + r) * kFeatTile)[q];
+            uint4* cp = reinterpret_cast<uint4*>(acti + (8 + r) * kFeatTile) + q;
+            const uint4 c = *cp;
             const float4 tf = reinterpret_cast<const float4*>(tfv + cat * kFeatTile)[q];
             const float4 rr = reinterpret_cast<const float4*>(rrv + cat * kFeatTile)[q];
             const uint32_t cc[4] = {c.x, c.y, c.z, c.w};
@@ -123,27 +122,18 @@ __device__ __forceinline__ void tile_features(float* act, float* scratch,
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
                 if (tt[e] > 0.f) {
-                    const float cf = __uint2float_rn(cc[e]);
+                    const float cf =
+                        (__int_as_float(0x4B000000u | (cc[e] & 0x7FFFFFu)) - 8388608.f) +
+                        ((cc[e] & 0x800000u) ? 8388608.f : 0.f);
                     const float qq = __fmul_rn(cf, ri[e]);
                     o[e] = fmaf(fmaf(-qq, tt[e], cf), ri[e], qq);
                 } else if (tt[e] == 0.f) {
                     o[e] = 0.f;
-                } else {  // total >= 2^24: exact u64 sum, one FP64 division
-                    const int base = cat == 0 ? 0 : (cat == 1 ? DSO_INSTR_SLOTS : DSO_INSTR_SLOTS + DSO_DTYPE_SLOTS);
-                    const int len = cat == 0 ? DSO_INSTR_SLOTS : (cat == 1 ? DSO_DTYPE_SLOTS : DSO_MEMSPACE_SLOTS);
-                    uint64_t s = 0;
-                    for (int i = 0; i < len; ++i) s += acti[(8 + base + i) * kFeatTile + 4 * q + e];
-                    o[e] = (float)((double)cc[e] / (double)s);
+                } else {
+                    o[e] = (float)((double)cc[e] / totd[cat * kFeatTile + 4 * q + e]);
                 }
             }
-            res[j] = make_float4(o[0], o[1], o[2], o[3]);
-        }
-        __syncthreads();
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-            const int r = rp + 8 * j;
-            if (r >= DSO_COUNT_ROWS) break;
-            reinterpret_cast<float4*>(act + (8 + r) * kFeatTile)[q] = res[j];
+            *reinterpret_cast<float4*>(cp) = make_float4(o[0], o[1], o[2], o[3]);
         }
     }
     __syncthreads();

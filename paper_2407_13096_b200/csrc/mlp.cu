@@ -5,264 +5,167 @@
 // de-standardised (forward_raw mlp.cpp:381-384) and clamped (predict_params
 // mlp.cpp:386-402, kBetaFloor mlp.cpp:15).
 //
-// Execution model (one persistent CTA per SM, 256 threads, ~165 KB smem):
-//   * the whole model (19,825 weights + biases) is staged ONCE per CTA into
-//     shared memory, transposed (k-major) and zero-padded per thread group;
-//   * a tile of 128 kernels lives in one k-major activation buffer
-//     act[134][128] (68.6 KB); every layer reads it, keeps its outputs in
-//     registers, syncs, and writes them back in place — nothing between the
-//     input load and the final result touches HBM;
-//   * layers are register-tiled FP32 GEMMs on the FMA pipe using Blackwell's
-//     packed FFMA2 (fma.rn.f32x2 — two FMAs per lane per instruction, with a
-//     scalar-broadcast operand so no duplication MOVs are needed):
-//       L1 134->100 : thread = 2 kernels x 26 neurons (pairs along n)
-//       L2 100->50  : thread = 2 kernels x 13 neurons (pairs along m)
-//       L3  50->25  : thread = 2 kernels x  7 neurons (pairs along m)
-//       L4  25->7   : thread = 2 kernels x  2 neurons (pairs along m)
-//     A warp shares its neuron group, so every weight load is a shared-memory
-//     broadcast; activation loads are 256 B contiguous per warp.
-//   Tensor cores are not used: TF32/BF16 cannot meet the 1e-5 relative
-//   contract on the predicted parameters.
+// Execution model — one persistent, warp-specialised CTA per SM (384 threads):
+//   * 8 CONSUMER warps run the MLP on a tile of 64 kernels held k-major in
+//     shared memory (act[134][64]); each layer is a register-tiled FP32 GEMM
+//     on the FMA pipe with Blackwell's packed FFMA2 (thread = 2 kernels x TN
+//     neurons, pairs along kernels, weights as scalar shared-memory broadcasts,
+//     operands of step k+1 in flight while step k issues); layer outputs
+//     overwrite act in place;
+//   * 4 PRODUCER warps, meanwhile, (a) finish the previous tile: clamp, then
+//     P(f), T(f), the eta objective and the lexicographic argmin over the
+//     whole frequency grid, and (b) run the feature stage of the tile after
+//     next (raw PTX counts -> per-category fractions fused with DCGM) straight
+//     into the free activation buffer;
+//   * two activation/output buffers ping-pong between the roles through named
+//     barriers FULL[s] (producer -> consumer: features in act[s], out[s] free)
+//     and READY[s] (consumer -> producer: predictions in out[s], act[s] free).
+// The MLP (FMA pipe) and the feature/sweep work (LSU/ALU + a little FMA) thus
+// overlap on every SM scheduler.  The model (weights ~100 KB) is staged once per
+// CTA; nothing between a kernel's 536 input bytes and its 16 result bytes
+// touches HBM.
 //
-// The fused pipeline kernel adds the feature stage in front (raw PTX counts ->
-// per-category fractions, fused with DCGM, straight into act) and the grid
-// sweep + eta objective + argmin behind (2 threads per kernel, each half the
-// core levels, merged with one shuffle), so a kernel's 536 input bytes become
-// its 16 result bytes without any intermediate HBM traffic.
+// Tensor cores are not used: TF32/BF16 products cannot meet the 1e-5 relative
+// contract on the predicted parameters.
 #include <math.h>
 
 #include <vector>
 
 #include "common.cuh"
-#include "features_core.cuh"
 #include "sweep_core.cuh"
 
 namespace dso_b200 {
 
 namespace {
 
-constexpr int kTile = 128;     // kernels per CTA tile
-constexpr int kThreads = 256;  // 8 warps
+constexpr int TM = 64;           // kernels per tile
+constexpr int RS = 64;           // act row stride (floats)
+constexpr int RS2 = RS / 2;
+constexpr int kConsumers = 256;  // 8 warps
+constexpr int kProducers = 128;  // 4 warps
+constexpr int kThreads = kConsumers + kProducers;
 
-// Packed (transposed, padded) weight layout in floats.  See model_upload.
-constexpr int kW1Stride = 112;  // 4 groups x 28 (26 used)
-constexpr int kW2Stride = 64;   // 4 groups x 16 (13 used)
-constexpr int kW3Stride = 32;   // 4 groups x 8  (7 used)
-constexpr int kW4Stride = 8;    // 7 used
-constexpr int kOffW1 = 0;
-constexpr int kOffW2 = kOffW1 + 134 * kW1Stride;  // 15008
-constexpr int kOffW3 = kOffW2 + 100 * kW2Stride;  // 21408
-constexpr int kOffW4 = kOffW3 + 50 * kW3Stride;   // 23008
-constexpr int kOffB1 = kOffW4 + 25 * kW4Stride;   // 23208
-constexpr int kOffB2 = kOffB1 + 104;
-constexpr int kOffB3 = kOffB2 + 52;
-constexpr int kOffB4 = kOffB3 + 28;
-constexpr int kModelFloats = kOffB4 + 8;          // 23400
-constexpr int kOffAct = kModelFloats;              // act[134][128]
-constexpr int kActFloats = 134 * kTile;
-constexpr int kOffOut = kOffAct + kActFloats;      // out[8][128] + stats
-constexpr int kOutFloats = 8 * kTile;
-constexpr int kOffStats = kOffOut + kOutFloats;    // mean[8], std[8], eta, K
-constexpr int kStatsFloats = 32;
-constexpr int kOffTables = kOffStats + kStatsFloats;  // core4[nc], mem2[nm] (pipeline)
-constexpr int kBaseFloats = kOffTables;
+// Named barriers (0 is __syncthreads).
+constexpr int BAR_CONS = 1, BAR_PROD = 2, BAR_FULL0 = 3, BAR_READY0 = 5;
 
-static_assert(kOffW2 % 4 == 0 && kOffW3 % 4 == 0 && kOffW4 % 4 == 0 && kOffB1 % 4 == 0 &&
-                  kModelFloats % 4 == 0 && kOffOut % 4 == 0 && kOffTables % 4 == 0,
+// Packed model (floats).  Layer l: [K][8 groups][TNP], neuron n = TN*g + t.
+constexpr int W1S = 0;                   // [134][8][16] TN 13 (104 >= 100)
+constexpr int W2S = W1S + 134 * 8 * 16;  // [100][8][8]  TN 7  (56 >= 50)
+constexpr int W3S = W2S + 100 * 8 * 8;   // [50][8][4]   TN 4  (32 >= 25)
+constexpr int W4S = W3S + 50 * 8 * 4;    // [25][8]      TN 1  (8 >= 7)
+constexpr int B1S = W4S + 25 * 8;        // [104]
+constexpr int B2S = B1S + 104;           // [56]
+constexpr int B3S = B2S + 56;            // [32]
+constexpr int B4S = B3S + 32;            // [8]
+constexpr int kModelFloats = B4S + 8;    // 25552
+// per-CTA shared memory beyond the model
+constexpr int ACT = kModelFloats;           // act[2][134][RS]
+constexpr int kActFloats = 134 * RS;
+constexpr int OUT = ACT + 2 * kActFloats;   // out[2][8][RS]  (raw predictions)
+constexpr int kOutFloats = 8 * RS;
+constexpr int SCR = OUT + 2 * kOutFloats;   // producer scratch: tf[3][64] rr[3][64]
+constexpr int kScrFloats = 6 * TM + 6 * TM + 2 * TM;  // + totd f64[3][64] + part u64[64]
+constexpr int STATS = SCR + kScrFloats;     // mean[8] std[8]
+constexpr int TABLES = STATS + 16;          // core4[nc], mem2[nm]
+static_assert(W2S % 4 == 0 && W3S % 4 == 0 && W4S % 4 == 0 && B1S % 4 == 0 &&
+                  kModelFloats % 4 == 0 && ACT % 4 == 0 && OUT % 4 == 0 && SCR % 4 == 0 &&
+                  TABLES % 4 == 0,
               "16-byte alignment of smem regions");
+
+// master (reference) layout offsets: W1 | W2 | W3 | W4 | b1 | b2 | b3 | b4
+constexpr int MW1 = 0, MW2 = MW1 + 100 * 134, MW3 = MW2 + 50 * 100, MW4 = MW3 + 25 * 50;
+constexpr int MB1 = MW4 + 7 * 25, MB2 = MB1 + 100, MB3 = MB2 + 50, MB4 = MB3 + 25;
+constexpr int kMasterFloats = MB4 + 7;
 
 __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
 
-// ---------------------------------------------------------------------------
-// Stage the packed model into shared memory (once per CTA).
-__device__ __forceinline__ void stage_model(float* smem, const float* __restrict__ packed) {
-    const float4* src = reinterpret_cast<const float4*>(packed);
-    float4* dst = reinterpret_cast<float4*>(smem);
-    for (int i = threadIdx.x; i < kModelFloats / 4; i += kThreads) dst[i] = __ldg(src + i);
+__device__ __forceinline__ void bar_sync(int id, int count) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ void bar_arrive(int id, int count) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
 
 // ---------------------------------------------------------------------------
-// The four layers on act[134][128] (k-major, kernels contiguous).
-// Precondition: act rows 0..133 hold the tile's fused features; __syncthreads
-// done.  Postcondition: out[n][m] (n < 7) holds forward_raw outputs
-// (de-standardised, NOT clamped); __syncthreads done.
-__device__ __forceinline__ void mlp_tile(float* smem) {
-    const float* W = smem;
-    float* act = smem + kOffAct;
-    float2* act2 = reinterpret_cast<float2*>(act);  // [row][64] pairs of kernels
-    const int tid = threadIdx.x;
-    const int mp = tid & 63;  // kernel pair: kernels 2mp, 2mp+1
-    const int g = tid >> 6;   // neuron group (uniform per warp)
+// Consumer: accumulate one dense layer (rows 0..K-1 of act in).
+template <int K, int TN, int TNP>
+__device__ __forceinline__ void dense_acc(const float* sm, const float* act, int woff, int ct,
+                                          float2 (&acc)[TN]) {
+    const int mp = ct & 31, g = ct >> 5;
+    const float2* in2 = reinterpret_cast<const float2*>(act);
+#pragma unroll
+    for (int t = 0; t < TN; ++t) acc[t] = f2(0.f, 0.f);
+    struct Op {
+        float2 a;
+        float w[TNP];
+    };
+    auto load = [&](Op& o, int k) {
+        o.a = in2[k * RS2 + mp];
+        const float* w = sm + woff + (k * 8 + g) * TNP;
+        if constexpr (TNP % 4 == 0) {
+#pragma unroll
+            for (int q = 0; q < TNP / 4; ++q) {
+                const float4 v = reinterpret_cast<const float4*>(w)[q];
+                o.w[4 * q] = v.x;
+                o.w[4 * q + 1] = v.y;
+                o.w[4 * q + 2] = v.z;
+                o.w[4 * q + 3] = v.w;
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < TNP; ++q) o.w[q] = w[q];
+        }
+    };
+    auto math = [&](const Op& o) {
+#pragma unroll
+        for (int t = 0; t < TN; ++t) acc[t] = ffma2(o.a, f2(o.w[t], o.w[t]), acc[t]);
+    };
+    Op A, B;
+    load(A, 0);
+#pragma unroll 1
+    for (int k = 0; k + 1 < K; k += 2) {
+        load(B, k + 1);
+        math(A);
+        load(A, k + 2 < K ? k + 2 : K - 1);
+        math(B);
+    }
+    if (K & 1) math(A);
+}
 
-    // Each layer's k-loop is software-pipelined over two register stages (A, B):
-    // the operands of step k+1 are in flight while step k's FFMA2s issue, and
-    // the stages alternate without register copies.  Only 2 warps share a
-    // scheduler, so shared-memory latency is hidden by this ILP, not by TLP.
-    // ---- L1: 134 -> 100 (neurons 26g .. 26g+25), pairs along n -------------
-    {
-        float2 acc0[13], acc1[13];
+template <int K, int TN, int TNP>
+__device__ __forceinline__ void dense_sigmoid_inplace(const float* sm, float* act, int woff,
+                                                      int boff, int ct) {
+    float2 acc[TN];
+    dense_acc<K, TN, TNP>(sm, act, woff, ct, acc);
+    bar_sync(BAR_CONS, kConsumers);  // every consumer has read its inputs
+    const int mp = ct & 31, g = ct >> 5;
+    float2* out2 = reinterpret_cast<float2*>(act);
 #pragma unroll
-        for (int p = 0; p < 13; ++p) acc0[p] = acc1[p] = f2(0.f, 0.f);
-        const float* wbase = W + kOffW1 + g * 28;
-        struct Op {
-            float2 a;
-            float4 v[6];
-            float2 l;
-        };
-        auto load = [&](Op& o, int k) {
-            const float* w = wbase + k * kW1Stride;
-            o.a = act2[k * 64 + mp];
-#pragma unroll
-            for (int q = 0; q < 6; ++q) o.v[q] = reinterpret_cast<const float4*>(w)[q];
-            o.l = reinterpret_cast<const float2*>(w)[12];
-        };
-        auto math = [&](const Op& o) {
-            float2 w[13];
-#pragma unroll
-            for (int q = 0; q < 6; ++q) {
-                w[2 * q] = f2(o.v[q].x, o.v[q].y);
-                w[2 * q + 1] = f2(o.v[q].z, o.v[q].w);
-            }
-            w[12] = o.l;
-#pragma unroll
-            for (int p = 0; p < 13; ++p) {
-                acc0[p] = ffma2(f2(o.a.x, o.a.x), w[p], acc0[p]);
-                acc1[p] = ffma2(f2(o.a.y, o.a.y), w[p], acc1[p]);
-            }
-        };
-        Op A, B;
-        load(A, 0);
-#pragma unroll 1
-        for (int k = 0; k < 134; k += 2) {
-            load(B, k + 1);
-            math(A);
-            load(A, k + 2 < 134 ? k + 2 : 133);
-            math(B);
-        }
-        __syncthreads();  // all reads of act done
-        const float* b = W + kOffB1 + g * 26;
-#pragma unroll
-        for (int p = 0; p < 13; ++p) {
-            const int n = g * 26 + 2 * p;
-            const float b0 = b[2 * p], b1 = b[2 * p + 1];
-            act2[n * 64 + mp] = f2(sigmoidf_fast(acc0[p].x + b0), sigmoidf_fast(acc1[p].x + b0));
-            act2[(n + 1) * 64 + mp] =
-                f2(sigmoidf_fast(acc0[p].y + b1), sigmoidf_fast(acc1[p].y + b1));
-        }
-        __syncthreads();
+    for (int t = 0; t < TN; ++t) {
+        const float bb = sm[boff + TN * g + t];
+        out2[(TN * g + t) * RS2 + mp] =
+            f2(sigmoidf_fast(acc[t].x + bb), sigmoidf_fast(acc[t].y + bb));
     }
-    // ---- L2: 100 -> 50 (neurons 13g .. 13g+12), pairs along m ----------------
-    {
-        float2 acc[13];
-#pragma unroll
-        for (int t = 0; t < 13; ++t) acc[t] = f2(0.f, 0.f);
-        const float* wbase = W + kOffW2 + g * 16;
-        struct Op {
-            float2 a;
-            float4 v0, v1, v2;
-            float v3;
-        };
-        auto load = [&](Op& o, int k) {
-            const float* w = wbase + k * kW2Stride;
-            o.a = act2[k * 64 + mp];
-            o.v0 = reinterpret_cast<const float4*>(w)[0];
-            o.v1 = reinterpret_cast<const float4*>(w)[1];
-            o.v2 = reinterpret_cast<const float4*>(w)[2];
-            o.v3 = w[12];
-        };
-        auto math = [&](const Op& o) {
-            const float w[13] = {o.v0.x, o.v0.y, o.v0.z, o.v0.w, o.v1.x, o.v1.y, o.v1.z,
-                                 o.v1.w, o.v2.x, o.v2.y, o.v2.z, o.v2.w, o.v3};
-#pragma unroll
-            for (int t = 0; t < 13; ++t) acc[t] = ffma2(o.a, f2(w[t], w[t]), acc[t]);
-        };
-        Op A, B;
-        load(A, 0);
-#pragma unroll 1
-        for (int k = 0; k < 100; k += 2) {
-            load(B, k + 1);
-            math(A);
-            load(A, k + 2 < 100 ? k + 2 : 99);
-            math(B);
-        }
-        __syncthreads();
-        const float* b = W + kOffB2 + g * 13;
-#pragma unroll
-        for (int t = 0; t < 13; ++t) {
-            const float bb = b[t];
-            act2[(g * 13 + t) * 64 + mp] =
-                f2(sigmoidf_fast(acc[t].x + bb), sigmoidf_fast(acc[t].y + bb));
-        }
-        __syncthreads();
-    }
-    // ---- L3: 50 -> 25 (neurons 7g .. 7g+6), pairs along m ---------------------
-    {
-        float2 acc[7];
-#pragma unroll
-        for (int t = 0; t < 7; ++t) acc[t] = f2(0.f, 0.f);
-        const float* wbase = W + kOffW3 + g * 8;
-        struct Op {
-            float2 a;
-            float4 v0, v1;
-        };
-        auto load = [&](Op& o, int k) {
-            const float* w = wbase + k * kW3Stride;
-            o.a = act2[k * 64 + mp];
-            o.v0 = reinterpret_cast<const float4*>(w)[0];
-            o.v1 = reinterpret_cast<const float4*>(w)[1];
-        };
-        auto math = [&](const Op& o) {
-            const float w[7] = {o.v0.x, o.v0.y, o.v0.z, o.v0.w, o.v1.x, o.v1.y, o.v1.z};
-#pragma unroll
-            for (int t = 0; t < 7; ++t) acc[t] = ffma2(o.a, f2(w[t], w[t]), acc[t]);
-        };
-        Op A, B;
-        load(A, 0);
-#pragma unroll 1
-        for (int k = 0; k < 50; k += 2) {
-            load(B, k + 1);
-            math(A);
-            load(A, k + 2 < 50 ? k + 2 : 49);
-            math(B);
-        }
-        __syncthreads();
-        const float* b = W + kOffB3 + g * 7;
-#pragma unroll
-        for (int t = 0; t < 7; ++t) {
-            const float bb = b[t];
-            act2[(g * 7 + t) * 64 + mp] =
-                f2(sigmoidf_fast(acc[t].x + bb), sigmoidf_fast(acc[t].y + bb));
-        }
-        __syncthreads();
-    }
-    // ---- L4: 25 -> 7 (neurons 2g, 2g+1), identity, de-standardise -------------
-    {
-        float2 acc[2] = {f2(0.f, 0.f), f2(0.f, 0.f)};
-        const float* wbase = W + kOffW4 + g * 2;
-#pragma unroll 5
-        for (int k = 0; k < 25; ++k) {
-            const float2 a = act2[k * 64 + mp];
-            const float2 w = *reinterpret_cast<const float2*>(wbase + k * kW4Stride);
-            acc[0] = ffma2(a, f2(w.x, w.x), acc[0]);
-            acc[1] = ffma2(a, f2(w.y, w.y), acc[1]);
-        }
-        const float* st = smem + kOffStats;  // mean[0..7], std[8..15]
-        float2* out2 = reinterpret_cast<float2*>(smem + kOffOut);
-#pragma unroll
-        for (int t = 0; t < 2; ++t) {
-            const int n = 2 * g + t;
-            if (n < 7) {
-                const float bb = W[kOffB4 + n];
-                const float s = st[8 + n], mu = st[n];
-                // forward_raw: (z * std) + mean, z = (W a) + b
-                out2[n * 64 + mp] = f2(fmaf(acc[t].x + bb, s, mu), fmaf(acc[t].y + bb, s, mu));
-            }
-        }
-        __syncthreads();
+    bar_sync(BAR_CONS, kConsumers);
+}
+
+// Full forward on act -> raw outputs (forward_raw, not clamped) in out rows 0..6.
+__device__ __forceinline__ void consumer_tile(const float* sm, float* act, float* out, int ct) {
+    dense_sigmoid_inplace<134, 13, 16>(sm, act, W1S, B1S, ct);
+    dense_sigmoid_inplace<100, 7, 8>(sm, act, W2S, B2S, ct);
+    dense_sigmoid_inplace<50, 4, 4>(sm, act, W3S, B3S, ct);
+    float2 acc[1];
+    dense_acc<25, 1, 1>(sm, act, W4S, ct, acc);
+    const int mp = ct & 31, g = ct >> 5;
+    if (g < 7) {
+        const float bb = sm[B4S + g], s = sm[STATS + 8 + g], mu = sm[STATS + g];
+        // forward_raw: (z * std) + mean, z = (W a) + b
+        reinterpret_cast<float2*>(out)[g * RS2 + mp] =
+            f2(fmaf(acc[0].x + bb, s, mu), fmaf(acc[0].y + bb, s, mu));
     }
 }
 
-// predict_params clamp (mlp.cpp:390-399) on out[.][m]; returns clamped flag.
+// predict_params clamp (mlp.cpp:390-399); returns the clamped flag.
 __device__ __forceinline__ bool clamp_params(float p[7]) {
     bool cl = false;
 #pragma unroll
@@ -278,15 +181,124 @@ __device__ __forceinline__ bool clamp_params(float p[7]) {
     return cl;
 }
 
-// Fused features already in HBM ([134][ld] float) -> act.  Full tiles: 17
-// 128-bit loads per thread, all in flight; ragged / unaligned tiles: scalar.
-__device__ __forceinline__ void load_features_fused(float* smem, const float* __restrict__ fused,
-                                                    int64_t t0, int64_t n, int64_t ld,
-                                                    bool vec_ok) {
-    float* act = smem + kOffAct;
-    const int tid = threadIdx.x;
-    if (vec_ok && t0 + kTile <= n) {
-        const int q = tid & 31, rp = tid >> 5;
+// ---------------------------------------------------------------------------
+// Producer: feature stage of one 64-kernel tile into act (128 threads).
+// featurize (ptx_features.cpp:311-329) + as_vector (mlp.cpp:307-314): per
+// category count/total, correctly rounded in FP32 (equal to the reference's
+// double quotient rounded to float for totals < 2^24), FP64
+// division for larger totals, zeros for a zero total.
+__device__ __forceinline__ void produce_features(float* act, float* scr,
+                                                 const uint32_t* __restrict__ counts,
+                                                 const float* __restrict__ dcgm, int64_t t0,
+                                                 int64_t n, int64_t ld, bool vec_ok, int pt) {
+    uint32_t* acti = reinterpret_cast<uint32_t*>(act);
+    const int q = pt & 15;   // kernels 4q .. 4q+3
+    const int rp = pt >> 4;  // row phase 0..7
+    // phase 1: all loads of the tile in flight
+    if (vec_ok && t0 + TM <= n) {
+        uint4 v[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            const int r = rp + 8 * j;
+            if (r < DSO_COUNT_ROWS)
+                v[j] = __ldg(reinterpret_cast<const uint4*>(counts + (int64_t)r * ld + t0) + q);
+        }
+        const float4 d = __ldg(reinterpret_cast<const float4*>(dcgm + (int64_t)rp * ld + t0) + q);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            const int r = rp + 8 * j;
+            if (r < DSO_COUNT_ROWS) reinterpret_cast<uint4*>(acti + (8 + r) * RS)[q] = v[j];
+        }
+        reinterpret_cast<float4*>(act + rp * RS)[q] = d;
+    } else {
+        const int m = pt & 63, h = pt >> 6;
+        const int64_t k = t0 + m;
+        const bool live = k < n;
+#pragma unroll 9
+        for (int r = h; r < DSO_COUNT_ROWS; r += 2)
+            acti[(8 + r) * RS + m] = live ? __ldg(counts + (int64_t)r * ld + k) : 0u;
+#pragma unroll
+        for (int r = h; r < 8; r += 2)
+            act[r * RS + m] = live ? __ldg(dcgm + (int64_t)r * ld + k) : 0.f;
+    }
+    bar_sync(BAR_PROD, kProducers);
+    // phase 2: exact integer totals per (kernel, category)
+    float* tfv = scr;                                                  // [3][64]
+    float* rrv = scr + 3 * TM;                                         // [3][64]
+    double* totd = reinterpret_cast<double*>(scr + 6 * TM);            // [3][64]
+    uint64_t* part = reinterpret_cast<uint64_t*>(scr + 12 * TM);       // [64]
+    constexpr int kSplit = 60;
+    const int m = pt & 63;
+    uint64_t sa = 0, sb = 0, sc = 0;
+    if (pt < TM) {
+        for (int r = 0; r < kSplit; ++r) sa += acti[(8 + r) * RS + m];
+    } else {
+        for (int r = kSplit; r < DSO_INSTR_SLOTS; ++r) sa += acti[(8 + r) * RS + m];
+        for (int r = 0; r < DSO_DTYPE_SLOTS; ++r) sb += acti[(8 + DSO_INSTR_SLOTS + r) * RS + m];
+        for (int r = 0; r < DSO_MEMSPACE_SLOTS; ++r)
+            sc += acti[(8 + DSO_INSTR_SLOTS + DSO_DTYPE_SLOTS + r) * RS + m];
+        part[m] = sa;
+    }
+    bar_sync(BAR_PROD, kProducers);
+    auto scale = [&](int cat, uint64_t tot) {
+        // tf = exact total as float, rr = RN(1/tf); tf 0 marks a zero total,
+        // -1 a total >= 2^24 (FP64 division by totd below)
+        float tf = 0.f, rr = 0.f;
+        if (tot != 0 && tot < (1u << 24)) {
+            tf = __uint2float_rn((uint32_t)tot);
+            rr = __frcp_rn(tf);
+        } else if (tot != 0) {
+            tf = -1.f;
+        }
+        tfv[cat * TM + m] = tf;
+        rrv[cat * TM + m] = rr;
+        totd[cat * TM + m] = (double)tot;
+    };
+    if (pt < TM) {
+        scale(0, sa + part[m]);
+    } else {
+        scale(1, sb);
+        scale(2, sc);
+    }
+    bar_sync(BAR_PROD, kProducers);
+    // phase 3: normalise in place (each entry reads only itself and its totals)
+#pragma unroll 4
+    for (int j = 0; j < 16; ++j) {
+        const int r = rp + 8 * j;
+        if (r >= DSO_COUNT_ROWS) break;
+        const int cat = r < DSO_INSTR_SLOTS ? 0 : (r < DSO_INSTR_SLOTS + DSO_DTYPE_SLOTS ? 1 : 2);
+        uint4* cp = reinterpret_cast<uint4*>(acti + (8 + r) * RS) + q;
+        const uint4 c = *cp;
+        const float4 tf = reinterpret_cast<const float4*>(tfv + cat * TM)[q];
+        const float4 rr = reinterpret_cast<const float4*>(rrv + cat * TM)[q];
+        const uint32_t cc[4] = {c.x, c.y, c.z, c.w};
+        const float tt[4] = {tf.x, tf.y, tf.z, tf.w};
+        const float ri[4] = {rr.x, rr.y, rr.z, rr.w};
+        float o[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            if (tt[e] > 0.f) {
+                // exact u32 -> f32 for counts < 2^24, on the ALU/FMA pipes
+                const float cf = (__int_as_float(0x4B000000u | (cc[e] & 0x7FFFFFu)) - 8388608.f) +
+                                 ((cc[e] & 0x800000u) ? 8388608.f : 0.f);
+                const float qq = __fmul_rn(cf, ri[e]);
+                o[e] = fmaf(fmaf(-qq, tt[e], cf), ri[e], qq);
+            } else if (tt[e] == 0.f) {
+                o[e] = 0.f;
+            } else {
+                o[e] = (float)((double)cc[e] / totd[cat * TM + 4 * q + e]);
+            }
+        }
+        *reinterpret_cast<float4*>(cp) = make_float4(o[0], o[1], o[2], o[3]);
+    }
+}
+
+// Producer: already-fused features ([134][ld] floats) into act.
+__device__ __forceinline__ void produce_fused(float* act, const float* __restrict__ fused,
+                                              int64_t t0, int64_t n, int64_t ld, bool vec_ok,
+                                              int pt) {
+    const int q = pt & 15, rp = pt >> 4;
+    if (vec_ok && t0 + TM <= n) {
         float4 v[17];
 #pragma unroll
         for (int j = 0; j < 17; ++j) {
@@ -297,24 +309,15 @@ __device__ __forceinline__ void load_features_fused(float* smem, const float* __
 #pragma unroll
         for (int j = 0; j < 17; ++j) {
             const int r = rp + 8 * j;
-            if (r < DSO_FUSED_ROWS) reinterpret_cast<float4*>(act + r * kTile)[q] = v[j];
+            if (r < DSO_FUSED_ROWS) reinterpret_cast<float4*>(act + r * RS)[q] = v[j];
         }
     } else {
-        const int m = tid & (kTile - 1);
-        const int h = tid >> 7;
+        const int m = pt & 63, h = pt >> 6;
         const int64_t k = t0 + m;
         const bool live = k < n;
 #pragma unroll 7
         for (int r = h; r < DSO_FUSED_ROWS; r += 2)
-            act[r * kTile + m] = live ? __ldg(fused + (int64_t)r * ld + k) : 0.f;
-    }
-    __syncthreads();
-}
-
-__device__ __forceinline__ void stage_stats(float* smem, const float* mean, const float* std_) {
-    if (threadIdx.x < 8) {
-        smem[kOffStats + threadIdx.x] = mean[threadIdx.x];
-        smem[kOffStats + 8 + threadIdx.x] = std_[threadIdx.x];
+            act[r * RS + m] = live ? __ldg(fused + (int64_t)r * ld + k) : 0.f;
     }
 }
 
@@ -323,158 +326,233 @@ struct Stats {
     float std_[8];
 };
 
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kThreads, 1) predict_kernel(
-    const float* __restrict__ packed, Stats stats, const float* __restrict__ fused, int64_t n,
-    int64_t ld, float* __restrict__ params, uint8_t* __restrict__ clamped,
-    float* __restrict__ raw) {
-    extern __shared__ __align__(16) float smem[];
-    stage_model(smem, packed);
-    stage_stats(smem, stats.mean, stats.std_);
-    __syncthreads();
-    const bool vec_ok = ((ld & 3) == 0) && ((reinterpret_cast<uintptr_t>(fused) & 15) == 0);
-    const int64_t tiles = (n + kTile - 1) / kTile;
-    for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-        const int64_t t0 = tile * kTile;
-        load_features_fused(smem, fused, t0, n, ld, vec_ok);
-        mlp_tile(smem);
-        if (threadIdx.x < kTile) {
-            const int m = threadIdx.x;
-            const int64_t k = t0 + m;
-            if (k < n) {
-                const float* out = smem + kOffOut;
-                float p[7];
+struct Job {
+    // inputs
+    const uint32_t* counts;
+    const float* dcgm;
+    const float* fused;
+    int64_t n, ld;
+    // sweep
+    const float4* core4;
+    const float2* mem2;
+    int nc, nm;
+    float eta, K;
+    // outputs
+    float* params;
+    uint8_t* clamped;
+    float* raw;
+    int32_t* idx;
+    float* cost;
+    float* energy;
+    float* time;
+    int64_t ld_out;
+};
+
+// Producer: finish a tile from its raw predictions in out: clamp and either
+// write the parameters (predict) or sweep the grid (pipeline).  2 threads per
+// kernel, each half of the core levels, merged with one shuffle.
+template <bool PIPE>
+__device__ __forceinline__ void produce_results(const float* sm, const float* out, const Job& J,
+                                                int64_t t0, int pt) {
+    const int m = pt >> 1, half = pt & 1;
+    const int64_t k = t0 + m;
+    float pr[7];
 #pragma unroll
-                for (int i = 0; i < 7; ++i) p[i] = out[i * kTile + m];
-                if (raw)
+    for (int i = 0; i < 7; ++i) pr[i] = out[i * RS + m];
+    if (!PIPE) {
+        if (half == 0 && k < J.n) {
+            if (J.raw)
 #pragma unroll
-                    for (int i = 0; i < 7; ++i) raw[i * ld + k] = p[i];
-                const bool cl = clamp_params(p);
+                for (int i = 0; i < 7; ++i) J.raw[i * J.ld_out + k] = pr[i];
+            const bool cl = clamp_params(pr);
 #pragma unroll
-                for (int i = 0; i < 7; ++i) params[i * ld + k] = p[i];
-                if (clamped) clamped[k] = cl ? 1 : 0;
-            }
+            for (int i = 0; i < 7; ++i) J.params[i * J.ld_out + k] = pr[i];
+            if (J.clamped) J.clamped[k] = cl ? 1 : 0;
         }
-        __syncthreads();
+        return;
+    }
+    const bool cl = clamp_params(pr);
+    const KParams p{pr[0], pr[1], pr[2], pr[3], pr[4], pr[5], pr[6]};
+    const float4* s_core = reinterpret_cast<const float4*>(sm + TABLES);
+    const float2* s_mem = reinterpret_cast<const float2*>(sm + TABLES + 4 * J.nc);
+    const int nc = J.nc, nm = J.nm;
+    const int i_split = (nc + 1) >> 1;
+    const int i_lo = half ? i_split : 0, i_hi = half ? nc : i_split;
+    Best b{__int_as_float(0x7fc00000), __int_as_float(0x7fc00000), i_lo * nm};
+    if (i_lo < i_hi) {
+        if (nm == 4)
+            b = sweep_levels<4>(p, s_core, s_mem, 4, i_lo, i_hi, J.eta, J.K);
+        else if (nm == 1)
+            b = sweep_levels<1>(p, s_core, s_mem, 1, i_lo, i_hi, J.eta, J.K);
+        else if (nm == 3)
+            b = sweep_levels<3>(p, s_core, s_mem, 3, i_lo, i_hi, J.eta, J.K);
+        else
+            b = sweep_levels<0>(p, s_core, s_mem, nm, i_lo, i_hi, J.eta, J.K);
+    }
+    Best o;
+    o.c = __shfl_xor_sync(0xffffffffu, b.c, 1);
+    o.e = __shfl_xor_sync(0xffffffffu, b.e, 1);
+    o.i = __shfl_xor_sync(0xffffffffu, b.i, 1);
+    if (half == 0 && k < J.n) {
+        if (i_split < nc) merge_best(b, o);  // the upper half holds the later pairs
+        J.idx[k] = b.i;
+        if (J.cost) J.cost[k] = b.c;
+        if (J.energy) J.energy[k] = b.e;
+        if (J.time) J.time[k] = time_at(p, s_core, s_mem, nm, b.i);
+        if (J.params)
+#pragma unroll
+            for (int i = 0; i < 7; ++i) J.params[i * J.ld_out + k] = pr[i];
+        if (J.clamped) J.clamped[k] = cl ? 1 : 0;
     }
 }
 
-// ---------------------------------------------------------------------------
-// Fused pipeline: counts + DCGM -> features -> MLP -> clamp -> sweep -> argmin.
-__global__ void __launch_bounds__(kThreads, 1) pipeline_kernel(
-    const float* __restrict__ packed, Stats stats, const float4* __restrict__ core4, int nc,
-    const float2* __restrict__ mem2, int nm, float eta, float K,
-    const uint32_t* __restrict__ counts, const float* __restrict__ dcgm, int64_t n, int64_t ld,
-    float* __restrict__ params_out, uint8_t* __restrict__ clamped_out,
-    int32_t* __restrict__ idx_out, float* __restrict__ cost_out, float* __restrict__ energy_out,
-    float* __restrict__ time_out, int64_t ld_out) {
-    extern __shared__ __align__(16) float smem[];
-    stage_model(smem, packed);
-    stage_stats(smem, stats.mean, stats.std_);
-    float4* s_core = reinterpret_cast<float4*>(smem + kOffTables);
-    float2* s_mem = reinterpret_cast<float2*>(smem + kOffTables + 4 * nc);
-    for (int i = threadIdx.x; i < nc; i += kThreads) s_core[i] = core4[i];
-    for (int j = threadIdx.x; j < nm; j += kThreads) s_mem[j] = mem2[j];
-    __syncthreads();
-
-    const int64_t tiles = (n + kTile - 1) / kTile;
-    const bool vec_ok = ((ld & 3) == 0) && ((reinterpret_cast<uintptr_t>(counts) & 15) == 0) &&
-                        ((reinterpret_cast<uintptr_t>(dcgm) & 15) == 0);
-    const int tid = threadIdx.x;
-    const int m = tid >> 1;    // kernel within tile (2 threads per kernel)
-    const int half = tid & 1;  // which half of the core levels
-    const int i_split = (nc + 1) >> 1;
-    const int i_lo = half ? i_split : 0;
-    const int i_hi = half ? nc : i_split;
-
-    for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-        const int64_t t0 = tile * kTile;
-        tile_features(smem + kOffAct, smem + kOffOut, counts, dcgm, t0, n, ld, vec_ok);
-        mlp_tile(smem);
-
-        // ---- clamp + sweep + argmin: 2 threads per kernel --------------------
-        const int64_t k = t0 + m;
-        const float* out = smem + kOffOut;
-        float pr[7];
-#pragma unroll
-        for (int i = 0; i < 7; ++i) pr[i] = out[i * kTile + m];
-        const bool cl = clamp_params(pr);
-        const KParams p{pr[0], pr[1], pr[2], pr[3], pr[4], pr[5], pr[6]};
-        Best b{__int_as_float(0x7fc00000), __int_as_float(0x7fc00000), i_lo * nm};
-        if (i_lo < i_hi) {
-            if (nm == 4)
-                b = sweep_levels<4>(p, s_core, s_mem, 4, i_lo, i_hi, eta, K);
-            else if (nm == 1)
-                b = sweep_levels<1>(p, s_core, s_mem, 1, i_lo, i_hi, eta, K);
-            else if (nm == 3)
-                b = sweep_levels<3>(p, s_core, s_mem, 3, i_lo, i_hi, eta, K);
-            else
-                b = sweep_levels<0>(p, s_core, s_mem, nm, i_lo, i_hi, eta, K);
+template <bool PIPE>
+__global__ void __launch_bounds__(kThreads, 1)
+    ws_kernel(const float* __restrict__ packed, Stats stats, Job J) {
+    extern __shared__ __align__(16) float sm[];
+    // ---- stage model, stats, tables (all threads) -----------------------------
+    {
+        const float4* src = reinterpret_cast<const float4*>(packed);
+        float4* dst = reinterpret_cast<float4*>(sm);
+        for (int i = threadIdx.x; i < kModelFloats / 4; i += kThreads) dst[i] = __ldg(src + i);
+        if (threadIdx.x < 8) {
+            sm[STATS + threadIdx.x] = stats.mean[threadIdx.x];
+            sm[STATS + 8 + threadIdx.x] = stats.std_[threadIdx.x];
         }
-        // merge the two halves (the upper half holds the later pairs)
-        Best o;
-        o.c = __shfl_xor_sync(0xffffffffu, b.c, 1);
-        o.e = __shfl_xor_sync(0xffffffffu, b.e, 1);
-        o.i = __shfl_xor_sync(0xffffffffu, b.i, 1);
-        if (half == 0 && k < n) {
-            if (i_split < nc) merge_best(b, o);
-            idx_out[k] = b.i;
-            if (cost_out) cost_out[k] = b.c;
-            if (energy_out) energy_out[k] = b.e;
-            if (time_out) time_out[k] = time_at(p, s_core, s_mem, nm, b.i);
-            if (params_out)
-#pragma unroll
-                for (int i = 0; i < 7; ++i) params_out[i * ld_out + k] = pr[i];
-            if (clamped_out) clamped_out[k] = cl ? 1 : 0;
+        if (PIPE) {
+            float4* sc = reinterpret_cast<float4*>(sm + TABLES);
+            float2* smm = reinterpret_cast<float2*>(sm + TABLES + 4 * J.nc);
+            for (int i = threadIdx.x; i < J.nc; i += kThreads) sc[i] = J.core4[i];
+            for (int j = threadIdx.x; j < J.nm; j += kThreads) smm[j] = J.mem2[j];
         }
-        __syncthreads();  // out/act reused by the next tile
     }
+    __syncthreads();
+    const int64_t tiles = (J.n + TM - 1) / TM;
+    const int64_t my_tiles =
+        (int64_t)blockIdx.x < tiles ? (tiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+    const int tid = threadIdx.x;
+    if (tid < kConsumers) {
+        // ================================ consumer ================================
+        for (int64_t i = 0; i < my_tiles; ++i) {
+            const int s = (int)(i & 1);
+            bar_sync(BAR_FULL0 + s, kThreads);  // features in act[s]; out[s] free
+            consumer_tile(sm, sm + ACT + s * kActFloats, sm + OUT + s * kOutFloats, tid);
+            bar_arrive(BAR_READY0 + s, kThreads);  // predictions in out[s]; act[s] free
+        }
+    } else {
+        // ================================ producer ================================
+        const int pt = tid - kConsumers;
+        float* scr = sm + SCR;
+        const bool vec_ok =
+            PIPE ? (((J.ld & 3) == 0) && ((reinterpret_cast<uintptr_t>(J.counts) & 15) == 0) &&
+                    ((reinterpret_cast<uintptr_t>(J.dcgm) & 15) == 0))
+                 : (((J.ld & 3) == 0) && ((reinterpret_cast<uintptr_t>(J.fused) & 15) == 0));
+        auto load_tile = [&](int64_t i) {
+            const int s = (int)(i & 1);
+            const int64_t t0 = (blockIdx.x + i * gridDim.x) * (int64_t)TM;
+            float* act = sm + ACT + s * kActFloats;
+            if (PIPE)
+                produce_features(act, scr, J.counts, J.dcgm, t0, J.n, J.ld, vec_ok, pt);
+            else
+                produce_fused(act, J.fused, t0, J.n, J.ld, vec_ok, pt);
+            bar_arrive(BAR_FULL0 + s, kThreads);
+        };
+        if (my_tiles > 0) load_tile(0);
+        if (my_tiles > 1) load_tile(1);
+        for (int64_t i = 0; i < my_tiles; ++i) {
+            const int s = (int)(i & 1);
+            const int64_t t0 = (blockIdx.x + i * gridDim.x) * (int64_t)TM;
+            bar_sync(BAR_READY0 + s, kThreads);
+            produce_results<PIPE>(sm, sm + OUT + s * kOutFloats, J, t0, pt);
+            // out[s] fully read and act[s] free -> tile i+2 may be staged there
+            bar_sync(BAR_PROD, kProducers);
+            if (i + 2 < my_tiles) load_tile(i + 2);
+        }
+    }
+}
+
+// Device-side repack of the master weights (reference layout, f32) into the
+// packed layout (after a training update).  Padding stays zero.
+__global__ void repack_kernel(const float* __restrict__ master, float* __restrict__ pk) {
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e < MW2) {
+        const int nn = e / 134, k = e - nn * 134;
+        pk[W1S + (k * 8 + nn / 13) * 16 + nn % 13] = master[e];
+    } else if (e < MW3) {
+        const int f = e - MW2, nn = f / 100, k = f - nn * 100;
+        pk[W2S + (k * 8 + nn / 7) * 8 + nn % 7] = master[e];
+    } else if (e < MW4) {
+        const int f = e - MW3, nn = f / 50, k = f - nn * 50;
+        pk[W3S + (k * 8 + nn / 4) * 4 + nn % 4] = master[e];
+    } else if (e < MB1) {
+        const int f = e - MW4, nn = f / 25, k = f - nn * 25;
+        pk[W4S + k * 8 + nn] = master[e];
+    } else if (e < MB2) {
+        pk[B1S + e - MB1] = master[e];
+    } else if (e < MB3) {
+        pk[B2S + e - MB2] = master[e];
+    } else if (e < MB4) {
+        pk[B3S + e - MB3] = master[e];
+    } else if (e < kMasterFloats) {
+        pk[B4S + e - MB4] = master[e];
+    }
+}
+
+size_t ws_smem_bytes(int nc, int nm) {
+    return (size_t)(TABLES + 4 * nc + 2 * nm) * sizeof(float);
+}
+
+Stats stats_of(const Ctx& cx) {
+    Stats s;
+    for (int i = 0; i < 8; ++i) {
+        s.mean[i] = cx.model.mean[i];
+        s.std_[i] = cx.model.std_[i];
+    }
+    return s;
+}
+
+template <bool PIPE>
+cudaError_t launch_ws(Ctx& cx, const Job& J) {
+    const size_t smem = ws_smem_bytes(PIPE ? J.nc : 0, PIPE ? J.nm : 0);
+    if (smem > 227 * 1024) return cudaErrorInvalidValue;
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(ws_kernel<PIPE>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             227 * 1024);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    const int64_t tiles = (J.n + TM - 1) / TM;
+    const int grid = (int)(tiles < cx.num_sms ? tiles : cx.num_sms);
+    ws_kernel<PIPE><<<grid, kThreads, smem, cx.stream>>>(cx.model.wt, stats_of(cx), J);
+    ++cx.launches;
+    return cudaGetLastError();
 }
 
 }  // namespace
 
-size_t mlp_smem_bytes() { return (size_t)kBaseFloats * sizeof(float); }
-
-static size_t pipeline_smem_bytes(int nc, int nm) {
-    return (size_t)(kBaseFloats + 4 * nc + 2 * nm) * sizeof(float);
-}
+size_t mlp_smem_bytes() { return ws_smem_bytes(0, 0); }
 
 // Pack the reference-layout model (W_l row-major [out][in], concatenated, in
-// double) into the transposed zero-padded FP32 layout the kernels expect.
+// double) into the padded FP32 layout the kernels stage into shared memory.
 cudaError_t model_upload(Ctx& cx, const double* W, const double* b) {
     std::vector<float> pk(kModelFloats, 0.f);
-    const double* W1 = W;
-    const double* W2 = W1 + 100 * 134;
-    const double* W3 = W2 + 50 * 100;
-    const double* W4 = W3 + 25 * 50;
-    for (int k = 0; k < 134; ++k)
-        for (int g = 0; g < 4; ++g)
-            for (int t = 0; t < 26; ++t) {
-                const int nn = 26 * g + t;
-                if (nn < 100) pk[kOffW1 + k * kW1Stride + g * 28 + t] = (float)W1[nn * 134 + k];
-            }
-    for (int k = 0; k < 100; ++k)
-        for (int g = 0; g < 4; ++g)
-            for (int t = 0; t < 13; ++t) {
-                const int nn = 13 * g + t;
-                if (nn < 50) pk[kOffW2 + k * kW2Stride + g * 16 + t] = (float)W2[nn * 100 + k];
-            }
-    for (int k = 0; k < 50; ++k)
-        for (int g = 0; g < 4; ++g)
-            for (int t = 0; t < 7; ++t) {
-                const int nn = 7 * g + t;
-                if (nn < 25) pk[kOffW3 + k * kW3Stride + g * 8 + t] = (float)W3[nn * 50 + k];
-            }
-    for (int k = 0; k < 25; ++k)
-        for (int nn = 0; nn < 7; ++nn) pk[kOffW4 + k * kW4Stride + nn] = (float)W4[nn * 25 + k];
-    const double* b1 = b;
-    const double* b2 = b1 + 100;
-    const double* b3 = b2 + 50;
-    const double* b4 = b3 + 25;
-    for (int i = 0; i < 100; ++i) pk[kOffB1 + i] = (float)b1[i];
-    for (int i = 0; i < 50; ++i) pk[kOffB2 + i] = (float)b2[i];
-    for (int i = 0; i < 25; ++i) pk[kOffB3 + i] = (float)b3[i];
-    for (int i = 0; i < 7; ++i) pk[kOffB4 + i] = (float)b4[i];
+    for (int nn = 0; nn < 100; ++nn)
+        for (int k = 0; k < 134; ++k)
+            pk[W1S + (k * 8 + nn / 13) * 16 + nn % 13] = (float)W[MW1 + nn * 134 + k];
+    for (int nn = 0; nn < 50; ++nn)
+        for (int k = 0; k < 100; ++k)
+            pk[W2S + (k * 8 + nn / 7) * 8 + nn % 7] = (float)W[MW2 + nn * 100 + k];
+    for (int nn = 0; nn < 25; ++nn)
+        for (int k = 0; k < 50; ++k)
+            pk[W3S + (k * 8 + nn / 4) * 4 + nn % 4] = (float)W[MW3 + nn * 50 + k];
+    for (int nn = 0; nn < 7; ++nn)
+        for (int k = 0; k < 25; ++k) pk[W4S + k * 8 + nn] = (float)W[MW4 + nn * 25 + k];
+    for (int i = 0; i < 100; ++i) pk[B1S + i] = (float)b[i];
+    for (int i = 0; i < 50; ++i) pk[B2S + i] = (float)b[100 + i];
+    for (int i = 0; i < 25; ++i) pk[B3S + i] = (float)b[150 + i];
+    for (int i = 0; i < 7; ++i) pk[B4S + i] = (float)b[175 + i];
     ModelDev& md = cx.model;
     if (!md.wt) {
         cudaError_t e = cudaMalloc(&md.wt, sizeof(float) * kModelFloats);
@@ -485,69 +563,25 @@ cudaError_t model_upload(Ctx& cx, const double* W, const double* b) {
                            cudaMemcpyHostToDevice, cx.stream);
 }
 
-// Device-side repack of the master weights (reference layout, f32) into the
-// packed inference layout, after a training update.  Padding stays zero.
-__global__ void repack_kernel(const float* __restrict__ master, float* __restrict__ pk) {
-    const int e = blockIdx.x * blockDim.x + threadIdx.x;
-    constexpr int MW2 = 100 * 134, MW3 = MW2 + 50 * 100, MW4 = MW3 + 25 * 50;
-    constexpr int MB1 = MW4 + 7 * 25, MB2 = MB1 + 100, MB3 = MB2 + 50, MB4 = MB3 + 25;
-    if (e < MW2) {
-        const int nn = e / 134, k = e - nn * 134;
-        pk[kOffW1 + k * kW1Stride + (nn / 26) * 28 + nn % 26] = master[e];
-    } else if (e < MW3) {
-        const int f = e - MW2, nn = f / 100, k = f - nn * 100;
-        pk[kOffW2 + k * kW2Stride + (nn / 13) * 16 + nn % 13] = master[e];
-    } else if (e < MW4) {
-        const int f = e - MW3, nn = f / 50, k = f - nn * 50;
-        pk[kOffW3 + k * kW3Stride + (nn / 7) * 8 + nn % 7] = master[e];
-    } else if (e < MB1) {
-        const int f = e - MW4, nn = f / 25, k = f - nn * 25;
-        pk[kOffW4 + k * kW4Stride + nn] = master[e];
-    } else if (e < MB2) {
-        pk[kOffB1 + e - MB1] = master[e];
-    } else if (e < MB3) {
-        pk[kOffB2 + e - MB2] = master[e];
-    } else if (e < MB4) {
-        pk[kOffB3 + e - MB3] = master[e];
-    } else if (e < MB4 + 7) {
-        pk[kOffB4 + e - MB4] = master[e];
-    }
-}
-
 cudaError_t launch_repack(Ctx& cx) {
-    const int total = 100 * 134 + 50 * 100 + 25 * 50 + 7 * 25 + 182;
-    repack_kernel<<<(total + 255) / 256, 256, 0, cx.stream>>>(cx.model.w_master, cx.model.wt);
+    repack_kernel<<<(kMasterFloats + 255) / 256, 256, 0, cx.stream>>>(cx.model.w_master,
+                                                                      cx.model.wt);
     ++cx.launches;
     return cudaGetLastError();
-}
-
-static Stats stats_of(const Ctx& cx) {
-    Stats s;
-    for (int i = 0; i < 8; ++i) {
-        s.mean[i] = cx.model.mean[i];
-        s.std_[i] = cx.model.std_[i];
-    }
-    return s;
 }
 
 cudaError_t launch_predict(Ctx& cx, const float* fused, int64_t n, int64_t ld, float* params,
                            uint8_t* clamped, float* raw) {
     if (n <= 0) return cudaSuccess;
-    const size_t smem = mlp_smem_bytes();
-    static bool attr_set = false;  // per process; same value for every device
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(predict_kernel,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)(227 * 1024));
-        if (e != cudaSuccess) return e;
-        attr_set = true;
-    }
-    const int64_t tiles = (n + kTile - 1) / kTile;
-    const int grid = (int)(tiles < cx.num_sms ? tiles : cx.num_sms);
-    predict_kernel<<<grid, kThreads, smem, cx.stream>>>(cx.model.wt, stats_of(cx), fused, n, ld,
-                                                       params, clamped, raw);
-    ++cx.launches;
-    return cudaGetLastError();
+    Job J{};
+    J.fused = fused;
+    J.n = n;
+    J.ld = ld;
+    J.params = params;
+    J.clamped = clamped;
+    J.raw = raw;
+    J.ld_out = ld;
+    return launch_ws<false>(cx, J);
 }
 
 cudaError_t launch_pipeline(Ctx& cx, const uint32_t* counts, const float* dcgm, int64_t n,
@@ -555,23 +589,25 @@ cudaError_t launch_pipeline(Ctx& cx, const uint32_t* counts, const float* dcgm, 
                             int32_t* idx, float* cost, float* energy, float* time,
                             int64_t ld_out) {
     if (n <= 0) return cudaSuccess;
-    const size_t smem = pipeline_smem_bytes(cx.dom.nc, cx.dom.nm);
-    if (smem > 227 * 1024) return cudaErrorInvalidValue;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(pipeline_kernel,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)(227 * 1024));
-        if (e != cudaSuccess) return e;
-        attr_set = true;
-    }
-    const int64_t tiles = (n + kTile - 1) / kTile;
-    const int grid = (int)(tiles < cx.num_sms ? tiles : cx.num_sms);
-    pipeline_kernel<<<grid, kThreads, smem, cx.stream>>>(
-        cx.model.wt, stats_of(cx), cx.dom.core4, cx.dom.nc, cx.dom.mem2, cx.dom.nm, eta, K,
-        counts, dcgm, n, ld, params, clamped, idx, cost, energy, time, ld_out);
-    ++cx.launches;
-    return cudaGetLastError();
+    Job J{};
+    J.counts = counts;
+    J.dcgm = dcgm;
+    J.n = n;
+    J.ld = ld;
+    J.core4 = cx.dom.core4;
+    J.mem2 = cx.dom.mem2;
+    J.nc = cx.dom.nc;
+    J.nm = cx.dom.nm;
+    J.eta = eta;
+    J.K = K;
+    J.params = params;
+    J.clamped = clamped;
+    J.idx = idx;
+    J.cost = cost;
+    J.energy = energy;
+    J.time = time;
+    J.ld_out = ld_out;
+    return launch_ws<true>(cx, J);
 }
 
 }  // namespace dso_b200
