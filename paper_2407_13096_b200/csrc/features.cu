@@ -29,7 +29,7 @@ namespace {
 // then written out row-contiguous with 128-bit stores.  72.7 KB of shared
 // memory per CTA -> 3 CTAs per SM, so one CTA's loads overlap another's math
 // and stores.
-__global__ void __launch_bounds__(256) featurize_kernel(const uint32_t* __restrict__ counts,
+__global__ void __launch_bounds__(256, 2) featurize_kernel(const uint32_t* __restrict__ counts,
                                                         const float* __restrict__ dcgm,
                                                         int64_t n, int64_t ld,
                                                         float* __restrict__ fused) {
@@ -97,7 +97,7 @@ __global__ void __launch_bounds__(256) dcgm_mean_kernel(const double* __restrict
 cudaError_t launch_featurize(Ctx& cx, const uint32_t* counts, const float* dcgm, int64_t n,
                              int64_t ld, float* fused) {
     if (n <= 0) return cudaSuccess;
-    const size_t smem = (size_t)(DSO_FUSED_ROWS * kFeatTile + 1280) * sizeof(float);
+    const size_t smem = (size_t)(DSO_FUSED_ROWS * kFeatTile + 1024) * sizeof(float);
     static bool attr = false;
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(featurize_kernel,

@@ -63,11 +63,10 @@ __device__ __forceinline__ void tile_features(float* act, float* scratch,
     }
     __syncthreads();
     // phase 2: exact totals (u64), split so both thread halves sum ~63 rows.
-    // scratch (1280 floats): tf[3][128], rr[3][128], totd f64[3][128], part u64[128]
+    // scratch (1024 floats): tf[3][128], rr[3][128], part u64[128]
     float* tfv = scratch;
     float* rrv = tfv + 3 * kFeatTile;
-    double* totd = reinterpret_cast<double*>(rrv + 3 * kFeatTile);
-    uint64_t* part = reinterpret_cast<uint64_t*>(totd + 3 * kFeatTile);
+    uint64_t* part = reinterpret_cast<uint64_t*>(rrv + 3 * kFeatTile);
     constexpr int kSplit = 60;
     const int m = tid & (kFeatTile - 1);
     uint64_t s_a = 0, s_b = 0, s_c = 0;
@@ -82,18 +81,19 @@ __device__ __forceinline__ void tile_features(float* act, float* scratch,
     }
     __syncthreads();
     // tf = total as float (exact below 2^24), rr = RN(1/tf); tf = 0 marks a zero
-    // total, tf = -1 a total >= 2^24 (FP64 division by totd in phase 3).
+    // total.  A total >= 2^24 is stored exactly as two 24-bit halves:
+    // tf = -hi, rr = lo (total = hi * 2^24 + lo), for the FP64 path of phase 3.
     auto scale = [&](int cat, uint64_t tot) {
         float tf = 0.f, rr = 0.f;
         if (tot != 0 && tot < (1u << 24)) {
             tf = __uint2float_rn((uint32_t)tot);
             rr = __frcp_rn(tf);
         } else if (tot != 0) {
-            tf = -1.f;
+            tf = -(float)(tot >> 24);               // exact: hi < 2^24 for totals < 2^48
+            rr = (float)(tot & 0xFFFFFFu);          // exact
         }
         tfv[cat * kFeatTile + m] = tf;
         rrv[cat * kFeatTile + m] = rr;
-        totd[cat * kFeatTile + m] = (double)tot;
     };
     if (tid < kFeatTile) {
         scale(0, s_a + part[m]);
@@ -130,7 +130,7 @@ __device__ __forceinline__ void tile_features(float* act, float* scratch,
                 } else if (tt[e] == 0.f) {
                     o[e] = 0.f;
                 } else {
-                    o[e] = (float)((double)cc[e] / totd[cat * kFeatTile + 4 * q + e]);
+                    o[e] = (float)((double)cc[e] / fma((double)-tt[e], 16777216.0, (double)ri[e]));
                 }
             }
             *reinterpret_cast<float4*>(cp) = make_float4(o[0], o[1], o[2], o[3]);

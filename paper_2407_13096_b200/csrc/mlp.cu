@@ -64,7 +64,7 @@ constexpr int kActFloats = 134 * RS;
 constexpr int OUT = ACT + 2 * kActFloats;   // out[2][8][RS]  (raw predictions)
 constexpr int kOutFloats = 8 * RS;
 constexpr int SCR = OUT + 2 * kOutFloats;   // producer scratch: tf[3][64] rr[3][64]
-constexpr int kScrFloats = 6 * TM + 6 * TM + 2 * TM;  // + totd f64[3][64] + part u64[64]
+constexpr int kScrFloats = 6 * TM + 2 * TM;  // + part u64[64]
 constexpr int STATS = SCR + kScrFloats;     // mean[8] std[8]
 constexpr int TABLES = STATS + 16;          // core4[nc], mem2[nm]
 static_assert(W2S % 4 == 0 && W3S % 4 == 0 && W4S % 4 == 0 && B1S % 4 == 0 &&
@@ -223,10 +223,9 @@ __device__ __forceinline__ void produce_features(float* act, float* scr,
     }
     bar_sync(BAR_PROD, kProducers);
     // phase 2: exact integer totals per (kernel, category)
-    float* tfv = scr;                                                  // [3][64]
-    float* rrv = scr + 3 * TM;                                         // [3][64]
-    double* totd = reinterpret_cast<double*>(scr + 6 * TM);            // [3][64]
-    uint64_t* part = reinterpret_cast<uint64_t*>(scr + 12 * TM);       // [64]
+    float* tfv = scr;                                            // [3][64]
+    float* rrv = scr + 3 * TM;                                   // [3][64]
+    uint64_t* part = reinterpret_cast<uint64_t*>(scr + 6 * TM);  // [64]
     constexpr int kSplit = 60;
     const int m = pt & 63;
     uint64_t sa = 0, sb = 0, sc = 0;
@@ -241,18 +240,19 @@ __device__ __forceinline__ void produce_features(float* act, float* scr,
     }
     bar_sync(BAR_PROD, kProducers);
     auto scale = [&](int cat, uint64_t tot) {
-        // tf = exact total as float, rr = RN(1/tf); tf 0 marks a zero total,
-        // -1 a total >= 2^24 (FP64 division by totd below)
+        // tf = exact total as float, rr = RN(1/tf); tf 0 marks a zero total.
+        // A total >= 2^24 is kept exactly as two 24-bit halves: tf = -hi,
+        // rr = lo (total = hi * 2^24 + lo), for the FP64 path below.
         float tf = 0.f, rr = 0.f;
         if (tot != 0 && tot < (1u << 24)) {
             tf = __uint2float_rn((uint32_t)tot);
             rr = __frcp_rn(tf);
         } else if (tot != 0) {
-            tf = -1.f;
+            tf = -(float)(tot >> 24);               // exact: hi < 2^24 for totals < 2^48
+            rr = (float)(tot & 0xFFFFFFu);          // exact
         }
         tfv[cat * TM + m] = tf;
         rrv[cat * TM + m] = rr;
-        totd[cat * TM + m] = (double)tot;
     };
     if (pt < TM) {
         scale(0, sa + part[m]);
@@ -286,7 +286,7 @@ __device__ __forceinline__ void produce_features(float* act, float* scr,
             } else if (tt[e] == 0.f) {
                 o[e] = 0.f;
             } else {
-                o[e] = (float)((double)cc[e] / totd[cat * TM + 4 * q + e]);
+                o[e] = (float)((double)cc[e] / fma((double)-tt[e], 16777216.0, (double)ri[e]));
             }
         }
         *reinterpret_cast<float4*>(cp) = make_float4(o[0], o[1], o[2], o[3]);
