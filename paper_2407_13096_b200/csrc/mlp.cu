@@ -5,13 +5,13 @@
 // de-standardised (forward_raw mlp.cpp:381-384) and clamped (predict_params
 // mlp.cpp:386-402, kBetaFloor mlp.cpp:15).
 //
-// Execution model — one persistent, warp-specialised CTA per SM (384 threads):
-//   * 8 CONSUMER warps run the MLP on a tile of 64 kernels held k-major in
-//     shared memory (act[134][64]); each layer is a register-tiled FP32 GEMM
-//     on the FMA pipe with Blackwell's packed FFMA2 (thread = 2 kernels x TN
-//     neurons, pairs along kernels, weights as scalar shared-memory broadcasts,
-//     operands of step k+1 in flight while step k issues); layer outputs
-//     overwrite act in place;
+// Execution model — one persistent, warp-specialised CTA per SM (256 threads):
+//   * 4 CONSUMER warps (one per SM sub-partition) run the MLP on a tile of 64
+//     kernels held k-major in shared memory (act[134][64]); each layer is a
+//     register-tiled FP32 GEMM on the FMA pipe with Blackwell's packed FFMA2
+//     (L1: thread = 2 kernels x 26 neurons, 26 FFMA2 per 8 shared loads;
+//     weights are warp-uniform broadcasts; operands of step k+1 in flight
+//     while step k issues); layer outputs overwrite act in place;
 //   * 4 PRODUCER warps, meanwhile, (a) finish the previous tile: clamp, then
 //     P(f), T(f), the eta objective and the lexicographic argmin over the
 //     whole frequency grid, and (b) run the feature stage of the tile after
@@ -41,23 +41,25 @@ namespace {
 constexpr int TM = 64;           // kernels per tile
 constexpr int RS = 64;           // act row stride (floats)
 constexpr int RS2 = RS / 2;
-constexpr int kConsumers = 256;  // 8 warps
+constexpr int kConsumers = 128;  // 4 warps: one per SM sub-partition
 constexpr int kProducers = 128;  // 4 warps
 constexpr int kThreads = kConsumers + kProducers;
 
 // Named barriers (0 is __syncthreads).
 constexpr int BAR_CONS = 1, BAR_PROD = 2, BAR_FULL0 = 3, BAR_READY0 = 5;
 
-// Packed model (floats).  Layer l: [K][8 groups][TNP], neuron n = TN*g + t.
-constexpr int W1S = 0;                   // [134][8][16] TN 13 (104 >= 100)
-constexpr int W2S = W1S + 134 * 8 * 16;  // [100][8][8]  TN 7  (56 >= 50)
-constexpr int W3S = W2S + 100 * 8 * 8;   // [50][8][4]   TN 4  (32 >= 25)
-constexpr int W4S = W3S + 50 * 8 * 4;    // [25][8]      TN 1  (8 >= 7)
+// Packed model (floats), k-major, one neuron group per consumer warp g (0..3):
+//   L1 [134][4][28] (26 used, n = 26g + t)   L2 [100][4][16] (13 used, n = 13g + t)
+//   L3 [50][4][8]   (7 used,  n = 7g + t)    L4 [25][8]      (n = 2g + t, t < 2)
+constexpr int W1S = 0;
+constexpr int W2S = W1S + 134 * 112;
+constexpr int W3S = W2S + 100 * 64;
+constexpr int W4S = W3S + 50 * 32;
 constexpr int B1S = W4S + 25 * 8;        // [104]
-constexpr int B2S = B1S + 104;           // [56]
-constexpr int B3S = B2S + 56;            // [32]
-constexpr int B4S = B3S + 32;            // [8]
-constexpr int kModelFloats = B4S + 8;    // 25552
+constexpr int B2S = B1S + 104;           // [52]
+constexpr int B3S = B2S + 52;            // [28]
+constexpr int B4S = B3S + 28;            // [8]
+constexpr int kModelFloats = B4S + 8;    // 23400
 // per-CTA shared memory beyond the model
 constexpr int ACT = kModelFloats;           // act[2][134][RS]
 constexpr int kActFloats = 134 * RS;
@@ -87,81 +89,176 @@ __device__ __forceinline__ void bar_arrive(int id, int count) {
 }
 
 // ---------------------------------------------------------------------------
-// Consumer: accumulate one dense layer (rows 0..K-1 of act in).
-template <int K, int TN, int TNP>
-__device__ __forceinline__ void dense_acc(const float* sm, const float* act, int woff, int ct,
-                                          float2 (&acc)[TN]) {
-    const int mp = ct & 31, g = ct >> 5;
-    const float2* in2 = reinterpret_cast<const float2*>(act);
+// Consumer (4 warps, thread ct = 0..127): the MLP on one 64-kernel tile held
+// k-major in act[134][64].  Thread = kernel pair mp (lane, kernels 2mp, 2mp+1)
+// x neuron group g (warp).  Each k-loop is software-pipelined over two register
+// stages (operands of step k+1 in flight while step k's FFMA2s issue, the
+// stages alternating without copies); each warp owns its SM sub-partition's
+// FMA pipe, so latency is covered by ILP (26 independent accumulator pairs in
+// L1), not by other warps.  Weights are warp-uniform -> shared-memory
+// broadcasts; an activation pair load is 256 contiguous bytes per warp.
+__device__ __forceinline__ void consumer_tile(const float* W, float* act, float* out, int ct) {
+    float2* act2 = reinterpret_cast<float2*>(act);  // [row][32] kernel pairs
+    const int mp = ct & 31;
+    const int g = ct >> 5;
+    // ---- L1: 134 -> 100 (neurons 26g .. 26g+25), pairs along n -------------
+    {
+        float2 acc0[13], acc1[13];
 #pragma unroll
-    for (int t = 0; t < TN; ++t) acc[t] = f2(0.f, 0.f);
-    struct Op {
-        float2 a;
-        float w[TNP];
-    };
-    auto load = [&](Op& o, int k) {
-        o.a = in2[k * RS2 + mp];
-        const float* w = sm + woff + (k * 8 + g) * TNP;
-        if constexpr (TNP % 4 == 0) {
+        for (int p = 0; p < 13; ++p) acc0[p] = acc1[p] = f2(0.f, 0.f);
+        const float* wbase = W + W1S + g * 28;
+        struct Op {
+            float2 a;
+            float4 v[6];
+            float2 l;
+        };
+        auto load = [&](Op& o, int k) {
+            const float* w = wbase + k * 112;
+            o.a = act2[k * RS2 + mp];
 #pragma unroll
-            for (int q = 0; q < TNP / 4; ++q) {
-                const float4 v = reinterpret_cast<const float4*>(w)[q];
-                o.w[4 * q] = v.x;
-                o.w[4 * q + 1] = v.y;
-                o.w[4 * q + 2] = v.z;
-                o.w[4 * q + 3] = v.w;
+            for (int q = 0; q < 6; ++q) o.v[q] = reinterpret_cast<const float4*>(w)[q];
+            o.l = reinterpret_cast<const float2*>(w)[12];
+        };
+        auto math = [&](const Op& o) {
+            float2 w[13];
+#pragma unroll
+            for (int q = 0; q < 6; ++q) {
+                w[2 * q] = f2(o.v[q].x, o.v[q].y);
+                w[2 * q + 1] = f2(o.v[q].z, o.v[q].w);
             }
-        } else {
+            w[12] = o.l;
 #pragma unroll
-            for (int q = 0; q < TNP; ++q) o.w[q] = w[q];
-        }
-    };
-    auto math = [&](const Op& o) {
-#pragma unroll
-        for (int t = 0; t < TN; ++t) acc[t] = ffma2(o.a, f2(o.w[t], o.w[t]), acc[t]);
-    };
-    Op A, B;
-    load(A, 0);
+            for (int p = 0; p < 13; ++p) {
+                acc0[p] = ffma2(f2(o.a.x, o.a.x), w[p], acc0[p]);
+                acc1[p] = ffma2(f2(o.a.y, o.a.y), w[p], acc1[p]);
+            }
+        };
+        Op A, B;
+        load(A, 0);
 #pragma unroll 1
-    for (int k = 0; k + 1 < K; k += 2) {
-        load(B, k + 1);
-        math(A);
-        load(A, k + 2 < K ? k + 2 : K - 1);
-        math(B);
-    }
-    if (K & 1) math(A);
-}
-
-template <int K, int TN, int TNP>
-__device__ __forceinline__ void dense_sigmoid_inplace(const float* sm, float* act, int woff,
-                                                      int boff, int ct) {
-    float2 acc[TN];
-    dense_acc<K, TN, TNP>(sm, act, woff, ct, acc);
-    bar_sync(BAR_CONS, kConsumers);  // every consumer has read its inputs
-    const int mp = ct & 31, g = ct >> 5;
-    float2* out2 = reinterpret_cast<float2*>(act);
+        for (int k = 0; k < 134; k += 2) {
+            load(B, k + 1);
+            math(A);
+            load(A, k + 2 < 134 ? k + 2 : 133);
+            math(B);
+        }
+        bar_sync(BAR_CONS, kConsumers);  // all reads of act done
+        const float* b = W + B1S + g * 26;
 #pragma unroll
-    for (int t = 0; t < TN; ++t) {
-        const float bb = sm[boff + TN * g + t];
-        out2[(TN * g + t) * RS2 + mp] =
-            f2(sigmoidf_fast(acc[t].x + bb), sigmoidf_fast(acc[t].y + bb));
+        for (int p = 0; p < 13; ++p) {
+            const int n = g * 26 + 2 * p;
+            const float b0 = b[2 * p], b1 = b[2 * p + 1];
+            act2[n * RS2 + mp] = f2(sigmoidf_fast(acc0[p].x + b0), sigmoidf_fast(acc1[p].x + b0));
+            act2[(n + 1) * RS2 + mp] =
+                f2(sigmoidf_fast(acc0[p].y + b1), sigmoidf_fast(acc1[p].y + b1));
+        }
+        bar_sync(BAR_CONS, kConsumers);
     }
-    bar_sync(BAR_CONS, kConsumers);
-}
-
-// Full forward on act -> raw outputs (forward_raw, not clamped) in out rows 0..6.
-__device__ __forceinline__ void consumer_tile(const float* sm, float* act, float* out, int ct) {
-    dense_sigmoid_inplace<134, 13, 16>(sm, act, W1S, B1S, ct);
-    dense_sigmoid_inplace<100, 7, 8>(sm, act, W2S, B2S, ct);
-    dense_sigmoid_inplace<50, 4, 4>(sm, act, W3S, B3S, ct);
-    float2 acc[1];
-    dense_acc<25, 1, 1>(sm, act, W4S, ct, acc);
-    const int mp = ct & 31, g = ct >> 5;
-    if (g < 7) {
-        const float bb = sm[B4S + g], s = sm[STATS + 8 + g], mu = sm[STATS + g];
-        // forward_raw: (z * std) + mean, z = (W a) + b
-        reinterpret_cast<float2*>(out)[g * RS2 + mp] =
-            f2(fmaf(acc[0].x + bb, s, mu), fmaf(acc[0].y + bb, s, mu));
+    // ---- L2: 100 -> 50 (neurons 13g .. 13g+12), pairs along m ----------------
+    {
+        float2 acc[13];
+#pragma unroll
+        for (int t = 0; t < 13; ++t) acc[t] = f2(0.f, 0.f);
+        const float* wbase = W + W2S + g * 16;
+        struct Op {
+            float2 a;
+            float4 v0, v1, v2;
+            float v3;
+        };
+        auto load = [&](Op& o, int k) {
+            const float* w = wbase + k * 64;
+            o.a = act2[k * RS2 + mp];
+            o.v0 = reinterpret_cast<const float4*>(w)[0];
+            o.v1 = reinterpret_cast<const float4*>(w)[1];
+            o.v2 = reinterpret_cast<const float4*>(w)[2];
+            o.v3 = w[12];
+        };
+        auto math = [&](const Op& o) {
+            const float w[13] = {o.v0.x, o.v0.y, o.v0.z, o.v0.w, o.v1.x, o.v1.y, o.v1.z,
+                                 o.v1.w, o.v2.x, o.v2.y, o.v2.z, o.v2.w, o.v3};
+#pragma unroll
+            for (int t = 0; t < 13; ++t) acc[t] = ffma2(o.a, f2(w[t], w[t]), acc[t]);
+        };
+        Op A, B;
+        load(A, 0);
+#pragma unroll 1
+        for (int k = 0; k < 100; k += 2) {
+            load(B, k + 1);
+            math(A);
+            load(A, k + 2 < 100 ? k + 2 : 99);
+            math(B);
+        }
+        bar_sync(BAR_CONS, kConsumers);
+        const float* b = W + B2S + g * 13;
+#pragma unroll
+        for (int t = 0; t < 13; ++t) {
+            const float bb = b[t];
+            act2[(g * 13 + t) * RS2 + mp] =
+                f2(sigmoidf_fast(acc[t].x + bb), sigmoidf_fast(acc[t].y + bb));
+        }
+        bar_sync(BAR_CONS, kConsumers);
+    }
+    // ---- L3: 50 -> 25 (neurons 7g .. 7g+6), pairs along m ---------------------
+    {
+        float2 acc[7];
+#pragma unroll
+        for (int t = 0; t < 7; ++t) acc[t] = f2(0.f, 0.f);
+        const float* wbase = W + W3S + g * 8;
+        struct Op {
+            float2 a;
+            float4 v0, v1;
+        };
+        auto load = [&](Op& o, int k) {
+            const float* w = wbase + k * 32;
+            o.a = act2[k * RS2 + mp];
+            o.v0 = reinterpret_cast<const float4*>(w)[0];
+            o.v1 = reinterpret_cast<const float4*>(w)[1];
+        };
+        auto math = [&](const Op& o) {
+            const float w[7] = {o.v0.x, o.v0.y, o.v0.z, o.v0.w, o.v1.x, o.v1.y, o.v1.z};
+#pragma unroll
+            for (int t = 0; t < 7; ++t) acc[t] = ffma2(o.a, f2(w[t], w[t]), acc[t]);
+        };
+        Op A, B;
+        load(A, 0);
+#pragma unroll 1
+        for (int k = 0; k < 50; k += 2) {
+            load(B, k + 1);
+            math(A);
+            load(A, k + 2 < 50 ? k + 2 : 49);
+            math(B);
+        }
+        bar_sync(BAR_CONS, kConsumers);
+        const float* b = W + B3S + g * 7;
+#pragma unroll
+        for (int t = 0; t < 7; ++t) {
+            const float bb = b[t];
+            act2[(g * 7 + t) * RS2 + mp] =
+                f2(sigmoidf_fast(acc[t].x + bb), sigmoidf_fast(acc[t].y + bb));
+        }
+        bar_sync(BAR_CONS, kConsumers);
+    }
+    // ---- L4: 25 -> 7 (neurons 2g, 2g+1), identity, de-standardise -------------
+    {
+        float2 acc[2] = {f2(0.f, 0.f), f2(0.f, 0.f)};
+        const float* wbase = W + W4S + g * 2;
+#pragma unroll 5
+        for (int k = 0; k < 25; ++k) {
+            const float2 a = act2[k * RS2 + mp];
+            const float2 w = *reinterpret_cast<const float2*>(wbase + k * 8);
+            acc[0] = ffma2(a, f2(w.x, w.x), acc[0]);
+            acc[1] = ffma2(a, f2(w.y, w.y), acc[1]);
+        }
+        float2* out2 = reinterpret_cast<float2*>(out);
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+            const int n = 2 * g + t;
+            if (n < 7) {
+                const float bb = W[B4S + n], s = W[STATS + 8 + n], mu = W[STATS + n];
+                // forward_raw: (z * std) + mean, z = (W a) + b
+                out2[n * RS2 + mp] = f2(fmaf(acc[t].x + bb, s, mu), fmaf(acc[t].y + bb, s, mu));
+            }
+        }
     }
 }
 
@@ -477,13 +574,13 @@ __global__ void repack_kernel(const float* __restrict__ master, float* __restric
     const int e = blockIdx.x * blockDim.x + threadIdx.x;
     if (e < MW2) {
         const int nn = e / 134, k = e - nn * 134;
-        pk[W1S + (k * 8 + nn / 13) * 16 + nn % 13] = master[e];
+        pk[W1S + k * 112 + (nn / 26) * 28 + nn % 26] = master[e];
     } else if (e < MW3) {
         const int f = e - MW2, nn = f / 100, k = f - nn * 100;
-        pk[W2S + (k * 8 + nn / 7) * 8 + nn % 7] = master[e];
+        pk[W2S + k * 64 + (nn / 13) * 16 + nn % 13] = master[e];
     } else if (e < MW4) {
         const int f = e - MW3, nn = f / 50, k = f - nn * 50;
-        pk[W3S + (k * 8 + nn / 4) * 4 + nn % 4] = master[e];
+        pk[W3S + k * 32 + (nn / 7) * 8 + nn % 7] = master[e];
     } else if (e < MB1) {
         const int f = e - MW4, nn = f / 25, k = f - nn * 25;
         pk[W4S + k * 8 + nn] = master[e];
@@ -540,13 +637,13 @@ cudaError_t model_upload(Ctx& cx, const double* W, const double* b) {
     std::vector<float> pk(kModelFloats, 0.f);
     for (int nn = 0; nn < 100; ++nn)
         for (int k = 0; k < 134; ++k)
-            pk[W1S + (k * 8 + nn / 13) * 16 + nn % 13] = (float)W[MW1 + nn * 134 + k];
+            pk[W1S + k * 112 + (nn / 26) * 28 + nn % 26] = (float)W[MW1 + nn * 134 + k];
     for (int nn = 0; nn < 50; ++nn)
         for (int k = 0; k < 100; ++k)
-            pk[W2S + (k * 8 + nn / 7) * 8 + nn % 7] = (float)W[MW2 + nn * 100 + k];
+            pk[W2S + k * 64 + (nn / 13) * 16 + nn % 13] = (float)W[MW2 + nn * 100 + k];
     for (int nn = 0; nn < 25; ++nn)
         for (int k = 0; k < 50; ++k)
-            pk[W3S + (k * 8 + nn / 4) * 4 + nn % 4] = (float)W[MW3 + nn * 50 + k];
+            pk[W3S + k * 32 + (nn / 7) * 8 + nn % 7] = (float)W[MW3 + nn * 50 + k];
     for (int nn = 0; nn < 7; ++nn)
         for (int k = 0; k < 25; ++k) pk[W4S + k * 8 + nn] = (float)W[MW4 + nn * 25 + k];
     for (int i = 0; i < 100; ++i) pk[B1S + i] = (float)b[i];

@@ -11,12 +11,13 @@ nvidia-smi -q -d CLOCK >> $OUT/nvidia-smi.txt 2>&1
 nproc > $OUT/nproc.txt; lscpu >> $OUT/nproc.txt 2>&1
 ( timeout 1200 python -m pytest tests -q -m gpu --timeout 600 -rf > $OUT/pytest_gpu.log 2>&1; echo "rc=$?" >> $OUT/pytest_gpu.log ) 
 ( timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "rc=$?" >> $OUT/smoke.log )
+( timeout 900 compute-sanitizer --tool memcheck --print-limit 20 python scripts/sanitize_run.py > $OUT/memcheck.log 2>&1; echo "rc=$?" >> $OUT/memcheck.log )
 ( timeout 900 python bench.py --steps 10 --warmup 3 > $OUT/bench.log 2>&1; echo "rc=$?" >> $OUT/bench.log )
 ( timeout 600 python bench.py --config c5 --steps 10 --warmup 3 > $OUT/bench_c5.log 2>&1; echo "rc=$?" >> $OUT/bench_c5.log )
 ( timeout 600 python bench.py --config c2 --steps 20 --warmup 3 --no-cpu > $OUT/bench_c2.log 2>&1; echo "rc=$?" >> $OUT/bench_c2.log )
 ( timeout 600 python bench.py --config c4 --steps 3 --warmup 3 --no-cpu > $OUT/bench_c4.log 2>&1; echo "rc=$?" >> $OUT/bench_c4.log )
 ( timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv \
     python bench.py --steps 2 --warmup 1 --kernels 4194304 --no-e2e --no-cpu > $OUT/ncu_launch_bench.log 2>&1; echo "rc=$?" >> $OUT/ncu_launch_bench.log )
-( timeout 900 ncu --set full --clock-control none --import-source on -k regex:pipeline_kernel -s 1 -c 1 \
-    -o $OUT/prof_pipeline python bench.py --steps 1 --warmup 1 --kernels 1048576 --no-e2e --no-cpu --no-stages > $OUT/ncu_full.log 2>&1; echo "rc=$?" >> $OUT/ncu_full.log )
+( timeout 900 ncu --set full --clock-control none --import-source on -k regex:ws_kernel -s 1 -c 1 \
+    -o $OUT/prof_pipeline python bench.py --steps 1 --warmup 1 --kernels 2097152 --no-e2e --no-cpu --no-stages > $OUT/ncu_full.log 2>&1; echo "rc=$?" >> $OUT/ncu_full.log )
 ls -la $OUT

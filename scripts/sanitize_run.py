@@ -1,0 +1,32 @@
+"""Small invocation of every device entry point, for compute-sanitizer runs."""
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2407_13096_b200 import config_domain, init_mlp  # noqa: E402
+from paper_2407_13096_b200.api import Context  # noqa: E402
+
+ctx = Context(0)
+for cfg in ("c1", "c3"):
+    ctx.set_domain(config_domain(cfg))
+    m = init_mlp(seed=1)
+    m.target_mean = np.array([60, 10, 0.01, 0.004, 0.15, 200, 200.0])
+    m.target_std = np.array([15, 3, 0.005, 0.001, 0.07, 100, 100.0])
+    ctx.set_model(m)
+    for n in (1, 63, 64, 65, 1000, 4099):
+        g = ctx.gen_synthetic(n, root=n)
+        f = ctx.featurize(g["counts"], g["dcgm"])
+        p, cl, raw = ctx.predict_params(f, want_raw=True)
+        ctx.brute_force_config(p, 0.8)
+        ctx.brute_force_config_exact(p.double().t().contiguous(), 0.8)
+        ctx.eta_sweep(p, np.arange(11) / 10.0)
+        ctx.pipeline(g["counts"], g["dcgm"], 0.8, want_params=True)
+        y = torch.randn((7, n), device="cuda")
+        gr, loss = ctx.train_grad(f, y)
+        ctx.train_apply(gr, 0.01, 1.0 / n)
+        ctx.dcgm_mean(torch.rand((3, 8, n), device="cuda", dtype=torch.float64))
+torch.cuda.synchronize()
+print("sanitize run ok")
