@@ -12,7 +12,7 @@ import enum
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libdso_b200.so")
+LIB_PATH = os.environ.get("DSO_B200_LIB") or os.path.join(_HERE, "lib", "libdso_b200.so")
 
 
 class ErrorKind(enum.IntEnum):

@@ -134,6 +134,21 @@ __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
     return *reinterpret_cast<float2*>(&D);
 }
 
+// Packed FP32x2 add / mul (FADD2 / FMUL2): same IEEE round-to-nearest result as
+// the scalar __fadd_rn / __fmul_rn on each lane.
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+    unsigned long long A = *reinterpret_cast<unsigned long long*>(&a);
+    unsigned long long B = *reinterpret_cast<unsigned long long*>(&b), D;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(D) : "l"(A), "l"(B));
+    return *reinterpret_cast<float2*>(&D);
+}
+__device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
+    unsigned long long A = *reinterpret_cast<unsigned long long*>(&a);
+    unsigned long long B = *reinterpret_cast<unsigned long long*>(&b), D;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(D) : "l"(A), "l"(B));
+    return *reinterpret_cast<float2*>(&D);
+}
+
 // FP32 pair evaluation shared by every sweep kernel (sweep, eta sweep, fused
 // pipeline) so all of them round identically.  Explicit _rn intrinsics stop
 // nvcc from re-contracting the expressions differently per kernel.

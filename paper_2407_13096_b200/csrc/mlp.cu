@@ -68,10 +68,11 @@ constexpr int kOutFloats = 8 * RS;
 constexpr int SCR = OUT + 2 * kOutFloats;   // producer scratch: tf[3][64] rr[3][64]
 constexpr int kScrFloats = 6 * TM + 2 * TM;  // + part u64[64]
 constexpr int STATS = SCR + kScrFloats;     // mean[8] std[8]
-constexpr int TABLES = STATS + 16;          // core4[nc], mem2[nm]
+constexpr int MBAR = STATS + 16;            // 2 mbarriers (u64) for the bulk tile loads
+constexpr int TABLES = MBAR + 4;            // core4[nc], mem2[nm]
 static_assert(W2S % 4 == 0 && W3S % 4 == 0 && W4S % 4 == 0 && B1S % 4 == 0 &&
                   kModelFloats % 4 == 0 && ACT % 4 == 0 && OUT % 4 == 0 && SCR % 4 == 0 &&
-                  TABLES % 4 == 0,
+                  MBAR % 2 == 0 && TABLES % 4 == 0,
               "16-byte alignment of smem regions");
 
 // master (reference) layout offsets: W1 | W2 | W3 | W4 | b1 | b2 | b3 | b4
@@ -80,6 +81,19 @@ constexpr int MB1 = MW4 + 7 * 25, MB2 = MB1 + 100, MB3 = MB2 + 50, MB4 = MB3 + 2
 constexpr int kMasterFloats = MB4 + 7;
 
 __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
+
+// Optional per-phase cycle accounting (debug builds only: -DDSO_PHASE_TIMING).
+#ifdef DSO_PHASE_TIMING
+__device__ unsigned long long g_phase_cycles[16];
+#define PT_BEGIN(v) long long v = clock64()
+#define PT_END(ph, v)                                                                   \
+    do {                                                                               \
+        if ((threadIdx.x & 127) == 0) atomicAdd(&g_phase_cycles[ph], clock64() - (v)); \
+    } while (0)
+#else
+#define PT_BEGIN(v) (void)0
+#define PT_END(ph, v) (void)0
+#endif
 
 __device__ __forceinline__ void bar_sync(int id, int count) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
@@ -133,6 +147,7 @@ __device__ __forceinline__ void consumer_tile(const float* W, float* act, float*
                 acc1[p] = ffma2(f2(o.a.y, o.a.y), w[p], acc1[p]);
             }
         };
+        PT_BEGIN(t_l1);
         Op A, B;
         load(A, 0);
 #pragma unroll 1
@@ -142,6 +157,8 @@ __device__ __forceinline__ void consumer_tile(const float* W, float* act, float*
             load(A, k + 2 < 134 ? k + 2 : 133);
             math(B);
         }
+        PT_END(1, t_l1);
+        PT_BEGIN(t_e1);
         bar_sync(BAR_CONS, kConsumers);  // all reads of act done
         const float* b = W + B1S + g * 26;
 #pragma unroll
@@ -153,6 +170,7 @@ __device__ __forceinline__ void consumer_tile(const float* W, float* act, float*
                 f2(sigmoidf_fast(acc0[p].y + b1), sigmoidf_fast(acc1[p].y + b1));
         }
         bar_sync(BAR_CONS, kConsumers);
+        PT_END(2, t_e1);
     }
     // ---- L2: 100 -> 50 (neurons 13g .. 13g+12), pairs along m ----------------
     {
@@ -179,6 +197,7 @@ __device__ __forceinline__ void consumer_tile(const float* W, float* act, float*
 #pragma unroll
             for (int t = 0; t < 13; ++t) acc[t] = ffma2(o.a, f2(w[t], w[t]), acc[t]);
         };
+        PT_BEGIN(t_l2);
         Op A, B;
         load(A, 0);
 #pragma unroll 1
@@ -188,6 +207,8 @@ __device__ __forceinline__ void consumer_tile(const float* W, float* act, float*
             load(A, k + 2 < 100 ? k + 2 : 99);
             math(B);
         }
+        PT_END(3, t_l2);
+        PT_BEGIN(t_e2);
         bar_sync(BAR_CONS, kConsumers);
         const float* b = W + B2S + g * 13;
 #pragma unroll
@@ -197,6 +218,7 @@ __device__ __forceinline__ void consumer_tile(const float* W, float* act, float*
                 f2(sigmoidf_fast(acc[t].x + bb), sigmoidf_fast(acc[t].y + bb));
         }
         bar_sync(BAR_CONS, kConsumers);
+        PT_END(4, t_e2);
     }
     // ---- L3: 50 -> 25 (neurons 7g .. 7g+6), pairs along m ---------------------
     {
@@ -219,6 +241,7 @@ __device__ __forceinline__ void consumer_tile(const float* W, float* act, float*
 #pragma unroll
             for (int t = 0; t < 7; ++t) acc[t] = ffma2(o.a, f2(w[t], w[t]), acc[t]);
         };
+        PT_BEGIN(t_l3);
         Op A, B;
         load(A, 0);
 #pragma unroll 1
@@ -228,6 +251,8 @@ __device__ __forceinline__ void consumer_tile(const float* W, float* act, float*
             load(A, k + 2 < 50 ? k + 2 : 49);
             math(B);
         }
+        PT_END(5, t_l3);
+        PT_BEGIN(t_e3);
         bar_sync(BAR_CONS, kConsumers);
         const float* b = W + B3S + g * 7;
 #pragma unroll
@@ -237,8 +262,10 @@ __device__ __forceinline__ void consumer_tile(const float* W, float* act, float*
                 f2(sigmoidf_fast(acc[t].x + bb), sigmoidf_fast(acc[t].y + bb));
         }
         bar_sync(BAR_CONS, kConsumers);
+        PT_END(6, t_e3);
     }
     // ---- L4: 25 -> 7 (neurons 2g, 2g+1), identity, de-standardise -------------
+    PT_BEGIN(t_l4);
     {
         float2 acc[2] = {f2(0.f, 0.f), f2(0.f, 0.f)};
         const float* wbase = W + W4S + g * 2;
@@ -260,6 +287,7 @@ __device__ __forceinline__ void consumer_tile(const float* W, float* act, float*
             }
         }
     }
+    PT_END(7, t_l4);
 }
 
 // predict_params clamp (mlp.cpp:390-399); returns the clamped flag.
@@ -284,30 +312,66 @@ __device__ __forceinline__ bool clamp_params(float p[7]) {
 // category count/total, correctly rounded in FP32 (equal to the reference's
 // double quotient rounded to float for totals < 2^24), FP64
 // division for larger totals, zeros for a zero total.
-__device__ __forceinline__ void produce_features(float* act, float* scr,
+//
+// Loading: a full, 16-byte-aligned tile is fetched with 134 asynchronous bulk
+// copies (cp.async.bulk -> UBLKCP, one 256-byte row segment each: 126 count
+// rows to act rows 8.., 8 DCGM rows to act rows 0..7) completing on an
+// mbarrier, issued BEFORE the producer sweeps the previous tile so the DRAM
+// latency hides behind the sweep.  Ragged/unaligned tiles load synchronously.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ bool issue_tile_loads(float* act, uint64_t* mbar,
                                                  const uint32_t* __restrict__ counts,
                                                  const float* __restrict__ dcgm, int64_t t0,
                                                  int64_t n, int64_t ld, bool vec_ok, int pt) {
+    if (!(vec_ok && t0 + TM <= n)) return false;
+    // act was last written through the generic proxy; order those writes before
+    // the async-proxy copies that overwrite it
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    const uint32_t bar = smem_u32(mbar);
+    if (pt == 0)
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                     "r"(134 * TM * 4)
+                     : "memory");
+    for (int row = pt; row < 134; row += kProducers) {
+        const void* src = row < 8 ? (const void*)(dcgm + (int64_t)row * ld + t0)
+                                  : (const void*)(counts + (int64_t)(row - 8) * ld + t0);
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                smem_u32(act + row * RS)),
+            "l"(src), "r"(TM * 4), "r"(bar)
+            : "memory");
+    }
+    return true;
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* mbar, uint32_t parity) {
+    const uint32_t bar = smem_u32(mbar);
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+            : "=r"(done)
+            : "r"(bar), "r"(parity)
+            : "memory");
+    }
+}
+
+__device__ __forceinline__ void produce_features(float* act, float* scr,
+                                                 const uint32_t* __restrict__ counts,
+                                                 const float* __restrict__ dcgm, int64_t t0,
+                                                 int64_t n, int64_t ld, bool issued,
+                                                 uint64_t* mbar, uint32_t& parity, int pt) {
     uint32_t* acti = reinterpret_cast<uint32_t*>(act);
     const int q = pt & 15;   // kernels 4q .. 4q+3
     const int rp = pt >> 4;  // row phase 0..7
-    // phase 1: all loads of the tile in flight
-    if (vec_ok && t0 + TM <= n) {
-        uint4 v[16];
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-            const int r = rp + 8 * j;
-            if (r < DSO_COUNT_ROWS)
-                v[j] = __ldg(reinterpret_cast<const uint4*>(counts + (int64_t)r * ld + t0) + q);
-        }
-        const float4 d = __ldg(reinterpret_cast<const float4*>(dcgm + (int64_t)rp * ld + t0) + q);
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-            const int r = rp + 8 * j;
-            if (r < DSO_COUNT_ROWS) reinterpret_cast<uint4*>(acti + (8 + r) * RS)[q] = v[j];
-        }
-        reinterpret_cast<float4*>(act + rp * RS)[q] = d;
+    if (issued) {
+        mbar_wait(mbar, parity);
+        parity ^= 1u;
     } else {
+        // synchronous path: ragged or unaligned tile
         const int m = pt & 63, h = pt >> 6;
         const int64_t k = t0 + m;
         const bool live = k < n;
@@ -516,6 +580,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             sm[STATS + threadIdx.x] = stats.mean[threadIdx.x];
             sm[STATS + 8 + threadIdx.x] = stats.std_[threadIdx.x];
         }
+        if (threadIdx.x == 0) {
+            uint64_t* mb = reinterpret_cast<uint64_t*>(sm + MBAR);
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(mb)));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(mb + 1)));
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
         if (PIPE) {
             float4* sc = reinterpret_cast<float4*>(sm + TABLES);
             float2* smm = reinterpret_cast<float2*>(sm + TABLES + 4 * J.nc);
@@ -532,7 +602,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ================================ consumer ================================
         for (int64_t i = 0; i < my_tiles; ++i) {
             const int s = (int)(i & 1);
+            PT_BEGIN(t_w);
             bar_sync(BAR_FULL0 + s, kThreads);  // features in act[s]; out[s] free
+            PT_END(0, t_w);
             consumer_tile(sm, sm + ACT + s * kActFloats, sm + OUT + s * kOutFloats, tid);
             bar_arrive(BAR_READY0 + s, kThreads);  // predictions in out[s]; act[s] free
         }
@@ -544,26 +616,40 @@ __global__ void __launch_bounds__(kThreads, 1)
             PIPE ? (((J.ld & 3) == 0) && ((reinterpret_cast<uintptr_t>(J.counts) & 15) == 0) &&
                     ((reinterpret_cast<uintptr_t>(J.dcgm) & 15) == 0))
                  : (((J.ld & 3) == 0) && ((reinterpret_cast<uintptr_t>(J.fused) & 15) == 0));
-        auto load_tile = [&](int64_t i) {
+        uint64_t* mbar = reinterpret_cast<uint64_t*>(sm + MBAR);
+        uint32_t par0 = 0u, par1 = 0u;  // mbarrier phase per buffer
+        auto t0_of = [&](int64_t i) { return (blockIdx.x + i * gridDim.x) * (int64_t)TM; };
+        auto issue = [&](int64_t i) -> bool {
+            if (!PIPE) return false;
             const int s = (int)(i & 1);
-            const int64_t t0 = (blockIdx.x + i * gridDim.x) * (int64_t)TM;
+            return issue_tile_loads(sm + ACT + s * kActFloats, mbar + s, J.counts, J.dcgm,
+                                    t0_of(i), J.n, J.ld, vec_ok, pt);
+        };
+        auto finish = [&](int64_t i, bool issued) {
+            const int s = (int)(i & 1);
             float* act = sm + ACT + s * kActFloats;
+            PT_BEGIN(t_f);
             if (PIPE)
-                produce_features(act, scr, J.counts, J.dcgm, t0, J.n, J.ld, vec_ok, pt);
+                produce_features(act, scr, J.counts, J.dcgm, t0_of(i), J.n, J.ld, issued,
+                                 mbar + s, s ? par1 : par0, pt);
             else
-                produce_fused(act, J.fused, t0, J.n, J.ld, vec_ok, pt);
+                produce_fused(act, J.fused, t0_of(i), J.n, J.ld, vec_ok, pt);
+            PT_END(10, t_f);
             bar_arrive(BAR_FULL0 + s, kThreads);
         };
-        if (my_tiles > 0) load_tile(0);
-        if (my_tiles > 1) load_tile(1);
+        for (int64_t i = 0; i < 2 && i < my_tiles; ++i) finish(i, issue(i));
         for (int64_t i = 0; i < my_tiles; ++i) {
             const int s = (int)(i & 1);
-            const int64_t t0 = (blockIdx.x + i * gridDim.x) * (int64_t)TM;
-            bar_sync(BAR_READY0 + s, kThreads);
-            produce_results<PIPE>(sm, sm + OUT + s * kOutFloats, J, t0, pt);
-            // out[s] fully read and act[s] free -> tile i+2 may be staged there
+            PT_BEGIN(t_w);
+            bar_sync(BAR_READY0 + s, kThreads);  // tile i predicted; act[s] free
+            PT_END(8, t_w);
+            const bool more = i + 2 < my_tiles;
+            const bool issued = more ? issue(i + 2) : false;  // loads fly during the sweep
+            PT_BEGIN(t_r);
+            produce_results<PIPE>(sm, sm + OUT + s * kOutFloats, J, t0_of(i), pt);
             bar_sync(BAR_PROD, kProducers);
-            if (i + 2 < my_tiles) load_tile(i + 2);
+            PT_END(9, t_r);
+            if (more) finish(i + 2, issued);
         }
     }
 }
@@ -630,6 +716,18 @@ cudaError_t launch_ws(Ctx& cx, const Job& J) {
 }  // namespace
 
 size_t mlp_smem_bytes() { return ws_smem_bytes(0, 0); }
+
+#ifdef DSO_PHASE_TIMING
+extern "C" int32_t dso_debug_phase_cycles(unsigned long long* out, int reset) {
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(out, g_phase_cycles, sizeof(unsigned long long) * 16);
+    if (reset) {
+        unsigned long long z[16] = {};
+        cudaMemcpyToSymbol(g_phase_cycles, z, sizeof z);
+    }
+    return 0;
+}
+#endif
 
 // Pack the reference-layout model (W_l row-major [out][in], concatenated, in
 // double) into the padded FP32 layout the kernels stage into shared memory.

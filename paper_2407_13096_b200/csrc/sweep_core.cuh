@@ -53,12 +53,60 @@ __device__ __forceinline__ void eval_pair(const KParams& p, float Pc, float Tb, 
     E = __fmul_rn(P, T);
 }
 
+// Two pairs (j, j+1) of one core level at once with packed FP32x2 ops; each
+// lane rounds exactly like eval_pair.
+__device__ __forceinline__ void eval_pair2(float Pc, float Tb, float t0, float2 G, float2 Ta,
+                                           float eta, float K, float2& C, float2& E) {
+    const float2 P = fadd2(make_float2(Pc, Pc), G);
+    const float2 T = fadd2(make_float2(t0, t0), make_float2(fmaxf(Ta.x, Tb), fmaxf(Ta.y, Tb)));
+    C = fmul2(ffma2(make_float2(eta, eta), P, make_float2(K, K)), T);
+    E = fmul2(P, T);
+}
+
 // Sweep core levels [i_lo, i_hi) (non-empty) x all memory levels.
 template <int NM>
 __device__ __forceinline__ Best sweep_levels(const KParams& p, const float4* __restrict__ s_core,
                                              const float2* __restrict__ s_mem, int nm_rt, int i_lo,
                                              int i_hi, float eta, float K) {
-    if constexpr (NM >= 2 && NM <= 4) {
+    if constexpr (NM == 2 || NM == 4) {
+        // memory levels in pairs: FADD2 / FMUL2 / FFMA2 evaluate two pairs per op
+        constexpr int NP = NM / 2;
+        float2 G[NP], Ta[NP];
+#pragma unroll
+        for (int h = 0; h < NP; ++h) {
+            G[h] = make_float2(__fmul_rn(p.g, s_mem[2 * h].x), __fmul_rn(p.g, s_mem[2 * h + 1].x));
+            Ta[h] = make_float2(__fmul_rn(p.a, s_mem[2 * h].y), __fmul_rn(p.a, s_mem[2 * h + 1].y));
+        }
+        Best ch[NM];
+        {
+            const float4 t = s_core[i_lo];
+            const float Pc = pc_f32(p.p0, p.kp, p.c, t);
+            const float Tb = __fmul_rn(p.b, t.z);
+#pragma unroll
+            for (int h = 0; h < NP; ++h) {
+                float2 C, E;
+                eval_pair2(Pc, Tb, p.t0, G[h], Ta[h], eta, K, C, E);
+                ch[2 * h] = Best{C.x, E.x, i_lo * NM + 2 * h};
+                ch[2 * h + 1] = Best{C.y, E.y, i_lo * NM + 2 * h + 1};
+            }
+        }
+#pragma unroll 2
+        for (int i = i_lo + 1; i < i_hi; ++i) {
+            const float4 t = s_core[i];
+            const float Pc = pc_f32(p.p0, p.kp, p.c, t);
+            const float Tb = __fmul_rn(p.b, t.z);
+#pragma unroll
+            for (int h = 0; h < NP; ++h) {
+                float2 C, E;
+                eval_pair2(Pc, Tb, p.t0, G[h], Ta[h], eta, K, C, E);
+                upd_best(ch[2 * h], C.x, E.x, i * NM + 2 * h);
+                upd_best(ch[2 * h + 1], C.y, E.y, i * NM + 2 * h + 1);
+            }
+        }
+#pragma unroll
+        for (int j = 1; j < NM; ++j) merge_best(ch[0], ch[j]);
+        return ch[0];
+    } else if constexpr (NM == 3) {
         float G[NM], Ta[NM];
 #pragma unroll
         for (int j = 0; j < NM; ++j) {

@@ -1,0 +1,45 @@
+"""Per-phase cycle breakdown of the warp-specialised kernel (debug library)."""
+import ctypes as C
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+os.environ["DSO_B200_LIB"] = os.path.join(ROOT, "paper_2407_13096_b200", "lib", "libdso_b200_phase.so")
+sys.path.insert(0, ROOT)
+import torch  # noqa: E402
+
+from paper_2407_13096_b200 import _lib, config_domain, init_mlp  # noqa: E402
+from paper_2407_13096_b200.api import Context  # noqa: E402
+
+L = _lib.lib()
+L.dso_debug_phase_cycles.argtypes = [C.c_void_p, C.c_int]
+names = ["c.wait_full", "c.L1", "c.L1_epi", "c.L2", "c.L2_epi", "c.L3", "c.L3_epi", "c.L4",
+         "p.wait_ready", "p.results", "p.features", "", "", "", "", ""]
+ctx = Context(0)
+n = 1 << 22
+for mode in ("pipeline", "predict"):
+    ctx.set_domain(config_domain("c3"))
+    import numpy as np
+    m = init_mlp(seed=424242)
+    m.target_mean = np.array([60, 10, 0.01, 0.004, 0.15, 200, 200.0])
+    m.target_std = np.array([15, 3, 0.005, 0.001, 0.07, 100, 100.0])
+    ctx.set_model(m)
+    g = ctx.gen_synthetic(n, root=3)
+    f = ctx.featurize(g["counts"], g["dcgm"])
+    buf = (C.c_ulonglong * 16)()
+    run = (lambda: ctx.pipeline(g["counts"], g["dcgm"], 0.8)) if mode == "pipeline" else \
+          (lambda: ctx.predict_params(f))
+    run()
+    L.dso_debug_phase_cycles(buf, 1)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    run()
+    e1.record()
+    torch.cuda.synchronize()
+    L.dso_debug_phase_cycles(buf, 1)
+    ms = e0.elapsed_time(e1)
+    tiles = n // 64
+    print(f"== {mode}: {ms:.3f} ms for {n} kernels; per tile (cycles, summed over 148 CTAs / tiles):")
+    for i, nm in enumerate(names):
+        if nm:
+            print(f"  {nm:14s} {buf[i] / tiles:10.0f}")
