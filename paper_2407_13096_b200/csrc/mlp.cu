@@ -5,14 +5,14 @@
 // de-standardised (forward_raw mlp.cpp:381-384) and clamped (predict_params
 // mlp.cpp:386-402, kBetaFloor mlp.cpp:15).
 //
-// Execution model — one persistent, warp-specialised CTA per SM (256 threads):
+// Execution model — one persistent, warp-specialised CTA per SM (384 threads):
 //   * 4 CONSUMER warps (one per SM sub-partition) run the MLP on a tile of 64
 //     kernels held k-major in shared memory (act[134][64]); each layer is a
 //     register-tiled FP32 GEMM on the FMA pipe with Blackwell's packed FFMA2
 //     (L1: thread = 2 kernels x 26 neurons, 26 FFMA2 per 8 shared loads;
 //     weights are warp-uniform broadcasts; operands of step k+1 in flight
 //     while step k issues); layer outputs overwrite act in place;
-//   * 4 PRODUCER warps, meanwhile, (a) finish the previous tile: clamp, then
+//   * 8 PRODUCER warps, meanwhile, (a) finish the previous tile: clamp, then
 //     P(f), T(f), the eta objective and the lexicographic argmin over the
 //     whole frequency grid, and (b) run the feature stage of the tile after
 //     next (raw PTX counts -> per-category fractions fused with DCGM) straight
@@ -42,7 +42,7 @@ constexpr int TM = 64;           // kernels per tile
 constexpr int RS = 64;           // act row stride (floats)
 constexpr int RS2 = RS / 2;
 constexpr int kConsumers = 128;  // 4 warps: one per SM sub-partition
-constexpr int kProducers = 128;  // 4 warps
+constexpr int kProducers = 256;  // 8 warps (two per SM sub-partition)
 constexpr int kThreads = kConsumers + kProducers;
 
 // Named barriers (0 is __syncthreads).
@@ -66,7 +66,7 @@ constexpr int kActFloats = 134 * RS;
 constexpr int OUT = ACT + 2 * kActFloats;   // out[2][8][RS]  (raw predictions)
 constexpr int kOutFloats = 8 * RS;
 constexpr int SCR = OUT + 2 * kOutFloats;   // producer scratch: tf[3][64] rr[3][64]
-constexpr int kScrFloats = 6 * TM + 2 * TM;  // + part u64[64]
+constexpr int kScrFloats = 6 * TM + 6 * TM;  // tf[3][64], rr[3][64] + part u64[3][64]
 constexpr int STATS = SCR + kScrFloats;     // mean[8] std[8]
 constexpr int MBAR = STATS + 16;            // 2 mbarriers (u64) for the bulk tile loads
 constexpr int TABLES = MBAR + 4;            // core4[nc], mem2[nm]
@@ -366,7 +366,7 @@ __device__ __forceinline__ void produce_features(float* act, float* scr,
                                                  uint64_t* mbar, uint32_t& parity, int pt) {
     uint32_t* acti = reinterpret_cast<uint32_t*>(act);
     const int q = pt & 15;   // kernels 4q .. 4q+3
-    const int rp = pt >> 4;  // row phase 0..7
+    const int rp = pt >> 4;  // row phase 0..15
     if (issued) {
         mbar_wait(mbar, parity);
         parity ^= 1u;
@@ -375,29 +375,31 @@ __device__ __forceinline__ void produce_features(float* act, float* scr,
         const int m = pt & 63, h = pt >> 6;
         const int64_t k = t0 + m;
         const bool live = k < n;
-#pragma unroll 9
-        for (int r = h; r < DSO_COUNT_ROWS; r += 2)
+#pragma unroll 8
+        for (int r = h; r < DSO_COUNT_ROWS; r += 4)
             acti[(8 + r) * RS + m] = live ? __ldg(counts + (int64_t)r * ld + k) : 0u;
 #pragma unroll
-        for (int r = h; r < 8; r += 2)
+        for (int r = h; r < 8; r += 4)
             act[r * RS + m] = live ? __ldg(dcgm + (int64_t)r * ld + k) : 0.f;
     }
     bar_sync(BAR_PROD, kProducers);
-    // phase 2: exact integer totals per (kernel, category)
+    // phase 2: exact integer totals per (kernel, category), 4 threads per kernel
     float* tfv = scr;                                            // [3][64]
     float* rrv = scr + 3 * TM;                                   // [3][64]
-    uint64_t* part = reinterpret_cast<uint64_t*>(scr + 6 * TM);  // [64]
-    constexpr int kSplit = 60;
-    const int m = pt & 63;
+    uint64_t* part = reinterpret_cast<uint64_t*>(scr + 6 * TM);  // [3][64]
+    const int m = pt & 63, qr = pt >> 6;
     uint64_t sa = 0, sb = 0, sc = 0;
-    if (pt < TM) {
-        for (int r = 0; r < kSplit; ++r) sa += acti[(8 + r) * RS + m];
+    if (qr < 3) {
+        const int lo = qr * 34, hi = qr == 2 ? DSO_INSTR_SLOTS : lo + 34;
+#pragma unroll 2
+        for (int r = lo; r < hi; ++r) sa += acti[(8 + r) * RS + m];
+        part[qr * TM + m] = sa;
     } else {
-        for (int r = kSplit; r < DSO_INSTR_SLOTS; ++r) sa += acti[(8 + r) * RS + m];
+#pragma unroll
         for (int r = 0; r < DSO_DTYPE_SLOTS; ++r) sb += acti[(8 + DSO_INSTR_SLOTS + r) * RS + m];
+#pragma unroll
         for (int r = 0; r < DSO_MEMSPACE_SLOTS; ++r)
             sc += acti[(8 + DSO_INSTR_SLOTS + DSO_DTYPE_SLOTS + r) * RS + m];
-        part[m] = sa;
     }
     bar_sync(BAR_PROD, kProducers);
     auto scale = [&](int cat, uint64_t tot) {
@@ -415,17 +417,17 @@ __device__ __forceinline__ void produce_features(float* act, float* scr,
         tfv[cat * TM + m] = tf;
         rrv[cat * TM + m] = rr;
     };
-    if (pt < TM) {
-        scale(0, sa + part[m]);
-    } else {
+    if (qr == 0) {
+        scale(0, part[m] + part[TM + m] + part[2 * TM + m]);
+    } else if (qr == 3) {
         scale(1, sb);
         scale(2, sc);
     }
     bar_sync(BAR_PROD, kProducers);
     // phase 3: normalise in place (each entry reads only itself and its totals)
-#pragma unroll 4
-    for (int j = 0; j < 16; ++j) {
-        const int r = rp + 8 * j;
+#pragma unroll 2
+    for (int j = 0; j < 8; ++j) {
+        const int r = rp + 16 * j;
         if (r >= DSO_COUNT_ROWS) break;
         const int cat = r < DSO_INSTR_SLOTS ? 0 : (r < DSO_INSTR_SLOTS + DSO_DTYPE_SLOTS ? 1 : 2);
         uint4* cp = reinterpret_cast<uint4*>(acti + (8 + r) * RS) + q;
@@ -458,18 +460,18 @@ __device__ __forceinline__ void produce_features(float* act, float* scr,
 __device__ __forceinline__ void produce_fused(float* act, const float* __restrict__ fused,
                                               int64_t t0, int64_t n, int64_t ld, bool vec_ok,
                                               int pt) {
-    const int q = pt & 15, rp = pt >> 4;
+    const int q = pt & 15, rp = pt >> 4;  // 16 row phases
     if (vec_ok && t0 + TM <= n) {
-        float4 v[17];
+        float4 v[9];
 #pragma unroll
-        for (int j = 0; j < 17; ++j) {
-            const int r = rp + 8 * j;
+        for (int j = 0; j < 9; ++j) {
+            const int r = rp + 16 * j;
             if (r < DSO_FUSED_ROWS)
                 v[j] = __ldg(reinterpret_cast<const float4*>(fused + (int64_t)r * ld + t0) + q);
         }
 #pragma unroll
-        for (int j = 0; j < 17; ++j) {
-            const int r = rp + 8 * j;
+        for (int j = 0; j < 9; ++j) {
+            const int r = rp + 16 * j;
             if (r < DSO_FUSED_ROWS) reinterpret_cast<float4*>(act + r * RS)[q] = v[j];
         }
     } else {
@@ -477,7 +479,7 @@ __device__ __forceinline__ void produce_fused(float* act, const float* __restric
         const int64_t k = t0 + m;
         const bool live = k < n;
 #pragma unroll 7
-        for (int r = h; r < DSO_FUSED_ROWS; r += 2)
+        for (int r = h; r < DSO_FUSED_ROWS; r += 4)
             act[r * RS + m] = live ? __ldg(fused + (int64_t)r * ld + k) : 0.f;
     }
 }
@@ -515,13 +517,13 @@ struct Job {
 template <bool PIPE>
 __device__ __forceinline__ void produce_results(const float* sm, const float* out, const Job& J,
                                                 int64_t t0, int pt) {
-    const int m = pt >> 1, half = pt & 1;
+    const int m = pt >> 2, qtr = pt & 3;  // 4 threads per kernel
     const int64_t k = t0 + m;
     float pr[7];
 #pragma unroll
     for (int i = 0; i < 7; ++i) pr[i] = out[i * RS + m];
     if (!PIPE) {
-        if (half == 0 && k < J.n) {
+        if (qtr == 0 && k < J.n) {
             if (J.raw)
 #pragma unroll
                 for (int i = 0; i < 7; ++i) J.raw[i * J.ld_out + k] = pr[i];
@@ -537,10 +539,11 @@ __device__ __forceinline__ void produce_results(const float* sm, const float* ou
     const float4* s_core = reinterpret_cast<const float4*>(sm + TABLES);
     const float2* s_mem = reinterpret_cast<const float2*>(sm + TABLES + 4 * J.nc);
     const int nc = J.nc, nm = J.nm;
-    const int i_split = (nc + 1) >> 1;
-    const int i_lo = half ? i_split : 0, i_hi = half ? nc : i_split;
+    // quarter qtr sweeps core levels [i_lo, i_hi): contiguous quarters in visit order
+    const int i_lo = (nc * qtr) >> 2, i_hi = (nc * (qtr + 1)) >> 2;
     Best b{__int_as_float(0x7fc00000), __int_as_float(0x7fc00000), i_lo * nm};
-    if (i_lo < i_hi) {
+    const bool empty = !(i_lo < i_hi);
+    if (!empty) {
         if (nm == 4)
             b = sweep_levels<4>(p, s_core, s_mem, 4, i_lo, i_hi, J.eta, J.K);
         else if (nm == 1)
@@ -550,12 +553,23 @@ __device__ __forceinline__ void produce_results(const float* sm, const float* ou
         else
             b = sweep_levels<0>(p, s_core, s_mem, nm, i_lo, i_hi, J.eta, J.K);
     }
-    Best o;
-    o.c = __shfl_xor_sync(0xffffffffu, b.c, 1);
-    o.e = __shfl_xor_sync(0xffffffffu, b.e, 1);
-    o.i = __shfl_xor_sync(0xffffffffu, b.i, 1);
-    if (half == 0 && k < J.n) {
-        if (i_split < nc) merge_best(b, o);  // the upper half holds the later pairs
+    // merge the quarters (merge_best is exact in any order: ties use the index)
+    bool emp = empty;
+#pragma unroll
+    for (int off = 1; off <= 2; off <<= 1) {
+        Best o;
+        o.c = __shfl_xor_sync(0xffffffffu, b.c, off);
+        o.e = __shfl_xor_sync(0xffffffffu, b.e, off);
+        o.i = __shfl_xor_sync(0xffffffffu, b.i, off);
+        const bool oemp = __shfl_xor_sync(0xffffffffu, (int)emp, off) != 0;
+        if (emp) {
+            if (!oemp) b = o;
+        } else if (!oemp) {
+            merge_best(b, o);
+        }
+        emp = emp && oemp;
+    }
+    if (qtr == 0 && k < J.n) {
         J.idx[k] = b.i;
         if (J.cost) J.cost[k] = b.c;
         if (J.energy) J.energy[k] = b.e;
