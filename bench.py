@@ -70,6 +70,9 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-stages", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=0)
+    ap.add_argument("--input", default="csr", choices=["csr", "dense"],
+                    help="PTX counts as sparse per-kernel lists (the reference's map shape) "
+                         "or dense [126][n] rows")
     return ap.parse_args()
 
 
@@ -246,8 +249,14 @@ def run_ours(args, rank, world, local_rank):
     if args.config == "c5":
         return run_train(args, rank, world, local_rank, ctx, dom, model, n)
     # inputs: this rank's shard [rank*n, (rank+1)*n) of the global synthetic stream
-    gen = ctx.gen_synthetic(n, root=ROOT_SEED, first=rank * n, params=(args.config == "c4"))
-    counts, dcgm = gen["counts"], gen["dcgm"]
+    csr = args.input == "csr" and args.config != "c4"
+    if csr:
+        gen = ctx.gen_synthetic_csr(n, root=ROOT_SEED, first=rank * n)
+        counts = None
+        dcgm = gen["dcgm"]
+    else:
+        gen = ctx.gen_synthetic(n, root=ROOT_SEED, first=rank * n, params=(args.config == "c4"))
+        counts, dcgm = gen["counts"], gen["dcgm"]
     etas = np.arange(101) / 100.0
     if args.config == "c4":
         params = gen["params"]
@@ -264,9 +273,12 @@ def run_ours(args, rank, world, local_rank):
         flops_per_step = n * dom.pairs * (9 + 3 * 101)  # P,T,E once + 3 per (pair, eta)
     else:
         out = ctx.alloc_pipeline_out(n)
-
-        def step():
-            ctx.pipeline(counts, dcgm, cfg["eta"], out=out)
+        if csr:
+            def step():
+                ctx.pipeline_csr(gen["row_ptr"], gen["entries"], dcgm, cfg["eta"], out=out)
+        else:
+            def step():
+                ctx.pipeline(counts, dcgm, cfg["eta"], out=out)
         units_per_step = n * dom.pairs
         flops_per_step = n * (MLP_FLOPS + PAIR_FLOPS * dom.pairs)
 
@@ -307,30 +319,52 @@ def run_ours(args, rank, world, local_rank):
     # ---- per-stage breakdown (same data, separate kernels) ---------------------------
     stages = None
     if not args.no_stages and args.config != "c4":
-        stages = stage_times(ctx, counts, dcgm, cfg, dom, n, stream)
+        dense = ctx.gen_synthetic(n, root=ROOT_SEED, first=rank * n, params=False)
+        stages = stage_times(ctx, dense["counts"], dense["dcgm"], cfg, dom, n, stream)
+        if csr:
+            a = torch.cuda.Event(enable_timing=True)
+            bb = torch.cuda.Event(enable_timing=True)
+            ctx.pipeline(dense["counts"], dense["dcgm"], cfg["eta"], out=out)
+            a.record(stream)
+            for _ in range(3):
+                ctx.pipeline(dense["counts"], dense["dcgm"], cfg["eta"], out=out)
+            bb.record(stream)
+            torch.cuda.synchronize()
+            stages["pipeline_dense_input_ms"] = a.elapsed_time(bb) / 3
+        del dense
 
     # ---- end to end through the C-ABI with pinned host buffers --------------------------
     e2e = None
     if not args.no_e2e and args.config != "c4":
-        hc = counts.cpu().pin_memory()
         hd = dcgm.cpu().pin_memory()
-        hout = ctx.alloc_pipeline_out(n, host=True, like=hc)
-        ctx.pipeline(hc, hd, cfg["eta"], out=hout)  # warm-up (staging buffers)
+        if csr:
+            hrp = gen["row_ptr"].cpu().pin_memory()
+            hent = gen["entries"].cpu().pin_memory()
+            h2d = (n + 1) * 8 + hent.numel() * 4 + n * 8 * 4
+            run_e2e = lambda o: ctx.pipeline_csr(hrp, hent, hd, cfg["eta"], out=o)  # noqa: E731
+        else:
+            hc = counts.cpu().pin_memory()
+            h2d = n * (126 * 4 + 8 * 4)
+            run_e2e = lambda o: ctx.pipeline(hc, hd, cfg["eta"], out=o)  # noqa: E731
+        hout = ctx.alloc_pipeline_out(n, host=True, like=hd)
+        run_e2e(hout)  # warm-up (staging buffers)
         k = max(1, min(args.steps, 5))
         barrier()
         t0 = time.perf_counter()
         for _ in range(k):
-            ctx.pipeline(hc, hd, cfg["eta"], out=hout)
+            run_e2e(hout)
         el = (time.perf_counter() - t0) / k
         te = torch.tensor([el], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         el = float(te.item())
         e2e = {"value": units_per_step * world / el, "unit": UNIT,
-               "h2d_bytes_per_step": int(n * (126 * 4 + 8 * 4)),
+               "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(n * 16), "ms_per_step": el * 1e3,
-               "steps": k, "timing": "host wall clock around synchronous C-ABI calls"}
-        del hc, hd, hout
+               "steps": k, "timing": "host wall clock around synchronous C-ABI calls "
+                                     "(dso_pipeline%s with DSO_HOST, pinned buffers)"
+                                     % ("_csr" if csr else "")}
+        del hd, hout
 
     if rank != 0:
         return
@@ -348,7 +382,8 @@ def run_ours(args, rank, world, local_rank):
         "peak_ffma_scalar": peak["ffma"],
         "nominal_peak": 148 * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12,
         "hbm_gbs_measured": peaks.get("hbm_gbs"),
-        "achieved_input_gbs": n * 536 / (ms * 1e-3) / 1e9 if args.config != "c4" else None,
+        "achieved_input_gbs": (n * (136 if csr else 536) / (ms * 1e-3) / 1e9
+                               if args.config != "c4" else None),
     }
     cpu = None
     if not args.no_cpu and world == 1:
@@ -361,6 +396,8 @@ def run_ours(args, rank, world, local_rank):
         "config": {"workload": cfg["desc"], "kernels_per_gpu": n, "grid": f"{cfg['nc']}x{cfg['nm']}",
                    "eta": cfg["eta"] if cfg["eta"] is not None else "0.00..1.00 (101)",
                    "parallelism": f"kernel-sharded x{world}, no collective",
+                   "input": ("sparse per-kernel PTX count lists (24 non-zeros/kernel) + DCGM"
+                             if csr else "dense [126][n] PTX counts + DCGM"),
                    "l2": "inputs > 126 MB L2 per step (no flush needed)"},
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
         "clocks": clk.summary(), "stages": stages,

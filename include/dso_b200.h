@@ -152,6 +152,18 @@ int32_t dso_pipeline(dso_ctx* ctx, const uint32_t* counts, const float* dcgm, in
                      int64_t ld, double eta, double pmax_w, float* params, uint8_t* clamped,
                      int32_t* idx, float* cost, float* energy, float* time, uint32_t flags);
 
+/* Same pipeline on SPARSE counts — the reference's own shape, one map of
+ * non-zero category counts per kernel (KernelInstructionCounts,
+ * ptx_features.hpp:31-37).  Kernel k's entries are
+ * entries[row_ptr[k] - ent_base .. row_ptr[k+1] - ent_base), each
+ * (count << 7) | slot with slot the count-row index (< 126, see counts above)
+ * and count < 2^25; slots listed twice are added.  dcgm is [8][ld].  With
+ * DSO_HOST, row_ptr/entries/dcgm/outputs are host memory (row_ptr[0..n]). */
+int32_t dso_pipeline_csr(dso_ctx* ctx, const uint64_t* row_ptr, const uint32_t* entries,
+                         uint64_t ent_base, const float* dcgm, int64_t n, int64_t ld,
+                         double eta, double pmax_w, float* params, uint8_t* clamped,
+                         int32_t* idx, float* cost, float* energy, float* time, uint32_t flags);
+
 /* ---- synthetic inputs (sim_harness.cpp:118-144 gen_kernel, on device) -------
  * Kernel k (0 <= k < n) is gen_kernel(Rng(root).fork(salt_base+first+k)
  * .next_u64()), as run_campaign seeds its corpus (sim_harness.cpp:241-242).
@@ -161,6 +173,12 @@ int32_t dso_pipeline(dso_ctx* ctx, const uint32_t* counts, const float* dcgm, in
 int32_t dso_gen_synthetic(dso_ctx* ctx, uint64_t root, uint64_t salt_base, int64_t first,
                           int64_t n, int64_t ld, float* params, uint32_t* counts,
                           float* dcgm);
+
+/* The synthetic stream in the sparse format: 24 entries per kernel (the slots
+ * features_from fills), row_ptr[k] = 24k for k <= n, dcgm [8][ld]. */
+int32_t dso_gen_synthetic_csr(dso_ctx* ctx, uint64_t root, uint64_t salt_base, int64_t first,
+                              int64_t n, uint64_t* row_ptr, uint32_t* entries, float* dcgm,
+                              int64_t ld);
 
 /* ---- predictor training (data-parallel) ------------------------------------
  * Mini-batch gradient of mse_loss (mlp.cpp:408-438) on the device model.

@@ -173,6 +173,19 @@ class Context:
             out["dcgm"] = d
         return out
 
+    def gen_synthetic_csr(self, n: int, root: int, salt_base: int = 0, first: int = 0,
+                          ld: int | None = None):
+        """The synthetic stream with sparse counts: row_ptr [n+1] int64 (24k),
+        entries [24n] int32 ((count << 7) | slot), dcgm [8, ld]."""
+        ld = n if ld is None else ld
+        rp = self._empty((n + 1,), torch.int64)
+        ent = self._empty((max(24 * n, 1),), torch.int32)
+        d = self._empty((8, ld), torch.float32)
+        self._raise(self._lib.dso_gen_synthetic_csr(self._h, C.c_uint64(root),
+                                                    C.c_uint64(salt_base), first, n, _ptr(rp),
+                                                    _ptr(ent), _ptr(d), ld))
+        return {"row_ptr": rp, "entries": ent, "dcgm": d}
+
     # -- feature stage ----------------------------------------------------------------
     def featurize(self, counts, dcgm, n: int | None = None, out=None):
         _check(counts, torch.int32, 126, "counts")
@@ -295,6 +308,29 @@ class Context:
             self._h, _ptr(counts), _ptr(dcgm), n, ld, eta, pmax, _ptr(out.get("params")),
             _ptr(out.get("clamped")), _ptr(out["idx"]), _ptr(out.get("cost")),
             _ptr(out.get("energy")), _ptr(out.get("time")), DSO_HOST if host else 0))
+        return out
+
+    def pipeline_csr(self, row_ptr, entries, dcgm, eta: float, pmax_w: float | None = None,
+                     n: int | None = None, ent_base: int = 0, want_params: bool = False,
+                     out: dict | None = None):
+        """Fused pipeline on sparse counts (dso_pipeline_csr): row_ptr [n+1] int64,
+        entries int32 ((count << 7) | slot), dcgm [8, ld] float32.  CUDA tensors run
+        on the device; CPU (pinned) tensors / numpy go through the chunked host path."""
+        pmax = self.domain.dev.pmax_w if pmax_w is None else pmax_w
+        host = not _is_cuda(row_ptr)
+        ld = dcgm.shape[1]
+        n = ld if n is None else n
+        if row_ptr.shape[0] < n + 1:
+            raise DsoError(ErrorKind.InvalidArgument, "row_ptr needs n + 1 entries")
+        if out is None:
+            out = self.alloc_pipeline_out(ld, host=host, want_params=want_params, like=dcgm)
+        if not host:
+            _check(dcgm, torch.float32, 8, "dcgm")
+        self._raise(self._lib.dso_pipeline_csr(
+            self._h, _ptr(row_ptr), _ptr(entries), C.c_uint64(ent_base), _ptr(dcgm), n, ld, eta,
+            pmax, _ptr(out.get("params")), _ptr(out.get("clamped")), _ptr(out["idx"]),
+            _ptr(out.get("cost")), _ptr(out.get("energy")), _ptr(out.get("time")),
+            DSO_HOST if host else 0))
         return out
 
     def alloc_pipeline_out(self, ld: int, host: bool = False, want_params: bool = False,

@@ -618,6 +618,131 @@ int32_t dso_pipeline(dso_ctx* ctx, const uint32_t* counts, const float* dcgm, in
     return kOk;
 }
 
+int32_t dso_gen_synthetic_csr(dso_ctx* ctx, uint64_t root, uint64_t salt_base, int64_t first,
+                              int64_t n, uint64_t* row_ptr, uint32_t* entries, float* dcgm,
+                              int64_t ld) {
+    int32_t st = check_ctx(ctx, false, false);
+    if (st) return st;
+    if ((st = check_batch(ctx, n, ld))) return st;
+    if (!row_ptr || (!entries && n)) return fail(ctx, kInvalidArgument, "row_ptr/entries required");
+    DSO_CUDA(ctx, launch_gen_csr(ctx->c, root, salt_base, first, n, row_ptr, entries, dcgm, ld));
+    return kOk;
+}
+
+int32_t dso_pipeline_csr(dso_ctx* ctx, const uint64_t* row_ptr, const uint32_t* entries,
+                         uint64_t ent_base, const float* dcgm, int64_t n, int64_t ld, double eta,
+                         double pmax, float* params, uint8_t* clamped, int32_t* idx, float* cost,
+                         float* energy, float* time, uint32_t flags) {
+    int32_t st = check_ctx(ctx, true, true);
+    if (st) return st;
+    if ((st = check_eta(ctx, eta))) return st;
+    if ((st = check_batch(ctx, n, ld))) return st;
+    if (!idx || !row_ptr || !dcgm) return fail(ctx, kInvalidArgument, "idx, row_ptr, dcgm required");
+    Ctx& c = ctx->c;
+    const float K = (float)((1.0 - eta) * pmax);
+    if (!(flags & DSO_HOST)) {
+        DSO_CUDA(ctx, launch_pipeline_csr(c, row_ptr, entries, ent_base, dcgm, n, ld, (float)eta,
+                                          K, params, clamped, idx, cost, energy, time, ld));
+        return kOk;
+    }
+    // ---- host buffers: chunked, double-buffered H2D / compute / D2H ----------------
+    const int64_t CH = std::min<int64_t>(n, (int64_t)1 << 21);
+    uint64_t max_ent = 0;
+    for (int64_t off = 0; off < n; off += CH) {
+        const int64_t m = std::min(CH, n - off);
+        max_ent = std::max<uint64_t>(max_ent, row_ptr[off + m] - row_ptr[off]);
+    }
+    const size_t in_b = (size_t)(CH + 1) * 8 + (size_t)max_ent * 4 + (size_t)CH * 8 * 4 + 64;
+    const size_t out_b = (size_t)CH * (4 + 4 + 4 + 4 + 7 * 4) + (size_t)CH + 64;
+    const size_t need = 2 * (in_b + out_b) + 512;
+    if (c.scratch_bytes < need) {
+        DSO_CUDA(ctx, cudaStreamSynchronize(c.stream));
+        cudaFree(c.scratch);
+        c.scratch = nullptr;
+        c.scratch_bytes = 0;
+        DSO_CUDA(ctx, cudaMalloc(&c.scratch, need));
+        c.scratch_bytes = need;
+    }
+    struct Buf {
+        uint64_t* rp;
+        uint32_t* ent;
+        float* dc;
+        int32_t* idx;
+        float *cost, *energy, *time, *params;
+        uint8_t* cl;
+    } buf[2];
+    auto align = [](char* p) { return (char*)(((uintptr_t)p + 15) & ~(uintptr_t)15); };
+    char* p = (char*)c.scratch;
+    for (int s = 0; s < 2; ++s) {
+        p = align(p);
+        buf[s].rp = (uint64_t*)p;
+        p = align(p + (size_t)(CH + 1) * 8);
+        buf[s].ent = (uint32_t*)p;
+        p = align(p + (size_t)max_ent * 4);
+        buf[s].dc = (float*)p;
+        p = align(p + (size_t)CH * 8 * 4);
+        buf[s].idx = (int32_t*)p;
+        p = align(p + (size_t)CH * 4);
+        buf[s].cost = (float*)p;
+        p = align(p + (size_t)CH * 4);
+        buf[s].energy = (float*)p;
+        p = align(p + (size_t)CH * 4);
+        buf[s].time = (float*)p;
+        p = align(p + (size_t)CH * 4);
+        buf[s].params = (float*)p;
+        p = align(p + (size_t)CH * 7 * 4);
+        buf[s].cl = (uint8_t*)p;
+        p += CH;
+    }
+    cudaStream_t h2d = c.aux[0], d2h = c.aux[1];
+    cudaEvent_t in_ready[2] = {c.ev[0], c.ev[1]};
+    cudaEvent_t done[2] = {c.ev[2], c.ev[3]};
+    cudaEvent_t drained[2] = {c.ev[4], c.ev[5]};
+    DSO_CUDA(ctx, cudaEventRecord(drained[0], c.stream));
+    DSO_CUDA(ctx, cudaEventRecord(drained[1], c.stream));
+    int64_t chunk_i = 0;
+    for (int64_t off = 0; off < n; off += CH, ++chunk_i) {
+        const int s = (int)(chunk_i & 1);
+        const int64_t m = std::min(CH, n - off);
+        Buf& B = buf[s];
+        const uint64_t e0 = row_ptr[off], e1 = row_ptr[off + m];
+        DSO_CUDA(ctx, cudaStreamWaitEvent(h2d, drained[s], 0));
+        DSO_CUDA(ctx, cudaMemcpyAsync(B.rp, row_ptr + off, (size_t)(m + 1) * 8,
+                                      cudaMemcpyHostToDevice, h2d));
+        if (e1 > e0)
+            DSO_CUDA(ctx, cudaMemcpyAsync(B.ent, entries + (e0 - ent_base), (size_t)(e1 - e0) * 4,
+                                          cudaMemcpyHostToDevice, h2d));
+        DSO_CUDA(ctx, cudaMemcpy2DAsync(B.dc, (size_t)CH * 4, dcgm + off, (size_t)ld * 4,
+                                        (size_t)m * 4, 8, cudaMemcpyHostToDevice, h2d));
+        DSO_CUDA(ctx, cudaEventRecord(in_ready[s], h2d));
+        DSO_CUDA(ctx, cudaStreamWaitEvent(c.stream, in_ready[s], 0));
+        DSO_CUDA(ctx, launch_pipeline_csr(c, B.rp, B.ent, e0, B.dc, m, CH, (float)eta, K,
+                                          params ? B.params : nullptr, clamped ? B.cl : nullptr,
+                                          B.idx, cost ? B.cost : nullptr,
+                                          energy ? B.energy : nullptr, time ? B.time : nullptr,
+                                          CH));
+        DSO_CUDA(ctx, cudaEventRecord(done[s], c.stream));
+        DSO_CUDA(ctx, cudaStreamWaitEvent(d2h, done[s], 0));
+        DSO_CUDA(ctx, cudaMemcpyAsync(idx + off, B.idx, 4 * m, cudaMemcpyDeviceToHost, d2h));
+        if (cost)
+            DSO_CUDA(ctx, cudaMemcpyAsync(cost + off, B.cost, 4 * m, cudaMemcpyDeviceToHost, d2h));
+        if (energy)
+            DSO_CUDA(ctx,
+                     cudaMemcpyAsync(energy + off, B.energy, 4 * m, cudaMemcpyDeviceToHost, d2h));
+        if (time)
+            DSO_CUDA(ctx, cudaMemcpyAsync(time + off, B.time, 4 * m, cudaMemcpyDeviceToHost, d2h));
+        if (params)
+            DSO_CUDA(ctx, cudaMemcpy2DAsync(params + off, (size_t)ld * 4, B.params,
+                                            (size_t)CH * 4, (size_t)m * 4, 7,
+                                            cudaMemcpyDeviceToHost, d2h));
+        if (clamped)
+            DSO_CUDA(ctx, cudaMemcpyAsync(clamped + off, B.cl, m, cudaMemcpyDeviceToHost, d2h));
+        DSO_CUDA(ctx, cudaEventRecord(drained[s], d2h));
+    }
+    DSO_CUDA(ctx, cudaStreamSynchronize(d2h));
+    return kOk;
+}
+
 int32_t dso_train_grad(dso_ctx* ctx, const float* x, const float* y, int64_t n, int64_t ld,
                        float* grad, double* loss_sum) {
     int32_t st = check_ctx(ctx, false, true);

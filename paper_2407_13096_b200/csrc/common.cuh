@@ -115,6 +115,12 @@ cudaError_t launch_pipeline(Ctx& c, const uint32_t* counts, const float* dcgm, i
                             int64_t ld, float eta, float K, float* params, uint8_t* clamped,
                             int32_t* idx, float* cost, float* energy, float* time,
                             int64_t ld_out);
+cudaError_t launch_pipeline_csr(Ctx& c, const uint64_t* row_ptr, const uint32_t* entries,
+                                uint64_t ent_base, const float* dcgm, int64_t n, int64_t ld,
+                                float eta, float K, float* params, uint8_t* clamped, int32_t* idx,
+                                float* cost, float* energy, float* time, int64_t ld_out);
+cudaError_t launch_gen_csr(Ctx& c, uint64_t root, uint64_t salt_base, int64_t first, int64_t n,
+                           uint64_t* row_ptr, uint32_t* entries, float* dcgm, int64_t ld);
 cudaError_t model_upload(Ctx& c, const double* W, const double* b);
 cudaError_t launch_train_grad(Ctx& c, const float* x, const float* y, int64_t n, int64_t ld,
                               float* grad, double* loss_sum_dev);

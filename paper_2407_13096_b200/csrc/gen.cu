@@ -143,7 +143,77 @@ __global__ void __launch_bounds__(256) gen_kernel_dev(uint64_t root, uint64_t sa
     }
 }
 
+// Sparse (CSR) variant: the same kernels as gen_kernel_dev, counts emitted as
+// the 24 slots features_from fills (sim_harness.cpp:70-95), in slot order, as
+// (count << 7) | slot; row_ptr[k] = 24 k (row_ptr[n] = 24 n).
+__global__ void __launch_bounds__(256) gen_csr_dev(uint64_t root, uint64_t salt_base,
+                                                   int64_t first, int64_t n,
+                                                   uint64_t* __restrict__ row_ptr,
+                                                   uint32_t* __restrict__ entries,
+                                                   float* __restrict__ dcgm, int64_t ld) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k <= n; k += stride) {
+        row_ptr[k] = 24u * (uint64_t)k;
+        if (k == n) continue;
+        DevRng r{root};
+        const uint64_t seed = r.fork(salt_base + (uint64_t)(first + k)).next();
+        DevRng rs{seed};
+        const double rho = rs.uniform01();
+        DevRng g = DevRng{seed}.fork(0x6e6b);
+        const double alpha = jittered(kAlpha, 1.0 - rho, g);
+        const double beta = jittered(kBeta, rho, g);
+        const double t0 = jittered(kT0, g.uniform01(), g);
+        const double gamma = jittered(kGamma, 1.0 - rho, g);
+        const double c = jittered(kC, rho, g);
+        const double p0 = jittered(kP0, g.uniform01(), g);
+        const double kappa = jittered(kKappa, g.uniform01(), g);
+        if (dcgm) {
+            const double za = encode(kAlpha, alpha), zb = encode(kBeta, beta),
+                         zt = encode(kT0, t0), zg = encode(kGamma, gamma), zc = encode(kC, c),
+                         zp = encode(kP0, p0), zk = encode(kKappa, kappa);
+            dcgm[k] = (float)(0.30 + 0.65 * zt);
+            dcgm[ld + k] = (float)(0.10 + 0.80 * zp);
+            dcgm[2 * ld + k] = (float)(0.02 + 0.60 * zg);
+            dcgm[3 * ld + k] = (float)(0.05 + 0.90 * za);
+            dcgm[4 * ld + k] = (float)(0.02 + 0.70 * zk);
+            dcgm[5 * ld + k] = (float)(0.05 + 0.90 * zb);
+            dcgm[6 * ld + k] = (float)(0.02 + 0.90 * zc);
+            dcgm[7 * ld + k] = (float)(0.05 + 0.45 * zb + 0.45 * zc);
+        }
+        const double s = beta / (alpha + beta);
+        const double arith = 0.70 * s;
+        const double mem = 0.70 * (1.0 - s);
+        const uint32_t cnt[24] = {
+            slot(0.35 * arith), slot(0.25 * arith), slot(0.40 * arith), slot(0.06),
+            slot(0.12),         slot(0.60 * mem),   slot(0.40 * mem),   slot(0.03),
+            slot(0.06),         slot(0.01),         slot(0.02),
+            slot(0.30 - 0.15 * s), slot(0.10), slot(0.07), slot(0.35 + 0.25 * s),
+            slot(0.08 - 0.05 * s), slot(0.05), slot(0.05 - 0.05 * s),
+            slot(0.20 + 0.15 * s), slot(0.05), slot(0.50 - 0.25 * s), slot(0.05), slot(0.08),
+            slot(0.12 + 0.10 * s)};
+        // slots in increasing order: add mul fma setp mov ld st cvt bra ret bar |
+        // .s32 .u32 .u64 .f32 .f64 .b32 .b64 | .reg .const .global .local .param .shared
+        const uint8_t sl[24] = {SL_ADD, SL_MUL, SL_FMA, SL_SETP, SL_MOV, SL_LD, SL_ST, SL_CVT,
+                                SL_BRA, SL_RET, SL_BAR,
+                                DT + 2, DT + 6, DT + 7, DT + 10, DT + 11, DT + 14, DT + 15,
+                                MS + 0, MS + 2, MS + 3, MS + 4, MS + 5, MS + 6};
+        uint32_t* e = entries + 24 * k;
+#pragma unroll
+        for (int i = 0; i < 24; ++i) e[i] = (cnt[i] << 7) | sl[i];
+    }
+}
+
 }  // namespace
+
+cudaError_t launch_gen_csr(Ctx& cx, uint64_t root, uint64_t salt_base, int64_t first, int64_t n,
+                           uint64_t* row_ptr, uint32_t* entries, float* dcgm, int64_t ld) {
+    if (n < 0) return cudaSuccess;
+    const int grid = grid_for(n + 1, 256, cx.num_sms, 16);
+    gen_csr_dev<<<grid, 256, 0, cx.stream>>>(root, salt_base, first, n, row_ptr, entries, dcgm,
+                                             ld);
+    ++cx.launches;
+    return cudaGetLastError();
+}
 
 cudaError_t launch_gen(Ctx& cx, uint64_t root, uint64_t salt_base, int64_t first, int64_t n,
                        int64_t ld, float* params, uint32_t* counts, float* dcgm) {

@@ -173,38 +173,46 @@ __device__ __forceinline__ void consumer_tile(const float* W, float* act, float*
         PT_END(2, t_e1);
     }
     // ---- L2: 100 -> 50 (neurons 13g .. 13g+12), pairs along m ----------------
+    // two k-steps per pipeline stage (26 FFMA2 per stage cover the load latency)
     {
         float2 acc[13];
 #pragma unroll
         for (int t = 0; t < 13; ++t) acc[t] = f2(0.f, 0.f);
         const float* wbase = W + W2S + g * 16;
         struct Op {
-            float2 a;
-            float4 v0, v1, v2;
-            float v3;
+            float2 a[2];
+            float4 v0[2], v1[2], v2[2];
+            float v3[2];
         };
         auto load = [&](Op& o, int k) {
-            const float* w = wbase + k * 64;
-            o.a = act2[k * RS2 + mp];
-            o.v0 = reinterpret_cast<const float4*>(w)[0];
-            o.v1 = reinterpret_cast<const float4*>(w)[1];
-            o.v2 = reinterpret_cast<const float4*>(w)[2];
-            o.v3 = w[12];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const float* w = wbase + (k + u) * 64;
+                o.a[u] = act2[(k + u) * RS2 + mp];
+                o.v0[u] = reinterpret_cast<const float4*>(w)[0];
+                o.v1[u] = reinterpret_cast<const float4*>(w)[1];
+                o.v2[u] = reinterpret_cast<const float4*>(w)[2];
+                o.v3[u] = w[12];
+            }
         };
         auto math = [&](const Op& o) {
-            const float w[13] = {o.v0.x, o.v0.y, o.v0.z, o.v0.w, o.v1.x, o.v1.y, o.v1.z,
-                                 o.v1.w, o.v2.x, o.v2.y, o.v2.z, o.v2.w, o.v3};
 #pragma unroll
-            for (int t = 0; t < 13; ++t) acc[t] = ffma2(o.a, f2(w[t], w[t]), acc[t]);
+            for (int u = 0; u < 2; ++u) {
+                const float w[13] = {o.v0[u].x, o.v0[u].y, o.v0[u].z, o.v0[u].w, o.v1[u].x,
+                                     o.v1[u].y, o.v1[u].z, o.v1[u].w, o.v2[u].x, o.v2[u].y,
+                                     o.v2[u].z, o.v2[u].w, o.v3[u]};
+#pragma unroll
+                for (int t = 0; t < 13; ++t) acc[t] = ffma2(o.a[u], f2(w[t], w[t]), acc[t]);
+            }
         };
         PT_BEGIN(t_l2);
         Op A, B;
         load(A, 0);
 #pragma unroll 1
-        for (int k = 0; k < 100; k += 2) {
-            load(B, k + 1);
+        for (int k = 0; k < 100; k += 4) {
+            load(B, k + 2);
             math(A);
-            load(A, k + 2 < 100 ? k + 2 : 99);
+            load(A, k + 4 < 100 ? k + 4 : 98);
             math(B);
         }
         PT_END(3, t_l2);
@@ -221,36 +229,45 @@ __device__ __forceinline__ void consumer_tile(const float* W, float* act, float*
         PT_END(4, t_e2);
     }
     // ---- L3: 50 -> 25 (neurons 7g .. 7g+6), pairs along m ---------------------
+    // two k-steps per stage; 50 = 12 double stages + 1 trailing pair
     {
         float2 acc[7];
 #pragma unroll
         for (int t = 0; t < 7; ++t) acc[t] = f2(0.f, 0.f);
         const float* wbase = W + W3S + g * 8;
         struct Op {
-            float2 a;
-            float4 v0, v1;
+            float2 a[2];
+            float4 v0[2], v1[2];
         };
         auto load = [&](Op& o, int k) {
-            const float* w = wbase + k * 32;
-            o.a = act2[k * RS2 + mp];
-            o.v0 = reinterpret_cast<const float4*>(w)[0];
-            o.v1 = reinterpret_cast<const float4*>(w)[1];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const float* w = wbase + (k + u) * 32;
+                o.a[u] = act2[(k + u) * RS2 + mp];
+                o.v0[u] = reinterpret_cast<const float4*>(w)[0];
+                o.v1[u] = reinterpret_cast<const float4*>(w)[1];
+            }
         };
         auto math = [&](const Op& o) {
-            const float w[7] = {o.v0.x, o.v0.y, o.v0.z, o.v0.w, o.v1.x, o.v1.y, o.v1.z};
 #pragma unroll
-            for (int t = 0; t < 7; ++t) acc[t] = ffma2(o.a, f2(w[t], w[t]), acc[t]);
+            for (int u = 0; u < 2; ++u) {
+                const float w[7] = {o.v0[u].x, o.v0[u].y, o.v0[u].z, o.v0[u].w,
+                                    o.v1[u].x, o.v1[u].y, o.v1[u].z};
+#pragma unroll
+                for (int t = 0; t < 7; ++t) acc[t] = ffma2(o.a[u], f2(w[t], w[t]), acc[t]);
+            }
         };
         PT_BEGIN(t_l3);
         Op A, B;
         load(A, 0);
 #pragma unroll 1
-        for (int k = 0; k < 50; k += 2) {
-            load(B, k + 1);
+        for (int k = 0; k < 48; k += 4) {
+            load(B, k + 2);
             math(A);
-            load(A, k + 2 < 50 ? k + 2 : 49);
+            load(A, k + 4);
             math(B);
         }
+        math(A);  // k = 48, 49
         PT_END(5, t_l3);
         PT_BEGIN(t_e3);
         bar_sync(BAR_CONS, kConsumers);
@@ -325,7 +342,8 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 __device__ __forceinline__ bool issue_tile_loads(float* act, uint64_t* mbar,
                                                  const uint32_t* __restrict__ counts,
                                                  const float* __restrict__ dcgm, int64_t t0,
-                                                 int64_t n, int64_t ld, bool vec_ok, int pt) {
+                                                 int64_t n, int64_t ld, bool vec_ok, int pt,
+                                                 int nrows = 134) {
     if (!(vec_ok && t0 + TM <= n)) return false;
     // act was last written through the generic proxy; order those writes before
     // the async-proxy copies that overwrite it
@@ -333,9 +351,9 @@ __device__ __forceinline__ bool issue_tile_loads(float* act, uint64_t* mbar,
     const uint32_t bar = smem_u32(mbar);
     if (pt == 0)
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
-                     "r"(134 * TM * 4)
+                     "r"(nrows * TM * 4)
                      : "memory");
-    for (int row = pt; row < 134; row += kProducers) {
+    for (int row = pt; row < nrows; row += kProducers) {
         const void* src = row < 8 ? (const void*)(dcgm + (int64_t)row * ld + t0)
                                   : (const void*)(counts + (int64_t)(row - 8) * ld + t0);
         asm volatile(
@@ -494,6 +512,9 @@ struct Job {
     const uint32_t* counts;
     const float* dcgm;
     const float* fused;
+    const uint64_t* row_ptr;  // CSR input: kernel k's entries are
+    const uint32_t* entries;  //   entries[row_ptr[k] - ent_base .. row_ptr[k+1] - ent_base)
+    uint64_t ent_base;
     int64_t n, ld;
     // sweep
     const float4* core4;
@@ -510,6 +531,167 @@ struct Job {
     float* time;
     int64_t ld_out;
 };
+
+// OR of a predicate over the producer warps (named-barrier reduction).
+__device__ __forceinline__ bool prod_any(bool v) {
+    uint32_t r;
+    asm volatile(
+        "{ .reg .pred p, q; setp.ne.u32 p, %1, 0; bar.red.or.pred q, %2, %3, p; selp.u32 %0, 1, 0, q; }"
+        : "=r"(r)
+        : "r"((uint32_t)v), "r"(BAR_PROD), "r"(kProducers)
+        : "memory");
+    return r != 0;
+}
+
+// ---------------------------------------------------------------------------
+// Producer, sparse input (the reference's own shape: one map of non-zero
+// category counts per kernel, ptx_features.hpp:31-37).  Entry = (count << 7) |
+// slot, slot = count-row index (< 126), count < 2^25; duplicate slots add.
+// 4 producer threads per kernel: the entries are prefetched into registers
+// before the producer sweeps the previous tile; afterwards the tile is
+// zero-filled, counts scattered with shared-memory atomics, category totals
+// reduced with shuffles, and only the listed entries are normalised.
+constexpr int kCsrRegs = 8;  // entries per thread held in registers (32 per kernel)
+
+struct CsrPrefetch {
+    uint32_t ent[kCsrRegs];
+    uint64_t first;  // index of this kernel's first entry
+    int cnt;         // number of entries of this kernel (0 for dead kernels)
+};
+
+__device__ __forceinline__ void csr_prefetch(const Job& J, int64_t t0, int pt, CsrPrefetch& P) {
+    const int m = pt >> 2, sub = pt & 3;
+    const int64_t k = t0 + m;
+    P.cnt = 0;
+    P.first = 0;
+    if (k < J.n) {
+        const uint64_t a = __ldg(J.row_ptr + k), b = __ldg(J.row_ptr + k + 1);
+        P.first = a - J.ent_base;
+        P.cnt = (int)(b - a);
+    }
+#pragma unroll
+    for (int e = 0; e < kCsrRegs; ++e) {
+        const int idx = sub + 4 * e;
+        P.ent[e] = idx < P.cnt ? __ldg(J.entries + P.first + idx) : 0u;
+    }
+}
+
+__device__ __forceinline__ int cat_of_row(int r) {
+    return r < DSO_INSTR_SLOTS ? 0 : (r < DSO_INSTR_SLOTS + DSO_DTYPE_SLOTS ? 1 : 2);
+}
+
+__device__ __forceinline__ float normalize_count(uint32_t c, float tf, float rr) {
+    if (tf > 0.f) {
+        const float cf = (__int_as_float(0x4B000000u | (c & 0x7FFFFFu)) - 8388608.f) +
+                         ((c & 0x800000u) ? 8388608.f : 0.f);
+        const float qq = __fmul_rn(cf, rr);
+        return fmaf(fmaf(-qq, tf, cf), rr, qq);
+    }
+    if (tf == 0.f) return 0.f;
+    return (float)((double)c / fma((double)-tf, 16777216.0, (double)rr));
+}
+
+__device__ __forceinline__ void csr_features(float* act, const Job& J, int64_t t0, int pt,
+                                             const CsrPrefetch& P, bool dcgm_issued,
+                                             uint64_t* mbar, uint32_t& parity) {
+    uint32_t* acti = reinterpret_cast<uint32_t*>(act);
+    const int m = pt >> 2, sub = pt & 3;
+    // zero-fill the count rows (8..133); DCGM rows arrive by bulk copy or here
+    {
+        float4* z = reinterpret_cast<float4*>(act + 8 * RS);
+        for (int i = pt; i < DSO_COUNT_ROWS * RS / 4; i += kProducers)
+            z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (!dcgm_issued) {
+            const int mm = pt & 63, h = pt >> 6;
+            const int64_t k = t0 + mm;
+            for (int r = h; r < 8; r += 4)
+                act[r * RS + mm] = k < J.n ? __ldg(J.dcgm + (int64_t)r * J.ld + k) : 0.f;
+        }
+    }
+    bar_sync(BAR_PROD, kProducers);
+    // pass 1: scatter-add counts, category totals
+    uint64_t tot[3] = {0, 0, 0};
+    auto scatter = [&](uint32_t e) {
+        const int slot = (int)(e & 127u);
+        const uint32_t c = e >> 7;
+        if (slot < DSO_COUNT_ROWS) {
+            atomicAdd(acti + (8 + slot) * RS + m, c);
+            const int cat = cat_of_row(slot);  // selects, not a dynamic index
+            tot[0] += cat == 0 ? c : 0u;
+            tot[1] += cat == 1 ? c : 0u;
+            tot[2] += cat == 2 ? c : 0u;
+        }
+    };
+#pragma unroll
+    for (int e = 0; e < kCsrRegs; ++e)
+        if (sub + 4 * e < P.cnt) scatter(P.ent[e]);
+    for (int idx = sub + 4 * kCsrRegs; idx < P.cnt; idx += 4) scatter(__ldg(J.entries + P.first + idx));
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        tot[c] += __shfl_xor_sync(0xffffffffu, tot[c], 1);
+        tot[c] += __shfl_xor_sync(0xffffffffu, tot[c], 2);
+    }
+    float tf[3], rr[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        tf[c] = 0.f;
+        rr[c] = 0.f;
+        if (tot[c] != 0 && tot[c] < (1u << 24)) {
+            tf[c] = __uint2float_rn((uint32_t)tot[c]);
+            rr[c] = __frcp_rn(tf[c]);
+        } else if (tot[c] != 0) {
+            tf[c] = -(float)(tot[c] >> 24);
+            rr[c] = (float)(tot[c] & 0xFFFFFFu);
+        }
+    }
+    if (dcgm_issued) {
+        mbar_wait(mbar, parity);
+        parity ^= 1u;
+    }
+    bar_sync(BAR_PROD, kProducers);
+    // pass 2: read the summed counts of this thread's slots, then overwrite them
+    // with the fractions (a slot listed twice gets the same value twice)
+    auto frac = [&](uint32_t e) -> float {
+        const int slot = (int)(e & 127u);
+        const int cat = cat_of_row(slot);
+        const uint32_t c = acti[(8 + slot) * RS + m];
+        return normalize_count(c, cat == 0 ? tf[0] : (cat == 1 ? tf[1] : tf[2]),
+                               cat == 0 ? rr[0] : (cat == 1 ? rr[1] : rr[2]));
+    };
+    float v[kCsrRegs];
+#pragma unroll
+    for (int e = 0; e < kCsrRegs; ++e)
+        v[e] = (sub + 4 * e < P.cnt && (P.ent[e] & 127u) < DSO_COUNT_ROWS) ? frac(P.ent[e]) : 0.f;
+    const bool spill = P.cnt > 4 * kCsrRegs;
+    bar_sync(BAR_PROD, kProducers);
+#pragma unroll
+    for (int e = 0; e < kCsrRegs; ++e)
+        if (sub + 4 * e < P.cnt && (P.ent[e] & 127u) < DSO_COUNT_ROWS)
+            act[(8 + (P.ent[e] & 127u)) * RS + m] = v[e];
+    if (prod_any(spill)) {
+        // more than 32 entries for some kernel: finish the tail in rounds of
+        // read (all threads) / barrier / write, so no slot is read after a write
+        for (int base = 4 * kCsrRegs; ; base += 4 * kCsrRegs) {
+            float w[kCsrRegs];
+            uint32_t ee[kCsrRegs];
+            bool any = false;
+#pragma unroll
+            for (int e = 0; e < kCsrRegs; ++e) {
+                const int idx = base + sub + 4 * e;
+                ee[e] = idx < P.cnt ? __ldg(J.entries + P.first + idx) : 0xFFFFFFFFu;
+                w[e] = (idx < P.cnt && (ee[e] & 127u) < DSO_COUNT_ROWS) ? frac(ee[e]) : 0.f;
+                any |= idx < P.cnt;
+            }
+            const bool more = prod_any(any);
+            if (!more) break;
+#pragma unroll
+            for (int e = 0; e < kCsrRegs; ++e)
+                if (ee[e] != 0xFFFFFFFFu && (ee[e] & 127u) < DSO_COUNT_ROWS)
+                    act[(8 + (ee[e] & 127u)) * RS + m] = w[e];
+            bar_sync(BAR_PROD, kProducers);
+        }
+    }
+}
 
 // Producer: finish a tile from its raw predictions in out: clamp and either
 // write the parameters (predict) or sweep the grid (pipeline).  2 threads per
@@ -581,9 +763,12 @@ __device__ __forceinline__ void produce_results(const float* sm, const float* ou
     }
 }
 
-template <bool PIPE>
+enum { MODE_PRED = 0, MODE_DENSE = 1, MODE_CSR = 2 };
+
+template <int MODE>
 __global__ void __launch_bounds__(kThreads, 1)
     ws_kernel(const float* __restrict__ packed, Stats stats, Job J) {
+    constexpr bool PIPE = MODE != MODE_PRED;
     extern __shared__ __align__(16) float sm[];
     // ---- stage model, stats, tables (all threads) -----------------------------
     {
@@ -626,26 +811,36 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ================================ producer ================================
         const int pt = tid - kConsumers;
         float* scr = sm + SCR;
+        const bool dcgm_ok = ((J.ld & 3) == 0) && ((reinterpret_cast<uintptr_t>(J.dcgm) & 15) == 0);
         const bool vec_ok =
-            PIPE ? (((J.ld & 3) == 0) && ((reinterpret_cast<uintptr_t>(J.counts) & 15) == 0) &&
-                    ((reinterpret_cast<uintptr_t>(J.dcgm) & 15) == 0))
-                 : (((J.ld & 3) == 0) && ((reinterpret_cast<uintptr_t>(J.fused) & 15) == 0));
+            MODE == MODE_DENSE ? (dcgm_ok && ((reinterpret_cast<uintptr_t>(J.counts) & 15) == 0))
+            : MODE == MODE_CSR ? dcgm_ok
+                               : (((J.ld & 3) == 0) && ((reinterpret_cast<uintptr_t>(J.fused) & 15) == 0));
         uint64_t* mbar = reinterpret_cast<uint64_t*>(sm + MBAR);
         uint32_t par0 = 0u, par1 = 0u;  // mbarrier phase per buffer
+        CsrPrefetch P;                  // CSR: entries of the tile being prefetched
         auto t0_of = [&](int64_t i) { return (blockIdx.x + i * gridDim.x) * (int64_t)TM; };
         auto issue = [&](int64_t i) -> bool {
-            if (!PIPE) return false;
             const int s = (int)(i & 1);
-            return issue_tile_loads(sm + ACT + s * kActFloats, mbar + s, J.counts, J.dcgm,
-                                    t0_of(i), J.n, J.ld, vec_ok, pt);
+            if (MODE == MODE_DENSE)
+                return issue_tile_loads(sm + ACT + s * kActFloats, mbar + s, J.counts, J.dcgm,
+                                        t0_of(i), J.n, J.ld, vec_ok, pt);
+            if (MODE == MODE_CSR) {
+                csr_prefetch(J, t0_of(i), pt, P);
+                return issue_tile_loads(sm + ACT + s * kActFloats, mbar + s, J.counts, J.dcgm,
+                                        t0_of(i), J.n, J.ld, vec_ok, pt, 8);
+            }
+            return false;
         };
         auto finish = [&](int64_t i, bool issued) {
             const int s = (int)(i & 1);
             float* act = sm + ACT + s * kActFloats;
             PT_BEGIN(t_f);
-            if (PIPE)
+            if (MODE == MODE_DENSE)
                 produce_features(act, scr, J.counts, J.dcgm, t0_of(i), J.n, J.ld, issued,
                                  mbar + s, s ? par1 : par0, pt);
+            else if (MODE == MODE_CSR)
+                csr_features(act, J, t0_of(i), pt, P, issued, mbar + s, s ? par1 : par0);
             else
                 produce_fused(act, J.fused, t0_of(i), J.n, J.ld, vec_ok, pt);
             PT_END(10, t_f);
@@ -708,13 +903,14 @@ Stats stats_of(const Ctx& cx) {
     return s;
 }
 
-template <bool PIPE>
+template <int MODE>
 cudaError_t launch_ws(Ctx& cx, const Job& J) {
+    constexpr bool PIPE = MODE != MODE_PRED;
     const size_t smem = ws_smem_bytes(PIPE ? J.nc : 0, PIPE ? J.nm : 0);
     if (smem > 227 * 1024) return cudaErrorInvalidValue;
     static bool attr = false;
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(ws_kernel<PIPE>,
+        cudaError_t e = cudaFuncSetAttribute(ws_kernel<MODE>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              227 * 1024);
         if (e != cudaSuccess) return e;
@@ -722,7 +918,7 @@ cudaError_t launch_ws(Ctx& cx, const Job& J) {
     }
     const int64_t tiles = (J.n + TM - 1) / TM;
     const int grid = (int)(tiles < cx.num_sms ? tiles : cx.num_sms);
-    ws_kernel<PIPE><<<grid, kThreads, smem, cx.stream>>>(cx.model.wt, stats_of(cx), J);
+    ws_kernel<MODE><<<grid, kThreads, smem, cx.stream>>>(cx.model.wt, stats_of(cx), J);
     ++cx.launches;
     return cudaGetLastError();
 }
@@ -790,7 +986,7 @@ cudaError_t launch_predict(Ctx& cx, const float* fused, int64_t n, int64_t ld, f
     J.clamped = clamped;
     J.raw = raw;
     J.ld_out = ld;
-    return launch_ws<false>(cx, J);
+    return launch_ws<MODE_PRED>(cx, J);
 }
 
 cudaError_t launch_pipeline(Ctx& cx, const uint32_t* counts, const float* dcgm, int64_t n,
@@ -816,7 +1012,35 @@ cudaError_t launch_pipeline(Ctx& cx, const uint32_t* counts, const float* dcgm, 
     J.energy = energy;
     J.time = time;
     J.ld_out = ld_out;
-    return launch_ws<true>(cx, J);
+    return launch_ws<MODE_DENSE>(cx, J);
+}
+
+cudaError_t launch_pipeline_csr(Ctx& cx, const uint64_t* row_ptr, const uint32_t* entries,
+                                uint64_t ent_base, const float* dcgm, int64_t n, int64_t ld,
+                                float eta, float K, float* params, uint8_t* clamped, int32_t* idx,
+                                float* cost, float* energy, float* time, int64_t ld_out) {
+    if (n <= 0) return cudaSuccess;
+    Job J{};
+    J.row_ptr = row_ptr;
+    J.entries = entries;
+    J.ent_base = ent_base;
+    J.dcgm = dcgm;
+    J.n = n;
+    J.ld = ld;
+    J.core4 = cx.dom.core4;
+    J.mem2 = cx.dom.mem2;
+    J.nc = cx.dom.nc;
+    J.nm = cx.dom.nm;
+    J.eta = eta;
+    J.K = K;
+    J.params = params;
+    J.clamped = clamped;
+    J.idx = idx;
+    J.cost = cost;
+    J.energy = energy;
+    J.time = time;
+    J.ld_out = ld_out;
+    return launch_ws<MODE_CSR>(cx, J);
 }
 
 }  // namespace dso_b200

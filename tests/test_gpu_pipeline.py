@@ -96,3 +96,101 @@ def test_pipeline_shards_equal_whole(ctx, port):
         r = ctx.pipeline(part["counts"], part["dcgm"], 0.8)
         np.testing.assert_array_equal(r["idx"].cpu().numpy(), whole["idx"].cpu().numpy()[a:b])
         np.testing.assert_array_equal(r["cost"].cpu().numpy(), whole["cost"].cpu().numpy()[a:b])
+
+
+# ---- sparse (CSR) input ---------------------------------------------------------------
+def csr_from_dense(counts, rng=None, dup=False):
+    """counts [n, 126] uint32 -> (row_ptr, entries) with entries (count << 7) | slot."""
+    rp, ent = [0], []
+    for k, row in enumerate(counts):
+        nz = np.flatnonzero(row)
+        items = [(int(row[s]) << 7) | int(s) for s in nz]
+        if dup and len(nz):  # split the first count over two entries (duplicates add)
+            s0 = int(nz[0])
+            c0 = int(row[s0])
+            items[0] = ((c0 // 2) << 7) | s0
+            items.append(((c0 - c0 // 2) << 7) | s0)
+        if rng is not None:
+            rng.shuffle(items)
+        ent.extend(items)
+        rp.append(len(ent))
+    return np.array(rp, np.int64), np.array(ent, np.uint32)
+
+
+def test_gen_csr_matches_dense(ctx):
+    n = 5000
+    d = ctx.gen_synthetic(n, root=41, params=False)
+    s = ctx.gen_synthetic_csr(n, root=41)
+    np.testing.assert_array_equal(s["dcgm"].cpu().numpy(), d["dcgm"].cpu().numpy())
+    rp = s["row_ptr"].cpu().numpy()
+    ent = s["entries"].cpu().numpy().view(np.uint32)
+    assert (rp == 24 * np.arange(n + 1)).all()
+    dense = np.zeros((n, 126), np.uint64)
+    for k in range(n):
+        for e in ent[rp[k]:rp[k + 1]]:
+            dense[k, e & 127] += e >> 7
+    np.testing.assert_array_equal(dense, d["counts"].cpu().numpy().T.view(np.uint32))
+
+
+@pytest.mark.parametrize("cfg", ["c1", "c2", "c3"])
+def test_pipeline_csr_equals_dense(ctx, port, cfg):
+    dom = config_domain(cfg)
+    ctx.set_domain(dom)
+    ctx.set_model(stats_model(port))
+    n = 20_000 + 37
+    d = ctx.gen_synthetic(n, root=43, params=False)
+    s = ctx.gen_synthetic_csr(n, root=43)
+    a = ctx.pipeline(d["counts"], d["dcgm"], 0.8, want_params=True)
+    b = ctx.pipeline_csr(s["row_ptr"], s["entries"], s["dcgm"], 0.8, want_params=True)
+    for f in ("idx", "cost", "energy", "time", "params", "clamped"):
+        np.testing.assert_array_equal(a[f].cpu().numpy(), b[f].cpu().numpy())
+
+
+def test_pipeline_csr_irregular(ctx, port):
+    """Random sparsity (0..126 non-zeros per kernel, > 32 exercises the spill
+    path), shuffled entry order, duplicate slots, empty kernels, ragged tail,
+    a non-zero ent_base — all equal to the dense pipeline bit for bit."""
+    dom = config_domain("c3")
+    ctx.set_domain(dom)
+    ctx.set_model(stats_model(port))
+    rng = np.random.default_rng(7)
+    n = 3000 + 13
+    counts = np.zeros((n, 126), np.uint32)
+    for k in range(n):
+        nnz = int(rng.integers(0, 127)) if k % 5 else int(rng.integers(0, 8))
+        slots = rng.choice(126, size=nnz, replace=False)
+        counts[k, slots] = rng.integers(1, 200_000, size=nnz)
+    counts[10] = 0
+    dcgm = rng.uniform(0, 1, size=(n, 8)).astype(np.float32)
+    rp, ent = csr_from_dense(counts, rng=rng, dup=True)
+    base = 1000
+    ent_pad = np.concatenate([np.zeros(base, np.uint32), ent])
+    rp_t = torch.from_numpy(rp + base).cuda()
+    ent_t = torch.from_numpy(ent.view(np.int32)).cuda()  # points at global index `base`
+    dc_t = torch.from_numpy(np.ascontiguousarray(dcgm.T)).cuda()
+    b = ctx.pipeline_csr(rp_t, ent_t, dc_t, 0.5, ent_base=base, want_params=True)
+    a = ctx.pipeline(torch.from_numpy(np.ascontiguousarray(counts.T).view(np.int32)).cuda(), dc_t,
+                     0.5, want_params=True)
+    for f in ("idx", "cost", "energy", "time", "params", "clamped"):
+        np.testing.assert_array_equal(a[f].cpu().numpy(), b[f].cpu().numpy())
+    # host buffers (chunked path) give the same answers
+    h = ctx.pipeline_csr(torch.from_numpy(rp).pin_memory(),
+                         torch.from_numpy(ent.view(np.int32)).pin_memory(),
+                         torch.from_numpy(np.ascontiguousarray(dcgm.T)).pin_memory(), 0.5,
+                         want_params=True)
+    for f in ("idx", "cost", "energy", "time", "params", "clamped"):
+        np.testing.assert_array_equal(h[f].numpy(), a[f].cpu().numpy())
+    del ent_pad
+
+
+def test_pipeline_csr_host_large(ctx, port):
+    dom = config_domain("c3")
+    ctx.set_domain(dom)
+    ctx.set_model(stats_model(port))
+    n = (1 << 21) + 4321  # more than one host chunk
+    s = ctx.gen_synthetic_csr(n, root=47)
+    dev_out = ctx.pipeline_csr(s["row_ptr"], s["entries"], s["dcgm"], 0.8, want_params=True)
+    host_out = ctx.pipeline_csr(s["row_ptr"].cpu().pin_memory(), s["entries"].cpu().pin_memory(),
+                                s["dcgm"].cpu().pin_memory(), 0.8, want_params=True)
+    for f in ("idx", "cost", "energy", "time", "params", "clamped"):
+        np.testing.assert_array_equal(host_out[f].numpy(), dev_out[f].cpu().numpy())
