@@ -591,8 +591,8 @@ __device__ __forceinline__ float normalize_count(uint32_t c, float tf, float rr)
     return (float)((double)c / fma((double)-tf, 16777216.0, (double)rr));
 }
 
-__device__ __forceinline__ void csr_features(float* act, const Job& J, int64_t t0, int pt,
-                                             const CsrPrefetch& P, bool dcgm_issued,
+__device__ __forceinline__ void csr_features(float* act, float* scr, const Job& J, int64_t t0,
+                                             int pt, const CsrPrefetch& P, bool dcgm_issued,
                                              uint64_t* mbar, uint32_t& parity) {
     uint32_t* acti = reinterpret_cast<uint32_t*>(act);
     const int m = pt >> 2, sub = pt & 3;
@@ -644,52 +644,58 @@ __device__ __forceinline__ void csr_features(float* act, const Job& J, int64_t t
             rr[c] = (float)(tot[c] & 0xFFFFFFu);
         }
     }
+    if (sub == 0) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            scr[c * TM + m] = tf[c];
+            scr[3 * TM + c * TM + m] = rr[c];
+        }
+    }
+    // (a barrier: every atomic and scale is in place)
+    const bool any_spill = prod_any(P.cnt > 4 * kCsrRegs);
+    if (!any_spill) {
+        // pass 2 (common case): read the summed counts of this thread's slots, then
+        // overwrite them with the fractions (a slot listed twice gets the same
+        // value twice); zero slots keep their zero fill
+        float v[kCsrRegs];
+#pragma unroll
+        for (int e = 0; e < kCsrRegs; ++e) {
+            v[e] = 0.f;
+            const int slot = (int)(P.ent[e] & 127u);
+            if (sub + 4 * e < P.cnt && slot < DSO_COUNT_ROWS) {
+                const int cat = cat_of_row(slot);
+                const uint32_t c = acti[(8 + slot) * RS + m];
+                v[e] = normalize_count(c, cat == 0 ? tf[0] : (cat == 1 ? tf[1] : tf[2]),
+                                       cat == 0 ? rr[0] : (cat == 1 ? rr[1] : rr[2]));
+            }
+        }
+        bar_sync(BAR_PROD, kProducers);
+#pragma unroll
+        for (int e = 0; e < kCsrRegs; ++e) {
+            const int slot = (int)(P.ent[e] & 127u);
+            if (sub + 4 * e < P.cnt && slot < DSO_COUNT_ROWS) act[(8 + slot) * RS + m] = v[e];
+        }
+    } else {
+        // some kernel has more than 32 entries: normalise the whole dense tile
+        // (every element read and written by the same thread, so no hazards)
+        const int q = pt & 15, rp = pt >> 4;
+#pragma unroll 2
+        for (int j = 0; j < 8; ++j) {
+            const int r = rp + 16 * j;
+            if (r >= DSO_COUNT_ROWS) break;
+            const int cat = cat_of_row(r);
+            uint4* cp = reinterpret_cast<uint4*>(acti + (8 + r) * RS) + q;
+            const uint4 c = *cp;
+            const float4 t4 = reinterpret_cast<const float4*>(scr + cat * TM)[q];
+            const float4 r4 = reinterpret_cast<const float4*>(scr + 3 * TM + cat * TM)[q];
+            *reinterpret_cast<float4*>(cp) =
+                make_float4(normalize_count(c.x, t4.x, r4.x), normalize_count(c.y, t4.y, r4.y),
+                            normalize_count(c.z, t4.z, r4.z), normalize_count(c.w, t4.w, r4.w));
+        }
+    }
     if (dcgm_issued) {
         mbar_wait(mbar, parity);
         parity ^= 1u;
-    }
-    bar_sync(BAR_PROD, kProducers);
-    // pass 2: read the summed counts of this thread's slots, then overwrite them
-    // with the fractions (a slot listed twice gets the same value twice)
-    auto frac = [&](uint32_t e) -> float {
-        const int slot = (int)(e & 127u);
-        const int cat = cat_of_row(slot);
-        const uint32_t c = acti[(8 + slot) * RS + m];
-        return normalize_count(c, cat == 0 ? tf[0] : (cat == 1 ? tf[1] : tf[2]),
-                               cat == 0 ? rr[0] : (cat == 1 ? rr[1] : rr[2]));
-    };
-    float v[kCsrRegs];
-#pragma unroll
-    for (int e = 0; e < kCsrRegs; ++e)
-        v[e] = (sub + 4 * e < P.cnt && (P.ent[e] & 127u) < DSO_COUNT_ROWS) ? frac(P.ent[e]) : 0.f;
-    const bool spill = P.cnt > 4 * kCsrRegs;
-    bar_sync(BAR_PROD, kProducers);
-#pragma unroll
-    for (int e = 0; e < kCsrRegs; ++e)
-        if (sub + 4 * e < P.cnt && (P.ent[e] & 127u) < DSO_COUNT_ROWS)
-            act[(8 + (P.ent[e] & 127u)) * RS + m] = v[e];
-    if (prod_any(spill)) {
-        // more than 32 entries for some kernel: finish the tail in rounds of
-        // read (all threads) / barrier / write, so no slot is read after a write
-        for (int base = 4 * kCsrRegs; ; base += 4 * kCsrRegs) {
-            float w[kCsrRegs];
-            uint32_t ee[kCsrRegs];
-            bool any = false;
-#pragma unroll
-            for (int e = 0; e < kCsrRegs; ++e) {
-                const int idx = base + sub + 4 * e;
-                ee[e] = idx < P.cnt ? __ldg(J.entries + P.first + idx) : 0xFFFFFFFFu;
-                w[e] = (idx < P.cnt && (ee[e] & 127u) < DSO_COUNT_ROWS) ? frac(ee[e]) : 0.f;
-                any |= idx < P.cnt;
-            }
-            const bool more = prod_any(any);
-            if (!more) break;
-#pragma unroll
-            for (int e = 0; e < kCsrRegs; ++e)
-                if (ee[e] != 0xFFFFFFFFu && (ee[e] & 127u) < DSO_COUNT_ROWS)
-                    act[(8 + (ee[e] & 127u)) * RS + m] = w[e];
-            bar_sync(BAR_PROD, kProducers);
-        }
     }
 }
 
@@ -840,7 +846,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 produce_features(act, scr, J.counts, J.dcgm, t0_of(i), J.n, J.ld, issued,
                                  mbar + s, s ? par1 : par0, pt);
             else if (MODE == MODE_CSR)
-                csr_features(act, J, t0_of(i), pt, P, issued, mbar + s, s ? par1 : par0);
+                csr_features(act, scr, J, t0_of(i), pt, P, issued, mbar + s, s ? par1 : par0);
             else
                 produce_fused(act, J.fused, t0_of(i), J.n, J.ld, vec_ok, pt);
             PT_END(10, t_f);
