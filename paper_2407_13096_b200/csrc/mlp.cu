@@ -6,20 +6,21 @@
 // mlp.cpp:386-402, kBetaFloor mlp.cpp:15).
 //
 // Execution model — one persistent, warp-specialised CTA per SM (384 threads):
-//   * 4 CONSUMER warps (one per SM sub-partition) run the MLP on a tile of 64
-//     kernels held k-major in shared memory (act[134][64]); each layer is a
+//   * two CONSUMER groups of 4 warps (one warp per SM sub-partition each) run
+//     the MLP on alternate tiles of 64 kernels held k-major in shared memory
+//     (act[134][64]); each layer is a
 //     register-tiled FP32 GEMM on the FMA pipe with Blackwell's packed FFMA2
 //     (L1: thread = 2 kernels x 26 neurons, 26 FFMA2 per 8 shared loads;
 //     weights are warp-uniform broadcasts; operands of step k+1 in flight
 //     while step k issues); layer outputs overwrite act in place;
-//   * 8 PRODUCER warps, meanwhile, (a) finish the previous tile: clamp, then
+//   * 4 PRODUCER warps, meanwhile, (a) finish the oldest tile: clamp, then
 //     P(f), T(f), the eta objective and the lexicographic argmin over the
-//     whole frequency grid, and (b) run the feature stage of the tile after
-//     next (raw PTX counts -> per-category fractions fused with DCGM) straight
-//     into the free activation buffer;
-//   * two activation/output buffers ping-pong between the roles through named
-//     barriers FULL[s] (producer -> consumer: features in act[s], out[s] free)
-//     and READY[s] (consumer -> producer: predictions in out[s], act[s] free).
+//     whole frequency grid, and (b) run the feature stage of a tile three ahead
+//     (raw PTX counts, dense or sparse -> per-category fractions fused with
+//     DCGM) straight into the buffer it frees;
+//   * three activation/output buffers rotate between the roles through named
+//     barriers FULL[b] (producer -> consumer: features in act[b], out[b] free)
+//     and READY[b] (consumer -> producer: predictions in out[b], act[b] free).
 // The MLP (FMA pipe) and the feature/sweep work (LSU/ALU + a little FMA) thus
 // overlap on every SM scheduler.  The model (weights ~100 KB) is staged once per
 // CTA; nothing between a kernel's 536 input bytes and its 16 result bytes
@@ -41,12 +42,18 @@ namespace {
 constexpr int TM = 64;           // kernels per tile
 constexpr int RS = 64;           // act row stride (floats)
 constexpr int RS2 = RS / 2;
-constexpr int kConsumers = 128;  // 4 warps: one per SM sub-partition
-constexpr int kProducers = 256;  // 8 warps (two per SM sub-partition)
-constexpr int kThreads = kConsumers + kProducers;
+constexpr int kGroupThreads = 128;  // one consumer group: 4 warps, one per SM sub-partition
+constexpr int kGroups = 2;          // two groups -> two consumer warps per scheduler
+constexpr int kConsumers = kGroups * kGroupThreads;
+constexpr int kProducers = 128;     // 4 warps
+constexpr int kThreads = kConsumers + kProducers;  // 384
+constexpr int TPK = kProducers / TM;               // producer threads per kernel (2)
+constexpr int kBufs = 3;                           // activation/output buffers
+constexpr int kHandoff = kProducers + kGroupThreads;  // threads on a FULL/READY barrier
+static_assert(kProducers == 128 && TPK == 2, "producer code is written for 4 warps");
 
 // Named barriers (0 is __syncthreads).
-constexpr int BAR_CONS = 1, BAR_PROD = 2, BAR_FULL0 = 3, BAR_READY0 = 5;
+constexpr int BAR_PROD = 1, BAR_CONS0 = 2, BAR_FULL0 = 4, BAR_READY0 = 7;
 
 // Packed model (floats), k-major, one neuron group per consumer warp g (0..3):
 //   L1 [134][4][28] (26 used, n = 26g + t)   L2 [100][4][16] (13 used, n = 13g + t)
@@ -61,15 +68,15 @@ constexpr int B3S = B2S + 52;            // [28]
 constexpr int B4S = B3S + 28;            // [8]
 constexpr int kModelFloats = B4S + 8;    // 23400
 // per-CTA shared memory beyond the model
-constexpr int ACT = kModelFloats;           // act[2][134][RS]
+constexpr int ACT = kModelFloats;           // act[3][134][RS]
 constexpr int kActFloats = 134 * RS;
-constexpr int OUT = ACT + 2 * kActFloats;   // out[2][8][RS]  (raw predictions)
+constexpr int OUT = ACT + kBufs * kActFloats;  // out[3][8][RS]  (raw predictions)
 constexpr int kOutFloats = 8 * RS;
-constexpr int SCR = OUT + 2 * kOutFloats;   // producer scratch: tf[3][64] rr[3][64]
+constexpr int SCR = OUT + kBufs * kOutFloats;   // producer scratch: tf[3][64] rr[3][64]
 constexpr int kScrFloats = 6 * TM + 6 * TM;  // tf[3][64], rr[3][64] + part u64[3][64]
 constexpr int STATS = SCR + kScrFloats;     // mean[8] std[8]
-constexpr int MBAR = STATS + 16;            // 2 mbarriers (u64) for the bulk tile loads
-constexpr int TABLES = MBAR + 4;            // core4[nc], mem2[nm]
+constexpr int MBAR = STATS + 16;            // 3 mbarriers (u64) for the bulk tile loads
+constexpr int TABLES = MBAR + 8;            // core4[nc], mem2[nm]
 static_assert(W2S % 4 == 0 && W3S % 4 == 0 && W4S % 4 == 0 && B1S % 4 == 0 &&
                   kModelFloats % 4 == 0 && ACT % 4 == 0 && OUT % 4 == 0 && SCR % 4 == 0 &&
                   MBAR % 2 == 0 && TABLES % 4 == 0,
@@ -86,9 +93,10 @@ __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b
 #ifdef DSO_PHASE_TIMING
 __device__ unsigned long long g_phase_cycles[16];
 #define PT_BEGIN(v) long long v = clock64()
-#define PT_END(ph, v)                                                                   \
-    do {                                                                               \
-        if ((threadIdx.x & 127) == 0) atomicAdd(&g_phase_cycles[ph], clock64() - (v)); \
+#define PT_END(ph, v)                                                                  \
+    do {                                                                              \
+        if (threadIdx.x == 0 || threadIdx.x == kProducers)                            \
+            atomicAdd(&g_phase_cycles[ph], clock64() - (v));                          \
     } while (0)
 #else
 #define PT_BEGIN(v) (void)0
@@ -111,7 +119,8 @@ __device__ __forceinline__ void bar_arrive(int id, int count) {
 // FMA pipe, so latency is covered by ILP (26 independent accumulator pairs in
 // L1), not by other warps.  Weights are warp-uniform -> shared-memory
 // broadcasts; an activation pair load is 256 contiguous bytes per warp.
-__device__ __forceinline__ void consumer_tile(const float* W, float* act, float* out, int ct) {
+__device__ __forceinline__ void consumer_tile(const float* W, float* act, float* out, int ct,
+                                              int cbar) {
     float2* act2 = reinterpret_cast<float2*>(act);  // [row][32] kernel pairs
     const int mp = ct & 31;
     const int g = ct >> 5;
@@ -159,7 +168,7 @@ __device__ __forceinline__ void consumer_tile(const float* W, float* act, float*
         }
         PT_END(1, t_l1);
         PT_BEGIN(t_e1);
-        bar_sync(BAR_CONS, kConsumers);  // all reads of act done
+        bar_sync(cbar, kGroupThreads);  // all reads of act done
         const float* b = W + B1S + g * 26;
 #pragma unroll
         for (int p = 0; p < 13; ++p) {
@@ -169,7 +178,7 @@ __device__ __forceinline__ void consumer_tile(const float* W, float* act, float*
             act2[(n + 1) * RS2 + mp] =
                 f2(sigmoidf_fast(acc0[p].y + b1), sigmoidf_fast(acc1[p].y + b1));
         }
-        bar_sync(BAR_CONS, kConsumers);
+        bar_sync(cbar, kGroupThreads);
         PT_END(2, t_e1);
     }
     // ---- L2: 100 -> 50 (neurons 13g .. 13g+12), pairs along m ----------------
@@ -217,7 +226,7 @@ __device__ __forceinline__ void consumer_tile(const float* W, float* act, float*
         }
         PT_END(3, t_l2);
         PT_BEGIN(t_e2);
-        bar_sync(BAR_CONS, kConsumers);
+        bar_sync(cbar, kGroupThreads);
         const float* b = W + B2S + g * 13;
 #pragma unroll
         for (int t = 0; t < 13; ++t) {
@@ -225,7 +234,7 @@ __device__ __forceinline__ void consumer_tile(const float* W, float* act, float*
             act2[(g * 13 + t) * RS2 + mp] =
                 f2(sigmoidf_fast(acc[t].x + bb), sigmoidf_fast(acc[t].y + bb));
         }
-        bar_sync(BAR_CONS, kConsumers);
+        bar_sync(cbar, kGroupThreads);
         PT_END(4, t_e2);
     }
     // ---- L3: 50 -> 25 (neurons 7g .. 7g+6), pairs along m ---------------------
@@ -270,7 +279,7 @@ __device__ __forceinline__ void consumer_tile(const float* W, float* act, float*
         math(A);  // k = 48, 49
         PT_END(5, t_l3);
         PT_BEGIN(t_e3);
-        bar_sync(BAR_CONS, kConsumers);
+        bar_sync(cbar, kGroupThreads);
         const float* b = W + B3S + g * 7;
 #pragma unroll
         for (int t = 0; t < 7; ++t) {
@@ -278,7 +287,7 @@ __device__ __forceinline__ void consumer_tile(const float* W, float* act, float*
             act2[(g * 7 + t) * RS2 + mp] =
                 f2(sigmoidf_fast(acc[t].x + bb), sigmoidf_fast(acc[t].y + bb));
         }
-        bar_sync(BAR_CONS, kConsumers);
+        bar_sync(cbar, kGroupThreads);
         PT_END(6, t_e3);
     }
     // ---- L4: 25 -> 7 (neurons 2g, 2g+1), identity, de-standardise -------------
@@ -377,47 +386,62 @@ __device__ __forceinline__ void mbar_wait(uint64_t* mbar, uint32_t parity) {
     }
 }
 
+// count / total, correctly rounded (Markstein), totals >= 2^24 in FP64
+__device__ __forceinline__ float normalize_count(uint32_t c, float tf, float rr) {
+    if (tf > 0.f) {
+        const float cf = (__int_as_float(0x4B000000u | (c & 0x7FFFFFu)) - 8388608.f) +
+                         ((c & 0x800000u) ? 8388608.f : 0.f);
+        const float qq = __fmul_rn(cf, rr);
+        return fmaf(fmaf(-qq, tf, cf), rr, qq);
+    }
+    if (tf == 0.f) return 0.f;
+    return (float)((double)c / fma((double)-tf, 16777216.0, (double)rr));
+}
+
 __device__ __forceinline__ void produce_features(float* act, float* scr,
                                                  const uint32_t* __restrict__ counts,
                                                  const float* __restrict__ dcgm, int64_t t0,
                                                  int64_t n, int64_t ld, bool issued,
-                                                 uint64_t* mbar, uint32_t& parity, int pt) {
+                                                 uint64_t* mbar, uint32_t& parbits, int bit,
+                                                 int pt) {
     uint32_t* acti = reinterpret_cast<uint32_t*>(act);
     const int q = pt & 15;   // kernels 4q .. 4q+3
-    const int rp = pt >> 4;  // row phase 0..15
+    const int rp = pt >> 4;  // row phase 0..7
     if (issued) {
-        mbar_wait(mbar, parity);
-        parity ^= 1u;
+        mbar_wait(mbar, (parbits >> bit) & 1u);
+        parbits ^= 1u << bit;
     } else {
         // synchronous path: ragged or unaligned tile
         const int m = pt & 63, h = pt >> 6;
         const int64_t k = t0 + m;
         const bool live = k < n;
-#pragma unroll 8
-        for (int r = h; r < DSO_COUNT_ROWS; r += 4)
+#pragma unroll 9
+        for (int r = h; r < DSO_COUNT_ROWS; r += 2)
             acti[(8 + r) * RS + m] = live ? __ldg(counts + (int64_t)r * ld + k) : 0u;
 #pragma unroll
-        for (int r = h; r < 8; r += 4)
+        for (int r = h; r < 8; r += 2)
             act[r * RS + m] = live ? __ldg(dcgm + (int64_t)r * ld + k) : 0.f;
     }
     bar_sync(BAR_PROD, kProducers);
-    // phase 2: exact integer totals per (kernel, category), 4 threads per kernel
+    // phase 2: exact integer totals per (kernel, category), 2 threads per kernel
     float* tfv = scr;                                            // [3][64]
     float* rrv = scr + 3 * TM;                                   // [3][64]
-    uint64_t* part = reinterpret_cast<uint64_t*>(scr + 6 * TM);  // [3][64]
-    const int m = pt & 63, qr = pt >> 6;
+    uint64_t* part = reinterpret_cast<uint64_t*>(scr + 6 * TM);  // [64]
+    constexpr int kSplit = 60;
+    const int m = pt & 63;
     uint64_t sa = 0, sb = 0, sc = 0;
-    if (qr < 3) {
-        const int lo = qr * 34, hi = qr == 2 ? DSO_INSTR_SLOTS : lo + 34;
-#pragma unroll 2
-        for (int r = lo; r < hi; ++r) sa += acti[(8 + r) * RS + m];
-        part[qr * TM + m] = sa;
+    if (pt < TM) {
+#pragma unroll 4
+        for (int r = 0; r < kSplit; ++r) sa += acti[(8 + r) * RS + m];
     } else {
+#pragma unroll 4
+        for (int r = kSplit; r < DSO_INSTR_SLOTS; ++r) sa += acti[(8 + r) * RS + m];
 #pragma unroll
         for (int r = 0; r < DSO_DTYPE_SLOTS; ++r) sb += acti[(8 + DSO_INSTR_SLOTS + r) * RS + m];
 #pragma unroll
         for (int r = 0; r < DSO_MEMSPACE_SLOTS; ++r)
             sc += acti[(8 + DSO_INSTR_SLOTS + DSO_DTYPE_SLOTS + r) * RS + m];
+        part[m] = sa;
     }
     bar_sync(BAR_PROD, kProducers);
     auto scale = [&](int cat, uint64_t tot) {
@@ -435,42 +459,26 @@ __device__ __forceinline__ void produce_features(float* act, float* scr,
         tfv[cat * TM + m] = tf;
         rrv[cat * TM + m] = rr;
     };
-    if (qr == 0) {
-        scale(0, part[m] + part[TM + m] + part[2 * TM + m]);
-    } else if (qr == 3) {
+    if (pt < TM) {
+        scale(0, sa + part[m]);
+    } else {
         scale(1, sb);
         scale(2, sc);
     }
     bar_sync(BAR_PROD, kProducers);
     // phase 3: normalise in place (each entry reads only itself and its totals)
-#pragma unroll 2
-    for (int j = 0; j < 8; ++j) {
-        const int r = rp + 16 * j;
+#pragma unroll 4
+    for (int j = 0; j < 16; ++j) {
+        const int r = rp + 8 * j;
         if (r >= DSO_COUNT_ROWS) break;
         const int cat = r < DSO_INSTR_SLOTS ? 0 : (r < DSO_INSTR_SLOTS + DSO_DTYPE_SLOTS ? 1 : 2);
         uint4* cp = reinterpret_cast<uint4*>(acti + (8 + r) * RS) + q;
         const uint4 c = *cp;
         const float4 tf = reinterpret_cast<const float4*>(tfv + cat * TM)[q];
         const float4 rr = reinterpret_cast<const float4*>(rrv + cat * TM)[q];
-        const uint32_t cc[4] = {c.x, c.y, c.z, c.w};
-        const float tt[4] = {tf.x, tf.y, tf.z, tf.w};
-        const float ri[4] = {rr.x, rr.y, rr.z, rr.w};
-        float o[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            if (tt[e] > 0.f) {
-                // exact u32 -> f32 for counts < 2^24, on the ALU/FMA pipes
-                const float cf = (__int_as_float(0x4B000000u | (cc[e] & 0x7FFFFFu)) - 8388608.f) +
-                                 ((cc[e] & 0x800000u) ? 8388608.f : 0.f);
-                const float qq = __fmul_rn(cf, ri[e]);
-                o[e] = fmaf(fmaf(-qq, tt[e], cf), ri[e], qq);
-            } else if (tt[e] == 0.f) {
-                o[e] = 0.f;
-            } else {
-                o[e] = (float)((double)cc[e] / fma((double)-tt[e], 16777216.0, (double)ri[e]));
-            }
-        }
-        *reinterpret_cast<float4*>(cp) = make_float4(o[0], o[1], o[2], o[3]);
+        *reinterpret_cast<float4*>(cp) =
+            make_float4(normalize_count(c.x, tf.x, rr.x), normalize_count(c.y, tf.y, rr.y),
+                        normalize_count(c.z, tf.z, rr.z), normalize_count(c.w, tf.w, rr.w));
     }
 }
 
@@ -478,18 +486,18 @@ __device__ __forceinline__ void produce_features(float* act, float* scr,
 __device__ __forceinline__ void produce_fused(float* act, const float* __restrict__ fused,
                                               int64_t t0, int64_t n, int64_t ld, bool vec_ok,
                                               int pt) {
-    const int q = pt & 15, rp = pt >> 4;  // 16 row phases
+    const int q = pt & 15, rp = pt >> 4;  // 8 row phases
     if (vec_ok && t0 + TM <= n) {
-        float4 v[9];
+        float4 v[17];
 #pragma unroll
-        for (int j = 0; j < 9; ++j) {
-            const int r = rp + 16 * j;
+        for (int j = 0; j < 17; ++j) {
+            const int r = rp + 8 * j;
             if (r < DSO_FUSED_ROWS)
                 v[j] = __ldg(reinterpret_cast<const float4*>(fused + (int64_t)r * ld + t0) + q);
         }
 #pragma unroll
-        for (int j = 0; j < 9; ++j) {
-            const int r = rp + 16 * j;
+        for (int j = 0; j < 17; ++j) {
+            const int r = rp + 8 * j;
             if (r < DSO_FUSED_ROWS) reinterpret_cast<float4*>(act + r * RS)[q] = v[j];
         }
     } else {
@@ -497,7 +505,7 @@ __device__ __forceinline__ void produce_fused(float* act, const float* __restric
         const int64_t k = t0 + m;
         const bool live = k < n;
 #pragma unroll 7
-        for (int r = h; r < DSO_FUSED_ROWS; r += 4)
+        for (int r = h; r < DSO_FUSED_ROWS; r += 2)
             act[r * RS + m] = live ? __ldg(fused + (int64_t)r * ld + k) : 0.f;
     }
 }
@@ -547,11 +555,11 @@ __device__ __forceinline__ bool prod_any(bool v) {
 // Producer, sparse input (the reference's own shape: one map of non-zero
 // category counts per kernel, ptx_features.hpp:31-37).  Entry = (count << 7) |
 // slot, slot = count-row index (< 126), count < 2^25; duplicate slots add.
-// 4 producer threads per kernel: the entries are prefetched into registers
+// 2 producer threads per kernel: the entries are prefetched into registers
 // before the producer sweeps the previous tile; afterwards the tile is
 // zero-filled, counts scattered with shared-memory atomics, category totals
 // reduced with shuffles, and only the listed entries are normalised.
-constexpr int kCsrRegs = 8;  // entries per thread held in registers (32 per kernel)
+constexpr int kCsrRegs = 12;  // entries per thread held in registers (24 per kernel)
 
 struct CsrPrefetch {
     uint32_t ent[kCsrRegs];
@@ -560,7 +568,7 @@ struct CsrPrefetch {
 };
 
 __device__ __forceinline__ void csr_prefetch(const Job& J, int64_t t0, int pt, CsrPrefetch& P) {
-    const int m = pt >> 2, sub = pt & 3;
+    const int m = pt / TPK, sub = pt % TPK;
     const int64_t k = t0 + m;
     P.cnt = 0;
     P.first = 0;
@@ -571,7 +579,7 @@ __device__ __forceinline__ void csr_prefetch(const Job& J, int64_t t0, int pt, C
     }
 #pragma unroll
     for (int e = 0; e < kCsrRegs; ++e) {
-        const int idx = sub + 4 * e;
+        const int idx = sub + TPK * e;
         P.ent[e] = idx < P.cnt ? __ldg(J.entries + P.first + idx) : 0u;
     }
 }
@@ -580,22 +588,12 @@ __device__ __forceinline__ int cat_of_row(int r) {
     return r < DSO_INSTR_SLOTS ? 0 : (r < DSO_INSTR_SLOTS + DSO_DTYPE_SLOTS ? 1 : 2);
 }
 
-__device__ __forceinline__ float normalize_count(uint32_t c, float tf, float rr) {
-    if (tf > 0.f) {
-        const float cf = (__int_as_float(0x4B000000u | (c & 0x7FFFFFu)) - 8388608.f) +
-                         ((c & 0x800000u) ? 8388608.f : 0.f);
-        const float qq = __fmul_rn(cf, rr);
-        return fmaf(fmaf(-qq, tf, cf), rr, qq);
-    }
-    if (tf == 0.f) return 0.f;
-    return (float)((double)c / fma((double)-tf, 16777216.0, (double)rr));
-}
 
 __device__ __forceinline__ void csr_features(float* act, float* scr, const Job& J, int64_t t0,
                                              int pt, const CsrPrefetch& P, bool dcgm_issued,
-                                             uint64_t* mbar, uint32_t& parity) {
+                                             uint64_t* mbar, uint32_t& parbits, int bit) {
     uint32_t* acti = reinterpret_cast<uint32_t*>(act);
-    const int m = pt >> 2, sub = pt & 3;
+    const int m = pt / TPK, sub = pt % TPK;
     // zero-fill the count rows (8..133); DCGM rows arrive by bulk copy or here
     {
         float4* z = reinterpret_cast<float4*>(act + 8 * RS);
@@ -604,7 +602,7 @@ __device__ __forceinline__ void csr_features(float* act, float* scr, const Job& 
         if (!dcgm_issued) {
             const int mm = pt & 63, h = pt >> 6;
             const int64_t k = t0 + mm;
-            for (int r = h; r < 8; r += 4)
+            for (int r = h; r < 8; r += kProducers / TM)
                 act[r * RS + mm] = k < J.n ? __ldg(J.dcgm + (int64_t)r * J.ld + k) : 0.f;
         }
     }
@@ -624,13 +622,13 @@ __device__ __forceinline__ void csr_features(float* act, float* scr, const Job& 
     };
 #pragma unroll
     for (int e = 0; e < kCsrRegs; ++e)
-        if (sub + 4 * e < P.cnt) scatter(P.ent[e]);
-    for (int idx = sub + 4 * kCsrRegs; idx < P.cnt; idx += 4) scatter(__ldg(J.entries + P.first + idx));
+        if (sub + TPK * e < P.cnt) scatter(P.ent[e]);
+    for (int idx = sub + TPK * kCsrRegs; idx < P.cnt; idx += TPK)
+        scatter(__ldg(J.entries + P.first + idx));
 #pragma unroll
-    for (int c = 0; c < 3; ++c) {
-        tot[c] += __shfl_xor_sync(0xffffffffu, tot[c], 1);
-        tot[c] += __shfl_xor_sync(0xffffffffu, tot[c], 2);
-    }
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int off = 1; off < TPK; off <<= 1) tot[c] += __shfl_xor_sync(0xffffffffu, tot[c], off);
     float tf[3], rr[3];
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
@@ -652,7 +650,7 @@ __device__ __forceinline__ void csr_features(float* act, float* scr, const Job& 
         }
     }
     // (a barrier: every atomic and scale is in place)
-    const bool any_spill = prod_any(P.cnt > 4 * kCsrRegs);
+    const bool any_spill = prod_any(P.cnt > TPK * kCsrRegs);
     if (!any_spill) {
         // pass 2 (common case): read the summed counts of this thread's slots, then
         // overwrite them with the fractions (a slot listed twice gets the same
@@ -662,7 +660,7 @@ __device__ __forceinline__ void csr_features(float* act, float* scr, const Job& 
         for (int e = 0; e < kCsrRegs; ++e) {
             v[e] = 0.f;
             const int slot = (int)(P.ent[e] & 127u);
-            if (sub + 4 * e < P.cnt && slot < DSO_COUNT_ROWS) {
+            if (sub + TPK * e < P.cnt && slot < DSO_COUNT_ROWS) {
                 const int cat = cat_of_row(slot);
                 const uint32_t c = acti[(8 + slot) * RS + m];
                 v[e] = normalize_count(c, cat == 0 ? tf[0] : (cat == 1 ? tf[1] : tf[2]),
@@ -673,15 +671,15 @@ __device__ __forceinline__ void csr_features(float* act, float* scr, const Job& 
 #pragma unroll
         for (int e = 0; e < kCsrRegs; ++e) {
             const int slot = (int)(P.ent[e] & 127u);
-            if (sub + 4 * e < P.cnt && slot < DSO_COUNT_ROWS) act[(8 + slot) * RS + m] = v[e];
+            if (sub + TPK * e < P.cnt && slot < DSO_COUNT_ROWS) act[(8 + slot) * RS + m] = v[e];
         }
     } else {
-        // some kernel has more than 32 entries: normalise the whole dense tile
+        // some kernel has more than 24 entries: normalise the whole dense tile
         // (every element read and written by the same thread, so no hazards)
         const int q = pt & 15, rp = pt >> 4;
 #pragma unroll 2
-        for (int j = 0; j < 8; ++j) {
-            const int r = rp + 16 * j;
+        for (int j = 0; j < 16; ++j) {
+            const int r = rp + 8 * j;
             if (r >= DSO_COUNT_ROWS) break;
             const int cat = cat_of_row(r);
             uint4* cp = reinterpret_cast<uint4*>(acti + (8 + r) * RS) + q;
@@ -694,8 +692,8 @@ __device__ __forceinline__ void csr_features(float* act, float* scr, const Job& 
         }
     }
     if (dcgm_issued) {
-        mbar_wait(mbar, parity);
-        parity ^= 1u;
+        mbar_wait(mbar, (parbits >> bit) & 1u);
+        parbits ^= 1u << bit;
     }
 }
 
@@ -705,7 +703,7 @@ __device__ __forceinline__ void csr_features(float* act, float* scr, const Job& 
 template <bool PIPE>
 __device__ __forceinline__ void produce_results(const float* sm, const float* out, const Job& J,
                                                 int64_t t0, int pt) {
-    const int m = pt >> 2, qtr = pt & 3;  // 4 threads per kernel
+    const int m = pt / TPK, qtr = pt % TPK;  // TPK threads per kernel
     const int64_t k = t0 + m;
     float pr[7];
 #pragma unroll
@@ -727,8 +725,8 @@ __device__ __forceinline__ void produce_results(const float* sm, const float* ou
     const float4* s_core = reinterpret_cast<const float4*>(sm + TABLES);
     const float2* s_mem = reinterpret_cast<const float2*>(sm + TABLES + 4 * J.nc);
     const int nc = J.nc, nm = J.nm;
-    // quarter qtr sweeps core levels [i_lo, i_hi): contiguous quarters in visit order
-    const int i_lo = (nc * qtr) >> 2, i_hi = (nc * (qtr + 1)) >> 2;
+    // part qtr sweeps core levels [i_lo, i_hi): contiguous parts in visit order
+    const int i_lo = nc * qtr / TPK, i_hi = nc * (qtr + 1) / TPK;
     Best b{__int_as_float(0x7fc00000), __int_as_float(0x7fc00000), i_lo * nm};
     const bool empty = !(i_lo < i_hi);
     if (!empty) {
@@ -744,7 +742,7 @@ __device__ __forceinline__ void produce_results(const float* sm, const float* ou
     // merge the quarters (merge_best is exact in any order: ties use the index)
     bool emp = empty;
 #pragma unroll
-    for (int off = 1; off <= 2; off <<= 1) {
+    for (int off = 1; off < TPK; off <<= 1) {
         Best o;
         o.c = __shfl_xor_sync(0xffffffffu, b.c, off);
         o.e = __shfl_xor_sync(0xffffffffu, b.e, off);
@@ -787,8 +785,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if (threadIdx.x == 0) {
             uint64_t* mb = reinterpret_cast<uint64_t*>(sm + MBAR);
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(mb)));
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(mb + 1)));
+            for (int b = 0; b < kBufs; ++b)
+                asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(mb + b)));
             asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         }
         if (PIPE) {
@@ -802,20 +800,27 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int64_t tiles = (J.n + TM - 1) / TM;
     const int64_t my_tiles =
         (int64_t)blockIdx.x < tiles ? (tiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+    // Roles: producers are warps 0..3, consumer group G (0, 1) warps 4+4G..7+4G.
+    // Tile i of this CTA goes to consumer group i % 2 through buffer i % 3, so
+    // each scheduler runs two consumer warps (one per group, on different tiles:
+    // one group's epilogue overlaps the other's FFMA2 stream) and one producer.
     const int tid = threadIdx.x;
-    if (tid < kConsumers) {
-        // ================================ consumer ================================
-        for (int64_t i = 0; i < my_tiles; ++i) {
-            const int s = (int)(i & 1);
+    if (tid >= kProducers) {
+        // ================================ consumers ================================
+        const int G = (tid - kProducers) / kGroupThreads;
+        const int ct = (tid - kProducers) % kGroupThreads;
+        for (int64_t i = G; i < my_tiles; i += kGroups) {
+            const int b = (int)(i % kBufs);
             PT_BEGIN(t_w);
-            bar_sync(BAR_FULL0 + s, kThreads);  // features in act[s]; out[s] free
+            bar_sync(BAR_FULL0 + b, kHandoff);  // features in act[b]; out[b] free
             PT_END(0, t_w);
-            consumer_tile(sm, sm + ACT + s * kActFloats, sm + OUT + s * kOutFloats, tid);
-            bar_arrive(BAR_READY0 + s, kThreads);  // predictions in out[s]; act[s] free
+            consumer_tile(sm, sm + ACT + b * kActFloats, sm + OUT + b * kOutFloats, ct,
+                          BAR_CONS0 + G);
+            bar_arrive(BAR_READY0 + b, kHandoff);  // predictions in out[b]; act[b] free
         }
     } else {
         // ================================ producer ================================
-        const int pt = tid - kConsumers;
+        const int pt = tid;
         float* scr = sm + SCR;
         const bool dcgm_ok = ((J.ld & 3) == 0) && ((reinterpret_cast<uintptr_t>(J.dcgm) & 15) == 0);
         const bool vec_ok =
@@ -823,48 +828,48 @@ __global__ void __launch_bounds__(kThreads, 1)
             : MODE == MODE_CSR ? dcgm_ok
                                : (((J.ld & 3) == 0) && ((reinterpret_cast<uintptr_t>(J.fused) & 15) == 0));
         uint64_t* mbar = reinterpret_cast<uint64_t*>(sm + MBAR);
-        uint32_t par0 = 0u, par1 = 0u;  // mbarrier phase per buffer
-        CsrPrefetch P;                  // CSR: entries of the tile being prefetched
+        uint32_t parbits = 0u;  // mbarrier phase bit per buffer
+        CsrPrefetch P;                             // CSR: entries of the tile being prefetched
         auto t0_of = [&](int64_t i) { return (blockIdx.x + i * gridDim.x) * (int64_t)TM; };
         auto issue = [&](int64_t i) -> bool {
-            const int s = (int)(i & 1);
+            const int b = (int)(i % kBufs);
             if (MODE == MODE_DENSE)
-                return issue_tile_loads(sm + ACT + s * kActFloats, mbar + s, J.counts, J.dcgm,
+                return issue_tile_loads(sm + ACT + b * kActFloats, mbar + b, J.counts, J.dcgm,
                                         t0_of(i), J.n, J.ld, vec_ok, pt);
             if (MODE == MODE_CSR) {
                 csr_prefetch(J, t0_of(i), pt, P);
-                return issue_tile_loads(sm + ACT + s * kActFloats, mbar + s, J.counts, J.dcgm,
+                return issue_tile_loads(sm + ACT + b * kActFloats, mbar + b, J.counts, J.dcgm,
                                         t0_of(i), J.n, J.ld, vec_ok, pt, 8);
             }
             return false;
         };
         auto finish = [&](int64_t i, bool issued) {
-            const int s = (int)(i & 1);
-            float* act = sm + ACT + s * kActFloats;
+            const int b = (int)(i % kBufs);
+            float* act = sm + ACT + b * kActFloats;
             PT_BEGIN(t_f);
             if (MODE == MODE_DENSE)
                 produce_features(act, scr, J.counts, J.dcgm, t0_of(i), J.n, J.ld, issued,
-                                 mbar + s, s ? par1 : par0, pt);
+                                 mbar + b, parbits, b, pt);
             else if (MODE == MODE_CSR)
-                csr_features(act, scr, J, t0_of(i), pt, P, issued, mbar + s, s ? par1 : par0);
+                csr_features(act, scr, J, t0_of(i), pt, P, issued, mbar + b, parbits, b);
             else
                 produce_fused(act, J.fused, t0_of(i), J.n, J.ld, vec_ok, pt);
             PT_END(10, t_f);
-            bar_arrive(BAR_FULL0 + s, kThreads);
+            bar_arrive(BAR_FULL0 + b, kHandoff);
         };
-        for (int64_t i = 0; i < 2 && i < my_tiles; ++i) finish(i, issue(i));
+        for (int64_t i = 0; i < kBufs && i < my_tiles; ++i) finish(i, issue(i));
         for (int64_t i = 0; i < my_tiles; ++i) {
-            const int s = (int)(i & 1);
+            const int b = (int)(i % kBufs);
             PT_BEGIN(t_w);
-            bar_sync(BAR_READY0 + s, kThreads);  // tile i predicted; act[s] free
+            bar_sync(BAR_READY0 + b, kHandoff);  // tile i predicted; act[b] free
             PT_END(8, t_w);
-            const bool more = i + 2 < my_tiles;
-            const bool issued = more ? issue(i + 2) : false;  // loads fly during the sweep
+            const bool more = i + kBufs < my_tiles;
+            const bool issued = more ? issue(i + kBufs) : false;  // loads fly during the sweep
             PT_BEGIN(t_r);
-            produce_results<PIPE>(sm, sm + OUT + s * kOutFloats, J, t0_of(i), pt);
+            produce_results<PIPE>(sm, sm + OUT + b * kOutFloats, J, t0_of(i), pt);
             bar_sync(BAR_PROD, kProducers);
             PT_END(9, t_r);
-            if (more) finish(i + 2, issued);
+            if (more) finish(i + kBufs, issued);
         }
     }
 }
