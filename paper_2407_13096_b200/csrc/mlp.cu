@@ -45,12 +45,18 @@ constexpr int RS2 = RS / 2;
 constexpr int kGroupThreads = 128;  // one consumer group: 4 warps, one per SM sub-partition
 constexpr int kGroups = 2;          // two groups -> two consumer warps per scheduler
 constexpr int kConsumers = kGroups * kGroupThreads;
-constexpr int kProducers = 128;     // 4 warps
-constexpr int kThreads = kConsumers + kProducers;  // 384
-constexpr int TPK = kProducers / TM;               // producer threads per kernel (2)
+constexpr int kProducers = 256;     // 8 warps (two warpgroups)
+constexpr int kThreads = kConsumers + kProducers;  // 512
+constexpr int TPK = kProducers / TM;               // producer threads per kernel (4)
+constexpr int RPH = kProducers / 16;               // row phases of a 16-quad tile sweep
 constexpr int kBufs = 3;                           // activation/output buffers
 constexpr int kHandoff = kProducers + kGroupThreads;  // threads on a FULL/READY barrier
-static_assert(kProducers == 128 && TPK == 2, "producer code is written for 4 warps");
+// Registers: the kernel launches with 128 per thread (512 threads); producers
+// release down to 96 and consumers grow to 160 (setmaxnreg; 256*96 + 256*160
+// = 64K), so the FFMA2 tiles keep their accumulators and operand stages.
+constexpr int kProducerRegs = 96;
+constexpr int kConsumerRegs = 160;
+static_assert(kProducers * kProducerRegs + kConsumers * kConsumerRegs <= 65536, "RF budget");
 
 // Named barriers (0 is __syncthreads).
 constexpr int BAR_PROD = 1, BAR_CONS0 = 2, BAR_FULL0 = 4, BAR_READY0 = 7;
@@ -406,7 +412,7 @@ __device__ __forceinline__ void produce_features(float* act, float* scr,
                                                  int pt) {
     uint32_t* acti = reinterpret_cast<uint32_t*>(act);
     const int q = pt & 15;   // kernels 4q .. 4q+3
-    const int rp = pt >> 4;  // row phase 0..7
+    const int rp = pt >> 4;  // row phase 0..RPH-1
     if (issued) {
         mbar_wait(mbar, (parbits >> bit) & 1u);
         parbits ^= 1u << bit;
@@ -415,33 +421,32 @@ __device__ __forceinline__ void produce_features(float* act, float* scr,
         const int m = pt & 63, h = pt >> 6;
         const int64_t k = t0 + m;
         const bool live = k < n;
-#pragma unroll 9
-        for (int r = h; r < DSO_COUNT_ROWS; r += 2)
+#pragma unroll 8
+        for (int r = h; r < DSO_COUNT_ROWS; r += kProducers / TM)
             acti[(8 + r) * RS + m] = live ? __ldg(counts + (int64_t)r * ld + k) : 0u;
 #pragma unroll
-        for (int r = h; r < 8; r += 2)
+        for (int r = h; r < 8; r += kProducers / TM)
             act[r * RS + m] = live ? __ldg(dcgm + (int64_t)r * ld + k) : 0.f;
     }
     bar_sync(BAR_PROD, kProducers);
-    // phase 2: exact integer totals per (kernel, category), 2 threads per kernel
+    // phase 2: exact integer totals per (kernel, category), 4 threads per kernel:
+    // three thirds of the instr rows, and dtype + memspace
     float* tfv = scr;                                            // [3][64]
     float* rrv = scr + 3 * TM;                                   // [3][64]
-    uint64_t* part = reinterpret_cast<uint64_t*>(scr + 6 * TM);  // [64]
-    constexpr int kSplit = 60;
-    const int m = pt & 63;
+    uint64_t* part = reinterpret_cast<uint64_t*>(scr + 6 * TM);  // [3][64]
+    const int m = pt & 63, qr = pt >> 6;
     uint64_t sa = 0, sb = 0, sc = 0;
-    if (pt < TM) {
-#pragma unroll 4
-        for (int r = 0; r < kSplit; ++r) sa += acti[(8 + r) * RS + m];
+    if (qr < 3) {
+        const int lo = qr * 34, hi = qr == 2 ? DSO_INSTR_SLOTS : lo + 34;
+#pragma unroll 2
+        for (int r = lo; r < hi; ++r) sa += acti[(8 + r) * RS + m];
+        part[qr * TM + m] = sa;
     } else {
-#pragma unroll 4
-        for (int r = kSplit; r < DSO_INSTR_SLOTS; ++r) sa += acti[(8 + r) * RS + m];
 #pragma unroll
         for (int r = 0; r < DSO_DTYPE_SLOTS; ++r) sb += acti[(8 + DSO_INSTR_SLOTS + r) * RS + m];
 #pragma unroll
         for (int r = 0; r < DSO_MEMSPACE_SLOTS; ++r)
             sc += acti[(8 + DSO_INSTR_SLOTS + DSO_DTYPE_SLOTS + r) * RS + m];
-        part[m] = sa;
     }
     bar_sync(BAR_PROD, kProducers);
     auto scale = [&](int cat, uint64_t tot) {
@@ -459,17 +464,17 @@ __device__ __forceinline__ void produce_features(float* act, float* scr,
         tfv[cat * TM + m] = tf;
         rrv[cat * TM + m] = rr;
     };
-    if (pt < TM) {
-        scale(0, sa + part[m]);
-    } else {
+    if (qr == 0) {
+        scale(0, part[m] + part[TM + m] + part[2 * TM + m]);
+    } else if (qr == 3) {
         scale(1, sb);
         scale(2, sc);
     }
     bar_sync(BAR_PROD, kProducers);
     // phase 3: normalise in place (each entry reads only itself and its totals)
 #pragma unroll 4
-    for (int j = 0; j < 16; ++j) {
-        const int r = rp + 8 * j;
+    for (int j = 0; j < (DSO_COUNT_ROWS + RPH - 1) / RPH; ++j) {
+        const int r = rp + RPH * j;
         if (r >= DSO_COUNT_ROWS) break;
         const int cat = r < DSO_INSTR_SLOTS ? 0 : (r < DSO_INSTR_SLOTS + DSO_DTYPE_SLOTS ? 1 : 2);
         uint4* cp = reinterpret_cast<uint4*>(acti + (8 + r) * RS) + q;
@@ -486,18 +491,19 @@ __device__ __forceinline__ void produce_features(float* act, float* scr,
 __device__ __forceinline__ void produce_fused(float* act, const float* __restrict__ fused,
                                               int64_t t0, int64_t n, int64_t ld, bool vec_ok,
                                               int pt) {
-    const int q = pt & 15, rp = pt >> 4;  // 8 row phases
+    const int q = pt & 15, rp = pt >> 4;  // RPH row phases
+    constexpr int NJ = (DSO_FUSED_ROWS + RPH - 1) / RPH;
     if (vec_ok && t0 + TM <= n) {
-        float4 v[17];
+        float4 v[NJ];
 #pragma unroll
-        for (int j = 0; j < 17; ++j) {
-            const int r = rp + 8 * j;
+        for (int j = 0; j < NJ; ++j) {
+            const int r = rp + RPH * j;
             if (r < DSO_FUSED_ROWS)
                 v[j] = __ldg(reinterpret_cast<const float4*>(fused + (int64_t)r * ld + t0) + q);
         }
 #pragma unroll
-        for (int j = 0; j < 17; ++j) {
-            const int r = rp + 8 * j;
+        for (int j = 0; j < NJ; ++j) {
+            const int r = rp + RPH * j;
             if (r < DSO_FUSED_ROWS) reinterpret_cast<float4*>(act + r * RS)[q] = v[j];
         }
     } else {
@@ -505,7 +511,7 @@ __device__ __forceinline__ void produce_fused(float* act, const float* __restric
         const int64_t k = t0 + m;
         const bool live = k < n;
 #pragma unroll 7
-        for (int r = h; r < DSO_FUSED_ROWS; r += 2)
+        for (int r = h; r < DSO_FUSED_ROWS; r += kProducers / TM)
             act[r * RS + m] = live ? __ldg(fused + (int64_t)r * ld + k) : 0.f;
     }
 }
@@ -559,7 +565,7 @@ __device__ __forceinline__ bool prod_any(bool v) {
 // before the producer sweeps the previous tile; afterwards the tile is
 // zero-filled, counts scattered with shared-memory atomics, category totals
 // reduced with shuffles, and only the listed entries are normalised.
-constexpr int kCsrRegs = 12;  // entries per thread held in registers (24 per kernel)
+constexpr int kCsrRegs = 24 / TPK;  // entries per thread held in registers (24 per kernel)
 
 struct CsrPrefetch {
     uint32_t ent[kCsrRegs];
@@ -678,8 +684,8 @@ __device__ __forceinline__ void csr_features(float* act, float* scr, const Job& 
         // (every element read and written by the same thread, so no hazards)
         const int q = pt & 15, rp = pt >> 4;
 #pragma unroll 2
-        for (int j = 0; j < 16; ++j) {
-            const int r = rp + 8 * j;
+        for (int j = 0; j < (DSO_COUNT_ROWS + RPH - 1) / RPH; ++j) {
+            const int r = rp + RPH * j;
             if (r >= DSO_COUNT_ROWS) break;
             const int cat = cat_of_row(r);
             uint4* cp = reinterpret_cast<uint4*>(acti + (8 + r) * RS) + q;
@@ -800,13 +806,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int64_t tiles = (J.n + TM - 1) / TM;
     const int64_t my_tiles =
         (int64_t)blockIdx.x < tiles ? (tiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
-    // Roles: producers are warps 0..3, consumer group G (0, 1) warps 4+4G..7+4G.
+    // Roles: producers are warps 0..7, consumer group G (0, 1) warps 8+4G..11+4G.
     // Tile i of this CTA goes to consumer group i % 2 through buffer i % 3, so
     // each scheduler runs two consumer warps (one per group, on different tiles:
     // one group's epilogue overlaps the other's FFMA2 stream) and one producer.
     const int tid = threadIdx.x;
     if (tid >= kProducers) {
         // ================================ consumers ================================
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kConsumerRegs));
         const int G = (tid - kProducers) / kGroupThreads;
         const int ct = (tid - kProducers) % kGroupThreads;
         for (int64_t i = G; i < my_tiles; i += kGroups) {
@@ -820,6 +827,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else {
         // ================================ producer ================================
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kProducerRegs));
         const int pt = tid;
         float* scr = sm + SCR;
         const bool dcgm_ok = ((J.ld & 3) == 0) && ((reinterpret_cast<uintptr_t>(J.dcgm) & 15) == 0);
