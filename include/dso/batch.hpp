@@ -1,0 +1,200 @@
+// dso/batch.hpp — drop-in batched GPU versions of the DSO hot path with the
+// reference's own types and error behaviour.
+//
+// Include next to the reference headers (proj/include/dso/*.hpp) and link
+// libdso_b200.so (include/dso_b200.h is the C-ABI underneath).  Every function
+// mirrors a reference function for a whole batch:
+//
+//   brute_force_config_batch  <-  brute_force_config   (optimizer.hpp:48-52)
+//                                 bit-exact: FP64 kernel in the reference's
+//                                 operation order (dso_sweep_f64)
+//   optimize_kernels          <-  featurize (ptx_features.hpp:55) +
+//                                 FusedFeatures::as_vector (mlp.hpp:20-25) +
+//                                 predict_params (mlp.hpp:66) +
+//                                 brute_force_config, fused on the GPU
+//                                 (dso_pipeline_csr; FP32, 1e-5 contract)
+//   GpuContext::set_domain    <-  validate(DvfsDomain) (optimizer.cpp:58-88)
+//   GpuContext::set_model     <-  validate(MlpModel)   (mlp.cpp:209-226)
+//
+// Failures throw dso::Error with the reference's ErrorKind (error.hpp:10-25);
+// a CUDA failure is reported as ErrorKind::IoError.  Like the reference the
+// functions validate before computing; per-kernel parameter validation
+// (dvfs_model.hpp:50-58) throws for the first invalid kernel in index order,
+// as a scalar loop over brute_force_config would.
+#pragma once
+
+#include <cstdint>
+#include <span>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "dso/dvfs_model.hpp"
+#include "dso/error.hpp"
+#include "dso/optimizer.hpp"
+#include "dso_b200.h"
+
+namespace dso {
+
+inline void check_status(int32_t status, const dso_ctx* ctx) {
+    if (status == DSO_OK) return;
+    const std::string msg = ctx ? dso_last_error(ctx) : std::string(dso_status_name(status));
+    if (status == DSO_ERR_CUDA) throw Error(ErrorKind::IoError, msg);
+    throw Error(static_cast<ErrorKind>(status - 1), msg);
+}
+
+// One device's state (stream, domain tables, model).  Not thread-safe: one
+// host thread per context, like the reference's single-writer rule.
+class GpuContext {
+public:
+    explicit GpuContext(int device = 0) {
+        check_status(dso_ctx_create(device, &ctx_), nullptr);
+    }
+    ~GpuContext() { dso_ctx_destroy(ctx_); }
+    GpuContext(const GpuContext&) = delete;
+    GpuContext& operator=(const GpuContext&) = delete;
+
+    dso_ctx* handle() const { return ctx_; }
+
+    void set_domain(const DvfsDomain& d) {
+        const double dev[5] = {d.dev.kappa_vf, d.dev.pmax_w, d.dev.vmin_v, d.dev.vmax_v,
+                               d.dev.mhz_per_unit};
+        check_status(dso_set_domain(ctx_, d.core_freqs_mhz.data(),
+                                    static_cast<int32_t>(d.core_freqs_mhz.size()),
+                                    d.mem_freqs_mhz.data(),
+                                    static_cast<int32_t>(d.mem_freqs_mhz.size()), dev),
+                     ctx_);
+        nm_ = d.mem_freqs_mhz.size();
+        core_ = d.core_freqs_mhz;
+        mem_ = d.mem_freqs_mhz;
+        dev_ = d.dev;
+    }
+
+    // MlpModel in the reference layout without Eigen: weights[l] row-major
+    // (sizes[l+1] x sizes[l]) concatenated, biases concatenated (model.schema.json).
+    void set_model(const std::vector<int32_t>& sizes, const std::vector<double>& weights,
+                   const std::vector<double>& biases, const std::vector<double>& target_mean,
+                   const std::vector<double>& target_std) {
+        check_status(dso_set_model(ctx_, sizes.data(), static_cast<int32_t>(sizes.size()),
+                                   weights.data(), biases.data(), target_mean.data(),
+                                   target_std.data()),
+                     ctx_);
+    }
+
+    const std::vector<double>& core() const { return core_; }
+    const std::vector<double>& mem() const { return mem_; }
+    const DeviceConstants& dev() const { return dev_; }
+    std::size_t nm() const { return nm_; }
+
+private:
+    dso_ctx* ctx_ = nullptr;
+    std::size_t nm_ = 0;
+    std::vector<double> core_, mem_;
+    DeviceConstants dev_{};
+};
+
+// brute_force_config for every element of params, bit-identical to the
+// reference (optimizer.cpp:90-117).  The context's domain must equal `domain`
+// (it is re-uploaded when it differs).
+inline std::vector<OptimizationResult> brute_force_config_batch(
+    std::span<const KernelModelParams> params, const DvfsDomain& domain, double eta,
+    double pmax_w, GpuContext& ctx) {
+    if (ctx.core() != domain.core_freqs_mhz || ctx.mem() != domain.mem_freqs_mhz ||
+        ctx.dev().kappa_vf != domain.dev.kappa_vf || ctx.dev().vmin_v != domain.dev.vmin_v ||
+        ctx.dev().vmax_v != domain.dev.vmax_v || ctx.dev().pmax_w != domain.dev.pmax_w ||
+        ctx.dev().mhz_per_unit != domain.dev.mhz_per_unit)
+        ctx.set_domain(domain);
+    const int64_t n = static_cast<int64_t>(params.size());
+    std::vector<int32_t> idx(n), ks(n);
+    std::vector<double> cost(n), energy(n), time(n);
+    static_assert(sizeof(KernelModelParams) == 7 * sizeof(double), "AoS layout");
+    check_status(dso_sweep_f64(ctx.handle(), reinterpret_cast<const double*>(params.data()), n,
+                               eta, pmax_w, idx.data(), cost.data(), energy.data(), time.data(),
+                               ks.data(), DSO_HOST),
+                 ctx.handle());
+    std::vector<OptimizationResult> out(n);
+    const std::size_t nm = domain.mem_freqs_mhz.size();
+    const long candidates = static_cast<long>(domain.core_freqs_mhz.size() * nm);
+    for (int64_t k = 0; k < n; ++k) {
+        if (ks[k]) {
+            // validate(params) (dvfs_model.hpp:50-58), first failure in index order
+            validate(params[k]);
+            throw Error(static_cast<ErrorKind>(ks[k] - 1), "invalid kernel parameters");
+        }
+        const std::size_t i = static_cast<std::size_t>(idx[k]) / nm;
+        const std::size_t j = static_cast<std::size_t>(idx[k]) % nm;
+        OptimizationResult& r = out[k];
+        const double fc = domain.core_freqs_mhz[i];
+        r.best = DvfsConfig{required_voltage_mhz(fc, domain.dev), fc, domain.mem_freqs_mhz[j]};
+        r.cost = cost[k];
+        r.energy_j = energy[k];
+        r.time_s = time[k];
+        r.candidates_evaluated = candidates;
+        r.fallback = false;
+    }
+    return out;
+}
+
+// Non-zero PTX category counts of one kernel: (count-row index, count) pairs —
+// the reference's KernelInstructionCounts maps (ptx_features.hpp:31-37) keyed
+// by position in the canonical category lists (instr 0..100, dtype 101..117,
+// memspace 118..125).
+struct SparseCounts {
+    std::vector<std::pair<int, std::uint32_t>> entries;
+};
+
+// DCGM ratios in DcgmMetricVector order (telemetry.hpp:13-28).
+using Dcgm8 = std::array<double, 8>;
+
+struct KernelDecision {
+    KernelModelParams params;  // predict_params output (clamped)
+    bool clamped = false;
+    std::size_t fc_idx = 0, fm_idx = 0;
+    double cost = 0, energy_j = 0, time_s = 0;  // FP32 evaluation at the chosen pair
+};
+
+// features -> predict_params -> brute_force_config for a batch of kernels on the
+// GPU (one fused kernel; host buffers are staged in overlapped chunks).
+inline std::vector<KernelDecision> optimize_kernels(std::span<const SparseCounts> counts,
+                                                    std::span<const Dcgm8> dcgm, double eta,
+                                                    double pmax_w, GpuContext& ctx) {
+    if (counts.size() != dcgm.size())
+        throw Error(ErrorKind::InvalidArgument, "counts and dcgm sizes differ");
+    const int64_t n = static_cast<int64_t>(counts.size());
+    std::vector<uint64_t> row_ptr(n + 1, 0);
+    std::vector<uint32_t> entries;
+    for (int64_t k = 0; k < n; ++k) {
+        for (auto [slot, c] : counts[k].entries) {
+            if (slot < 0 || slot >= DSO_COUNT_ROWS || c >= (1u << 25))
+                throw Error(ErrorKind::InvalidArgument, "count slot or value out of range");
+            entries.push_back((c << 7) | static_cast<uint32_t>(slot));
+        }
+        row_ptr[k + 1] = entries.size();
+    }
+    std::vector<float> dc(8 * n), params(7 * n), cost(n), energy(n), time(n);
+    std::vector<int32_t> idx(n);
+    std::vector<uint8_t> cl(n);
+    for (int64_t k = 0; k < n; ++k)
+        for (int m = 0; m < 8; ++m) dc[m * n + k] = static_cast<float>(dcgm[k][m]);
+    check_status(dso_pipeline_csr(ctx.handle(), row_ptr.data(), entries.data(), 0, dc.data(), n,
+                                  n, eta, pmax_w, params.data(), cl.data(), idx.data(),
+                                  cost.data(), energy.data(), time.data(), DSO_HOST),
+                 ctx.handle());
+    std::vector<KernelDecision> out(n);
+    const std::size_t nm = ctx.nm();
+    for (int64_t k = 0; k < n; ++k) {
+        KernelDecision& d = out[k];
+        d.params = KernelModelParams{params[0 * n + k], params[1 * n + k], params[2 * n + k],
+                                     params[3 * n + k], params[4 * n + k], params[5 * n + k],
+                                     params[6 * n + k]};
+        d.clamped = cl[k] != 0;
+        d.fc_idx = static_cast<std::size_t>(idx[k]) / nm;
+        d.fm_idx = static_cast<std::size_t>(idx[k]) % nm;
+        d.cost = cost[k];
+        d.energy_j = energy[k];
+        d.time_s = time[k];
+    }
+    return out;
+}
+
+}  // namespace dso

@@ -24,7 +24,7 @@
  *                               (category order ptx_features.cpp:18-49)
  *       dcgm    float [8][ld]   smact smocc tenso drama fp64a fp32a fp16a intac
  *                               (telemetry.hpp:13-28)
- *       fused   float [134][ld] FusedFeatures::as_vector order (mlp.cpp:307-314)
+ *       fused   float [134][ld] FusedFeatures::as_vector order (mlp.cpp:158-165)
  *     idx = fc_idx * nm + fm_idx (brute_force loop order, optimizer.cpp:99-100).
  *   - All launches are asynchronous on the context stream; dso_sync() waits.
  *     Pass DSO_HOST in flags (where offered) for host buffers: the call then
@@ -83,7 +83,7 @@ int32_t dso_validate_domain(const double* core_mhz, int32_t nc, const double* me
                             int32_t nm, const double* dev, char* msg, int32_t msg_len);
 
 /* ---- model: replaces the MlpModel argument + validate(MlpModel) -----------
- * mlp.hpp:35-42, mlp.cpp:358-375.  weights: per layer l, sizes[l+1] x sizes[l]
+ * mlp.hpp:35-42, mlp.cpp:209-226.  weights: per layer l, sizes[l+1] x sizes[l]
  * row-major, concatenated (model.schema.json order, json_io.cpp:154-160);
  * biases concatenated; mean/std of size sizes[n_sizes-1], std > 0. */
 int32_t dso_set_model(dso_ctx* ctx, const int32_t* layer_sizes, int32_t n_sizes,
@@ -93,7 +93,7 @@ int32_t dso_set_model(dso_ctx* ctx, const int32_t* layer_sizes, int32_t n_sizes,
 int32_t dso_get_model(dso_ctx* ctx, double* weights, double* biases);
 
 /* ---- host helpers (host C++ inside the library, no device work) ----------- */
-/* init_mlp (mlp.cpp:333-356): Glorot-uniform from Rng(seed), zero biases. */
+/* init_mlp (mlp.cpp:184-207): Glorot-uniform from Rng(seed), zero biases. */
 int32_t dso_init_mlp(const int32_t* layer_sizes, int32_t n_sizes, uint64_t seed,
                      double* weights, double* biases);
 /* shuffled_indices (rng.hpp:58-64) from Rng(seed) state; advances *state. */
@@ -101,7 +101,7 @@ int32_t dso_shuffled_indices(uint64_t n, uint64_t* rng_state, uint64_t* out);
 
 /* ---- feature stage ---------------------------------------------------------
  * featurize (ptx_features.cpp:311-329) + FusedFeatures::as_vector
- * (mlp.cpp:307-314): per category count/total (all-zero for a zero total),
+ * (mlp.cpp:158-165): per category count/total (all-zero for a zero total),
  * fused with the already-averaged DCGM vector.  Results equal the reference's
  * double features rounded once to float. */
 int32_t dso_featurize(dso_ctx* ctx, const uint32_t* counts, const float* dcgm, int64_t n,
@@ -114,7 +114,7 @@ int32_t dso_dcgm_mean(dso_ctx* ctx, const double* samples, int64_t rows, int64_t
                       int64_t ld, float* out, int64_t* bad_row);
 
 /* ---- predictor inference ---------------------------------------------------
- * predict_params (mlp.cpp:386-402) = forward_raw (mlp.cpp:381-384) + clamp:
+ * predict_params (mlp.cpp:237-253) = forward_raw (mlp.cpp:232-235) + clamp:
  * negative outputs -> 0, alpha+beta <= 0 -> beta = 1e-12; clamped[k] flags it.
  * raw (optional, float [7][ld]) receives forward_raw before clamping. */
 int32_t dso_predict(dso_ctx* ctx, const float* fused, int64_t n, int64_t ld, float* params,
@@ -181,7 +181,7 @@ int32_t dso_gen_synthetic_csr(dso_ctx* ctx, uint64_t root, uint64_t salt_base, i
                               int64_t ld);
 
 /* ---- predictor training (data-parallel) ------------------------------------
- * Mini-batch gradient of mse_loss (mlp.cpp:408-438) on the device model.
+ * Mini-batch gradient of mse_loss (mlp.cpp:259-289) on the device model.
  * x float [in][ld] (fused features), y_std float [out][ld] (standardized
  * targets).  grad (device, weights then biases, same layout as dso_set_model)
  * receives the SUM over the batch of per-sample gradients of
@@ -190,7 +190,7 @@ int32_t dso_gen_synthetic_csr(dso_ctx* ctx, uint64_t root, uint64_t salt_base, i
  * data-parallel step is: grad -> allreduce(sum) -> apply. */
 int32_t dso_train_grad(dso_ctx* ctx, const float* x, const float* y_std, int64_t n,
                        int64_t ld, float* grad, double* loss_sum);
-/* W -= lr * scale * grad  (sgd update, mlp.cpp:254-257). */
+/* W -= lr * scale * grad  (sgd update, mlp.cpp:105-108). */
 int32_t dso_train_apply(dso_ctx* ctx, const float* grad, double lr, double scale);
 /* Number of parameters (weights + biases) of the device model. */
 int64_t dso_model_param_count(const dso_ctx* ctx);

@@ -261,7 +261,7 @@ void orc_gen_seeded(const uint64_t* seeds, int64_t n, double* params, uint32_t* 
 }
 
 /* ====================================================================== */
-/* Features: ptx_features.cpp:311-329, telemetry.cpp:63-101, mlp.cpp:307-314 */
+/* Features: ptx_features.cpp:311-329, telemetry.cpp:63-101, mlp.cpp:158-165 */
 /* ====================================================================== */
 
 static const int kCatBase[3] = {0, 101, 118};
@@ -304,7 +304,7 @@ int orc_dcgm_mean(const double* samples, int64_t rows, double* out, int64_t* bad
     return ORC_OK;
 }
 
-/* FusedFeatures::as_vector, mlp.cpp:307-314: [dcgm 8 | instr 101 | dtype 17 | memspace 8] */
+/* FusedFeatures::as_vector, mlp.cpp:158-165: [dcgm 8 | instr 101 | dtype 17 | memspace 8] */
 void orc_fuse(const uint32_t* counts, const double* dcgm, int64_t n, double* fused) {
     for (int64_t k = 0; k < n; ++k) {
         double* f = fused + 134 * k;
@@ -314,7 +314,7 @@ void orc_fuse(const uint32_t* counts, const double* dcgm, int64_t n, double* fus
 }
 
 /* ====================================================================== */
-/* MLP: src/mlp.cpp:166-253                                                 */
+/* MLP: src/mlp.cpp:17-253                                                 */
 /* ====================================================================== */
 
 int64_t orc_mlp_weight_count(const int* sizes, int nl) {
@@ -329,7 +329,7 @@ int64_t orc_mlp_bias_count(const int* sizes, int nl) {
     return t;
 }
 
-/* init_mlp, mlp.cpp:333-356: Glorot-uniform drawn row-major from Rng(seed). */
+/* init_mlp, mlp.cpp:184-207: Glorot-uniform drawn row-major from Rng(seed). */
 int orc_init_mlp(const int* sizes, int nl, uint64_t seed, double* W, double* b) {
     if (nl < 2) return ORC_InvalidModel;
     for (int l = 0; l < nl; ++l)
@@ -345,7 +345,7 @@ int orc_init_mlp(const int* sizes, int nl, uint64_t seed, double* W, double* b) 
     return ORC_OK;
 }
 
-/* sigmoid, mlp.cpp:166-168 */
+/* sigmoid, mlp.cpp:17-20 */
 static double sigmoid(double z) { return 1.0 / (1.0 + exp(-z)); }
 
 static int max_width(const int* sizes, int nl) {
@@ -355,7 +355,7 @@ static int max_width(const int* sizes, int nl) {
     return w;
 }
 
-/* forward_trace, mlp.cpp:171-181, one column.  acts must hold sum(sizes)
+/* forward_trace, mlp.cpp:22-32, one column.  acts must hold sum(sizes)
  * doubles; returns pointer to the (standardized) output activations. */
 static double* forward_trace1(const int* sizes, int nl, const double* W, const double* b,
                               const double* x, double* acts) {
@@ -384,7 +384,7 @@ static int64_t act_total(const int* sizes, int nl) {
     return t;
 }
 
-/* forward_raw, mlp.cpp:381-384: (out .* std) + mean */
+/* forward_raw, mlp.cpp:232-235: (out .* std) + mean */
 void orc_forward_raw(const int* sizes, int nl, const double* W, const double* b,
                      const double* mean, const double* std, const double* x, int64_t n,
                      double* out) {
@@ -397,7 +397,7 @@ void orc_forward_raw(const int* sizes, int nl, const double* W, const double* b,
     free(acts);
 }
 
-/* predict_params, mlp.cpp:386-402 (kBetaFloor mlp.cpp:15) */
+/* predict_params, mlp.cpp:237-253 (kBetaFloor mlp.cpp:15) */
 static void predict_one(const int* sizes, int nl, const double* W, const double* b,
                         const double* mean, const double* std, const double* x, double* acts,
                         double* p, uint8_t* clamped) {
@@ -476,10 +476,10 @@ void orc_predict_params(const int* sizes, int nl, const double* W, const double*
 }
 
 /* ====================================================================== */
-/* Training: mlp.cpp:206-289 (loss, backprop, SGD epoch, target stats)      */
+/* Training: mlp.cpp:57-130,259-289 (target stats, SGD epoch, loss, backprop)      */
 /* ====================================================================== */
 
-/* mse_loss, mlp.cpp:408-412: 0.5 * ||out - y||^2 / (B * out_dim) */
+/* mse_loss, mlp.cpp:259-263: 0.5 * ||out - y||^2 / (B * out_dim) */
 double orc_mse_loss(const int* sizes, int nl, const double* W, const double* b,
                     const double* x, const double* y, int64_t B) {
     const int in = sizes[0], od = sizes[nl - 1];
@@ -496,7 +496,7 @@ double orc_mse_loss(const int* sizes, int nl, const double* W, const double* b,
     return 0.5 * sq / (double)(B * od);
 }
 
-/* analytic_gradients, mlp.cpp:414-438 */
+/* analytic_gradients, mlp.cpp:265-289 */
 void orc_analytic_gradients(const int* sizes, int nl, const double* W, const double* b,
                             const double* x, const double* y, int64_t B, double* gW,
                             double* gb) {
@@ -545,7 +545,7 @@ void orc_analytic_gradients(const int* sizes, int nl, const double* W, const dou
     free(nd);
 }
 
-/* numeric_gradients, mlp.cpp:440-471 (central differences) */
+/* numeric_gradients, mlp.cpp:291-322 (central differences) */
 void orc_numeric_gradients(const int* sizes, int nl, const double* W, const double* b,
                            const double* x, const double* y, int64_t B, double eps,
                            double* gW, double* gb) {
@@ -576,7 +576,7 @@ void orc_numeric_gradients(const int* sizes, int nl, const double* W, const doub
     free(bp);
 }
 
-/* target_stats, mlp.cpp:206-228 (population std; zero variance -> std 1, mean 0) */
+/* target_stats, mlp.cpp:57-79 (population std; zero variance -> std 1, mean 0) */
 int orc_target_stats(const double* t, int64_t n, int od, double* mean, double* std) {
     int degenerate = 0;
     for (int i = 0; i < od; ++i) mean[i] = 0.0;
@@ -600,7 +600,7 @@ int orc_target_stats(const double* t, int64_t n, int od, double* mean, double* s
     return degenerate;
 }
 
-/* sgd_epoch, mlp.cpp:233-261 */
+/* sgd_epoch, mlp.cpp:84-112 */
 double orc_sgd_epoch(const int* sizes, int nl, double* W, double* b, const double* feats,
                      const double* targets, int64_t n, const double* mean, const double* std,
                      double lr, int batch, uint64_t* rng_state) {

@@ -79,13 +79,13 @@ void orc_gen_seeded(const uint64_t* seeds, int64_t n, double* params, uint32_t* 
 int orc_gen_kernel_rho(uint64_t seed, double rho, double* params, uint32_t* counts,
                        double* dcgm, double* fused);
 
-/* ---- features (ptx_features.cpp:311-329, telemetry.cpp:63-101, mlp.cpp:307-314) */
+/* ---- features (ptx_features.cpp:311-329, telemetry.cpp:63-101, mlp.cpp:158-165) */
 void orc_featurize(const uint32_t* counts, int64_t n, double* out126);
 /* samples [rows][8]; returns status, *bad_row = 1-based offending row */
 int orc_dcgm_mean(const double* samples, int64_t rows, double* out, int64_t* bad_row);
 void orc_fuse(const uint32_t* counts, const double* dcgm, int64_t n, double* fused);
 
-/* ---- MLP (mlp.cpp:166-253) ----------------------------------------------- */
+/* ---- MLP (mlp.cpp:17-253) ----------------------------------------------- */
 /* Model: nl = number of layer sizes; weights concatenated row-major per layer
  * (shape sizes[l+1] x sizes[l]); biases concatenated; mean/std size sizes[nl-1]. */
 int64_t orc_mlp_weight_count(const int* sizes, int nl);
@@ -114,7 +114,7 @@ void orc_numeric_gradients(const int* sizes, int nl, const double* W, const doub
 double orc_sgd_epoch(const int* sizes, int nl, double* W, double* b, const double* feats,
                      const double* targets, int64_t n, const double* mean,
                      const double* std, double lr, int batch, uint64_t* rng_state);
-/* target_stats (mlp.cpp:206-228): returns number of degenerate dims */
+/* target_stats (mlp.cpp:57-79): returns number of degenerate dims */
 int orc_target_stats(const double* targets, int64_t n, int out, double* mean, double* std);
 
 /* ---- sweep (optimizer.cpp:18-117) ---------------------------------------- */

@@ -4,15 +4,15 @@ Each method replaces one reference function for a whole batch of GPU kernels
 (citations are to /root/reference/proj):
 
     Context.featurize          featurize + FusedFeatures::as_vector
-                               (ptx_features.cpp:311-329, mlp.cpp:307-314)
+                               (ptx_features.cpp:311-329, mlp.cpp:158-165)
     Context.dcgm_mean          load_dcgm_samples' per-metric mean (telemetry.cpp:73-89)
-    Context.predict_params     predict_params / forward_raw (mlp.cpp:381-402)
+    Context.predict_params     predict_params / forward_raw (mlp.cpp:232-253)
     Context.brute_force_config brute_force_config (optimizer.cpp:90-117), FP32
     Context.brute_force_config_exact  the same in FP64, bit-exact, reference AoS layout
     Context.eta_sweep          brute_force_config at many etas
     Context.pipeline           counts + DCGM -> features -> predict -> sweep -> argmin
     Context.gen_synthetic      gen_kernel for a seeded stream (sim_harness.cpp:118-144)
-    Context.train_grad / train_apply   analytic_gradients + SGD update (mlp.cpp:233-289,414-438)
+    Context.train_grad / train_apply   analytic_gradients + SGD update (mlp.cpp:84-112,265-289)
 
 Device arrays are torch CUDA tensors in structure-of-arrays layout
 [rows, ld] (see the header).  Errors raise DsoError with the reference's
@@ -132,7 +132,7 @@ class Context:
         self.domain = domain
 
     def set_model(self, model: MlpModel) -> None:
-        """validate(MlpModel) (mlp.cpp:358-375) + packed FP32 upload."""
+        """validate(MlpModel) (mlp.cpp:209-226) + packed FP32 upload."""
         validate_model(model)
         W, b = model.flat()
         sizes = (C.c_int32 * len(model.layer_sizes))(*model.layer_sizes)
@@ -387,5 +387,5 @@ class Context:
         return grad, loss
 
     def train_apply(self, grad, lr: float, scale: float) -> None:
-        """W -= lr * scale * grad on the device model (mlp.cpp:254-257)."""
+        """W -= lr * scale * grad on the device model (mlp.cpp:105-108)."""
         self._raise(self._lib.dso_train_apply(self._h, _ptr(grad), lr, scale))

@@ -298,7 +298,7 @@ int32_t dso_validate_domain(const double* core, int32_t nc, const double* mem, i
 int32_t dso_set_model(dso_ctx* ctx, const int32_t* sizes, int32_t n_sizes, const double* W,
                       const double* b, const double* mean, const double* std_) {
     if (!ctx) return kInvalidArgument;
-    // validate(MlpModel) mlp.cpp:358-375 (shapes come from sizes here)
+    // validate(MlpModel) mlp.cpp:209-226 (shapes come from sizes here)
     if (!sizes || n_sizes < 2) return fail(ctx, kInvalidModel, "layer bookkeeping is inconsistent");
     for (int i = 0; i < n_sizes; ++i)
         if (sizes[i] <= 0) return fail(ctx, kInvalidModel, "layer sizes must be positive");
@@ -313,7 +313,7 @@ int32_t dso_set_model(dso_ctx* ctx, const int32_t* sizes, int32_t n_sizes, const
     if (!is_default)
         return fail(ctx, kInvalidModel,
                     "device kernels implement the default topology 134-100-50-25-7 "
-                    "(default_layer_sizes, mlp.cpp:326) only");
+                    "(default_layer_sizes, mlp.cpp:177) only");
     Ctx& c = ctx->c;
     DSO_CUDA(ctx, cudaSetDevice(c.device));
     ModelDev& md = c.model;
@@ -357,7 +357,7 @@ int32_t dso_get_model(dso_ctx* ctx, double* W, double* b) {
 }
 
 int32_t dso_init_mlp(const int32_t* sizes, int32_t n, uint64_t seed, double* W, double* b) {
-    // init_mlp, mlp.cpp:333-356
+    // init_mlp, mlp.cpp:184-207
     if (!sizes || n < 2) return kInvalidModel;
     for (int i = 0; i < n; ++i)
         if (sizes[i] <= 0) return kInvalidModel;

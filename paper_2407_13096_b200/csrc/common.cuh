@@ -47,7 +47,7 @@ struct DomainDev {
 };
 
 // Device model: transposed, zero-padded weights for the FP32 MLP kernels.
-// Only the default topology 134-100-50-25-7 (mlp.cpp:326) runs on the fused
+// Only the default topology 134-100-50-25-7 (mlp.cpp:177) runs on the fused
 // kernels; other topologies are rejected by dso_set_model with InvalidModel
 // for the device path (the reference trains probe nets only in unit tests).
 struct ModelDev {
@@ -170,7 +170,7 @@ __device__ __forceinline__ float cost_f32(float eta, float K, float P, float T) 
     return __fmul_rn(fmaf(eta, P, K), T);
 }
 
-// sigmoid (mlp.cpp:166-168) in FP32: 1 / (1 + 2^(-z log2 e)) with the
+// sigmoid (mlp.cpp:17-20) in FP32: 1 / (1 + 2^(-z log2 e)) with the
 // approximate MUFU ex2/rcp (rel. error ~2^-22 each; no denormal fix-up code).
 __device__ __forceinline__ float sigmoidf_fast(float z) {
     float e, r;

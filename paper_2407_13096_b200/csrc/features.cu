@@ -3,7 +3,7 @@
 //
 // featurize (reference proj/src/ptx_features.cpp:311-329): per category
 // (instr 101 | dtype 17 | memspace 8) v[i] = count[i] / total, all-zero when
-// the category total is 0; as_vector (mlp.cpp:307-314) places the 8 DCGM
+// the category total is 0; as_vector (mlp.cpp:158-165) places the 8 DCGM
 // ratios first.  The reference computes count/total in double and we emit
 // float: for totals < 2^24 the correctly rounded FP32 quotient equals the
 // double quotient rounded to float (no double-rounding case exists when both

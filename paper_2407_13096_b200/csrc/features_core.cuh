@@ -2,7 +2,7 @@
 // the standalone featurize kernel and the fused pipeline.
 //
 // featurize (reference proj/src/ptx_features.cpp:311-329) + as_vector
-// (mlp.cpp:307-314): per category (instr 101 | dtype 17 | memspace 8)
+// (mlp.cpp:158-165): per category (instr 101 | dtype 17 | memspace 8)
 // v[i] = count[i] / total, all-zero for a zero total, DCGM ratios first.  The
 // reference divides in double; for totals < 2^24 the correctly rounded FP32
 // quotient equals that double rounded to float.  Tile layout:

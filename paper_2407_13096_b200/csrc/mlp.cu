@@ -1,9 +1,9 @@
 // mlp.cu — predictor inference and the fused pipeline (sm_100a).
 //
-// Predictor: the reference MLP 134-100-50-25-7 (proj/src/mlp.cpp:326), sigmoid
-// hidden layers, identity output (forward_trace mlp.cpp:171-181), output
-// de-standardised (forward_raw mlp.cpp:381-384) and clamped (predict_params
-// mlp.cpp:386-402, kBetaFloor mlp.cpp:15).
+// Predictor: the reference MLP 134-100-50-25-7 (proj/src/mlp.cpp:177), sigmoid
+// hidden layers, identity output (forward_trace mlp.cpp:22-32), output
+// de-standardised (forward_raw mlp.cpp:232-235) and clamped (predict_params
+// mlp.cpp:237-253, kBetaFloor mlp.cpp:15).
 //
 // Execution model — one persistent, warp-specialised CTA per SM (384 threads):
 //   * two CONSUMER groups of 4 warps (one warp per SM sub-partition each) run
@@ -322,7 +322,7 @@ __device__ __forceinline__ void consumer_tile(const float* W, float* act, float*
     PT_END(7, t_l4);
 }
 
-// predict_params clamp (mlp.cpp:390-399); returns the clamped flag.
+// predict_params clamp (mlp.cpp:241-250); returns the clamped flag.
 __device__ __forceinline__ bool clamp_params(float p[7]) {
     bool cl = false;
 #pragma unroll
@@ -340,7 +340,7 @@ __device__ __forceinline__ bool clamp_params(float p[7]) {
 
 // ---------------------------------------------------------------------------
 // Producer: feature stage of one 64-kernel tile into act (128 threads).
-// featurize (ptx_features.cpp:311-329) + as_vector (mlp.cpp:307-314): per
+// featurize (ptx_features.cpp:311-329) + as_vector (mlp.cpp:158-165): per
 // category count/total, correctly rounded in FP32 (equal to the reference's
 // double quotient rounded to float for totals < 2^24), FP64
 // division for larger totals, zeros for a zero total.

@@ -3,7 +3,7 @@
 Weights are kept in the reference layout (W_l of shape (sizes[l+1], sizes[l]),
 row-major, float64) so a model round-trips with the reference's model JSON
 (json_io.cpp:145-206).  init_mlp runs the library's host C++ restatement of
-mlp.cpp:333-356 (Glorot-uniform from the splitmix64 Rng).
+mlp.cpp:184-207 (Glorot-uniform from the splitmix64 Rng).
 """
 
 from __future__ import annotations
@@ -20,7 +20,7 @@ K_PARAMS = 7            # mlp.hpp:16
 
 
 def default_layer_sizes() -> list[int]:
-    """mlp.cpp:326."""
+    """mlp.cpp:177."""
     return [K_FUSED_FEATURES, 100, 50, 25, K_PARAMS]
 
 
@@ -60,7 +60,7 @@ def split_flat(sizes, W, b):
 
 
 def init_mlp(layer_sizes=None, seed: int = 0) -> MlpModel:
-    """init_mlp (mlp.cpp:333-356)."""
+    """init_mlp (mlp.cpp:184-207)."""
     sizes = list(default_layer_sizes() if layer_sizes is None else layer_sizes)
     arr = (C.c_int32 * len(sizes))(*sizes)
     nw = sum(sizes[l] * sizes[l + 1] for l in range(len(sizes) - 1))
@@ -80,7 +80,7 @@ def init_mlp(layer_sizes=None, seed: int = 0) -> MlpModel:
 
 
 def validate_model(m: MlpModel) -> None:
-    """validate(MlpModel), mlp.cpp:358-375."""
+    """validate(MlpModel), mlp.cpp:209-226."""
     s = list(m.layer_sizes)
     if len(s) < 2 or len(m.weights) != len(s) - 1 or len(m.biases) != len(m.weights):
         raise DsoError(ErrorKind.InvalidModel, "layer bookkeeping is inconsistent")

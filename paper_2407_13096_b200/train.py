@@ -1,12 +1,12 @@
 """Predictor training: data-parallel mini-batch SGD on the device model.
 
-Mirrors the reference's sgd_epoch / fit_model (proj/src/mlp.cpp:233-279):
+Mirrors the reference's sgd_epoch / fit_model (proj/src/mlp.cpp:84-130):
 targets standardized with the dataset's population mean/std (target_stats,
-mlp.cpp:206-228; zero-variance dims left unscaled), per-epoch order from
-shuffled_indices(Rng(seed).fork(0x5d0)) (mlp.cpp:236,272), contiguous batches
+mlp.cpp:57-79; zero-variance dims left unscaled), per-epoch order from
+shuffled_indices(Rng(seed).fork(0x5d0)) (mlp.cpp:87,123), contiguous batches
 in that order (last one partial), the loss of each batch taken on the
-pre-update weights (mlp.cpp:251-252), W -= lr * g (mlp.cpp:254-257), a NaN
-epoch loss stops training (mlp.cpp:276).
+pre-update weights (mlp.cpp:102-103), W -= lr * g (mlp.cpp:105-108), a NaN
+epoch loss stops training (mlp.cpp:126).
 
 Data parallel: every rank computes the batch-sum gradient of
 its shard of each global batch on the GPU (dso_train_grad), the sums are
@@ -27,7 +27,7 @@ from ._lib import lib
 
 
 def target_stats(targets):
-    """target_stats (mlp.cpp:206-228) on a [n, out] float64 array: population
+    """target_stats (mlp.cpp:57-79) on a [n, out] float64 array: population
     mean / std; zero-variance dims get mean 0, std 1 and are reported."""
     t = np.asarray(targets, np.float64)
     mean = t.mean(0)
@@ -87,7 +87,7 @@ class DataParallelTrainer:
         return t
 
     def step(self, x_local, y_local, n_local: int, global_batch: int, out_dim: int = 7):
-        """One synchronous step; returns the batch's mse_loss (mlp.cpp:408-412) on the
+        """One synchronous step; returns the batch's mse_loss (mlp.cpp:259-263) on the
         pre-update weights, as a 0-dim tensor on the device."""
         grad, loss = self.grad_fn(x_local, y_local, n_local)
         self.allreduce(grad)

@@ -1,5 +1,5 @@
 """GPU parity: predictor training step vs the oracle (analytic_gradients, mse_loss,
-sgd update — reference proj/src/mlp.cpp:233-289, 408-438).
+sgd update — reference proj/src/mlp.cpp:84-112, 259-289).
 
 FP32 on the device vs double in the oracle.  Tolerances:
 per-layer max |g_gpu - g_ref| <= 2e-5 * max|g_ref| (entries summed over the
