@@ -10,7 +10,7 @@
 //     the MLP on alternate tiles of 64 kernels held k-major in shared memory
 //     (act[134][64]); each layer is a
 //     register-tiled FP32 GEMM on the FMA pipe with Blackwell's packed FFMA2
-//     (L1: thread = 2 kernels x 26 neurons, 26 FFMA2 per 8 shared loads;
+//     (L1: thread = 4 kernels x 13 neurons, 26 FFMA2 per 5 shared loads;
 //     weights are warp-uniform broadcasts; operands of step k+1 in flight
 //     while step k issues); layer outputs overwrite act in place;
 //   * 4 PRODUCER warps, meanwhile, (a) finish the oldest tile: clamp, then
@@ -30,6 +30,8 @@
 // contract on the predicted parameters.
 #include <math.h>
 
+#include <cmath>
+#include <cstring>
 #include <vector>
 
 #include "common.cuh"
@@ -61,18 +63,37 @@ static_assert(kProducers * kProducerRegs + kConsumers * kConsumerRegs <= 65536, 
 // Named barriers (0 is __syncthreads).
 constexpr int BAR_PROD = 1, BAR_CONS0 = 2, BAR_FULL0 = 4, BAR_READY0 = 7;
 
-// Packed model (floats), k-major, one neuron group per consumer warp g (0..3):
-//   L1 [134][4][28] (26 used, n = 26g + t)   L2 [100][4][16] (13 used, n = 13g + t)
-//   L3 [50][4][8]   (7 used,  n = 7g + t)    L4 [25][8]      (n = 2g + t, t < 2)
+// Packed model (floats), k-major.  Consumer warp g (0..3) of a group owns a
+// neuron block; inside it lane = 2*mg + ng: kernel quad mg (kernels 4mg..4mg+3)
+// x neuron half ng, so a warp's loads are 16 distinct activation quads (each
+// read by a lane pair) and 2 distinct weight vectors — both cost one
+// shared-memory wavefront per 128 bytes (a warp-uniform load costs one per 8).
+//   L1 [134][4][2][16] (13 used, n = 26g + 13ng + t)
+//   L2 [100][4][2][8]  (7 used,  n = 14g + 7ng + t; 56 slots for 50)
+//   L3 [50][4][8]      (7 used,  n = 7g + t; lane = kernel pair)
+//   L4 [25][8]         (n = 2g + t, t < 2)
 constexpr int W1S = 0;
-constexpr int W2S = W1S + 134 * 112;
+constexpr int W2S = W1S + 134 * 128;
 constexpr int W3S = W2S + 100 * 64;
 constexpr int W4S = W3S + 50 * 32;
-constexpr int B1S = W4S + 25 * 8;        // [104]
-constexpr int B2S = B1S + 104;           // [52]
-constexpr int B3S = B2S + 52;            // [28]
+constexpr int B1S = W4S + 25 * 8;        // [104] by neuron
+constexpr int B2S = B1S + 104;           // [56]
+constexpr int B3S = B2S + 56;            // [28]
 constexpr int B4S = B3S + 28;            // [8]
-constexpr int kModelFloats = B4S + 8;    // 23400
+constexpr int FLAGW = B4S + 8;           // int: count of non-finite W1 entries
+constexpr int kModelFloats = FLAGW + 4;  // 25552
+__host__ __device__ __forceinline__ int pk_w1(int nn, int k) {
+    const int g = nn / 26, r = nn % 26;
+    return W1S + k * 128 + g * 32 + (r / 13) * 16 + r % 13;
+}
+__host__ __device__ __forceinline__ int pk_w2(int nn, int k) {
+    const int g = nn / 14, r = nn % 14;
+    return W2S + k * 64 + g * 16 + (r / 7) * 8 + r % 7;
+}
+__host__ __device__ __forceinline__ int pk_w3(int nn, int k) {
+    return W3S + k * 32 + (nn / 7) * 8 + nn % 7;
+}
+__host__ __device__ __forceinline__ int pk_w4(int nn, int k) { return W4S + k * 8 + nn; }
 // per-CTA shared memory beyond the model
 constexpr int ACT = kModelFloats;           // act[3][134][RS]
 constexpr int kActFloats = 134 * RS;
@@ -80,12 +101,20 @@ constexpr int OUT = ACT + kBufs * kActFloats;  // out[3][8][RS]  (raw prediction
 constexpr int kOutFloats = 8 * RS;
 constexpr int SCR = OUT + kBufs * kOutFloats;   // producer scratch: tf[3][64] rr[3][64]
 constexpr int kScrFloats = 6 * TM + 6 * TM;  // tf[3][64], rr[3][64] + part u64[3][64]
+static_assert(kScrFloats >= 3 * TPK * TM, "sweep merge scratch");
 constexpr int STATS = SCR + kScrFloats;     // mean[8] std[8]
 constexpr int MBAR = STATS + 16;            // 3 mbarriers (u64) for the bulk tile loads
-constexpr int TABLES = MBAR + 8;            // core4[nc], mem2[nm]
+// L1 input-row lists, one per buffer: u16 row indices (pairs packed per u32),
+// the rows of the tile that are not all zero (plus one zero row to make the
+// count even); the count per buffer; the producer's row mask under assembly.
+constexpr int ROWS = MBAR + 8;              // u32 [3][68]
+constexpr int kRowWords = 68;
+constexpr int ROWCNT = ROWS + kBufs * kRowWords;  // int [3] (+1 pad)
+constexpr int MASKW = ROWCNT + 4;           // u32 [4]: slots 0..125 present in the tile
+constexpr int TABLES = MASKW + 4;           // core4[nc], mem2[nm]
 static_assert(W2S % 4 == 0 && W3S % 4 == 0 && W4S % 4 == 0 && B1S % 4 == 0 &&
                   kModelFloats % 4 == 0 && ACT % 4 == 0 && OUT % 4 == 0 && SCR % 4 == 0 &&
-                  MBAR % 2 == 0 && TABLES % 4 == 0,
+                  MBAR % 2 == 0 && ROWS % 4 == 0 && TABLES % 4 == 0,
               "16-byte alignment of smem regions");
 
 // master (reference) layout offsets: W1 | W2 | W3 | W4 | b1 | b2 | b3 | b4
@@ -125,99 +154,117 @@ __device__ __forceinline__ void bar_arrive(int id, int count) {
 // FMA pipe, so latency is covered by ILP (26 independent accumulator pairs in
 // L1), not by other warps.  Weights are warp-uniform -> shared-memory
 // broadcasts; an activation pair load is 256 contiguous bytes per warp.
-__device__ __forceinline__ void consumer_tile(const float* W, float* act, float* out, int ct,
-                                              int cbar) {
+__device__ __forceinline__ void consumer_tile(const float* W, float* act, float* out,
+                                              const uint32_t* rows, int nrows, int ct, int cbar) {
     float2* act2 = reinterpret_cast<float2*>(act);  // [row][32] kernel pairs
     const int mp = ct & 31;
     const int g = ct >> 5;
-    // ---- L1: 134 -> 100 (neurons 26g .. 26g+25), pairs along n -------------
+    const int ng = ct & 1, mg = (ct >> 1) & 15;  // neuron half, kernel quad
+    const float4* act4 = reinterpret_cast<const float4*>(act) + mg;  // row k at act4[k * RS4]
+    float4* act4w = reinterpret_cast<float4*>(act) + mg;
+    constexpr int RS4 = RS / 4;
+    // ---- L1: 134 -> 100; thread = 4 kernels x 13 neurons (26g + 13ng + t) -------
+    // two k-steps per pipeline stage: 52 FFMA2 between a load and its use
     {
-        float2 acc0[13], acc1[13];
+        float2 acc0[13], acc1[13];  // kernels (4mg, 4mg+1), (4mg+2, 4mg+3)
 #pragma unroll
-        for (int p = 0; p < 13; ++p) acc0[p] = acc1[p] = f2(0.f, 0.f);
-        const float* wbase = W + W1S + g * 28;
+        for (int t = 0; t < 13; ++t) acc0[t] = acc1[t] = f2(0.f, 0.f);
+        const float* wbase = W + W1S + g * 32 + ng * 16;
         struct Op {
-            float2 a;
-            float4 v[6];
-            float2 l;
+            float4 a[2];
+            float4 v[2][3];
+            float l[2];
         };
-        auto load = [&](Op& o, int k) {
-            const float* w = wbase + k * 112;
-            o.a = act2[k * RS2 + mp];
+        // j indexes the tile's row list (two rows per u32): only input rows that
+        // are non-zero somewhere in the tile are visited.  Skipping an all-zero
+        // row is exact: fma(+0, w, acc) == acc for finite w (FLAGW guards it).
+        auto load = [&](Op& o, int j) {
+            const uint32_t rr = rows[j >> 1];
 #pragma unroll
-            for (int q = 0; q < 6; ++q) o.v[q] = reinterpret_cast<const float4*>(w)[q];
-            o.l = reinterpret_cast<const float2*>(w)[12];
+            for (int u = 0; u < 2; ++u) {
+                const int k = u ? (int)(rr >> 16) : (int)(rr & 0xFFFFu);
+                const float* w = wbase + k * 128;
+                o.a[u] = act4[k * RS4];
+#pragma unroll
+                for (int q = 0; q < 3; ++q) o.v[u][q] = reinterpret_cast<const float4*>(w)[q];
+                o.l[u] = w[12];
+            }
         };
         auto math = [&](const Op& o) {
-            float2 w[13];
 #pragma unroll
-            for (int q = 0; q < 6; ++q) {
-                w[2 * q] = f2(o.v[q].x, o.v[q].y);
-                w[2 * q + 1] = f2(o.v[q].z, o.v[q].w);
-            }
-            w[12] = o.l;
+            for (int u = 0; u < 2; ++u) {
+                const float w[13] = {o.v[u][0].x, o.v[u][0].y, o.v[u][0].z, o.v[u][0].w,
+                                     o.v[u][1].x, o.v[u][1].y, o.v[u][1].z, o.v[u][1].w,
+                                     o.v[u][2].x, o.v[u][2].y, o.v[u][2].z, o.v[u][2].w,
+                                     o.l[u]};
+                const float2 a01 = f2(o.a[u].x, o.a[u].y), a23 = f2(o.a[u].z, o.a[u].w);
 #pragma unroll
-            for (int p = 0; p < 13; ++p) {
-                acc0[p] = ffma2(f2(o.a.x, o.a.x), w[p], acc0[p]);
-                acc1[p] = ffma2(f2(o.a.y, o.a.y), w[p], acc1[p]);
+                for (int t = 0; t < 13; ++t) {
+                    acc0[t] = ffma2(a01, f2(w[t], w[t]), acc0[t]);
+                    acc1[t] = ffma2(a23, f2(w[t], w[t]), acc1[t]);
+                }
             }
         };
         PT_BEGIN(t_l1);
         Op A, B;
         load(A, 0);
+        int j = 0;  // nrows is even and >= 2
 #pragma unroll 1
-        for (int k = 0; k < 134; k += 2) {
-            load(B, k + 1);
+        for (; j + 4 <= nrows; j += 4) {
+            load(B, j + 2);
             math(A);
-            load(A, k + 2 < 134 ? k + 2 : 133);
+            load(A, j + 4 < nrows ? j + 4 : nrows - 2);
             math(B);
         }
+        if (j < nrows) math(A);  // j == nrows - 2
         PT_END(1, t_l1);
         PT_BEGIN(t_e1);
         bar_sync(cbar, kGroupThreads);  // all reads of act done
-        const float* b = W + B1S + g * 26;
+        const int n0 = g * 26 + ng * 13;
 #pragma unroll
-        for (int p = 0; p < 13; ++p) {
-            const int n = g * 26 + 2 * p;
-            const float b0 = b[2 * p], b1 = b[2 * p + 1];
-            act2[n * RS2 + mp] = f2(sigmoidf_fast(acc0[p].x + b0), sigmoidf_fast(acc1[p].x + b0));
-            act2[(n + 1) * RS2 + mp] =
-                f2(sigmoidf_fast(acc0[p].y + b1), sigmoidf_fast(acc1[p].y + b1));
+        for (int t = 0; t < 13; ++t) {
+            const float bb = W[B1S + n0 + t];
+            if (n0 + t < 100)
+                act4w[(n0 + t) * RS4] =
+                    make_float4(sigmoidf_fast(acc0[t].x + bb), sigmoidf_fast(acc0[t].y + bb),
+                                sigmoidf_fast(acc1[t].x + bb), sigmoidf_fast(acc1[t].y + bb));
         }
         bar_sync(cbar, kGroupThreads);
         PT_END(2, t_e1);
     }
-    // ---- L2: 100 -> 50 (neurons 13g .. 13g+12), pairs along m ----------------
-    // two k-steps per pipeline stage (26 FFMA2 per stage cover the load latency)
+    // ---- L2: 100 -> 50; thread = 4 kernels x 7 neurons (14g + 7ng + t) -----------
     {
-        float2 acc[13];
+        float2 acc0[7], acc1[7];
 #pragma unroll
-        for (int t = 0; t < 13; ++t) acc[t] = f2(0.f, 0.f);
-        const float* wbase = W + W2S + g * 16;
+        for (int t = 0; t < 7; ++t) acc0[t] = acc1[t] = f2(0.f, 0.f);
+        const float* wbase = W + W2S + g * 16 + ng * 8;
         struct Op {
-            float2 a[2];
-            float4 v0[2], v1[2], v2[2];
-            float v3[2];
+            float4 a[2];
+            float4 v[2];
+            float2 x[2];
+            float l[2];
         };
         auto load = [&](Op& o, int k) {
 #pragma unroll
             for (int u = 0; u < 2; ++u) {
                 const float* w = wbase + (k + u) * 64;
-                o.a[u] = act2[(k + u) * RS2 + mp];
-                o.v0[u] = reinterpret_cast<const float4*>(w)[0];
-                o.v1[u] = reinterpret_cast<const float4*>(w)[1];
-                o.v2[u] = reinterpret_cast<const float4*>(w)[2];
-                o.v3[u] = w[12];
+                o.a[u] = act4[(k + u) * RS4];
+                o.v[u] = reinterpret_cast<const float4*>(w)[0];
+                o.x[u] = reinterpret_cast<const float2*>(w)[2];
+                o.l[u] = w[6];
             }
         };
         auto math = [&](const Op& o) {
 #pragma unroll
             for (int u = 0; u < 2; ++u) {
-                const float w[13] = {o.v0[u].x, o.v0[u].y, o.v0[u].z, o.v0[u].w, o.v1[u].x,
-                                     o.v1[u].y, o.v1[u].z, o.v1[u].w, o.v2[u].x, o.v2[u].y,
-                                     o.v2[u].z, o.v2[u].w, o.v3[u]};
+                const float w[7] = {o.v[u].x, o.v[u].y, o.v[u].z, o.v[u].w,
+                                    o.x[u].x, o.x[u].y, o.l[u]};
+                const float2 a01 = f2(o.a[u].x, o.a[u].y), a23 = f2(o.a[u].z, o.a[u].w);
 #pragma unroll
-                for (int t = 0; t < 13; ++t) acc[t] = ffma2(o.a[u], f2(w[t], w[t]), acc[t]);
+                for (int t = 0; t < 7; ++t) {
+                    acc0[t] = ffma2(a01, f2(w[t], w[t]), acc0[t]);
+                    acc1[t] = ffma2(a23, f2(w[t], w[t]), acc1[t]);
+                }
             }
         };
         PT_BEGIN(t_l2);
@@ -233,12 +280,14 @@ __device__ __forceinline__ void consumer_tile(const float* W, float* act, float*
         PT_END(3, t_l2);
         PT_BEGIN(t_e2);
         bar_sync(cbar, kGroupThreads);
-        const float* b = W + B2S + g * 13;
+        const int n0 = g * 14 + ng * 7;
 #pragma unroll
-        for (int t = 0; t < 13; ++t) {
-            const float bb = b[t];
-            act2[(g * 13 + t) * RS2 + mp] =
-                f2(sigmoidf_fast(acc[t].x + bb), sigmoidf_fast(acc[t].y + bb));
+        for (int t = 0; t < 7; ++t) {
+            const float bb = W[B2S + n0 + t];
+            if (n0 + t < 50)
+                act4w[(n0 + t) * RS4] =
+                    make_float4(sigmoidf_fast(acc0[t].x + bb), sigmoidf_fast(acc0[t].y + bb),
+                                sigmoidf_fast(acc1[t].x + bb), sigmoidf_fast(acc1[t].y + bb));
         }
         bar_sync(cbar, kGroupThreads);
         PT_END(4, t_e2);
@@ -590,6 +639,43 @@ __device__ __forceinline__ void csr_prefetch(const Job& J, int64_t t0, int pt, C
     }
 }
 
+// L1 row list of one tile (see ROWS): the 8 DCGM rows, then every count row
+// whose slot is set in maskw, in increasing order, padded to an even count with
+// an all-zero row.  identity: all 134 rows (dense/fused input, or non-finite
+// W1, where skipping would not be exact).  Threads pt < 135 take part.
+__device__ __forceinline__ void build_row_list(uint32_t* rows, int* cnt, const uint32_t* maskw,
+                                               bool identity, int pt) {
+    uint16_t* r16 = reinterpret_cast<uint16_t*>(rows);
+    if (identity) {
+        if (pt < DSO_FUSED_ROWS) r16[pt] = (uint16_t)pt;
+        if (pt == DSO_FUSED_ROWS) *cnt = DSO_FUSED_ROWS;
+        return;
+    }
+    const uint32_t m0 = maskw[0], m1 = maskw[1], m2 = maskw[2], m3 = maskw[3] & 0x3FFFFFFFu;
+    if (pt < 8) {
+        r16[pt] = (uint16_t)pt;
+    } else if (pt < DSO_FUSED_ROWS) {
+        const int slot = pt - 8, w = slot >> 5;
+        const uint32_t word = w == 0 ? m0 : (w == 1 ? m1 : (w == 2 ? m2 : m3));
+        if ((word >> (slot & 31)) & 1u) {
+            const uint32_t below = word & ((1u << (slot & 31)) - 1u);
+            const int pos = 8 + __popc(below) + (w > 0 ? __popc(m0) : 0) +
+                            (w > 1 ? __popc(m1) : 0) + (w > 2 ? __popc(m2) : 0);
+            r16[pos] = (uint16_t)pt;
+        }
+    } else if (pt == DSO_FUSED_ROWS) {
+        int n = 8 + __popc(m0) + __popc(m1) + __popc(m2) + __popc(m3);
+        if (n & 1) {  // pad with the first absent slot (exists: n <= 133)
+            const int s0 = ~m0 ? __ffs(~m0) - 1
+                         : ~m1 ? 32 + __ffs(~m1) - 1
+                         : ~m2 ? 64 + __ffs(~m2) - 1
+                               : 96 + __ffs(~m3) - 1;
+            r16[n++] = (uint16_t)(8 + s0);
+        }
+        *cnt = n;
+    }
+}
+
 __device__ __forceinline__ int cat_of_row(int r) {
     return r < DSO_INSTR_SLOTS ? 0 : (r < DSO_INSTR_SLOTS + DSO_DTYPE_SLOTS ? 1 : 2);
 }
@@ -597,7 +683,9 @@ __device__ __forceinline__ int cat_of_row(int r) {
 
 __device__ __forceinline__ void csr_features(float* act, float* scr, const Job& J, int64_t t0,
                                              int pt, const CsrPrefetch& P, bool dcgm_issued,
-                                             uint64_t* mbar, uint32_t& parbits, int bit) {
+                                             uint64_t* mbar, uint32_t& parbits, int bit,
+                                             uint32_t* rows, int* rcnt, uint32_t* maskw,
+                                             bool skip_ok) {
     uint32_t* acti = reinterpret_cast<uint32_t*>(act);
     const int m = pt / TPK, sub = pt % TPK;
     // zero-fill the count rows (8..133); DCGM rows arrive by bulk copy or here
@@ -605,6 +693,7 @@ __device__ __forceinline__ void csr_features(float* act, float* scr, const Job& 
         float4* z = reinterpret_cast<float4*>(act + 8 * RS);
         for (int i = pt; i < DSO_COUNT_ROWS * RS / 4; i += kProducers)
             z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (pt < 4) maskw[pt] = 0u;
         if (!dcgm_issued) {
             const int mm = pt & 63, h = pt >> 6;
             const int64_t k = t0 + mm;
@@ -615,11 +704,18 @@ __device__ __forceinline__ void csr_features(float* act, float* scr, const Job& 
     bar_sync(BAR_PROD, kProducers);
     // pass 1: scatter-add counts, category totals
     uint64_t tot[3] = {0, 0, 0};
+    uint32_t mk0 = 0, mk1 = 0, mk2 = 0, mk3 = 0;  // slots with a non-zero count
     auto scatter = [&](uint32_t e) {
         const int slot = (int)(e & 127u);
         const uint32_t c = e >> 7;
         if (slot < DSO_COUNT_ROWS) {
             atomicAdd(acti + (8 + slot) * RS + m, c);
+            const uint32_t bitv = c ? 1u << (slot & 31) : 0u;
+            const int w = slot >> 5;
+            mk0 |= w == 0 ? bitv : 0u;
+            mk1 |= w == 1 ? bitv : 0u;
+            mk2 |= w == 2 ? bitv : 0u;
+            mk3 |= w == 3 ? bitv : 0u;
             const int cat = cat_of_row(slot);  // selects, not a dynamic index
             tot[0] += cat == 0 ? c : 0u;
             tot[1] += cat == 1 ? c : 0u;
@@ -635,6 +731,16 @@ __device__ __forceinline__ void csr_features(float* act, float* scr, const Job& 
     for (int c = 0; c < 3; ++c)
 #pragma unroll
         for (int off = 1; off < TPK; off <<= 1) tot[c] += __shfl_xor_sync(0xffffffffu, tot[c], off);
+    mk0 = __reduce_or_sync(0xffffffffu, mk0);
+    mk1 = __reduce_or_sync(0xffffffffu, mk1);
+    mk2 = __reduce_or_sync(0xffffffffu, mk2);
+    mk3 = __reduce_or_sync(0xffffffffu, mk3);
+    if ((pt & 31) == 0) {
+        if (mk0) atomicOr(maskw + 0, mk0);
+        if (mk1) atomicOr(maskw + 1, mk1);
+        if (mk2) atomicOr(maskw + 2, mk2);
+        if (mk3) atomicOr(maskw + 3, mk3);
+    }
     float tf[3], rr[3];
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
@@ -657,6 +763,7 @@ __device__ __forceinline__ void csr_features(float* act, float* scr, const Job& 
     }
     // (a barrier: every atomic and scale is in place)
     const bool any_spill = prod_any(P.cnt > TPK * kCsrRegs);
+    build_row_list(rows, rcnt, maskw, !skip_ok, pt);  // the mask is complete here
     if (!any_spill) {
         // pass 2 (common case): read the summed counts of this thread's slots, then
         // overwrite them with the fractions (a slot listed twice gets the same
@@ -704,12 +811,16 @@ __device__ __forceinline__ void csr_features(float* act, float* scr, const Job& 
 }
 
 // Producer: finish a tile from its raw predictions in out: clamp and either
-// write the parameters (predict) or sweep the grid (pipeline).  2 threads per
-// kernel, each half of the core levels, merged with one shuffle.
+// write the parameters (predict) or sweep the grid (pipeline).  TPK threads per
+// kernel, each a contiguous quarter of the core levels.  Thread pt takes kernel
+// pt % 64 and quarter pt / 64, so a warp's 32 lanes read the SAME core-level
+// entry (a broadcast, not a 4-way bank conflict per quarter-warp); the quarters
+// meet through the producer scratch (free here: the feature stage that uses it
+// is ordered before and after by producer barriers).
 template <bool PIPE>
 __device__ __forceinline__ void produce_results(const float* sm, const float* out, const Job& J,
                                                 int64_t t0, int pt) {
-    const int m = pt / TPK, qtr = pt % TPK;  // TPK threads per kernel
+    const int m = pt % TM, qtr = pt / TM;
     const int64_t k = t0 + m;
     float pr[7];
 #pragma unroll
@@ -733,9 +844,8 @@ __device__ __forceinline__ void produce_results(const float* sm, const float* ou
     const int nc = J.nc, nm = J.nm;
     // part qtr sweeps core levels [i_lo, i_hi): contiguous parts in visit order
     const int i_lo = nc * qtr / TPK, i_hi = nc * (qtr + 1) / TPK;
-    Best b{__int_as_float(0x7fc00000), __int_as_float(0x7fc00000), i_lo * nm};
-    const bool empty = !(i_lo < i_hi);
-    if (!empty) {
+    Best b{__int_as_float(0x7fc00000), __int_as_float(0x7fc00000), -1};  // i = -1: empty part
+    if (i_lo < i_hi) {
         if (nm == 4)
             b = sweep_levels<4>(p, s_core, s_mem, 4, i_lo, i_hi, J.eta, J.K);
         else if (nm == 1)
@@ -746,30 +856,37 @@ __device__ __forceinline__ void produce_results(const float* sm, const float* ou
             b = sweep_levels<0>(p, s_core, s_mem, nm, i_lo, i_hi, J.eta, J.K);
     }
     // merge the quarters (merge_best is exact in any order: ties use the index)
-    bool emp = empty;
+    float* xc = const_cast<float*>(sm) + SCR;  // [TPK][64] cost, energy, index
+    float* xe = xc + TPK * TM;
+    int* xi = reinterpret_cast<int*>(xe + TPK * TM);
+    xc[qtr * TM + m] = b.c;
+    xe[qtr * TM + m] = b.e;
+    xi[qtr * TM + m] = b.i;
+    bar_sync(BAR_PROD, kProducers);
+    Best r{0.f, 0.f, -1};
 #pragma unroll
-    for (int off = 1; off < TPK; off <<= 1) {
-        Best o;
-        o.c = __shfl_xor_sync(0xffffffffu, b.c, off);
-        o.e = __shfl_xor_sync(0xffffffffu, b.e, off);
-        o.i = __shfl_xor_sync(0xffffffffu, b.i, off);
-        const bool oemp = __shfl_xor_sync(0xffffffffu, (int)emp, off) != 0;
-        if (emp) {
-            if (!oemp) b = o;
-        } else if (!oemp) {
-            merge_best(b, o);
-        }
-        emp = emp && oemp;
+    for (int q = 0; q < TPK; ++q) {
+        const Best o{xc[q * TM + m], xe[q * TM + m], xi[q * TM + m]};
+        if (o.i < 0) continue;
+        if (r.i < 0)
+            r = o;
+        else
+            merge_best(r, o);
     }
-    if (qtr == 0 && k < J.n) {
-        J.idx[k] = b.i;
-        if (J.cost) J.cost[k] = b.c;
-        if (J.energy) J.energy[k] = b.e;
-        if (J.time) J.time[k] = time_at(p, s_core, s_mem, nm, b.i);
-        if (J.params)
+    if (k < J.n) {
+        // output duties split over the quarters
+        if (qtr == 0) {
+            J.idx[k] = r.i;
+            if (J.cost) J.cost[k] = r.c;
+        } else if (qtr == 1) {
+            if (J.energy) J.energy[k] = r.e;
+            if (J.clamped) J.clamped[k] = cl ? 1 : 0;
+        } else if (qtr == 2) {
+            if (J.time) J.time[k] = time_at(p, s_core, s_mem, nm, r.i);
+        } else if (J.params) {
 #pragma unroll
             for (int i = 0; i < 7; ++i) J.params[i * J.ld_out + k] = pr[i];
-        if (J.clamped) J.clamped[k] = cl ? 1 : 0;
+        }
     }
 }
 
@@ -821,8 +938,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             PT_BEGIN(t_w);
             bar_sync(BAR_FULL0 + b, kHandoff);  // features in act[b]; out[b] free
             PT_END(0, t_w);
-            consumer_tile(sm, sm + ACT + b * kActFloats, sm + OUT + b * kOutFloats, ct,
-                          BAR_CONS0 + G);
+            consumer_tile(sm, sm + ACT + b * kActFloats, sm + OUT + b * kOutFloats,
+                          reinterpret_cast<const uint32_t*>(sm + ROWS) + b * kRowWords,
+                          reinterpret_cast<const int*>(sm + ROWCNT)[b], ct, BAR_CONS0 + G);
             bar_arrive(BAR_READY0 + b, kHandoff);  // predictions in out[b]; act[b] free
         }
     } else {
@@ -837,6 +955,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                : (((J.ld & 3) == 0) && ((reinterpret_cast<uintptr_t>(J.fused) & 15) == 0));
         uint64_t* mbar = reinterpret_cast<uint64_t*>(sm + MBAR);
         uint32_t parbits = 0u;  // mbarrier phase bit per buffer
+        const bool skip_ok = reinterpret_cast<const int*>(sm)[FLAGW] == 0;  // W1 all finite
         CsrPrefetch P;                             // CSR: entries of the tile being prefetched
         auto t0_of = [&](int64_t i) { return (blockIdx.x + i * gridDim.x) * (int64_t)TM; };
         auto issue = [&](int64_t i) -> bool {
@@ -855,13 +974,17 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int b = (int)(i % kBufs);
             float* act = sm + ACT + b * kActFloats;
             PT_BEGIN(t_f);
+            uint32_t* rows = reinterpret_cast<uint32_t*>(sm + ROWS) + b * kRowWords;
+            int* rcnt = reinterpret_cast<int*>(sm + ROWCNT) + b;
             if (MODE == MODE_DENSE)
                 produce_features(act, scr, J.counts, J.dcgm, t0_of(i), J.n, J.ld, issued,
                                  mbar + b, parbits, b, pt);
             else if (MODE == MODE_CSR)
-                csr_features(act, scr, J, t0_of(i), pt, P, issued, mbar + b, parbits, b);
+                csr_features(act, scr, J, t0_of(i), pt, P, issued, mbar + b, parbits, b, rows,
+                             rcnt, reinterpret_cast<uint32_t*>(sm + MASKW), skip_ok);
             else
                 produce_fused(act, J.fused, t0_of(i), J.n, J.ld, vec_ok, pt);
+            if (MODE != MODE_CSR) build_row_list(rows, rcnt, nullptr, true, pt);
             PT_END(10, t_f);
             bar_arrive(BAR_FULL0 + b, kHandoff);
         };
@@ -888,16 +1011,17 @@ __global__ void repack_kernel(const float* __restrict__ master, float* __restric
     const int e = blockIdx.x * blockDim.x + threadIdx.x;
     if (e < MW2) {
         const int nn = e / 134, k = e - nn * 134;
-        pk[W1S + k * 112 + (nn / 26) * 28 + nn % 26] = master[e];
+        pk[pk_w1(nn, k)] = master[e];
+        if (!isfinite(master[e])) atomicAdd(reinterpret_cast<int*>(pk + FLAGW), 1);
     } else if (e < MW3) {
         const int f = e - MW2, nn = f / 100, k = f - nn * 100;
-        pk[W2S + k * 64 + (nn / 13) * 16 + nn % 13] = master[e];
+        pk[pk_w2(nn, k)] = master[e];
     } else if (e < MW4) {
         const int f = e - MW3, nn = f / 50, k = f - nn * 50;
-        pk[W3S + k * 32 + (nn / 7) * 8 + nn % 7] = master[e];
+        pk[pk_w3(nn, k)] = master[e];
     } else if (e < MB1) {
         const int f = e - MW4, nn = f / 25, k = f - nn * 25;
-        pk[W4S + k * 8 + nn] = master[e];
+        pk[pk_w4(nn, k)] = master[e];
     } else if (e < MB2) {
         pk[B1S + e - MB1] = master[e];
     } else if (e < MB3) {
@@ -964,15 +1088,18 @@ cudaError_t model_upload(Ctx& cx, const double* W, const double* b) {
     std::vector<float> pk(kModelFloats, 0.f);
     for (int nn = 0; nn < 100; ++nn)
         for (int k = 0; k < 134; ++k)
-            pk[W1S + k * 112 + (nn / 26) * 28 + nn % 26] = (float)W[MW1 + nn * 134 + k];
+            pk[pk_w1(nn, k)] = (float)W[MW1 + nn * 134 + k];
     for (int nn = 0; nn < 50; ++nn)
         for (int k = 0; k < 100; ++k)
-            pk[W2S + k * 64 + (nn / 13) * 16 + nn % 13] = (float)W[MW2 + nn * 100 + k];
+            pk[pk_w2(nn, k)] = (float)W[MW2 + nn * 100 + k];
     for (int nn = 0; nn < 25; ++nn)
         for (int k = 0; k < 50; ++k)
-            pk[W3S + k * 32 + (nn / 7) * 8 + nn % 7] = (float)W[MW3 + nn * 50 + k];
+            pk[pk_w3(nn, k)] = (float)W[MW3 + nn * 50 + k];
     for (int nn = 0; nn < 7; ++nn)
-        for (int k = 0; k < 25; ++k) pk[W4S + k * 8 + nn] = (float)W[MW4 + nn * 25 + k];
+        for (int k = 0; k < 25; ++k) pk[pk_w4(nn, k)] = (float)W[MW4 + nn * 25 + k];
+    int nonfinite = 0;
+    for (int e = 0; e < MW2; ++e) nonfinite += std::isfinite((float)W[MW1 + e]) ? 0 : 1;
+    memcpy(&pk[FLAGW], &nonfinite, sizeof(int));
     for (int i = 0; i < 100; ++i) pk[B1S + i] = (float)b[i];
     for (int i = 0; i < 50; ++i) pk[B2S + i] = (float)b[100 + i];
     for (int i = 0; i < 25; ++i) pk[B3S + i] = (float)b[150 + i];
@@ -988,6 +1115,8 @@ cudaError_t model_upload(Ctx& cx, const double* W, const double* b) {
 }
 
 cudaError_t launch_repack(Ctx& cx) {
+    cudaError_t e = cudaMemsetAsync(cx.model.wt + FLAGW, 0, sizeof(int), cx.stream);
+    if (e != cudaSuccess) return e;
     repack_kernel<<<(kMasterFloats + 255) / 256, 256, 0, cx.stream>>>(cx.model.w_master,
                                                                       cx.model.wt);
     ++cx.launches;

@@ -194,3 +194,31 @@ def test_pipeline_csr_host_large(ctx, port):
                                 s["dcgm"].cpu().pin_memory(), 0.8, want_params=True)
     for f in ("idx", "cost", "energy", "time", "params", "clamped"):
         np.testing.assert_array_equal(host_out[f].numpy(), dev_out[f].cpu().numpy())
+
+
+def test_pipeline_csr_nonfinite_weight_disables_row_skipping(ctx, port):
+    """The CSR path skips all-zero input rows of a tile (exact for finite W1).
+    An infinite W1 entry on an absent slot makes the reference's product
+    inf * 0 = NaN, so the skip must switch off: CSR == dense, NaNs included."""
+    dom = config_domain("c3")
+    ctx.set_domain(dom)
+    m = stats_model(port)
+    n = 4096 + 5
+    d = ctx.gen_synthetic(n, root=53, params=False)
+    counts = d["counts"].cpu().numpy().T.view(np.uint32)
+    absent = int(np.flatnonzero(counts.sum(axis=0) == 0)[0])  # a slot no kernel uses
+    m.weights[0] = m.weights[0].copy()
+    m.weights[0][3, 8 + absent] = np.inf  # neuron 3, fused row 8 + slot
+    ctx.set_model(m)
+    s = ctx.gen_synthetic_csr(n, root=53)
+    a = ctx.pipeline(d["counts"], d["dcgm"], 0.8, want_params=True)
+    b = ctx.pipeline_csr(s["row_ptr"], s["entries"], s["dcgm"], 0.8, want_params=True)
+    assert np.isnan(a["params"].cpu().numpy()).any() or (a["clamped"].cpu().numpy() != 0).any()
+    for f in ("idx", "cost", "energy", "time", "params", "clamped"):
+        np.testing.assert_array_equal(a[f].cpu().numpy(), b[f].cpu().numpy())
+    # finite again: skipping back on, still equal
+    ctx.set_model(stats_model(port))
+    a = ctx.pipeline(d["counts"], d["dcgm"], 0.8, want_params=True)
+    b = ctx.pipeline_csr(s["row_ptr"], s["entries"], s["dcgm"], 0.8, want_params=True)
+    for f in ("idx", "cost", "energy", "time", "params", "clamped"):
+        np.testing.assert_array_equal(a[f].cpu().numpy(), b[f].cpu().numpy())
