@@ -69,6 +69,11 @@ const char* dso_last_error(const dso_ctx* ctx);
 const char* dso_status_name(int32_t status);
 /* Number of device kernel launches issued on ctx so far (evidence counter). */
 int64_t dso_launch_count(const dso_ctx* ctx);
+/* Tuning / verification switches (no reference counterpart; results never
+ * depend on them).  key "fast_sweep": 1 (default) lets the FP32 sweeps use the
+ * group-minimum argmin (bit-identical, see sweep_core.cuh), 0 forces the
+ * pair-by-pair lexicographic scan.  Unknown key -> InvalidArgument. */
+int32_t dso_set_option(dso_ctx* ctx, const char* key, int64_t value);
 
 /* ---- domain: replaces the DvfsDomain argument + validate(DvfsDomain) ------
  * optimizer.hpp:14-20, optimizer.cpp:58-88, dvfs_model.hpp:60-70.

@@ -85,6 +85,8 @@ def _declare(L: C.CDLL) -> None:
     L.dso_status_name.restype = C.c_char_p
     L.dso_launch_count.argtypes = [vp]
     L.dso_launch_count.restype = i64
+    L.dso_set_option.argtypes = [vp, C.c_char_p, i64]
+    L.dso_set_option.restype = i32
     L.dso_set_domain.argtypes = [vp, P(d), i32, P(d), i32, P(d)]
     L.dso_validate_domain.argtypes = [P(d), i32, P(d), i32, P(d), C.c_char_p, i32]
     L.dso_validate_domain.restype = i32
@@ -121,7 +123,7 @@ def _declare(L: C.CDLL) -> None:
 # Every symbol include/dso_b200.h declares (checked by tests/test_abi.py).
 EXPORTED = (
     "dso_ctx_create", "dso_ctx_destroy", "dso_ctx_set_stream", "dso_sync", "dso_last_error",
-    "dso_status_name", "dso_launch_count", "dso_set_domain", "dso_validate_domain", "dso_set_model", "dso_get_model",
+    "dso_status_name", "dso_launch_count", "dso_set_option", "dso_set_domain", "dso_validate_domain", "dso_set_model", "dso_get_model",
     "dso_init_mlp", "dso_shuffled_indices", "dso_featurize", "dso_dcgm_mean", "dso_predict",
     "dso_sweep", "dso_sweep_f64", "dso_eta_sweep", "dso_pipeline", "dso_pipeline_csr",
     "dso_gen_synthetic", "dso_gen_synthetic_csr",

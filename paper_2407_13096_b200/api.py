@@ -112,6 +112,10 @@ class Context:
     def sync(self) -> None:
         self._raise(self._lib.dso_sync(self._h))
 
+    def set_option(self, key: str, value: int) -> None:
+        """dso_set_option: verification/tuning switches (e.g. "fast_sweep")."""
+        self._raise(self._lib.dso_set_option(self._h, key.encode(), int(value)))
+
     @property
     def launch_count(self) -> int:
         """Device kernels launched through this context (evidence counter)."""

@@ -235,6 +235,15 @@ const char* dso_status_name(int32_t st) {
 
 int64_t dso_launch_count(const dso_ctx* ctx) { return ctx ? ctx->c.launches : 0; }
 
+int32_t dso_set_option(dso_ctx* ctx, const char* key, int64_t value) {
+    if (!ctx || !key) return kInvalidArgument;
+    if (std::string(key) == "fast_sweep") {
+        ctx->c.fast_sweep = value != 0;
+        return kOk;
+    }
+    return fail(ctx, kInvalidArgument, std::string("unknown option: ") + key);
+}
+
 int32_t dso_set_domain(dso_ctx* ctx, const double* core, int32_t nc, const double* mem,
                        int32_t nm, const double* dev) {
     if (!ctx || !dev) return kInvalidArgument;
@@ -277,6 +286,16 @@ int32_t dso_set_domain(dso_ctx* ctx, const double* core, int32_t nc, const doubl
     DSO_CUDA(ctx, cudaMemcpy(c.dom.mem_d, mem, sizeof(double) * nm, cudaMemcpyHostToDevice));
     c.dom.nc = nc;
     c.dom.nm = nm;
+    // bounds that keep every f32 cost finite for params <= 1e12 and |K| <= 1e21
+    // (P <= 1e12 (1 + vc + fm + vc^2 fc) <= 1e21, T <= 1e12 (1 + 1/fm + 1/fc) <= 1e15)
+    bool fast = true;
+    for (int i = 0; i < nc; ++i)
+        fast = fast && core4[i].x >= 0.f && core4[i].x <= 1e3f && core4[i].y >= 0.f &&
+               core4[i].y <= 1e8f && core4[i].z >= 0.f && core4[i].z <= 1e3f;
+    for (int j = 0; j < nm; ++j)
+        fast = fast && mem2[j].x >= 0.f && mem2[j].x <= 1e6f && mem2[j].y >= 0.f &&
+               mem2[j].y <= 1e3f;
+    c.dom.fast_ok = fast;
     c.has_domain = true;
     return kOk;
 }
@@ -500,7 +519,9 @@ int32_t dso_eta_sweep(dso_ctx* ctx, const float* params, int64_t n, int64_t ld,
     DSO_CUDA(ctx, cudaMallocAsync(&d, sizeof(float2) * n_eta, c.stream));
     DSO_CUDA(ctx, cudaMemcpyAsync(d, ek.data(), sizeof(float2) * n_eta, cudaMemcpyHostToDevice,
                                   c.stream));
-    DSO_CUDA(ctx, launch_eta_sweep(c, params, n, ld, d, n_eta, idx, cost, ld_out));
+    bool fast = true;
+    for (int e = 0; e < n_eta; ++e) fast = fast && fast_sweep_ok(c, ek[e].y);
+    DSO_CUDA(ctx, launch_eta_sweep(c, params, n, ld, d, n_eta, idx, cost, ld_out, fast));
     DSO_CUDA(ctx, cudaFreeAsync(d, c.stream));
     DSO_CUDA(ctx, cudaStreamSynchronize(c.stream));  // ek lifetime
     return kOk;

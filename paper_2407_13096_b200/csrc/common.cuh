@@ -44,6 +44,9 @@ struct DomainDev {
     // f64 exact path: per core level {vc, fc}; per mem level fm
     double2* core_d;  // [nc]
     double* mem_d;    // [nm]
+    // the f32 tables are within the bounds under which the fast exact sweep's
+    // costs stay finite (sweep_core.cuh sweep_best)
+    bool fast_ok;
 };
 
 // Device model: transposed, zero-padded weights for the FP32 MLP kernels.
@@ -80,6 +83,7 @@ struct Ctx {
     cudaStream_t aux[3] = {nullptr, nullptr, nullptr};
     cudaEvent_t ev[8] = {};
     int num_sms = 148;
+    bool fast_sweep = true;         // dso_set_option("fast_sweep")
     void* train_scratch = nullptr;  // per-CTA partial gradients
     size_t train_scratch_bytes = 0;
 };
@@ -102,7 +106,7 @@ cudaError_t launch_sweep_f64(Ctx& c, const double* params, int64_t n, double eta
                              int32_t* kstatus);
 cudaError_t launch_eta_sweep(Ctx& c, const float* params, int64_t n, int64_t ld,
                              const float2* etaK_dev, int n_eta, int32_t* idx, float* cost,
-                             int64_t ld_out);
+                             int64_t ld_out, bool fast);
 cudaError_t launch_gen(Ctx& c, uint64_t root, uint64_t salt_base, int64_t first, int64_t n,
                        int64_t ld, float* params, uint32_t* counts, float* dcgm);
 cudaError_t launch_featurize(Ctx& c, const uint32_t* counts, const float* dcgm, int64_t n,
@@ -177,6 +181,11 @@ __device__ __forceinline__ float sigmoidf_fast(float z) {
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(z * -1.4426950408889634f));
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(1.0f + e));
     return r;
+}
+
+// Fast-sweep precondition on the domain and the objective constant K = (1-eta)*pmax.
+inline bool fast_sweep_ok(const Ctx& cx, float K) {
+    return cx.fast_sweep && cx.dom.fast_ok && K == K && K <= 1e21f && K >= -1e21f;
 }
 
 inline int grid_for(int64_t n, int block, int num_sms, int per_sm) {

@@ -97,8 +97,10 @@ __host__ __device__ __forceinline__ int pk_w4(int nn, int k) { return W4S + k * 
 // per-CTA shared memory beyond the model
 constexpr int ACT = kModelFloats;           // act[3][134][RS]
 constexpr int kActFloats = 134 * RS;
-constexpr int OUT = ACT + kBufs * kActFloats;  // out[3][8][RS]  (raw predictions)
-constexpr int kOutFloats = 8 * RS;
+// out[3][11][RS]: rows 0..6 raw predictions, rows 8..10 the upper half's sweep
+// result (cost, energy, index) for the consumer-side merge
+constexpr int OUT = ACT + kBufs * kActFloats;
+constexpr int kOutFloats = 11 * RS;
 constexpr int SCR = OUT + kBufs * kOutFloats;   // producer scratch: tf[3][64] rr[3][64]
 constexpr int kScrFloats = 6 * TM + 6 * TM;  // tf[3][64], rr[3][64] + part u64[3][64]
 static_assert(kScrFloats >= 3 * TPK * TM, "sweep merge scratch");
@@ -584,6 +586,7 @@ struct Job {
     const float2* mem2;
     int nc, nm;
     float eta, K;
+    bool fast;  // fast exact sweep allowed (fast_sweep_ok)
     // outputs
     float* params;
     uint8_t* clamped;
@@ -847,13 +850,13 @@ __device__ __forceinline__ void produce_results(const float* sm, const float* ou
     Best b{__int_as_float(0x7fc00000), __int_as_float(0x7fc00000), -1};  // i = -1: empty part
     if (i_lo < i_hi) {
         if (nm == 4)
-            b = sweep_levels<4>(p, s_core, s_mem, 4, i_lo, i_hi, J.eta, J.K);
+            b = sweep_best<4>(p, s_core, s_mem, 4, i_lo, i_hi, J.eta, J.K, J.fast);
         else if (nm == 1)
-            b = sweep_levels<1>(p, s_core, s_mem, 1, i_lo, i_hi, J.eta, J.K);
+            b = sweep_best<1>(p, s_core, s_mem, 1, i_lo, i_hi, J.eta, J.K, J.fast);
         else if (nm == 3)
-            b = sweep_levels<3>(p, s_core, s_mem, 3, i_lo, i_hi, J.eta, J.K);
+            b = sweep_best<3>(p, s_core, s_mem, 3, i_lo, i_hi, J.eta, J.K, J.fast);
         else
-            b = sweep_levels<0>(p, s_core, s_mem, nm, i_lo, i_hi, J.eta, J.K);
+            b = sweep_best<0>(p, s_core, s_mem, nm, i_lo, i_hi, J.eta, J.K, false);
     }
     // merge the quarters (merge_best is exact in any order: ties use the index)
     float* xc = const_cast<float*>(sm) + SCR;  // [TPK][64] cost, energy, index
@@ -887,6 +890,60 @@ __device__ __forceinline__ void produce_results(const float* sm, const float* ou
 #pragma unroll
             for (int i = 0; i < 7; ++i) J.params[i * J.ld_out + k] = pr[i];
         }
+    }
+}
+
+// Consumer group, pipeline modes: finish its own tile right after L4 — clamp,
+// then the grid sweep + eta objective + lexicographic argmin (sweep_best),
+// thread ct = kernel ct % 64 x half ct / 64 of the core levels (a warp reads
+// one core level at a time: a broadcast).  The upper half's result meets the
+// lower half's through out rows 8..10 (merge_best: exact in any order).
+__device__ __forceinline__ void consumer_sweep(const float* sm, float* out, const Job& J,
+                                               int64_t t0, int ct, int cbar) {
+    const int m = ct % TM, h = ct / TM;
+    const int64_t k = t0 + m;
+    bar_sync(cbar, kGroupThreads);  // L4 outputs in out
+    float pr[7];
+#pragma unroll
+    for (int i = 0; i < 7; ++i) pr[i] = out[i * RS + m];
+    const bool cl = clamp_params(pr);
+    const KParams p{pr[0], pr[1], pr[2], pr[3], pr[4], pr[5], pr[6]};
+    const float4* s_core = reinterpret_cast<const float4*>(sm + TABLES);
+    const float2* s_mem = reinterpret_cast<const float2*>(sm + TABLES + 4 * J.nc);
+    const int nc = J.nc, nm = J.nm;
+    const int i_lo = h ? nc / 2 : 0, i_hi = h ? nc : nc / 2;
+    Best b{__int_as_float(0x7fc00000), __int_as_float(0x7fc00000), -1};  // i = -1: empty half
+    if (i_lo < i_hi) {
+        if (nm == 4)
+            b = sweep_best<4>(p, s_core, s_mem, 4, i_lo, i_hi, J.eta, J.K, J.fast);
+        else if (nm == 1)
+            b = sweep_best<1>(p, s_core, s_mem, 1, i_lo, i_hi, J.eta, J.K, J.fast);
+        else if (nm == 3)
+            b = sweep_best<3>(p, s_core, s_mem, 3, i_lo, i_hi, J.eta, J.K, J.fast);
+        else if (nm == 2)
+            b = sweep_best<2>(p, s_core, s_mem, 2, i_lo, i_hi, J.eta, J.K, J.fast);
+        else
+            b = sweep_best<0>(p, s_core, s_mem, nm, i_lo, i_hi, J.eta, J.K, false);
+    }
+    if (h) {
+        out[8 * RS + m] = b.c;
+        out[9 * RS + m] = b.e;
+        reinterpret_cast<int*>(out)[10 * RS + m] = b.i;
+        if (k < J.n) {
+            if (J.clamped) J.clamped[k] = cl ? 1 : 0;
+            if (J.params)
+#pragma unroll
+                for (int i = 0; i < 7; ++i) J.params[i * J.ld_out + k] = pr[i];
+        }
+    }
+    bar_sync(cbar, kGroupThreads);
+    if (!h && k < J.n) {
+        const Best o{out[8 * RS + m], out[9 * RS + m], reinterpret_cast<const int*>(out)[10 * RS + m]};
+        if (o.i >= 0) merge_best(b, o);
+        J.idx[k] = b.i;
+        if (J.cost) J.cost[k] = b.c;
+        if (J.energy) J.energy[k] = b.e;
+        if (J.time) J.time[k] = time_at(p, s_core, s_mem, nm, b.i);
     }
 }
 
@@ -941,7 +998,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             consumer_tile(sm, sm + ACT + b * kActFloats, sm + OUT + b * kOutFloats,
                           reinterpret_cast<const uint32_t*>(sm + ROWS) + b * kRowWords,
                           reinterpret_cast<const int*>(sm + ROWCNT)[b], ct, BAR_CONS0 + G);
-            bar_arrive(BAR_READY0 + b, kHandoff);  // predictions in out[b]; act[b] free
+            if (PIPE) {
+                PT_BEGIN(t_s);
+                consumer_sweep(sm, sm + OUT + b * kOutFloats, J,
+                               (blockIdx.x + i * gridDim.x) * (int64_t)TM, ct, BAR_CONS0 + G);
+                PT_END(11, t_s);
+            }
+            // PIPE: tile finished, act[b]/out[b] free; PRED: predictions in out[b]
+            bar_arrive(BAR_READY0 + b, kHandoff);
         }
     } else {
         // ================================ producer ================================
@@ -988,19 +1052,45 @@ __global__ void __launch_bounds__(kThreads, 1)
             PT_END(10, t_f);
             bar_arrive(BAR_FULL0 + b, kHandoff);
         };
-        for (int64_t i = 0; i < kBufs && i < my_tiles; ++i) finish(i, issue(i));
-        for (int64_t i = 0; i < my_tiles; ++i) {
-            const int b = (int)(i % kBufs);
-            PT_BEGIN(t_w);
-            bar_sync(BAR_READY0 + b, kHandoff);  // tile i predicted; act[b] free
-            PT_END(8, t_w);
-            const bool more = i + kBufs < my_tiles;
-            const bool issued = more ? issue(i + kBufs) : false;  // loads fly during the sweep
-            PT_BEGIN(t_r);
-            produce_results<PIPE>(sm, sm + OUT + b * kOutFloats, J, t0_of(i), pt);
-            bar_sync(BAR_PROD, kProducers);
-            PT_END(9, t_r);
-            if (more) finish(i + kBufs, issued);
+        if (!PIPE) {
+            for (int64_t i = 0; i < kBufs && i < my_tiles; ++i) finish(i, issue(i));
+            for (int64_t i = 0; i < my_tiles; ++i) {
+                const int b = (int)(i % kBufs);
+                PT_BEGIN(t_w);
+                bar_sync(BAR_READY0 + b, kHandoff);  // tile i predicted; act[b] free
+                PT_END(8, t_w);
+                const bool more = i + kBufs < my_tiles;
+                const bool issued = more ? issue(i + kBufs) : false;  // loads fly meanwhile
+                PT_BEGIN(t_r);
+                produce_results<false>(sm, sm + OUT + b * kOutFloats, J, t0_of(i), pt);
+                bar_sync(BAR_PROD, kProducers);
+                PT_END(9, t_r);
+                if (more) finish(i + kBufs, issued);
+            }
+        } else {
+            // pipeline: the consumers finish their tiles; the producers only keep
+            // the buffers filled.  CSR entries of the next tile are prefetched
+            // into registers while the producers wait for its buffer.
+            if (MODE == MODE_CSR && my_tiles > 0) csr_prefetch(J, t0_of(0), pt, P);
+            for (int64_t i = 0; i < my_tiles; ++i) {
+                const int b = (int)(i % kBufs);
+                if (i >= kBufs) {
+                    PT_BEGIN(t_w);
+                    bar_sync(BAR_READY0 + b, kHandoff);  // tile i - kBufs finished
+                    PT_END(8, t_w);
+                }
+                bool issued;
+                if (MODE == MODE_CSR)
+                    issued = issue_tile_loads(sm + ACT + b * kActFloats, mbar + b, J.counts,
+                                              J.dcgm, t0_of(i), J.n, J.ld, vec_ok, pt, 8);
+                else
+                    issued = issue(i);
+                finish(i, issued);
+                if (MODE == MODE_CSR && i + 1 < my_tiles) csr_prefetch(J, t0_of(i + 1), pt, P);
+            }
+            // match the consumers' READY arrivals of the last tiles
+            for (int64_t i = my_tiles > kBufs ? my_tiles - kBufs : 0; i < my_tiles; ++i)
+                bar_sync(BAR_READY0 + (int)(i % kBufs), kHandoff);
         }
     }
 }
@@ -1153,6 +1243,7 @@ cudaError_t launch_pipeline(Ctx& cx, const uint32_t* counts, const float* dcgm, 
     J.nm = cx.dom.nm;
     J.eta = eta;
     J.K = K;
+    J.fast = fast_sweep_ok(cx, K);
     J.params = params;
     J.clamped = clamped;
     J.idx = idx;
@@ -1181,6 +1272,7 @@ cudaError_t launch_pipeline_csr(Ctx& cx, const uint64_t* row_ptr, const uint32_t
     J.nm = cx.dom.nm;
     J.eta = eta;
     J.K = K;
+    J.fast = fast_sweep_ok(cx, K);
     J.params = params;
     J.clamped = clamped;
     J.idx = idx;

@@ -20,6 +20,8 @@
 // (28 B in, 16 B out per kernel for nc*nm pairs).
 #include <math.h>
 
+#include <type_traits>
+
 #include "common.cuh"
 #include "sweep_core.cuh"
 
@@ -42,7 +44,7 @@ __global__ void __launch_bounds__(kBlock) sweep_f32_kernel(
     const float* __restrict__ params, int64_t n, int64_t ld, const float4* __restrict__ core4,
     int nc, const float2* __restrict__ mem2, int nm_rt, float eta, float K,
     int32_t* __restrict__ idx, float* __restrict__ cost, float* __restrict__ energy,
-    float* __restrict__ time, int32_t* __restrict__ kstatus) {
+    float* __restrict__ time, int32_t* __restrict__ kstatus, bool fast) {
     __shared__ float4 s_core[kMaxCore];
     __shared__ float2 s_mem[kMaxMem];
     const int nm = NM > 0 ? NM : nm_rt;
@@ -68,7 +70,7 @@ __global__ void __launch_bounds__(kBlock) sweep_f32_kernel(
             if (kstatus) kstatus[k] = kInvalidArgument;
             continue;
         }
-        const Best b = sweep_levels<NM>(p, s_core, s_mem, nm, 0, nc, eta, K);
+        const Best b = sweep_best<NM>(p, s_core, s_mem, nm, 0, nc, eta, K, fast);
         idx[k] = b.i;
         if (cost) cost[k] = b.c;
         if (energy) energy[k] = b.e;
@@ -234,6 +236,110 @@ __global__ void __launch_bounds__(128) eta_sweep_kernel(
     }
 }
 
+// Fast exact eta sweep (NM = 1..4): per group of 8 pairs, P and T are formed
+// once and shared by the chunk's CH etas; per eta the group costs take 8
+// packed FFMA2/FMUL2 and a min tree, and the running minimum keeps the first
+// group attaining it (sweep_best's scheme, sweep_core.cuh).  Afterwards each
+// eta's winning group is replayed with the lexicographic rule; an eta whose
+// minimum was reached by two groups (its bit in `ties`) is rescanned in full.
+// Every eta's (idx, cost) therefore equals dso_sweep's at that eta, bit for bit.
+// Out of line so the unrolled per-eta calls keep the eta state in registers.
+template <int NM>
+__device__ __noinline__ Best replay_levels(const KParams p, const float4* s_core,
+                                           const float2* s_mem, int lo, int hi, float eta,
+                                           float K) {
+    return sweep_levels<NM>(p, s_core, s_mem, NM, lo, hi, eta, K);
+}
+
+template <int CH, int NM>
+__global__ void __launch_bounds__(128) eta_sweep_fast_kernel(
+    const float* __restrict__ params, int64_t n, int64_t ld, const float4* __restrict__ core4,
+    int nc, const float2* __restrict__ mem2, const float2* __restrict__ etaK, int n_eta,
+    int32_t* __restrict__ idx, float* __restrict__ cost, int64_t ld_out) {
+    static_assert(CH <= 32, "tie bits");
+    constexpr int GL = FastGroup<NM>::GL;
+    constexpr int GH = GL * NM / 2;
+    __shared__ float4 s_core[kMaxCore];
+    __shared__ float2 s_mem[NM];
+    for (int i = threadIdx.x; i < nc; i += blockDim.x) s_core[i] = core4[i];
+    if (threadIdx.x < NM) s_mem[threadIdx.x] = mem2[threadIdx.x];
+    __syncthreads();
+    const int e0 = blockIdx.y * CH;
+    float ev[CH], Kv[CH];
+#pragma unroll
+    for (int e = 0; e < CH; ++e) {
+        const int ee = e0 + e < n_eta ? e0 + e : n_eta - 1;
+        ev[e] = etaK[ee].x;
+        Kv[e] = etaK[ee].y;
+    }
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride) {
+        KParams p;
+        p.p0 = __ldg(params + k);
+        p.kp = __ldg(params + ld + k);
+        p.g = __ldg(params + 2 * ld + k);
+        p.c = __ldg(params + 3 * ld + k);
+        p.t0 = __ldg(params + 4 * ld + k);
+        p.a = __ldg(params + 5 * ld + k);
+        p.b = __ldg(params + 6 * ld + k);
+        if (params_invalid(p.p0, p.kp, p.g, p.c, p.t0, p.a, p.b)) {
+#pragma unroll
+            for (int e = 0; e < CH; ++e)
+                if (e0 + e < n_eta) {
+                    idx[(int64_t)(e0 + e) * ld_out + k] = -1;
+                    if (cost) cost[(int64_t)(e0 + e) * ld_out + k] = __int_as_float(0x7fc00000);
+                }
+            continue;
+        }
+        const bool fast = params_fast(p);
+        float bc[CH];
+        int bg[CH];
+        uint32_t ties = fast ? 0u : 0xffffffffu;
+#pragma unroll
+        for (int e = 0; e < CH; ++e) {
+            bc[e] = __int_as_float(0x7f800000);
+            bg[e] = 0;
+        }
+        if (fast) {
+            float G[NM], Ta1[NM];
+#pragma unroll
+            for (int j = 0; j < NM; ++j) {
+                G[j] = __fmul_rn(p.g, s_mem[j].x);
+                Ta1[j] = __fadd_rn(p.t0, __fmul_rn(p.a, s_mem[j].y));
+            }
+            auto group = [&](int i, auto tail) {
+                float pc[GL], tb[GL];
+                group_levels<NM, decltype(tail)::value>(p, s_core, i, nc, pc, tb);
+                float2 P2[GH], T2[GH];
+                group_pt<NM>(pc, tb, Ta1, G, P2, T2);
+#pragma unroll
+                for (int e = 0; e < CH; ++e) {
+                    const float m = group_min_cost<NM>(P2, T2, ev[e], Kv[e]);
+                    ties |= m == bc[e] ? 1u << e : 0u;
+                    bg[e] = m < bc[e] ? i : bg[e];
+                    bc[e] = fminf(m, bc[e]);
+                }
+            };
+            int i = 0;
+#pragma unroll 1
+            for (; i + GL <= nc; i += GL) group(i, std::false_type{});
+            if (i < nc) group(i, std::true_type{});
+        }
+        // replay each eta's winning group (or, on a tie, every level) exactly
+#pragma unroll
+        for (int e = 0; e < CH; ++e) {
+            if (e0 + e < n_eta) {
+                const bool full = (ties >> e) & 1u;
+                const int lo = full ? 0 : bg[e];
+                const int hi = full ? nc : min(bg[e] + GL, nc);
+                const Best b = replay_levels<NM>(p, s_core, s_mem, lo, hi, ev[e], Kv[e]);
+                idx[(int64_t)(e0 + e) * ld_out + k] = b.i;
+                if (cost) cost[(int64_t)(e0 + e) * ld_out + k] = b.c;
+            }
+        }
+    }
+}
+
 }  // namespace
 
 cudaError_t launch_sweep_f32(Ctx& cx, const float* params, int64_t n, int64_t ld, float eta,
@@ -245,7 +351,8 @@ cudaError_t launch_sweep_f32(Ctx& cx, const float* params, int64_t n, int64_t ld
 #define DSO_SWEEP_CASE(NMV)                                                                    \
     sweep_f32_kernel<NMV><<<grid, kBlock, 0, cx.stream>>>(params, n, ld, d.core4, d.nc, d.mem2, \
                                                           d.nm, eta, K, idx, cost, energy,      \
-                                                          time, kstatus)
+                                                          time, kstatus, fast)
+    const bool fast = fast_sweep_ok(cx, K);
     switch (d.nm) {
         case 1: DSO_SWEEP_CASE(1); break;
         case 2: DSO_SWEEP_CASE(2); break;
@@ -272,9 +379,28 @@ cudaError_t launch_sweep_f64(Ctx& cx, const double* params, int64_t n, double et
 
 cudaError_t launch_eta_sweep(Ctx& cx, const float* params, int64_t n, int64_t ld,
                              const float2* etaK_dev, int n_eta, int32_t* idx, float* cost,
-                             int64_t ld_out) {
+                             int64_t ld_out, bool fast) {
     if (n <= 0 || n_eta <= 0) return cudaSuccess;
     const DomainDev& d = cx.dom;
+    if (fast && d.nm >= 1 && d.nm <= 4) {
+        // chunks of up to 26 etas (101 -> 4 chunks of 26, 3 padding slots)
+        constexpr int CH = 26;
+        const int chunks = (n_eta + CH - 1) / CH;
+        const int gx = grid_for(n, 128, cx.num_sms, 16);
+        dim3 grid(gx, chunks);
+#define DSO_ETA_FAST(NMV)                                                                   \
+    eta_sweep_fast_kernel<CH, NMV><<<grid, 128, 0, cx.stream>>>(                            \
+        params, n, ld, d.core4, d.nc, d.mem2, etaK_dev, n_eta, idx, cost, ld_out)
+        switch (d.nm) {
+            case 1: DSO_ETA_FAST(1); break;
+            case 2: DSO_ETA_FAST(2); break;
+            case 3: DSO_ETA_FAST(3); break;
+            default: DSO_ETA_FAST(4); break;
+        }
+#undef DSO_ETA_FAST
+        ++cx.launches;
+        return cudaGetLastError();
+    }
     // pick the chunk size with the least padding (ties -> larger chunk)
     const int cands[3] = {17, 8, 4};
     int best = 17, best_slots = 1 << 30;

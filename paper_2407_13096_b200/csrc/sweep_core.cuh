@@ -194,6 +194,161 @@ __device__ __forceinline__ Best sweep_levels(const KParams& p, const float4* __r
     }
 }
 
+// ---------------------------------------------------------------------------
+// Fast exact sweep: the same argmin as sweep_levels, with about a third of its
+// comparator work.
+//
+// The core levels are visited in groups of GL = 8/NM levels (8 pairs).  Per
+// group only the minimum cost is formed (a min-tree: FMNMX), and the running
+// minimum over groups keeps the FIRST group attaining it (strict <).  The
+// exact lexicographic rule (cost, then energy, then visit order — better(),
+// optimizer.cpp:27-32) is then replayed by sweep_levels over the 8 pairs of
+// the winning group only.  This equals the full sequential scan unless another
+// group reaches the same minimum cost exactly; that is detected (m == best at
+// any group) and the whole range is then rescanned by sweep_levels.
+//
+// T is formed as max(t0 + a/fm, t0 + b/fc): round-to-nearest is monotone, so
+// fl(t0 + max(x, y)) == max(fl(t0 + x), fl(t0 + y)) — every cost is
+// bit-identical to eval_pair's.  Preconditions (else sweep_levels runs):
+// finite params <= 1e12 per kernel and a domain / K within the bounds checked
+// on the host (DomainDev::fast_ok), which keep every cost finite, so there are
+// no NaNs for FMNMX to drop.
+__device__ __forceinline__ bool params_fast(const KParams& p) {
+    const float m = fmaxf(fmaxf(fmaxf(p.p0, p.kp), fmaxf(p.g, p.c)),
+                          fmaxf(fmaxf(p.t0, p.a), p.b));
+    // fmaxf drops NaN operands: test finiteness of the sum separately
+    const float s = ((p.p0 + p.kp) + (p.g + p.c)) + ((p.t0 + p.a) + p.b);
+    return m <= 1e12f && s == s;
+}
+
+template <int NM>
+struct FastGroup {
+    static constexpr int GL = NM == 3 ? 2 : 8 / NM;  // core levels per group (NM = 1..4)
+};
+
+__device__ __forceinline__ float fmin3(float a, float b, float c) {
+    float r;
+    asm("min.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+    return r;
+}
+
+// Per-level terms of a group of GL core levels starting at i: Pc and
+// t0 + b/fc.  TAIL: the group is cut at i_end; missing levels repeat the last
+// one (a repeated pair has the same cost, so the group minimum is unchanged).
+template <int NM, bool TAIL>
+__device__ __forceinline__ void group_levels(const KParams& p, const float4* __restrict__ s_core,
+                                             int i, int i_end, float* pc, float* tb) {
+#pragma unroll
+    for (int l = 0; l < FastGroup<NM>::GL; ++l) {
+        const float4 t = s_core[TAIL ? min(i + l, i_end - 1) : i + l];
+        pc[l] = pc_f32(p.p0, p.kp, p.c, t);
+        tb[l] = __fadd_rn(p.t0, __fmul_rn(p.b, t.z));
+    }
+}
+
+// P and T of the group's GP = GL*NM pairs, in visit order, two per packed op.
+template <int NM>
+__device__ __forceinline__ void group_pt(const float* pc, const float* tb, const float* Ta1,
+                                         const float* G, float2* P2, float2* T2) {
+    constexpr int GP = FastGroup<NM>::GL * NM;
+    static_assert(GP % 2 == 0, "groups hold an even number of pairs");
+#pragma unroll
+    for (int q = 0; q < GP; q += 2) {
+        const int l0 = q / NM, j0 = q % NM, l1 = (q + 1) / NM, j1 = (q + 1) % NM;
+        P2[q / 2] = fadd2(make_float2(pc[l0], pc[l1]), make_float2(G[j0], G[j1]));
+        T2[q / 2] = make_float2(fmaxf(Ta1[j0], tb[l0]), fmaxf(Ta1[j1], tb[l1]));
+    }
+}
+
+// Minimum cost over the group: C = (eta*P + K) * T per pair (cost_f32's
+// rounding), then a three-input min tree (FMNMX3).
+template <int NM>
+__device__ __forceinline__ float group_min_cost(const float2* P2, const float2* T2, float eta,
+                                                float K) {
+    constexpr int GP = FastGroup<NM>::GL * NM;
+    float c[GP];
+#pragma unroll
+    for (int q = 0; q < GP / 2; ++q) {
+        const float2 C = fmul2(ffma2(make_float2(eta, eta), P2[q], make_float2(K, K)), T2[q]);
+        c[2 * q] = C.x;
+        c[2 * q + 1] = C.y;
+    }
+    if constexpr (GP == 8) {
+        return fminf(fmin3(c[0], c[1], c[2]), fmin3(c[3], c[4], fmin3(c[5], c[6], c[7])));
+    } else {
+        static_assert(GP == 6, "group sizes 8 (NM = 1, 2, 4) and 6 (NM = 3)");
+        return fminf(fmin3(c[0], c[1], c[2]), fmin3(c[3], c[4], c[5]));
+    }
+}
+
+template <int NM, bool TAIL>
+__device__ __forceinline__ float group_min(const KParams& p, const float4* __restrict__ s_core,
+                                           const float* Ta1, const float* G, int i, int i_end,
+                                           float eta, float K) {
+    constexpr int GL = FastGroup<NM>::GL;
+    float pc[GL], tb[GL];
+    group_levels<NM, TAIL>(p, s_core, i, i_end, pc, tb);
+    float2 P2[GL * NM / 2], T2[GL * NM / 2];
+    group_pt<NM>(pc, tb, Ta1, G, P2, T2);
+    return group_min_cost<NM>(P2, T2, eta, K);
+}
+
+// Exact sweep of core levels [i_lo, i_hi) (non-empty) x all memory levels:
+// identical result to sweep_levels<NM>(..., i_lo, i_hi, ...).
+template <int NM>
+__device__ __forceinline__ Best sweep_best(const KParams& p, const float4* __restrict__ s_core,
+                                           const float2* __restrict__ s_mem, int nm_rt, int i_lo,
+                                           int i_hi, float eta, float K, bool fast) {
+    int lo = i_lo, hi = i_hi;
+    if constexpr (NM >= 1 && NM <= 4) {
+        constexpr int GL = FastGroup<NM>::GL;
+        if (fast && params_fast(p)) {
+            float G[NM], Ta1[NM];
+#pragma unroll
+            for (int j = 0; j < NM; ++j) {
+                G[j] = __fmul_rn(p.g, s_mem[j].x);
+                Ta1[j] = __fadd_rn(p.t0, __fmul_rn(p.a, s_mem[j].y));
+            }
+            float bc = __int_as_float(0x7f800000);
+            int bg = i_lo;
+            bool tie = false;
+            int i = i_lo;
+            // four independent groups per step: their loads and min trees overlap
+            // (a single group is a ~80-cycle dependency chain); folded in order
+#pragma unroll 1
+            for (; i + 4 * GL <= i_hi; i += 4 * GL) {
+                float m[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    m[u] = group_min<NM, false>(p, s_core, Ta1, G, i + u * GL, i_hi, eta, K);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    tie |= (m[u] == bc);
+                    bg = m[u] < bc ? i + u * GL : bg;
+                    bc = fminf(m[u], bc);
+                }
+            }
+#pragma unroll 1
+            for (; i + GL <= i_hi; i += GL) {
+                const float m = group_min<NM, false>(p, s_core, Ta1, G, i, i_hi, eta, K);
+                tie |= (m == bc);
+                bg = m < bc ? i : bg;
+                bc = fminf(m, bc);
+            }
+            if (i < i_hi) {
+                const float m = group_min<NM, true>(p, s_core, Ta1, G, i, i_hi, eta, K);
+                tie |= (m == bc);
+                bg = m < bc ? i : bg;
+            }
+            if (!tie) {
+                lo = bg;
+                hi = min(bg + GL, i_hi);
+            }
+        }
+    }
+    return sweep_levels<NM>(p, s_core, s_mem, nm_rt, lo, hi, eta, K);
+}
+
 __device__ __forceinline__ float time_at(const KParams& p, const float4* s_core,
                                          const float2* s_mem, int nm, int idx) {
     const int i = idx / nm, j = idx - i * nm;

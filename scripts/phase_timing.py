@@ -14,10 +14,10 @@ from paper_2407_13096_b200.api import Context  # noqa: E402
 L = _lib.lib()
 L.dso_debug_phase_cycles.argtypes = [C.c_void_p, C.c_int]
 names = ["c.wait_full", "c.L1", "c.L1_epi", "c.L2", "c.L2_epi", "c.L3", "c.L3_epi", "c.L4",
-         "p.wait_ready", "p.results", "p.features", "", "", "", "", ""]
+         "p.wait_ready", "p.results", "p.features", "c.sweep", "", "", "", ""]
 ctx = Context(0)
 n = 1 << 22
-for mode in ("pipeline", "predict"):
+for mode in ("pipeline_csr", "pipeline", "predict"):
     ctx.set_domain(config_domain("c3"))
     import numpy as np
     m = init_mlp(seed=424242)
@@ -25,10 +25,12 @@ for mode in ("pipeline", "predict"):
     m.target_std = np.array([15, 3, 0.005, 0.001, 0.07, 100, 100.0])
     ctx.set_model(m)
     g = ctx.gen_synthetic(n, root=3)
+    gc = ctx.gen_synthetic_csr(n, root=3)
     f = ctx.featurize(g["counts"], g["dcgm"])
     buf = (C.c_ulonglong * 16)()
-    run = (lambda: ctx.pipeline(g["counts"], g["dcgm"], 0.8)) if mode == "pipeline" else \
-          (lambda: ctx.predict_params(f))
+    run = {"pipeline": lambda: ctx.pipeline(g["counts"], g["dcgm"], 0.8),
+           "pipeline_csr": lambda: ctx.pipeline_csr(gc["row_ptr"], gc["entries"], gc["dcgm"], 0.8),
+           "predict": lambda: ctx.predict_params(f)}[mode]
     run()
     L.dso_debug_phase_cycles(buf, 1)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

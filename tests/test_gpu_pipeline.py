@@ -222,3 +222,25 @@ def test_pipeline_csr_nonfinite_weight_disables_row_skipping(ctx, port):
     b = ctx.pipeline_csr(s["row_ptr"], s["entries"], s["dcgm"], 0.8, want_params=True)
     for f in ("idx", "cost", "energy", "time", "params", "clamped"):
         np.testing.assert_array_equal(a[f].cpu().numpy(), b[f].cpu().numpy())
+
+
+@pytest.mark.parametrize("cfg", ["c2", "c3"])
+def test_pipeline_fast_sweep_bit_identical(ctx, port, cfg):
+    """The fused kernel's group-minimum sweep == the pair-by-pair scan, bit for bit."""
+    dom = config_domain(cfg)
+    ctx.set_domain(dom)
+    ctx.set_model(stats_model(port))
+    n = 50_000 + 7
+    g = ctx.gen_synthetic_csr(n, root=0x5EED, first=3)
+    outs = []
+    try:
+        for fast in (1, 0):
+            ctx.set_option("fast_sweep", fast)
+            for eta in (0.0, 0.8):
+                o = ctx.pipeline_csr(g["row_ptr"], g["entries"], g["dcgm"], eta)
+                outs.append({k: v.cpu().numpy() for k, v in o.items() if v is not None})
+    finally:
+        ctx.set_option("fast_sweep", 1)
+    for a, b in zip(outs[:2], outs[2:]):
+        for k in a:
+            np.testing.assert_array_equal(a[k].view(np.uint8), b[k].view(np.uint8), err_msg=k)

@@ -160,3 +160,74 @@ def test_sweep_errors(ctx):
     assert e.value.kind == ErrorKind.InvalidArgument
     r = ctx.brute_force_config(soa(np.zeros((0, 7)), ld=1), 0.5, n=0)
     assert r["idx"].shape[0] == 1
+
+
+def _tie_params(rng, n):
+    """Random params plus kernels built to tie: equal costs across core levels
+    (kp = c = g = b = 0), coarse values, zeros, huge and non-finite entries."""
+    base = np.column_stack([rng.uniform(40, 90, n), rng.uniform(5, 15, n),
+                            rng.uniform(0.004, 0.02, n), rng.uniform(0.002, 0.0055, n),
+                            rng.uniform(0.04, 0.3, n), rng.uniform(40, 400, n),
+                            rng.uniform(40, 400, n)])
+    q = n // 8
+    base[:q, [1, 2, 3, 6]] = 0.0                       # cost constant along fc
+    base[q:2 * q] = np.round(base[q:2 * q])            # coarse values
+    base[2 * q:3 * q, 0:4] = 0.0                       # P == 0 -> C = K*T
+    base[3 * q:3 * q + 8, 5] = 3e13                    # beyond the fast-path bound
+    base[3 * q + 8:3 * q + 16, 4] = np.inf
+    base[3 * q + 16:3 * q + 24, 0] = np.nan
+    base[3 * q + 24:3 * q + 32, 1] = -1.0              # invalid -> kstatus
+    return base
+
+
+@pytest.mark.parametrize("name", ["toy", "c1", "c1_literal", "c2", "c3", "grid10x10"])
+def test_fast_sweep_bit_identical(ctx, golden_sweep, name):
+    """The group-minimum sweep (default) equals the pair-by-pair lexicographic
+    scan bit for bit: idx, cost, energy, time, kstatus — including exact ties."""
+    g = golden_sweep
+    set_golden_domain(ctx, g, name)
+    rng = np.random.default_rng(11)
+    params = np.concatenate([g[f"{name}/params"], _tie_params(rng, 40_000)])
+    p = soa(params)
+    try:
+        for eta in (0.0, 0.3, 0.8, 1.0):
+            ctx.set_option("fast_sweep", 1)
+            a = {k: v.cpu().numpy() for k, v in ctx.brute_force_config(p, eta).items()}
+            ctx.set_option("fast_sweep", 0)
+            b = {k: v.cpu().numpy() for k, v in ctx.brute_force_config(p, eta).items()}
+            for k in ("idx", "kstatus"):
+                np.testing.assert_array_equal(a[k], b[k], err_msg=f"{k} eta={eta}")
+            for k in ("cost", "energy", "time"):
+                np.testing.assert_array_equal(a[k].view(np.uint32), b[k].view(np.uint32),
+                                              err_msg=f"{k} eta={eta}")
+    finally:
+        ctx.set_option("fast_sweep", 1)
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "grid10x10"])
+def test_fast_eta_sweep_bit_identical(ctx, golden_sweep, name):
+    g = golden_sweep
+    set_golden_domain(ctx, g, name)
+    rng = np.random.default_rng(12)
+    params = np.concatenate([g[f"{name}/params"], _tie_params(rng, 8_000)])
+    p = soa(params)
+    etas = np.arange(101) / 100.0
+    try:
+        ctx.set_option("fast_sweep", 1)
+        ia, ca = (x.cpu().numpy() for x in ctx.eta_sweep(p, etas))
+        ctx.set_option("fast_sweep", 0)
+        ib, cb = (x.cpu().numpy() for x in ctx.eta_sweep(p, etas))
+    finally:
+        ctx.set_option("fast_sweep", 1)
+    np.testing.assert_array_equal(ia, ib)
+    np.testing.assert_array_equal(ca.view(np.uint32), cb.view(np.uint32))
+    # and each row equals the single-eta sweep
+    for e in (0, 7, 50, 100):
+        r = ctx.brute_force_config(p, float(etas[e]))
+        np.testing.assert_array_equal(ia[e], r["idx"].cpu().numpy())
+
+
+def test_set_option_errors(ctx):
+    with pytest.raises(DsoError) as e:
+        ctx.set_option("no_such_option", 1)
+    assert e.value.kind == ErrorKind.InvalidArgument
