@@ -37,6 +37,11 @@ UNIT = "(kernel, freq-pair) evals/s"
 ROOT_SEED = 0xD50B203
 MLP_FLOPS = 2 * (134 * 100 + 100 * 50 + 50 * 25 + 25 * 7)  # 39,650 per kernel
 PAIR_FLOPS = 14
+
+
+def mlp_flops_sparse(l1_rows):
+    """MLP flops per kernel when layer 1 sees l1_rows non-zero inputs."""
+    return 2 * (l1_rows * 100 + 100 * 50 + 50 * 25 + 25 * 7)
 CONFIGS = {
     "c2": dict(n=1 << 20, nc=64, nm=1, eta=0.8,
                desc="C2: 1M kernels x 64 core x 1 mem freqs, eta 0.8"),
@@ -286,6 +291,12 @@ def run_ours(args, rank, world, local_rank):
                 ctx.pipeline(counts, dcgm, cfg["eta"], out=out)
         units_per_step = n * dom.pairs
         flops_per_step = n * (MLP_FLOPS + PAIR_FLOPS * dom.pairs)
+        if csr:
+            # Sparse input: layer 1 only needs the rows a kernel lists (8 DCGM rows +
+            # its non-zero count slots; the kernel skips all-zero rows exactly), so
+            # the algorithmic work is 2*100*(8 + nnz) there, not 2*100*134.
+            nnz = float((gen["row_ptr"][n] - gen["row_ptr"][0]).item()) / n
+            flops_per_step = n * (mlp_flops_sparse(8 + nnz) + PAIR_FLOPS * dom.pairs)
 
     # measured FP32 peak (roofline denominator for the FP32-pipe-bound kernels)
     peak = {}
@@ -384,7 +395,13 @@ def run_ours(args, rank, world, local_rank):
         "algorithmic_bytes_per_launch": n * ((136 if csr else 536) + 16)
         if args.config != "c4" else None,
         "kernel": "pipeline_kernel" if args.config != "c4" else "eta_sweep_kernel",
-        "flops_per_kernel": (MLP_FLOPS + PAIR_FLOPS * dom.pairs) if args.config != "c4" else None,
+        "flops_per_kernel": flops_per_step / n if args.config != "c4" else None,
+        "flops_note": ("layer 1 counted on the 8 DCGM + non-zero count rows of each kernel "
+                       "(CSR input; all-zero rows are skipped exactly); the dense-input "
+                       "count (SURVEY.md §8(d): 39,650 + 14 per pair) is "
+                       "flops_per_kernel_dense" if csr and args.config != "c4" else None),
+        "flops_per_kernel_dense": (MLP_FLOPS + PAIR_FLOPS * dom.pairs)
+        if args.config != "c4" else None,
         "peak_source": ("measured in this run by dso_probe_fp32_peak (FFMA2 loop, 148x4 CTAs); "
                         "MEASURED_PEAKS.json has no FP32 figure"),
         "peak_ffma_scalar": peak["ffma"],

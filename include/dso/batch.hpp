@@ -8,6 +8,9 @@
 //   brute_force_config_batch  <-  brute_force_config   (optimizer.hpp:48-52)
 //                                 bit-exact: FP64 kernel in the reference's
 //                                 operation order (dso_sweep_f64)
+//   optimal_config_batch      <-  optimal_config       (optimizer.hpp:39-46)
+//                                 bit-exact incl. fallback, presnap and
+//                                 candidates_evaluated (dso_optimal_config)
 //   optimize_kernels          <-  featurize (ptx_features.hpp:55) +
 //                                 FusedFeatures::as_vector (mlp.hpp:20-25) +
 //                                 predict_params (mlp.hpp:66) +
@@ -93,17 +96,22 @@ private:
     DeviceConstants dev_{};
 };
 
+// Re-upload the context's domain when it differs from `domain`.
+inline void sync_domain(GpuContext& ctx, const DvfsDomain& domain) {
+    if (ctx.core() != domain.core_freqs_mhz || ctx.mem() != domain.mem_freqs_mhz ||
+        ctx.dev().kappa_vf != domain.dev.kappa_vf || ctx.dev().vmin_v != domain.dev.vmin_v ||
+        ctx.dev().vmax_v != domain.dev.vmax_v || ctx.dev().pmax_w != domain.dev.pmax_w ||
+        ctx.dev().mhz_per_unit != domain.dev.mhz_per_unit)
+        ctx.set_domain(domain);
+}
+
 // brute_force_config for every element of params, bit-identical to the
 // reference (optimizer.cpp:90-117).  The context's domain must equal `domain`
 // (it is re-uploaded when it differs).
 inline std::vector<OptimizationResult> brute_force_config_batch(
     std::span<const KernelModelParams> params, const DvfsDomain& domain, double eta,
     double pmax_w, GpuContext& ctx) {
-    if (ctx.core() != domain.core_freqs_mhz || ctx.mem() != domain.mem_freqs_mhz ||
-        ctx.dev().kappa_vf != domain.dev.kappa_vf || ctx.dev().vmin_v != domain.dev.vmin_v ||
-        ctx.dev().vmax_v != domain.dev.vmax_v || ctx.dev().pmax_w != domain.dev.pmax_w ||
-        ctx.dev().mhz_per_unit != domain.dev.mhz_per_unit)
-        ctx.set_domain(domain);
+    sync_domain(ctx, domain);
     const int64_t n = static_cast<int64_t>(params.size());
     std::vector<int32_t> idx(n), ks(n);
     std::vector<double> cost(n), energy(n), time(n);
@@ -131,6 +139,47 @@ inline std::vector<OptimizationResult> brute_force_config_batch(
         r.time_s = time[k];
         r.candidates_evaluated = candidates;
         r.fallback = false;
+    }
+    return out;
+}
+
+// optimal_config for every element of params, bit-identical to the reference
+// (optimizer.cpp:119-205): best, cost, energy_j, time_s, candidates_evaluated,
+// fallback and presnap_{vc,fc_mhz,fm_mhz}.
+inline std::vector<OptimizationResult> optimal_config_batch(
+    std::span<const KernelModelParams> params, const DvfsDomain& domain, double eta,
+    double pmax_w, GpuContext& ctx) {
+    sync_domain(ctx, domain);
+    const int64_t n = static_cast<int64_t>(params.size());
+    std::vector<int32_t> idx(n), ks(n);
+    std::vector<double> cost(n), energy(n), time(n), pre(3 * n);
+    std::vector<int64_t> cand(n);
+    std::vector<uint8_t> fb(n);
+    check_status(dso_optimal_config(ctx.handle(), reinterpret_cast<const double*>(params.data()),
+                                    n, eta, pmax_w, idx.data(), cost.data(), energy.data(),
+                                    time.data(), cand.data(), fb.data(), pre.data(), ks.data(),
+                                    DSO_HOST),
+                 ctx.handle());
+    std::vector<OptimizationResult> out(n);
+    const std::size_t nm = domain.mem_freqs_mhz.size();
+    for (int64_t k = 0; k < n; ++k) {
+        if (ks[k]) {
+            validate(params[k]);
+            throw Error(static_cast<ErrorKind>(ks[k] - 1), "invalid kernel parameters");
+        }
+        const std::size_t i = static_cast<std::size_t>(idx[k]) / nm;
+        const std::size_t j = static_cast<std::size_t>(idx[k]) % nm;
+        OptimizationResult& r = out[k];
+        const double fc = domain.core_freqs_mhz[i];
+        r.best = DvfsConfig{required_voltage_mhz(fc, domain.dev), fc, domain.mem_freqs_mhz[j]};
+        r.cost = cost[k];
+        r.energy_j = energy[k];
+        r.time_s = time[k];
+        r.candidates_evaluated = static_cast<long>(cand[k]);
+        r.fallback = fb[k] != 0;
+        r.presnap_vc = pre[3 * k];
+        r.presnap_fc_mhz = pre[3 * k + 1];
+        r.presnap_fm_mhz = pre[3 * k + 2];
     }
     return out;
 }

@@ -143,6 +143,17 @@ int32_t dso_sweep_f64(dso_ctx* ctx, const double* params_aos, int64_t n, double 
                       double pmax_w, int32_t* idx, double* cost, double* energy,
                       double* time, int32_t* kstatus, uint32_t flags);
 
+/* optimal_config (optimizer.cpp:119-205, optimizer.hpp:39-46): the structured
+ * Theorem-1 search, FP64, bit-identical to the reference per kernel.  params
+ * AoS [n][7] double like dso_sweep_f64.  Outputs per kernel: idx (fc_idx*nm +
+ * fm_idx), cost, energy, time, candidates (candidates_evaluated), fallback
+ * (0/1), presnap [n][3] = {presnap_vc, presnap_fc_mhz, presnap_fm_mhz}, kstatus.
+ * Every output but idx may be NULL.  flags: DSO_HOST for host buffers. */
+int32_t dso_optimal_config(dso_ctx* ctx, const double* params_aos, int64_t n, double eta,
+                           double pmax_w, int32_t* idx, double* cost, double* energy,
+                           double* time, int64_t* candidates, uint8_t* fallback,
+                           double* presnap, int32_t* kstatus, uint32_t flags);
+
 /* eta sweep: brute_force_config at n_eta etas in one pass over the grid.
  * idx/cost are [n_eta][ld_out]. */
 int32_t dso_eta_sweep(dso_ctx* ctx, const float* params, int64_t n, int64_t ld,

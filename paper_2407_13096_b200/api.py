@@ -278,6 +278,39 @@ class Context:
                                             _ptr(out["kstatus"]), flags))
         return out
 
+    def optimal_config(self, params_aos, eta: float, pmax_w: float | None = None):
+        """FP64, bit-exact optimal_config (optimizer.cpp:119-205) over KernelModelParams[n]
+        (AoS [n, 7]): dict(idx, cost, energy, time, candidates, fallback, presnap [n, 3],
+        kstatus).  CUDA float64 tensor or host numpy array (staged by the library)."""
+        pmax = self.domain.dev.pmax_w if pmax_w is None else pmax_w
+        if _is_cuda(params_aos):
+            if params_aos.dtype != torch.float64 or params_aos.dim() != 2 \
+                    or params_aos.shape[1] != 7 or not params_aos.is_contiguous():
+                raise DsoError(ErrorKind.InvalidArgument, "params must be contiguous f64 [n, 7]")
+            n = params_aos.shape[0]
+            out = {k: self._empty((n,), torch.float64) for k in ("cost", "energy", "time")}
+            out["idx"] = self._empty((n,), torch.int32)
+            out["kstatus"] = self._empty((n,), torch.int32)
+            out["candidates"] = self._empty((n,), torch.int64)
+            out["fallback"] = self._empty((n,), torch.uint8)
+            out["presnap"] = self._empty((n, 3), torch.float64)
+            flags = 0
+        else:
+            params_aos = np.ascontiguousarray(params_aos, np.float64).reshape(-1, 7)
+            n = len(params_aos)
+            out = {k: np.empty(n) for k in ("cost", "energy", "time")}
+            out["idx"] = np.empty(n, np.int32)
+            out["kstatus"] = np.empty(n, np.int32)
+            out["candidates"] = np.empty(n, np.int64)
+            out["fallback"] = np.empty(n, np.uint8)
+            out["presnap"] = np.empty((n, 3))
+            flags = DSO_HOST
+        self._raise(self._lib.dso_optimal_config(
+            self._h, _ptr(params_aos), n, eta, pmax, _ptr(out["idx"]), _ptr(out["cost"]),
+            _ptr(out["energy"]), _ptr(out["time"]), _ptr(out["candidates"]),
+            _ptr(out["fallback"]), _ptr(out["presnap"]), _ptr(out["kstatus"]), flags))
+        return out
+
     def eta_sweep(self, params, etas, pmax_w: float | None = None, n: int | None = None):
         """brute_force_config at every eta: (idx [n_eta, ld], cost [n_eta, ld])."""
         _check(params, torch.float32, 7, "params")

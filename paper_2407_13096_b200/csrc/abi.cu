@@ -8,6 +8,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <cmath>
 #include <new>
 #include <string>
 #include <vector>
@@ -181,6 +182,8 @@ int32_t dso_ctx_destroy(dso_ctx* ctx) {
     cudaFree(c.dom.mem2);
     cudaFree(c.dom.core_d);
     cudaFree(c.dom.mem_d);
+    cudaFree(c.dom.g1_d);
+    cudaFree(c.dom.sd_g1);
     cudaFree(c.model.wt);
     cudaFree(c.model.w_master);
     cudaFree(c.scratch);
@@ -257,6 +260,8 @@ int32_t dso_set_domain(dso_ctx* ctx, const double* core, int32_t nc, const doubl
     std::vector<float4> core4(nc);
     std::vector<float2> mem2(nm);
     std::vector<double2> core_d(nc);
+    std::vector<double> g1(nc);
+    std::vector<int> sd(nc);
     for (int i = 0; i < nc; ++i) {
         // required_voltage_mhz (dvfs_model.hpp:117-128), in double
         const double norm = core[i] / dev[4];
@@ -265,7 +270,14 @@ int32_t dso_set_domain(dso_ctx* ctx, const double* core, int32_t nc, const doubl
         core4[i] = make_float4((float)vc, (float)(vc * vc * core[i]), (float)(1.0 / core[i]),
                                (float)core[i]);
         core_d[i] = make_double2(vc, core[i]);
+        // to_mhz(max_core_freq(vc)) (dvfs_model.hpp:107-113, optimizer.cpp:141-142)
+        g1[i] = (std::sqrt((vc - dev[0]) / 2.0) + dev[0]) * dev[4];
         c.dom_core[i] = core[i];
+    }
+    for (int i = 0; i < nc; ++i) {  // snap_down(cores, g1) (optimizer.cpp:43-48)
+        sd[i] = -1;
+        for (int j = 0; j < nc; ++j)
+            if (core[j] <= g1[i] * (1.0 + 1e-12)) sd[i] = j;
     }
     for (int j = 0; j < nm; ++j) {
         mem2[j] = make_float2((float)mem[j], (float)(1.0 / mem[j]));
@@ -284,6 +296,10 @@ int32_t dso_set_domain(dso_ctx* ctx, const double* core, int32_t nc, const doubl
     DSO_CUDA(ctx, cudaMemcpy(c.dom.core_d, core_d.data(), sizeof(double2) * nc,
                              cudaMemcpyHostToDevice));
     DSO_CUDA(ctx, cudaMemcpy(c.dom.mem_d, mem, sizeof(double) * nm, cudaMemcpyHostToDevice));
+    DSO_CUDA(ctx, ensure(c.dom.g1_d, nc));
+    DSO_CUDA(ctx, ensure(c.dom.sd_g1, nc));
+    DSO_CUDA(ctx, cudaMemcpy(c.dom.g1_d, g1.data(), sizeof(double) * nc, cudaMemcpyHostToDevice));
+    DSO_CUDA(ctx, cudaMemcpy(c.dom.sd_g1, sd.data(), sizeof(int) * nc, cudaMemcpyHostToDevice));
     c.dom.nc = nc;
     c.dom.nm = nm;
     // bounds that keep every f32 cost finite for params <= 1e12 and |K| <= 1e21
@@ -496,6 +512,65 @@ int32_t dso_sweep_f64(dso_ctx* ctx, const double* params, int64_t n, double eta,
         if (time) DSO_CUDA(ctx, cudaMemcpyAsync(time + off, dt, 8 * m, cudaMemcpyDeviceToHost, c.stream));
         if (kstatus)
             DSO_CUDA(ctx, cudaMemcpyAsync(kstatus + off, dk, 4 * m, cudaMemcpyDeviceToHost, c.stream));
+    }
+    DSO_CUDA(ctx, cudaStreamSynchronize(c.stream));
+    return kOk;
+}
+
+int32_t dso_optimal_config(dso_ctx* ctx, const double* params, int64_t n, double eta,
+                           double pmax, int32_t* idx, double* cost, double* energy,
+                           double* time, int64_t* candidates, uint8_t* fallback,
+                           double* presnap, int32_t* kstatus, uint32_t flags) {
+    int32_t st = check_ctx(ctx, true, false);
+    if (st) return st;
+    if ((st = check_eta(ctx, eta))) return st;  // optimizer.cpp:123-124
+    if (n < 0) return fail(ctx, kInvalidArgument, "n < 0");
+    if (!idx) return fail(ctx, kInvalidArgument, "idx output is required");
+    const double K = (1.0 - eta) * pmax;
+    Ctx& c = ctx->c;
+    if (!(flags & DSO_HOST)) {
+        DSO_CUDA(ctx, launch_optimal_config(c, params, n, eta, K, idx, cost, energy, time,
+                                            candidates, fallback, presnap, kstatus));
+        return kOk;
+    }
+    // host buffers: stage through the device in chunks on the context stream
+    const int64_t chunk = std::min<int64_t>(std::max<int64_t>(n, 1), 1 << 21);
+    const size_t per = 7 * 8 + 3 * 8 + 8 + 3 * 8 + 4 + 4 + 1;
+    const size_t need = (size_t)chunk * per + 64;
+    if (c.scratch_bytes < need) {
+        DSO_CUDA(ctx, cudaStreamSynchronize(c.stream));
+        cudaFree(c.scratch);
+        c.scratch = nullptr;
+        c.scratch_bytes = 0;
+        DSO_CUDA(ctx, cudaMalloc(&c.scratch, need));
+        c.scratch_bytes = need;
+    }
+    double* dp = (double*)c.scratch;
+    double* dc = dp + 7 * chunk;
+    double* de = dc + chunk;
+    double* dt = de + chunk;
+    double* dps = dt + chunk;
+    int64_t* dn = (int64_t*)(dps + 3 * chunk);
+    int32_t* di = (int32_t*)(dn + chunk);
+    int32_t* dk = di + chunk;
+    uint8_t* df = (uint8_t*)(dk + chunk);
+    for (int64_t off = 0; off < n; off += chunk) {
+        const int64_t m = std::min(chunk, n - off);
+        DSO_CUDA(ctx, cudaMemcpyAsync(dp, params + 7 * off, sizeof(double) * 7 * m,
+                                      cudaMemcpyHostToDevice, c.stream));
+        DSO_CUDA(ctx, launch_optimal_config(c, dp, m, eta, K, di, dc, de, dt, dn, df, dps, dk));
+        auto back = [&](void* h, const void* d, size_t bytes) {
+            return h ? cudaMemcpyAsync(h, d, bytes, cudaMemcpyDeviceToHost, c.stream)
+                     : cudaSuccess;
+        };
+        DSO_CUDA(ctx, back(idx + off, di, 4 * m));
+        DSO_CUDA(ctx, back(cost ? cost + off : nullptr, dc, 8 * m));
+        DSO_CUDA(ctx, back(energy ? energy + off : nullptr, de, 8 * m));
+        DSO_CUDA(ctx, back(time ? time + off : nullptr, dt, 8 * m));
+        DSO_CUDA(ctx, back(candidates ? candidates + off : nullptr, dn, 8 * m));
+        DSO_CUDA(ctx, back(fallback ? fallback + off : nullptr, df, m));
+        DSO_CUDA(ctx, back(presnap ? presnap + 3 * off : nullptr, dps, 24 * m));
+        DSO_CUDA(ctx, back(kstatus ? kstatus + off : nullptr, dk, 4 * m));
     }
     DSO_CUDA(ctx, cudaStreamSynchronize(c.stream));
     return kOk;

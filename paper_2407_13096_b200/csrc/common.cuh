@@ -44,6 +44,10 @@ struct DomainDev {
     // f64 exact path: per core level {vc, fc}; per mem level fm
     double2* core_d;  // [nc]
     double* mem_d;    // [nm]
+    // optimal_config: g1 = to_mhz(max_core_freq(vc)) per level and its
+    // snap_down(cores, g1) index (optimizer.cpp:141-145), host double
+    double* g1_d;     // [nc]
+    int* sd_g1;       // [nc]
     // the f32 tables are within the bounds under which the fast exact sweep's
     // costs stay finite (sweep_core.cuh sweep_best)
     bool fast_ok;
@@ -107,6 +111,10 @@ cudaError_t launch_sweep_f64(Ctx& c, const double* params, int64_t n, double eta
 cudaError_t launch_eta_sweep(Ctx& c, const float* params, int64_t n, int64_t ld,
                              const float2* etaK_dev, int n_eta, int32_t* idx, float* cost,
                              int64_t ld_out, bool fast);
+cudaError_t launch_optimal_config(Ctx& c, const double* params, int64_t n, double eta,
+                                  double K, int32_t* idx, double* cost, double* energy,
+                                  double* time, int64_t* candidates, uint8_t* fallback,
+                                  double* presnap, int32_t* kstatus);
 cudaError_t launch_gen(Ctx& c, uint64_t root, uint64_t salt_base, int64_t first, int64_t n,
                        int64_t ld, float* params, uint32_t* counts, float* dcgm);
 cudaError_t launch_featurize(Ctx& c, const uint32_t* counts, const float* dcgm, int64_t n,
@@ -187,6 +195,21 @@ __device__ __forceinline__ float sigmoidf_fast(float z) {
 inline bool fast_sweep_ok(const Ctx& cx, float K) {
     return cx.fast_sweep && cx.dom.fast_ok && K == K && K <= 1e21f && K >= -1e21f;
 }
+
+// Two sigmoids of (acc + bias) with packed FP32x2 arithmetic around the MUFU
+// ex2/rcp: nbl = -bias*log2(e) per neuron; 1/(1 + 2^(acc*(-log2 e) + nbl)).
+__device__ __forceinline__ float2 sigmoid2_bias(float2 acc, float nbl) {
+    constexpr float kNL2E = -1.4426950408889634f;
+    const float2 z = ffma2(acc, make_float2(kNL2E, kNL2E), make_float2(nbl, nbl));
+    float e0, e1, r0, r1;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e0) : "f"(z.x));
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e1) : "f"(z.y));
+    const float2 d = fadd2(make_float2(1.f, 1.f), make_float2(e0, e1));
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r0) : "f"(d.x));
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r1) : "f"(d.y));
+    return make_float2(r0, r1);
+}
+__device__ __forceinline__ float neg_bias_log2e(float b) { return b * -1.4426950408889634f; }
 
 inline int grid_for(int64_t n, int block, int num_sms, int per_sm) {
     int64_t blocks = (n + block - 1) / block;

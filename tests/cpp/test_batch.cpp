@@ -86,6 +86,48 @@ int main() {
             CHECK(bad == 0);
         }
     }
+    // optimal_config_batch == the reference's optimal_config, every field incl.
+    // fallback / presnap (test_optimizer.cpp:101-197 scaled; knee below the
+    // core table forces the flagged brute-force fallback)
+    {
+        auto same_opt = [](const OptimizationResult& a, const OptimizationResult& b) {
+            auto eq = [](double x, double y) { return x == y || (x != x && y != y); };
+            return a.best.vc == b.best.vc && a.best.fc_mhz == b.best.fc_mhz &&
+                   a.best.fm_mhz == b.best.fm_mhz && eq(a.cost, b.cost) &&
+                   eq(a.energy_j, b.energy_j) && eq(a.time_s, b.time_s) &&
+                   a.candidates_evaluated == b.candidates_evaluated &&
+                   a.fallback == b.fallback && eq(a.presnap_vc, b.presnap_vc) &&
+                   eq(a.presnap_fc_mhz, b.presnap_fc_mhz) && eq(a.presnap_fm_mhz, b.presnap_fm_mhz);
+        };
+        for (int which = 0; which < 2; ++which) {
+            DvfsDomain d = which ? default_domain() : toy_domain();
+            Rng rng(505 + which);
+            for (double eta : {0.0, 0.5, 0.8, 1.0}) {
+                std::vector<KernelModelParams> p{kRef};
+                for (int i = 0; i < 50000; ++i) {
+                    const double s = which ? 1.0 : 0.05;
+                    KernelModelParams q{rng.uniform(40, 90) * s, rng.uniform(5, 15) * s,
+                                        rng.uniform(0.004, 0.02), rng.uniform(0.002, 0.0055),
+                                        rng.uniform(0.04, 0.3), rng.uniform(1, 440),
+                                        rng.uniform(1, 440)};
+                    if (i % 7 == 0) q.alpha = 0.0;
+                    if (i % 11 == 0) q.beta = 0.0;
+                    if (i % 13 == 0) q.beta = q.alpha * 1e-3;  // knee below the table
+                    if (!(q.alpha + q.beta > 0.0)) q.beta = 1.0;
+                    p.push_back(q);
+                }
+                auto g = optimal_config_batch(p, d, eta, d.dev.pmax_w, ctx);
+                int bad = 0, fb = 0;
+                for (std::size_t i = 0; i < p.size(); ++i) {
+                    const OptimizationResult r = optimal_config(p[i], d, eta, d.dev.pmax_w);
+                    bad += !same_opt(g[i], r);
+                    fb += r.fallback;
+                }
+                CHECK(bad == 0);
+                CHECK(fb > 0);
+            }
+        }
+    }
     // error behaviour: the reference's kinds (test_optimizer.cpp:199-214)
     {
         DvfsDomain d = default_domain();
