@@ -112,3 +112,146 @@ def epoch_batches(n: int, batch: int):
 
 def is_nan_loss(v) -> bool:
     return not math.isfinite(float(v))
+
+
+# ---------------------------------------------------------------------------
+# Training orchestration on the device model: fit_model, prediction_mape_pct,
+# cross_validate, train (reference proj/src/mlp.cpp:35-130, 348-437;
+# mlp.hpp:75-121).  The dataset is a pair of float64 arrays, features [n, 134]
+# and raw targets [n, 7] (TrainingExample, mlp.hpp:50-53).  Every epoch's
+# shuffled order is gathered on the device once; batches are then contiguous
+# column slices fed to dso_train_grad / dso_train_apply, and the epoch loss is
+# read back once per epoch.
+
+K_MAPE_FLOOR = 1e-9  # kMapeDenominatorFloor, mlp.cpp:14
+K_FOLDS = 3          # cross_validate, mlp.cpp:359
+
+
+def canonicalize(features, targets):
+    """canonicalize (mlp.cpp:35-50): lexicographic sort by features, then targets."""
+    f = np.asarray(features, np.float64)
+    t = np.asarray(targets, np.float64)
+    keys = np.concatenate([f, t], axis=1)
+    order = np.lexsort(keys.T[::-1]) if len(keys) else np.zeros(0, np.int64)
+    return f[order], t[order]
+
+
+def _dev_cols(a):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(np.asarray(a, np.float32).T)).cuda()
+
+
+def fit_model(ctx, features, targets, sizes, mean, std, lr: float, batch_size: int,
+              epochs: int, seed: int):
+    """fit_model (mlp.cpp:115-130) on the GPU: init_mlp(sizes, seed), per-epoch
+    sgd_epoch (mlp.cpp:84-112) with order shuffled_indices(Rng(seed).fork(0x5d0)),
+    loss of every batch on the pre-update weights, stop after a NaN epoch.
+    Returns (model, epoch_loss_trace)."""
+    import torch
+
+    from .model import init_mlp
+    m = init_mlp(list(sizes), seed=seed)
+    m.target_mean, m.target_std = np.array(mean, np.float64), np.array(std, np.float64)
+    ctx.set_model(m)
+    f = np.asarray(features, np.float64)
+    y = (np.asarray(targets, np.float64) - m.target_mean) / m.target_std
+    X, Y = _dev_cols(f), _dev_cols(y)
+    n = X.shape[1]
+    out_dim = Y.shape[0]
+    state = fork(seed, 0x5D0)
+    grad = torch.empty((ctx.n_model_params,), dtype=torch.float32, device=X.device)
+    trace = []
+    for _ in range(epochs):
+        order, state = shuffled_order(n, state)
+        idx = torch.from_numpy(order).to(X.device)
+        Xe, Ye = X.index_select(1, idx), Y.index_select(1, idx)
+        acc = torch.zeros((), dtype=torch.float64, device=X.device)
+        nb = 0
+        for start, b in epoch_batches(n, batch_size):
+            g, loss = ctx.train_grad_slice(Xe, Ye, start, b, grad=grad)
+            acc += loss[0] / (b * out_dim)
+            ctx.train_apply(g, lr, 1.0 / (b * out_dim))
+            nb += 1
+        v = float(acc.item()) / nb
+        v = v if math.isfinite(v) else float("nan")
+        trace.append(v)
+        if math.isnan(v):
+            break
+    return ctx.get_model(), trace
+
+
+def prediction_mape_pct(ctx, model, features, targets) -> float:
+    """prediction_mape_pct (mlp.cpp:132-146) with the device forward_raw
+    (dso_predict's raw output): inf when any prediction is non-finite."""
+    ctx.set_model(model)
+    t = np.asarray(targets, np.float64)
+    _, _, raw = ctx.predict_params(_dev_cols(features), want_raw=True)
+    pred = raw.cpu().numpy().T.astype(np.float64)
+    if not np.isfinite(pred).all():
+        return float("inf")
+    return float(100.0 * np.mean(np.abs(pred - t) / np.maximum(np.abs(t), K_MAPE_FLOOR)))
+
+
+def cross_validate(ctx, features, targets, grid, seed: int, epochs: int, sizes=None):
+    """cross_validate (mlp.cpp:348-411): 3 folds from shuffled_indices(Rng(seed)
+    .fork(0xf01d)) over the canonical order; per cell and fold a fit_model on the
+    training split with its own target_stats, run seed seed + 1000003*fold +
+    29*cell; MAPE on the validation split (inf when diverged or a split is
+    empty); lowest mean wins, ties to smaller lr, then smaller batch.
+    Returns {"table": [(lr, batch, [fold mapes], mean)], "best": (lr, batch)}."""
+    from ._lib import DsoError, ErrorKind
+    f, t = canonicalize(features, targets)
+    n = len(f)
+    if n < 3:
+        raise DsoError(ErrorKind.DatasetTooSmall,
+                       f"cross-validation needs at least 3 examples, got {n}")
+    if not grid:
+        raise DsoError(ErrorKind.InvalidArgument, "empty hyperparameter grid")
+    sizes = list(sizes) if sizes else [f.shape[1], 100, 50, 25, t.shape[1]]
+    sizes[0], sizes[-1] = f.shape[1], t.shape[1]
+    order, _ = shuffled_order(n, fork(seed, 0xF01D))
+    fold_of = np.empty(n, np.int64)
+    fold_of[order] = np.arange(n) % K_FOLDS
+    table = []
+    for ci, (lr, bs) in enumerate(grid):
+        mapes = []
+        for fold in range(K_FOLDS):
+            tr, va = fold_of != fold, fold_of == fold
+            if not tr.any() or not va.any():
+                mapes.append(float("inf"))
+                continue
+            mean, std, _ = target_stats(t[tr])
+            run_seed = (seed + 1000003 * fold + 29 * ci) & ((1 << 64) - 1)
+            m, trace = fit_model(ctx, f[tr], t[tr], sizes, mean, std, lr, bs, epochs, run_seed)
+            diverged = bool(trace) and math.isnan(trace[-1])
+            mapes.append(float("inf") if diverged else
+                         prediction_mape_pct(ctx, m, f[va], t[va]))
+        table.append((float(lr), int(bs), mapes, sum(mapes) / K_FOLDS))
+    best = table[0]
+    for row in table:
+        if row[3] < best[3] or (row[3] == best[3] and (
+                row[0] < best[0] or (row[0] == best[0] and row[1] < best[1]))):
+            best = row
+    return {"table": table, "best": (best[0], best[1])}
+
+
+def train(ctx, features, targets, grid, seed: int, epochs: int, sizes=None):
+    """train (mlp.cpp:413-437): checks, cross-validation over grid, then a final
+    fit_model on the whole canonical dataset with the winning cell.
+    Returns {"model", "cv", "epoch_loss", "degenerate_targets"}."""
+    from ._lib import DsoError, ErrorKind
+    f = np.asarray(features, np.float64)
+    t = np.asarray(targets, np.float64)
+    if len(f) < 3:
+        raise DsoError(ErrorKind.DatasetTooSmall,
+                       f"training needs at least 3 examples, got {len(f)}")
+    if not (np.isfinite(f).all() and np.isfinite(t).all()):
+        raise DsoError(ErrorKind.InvalidArgument, "dataset contains non-finite values")
+    f, t = canonicalize(f, t)
+    sizes = list(sizes) if sizes else [f.shape[1], 100, 50, 25, t.shape[1]]
+    sizes[0], sizes[-1] = f.shape[1], t.shape[1]
+    cv = cross_validate(ctx, f, t, grid, seed, epochs, sizes)
+    mean, std, degenerate = target_stats(t)
+    lr, bs = cv["best"]
+    model, trace = fit_model(ctx, f, t, sizes, mean, std, lr, bs, epochs, seed)
+    return {"model": model, "cv": cv, "epoch_loss": trace, "degenerate_targets": degenerate}

@@ -108,3 +108,88 @@ def test_training_reduces_loss(ctx, port):
         losses.append(tot)
     assert all(b <= a * (1 + 1e-9) for a, b in zip(losses, losses[1:])), losses
     assert losses[-1] < 0.99 * losses[0], losses
+
+
+# ---- orchestration: fit_model / cross_validate / train (mlp.cpp:115-130, 348-437) ----
+
+def _oracle_fit(port, feats, targets, sizes, mean, std, lr, batch, epochs, seed):
+    """fit_model restated on the double oracle (sgd_epoch, init_mlp)."""
+    from paper_2407_13096_b200.train import fork
+    ws, bs = port.init_mlp(sizes, seed)
+    m = init_mlp(list(sizes), seed=seed)
+    m.weights, m.biases = ws, bs
+    m.target_mean, m.target_std = mean, std
+    state = fork(seed, 0x5D0)
+    trace = []
+    for _ in range(epochs):
+        loss, m.weights, m.biases, state = port.sgd_epoch(m, feats, targets, mean, std, lr,
+                                                          batch, state)
+        trace.append(loss)
+        if np.isnan(loss):
+            break
+    return m, trace
+
+
+def _corpus(port, n, root):
+    g = port.gen_stream(root, n, want=("params", "fused"))
+    return g["fused"], g["params"]
+
+
+def test_fit_model_vs_oracle(ctx, port):
+    from paper_2407_13096_b200.train import canonicalize, fit_model, target_stats as ts
+    f, t = canonicalize(*_corpus(port, 40, 0xACCE5505))
+    sizes = [134, 100, 50, 25, 7]
+    mean, std, _ = ts(t)
+    got, trace = fit_model(ctx, f, t, sizes, mean, std, 0.05, 8, 6, 1234)
+    want, wtrace = _oracle_fit(port, f, t, sizes, mean, std, 0.05, 8, 6, 1234)
+    assert len(trace) == len(wtrace) == 6
+    np.testing.assert_allclose(trace, wtrace, rtol=2e-4)
+    for a, b in zip(got.weights + got.biases, want.weights + want.biases):
+        assert np.abs(a - b).max() <= 2e-4 * np.abs(b).max()
+
+
+def test_cross_validate_and_train_vs_oracle(ctx, port):
+    """3 folds x 2 cells: per-fold validation MAPEs within 1e-3 relative of the
+    double oracle's, the same winning cell, and the final model's trace."""
+    from paper_2407_13096_b200.train import (canonicalize, cross_validate, fork,
+                                             shuffled_order, target_stats as ts, train)
+    f0, t0 = _corpus(port, 30, 0xACCE5506)
+    grid = [(0.05, 8), (0.02, 16)]
+    seed, epochs = 99, 8
+    cv = cross_validate(ctx, f0, t0, grid, seed, epochs)
+    f, t = canonicalize(f0, t0)
+    order, _ = shuffled_order(len(f), fork(seed, 0xF01D))
+    fold_of = np.empty(len(f), np.int64)
+    fold_of[order] = np.arange(len(f)) % 3
+    sizes = [134, 100, 50, 25, 7]
+    for ci, (lr, bs) in enumerate(grid):
+        for fold in range(3):
+            tr, va = fold_of != fold, fold_of == fold
+            mean, std, _ = ts(t[tr])
+            m, _ = _oracle_fit(port, f[tr], t[tr], sizes, mean, std, lr, bs, epochs,
+                               seed + 1000003 * fold + 29 * ci)
+            pred = port.forward_raw(m, f[va])
+            mape = 100 * np.mean(np.abs(pred - t[va]) / np.maximum(np.abs(t[va]), 1e-9))
+            assert cv["table"][ci][2][fold] == pytest.approx(mape, rel=1e-3)
+    means = [row[3] for row in cv["table"]]
+    assert cv["best"] == grid[int(np.argmin(means))]
+    res = train(ctx, f0, t0, grid, seed, epochs)
+    assert res["cv"]["best"] == cv["best"]
+    assert len(res["epoch_loss"]) == epochs
+
+
+def test_train_errors(ctx):
+    from paper_2407_13096_b200 import DsoError, ErrorKind
+    from paper_2407_13096_b200.train import cross_validate, train
+    f, t = np.random.rand(2, 134), np.random.rand(2, 7)
+    with pytest.raises(DsoError) as e:
+        train(ctx, f, t, [(0.1, 8)], 1, 1)
+    assert e.value.kind == ErrorKind.DatasetTooSmall
+    f, t = np.random.rand(5, 134), np.random.rand(5, 7)
+    t[2, 3] = np.nan
+    with pytest.raises(DsoError) as e:
+        train(ctx, f, t, [(0.1, 8)], 1, 1)
+    assert e.value.kind == ErrorKind.InvalidArgument
+    with pytest.raises(DsoError) as e:
+        cross_validate(ctx, np.random.rand(5, 134), np.random.rand(5, 7), [], 1, 1)
+    assert e.value.kind == ErrorKind.InvalidArgument
