@@ -946,10 +946,17 @@ __device__ __forceinline__ void consumer_sweep(const float* sm, float* out, cons
 
 enum { MODE_PRED = 0, MODE_DENSE = 1, MODE_CSR = 2 };
 
+// Where the pipeline's grid sweep runs: on the producer warps (which then also
+// clamp and write the results) or at the end of each consumer group's tile.
+#ifndef DSO_SWEEP_ON_PRODUCER
+#define DSO_SWEEP_ON_PRODUCER 0
+#endif
+
 template <int MODE>
 __global__ void __launch_bounds__(kThreads, 1)
     ws_kernel(const float* __restrict__ packed, Stats stats, Job J) {
     constexpr bool PIPE = MODE != MODE_PRED;
+    constexpr bool CSWEEP = PIPE && !DSO_SWEEP_ON_PRODUCER;  // consumers sweep
     extern __shared__ __align__(16) float sm[];
     // ---- stage model, stats, tables (all threads) -----------------------------
     {
@@ -995,7 +1002,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             consumer_tile(sm, sm + ACT + b * kActFloats, sm + OUT + b * kOutFloats,
                           reinterpret_cast<const uint32_t*>(sm + ROWS) + b * kRowWords,
                           reinterpret_cast<const int*>(sm + ROWCNT)[b], ct, BAR_CONS0 + G);
-            if (PIPE) {
+            if (CSWEEP) {
                 PT_BEGIN(t_s);
                 consumer_sweep(sm, sm + OUT + b * kOutFloats, J,
                                (blockIdx.x + i * gridDim.x) * (int64_t)TM, ct, BAR_CONS0 + G);
@@ -1049,7 +1056,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             PT_END(10, t_f);
             bar_arrive(BAR_FULL0 + b, kHandoff);
         };
-        if (!PIPE) {
+        if (!CSWEEP) {
             for (int64_t i = 0; i < kBufs && i < my_tiles; ++i) finish(i, issue(i));
             for (int64_t i = 0; i < my_tiles; ++i) {
                 const int b = (int)(i % kBufs);
@@ -1059,7 +1066,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const bool more = i + kBufs < my_tiles;
                 const bool issued = more ? issue(i + kBufs) : false;  // loads fly meanwhile
                 PT_BEGIN(t_r);
-                produce_results<false>(sm, sm + OUT + b * kOutFloats, J, t0_of(i), pt);
+                produce_results<PIPE>(sm, sm + OUT + b * kOutFloats, J, t0_of(i), pt);
                 bar_sync(BAR_PROD, kProducers);
                 PT_END(9, t_r);
                 if (more) finish(i + kBufs, issued);

@@ -27,7 +27,7 @@ namespace dso_b200 {
 namespace {
 
 constexpr int TM = 64;       // samples per tile
-constexpr int RS = 68;       // row stride (floats) of activation buffers (bank padding)
+constexpr int RS = 64;       // row stride (floats) of activation buffers
 constexpr int RS2 = RS / 2;  // in float2 units
 constexpr int kThreads = 256;
 
@@ -40,14 +40,20 @@ constexpr int B1S = W4S + 25 * 8;          // [104]
 constexpr int B2S = B1S + 104;             // [56]
 constexpr int B3S = B2S + 56;              // [32]
 constexpr int B4S = B3S + 32;              // [8]
-constexpr int A0S = B4S + 8;               // [140][RS]  (rows 134..139 zero)
-constexpr int A1S = A0S + 140 * RS;        // [104][RS]
+// transposed copies for the delta recursion: [N_out][8 k-groups][TKP], k = TK*g + t
+constexpr int T2S = B4S + 8;               // W2: [50][8][16], TK 13
+constexpr int T3S = T2S + 50 * 8 * 16;     // W3: [25][8][8],  TK 7
+constexpr int T4S = T3S + 25 * 8 * 8;      // W4: [7][8][4],   TK 4
+constexpr int A0S = T4S + 7 * 8 * 4;       // [134][RS]
+constexpr int A1S = A0S + 134 * RS;        // [104][RS]
 constexpr int A2S = A1S + 104 * RS;        // [56][RS]
 constexpr int A3S = A2S + 56 * RS;         // [32][RS]
 constexpr int OS = A3S + 32 * RS;          // [8][RS]   output, then delta4
 constexpr int YS = OS + 8 * RS;            // [8][RS]   targets
 constexpr int kSmemFloats = YS + 8 * RS;
-static_assert(A0S % 4 == 0 && W2S % 4 == 0 && W3S % 4 == 0 && W4S % 4 == 0, "alignment");
+static_assert(kSmemFloats * 4 <= 227 * 1024, "shared memory");
+static_assert(A0S % 4 == 0 && W2S % 4 == 0 && W3S % 4 == 0 && W4S % 4 == 0 && T2S % 4 == 0 &&
+                  T3S % 4 == 0 && T4S % 4 == 0, "alignment");
 
 // master (reference) layout offsets: W1 | W2 | W3 | W4 | b1 | b2 | b3 | b4
 constexpr int MW1 = 0, MW2 = MW1 + 100 * 134, MW3 = MW2 + 50 * 100, MW4 = MW3 + 25 * 50;
@@ -79,8 +85,18 @@ __device__ void stage_weights(float* sm, const float* __restrict__ m) {
     for (int i = threadIdx.x; i < 50; i += kThreads) sm[B2S + i] = m[MB2 + i];
     for (int i = threadIdx.x; i < 25; i += kThreads) sm[B3S + i] = m[MB3 + i];
     for (int i = threadIdx.x; i < 7; i += kThreads) sm[B4S + i] = m[MB4 + i];
-    // zero padding rows of A0 (k = 134..139 feed gW1's 14-wide k blocks)
-    for (int i = threadIdx.x; i < 6 * RS; i += kThreads) sm[A0S + 134 * RS + i] = 0.f;
+    for (int e = threadIdx.x; e < 50 * 100; e += kThreads) {
+        const int n = e / 100, k = e - n * 100;
+        sm[T2S + (n * 8 + k / 13) * 16 + k % 13] = m[MW2 + e];
+    }
+    for (int e = threadIdx.x; e < 25 * 50; e += kThreads) {
+        const int n = e / 50, k = e - n * 50;
+        sm[T3S + (n * 8 + k / 7) * 8 + k % 7] = m[MW3 + e];
+    }
+    for (int e = threadIdx.x; e < 7 * 25; e += kThreads) {
+        const int n = e / 25, k = e - n * 25;
+        sm[T4S + (n * 8 + k / 4) * 4 + k % 4] = m[MW4 + e];
+    }
 }
 
 // Dense layer on a 64-sample tile: out[TN*g+t][m] = act(sum_k W[k][g][t] in[k][m] + b).
@@ -143,26 +159,31 @@ __device__ __forceinline__ void dense(const float* sm, int woff, int boff, int i
 // thread = (sample pair, group of TK consecutive k); weights read as scalar
 // broadcasts from the packed [K][8][TNP] layout of layer l.  Returns values in
 // registers (the caller writes them over a_l after a barrier).
-template <int KOUT, int TK, int NIN, int TN, int TNP>
-__device__ __forceinline__ void backprop(const float* sm, int woff, int din_off, int a_off,
+template <int KOUT, int TK, int NIN, int TKP>
+__device__ __forceinline__ void backprop(const float* sm, int toff, int din_off, int a_off,
                                          float2 (&res)[TK]) {
     const int mp = threadIdx.x & 31, kg = threadIdx.x >> 5;
     const float2* d2 = reinterpret_cast<const float2*>(sm + din_off);
     const float2* a2 = reinterpret_cast<const float2*>(sm + a_off);
 #pragma unroll
     for (int t = 0; t < TK; ++t) res[t] = f2(0.f, 0.f);
+    // weights W[n][TK*kg + t] are contiguous in the transposed copy (warp-uniform
+    // broadcast loads, TKP/4 LDS.128 per n)
 #pragma unroll 2
     for (int n = 0; n < NIN; ++n) {
         const float2 d = d2[n * RS2 + mp];
-        const int gofs = (n / TN) * TNP + n % TN;
+        const float4* w4 = reinterpret_cast<const float4*>(sm + toff + (n * 8 + kg) * TKP);
+        float w[TKP];
 #pragma unroll
-        for (int t = 0; t < TK; ++t) {
-            const int k = kg * TK + t;
-            if (k < KOUT) {
-                const float w = sm[woff + k * 8 * TNP + gofs];
-                res[t] = ffma2(d, f2(w, w), res[t]);
-            }
+        for (int q = 0; q < TKP / 4; ++q) {
+            const float4 v = w4[q];
+            w[4 * q] = v.x;
+            w[4 * q + 1] = v.y;
+            w[4 * q + 2] = v.z;
+            w[4 * q + 3] = v.w;
         }
+#pragma unroll
+        for (int t = 0; t < TK; ++t) res[t] = ffma2(d, f2(w[t], w[t]), res[t]);
     }
 #pragma unroll
     for (int t = 0; t < TK; ++t) {
@@ -185,64 +206,33 @@ __device__ __forceinline__ void store_delta(float* sm, int a_off, const float2 (
     }
 }
 
-// acc[i][j] += sum_m D[n0+i][m] * A[k0+j][m] over the 64 samples of the tile.
-template <int TNB, int TKB>
-__device__ __forceinline__ void outer_acc(const float* sm, int d_off, int a_off, int n0, int k0,
-                                          float (&acc)[TNB][TKB]) {
-#pragma unroll 2
-    for (int mq = 0; mq < TM / 4; ++mq) {
-        float4 d[TNB], a[TKB];
-#pragma unroll
-        for (int i = 0; i < TNB; ++i)
-            d[i] = reinterpret_cast<const float4*>(sm + d_off + (n0 + i) * RS)[mq];
-#pragma unroll
-        for (int j = 0; j < TKB; ++j)
-            a[j] = reinterpret_cast<const float4*>(sm + a_off + (k0 + j) * RS)[mq];
-#pragma unroll
-        for (int i = 0; i < TNB; ++i)
-#pragma unroll
-            for (int j = 0; j < TKB; ++j) {
-                acc[i][j] = fmaf(d[i].x, a[j].x, acc[i][j]);
-                acc[i][j] = fmaf(d[i].y, a[j].y, acc[i][j]);
-                acc[i][j] = fmaf(d[i].z, a[j].z, acc[i][j]);
-                acc[i][j] = fmaf(d[i].w, a[j].w, acc[i][j]);
-            }
+// Rows of one 64-sample tile, smem [R][RS] (feature-major) -> global rows
+// [R][lds] at column t0 (lds % 4 == 0, t0 % 64 == 0: float4 stores).
+__device__ __forceinline__ void write_rows(const float* sm, int off, int R, float* __restrict__ g,
+                                           int64_t lds, int64_t t0) {
+    for (int e = threadIdx.x; e < R * (TM / 4); e += kThreads) {
+        const int r = e / (TM / 4), q = e % (TM / 4);
+        const float4 v = reinterpret_cast<const float4*>(sm + off + r * RS)[q];
+        reinterpret_cast<float4*>(g + (int64_t)r * lds + t0)[q] = v;
     }
 }
 
-__device__ __forceinline__ float row_sum(const float* sm, int off) {
-    float s = 0.f;
-#pragma unroll
-    for (int mq = 0; mq < TM / 4; ++mq) {
-        const float4 v = reinterpret_cast<const float4*>(sm + off)[mq];
-        s += (v.x + v.y) + (v.z + v.w);
-    }
-    return s;
-}
+// Scratch rows written by train_fb_kernel (feature-major [row][lds]):
+// deltas D1 | D2 | D3 | D4 then activations A1 | A2 | A3.
+constexpr int SD1 = 0, SD2 = 100, SD3 = 150, SD4 = 175, SA1 = 182, SA2 = 282, SA3 = 332;
+constexpr int kScratchRows = 357;
 
+// Forward (forward_trace) and the backward deltas (analytic_gradients' delta
+// recursion) of 64-sample tiles; activations and deltas go to the scratch rows
+// for train_wgrad_kernel, the per-CTA loss sum to loss_partial.
 __global__ void __launch_bounds__(kThreads, 1)
-    train_grad_kernel(const float* __restrict__ master, const float* __restrict__ x,
-                      const float* __restrict__ y, int64_t n, int64_t ld,
-                      float* __restrict__ partial, double* __restrict__ loss_partial) {
+    train_fb_kernel(const float* __restrict__ master, const float* __restrict__ x,
+                    const float* __restrict__ y, int64_t n, int64_t ld,
+                    float* __restrict__ scr, int64_t lds, double* __restrict__ loss_partial) {
     extern __shared__ __align__(16) float sm[];
     stage_weights(sm, master);
     __syncthreads();
     const int tid = threadIdx.x;
-    // owned gradient blocks (threads 0..249; 250..255 own only a bias slot)
-    const bool own = tid < 250;
-    const int nb = tid / 10, kb = tid % 10;
-    float g1[4][14], g2[2][10], g3[1][5], g4[1][1], gb = 0.f;
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 14; ++j) g1[i][j] = 0.f;
-#pragma unroll
-    for (int i = 0; i < 2; ++i)
-#pragma unroll
-        for (int j = 0; j < 10; ++j) g2[i][j] = 0.f;
-#pragma unroll
-    for (int j = 0; j < 5; ++j) g3[0][j] = 0.f;
-    g4[0][0] = 0.f;
     double loss = 0.0;
 
     const int64_t tiles = (n + TM - 1) / TM;
@@ -250,9 +240,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int64_t t0 = tile * TM;
         const int valid = (int)(n - t0 < TM ? n - t0 : TM);
         // ---- stage inputs (zeros for dead samples) ------------------------------
-        for (int e = tid; e < 134 * TM; e += kThreads) {
-            const int r = e / TM, m = e - r * TM;
-            sm[A0S + r * RS + m] = m < valid ? __ldg(x + (int64_t)r * ld + t0 + m) : 0.f;
+        if (valid == TM && (ld & 3) == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0) {
+            for (int e = tid; e < 134 * (TM / 4); e += kThreads) {
+                const int r = e / (TM / 4), q = e % (TM / 4);
+                reinterpret_cast<float4*>(sm + A0S + r * RS)[q] =
+                    __ldg(reinterpret_cast<const float4*>(x + (int64_t)r * ld + t0) + q);
+            }
+        } else {
+            for (int e = tid; e < 134 * TM; e += kThreads) {
+                const int r = e / TM, m = e - r * TM;
+                sm[A0S + r * RS + m] = m < valid ? __ldg(x + (int64_t)r * ld + t0 + m) : 0.f;
+            }
         }
         for (int e = tid; e < 8 * TM; e += kThreads) {
             const int r = e / TM, m = e - r * TM;
@@ -268,6 +266,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncthreads();
         dense<25, 1, 1, false>(sm, W4S, B4S, A3S, OS);
         __syncthreads();
+        write_rows(sm, A1S, 100, scr + SA1 * lds, lds, t0);
+        write_rows(sm, A2S, 50, scr + SA2 * lds, lds, t0);
+        write_rows(sm, A3S, 25, scr + SA3 * lds, lds, t0);
         // ---- residual and loss: delta4 = out - y (dead samples 0) -----------------
         if (tid < TM) {
             float l = 0.f;
@@ -280,62 +281,28 @@ __global__ void __launch_bounds__(kThreads, 1)
             loss += 0.5 * (double)l;
         }
         __syncthreads();
-        // ---- layer 4: gW4 += d4 a3^T; d3 = (W4^T d4) .* a3(1-a3) ---------------------
-        if (tid < 175) {
-            float a4[1][1] = {{0.f}};
-            outer_acc<1, 1>(sm, OS, A3S, tid / 25, tid % 25, a4);
-            g4[0][0] += a4[0][0];
-        }
+        write_rows(sm, OS, 7, scr + SD4 * lds, lds, t0);
+        // ---- d3 = (W4^T d4) .* a3(1-a3), d2, d1 likewise ------------------------------
         float2 r3[4];
-        backprop<25, 4, 7, 1, 1>(sm, W4S, OS, A3S, r3);
+        backprop<25, 4, 7, 4>(sm, T4S, OS, A3S, r3);
         __syncthreads();
         store_delta<25, 4>(sm, A3S, r3);
         __syncthreads();
-        // ---- layer 3: gW3 += d3 a2^T; d2 = (W3^T d3) .* a2(1-a2) ---------------------
-        if (own) outer_acc<1, 5>(sm, A3S, A2S, nb, kb * 5, g3);
+        write_rows(sm, A3S, 25, scr + SD3 * lds, lds, t0);
         float2 r2[7];
-        backprop<50, 7, 25, 4, 4>(sm, W3S, A3S, A2S, r2);
+        backprop<50, 7, 25, 8>(sm, T3S, A3S, A2S, r2);
         __syncthreads();
         store_delta<50, 7>(sm, A2S, r2);
         __syncthreads();
-        // ---- layer 2: gW2 += d2 a1^T; d1 = (W2^T d2) .* a1(1-a1) ---------------------
-        if (own) outer_acc<2, 10>(sm, A2S, A1S, nb * 2, kb * 10, g2);
+        write_rows(sm, A2S, 50, scr + SD2 * lds, lds, t0);
         float2 r1[13];
-        backprop<100, 13, 50, 7, 8>(sm, W2S, A2S, A1S, r1);
+        backprop<100, 13, 50, 16>(sm, T2S, A2S, A1S, r1);
         __syncthreads();
         store_delta<100, 13>(sm, A1S, r1);
         __syncthreads();
-        // ---- layer 1: gW1 += d1 a0^T; biases -------------------------------------------
-        if (own) outer_acc<4, 14>(sm, A1S, A0S, nb * 4, kb * 14, g1);
-        if (tid < 100)
-            gb += row_sum(sm, A1S + tid * RS);
-        else if (tid < 150)
-            gb += row_sum(sm, A2S + (tid - 100) * RS);
-        else if (tid < 175)
-            gb += row_sum(sm, A3S + (tid - 150) * RS);
-        else if (tid < 182)
-            gb += row_sum(sm, OS + (tid - 175) * RS);
+        write_rows(sm, A1S, 100, scr + SD1 * lds, lds, t0);
         __syncthreads();
     }
-    // ---- write this CTA's partial gradient (master layout) ----------------------------
-    float* P = partial + (int64_t)blockIdx.x * kMasterFloats;
-    if (own) {
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-            for (int j = 0; j < 14; ++j) {
-                const int nn = nb * 4 + i, k = kb * 14 + j;
-                if (k < 134) P[MW1 + nn * 134 + k] = g1[i][j];
-            }
-#pragma unroll
-        for (int i = 0; i < 2; ++i)
-#pragma unroll
-            for (int j = 0; j < 10; ++j) P[MW2 + (nb * 2 + i) * 100 + kb * 10 + j] = g2[i][j];
-#pragma unroll
-        for (int j = 0; j < 5; ++j) P[MW3 + nb * 50 + kb * 5 + j] = g3[0][j];
-    }
-    if (tid < 175) P[MW4 + (tid / 25) * 25 + tid % 25] = g4[0][0];
-    if (tid < 182) P[MB1 + tid] = gb;
     // loss: block reduce of the 64 per-sample-thread partials
     __shared__ double red[kThreads / 32];
     double v = loss;
@@ -347,6 +314,182 @@ __global__ void __launch_bounds__(kThreads, 1)
         double s = 0.0;
         for (int w = 0; w < kThreads / 32; ++w) s += red[w];
         loss_partial[blockIdx.x] = s;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Weight gradients gW_l = D_l A_{l-1}^T and bias gradients sum_m D_l, summed
+// over a contiguous sample range per CTA (split-K; partials reduced in CTA order
+// by reduce_partials).  Chunks of 32 samples are staged TRANSPOSED into shared
+// memory (sample-major: one 532-float record per sample holding D1 | A0 | D2 |
+// A1 | D3 | A2 | D4 | A3), so a thread's 8x8 output tile accumulates with packed
+// FFMA2 over k pairs: {g[n][k], g[n][k+1]} += d[m][n] * {a[m][k], a[m][k+1]}
+// (4 LDS.128 per 32 FFMA2).  The next chunk's global loads are issued before
+// the current chunk's math (register double-buffering).
+constexpr int WG_THREADS = 384;
+constexpr int WG_CHUNK = 32;
+constexpr int WG_REC = 532;  // floats per sample record (16-byte multiple, 133 odd)
+// record offsets (padded row counts: 104 | 136 | 56 | 104 | 32 | 56 | 8 | 32)
+constexpr int RD1 = 0, RA0 = 104, RD2 = 240, RA1 = 296, RD3 = 400, RA2 = 432, RD4 = 488,
+              RA3 = 496;
+constexpr int WG_ROWS = 491;  // rows staged per sample (valid rows only)
+constexpr int WG_TILES = 221 + 91 + 28 + 4;
+constexpr int WG_F4 = WG_ROWS * (WG_CHUNK / 4);  // float4 loads per chunk
+constexpr int WG_LOADS = (WG_F4 + WG_THREADS - 1) / WG_THREADS;
+
+// staged row r (0..490) -> (record offset, global source row, from x?)
+__device__ __forceinline__ void wg_row(int r, int& off, int& src, bool& from_x) {
+    from_x = false;
+    if (r < 100) { off = RD1 + r; src = SD1 + r; return; }
+    r -= 100;
+    if (r < 134) { off = RA0 + r; src = r; from_x = true; return; }
+    r -= 134;
+    if (r < 50) { off = RD2 + r; src = SD2 + r; return; }
+    r -= 50;
+    if (r < 100) { off = RA1 + r; src = SA1 + r; return; }
+    r -= 100;
+    if (r < 25) { off = RD3 + r; src = SD3 + r; return; }
+    r -= 25;
+    if (r < 50) { off = RA2 + r; src = SA2 + r; return; }
+    r -= 50;
+    if (r < 7) { off = RD4 + r; src = SD4 + r; return; }
+    r -= 7;
+    off = RA3 + r;
+    src = SA3 + r;
+}
+
+__global__ void __launch_bounds__(WG_THREADS, 1)
+    train_wgrad_kernel(const float* __restrict__ x, int64_t ld, const float* __restrict__ scr,
+                       int64_t lds, int64_t n, int64_t per_cta, float* __restrict__ partial) {
+    extern __shared__ __align__(16) float sm[];  // [2][WG_CHUNK][WG_REC]
+    const int tid = threadIdx.x;
+    const int64_t s_lo = (int64_t)blockIdx.x * per_cta;
+    const int64_t s_hi = s_lo + per_cta < n ? s_lo + per_cta : n;
+    for (int i = tid; i < 2 * WG_CHUNK * WG_REC; i += WG_THREADS) sm[i] = 0.f;  // padding
+    // this thread's output tile
+    int dOff = 0, aOff = 0, n0 = 0, k0 = 0, layer = -1;
+    if (tid < 221) { layer = 0; n0 = 8 * (tid / 17); k0 = 8 * (tid % 17); dOff = RD1; aOff = RA0; }
+    else if (tid < 312) { const int u = tid - 221; layer = 1; n0 = 8 * (u / 13); k0 = 8 * (u % 13); dOff = RD2; aOff = RA1; }
+    else if (tid < 340) { const int u = tid - 312; layer = 2; n0 = 8 * (u / 7); k0 = 8 * (u % 7); dOff = RD3; aOff = RA2; }
+    else if (tid < 344) { const int u = tid - 340; layer = 3; n0 = 0; k0 = 8 * u; dOff = RD4; aOff = RA3; }
+    float2 acc[8][4];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = make_float2(0.f, 0.f);
+    float bsum[5] = {0.f, 0.f, 0.f, 0.f, 0.f};  // bias threads: rows bt, bt+40, ...
+    const int bt = tid - WG_TILES;
+    const bool xvec = (ld & 3) == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0;
+    float4 st[WG_LOADS];
+    auto load = [&](int64_t c0) {
+#pragma unroll
+        for (int u = 0; u < WG_LOADS; ++u) {
+            const int e = tid + u * WG_THREADS;
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (e < WG_F4) {
+                const int r = e / (WG_CHUNK / 4), q = e % (WG_CHUNK / 4);
+                int off, src;
+                bool fx;
+                wg_row(r, off, src, fx);
+                const int64_t m0 = c0 + 4 * q;
+                const float* base = fx ? x + (int64_t)src * ld : scr + (int64_t)src * lds;
+                if (m0 + 4 <= s_hi && (!fx || xvec)) {
+                    v = __ldg(reinterpret_cast<const float4*>(base + m0));
+                } else {
+                    if (m0 < s_hi) v.x = __ldg(base + m0);
+                    if (m0 + 1 < s_hi) v.y = __ldg(base + m0 + 1);
+                    if (m0 + 2 < s_hi) v.z = __ldg(base + m0 + 2);
+                    if (m0 + 3 < s_hi) v.w = __ldg(base + m0 + 3);
+                }
+            }
+            st[u] = v;
+        }
+    };
+    auto store = [&](float* buf) {
+#pragma unroll
+        for (int u = 0; u < WG_LOADS; ++u) {
+            const int e = tid + u * WG_THREADS;
+            if (e < WG_F4) {
+                const int r = e / (WG_CHUNK / 4), q = e % (WG_CHUNK / 4);
+                int off, src;
+                bool fx;
+                wg_row(r, off, src, fx);
+                float* d = buf + (4 * q) * WG_REC + off;
+                d[0] = st[u].x;
+                d[WG_REC] = st[u].y;
+                d[2 * WG_REC] = st[u].z;
+                d[3 * WG_REC] = st[u].w;
+            }
+        }
+    };
+    __syncthreads();
+    int cur = 0;
+    if (s_lo < s_hi) {
+        load(s_lo);
+        store(sm);
+    }
+    __syncthreads();
+    for (int64_t c0 = s_lo; c0 < s_hi; c0 += WG_CHUNK) {
+        const bool more = c0 + WG_CHUNK < s_hi;
+        if (more) load(c0 + WG_CHUNK);  // in flight during the math below
+        const float* buf = sm + cur * WG_CHUNK * WG_REC;
+        if (layer >= 0) {
+#pragma unroll 4
+            for (int m = 0; m < WG_CHUNK; ++m) {
+                const float* rec = buf + m * WG_REC;
+                const float4 d0 = *reinterpret_cast<const float4*>(rec + dOff + n0);
+                const float4 d1 = *reinterpret_cast<const float4*>(rec + dOff + n0 + 4);
+                const float4 a0 = *reinterpret_cast<const float4*>(rec + aOff + k0);
+                const float4 a1 = *reinterpret_cast<const float4*>(rec + aOff + k0 + 4);
+                const float dv[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
+                const float2 av[4] = {make_float2(a0.x, a0.y), make_float2(a0.z, a0.w),
+                                      make_float2(a1.x, a1.y), make_float2(a1.z, a1.w)};
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+                        acc[i][j] = ffma2(make_float2(dv[i], dv[i]), av[j], acc[i][j]);
+            }
+        } else if (bt >= 0) {
+            // bias gradients: rows of D1 (100) | D2 (50) | D3 (25) | D4 (7) = 182
+#pragma unroll
+            for (int u = 0; u < 5; ++u) {
+                const int r = bt + 40 * u;
+                if (r < 182) {
+                    const int off = r < 100 ? RD1 + r
+                                  : r < 150 ? RD2 + (r - 100)
+                                  : r < 175 ? RD3 + (r - 150)
+                                            : RD4 + (r - 175);
+                    float sacc = 0.f;
+                    for (int m = 0; m < WG_CHUNK; ++m) sacc += buf[m * WG_REC + off];
+                    bsum[u] += sacc;
+                }
+            }
+        }
+        if (more) store(sm + (cur ^ 1) * WG_CHUNK * WG_REC);
+        __syncthreads();
+        cur ^= 1;
+    }
+    // ---- this CTA's partial gradient, master layout ------------------------------------
+    float* P = partial + (int64_t)blockIdx.x * kMasterFloats;
+    if (layer >= 0) {
+        const int NO[4] = {100, 50, 25, 7}, KI[4] = {134, 100, 50, 25};
+        const int WO[4] = {MW1, MW2, MW3, MW4};
+        const int no = NO[layer], ki = KI[layer], wo = WO[layer];
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int nn = n0 + i, k = k0 + 2 * j;
+                if (nn < no && k < ki) P[wo + nn * ki + k] = acc[i][j].x;
+                if (nn < no && k + 1 < ki) P[wo + nn * ki + k + 1] = acc[i][j].y;
+            }
+    } else if (bt >= 0) {
+#pragma unroll
+        for (int u = 0; u < 5; ++u) {
+            const int r = bt + 40 * u;
+            if (r < 182) P[MB1 + r] = bsum[u];
+        }
     }
 }
 
@@ -377,7 +520,11 @@ __global__ void sgd_apply(float* __restrict__ master, const float* __restrict__ 
 cudaError_t launch_train_grad(Ctx& cx, const float* x, const float* y, int64_t n, int64_t ld,
                               float* grad, double* loss_sum_dev) {
     const int parts = cx.num_sms;
-    const size_t need = (size_t)parts * kMasterFloats * sizeof(float) + parts * sizeof(double);
+    const int64_t lds = ((n + TM - 1) / TM) * TM;  // scratch row length (whole tiles)
+    const size_t part_b = (size_t)parts * kMasterFloats * sizeof(float);
+    const size_t loss_b = (size_t)parts * sizeof(double);
+    const size_t act_b = (size_t)kScratchRows * (size_t)(lds > 0 ? lds : TM) * sizeof(float);
+    const size_t need = part_b + loss_b + act_b + 256;
     if (cx.train_scratch_bytes < need) {
         cudaFree(cx.train_scratch);
         cx.train_scratch = nullptr;
@@ -388,20 +535,30 @@ cudaError_t launch_train_grad(Ctx& cx, const float* x, const float* y, int64_t n
     }
     float* partial = (float*)cx.train_scratch;
     double* lp = (double*)(partial + (size_t)parts * kMasterFloats);
+    float* act = (float*)(((uintptr_t)(lp + parts) + 255) & ~(uintptr_t)255);
     static bool attr = false;
     const size_t smem = (size_t)kSmemFloats * sizeof(float);
+    const size_t smem_wg = (size_t)2 * WG_CHUNK * WG_REC * sizeof(float);
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(train_grad_kernel,
+        cudaError_t e = cudaFuncSetAttribute(train_fb_kernel,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        e = cudaFuncSetAttribute(train_wgrad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem_wg);
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    // CTAs with no tile still write zero partials, so every slot is defined
-    train_grad_kernel<<<parts, kThreads, smem, cx.stream>>>(cx.model.w_master, x, y, n, ld,
-                                                            partial, lp);
+    // CTAs with no tile / no samples still write their (zero) partials
+    train_fb_kernel<<<parts, kThreads, smem, cx.stream>>>(cx.model.w_master, x, y, n, ld, act,
+                                                          lds, lp);
+    int64_t per = (n + parts - 1) / parts;
+    per = ((per + WG_CHUNK - 1) / WG_CHUNK) * WG_CHUNK;
+    if (per == 0) per = WG_CHUNK;
+    train_wgrad_kernel<<<parts, WG_THREADS, smem_wg, cx.stream>>>(x, ld, act, lds, n, per,
+                                                                  partial);
     reduce_partials<<<(kMasterFloats + 255) / 256, 256, 0, cx.stream>>>(partial, parts, lp, grad,
                                                                         loss_sum_dev);
-    cx.launches += 2;
+    cx.launches += 3;
     return cudaGetLastError();
 }
 
