@@ -184,6 +184,8 @@ int32_t dso_ctx_destroy(dso_ctx* ctx) {
     cudaFree(c.dom.mem_d);
     cudaFree(c.dom.g1_d);
     cudaFree(c.dom.sd_g1);
+    cudaFree(c.eta_dev);
+    cudaFree(c.flag_dev);
     cudaFree(c.model.wt);
     cudaFree(c.model.w_master);
     cudaFree(c.scratch);
@@ -435,13 +437,12 @@ int32_t dso_dcgm_mean(dso_ctx* ctx, const double* samples, int64_t rows, int64_t
     if (st) return st;
     if ((st = check_batch(ctx, n, ld))) return st;
     if (rows < 1) return fail(ctx, kEmptyTrace, "no data rows");
-    int* flag = nullptr;
-    DSO_CUDA(ctx, cudaMallocAsync(&flag, sizeof(int), ctx->c.stream));
+    if (!ctx->c.flag_dev) DSO_CUDA(ctx, cudaMalloc(&ctx->c.flag_dev, sizeof(int)));
+    int* flag = ctx->c.flag_dev;
     DSO_CUDA(ctx, cudaMemsetAsync(flag, 0, sizeof(int), ctx->c.stream));
     DSO_CUDA(ctx, launch_dcgm_mean(ctx->c, samples, rows, n, ld, out, bad_row, flag));
     int h = 0;
     DSO_CUDA(ctx, cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->c.stream));
-    DSO_CUDA(ctx, cudaFreeAsync(flag, ctx->c.stream));
     DSO_CUDA(ctx, cudaStreamSynchronize(ctx->c.stream));
     if (h) return fail(ctx, kOutOfRange, "metric value outside [0, 1] (see bad_row)");
     return kOk;
@@ -590,15 +591,22 @@ int32_t dso_eta_sweep(dso_ctx* ctx, const float* params, int64_t n, int64_t ld,
         ek[e] = make_float2((float)etas[e], (float)((1.0 - etas[e]) * pmax));
     }
     Ctx& c = ctx->c;
-    float2* d = nullptr;
-    DSO_CUDA(ctx, cudaMallocAsync(&d, sizeof(float2) * n_eta, c.stream));
-    DSO_CUDA(ctx, cudaMemcpyAsync(d, ek.data(), sizeof(float2) * n_eta, cudaMemcpyHostToDevice,
-                                  c.stream));
+    // per-context eta table (grown on demand); a pageable H2D copy returns once
+    // the host data is staged, so ek may go out of scope afterwards
+    if (c.eta_cap < n_eta) {
+        DSO_CUDA(ctx, cudaStreamSynchronize(c.stream));
+        cudaFree(c.eta_dev);
+    cudaFree(c.flag_dev);
+        c.eta_dev = nullptr;
+        c.eta_cap = 0;
+        DSO_CUDA(ctx, cudaMalloc(&c.eta_dev, sizeof(float2) * n_eta));
+        c.eta_cap = n_eta;
+    }
+    DSO_CUDA(ctx, cudaMemcpyAsync(c.eta_dev, ek.data(), sizeof(float2) * n_eta,
+                                  cudaMemcpyHostToDevice, c.stream));
     bool fast = true;
     for (int e = 0; e < n_eta; ++e) fast = fast && fast_sweep_ok(c, ek[e].y);
-    DSO_CUDA(ctx, launch_eta_sweep(c, params, n, ld, d, n_eta, idx, cost, ld_out, fast));
-    DSO_CUDA(ctx, cudaFreeAsync(d, c.stream));
-    DSO_CUDA(ctx, cudaStreamSynchronize(c.stream));  // ek lifetime
+    DSO_CUDA(ctx, launch_eta_sweep(c, params, n, ld, c.eta_dev, n_eta, idx, cost, ld_out, fast));
     return kOk;
 }
 

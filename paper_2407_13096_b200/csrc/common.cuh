@@ -88,6 +88,9 @@ struct Ctx {
     cudaEvent_t ev[8] = {};
     int num_sms = 148;
     bool fast_sweep = true;         // dso_set_option("fast_sweep")
+    float2* eta_dev = nullptr;      // dso_eta_sweep's (eta, K) table
+    int eta_cap = 0;
+    int* flag_dev = nullptr;        // dso_dcgm_mean's out-of-range flag
     void* train_scratch = nullptr;  // per-CTA partial gradients
     size_t train_scratch_bytes = 0;
 };

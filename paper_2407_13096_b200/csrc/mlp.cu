@@ -61,7 +61,7 @@ constexpr int kConsumerRegs = 160;
 static_assert(kProducers * kProducerRegs + kConsumers * kConsumerRegs <= 65536, "RF budget");
 
 // Named barriers (0 is __syncthreads).
-constexpr int BAR_PROD = 1, BAR_CONS0 = 2, BAR_FULL0 = 4, BAR_READY0 = 7;
+constexpr int BAR_PROD = 1, BAR_CONS0 = 2, BAR_FULL0 = 4, BAR_READY0 = 7, BAR_START = 10;
 
 // Packed model (floats), k-major.  Consumer warp g (0..3) of a group owns a
 // neuron block; inside it lane = 2*mg + ng: kernel quad mg (kernels 4mg..4mg+3)
@@ -157,7 +157,8 @@ __device__ __forceinline__ void bar_arrive(int id, int count) {
 // L1), not by other warps.  Weights are warp-uniform -> shared-memory
 // broadcasts; an activation pair load is 256 contiguous bytes per warp.
 __device__ __forceinline__ void consumer_tile(const float* W, float* act, float* out,
-                                              const uint32_t* rows, int nrows, int ct, int cbar) {
+                                              const uint32_t* rows, int nrows, int ct, int cbar,
+                                              bool signal_start = false) {
     float2* act2 = reinterpret_cast<float2*>(act);  // [row][32] kernel pairs
     const int mp = ct & 31;
     const int g = ct >> 5;
@@ -280,6 +281,10 @@ __device__ __forceinline__ void consumer_tile(const float* W, float* act, float*
             math(B);
         }
         PT_END(3, t_l2);
+        // group 0's first tile releases group 1 here (BAR_START): the groups then
+        // run half a tile apart, so one group's epilogues / sweep overlap the
+        // other's FFMA2 streams instead of coinciding with them
+        if (signal_start) bar_arrive(BAR_START, 2 * kGroupThreads);
         PT_BEGIN(t_e2);
         bar_sync(cbar, kGroupThreads);
         const int n0 = g * 14 + ng * 7;
@@ -994,6 +999,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kConsumerRegs));
         const int G = (tid - kProducers) / kGroupThreads;
         const int ct = (tid - kProducers) % kGroupThreads;
+        // stagger: group 1 starts once group 0 is half way through its first tile
+        // (group 0 arrives only if it has a tile; otherwise nobody waits)
+        const bool stagger = my_tiles > 1;
+        if (G == 1 && stagger) bar_sync(BAR_START, 2 * kGroupThreads);
         for (int64_t i = G; i < my_tiles; i += kGroups) {
             const int b = (int)(i % kBufs);
             PT_BEGIN(t_w);
@@ -1001,7 +1010,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             PT_END(0, t_w);
             consumer_tile(sm, sm + ACT + b * kActFloats, sm + OUT + b * kOutFloats,
                           reinterpret_cast<const uint32_t*>(sm + ROWS) + b * kRowWords,
-                          reinterpret_cast<const int*>(sm + ROWCNT)[b], ct, BAR_CONS0 + G);
+                          reinterpret_cast<const int*>(sm + ROWCNT)[b], ct, BAR_CONS0 + G,
+                          G == 0 && i == 0 && stagger);
             if (CSWEEP) {
                 PT_BEGIN(t_s);
                 consumer_sweep(sm, sm + OUT + b * kOutFloats, J,

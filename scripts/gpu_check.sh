@@ -20,4 +20,11 @@ nproc > $OUT/nproc.txt; lscpu >> $OUT/nproc.txt 2>&1
     python bench.py --steps 2 --warmup 1 --kernels 4194304 --no-e2e --no-cpu > $OUT/ncu_launch_bench.log 2>&1; echo "rc=$?" >> $OUT/ncu_launch_bench.log )
 ( timeout 900 ncu --set full --clock-control none --import-source on -k regex:ws_kernel -s 1 -c 1 \
     -o $OUT/prof_pipeline python bench.py --steps 1 --warmup 1 --kernels 2097152 --no-e2e --no-cpu --no-stages > $OUT/ncu_full.log 2>&1; echo "rc=$?" >> $OUT/ncu_full.log )
+( timeout 600 ncu --set full --clock-control none --import-source on -k regex:eta_sweep_fast -s 1 -c 1 \
+    -o $OUT/prof_eta python bench.py --config c4 --steps 1 --warmup 1 --kernels 1048576 --no-cpu > $OUT/ncu_eta.log 2>&1; echo "rc=$?" >> $OUT/ncu_eta.log )
+( timeout 600 ncu --set full --clock-control none --import-source on -k regex:"train_fb|train_wgrad" -s 2 -c 2 \
+    -o $OUT/prof_train python bench.py --config c5 --steps 1 --warmup 1 --no-cpu > $OUT/ncu_train.log 2>&1; echo "rc=$?" >> $OUT/ncu_train.log )
+( timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_c5.csv \
+    python bench.py --config c5 --steps 2 --warmup 1 --no-cpu > /dev/null 2>&1 )
+( timeout 300 python scripts/phase_timing.py > $OUT/phase_timing.txt 2>&1 )
 ls -la $OUT

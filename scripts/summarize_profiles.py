@@ -55,6 +55,26 @@ if os.path.exists(rep):
         out = subprocess.run([sys.executable, "scripts/ncu_lines.py", rep, "40"],
                              capture_output=True, text=True).stdout
         f.write(out)
+# secondary kernels: eta sweep (C4) and training (C5) key metrics
+for rep_name, tag in (("prof_eta.ncu-rep", "eta_sweep"), ("prof_train.ncu-rep", "train")):
+    rp = os.path.join(src, rep_name)
+    if not os.path.exists(rp):
+        continue
+    txt = subprocess.run(["ncu", "-i", rp, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
+    rows = list(csv.reader(io.StringIO(txt)))
+    with open(os.path.join(dst, f"ncu_{tag}_metrics.txt"), "w") as f:
+        f.write(f"# ncu --set full --clock-control none capture of {rp}\n")
+        for vals in rows[2:]:
+            d = dict(zip(rows[0], vals))
+            u = dict(zip(rows[0], rows[1]))
+            f.write(f"## {d.get('Kernel Name')}\n")
+            for k in KEYS[1:]:
+                f.write(f"{k}\t{d.get(k)}\t{u.get(k, '')}\n")
+for extra in ("phase_timing.txt", "launches_c5.csv"):
+    p = os.path.join(src, extra)
+    if os.path.exists(p):
+        shutil.copy(p, os.path.join(dst, extra))
 lc = os.path.join(src, "launches.csv")
 if os.path.exists(lc):
     rows = list(csv.reader(open(lc)))
