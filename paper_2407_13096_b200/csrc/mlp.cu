@@ -97,10 +97,9 @@ __host__ __device__ __forceinline__ int pk_w4(int nn, int k) { return W4S + k * 
 // per-CTA shared memory beyond the model
 constexpr int ACT = kModelFloats;           // act[3][134][RS]
 constexpr int kActFloats = 134 * RS;
-// out[3][11][RS]: rows 0..6 raw predictions, rows 8..10 the upper half's sweep
-// result (cost, energy, index) for the consumer-side merge
+// out[3][8][RS]: rows 0..6 raw predictions
 constexpr int OUT = ACT + kBufs * kActFloats;
-constexpr int kOutFloats = 11 * RS;
+constexpr int kOutFloats = 8 * RS;
 constexpr int SCR = OUT + kBufs * kOutFloats;   // producer scratch: tf[3][64] rr[3][64]
 constexpr int kScrFloats = 6 * TM + 6 * TM;  // tf[3][64], rr[3][64] + part u64[3][64]
 static_assert(kScrFloats >= 3 * TPK * TM, "sweep merge scratch");
@@ -113,10 +112,13 @@ constexpr int ROWS = MBAR + 8;              // u32 [3][68]
 constexpr int kRowWords = 68;
 constexpr int ROWCNT = ROWS + kBufs * kRowWords;  // int [3] (+1 pad)
 constexpr int MASKW = ROWCNT + 4;           // u32 [4]: slots 0..125 present in the tile
-constexpr int TABLES = MASKW + 4;           // core4[nc], mem2[nm]
+constexpr int kCSweep = 64;                 // kernels per tile swept by the consumer group
+constexpr int CSCR = MASKW + 4;             // consumer merge scratch [2 groups][3][4][32]
+constexpr int kCScrFloats = 3 * (kGroupThreads / kCSweep) * kCSweep;
+constexpr int TABLES = CSCR + 2 * kCScrFloats;  // core4[nc], mem2[nm]
 static_assert(W2S % 4 == 0 && W3S % 4 == 0 && W4S % 4 == 0 && B1S % 4 == 0 &&
                   kModelFloats % 4 == 0 && ACT % 4 == 0 && OUT % 4 == 0 && SCR % 4 == 0 &&
-                  MBAR % 2 == 0 && ROWS % 4 == 0 && TABLES % 4 == 0,
+                  MBAR % 2 == 0 && ROWS % 4 == 0 && TABLES % 4 == 0 && CSCR % 4 == 0,
               "16-byte alignment of smem regions");
 
 // master (reference) layout offsets: W1 | W2 | W3 | W4 | b1 | b2 | b3 | b4
@@ -815,23 +817,106 @@ __device__ __forceinline__ void csr_features(float* act, float* scr, const Job& 
     }
 }
 
-// Producer: finish a tile from its raw predictions in out: clamp and either
-// write the parameters (predict) or sweep the grid (pipeline).  TPK threads per
-// kernel, each a contiguous quarter of the core levels.  Thread pt takes kernel
-// pt % 64 and quarter pt / 64, so a warp's 32 lanes read the SAME core-level
-// entry (a broadcast, not a 4-way bank conflict per quarter-warp); the quarters
-// meet through the producer scratch (free here: the feature stage that uses it
-// is ordered before and after by producer barriers).
-template <bool PIPE>
-__device__ __forceinline__ void produce_results(const float* sm, const float* out, const Job& J,
-                                                int64_t t0, int pt) {
-    const int m = pt % TM, qtr = pt / TM;
-    const int64_t k = t0 + m;
+template <int UNR>
+__device__ __forceinline__ Best sweep_dispatch(const KParams& p, const float4* s_core,
+                                               const float2* s_mem, const Job& J, int i_lo,
+                                               int i_hi) {
+    Best b{__int_as_float(0x7fc00000), __int_as_float(0x7fc00000), -1};  // i = -1: empty part
+    if (i_lo >= i_hi) return b;
+    const int nm = J.nm;
+    if (nm == 4) return sweep_best<4, UNR>(p, s_core, s_mem, 4, i_lo, i_hi, J.eta, J.K, J.fast);
+    if (nm == 1) return sweep_best<1, UNR>(p, s_core, s_mem, 1, i_lo, i_hi, J.eta, J.K, J.fast);
+    if (nm == 3) return sweep_best<3, UNR>(p, s_core, s_mem, 3, i_lo, i_hi, J.eta, J.K, J.fast);
+    if (nm == 2) return sweep_best<2, UNR>(p, s_core, s_mem, 2, i_lo, i_hi, J.eta, J.K, J.fast);
+    return sweep_best<0, UNR>(p, s_core, s_mem, nm, i_lo, i_hi, J.eta, J.K, false);
+}
+
+// Merge P parts [P][NK] of (cost, energy, index) for kernel m (merge_best is
+// exact in any order; an empty part has index -1).
+template <int P, int NK>
+__device__ __forceinline__ Best merge_parts(const float* xc, int m) {
+    const float* xe = xc + P * NK;
+    const int* xi = reinterpret_cast<const int*>(xe + P * NK);
+    Best r{0.f, 0.f, -1};
+#pragma unroll
+    for (int q = 0; q < P; ++q) {
+        const Best o{xc[q * NK + m], xe[q * NK + m], xi[q * NK + m]};
+        if (o.i < 0) continue;
+        if (r.i < 0)
+            r = o;
+        else
+            merge_best(r, o);
+    }
+    return r;
+}
+
+// Results of one kernel of the tile: clamp flag / params / argmin outputs,
+// split over four output duties (part 0..3).
+__device__ __forceinline__ void write_result(const Job& J, int64_t k, int duty, const Best& r,
+                                             bool cl, const float (&pr)[7], const KParams& p,
+                                             const float4* s_core, const float2* s_mem) {
+    if (k >= J.n) return;
+    if (duty == 0) {
+        J.idx[k] = r.i;
+        if (J.cost) J.cost[k] = r.c;
+    } else if (duty == 1) {
+        if (J.energy) J.energy[k] = r.e;
+        if (J.clamped) J.clamped[k] = cl ? 1 : 0;
+    } else if (duty == 2) {
+        if (J.time) J.time[k] = time_at(p, s_core, s_mem, J.nm, r.i);
+    } else if (duty == 3 && J.params) {
+#pragma unroll
+        for (int i = 0; i < 7; ++i) J.params[i * J.ld_out + k] = pr[i];
+    }
+}
+
+// Consumer group, pipeline modes: right after L4 it reads the predictions of
+// kernels [0, kCSweep) of its tile, releases the buffer to the producer
+// (READY: act free, out readable — the producer sweeps kernels [kCSweep, 64)),
+// then clamps and sweeps its own kernels, 4 threads per kernel (a quarter of
+// the core levels each; a warp reads one core level at a time: a broadcast),
+// merging the quarters through its own scratch cs.
+__device__ __forceinline__ void consumer_sweep(const float* sm, const float* out, const Job& J,
+                                               int64_t t0, int ct, int cbar, int ready_bar,
+                                               float* cs) {
+    constexpr int P = kGroupThreads / kCSweep;
+    const int m = ct % kCSweep, part = ct / kCSweep;
+    bar_sync(cbar, kGroupThreads);  // L4 outputs in out
     float pr[7];
 #pragma unroll
     for (int i = 0; i < 7; ++i) pr[i] = out[i * RS + m];
+    bar_arrive(ready_bar, kHandoff);  // out[b] / act[b] handed to the producer
+    const bool cl = clamp_params(pr);
+    const KParams p{pr[0], pr[1], pr[2], pr[3], pr[4], pr[5], pr[6]};
+    const float4* s_core = reinterpret_cast<const float4*>(sm + TABLES);
+    const float2* s_mem = reinterpret_cast<const float2*>(sm + TABLES + 4 * J.nc);
+    const Best b = sweep_dispatch<4>(p, s_core, s_mem, J, J.nc * part / P, J.nc * (part + 1) / P);
+    cs[part * kCSweep + m] = b.c;
+    cs[P * kCSweep + part * kCSweep + m] = b.e;
+    reinterpret_cast<int*>(cs)[2 * P * kCSweep + part * kCSweep + m] = b.i;
+    bar_sync(cbar, kGroupThreads);
+    const Best r = merge_parts<P, kCSweep>(cs, m);
+#pragma unroll
+    for (int d = 0; d < 4; ++d)  // the four output duties spread over the parts
+        if (d * P / 4 == part) write_result(J, t0 + m, d, r, cl, pr, p, s_core, s_mem);
+}
+
+enum { MODE_PRED = 0, MODE_DENSE = 1, MODE_CSR = 2 };
+
+// Producer, after READY: predict mode writes the tile's clamped parameters;
+// pipeline mode sweeps kernels [kCSweep, 64) of the tile (the consumer group
+// sweeps the rest), 8 threads per kernel (an eighth of the core levels each,
+// a warp reading one level at a time), merged through the producer scratch.
+template <bool PIPE>
+__device__ __forceinline__ void produce_results(const float* sm, const float* out, const Job& J,
+                                                int64_t t0, int pt) {
     if (!PIPE) {
-        if (qtr == 0 && k < J.n) {
+        const int m = pt % TM;
+        const int64_t k = t0 + m;
+        if (pt < TM && k < J.n) {
+            float pr[7];
+#pragma unroll
+            for (int i = 0; i < 7; ++i) pr[i] = out[i * RS + m];
             if (J.raw)
 #pragma unroll
                 for (int i = 0; i < 7; ++i) J.raw[i * J.ld_out + k] = pr[i];
@@ -842,69 +927,11 @@ __device__ __forceinline__ void produce_results(const float* sm, const float* ou
         }
         return;
     }
-    const bool cl = clamp_params(pr);
-    const KParams p{pr[0], pr[1], pr[2], pr[3], pr[4], pr[5], pr[6]};
-    const float4* s_core = reinterpret_cast<const float4*>(sm + TABLES);
-    const float2* s_mem = reinterpret_cast<const float2*>(sm + TABLES + 4 * J.nc);
-    const int nc = J.nc, nm = J.nm;
-    // part qtr sweeps core levels [i_lo, i_hi): contiguous parts in visit order
-    const int i_lo = nc * qtr / TPK, i_hi = nc * (qtr + 1) / TPK;
-    Best b{__int_as_float(0x7fc00000), __int_as_float(0x7fc00000), -1};  // i = -1: empty part
-    if (i_lo < i_hi) {
-        if (nm == 4)
-            b = sweep_best<4>(p, s_core, s_mem, 4, i_lo, i_hi, J.eta, J.K, J.fast);
-        else if (nm == 1)
-            b = sweep_best<1>(p, s_core, s_mem, 1, i_lo, i_hi, J.eta, J.K, J.fast);
-        else if (nm == 3)
-            b = sweep_best<3>(p, s_core, s_mem, 3, i_lo, i_hi, J.eta, J.K, J.fast);
-        else
-            b = sweep_best<0>(p, s_core, s_mem, nm, i_lo, i_hi, J.eta, J.K, false);
-    }
-    // merge the quarters (merge_best is exact in any order: ties use the index)
-    float* xc = const_cast<float*>(sm) + SCR;  // [TPK][64] cost, energy, index
-    float* xe = xc + TPK * TM;
-    int* xi = reinterpret_cast<int*>(xe + TPK * TM);
-    xc[qtr * TM + m] = b.c;
-    xe[qtr * TM + m] = b.e;
-    xi[qtr * TM + m] = b.i;
-    bar_sync(BAR_PROD, kProducers);
-    Best r{0.f, 0.f, -1};
-#pragma unroll
-    for (int q = 0; q < TPK; ++q) {
-        const Best o{xc[q * TM + m], xe[q * TM + m], xi[q * TM + m]};
-        if (o.i < 0) continue;
-        if (r.i < 0)
-            r = o;
-        else
-            merge_best(r, o);
-    }
-    if (k < J.n) {
-        // output duties split over the quarters
-        if (qtr == 0) {
-            J.idx[k] = r.i;
-            if (J.cost) J.cost[k] = r.c;
-        } else if (qtr == 1) {
-            if (J.energy) J.energy[k] = r.e;
-            if (J.clamped) J.clamped[k] = cl ? 1 : 0;
-        } else if (qtr == 2) {
-            if (J.time) J.time[k] = time_at(p, s_core, s_mem, nm, r.i);
-        } else if (J.params) {
-#pragma unroll
-            for (int i = 0; i < 7; ++i) J.params[i * J.ld_out + k] = pr[i];
-        }
-    }
-}
-
-// Consumer group, pipeline modes: finish its own tile right after L4 — clamp,
-// then the grid sweep + eta objective + lexicographic argmin (sweep_best),
-// thread ct = kernel ct % 64 x half ct / 64 of the core levels (a warp reads
-// one core level at a time: a broadcast).  The upper half's result meets the
-// lower half's through out rows 8..10 (merge_best: exact in any order).
-__device__ __forceinline__ void consumer_sweep(const float* sm, float* out, const Job& J,
-                                               int64_t t0, int ct, int cbar) {
-    const int m = ct % TM, h = ct / TM;
-    const int64_t k = t0 + m;
-    bar_sync(cbar, kGroupThreads);  // L4 outputs in out
+    if constexpr (kCSweep < TM) {
+    constexpr int NK = kCSweep < TM ? TM - kCSweep : 32;  // kernels swept here
+    constexpr int P = kProducers / NK;   // parts per kernel
+    static_assert(P * NK == kProducers && 3 * P * NK <= kScrFloats, "producer sweep split");
+    const int mm = pt % NK, part = pt / NK, m = kCSweep + mm;
     float pr[7];
 #pragma unroll
     for (int i = 0; i < 7; ++i) pr[i] = out[i * RS + m];
@@ -912,56 +939,23 @@ __device__ __forceinline__ void consumer_sweep(const float* sm, float* out, cons
     const KParams p{pr[0], pr[1], pr[2], pr[3], pr[4], pr[5], pr[6]};
     const float4* s_core = reinterpret_cast<const float4*>(sm + TABLES);
     const float2* s_mem = reinterpret_cast<const float2*>(sm + TABLES + 4 * J.nc);
-    const int nc = J.nc, nm = J.nm;
-    const int i_lo = h ? nc / 2 : 0, i_hi = h ? nc : nc / 2;
-    Best b{__int_as_float(0x7fc00000), __int_as_float(0x7fc00000), -1};  // i = -1: empty half
-    if (i_lo < i_hi) {
-        if (nm == 4)
-            b = sweep_best<4>(p, s_core, s_mem, 4, i_lo, i_hi, J.eta, J.K, J.fast);
-        else if (nm == 1)
-            b = sweep_best<1>(p, s_core, s_mem, 1, i_lo, i_hi, J.eta, J.K, J.fast);
-        else if (nm == 3)
-            b = sweep_best<3>(p, s_core, s_mem, 3, i_lo, i_hi, J.eta, J.K, J.fast);
-        else if (nm == 2)
-            b = sweep_best<2>(p, s_core, s_mem, 2, i_lo, i_hi, J.eta, J.K, J.fast);
-        else
-            b = sweep_best<0>(p, s_core, s_mem, nm, i_lo, i_hi, J.eta, J.K, false);
+    const Best b = sweep_dispatch<2>(p, s_core, s_mem, J, J.nc * part / P, J.nc * (part + 1) / P);
+    float* xc = const_cast<float*>(sm) + SCR;  // [P][NK] cost, energy, index
+    xc[part * NK + mm] = b.c;
+    xc[P * NK + part * NK + mm] = b.e;
+    reinterpret_cast<int*>(xc)[2 * P * NK + part * NK + mm] = b.i;
+    bar_sync(BAR_PROD, kProducers);
+    if (part < 4) {
+        const Best r = merge_parts<P, NK>(xc, mm);
+        write_result(J, t0 + m, part, r, cl, pr, p, s_core, s_mem);
     }
-    if (h) {
-        out[8 * RS + m] = b.c;
-        out[9 * RS + m] = b.e;
-        reinterpret_cast<int*>(out)[10 * RS + m] = b.i;
-        if (k < J.n) {
-            if (J.clamped) J.clamped[k] = cl ? 1 : 0;
-            if (J.params)
-#pragma unroll
-                for (int i = 0; i < 7; ++i) J.params[i * J.ld_out + k] = pr[i];
-        }
-    }
-    bar_sync(cbar, kGroupThreads);
-    if (!h && k < J.n) {
-        const Best o{out[8 * RS + m], out[9 * RS + m], reinterpret_cast<const int*>(out)[10 * RS + m]};
-        if (o.i >= 0) merge_best(b, o);
-        J.idx[k] = b.i;
-        if (J.cost) J.cost[k] = b.c;
-        if (J.energy) J.energy[k] = b.e;
-        if (J.time) J.time[k] = time_at(p, s_core, s_mem, nm, b.i);
     }
 }
-
-enum { MODE_PRED = 0, MODE_DENSE = 1, MODE_CSR = 2 };
-
-// Where the pipeline's grid sweep runs: on the producer warps (which then also
-// clamp and write the results) or at the end of each consumer group's tile.
-#ifndef DSO_SWEEP_ON_PRODUCER
-#define DSO_SWEEP_ON_PRODUCER 0
-#endif
 
 template <int MODE>
 __global__ void __launch_bounds__(kThreads, 1)
     ws_kernel(const float* __restrict__ packed, Stats stats, Job J) {
     constexpr bool PIPE = MODE != MODE_PRED;
-    constexpr bool CSWEEP = PIPE && !DSO_SWEEP_ON_PRODUCER;  // consumers sweep
     extern __shared__ __align__(16) float sm[];
     // ---- stage model, stats, tables (all threads) -----------------------------
     {
@@ -1012,14 +1006,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                           reinterpret_cast<const uint32_t*>(sm + ROWS) + b * kRowWords,
                           reinterpret_cast<const int*>(sm + ROWCNT)[b], ct, BAR_CONS0 + G,
                           G == 0 && i == 0 && stagger);
-            if (CSWEEP) {
+            if (PIPE) {
+                // READY is arrived inside, as soon as the predictions are read
                 PT_BEGIN(t_s);
                 consumer_sweep(sm, sm + OUT + b * kOutFloats, J,
-                               (blockIdx.x + i * gridDim.x) * (int64_t)TM, ct, BAR_CONS0 + G);
+                               (blockIdx.x + i * gridDim.x) * (int64_t)TM, ct, BAR_CONS0 + G,
+                               BAR_READY0 + b, sm + CSCR + G * kCScrFloats);
                 PT_END(11, t_s);
+            } else {
+                bar_arrive(BAR_READY0 + b, kHandoff);  // predictions in out[b]; act[b] free
             }
-            // PIPE: tile finished, act[b]/out[b] free; PRED: predictions in out[b]
-            bar_arrive(BAR_READY0 + b, kHandoff);
         }
     } else {
         // ================================ producer ================================
@@ -1066,45 +1062,19 @@ __global__ void __launch_bounds__(kThreads, 1)
             PT_END(10, t_f);
             bar_arrive(BAR_FULL0 + b, kHandoff);
         };
-        if (!CSWEEP) {
-            for (int64_t i = 0; i < kBufs && i < my_tiles; ++i) finish(i, issue(i));
-            for (int64_t i = 0; i < my_tiles; ++i) {
-                const int b = (int)(i % kBufs);
-                PT_BEGIN(t_w);
-                bar_sync(BAR_READY0 + b, kHandoff);  // tile i predicted; act[b] free
-                PT_END(8, t_w);
-                const bool more = i + kBufs < my_tiles;
-                const bool issued = more ? issue(i + kBufs) : false;  // loads fly meanwhile
-                PT_BEGIN(t_r);
-                produce_results<PIPE>(sm, sm + OUT + b * kOutFloats, J, t0_of(i), pt);
-                bar_sync(BAR_PROD, kProducers);
-                PT_END(9, t_r);
-                if (more) finish(i + kBufs, issued);
-            }
-        } else {
-            // pipeline: the consumers finish their tiles; the producers only keep
-            // the buffers filled.  CSR entries of the next tile are prefetched
-            // into registers while the producers wait for its buffer.
-            if (MODE == MODE_CSR && my_tiles > 0) csr_prefetch(J, t0_of(0), pt, P);
-            for (int64_t i = 0; i < my_tiles; ++i) {
-                const int b = (int)(i % kBufs);
-                if (i >= kBufs) {
-                    PT_BEGIN(t_w);
-                    bar_sync(BAR_READY0 + b, kHandoff);  // tile i - kBufs finished
-                    PT_END(8, t_w);
-                }
-                bool issued;
-                if (MODE == MODE_CSR)
-                    issued = issue_tile_loads(sm + ACT + b * kActFloats, mbar + b, J.counts,
-                                              J.dcgm, t0_of(i), J.n, J.ld, vec_ok, pt, 8);
-                else
-                    issued = issue(i);
-                finish(i, issued);
-                if (MODE == MODE_CSR && i + 1 < my_tiles) csr_prefetch(J, t0_of(i + 1), pt, P);
-            }
-            // match the consumers' READY arrivals of the last tiles
-            for (int64_t i = my_tiles > kBufs ? my_tiles - kBufs : 0; i < my_tiles; ++i)
-                bar_sync(BAR_READY0 + (int)(i % kBufs), kHandoff);
+        for (int64_t i = 0; i < kBufs && i < my_tiles; ++i) finish(i, issue(i));
+        for (int64_t i = 0; i < my_tiles; ++i) {
+            const int b = (int)(i % kBufs);
+            PT_BEGIN(t_w);
+            bar_sync(BAR_READY0 + b, kHandoff);  // tile i predicted; act[b] free
+            PT_END(8, t_w);
+            const bool more = i + kBufs < my_tiles;
+            const bool issued = more ? issue(i + kBufs) : false;  // loads fly meanwhile
+            PT_BEGIN(t_r);
+            produce_results<PIPE>(sm, sm + OUT + b * kOutFloats, J, t0_of(i), pt);
+            bar_sync(BAR_PROD, kProducers);
+            PT_END(9, t_r);
+            if (more) finish(i + kBufs, issued);
         }
     }
 }

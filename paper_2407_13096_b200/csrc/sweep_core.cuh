@@ -295,7 +295,7 @@ __device__ __forceinline__ float group_min(const KParams& p, const float4* __res
 
 // Exact sweep of core levels [i_lo, i_hi) (non-empty) x all memory levels:
 // identical result to sweep_levels<NM>(..., i_lo, i_hi, ...).
-template <int NM>
+template <int NM, int UNR = 4>
 __device__ __forceinline__ Best sweep_best(const KParams& p, const float4* __restrict__ s_core,
                                            const float2* __restrict__ s_mem, int nm_rt, int i_lo,
                                            int i_hi, float eta, float K, bool fast) {
@@ -313,16 +313,16 @@ __device__ __forceinline__ Best sweep_best(const KParams& p, const float4* __res
             int bg = i_lo;
             bool tie = false;
             int i = i_lo;
-            // four independent groups per step: their loads and min trees overlap
+            // UNR independent groups per step: their loads and min trees overlap
             // (a single group is a ~80-cycle dependency chain); folded in order
 #pragma unroll 1
-            for (; i + 4 * GL <= i_hi; i += 4 * GL) {
-                float m[4];
+            for (; i + UNR * GL <= i_hi; i += UNR * GL) {
+                float m[UNR];
 #pragma unroll
-                for (int u = 0; u < 4; ++u)
+                for (int u = 0; u < UNR; ++u)
                     m[u] = group_min<NM, false>(p, s_core, Ta1, G, i + u * GL, i_hi, eta, K);
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
+                for (int u = 0; u < UNR; ++u) {
                     tie |= (m[u] == bc);
                     bg = m[u] < bc ? i + u * GL : bg;
                     bc = fminf(m[u], bc);
