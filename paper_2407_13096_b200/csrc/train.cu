@@ -236,11 +236,30 @@ __global__ void __launch_bounds__(kThreads, 1)
     double loss = 0.0;
 
     const int64_t tiles = (n + TM - 1) / TM;
+    const bool xvec = (ld & 3) == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0;
+    auto full_tile = [&](int64_t tile) { return tile * TM + TM <= n; };
+    // x of a full, aligned tile -> A0 with 16-byte cp.async (no registers); it is
+    // issued for the NEXT tile as soon as layer 1 has consumed A0, so the loads
+    // fly during layers 2..4 and the backward pass
+    auto prefetch_x = [&](int64_t tile) {
+        const int64_t t0 = tile * TM;
+        for (int e = tid; e < 134 * (TM / 4); e += kThreads) {
+            const int r = e / (TM / 4), q = e % (TM / 4);
+            const uint32_t dst = (uint32_t)__cvta_generic_to_shared(sm + A0S + r * RS + 4 * q);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst),
+                         "l"(x + (int64_t)r * ld + t0 + 4 * q)
+                         : "memory");
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    bool prefetched = false;
     for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
         const int64_t t0 = tile * TM;
         const int valid = (int)(n - t0 < TM ? n - t0 : TM);
         // ---- stage inputs (zeros for dead samples) ------------------------------
-        if (valid == TM && (ld & 3) == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0) {
+        if (prefetched) {
+            asm volatile("cp.async.wait_all;" ::: "memory");
+        } else if (valid == TM && xvec) {
             for (int e = tid; e < 134 * (TM / 4); e += kThreads) {
                 const int r = e / (TM / 4), q = e % (TM / 4);
                 reinterpret_cast<float4*>(sm + A0S + r * RS)[q] =
@@ -260,6 +279,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ---- forward (forward_trace) -------------------------------------------------
         dense<134, 13, 16, true>(sm, W1S, B1S, A0S, A1S);
         __syncthreads();
+        const int64_t next = tile + gridDim.x;
+        prefetched = next < tiles && xvec && full_tile(next);
+        if (prefetched) prefetch_x(next);
         dense<100, 7, 8, true>(sm, W2S, B2S, A1S, A2S);
         __syncthreads();
         dense<50, 4, 4, true>(sm, W3S, B3S, A2S, A3S);
@@ -328,10 +350,17 @@ __global__ void __launch_bounds__(kThreads, 1)
 // the current chunk's math (register double-buffering).
 constexpr int WG_THREADS = 384;
 constexpr int WG_CHUNK = 32;
-constexpr int WG_REC = 532;  // floats per sample record (16-byte multiple, 133 odd)
-// record offsets (padded row counts: 104 | 136 | 56 | 104 | 32 | 56 | 8 | 32)
-constexpr int RD1 = 0, RA0 = 104, RD2 = 240, RA1 = 296, RD3 = 400, RA2 = 432, RD4 = 488,
-              RA3 = 496;
+// Record layout: every operand row block of 8 (one thread tile's n or k block)
+// is stored with a 12-float stride, so the 16-byte chunks of consecutive blocks
+// fall in different bank groups (a warp's 17 k blocks read in 3 wavefronts).
+constexpr int WG_BLK = 12;
+constexpr int blk_off(int r) { return (r / 8) * WG_BLK + r % 8; }
+// segment starts (in floats): D1 13 blocks | A0 17 | D2 7 | A1 13 | D3 4 | A2 7 | D4 1 | A3 4
+constexpr int RD1 = 0, RA0 = RD1 + 13 * WG_BLK, RD2 = RA0 + 17 * WG_BLK, RA1 = RD2 + 7 * WG_BLK,
+              RD3 = RA1 + 13 * WG_BLK, RA2 = RD3 + 4 * WG_BLK, RD4 = RA2 + 7 * WG_BLK,
+              RA3 = RD4 + 1 * WG_BLK;
+constexpr int WG_REC = RA3 + 4 * WG_BLK + 4;  // floats per sample record (16-byte multiple)
+static_assert(WG_REC % 4 == 0 && 2 * WG_CHUNK * WG_REC * 4 <= 227 * 1024, "wgrad smem");
 constexpr int WG_ROWS = 491;  // rows staged per sample (valid rows only)
 constexpr int WG_TILES = 221 + 91 + 28 + 4;
 constexpr int WG_F4 = WG_ROWS * (WG_CHUNK / 4);  // float4 loads per chunk
@@ -340,21 +369,21 @@ constexpr int WG_LOADS = (WG_F4 + WG_THREADS - 1) / WG_THREADS;
 // staged row r (0..490) -> (record offset, global source row, from x?)
 __device__ __forceinline__ void wg_row(int r, int& off, int& src, bool& from_x) {
     from_x = false;
-    if (r < 100) { off = RD1 + r; src = SD1 + r; return; }
+    if (r < 100) { off = RD1 + blk_off(r); src = SD1 + r; return; }
     r -= 100;
-    if (r < 134) { off = RA0 + r; src = r; from_x = true; return; }
+    if (r < 134) { off = RA0 + blk_off(r); src = r; from_x = true; return; }
     r -= 134;
-    if (r < 50) { off = RD2 + r; src = SD2 + r; return; }
+    if (r < 50) { off = RD2 + blk_off(r); src = SD2 + r; return; }
     r -= 50;
-    if (r < 100) { off = RA1 + r; src = SA1 + r; return; }
+    if (r < 100) { off = RA1 + blk_off(r); src = SA1 + r; return; }
     r -= 100;
-    if (r < 25) { off = RD3 + r; src = SD3 + r; return; }
+    if (r < 25) { off = RD3 + blk_off(r); src = SD3 + r; return; }
     r -= 25;
-    if (r < 50) { off = RA2 + r; src = SA2 + r; return; }
+    if (r < 50) { off = RA2 + blk_off(r); src = SA2 + r; return; }
     r -= 50;
-    if (r < 7) { off = RD4 + r; src = SD4 + r; return; }
+    if (r < 7) { off = RD4 + blk_off(r); src = SD4 + r; return; }
     r -= 7;
-    off = RA3 + r;
+    off = RA3 + blk_off(r);
     src = SA3 + r;
 }
 
@@ -434,21 +463,37 @@ __global__ void __launch_bounds__(WG_THREADS, 1)
         if (more) load(c0 + WG_CHUNK);  // in flight during the math below
         const float* buf = sm + cur * WG_CHUNK * WG_REC;
         if (layer >= 0) {
-#pragma unroll 4
-            for (int m = 0; m < WG_CHUNK; ++m) {
+            // two register stages: sample m+1's operands load while m's FFMA2s issue
+            struct Op {
+                float4 d0, d1, a0, a1;
+            };
+            const int dB = dOff + (n0 / 8) * WG_BLK, aB = aOff + (k0 / 8) * WG_BLK;
+            auto ld = [&](Op& o, int m) {
                 const float* rec = buf + m * WG_REC;
-                const float4 d0 = *reinterpret_cast<const float4*>(rec + dOff + n0);
-                const float4 d1 = *reinterpret_cast<const float4*>(rec + dOff + n0 + 4);
-                const float4 a0 = *reinterpret_cast<const float4*>(rec + aOff + k0);
-                const float4 a1 = *reinterpret_cast<const float4*>(rec + aOff + k0 + 4);
-                const float dv[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
-                const float2 av[4] = {make_float2(a0.x, a0.y), make_float2(a0.z, a0.w),
-                                      make_float2(a1.x, a1.y), make_float2(a1.z, a1.w)};
+                o.d0 = *reinterpret_cast<const float4*>(rec + dB);
+                o.d1 = *reinterpret_cast<const float4*>(rec + dB + 4);
+                o.a0 = *reinterpret_cast<const float4*>(rec + aB);
+                o.a1 = *reinterpret_cast<const float4*>(rec + aB + 4);
+            };
+            auto fma = [&](const Op& o) {
+                const float dv[8] = {o.d0.x, o.d0.y, o.d0.z, o.d0.w,
+                                     o.d1.x, o.d1.y, o.d1.z, o.d1.w};
+                const float2 av[4] = {make_float2(o.a0.x, o.a0.y), make_float2(o.a0.z, o.a0.w),
+                                      make_float2(o.a1.x, o.a1.y), make_float2(o.a1.z, o.a1.w)};
 #pragma unroll
                 for (int i = 0; i < 8; ++i)
 #pragma unroll
                     for (int j = 0; j < 4; ++j)
                         acc[i][j] = ffma2(make_float2(dv[i], dv[i]), av[j], acc[i][j]);
+            };
+            Op A, B;
+            ld(A, 0);
+#pragma unroll 1
+            for (int m = 0; m < WG_CHUNK; m += 2) {
+                ld(B, m + 1);
+                fma(A);
+                if (m + 2 < WG_CHUNK) ld(A, m + 2);
+                fma(B);
             }
         } else if (bt >= 0) {
             // bias gradients: rows of D1 (100) | D2 (50) | D3 (25) | D4 (7) = 182
@@ -456,10 +501,10 @@ __global__ void __launch_bounds__(WG_THREADS, 1)
             for (int u = 0; u < 5; ++u) {
                 const int r = bt + 40 * u;
                 if (r < 182) {
-                    const int off = r < 100 ? RD1 + r
-                                  : r < 150 ? RD2 + (r - 100)
-                                  : r < 175 ? RD3 + (r - 150)
-                                            : RD4 + (r - 175);
+                    const int off = r < 100 ? RD1 + blk_off(r)
+                                  : r < 150 ? RD2 + blk_off(r - 100)
+                                  : r < 175 ? RD3 + blk_off(r - 150)
+                                            : RD4 + blk_off(r - 175);
                     float sacc = 0.f;
                     for (int m = 0; m < WG_CHUNK; ++m) sacc += buf[m * WG_REC + off];
                     bsum[u] += sacc;
