@@ -154,6 +154,23 @@ int32_t dso_optimal_config(dso_ctx* ctx, const double* params_aos, int64_t n, do
                            double* time, int64_t* candidates, uint8_t* fallback,
                            double* presnap, int32_t* kstatus, uint32_t flags);
 
+/* param_fit for a batch of kernels measured on one configuration grid:
+ * fit_power (param_fit.cpp:43-77) and fit_time (param_fit.cpp:79-247), the
+ * regressions run_campaign applies to every measurement sweep
+ * (sim_harness.cpp:269-270).  cfg [S][3] host = {vc, fc_mhz, fm_mhz} per sample
+ * (shared by all kernels); power / time [S][ld] (either may be NULL to skip that
+ * fit).  Outputs [rows][ld]:
+ *   pfit [6]: p0, kappa_pow, gamma, c, mape_pct, constraint_active
+ *   tfit [8]: t0, alpha, beta, mape_pct, constraint_active,
+ *             partial_identifiability, iterations, final rss
+ * and per-kernel status (0, or 1 + ErrorKind: RankDeficient / InvalidArgument /
+ * Underdetermined as the reference throws).  FP64; coefficients equal the
+ * reference's to rounding (the QR solve operator is applied as a matrix).
+ * flags: DSO_HOST for host power/time/outputs. */
+int32_t dso_param_fit(dso_ctx* ctx, const double* cfg, int32_t S, const double* power,
+                      const double* time, int64_t n, int64_t ld, double* pfit,
+                      int32_t* pstatus, double* tfit, int32_t* tstatus, uint32_t flags);
+
 /* eta sweep: brute_force_config at n_eta etas in one pass over the grid.
  * idx/cost are [n_eta][ld_out]. */
 int32_t dso_eta_sweep(dso_ctx* ctx, const float* params, int64_t n, int64_t ld,

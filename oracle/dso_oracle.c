@@ -828,3 +828,318 @@ int orc_pipeline(const uint32_t* counts, const double* dcgm, int64_t n, const in
     free(s.vc);
     return ORC_OK;
 }
+
+/* ===========================================================================
+ * param_fit (proj/src/param_fit.cpp) — TEST INFRASTRUCTURE ONLY.
+ *
+ * The reference solves its least-squares problems with Eigen's
+ * ColPivHouseholderQR (threshold 1e-10, param_fit.cpp:29-31,108-110).  Eigen is
+ * absent here; orc_cpqr_* restate that algorithm (Householder QR with column
+ * pivoting by updated column norms, Eigen 3.4 ColPivHouseholderQR::computeInPlace,
+ * rank() = #|R_ii| > threshold * maxpivot among the nonzero pivots, solve() =
+ * Q^T b, upper-triangular solve on the nonzero pivots, permute back) with naive
+ * summation (Eigen vectorises its reductions, so results agree to rounding).
+ * ======================================================================== */
+#define ORC_QR_MAXC 4
+
+typedef struct {
+    int rows, cols, nonzero, perm[ORC_QR_MAXC];
+    double maxpivot, hcoef[ORC_QR_MAXC];
+    double* a; /* column-major rows x cols, overwritten by R (upper) + Householder essentials */
+} orc_qr;
+
+static double orc_colnorm(const double* a, int n) {
+    double s = 0.0;
+    for (int i = 0; i < n; ++i) s += a[i] * a[i];
+    return sqrt(s);
+}
+
+/* Eigen 3.4 ColPivHouseholderQR<MatrixXd>::computeInPlace */
+static void orc_cpqr_compute(orc_qr* q) {
+    const int rows = q->rows, cols = q->cols, size = rows < cols ? rows : cols;
+    double* a = q->a;
+    double normsU[ORC_QR_MAXC], normsD[ORC_QR_MAXC], maxn = 0.0;
+    for (int k = 0; k < cols; ++k) {
+        normsD[k] = normsU[k] = orc_colnorm(a + (size_t)k * rows, rows);
+        if (normsU[k] > maxn) maxn = normsU[k];
+        q->perm[k] = k;
+    }
+    const double eps = 2.220446049250313e-16;
+    const double thr_helper = (maxn * eps) * (maxn * eps) / (double)rows;
+    const double downdate_thr = sqrt(eps);
+    q->nonzero = size;
+    q->maxpivot = 0.0;
+    for (int k = 0; k < size; ++k) {
+        int big = k;
+        for (int j = k + 1; j < cols; ++j)
+            if (normsU[j] > normsU[big]) big = j;
+        const double big_sq = normsU[big] * normsU[big];
+        if (q->nonzero == size && big_sq < thr_helper * (double)(rows - k)) q->nonzero = k;
+        if (big != k) {
+            for (int i = 0; i < rows; ++i) {
+                double t = a[(size_t)k * rows + i];
+                a[(size_t)k * rows + i] = a[(size_t)big * rows + i];
+                a[(size_t)big * rows + i] = t;
+            }
+            double t = normsU[k]; normsU[k] = normsU[big]; normsU[big] = t;
+            t = normsD[k]; normsD[k] = normsD[big]; normsD[big] = t;
+            int tp = q->perm[k]; q->perm[k] = q->perm[big]; q->perm[big] = tp;
+        }
+        /* makeHouseholderInPlace on column k, rows k.. */
+        double* v = a + (size_t)k * rows + k;
+        const int m = rows - k;
+        double tail = 0.0;
+        for (int i = 1; i < m; ++i) tail += v[i] * v[i];
+        const double c0 = v[0];
+        double tau, beta;
+        if (tail <= 2.2250738585072014e-308) {
+            tau = 0.0;
+            beta = c0;
+            for (int i = 1; i < m; ++i) v[i] = 0.0;
+        } else {
+            beta = sqrt(c0 * c0 + tail);
+            if (c0 >= 0.0) beta = -beta;
+            for (int i = 1; i < m; ++i) v[i] = v[i] / (c0 - beta);
+            tau = (beta - c0) / beta;
+        }
+        v[0] = beta;
+        q->hcoef[k] = tau;
+        if (fabs(beta) > q->maxpivot) q->maxpivot = fabs(beta);
+        /* apply H = I - tau [1; v] [1; v]^T to the remaining columns */
+        for (int j = k + 1; j < cols; ++j) {
+            double* c = a + (size_t)j * rows + k;
+            double w = c[0];
+            for (int i = 1; i < m; ++i) w += v[i] * c[i];
+            w *= tau;
+            c[0] -= w;
+            for (int i = 1; i < m; ++i) c[i] -= w * v[i];
+        }
+        /* column norm downdates */
+        for (int j = k + 1; j < cols; ++j) {
+            if (normsU[j] != 0.0) {
+                double t = fabs(a[(size_t)j * rows + k]) / normsU[j];
+                t = (1.0 + t) * (1.0 - t);
+                if (t < 0.0) t = 0.0;
+                const double r = normsU[j] / normsD[j];
+                const double t2 = t * r * r;
+                if (t2 <= downdate_thr) {
+                    normsD[j] = orc_colnorm(a + (size_t)j * rows + k + 1, rows - k - 1);
+                    normsU[j] = normsD[j];
+                } else {
+                    normsU[j] *= sqrt(t);
+                }
+            }
+        }
+    }
+}
+
+static int orc_cpqr_rank(const orc_qr* q, double threshold) {
+    const double pt = fabs(q->maxpivot) * threshold;
+    int r = 0;
+    for (int i = 0; i < q->nonzero; ++i) r += fabs(q->a[(size_t)i * q->rows + i]) > pt;
+    return r;
+}
+
+/* solve(b): x = P [R11^-1 (Q^T b)_top; 0] */
+static void orc_cpqr_solve(const orc_qr* q, const double* b, double* x, double* work) {
+    const int rows = q->rows, cols = q->cols, size = rows < cols ? rows : cols;
+    for (int i = 0; i < rows; ++i) work[i] = b[i];
+    for (int k = 0; k < size; ++k) {
+        const double* v = q->a + (size_t)k * rows + k;
+        double w = work[k];
+        for (int i = 1; i < rows - k; ++i) w += v[i] * work[k + i];
+        w *= q->hcoef[k];
+        work[k] -= w;
+        for (int i = 1; i < rows - k; ++i) work[k + i] -= w * v[i];
+    }
+    const int nz = q->nonzero;
+    double c[ORC_QR_MAXC];
+    for (int i = nz - 1; i >= 0; --i) {
+        double s = work[i];
+        for (int j = i + 1; j < nz; ++j) s -= q->a[(size_t)j * rows + i] * c[j];
+        c[i] = s / q->a[(size_t)i * rows + i];
+    }
+    for (int i = nz; i < cols; ++i) c[i] = 0.0;
+    for (int i = 0; i < cols; ++i) x[q->perm[i]] = c[i];
+}
+
+static double orc_mape_pct(const double* pred, const double* obs, int n) { /* param_fit.cpp:19-24 */
+    double acc = 0.0;
+    for (int i = 0; i < n; ++i) acc += fabs(pred[i] - obs[i]) / fabs(obs[i]);
+    return 100.0 * acc / (double)n;
+}
+
+/* fit_power (param_fit.cpp:43-77).  cfg [S][3] = vc, fc_mhz, fm_mhz.
+ * out = p0, kappa_pow, gamma, c, mape_pct, constraint_active. */
+int orc_fit_power(const double* cfg, const double* power, int S, double* out) {
+    if (S < 4) return ORC_RankDeficient;
+    for (int i = 0; i < S; ++i)
+        if (!(power[i] > 0.0)) return ORC_InvalidArgument;
+    double* a = (double*)malloc(sizeof(double) * 4 * S + sizeof(double) * 2 * S);
+    double* work = a + 4 * S;
+    double* pred = work + S;
+    for (int i = 0; i < S; ++i) {
+        const double vc = cfg[3 * i], fc = cfg[3 * i + 1], fm = cfg[3 * i + 2];
+        a[i] = 1.0;
+        a[S + i] = vc;
+        a[2 * S + i] = fm;
+        a[3 * S + i] = vc * vc * fc;
+    }
+    orc_qr q = {S, 4, 0, {0}, 0.0, {0}, a};
+    orc_cpqr_compute(&q);
+    if (orc_cpqr_rank(&q, 1e-10) < 4) {
+        free(a);
+        return ORC_RankDeficient;
+    }
+    double coef[4];
+    orc_cpqr_solve(&q, power, coef, work);
+    int active = 0;
+    for (int j = 0; j < 4; ++j)
+        if (coef[j] < 0.0) {
+            coef[j] = 0.0;
+            active = 1;
+        }
+    for (int i = 0; i < S; ++i) {  /* design * coef (design rebuilt: a was overwritten) */
+        const double vc = cfg[3 * i], fc = cfg[3 * i + 1], fm = cfg[3 * i + 2];
+        pred[i] = coef[0] * 1.0 + coef[1] * vc + coef[2] * fm + coef[3] * (vc * vc * fc);
+    }
+    for (int j = 0; j < 4; ++j) out[j] = coef[j];
+    out[4] = orc_mape_pct(pred, power, S);
+    out[5] = active;
+    free(a);
+    return ORC_OK;
+}
+
+/* solve_assignment / the iteration solve of fit_time for a branch assignment
+ * (mem[i] = 1: memory branch).  Returns the rank-deficiency flag. */
+static int orc_time_solve(const double* y, const double* ifm, const double* ifc, const uint8_t* mem,
+                          int n, double* coef3, int* any_mem, int* any_core, double* scratch) {
+    *any_mem = *any_core = 0;
+    for (int i = 0; i < n; ++i) {
+        if (mem[i]) *any_mem = 1; else *any_core = 1;
+    }
+    const int cols = 1 + *any_mem + *any_core;
+    const int mc = *any_mem ? 1 : -1, cc = *any_core ? (*any_mem ? 2 : 1) : -1;
+    double* a = scratch;
+    double* work = scratch + 3 * n;
+    for (int i = 0; i < cols * n; ++i) a[i] = 0.0;
+    for (int i = 0; i < n; ++i) {
+        a[i] = 1.0;
+        if (mem[i]) a[(size_t)mc * n + i] = ifm[i]; else a[(size_t)cc * n + i] = ifc[i];
+    }
+    orc_qr q = {n, cols, 0, {0}, 0.0, {0}, a};
+    orc_cpqr_compute(&q);
+    if (orc_cpqr_rank(&q, 1e-10) < cols) return 1;
+    double c[3] = {0, 0, 0};
+    orc_cpqr_solve(&q, y, c, work);
+    coef3[0] = c[0];
+    coef3[1] = *any_mem ? c[mc] : 0.0;
+    coef3[2] = *any_core ? c[cc] : 0.0;
+    return 0;
+}
+
+static int orc_cmp_double(const void* x, const void* y) {
+    const double a = *(const double*)x, b = *(const double*)y;
+    return a < b ? -1 : (a > b ? 1 : 0);
+}
+
+/* fit_time (param_fit.cpp:79-247).  out = t0, alpha, beta, mape_pct,
+ * constraint_active, partial_identifiability, iterations, final rss;
+ * branch_out (optional) [S] = 1 for the memory branch. */
+int orc_fit_time(const double* cfg, const double* tm, int S, double* out, uint8_t* branch_out) {
+    if (S < 3) return ORC_Underdetermined;
+    for (int i = 0; i < S; ++i)
+        if (!(tm[i] > 0.0)) return ORC_InvalidArgument;
+    double* buf = (double*)malloc(sizeof(double) * (size_t)S * 10);
+    double *ifm = buf, *ifc = buf + S, *ratios = buf + 2 * S, *cuts = buf + 3 * S,
+           *scratch = buf + 4 * S;
+    uint8_t* branch = (uint8_t*)malloc((size_t)S * 2);
+    uint8_t* assign = branch + S;
+    double ysq = 0.0;
+    for (int i = 0; i < S; ++i) {
+        ifm[i] = 1.0 / cfg[3 * i + 2];
+        ifc[i] = 1.0 / cfg[3 * i + 1];
+        ysq += tm[i] * tm[i];
+    }
+    for (int i = 0; i < S; ++i) ratios[i] = ifm[i] / ifc[i];
+    for (int i = 0; i < S; ++i) cuts[i] = ratios[i];
+    qsort(cuts, S, sizeof(double), orc_cmp_double);
+    int nu = 0;
+    for (int i = 0; i < S; ++i)
+        if (nu == 0 || cuts[i] != cuts[nu - 1]) cuts[nu++] = cuts[i];
+    const double inf = 1.0 / 0.0;
+    for (int i = 0; i < S; ++i) branch[i] = 0; /* Core */
+    double best = inf;
+    const double slack = 1e-12 * (ysq + 1.0);
+    for (int c = 0; c <= nu; ++c) {  /* ordered: inf, cuts[0], cuts[1..] */
+        const double cut = c == 0 ? inf : cuts[c - 1];
+        for (int i = 0; i < S; ++i) assign[i] = ratios[i] >= cut;
+        double co[3];
+        int am, ac;
+        double rss = inf;
+        if (!orc_time_solve(tm, ifm, ifc, assign, S, co, &am, &ac, scratch)) {
+            const double t0 = co[0], al = am ? (co[1] > 0.0 ? co[1] : 0.0) : 0.0,
+                         be = ac ? (co[2] > 0.0 ? co[2] : 0.0) : 0.0;
+            rss = 0.0;
+            for (int i = 0; i < S; ++i) {
+                const double x = al * ifm[i], z = be * ifc[i];
+                const double pred = t0 + (x < z ? z : x);
+                rss += (pred - tm[i]) * (pred - tm[i]);
+            }
+        }
+        if (rss < best - slack) {
+            best = rss;
+            memcpy(branch, assign, (size_t)S);
+        }
+    }
+    if (!(best < inf) && !(best > -inf)) { /* not finite */ }
+    if (!isfinite(best)) {
+        free(buf); free(branch);
+        return ORC_Underdetermined;
+    }
+    double t0 = 0.0, al = 0.0, be = 0.0, rss = 0.0;
+    int iters = 0, active = 0;
+    for (int it = 0; it < 50; ++it) {
+        ++iters;
+        double co[3];
+        int am, ac;
+        if (orc_time_solve(tm, ifm, ifc, branch, S, co, &am, &ac, scratch)) {
+            free(buf); free(branch);
+            return ORC_Underdetermined;
+        }
+        t0 = co[0];
+        al = am ? co[1] : 0.0;
+        be = ac ? co[2] : 0.0;
+        active = 0;
+        if (al < 0.0) { al = 0.0; active = 1; }
+        if (be < 0.0) { be = 0.0; active = 1; }
+        rss = 0.0;
+        for (int i = 0; i < S; ++i) {
+            const double x = al * ifm[i], z = be * ifc[i];
+            const double pred = t0 + (x < z ? z : x);
+            rss += (pred - tm[i]) * (pred - tm[i]);
+        }
+        int changed = 0;
+        for (int i = 0; i < S; ++i) {
+            const uint8_t want = al * ifm[i] >= be * ifc[i];
+            if (want != branch[i]) { branch[i] = want; changed = 1; }
+        }
+        if (!changed) break;
+    }
+    int all_mem = 1, all_core = 1;
+    for (int i = 0; i < S; ++i) { if (branch[i]) all_core = 0; else all_mem = 0; }
+    const int partial = all_mem || all_core;
+    if (t0 < 0.0) { t0 = 0.0; active = 1; }
+    if (partial) { if (all_mem) be = 0.0; else al = 0.0; }
+    double* pred = scratch;
+    for (int i = 0; i < S; ++i) {
+        const double x = al * ifm[i], z = be * ifc[i];
+        pred[i] = t0 + (x < z ? z : x);
+    }
+    out[0] = t0; out[1] = al; out[2] = be;
+    out[3] = orc_mape_pct(pred, tm, S);
+    out[4] = active; out[5] = partial; out[6] = iters; out[7] = rss;
+    if (branch_out) memcpy(branch_out, branch, (size_t)S);
+    free(buf); free(branch);
+    return ORC_OK;
+}

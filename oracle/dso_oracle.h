@@ -136,6 +136,11 @@ int orc_pipeline(const uint32_t* counts, const double* dcgm, int64_t n, const in
                  uint8_t* clamped, int32_t* idx, double* cost, double* energy, double* time,
                  int threads);
 
+/* ---- param_fit (param_fit.cpp:43-247): cfg [S][3] = vc, fc_mhz, fm_mhz ---- */
+int orc_fit_power(const double* cfg, const double* power, int S, double* out /* [6] */);
+int orc_fit_time(const double* cfg, const double* time_s, int S, double* out /* [8] */,
+                 uint8_t* branch_out /* [S] or NULL */);
+
 #ifdef __cplusplus
 }
 #endif

@@ -99,6 +99,10 @@ class Port:
         L.orc_mlp_bias_count.restype = C.c_int64
         L.orc_mlp_bias_count.argtypes = [_int, C.c_int]
         L.orc_init_mlp.argtypes = [_int, C.c_int, C.c_uint64, _d, _d]
+        L.orc_fit_power.argtypes = [_d, _d, C.c_int, _d]
+        L.orc_fit_power.restype = C.c_int
+        L.orc_fit_time.argtypes = [_d, _d, C.c_int, _d, _u8]
+        L.orc_fit_time.restype = C.c_int
         L.orc_forward_raw.argtypes = [_int, C.c_int, _d, _d, _d, _d, _d, C.c_int64, _d]
         L.orc_predict_params.argtypes = [_int, C.c_int, _d, _d, _d, _d, _d, C.c_int64, _d,
                                          _u8, C.c_int]
@@ -296,6 +300,25 @@ class Port:
                                       _p(std, _d), lr, batch, C.byref(s))
         ws, bs = _split(model.layer_sizes, m.W, m.b)
         return loss, ws, bs, s.value
+
+    # --- param_fit (param_fit.cpp:43-247) ---------------------------------------
+    def fit_power(self, cfg, power):
+        """(status, [p0, kappa_pow, gamma, c, mape_pct, constraint_active])."""
+        cfg = _f64(cfg).reshape(-1, 3)
+        power = _f64(power)
+        out = np.zeros(6)
+        st = self.lib.orc_fit_power(_p(cfg, _d), _p(power, _d), len(power), _p(out, _d))
+        return st, out
+
+    def fit_time(self, cfg, time_s):
+        """(status, [t0, alpha, beta, mape_pct, constraint_active, partial, iterations,
+        rss], branch[S] (1 = memory))."""
+        cfg = _f64(cfg).reshape(-1, 3)
+        t = _f64(time_s)
+        out = np.zeros(8)
+        br = np.zeros(len(t), np.uint8)
+        st = self.lib.orc_fit_time(_p(cfg, _d), _p(t, _d), len(t), _p(out, _d), _p(br, _u8))
+        return st, out, br
 
     # --- sweep -----------------------------------------------------------------
     def brute_force(self, params, core, mem, dev, eta, pmax, threads: int | None = None):

@@ -101,6 +101,8 @@ def _declare(L: C.CDLL) -> None:
     L.dso_sweep_f64.argtypes = [vp, vp, i64, d, d, vp, vp, vp, vp, vp, u32]
     L.dso_optimal_config.argtypes = [vp, vp, i64, d, d, vp, vp, vp, vp, vp, vp, vp, vp, u32]
     L.dso_optimal_config.restype = i32
+    L.dso_param_fit.argtypes = [vp, vp, i32, vp, vp, i64, i64, vp, vp, vp, vp, u32]
+    L.dso_param_fit.restype = i32
     L.dso_eta_sweep.argtypes = [vp, vp, i64, i64, P(d), i32, d, vp, vp, i64]
     L.dso_pipeline.argtypes = [vp, vp, vp, i64, i64, d, d, vp, vp, vp, vp, vp, vp, u32]
     L.dso_pipeline_csr.argtypes = [vp, vp, vp, u64, vp, i64, i64, d, d, vp, vp, vp, vp, vp, vp, u32]
@@ -127,7 +129,7 @@ EXPORTED = (
     "dso_ctx_create", "dso_ctx_destroy", "dso_ctx_set_stream", "dso_sync", "dso_last_error",
     "dso_status_name", "dso_launch_count", "dso_set_option", "dso_set_domain", "dso_validate_domain", "dso_set_model", "dso_get_model",
     "dso_init_mlp", "dso_shuffled_indices", "dso_featurize", "dso_dcgm_mean", "dso_predict",
-    "dso_sweep", "dso_sweep_f64", "dso_optimal_config", "dso_eta_sweep", "dso_pipeline",
+    "dso_sweep", "dso_sweep_f64", "dso_optimal_config", "dso_param_fit", "dso_eta_sweep", "dso_pipeline",
     "dso_pipeline_csr",
     "dso_gen_synthetic", "dso_gen_synthetic_csr",
     "dso_train_grad", "dso_train_apply", "dso_model_param_count", "dso_probe_fp32_peak",

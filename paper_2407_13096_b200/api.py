@@ -311,6 +311,38 @@ class Context:
             _ptr(out["fallback"]), _ptr(out["presnap"]), _ptr(out["kstatus"]), flags))
         return out
 
+    def param_fit(self, cfg, power=None, time=None):
+        """Batched fit_power / fit_time (param_fit.cpp:43-247) of n kernels measured on one
+        grid.  cfg [S, 3] = (vc, fc_mhz, fm_mhz); power / time [S, n] float64 (CUDA tensors or
+        host numpy; either may be None).  Returns dict(pfit [6, n], pstatus [n],
+        tfit [8, n], tstatus [n]) — see include/dso_b200.h for the rows."""
+        cfg = np.ascontiguousarray(cfg, np.float64).reshape(-1, 3)
+        S = len(cfg)
+        ref = power if power is not None else time
+        host = not _is_cuda(ref)
+        if host:
+            power = None if power is None else np.ascontiguousarray(power, np.float64)
+            time = None if time is None else np.ascontiguousarray(time, np.float64)
+            n = ref.shape[1]
+            mk = lambda shape, dt: np.empty(shape, dt)  # noqa: E731
+        else:
+            for t in (power, time):
+                if t is not None and (t.dtype != torch.float64 or not t.is_contiguous()):
+                    raise DsoError(ErrorKind.InvalidArgument, "power/time must be contiguous f64")
+            n = ref.shape[1]
+            mk = lambda shape, dt: self._empty(shape, {np.float64: torch.float64,  # noqa: E731
+                                                        np.int32: torch.int32}[dt])
+        out = {}
+        if power is not None:
+            out["pfit"], out["pstatus"] = mk((6, n), np.float64), mk((n,), np.int32)
+        if time is not None:
+            out["tfit"], out["tstatus"] = mk((8, n), np.float64), mk((n,), np.int32)
+        self._raise(self._lib.dso_param_fit(
+            self._h, cfg.ctypes.data, S, _ptr(power), _ptr(time), n, n, _ptr(out.get("pfit")),
+            _ptr(out.get("pstatus")), _ptr(out.get("tfit")), _ptr(out.get("tstatus")),
+            DSO_HOST if host else 0))
+        return out
+
     def eta_sweep(self, params, etas, pmax_w: float | None = None, n: int | None = None):
         """brute_force_config at every eta: (idx [n_eta, ld], cost [n_eta, ld])."""
         _check(params, torch.float32, 7, "params")

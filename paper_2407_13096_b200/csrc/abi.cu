@@ -186,6 +186,7 @@ int32_t dso_ctx_destroy(dso_ctx* ctx) {
     cudaFree(c.dom.sd_g1);
     cudaFree(c.eta_dev);
     cudaFree(c.flag_dev);
+    fit_plan_free(c);
     cudaFree(c.model.wt);
     cudaFree(c.model.w_master);
     cudaFree(c.scratch);
@@ -577,6 +578,63 @@ int32_t dso_optimal_config(dso_ctx* ctx, const double* params, int64_t n, double
     return kOk;
 }
 
+int32_t dso_param_fit(dso_ctx* ctx, const double* cfg, int32_t S, const double* power,
+                      const double* time, int64_t n, int64_t ld, double* pfit,
+                      int32_t* pstatus, double* tfit, int32_t* tstatus, uint32_t flags) {
+    int32_t st = check_ctx(ctx, false, false);
+    if (st) return st;
+    if ((st = check_batch(ctx, n, ld))) return st;
+    if (S < 0 || (S > 0 && !cfg)) return fail(ctx, kInvalidArgument, "bad sample grid");
+    if (!power && !time) return fail(ctx, kInvalidArgument, "power and time are both NULL");
+    Ctx& c = ctx->c;
+    DSO_CUDA(ctx, fit_prepare(c, cfg, S));
+    if (!(flags & DSO_HOST)) {
+        DSO_CUDA(ctx, launch_param_fit(c, power, time, n, ld, pfit, pstatus, tfit, tstatus));
+        return kOk;
+    }
+    // host buffers: chunks of kernels staged through the device
+    const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(n, (int64_t)(1 << 28) / (16 * (S + 8))));
+    const size_t per = (size_t)8 * (2 * (size_t)S + 6 + 8) + 8;
+    const size_t need = (size_t)chunk * per + 256;
+    if (c.scratch_bytes < need) {
+        DSO_CUDA(ctx, cudaStreamSynchronize(c.stream));
+        cudaFree(c.scratch);
+        c.scratch = nullptr;
+        c.scratch_bytes = 0;
+        DSO_CUDA(ctx, cudaMalloc(&c.scratch, need));
+        c.scratch_bytes = need;
+    }
+    double* dp = (double*)c.scratch;
+    double* dt = dp + (size_t)S * chunk;
+    double* dpf = dt + (size_t)S * chunk;
+    double* dtf = dpf + 6 * (size_t)chunk;
+    int32_t* dps = (int32_t*)(dtf + 8 * (size_t)chunk);
+    int32_t* dts = dps + chunk;
+    for (int64_t off = 0; off < n; off += chunk) {
+        const int64_t m = std::min(chunk, n - off);
+        if (power)
+            DSO_CUDA(ctx, cudaMemcpy2DAsync(dp, m * 8, power + off, ld * 8, m * 8, S,
+                                            cudaMemcpyHostToDevice, c.stream));
+        if (time)
+            DSO_CUDA(ctx, cudaMemcpy2DAsync(dt, m * 8, time + off, ld * 8, m * 8, S,
+                                            cudaMemcpyHostToDevice, c.stream));
+        DSO_CUDA(ctx, launch_param_fit(c, power ? dp : nullptr, time ? dt : nullptr, m, m, dpf,
+                                       dps, dtf, dts));
+        if (power && pfit)
+            DSO_CUDA(ctx, cudaMemcpy2DAsync(pfit + off, ld * 8, dpf, m * 8, m * 8, 6,
+                                            cudaMemcpyDeviceToHost, c.stream));
+        if (power && pstatus)
+            DSO_CUDA(ctx, cudaMemcpyAsync(pstatus + off, dps, 4 * m, cudaMemcpyDeviceToHost, c.stream));
+        if (time && tfit)
+            DSO_CUDA(ctx, cudaMemcpy2DAsync(tfit + off, ld * 8, dtf, m * 8, m * 8, 8,
+                                            cudaMemcpyDeviceToHost, c.stream));
+        if (time && tstatus)
+            DSO_CUDA(ctx, cudaMemcpyAsync(tstatus + off, dts, 4 * m, cudaMemcpyDeviceToHost, c.stream));
+    }
+    DSO_CUDA(ctx, cudaStreamSynchronize(c.stream));
+    return kOk;
+}
+
 int32_t dso_eta_sweep(dso_ctx* ctx, const float* params, int64_t n, int64_t ld,
                       const double* etas, int32_t n_eta, double pmax, int32_t* idx,
                       float* cost, int64_t ld_out) {
@@ -597,6 +655,7 @@ int32_t dso_eta_sweep(dso_ctx* ctx, const float* params, int64_t n, int64_t ld,
         DSO_CUDA(ctx, cudaStreamSynchronize(c.stream));
         cudaFree(c.eta_dev);
     cudaFree(c.flag_dev);
+    fit_plan_free(c);
         c.eta_dev = nullptr;
         c.eta_cap = 0;
         DSO_CUDA(ctx, cudaMalloc(&c.eta_dev, sizeof(float2) * n_eta));

@@ -91,6 +91,7 @@ struct Ctx {
     float2* eta_dev = nullptr;      // dso_eta_sweep's (eta, K) table
     int eta_cap = 0;
     int* flag_dev = nullptr;        // dso_dcgm_mean's out-of-range flag
+    void* fit_plan = nullptr;       // dso_param_fit's factored designs (fit.cu)
     void* train_scratch = nullptr;  // per-CTA partial gradients
     size_t train_scratch_bytes = 0;
 };
@@ -118,6 +119,11 @@ cudaError_t launch_optimal_config(Ctx& c, const double* params, int64_t n, doubl
                                   double K, int32_t* idx, double* cost, double* energy,
                                   double* time, int64_t* candidates, uint8_t* fallback,
                                   double* presnap, int32_t* kstatus);
+cudaError_t fit_prepare(Ctx& c, const double* cfg, int S);
+void fit_plan_free(Ctx& c);
+cudaError_t launch_param_fit(Ctx& c, const double* power, const double* time, int64_t n,
+                             int64_t ld, double* pfit, int32_t* pstatus, double* tfit,
+                             int32_t* tstatus);
 cudaError_t launch_gen(Ctx& c, uint64_t root, uint64_t salt_base, int64_t first, int64_t n,
                        int64_t ld, float* params, uint32_t* counts, float* dcgm);
 cudaError_t launch_featurize(Ctx& c, const uint32_t* counts, const float* dcgm, int64_t n,
