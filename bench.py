@@ -557,7 +557,25 @@ def stage_times(ctx, counts, dcgm, cfg, dom, n, stream):
     p64 = params[:, : min(n, 1 << 22)].double().t().contiguous()
     res["sweep_f64_ms_4M"] = t(lambda: ctx.brute_force_config_exact(p64, cfg["eta"]))
     res["sweep_f64_pairs_per_s"] = p64.shape[0] * dom.pairs / (res["sweep_f64_ms_4M"] * 1e-3)
-    del fused, params, p64
+    res["optimal_config_ms_4M"] = t(lambda: ctx.optimal_config(p64, cfg["eta"]))
+    res["optimal_config_kernels_per_s"] = p64.shape[0] / (res["optimal_config_ms_4M"] * 1e-3)
+    # param_fit: 1M kernels measured on the reference's default 14x3 grid (run_campaign)
+    nf = min(n, 1 << 20)
+    core = [705.0 + 52.0 * k for k in range(13)] + [1380.0]
+    grid = []
+    for fc in core:
+        d = fc / 1000.0 - 0.5
+        for fm in (438.0, 658.0, 877.0):
+            grid.append([2.0 * d * d + 0.5, fc, fm])
+    g = torch.tensor(grid, dtype=torch.float64, device=params.device)
+    pp = p64[:nf].t()  # [7, nf]
+    vc, fc, fm = g[:, 0:1], g[:, 1:2], g[:, 2:3]
+    P = ((pp[0] + pp[1] * vc) + pp[2] * fm) + ((pp[3] * vc) * vc) * fc      # [42, nf]
+    T = pp[4] + torch.maximum(pp[5] / fm, pp[6] / fc)
+    P, T = P.contiguous(), T.contiguous()
+    res["param_fit_ms_1M"] = t(lambda: ctx.param_fit(grid, P, T))
+    res["param_fit_kernels_per_s"] = nf / (res["param_fit_ms_1M"] * 1e-3)
+    del fused, params, p64, P, T
     return res
 
 

@@ -11,6 +11,9 @@
 //   optimal_config_batch      <-  optimal_config       (optimizer.hpp:39-46)
 //                                 bit-exact incl. fallback, presnap and
 //                                 candidates_evaluated (dso_optimal_config)
+//   fit_power_batch /         <-  fit_power / fit_time (param_fit.hpp:45-56)
+//   fit_time_batch                for many kernels measured on one grid
+//                                 (dso_param_fit; FP64, equal to rounding)
 //   optimize_kernels          <-  featurize (ptx_features.hpp:55) +
 //                                 FusedFeatures::as_vector (mlp.hpp:20-25) +
 //                                 predict_params (mlp.hpp:66) +
@@ -35,6 +38,7 @@
 #include "dso/dvfs_model.hpp"
 #include "dso/error.hpp"
 #include "dso/optimizer.hpp"
+#include "dso/param_fit.hpp"
 #include "dso_b200.h"
 
 namespace dso {
@@ -180,6 +184,81 @@ inline std::vector<OptimizationResult> optimal_config_batch(
         r.presnap_vc = pre[3 * k];
         r.presnap_fc_mhz = pre[3 * k + 1];
         r.presnap_fm_mhz = pre[3 * k + 2];
+    }
+    return out;
+}
+
+// fit_power / fit_time for kernels measured on one grid `cfg` (every kernel's
+// sample s was taken at cfg[s], as measure_sweep produces, sim_harness.cpp:157-170):
+// power[k][s] / time[k][s].  Throws like a scalar loop over the reference (the
+// first failing kernel in index order); TimeFit::branch and rss_trace are not
+// reproduced (branch is rebuilt from the fitted coefficients; the trace holds
+// the final rss only).
+inline std::vector<PowerFit> fit_power_batch(const std::vector<DvfsConfig>& cfg,
+                                             const std::vector<std::vector<double>>& power,
+                                             GpuContext& ctx) {
+    const int S = static_cast<int>(cfg.size());
+    const int64_t n = static_cast<int64_t>(power.size());
+    std::vector<double> c(3 * S), P((size_t)S * n), fit(6 * (size_t)n);
+    std::vector<int32_t> st(n);
+    for (int s = 0; s < S; ++s) {
+        c[3 * s] = cfg[s].vc;
+        c[3 * s + 1] = cfg[s].fc_mhz;
+        c[3 * s + 2] = cfg[s].fm_mhz;
+    }
+    for (int64_t k = 0; k < n; ++k) {
+        if (static_cast<int>(power[k].size()) != S)
+            throw Error(ErrorKind::InvalidArgument, "sample count differs from the grid");
+        for (int s = 0; s < S; ++s) P[(size_t)s * n + k] = power[k][s];
+    }
+    check_status(dso_param_fit(ctx.handle(), c.data(), S, P.data(), nullptr, n, n, fit.data(),
+                               st.data(), nullptr, nullptr, DSO_HOST),
+                 ctx.handle());
+    std::vector<PowerFit> out(n);
+    for (int64_t k = 0; k < n; ++k) {
+        if (st[k]) throw Error(static_cast<ErrorKind>(st[k] - 1), "fit_power failed");
+        out[k] = PowerFit{fit[k], fit[n + k], fit[2 * n + k], fit[3 * n + k], fit[4 * n + k],
+                          fit[5 * n + k] != 0.0};
+    }
+    return out;
+}
+
+inline std::vector<TimeFit> fit_time_batch(const std::vector<DvfsConfig>& cfg,
+                                           const std::vector<std::vector<double>>& time,
+                                           GpuContext& ctx) {
+    const int S = static_cast<int>(cfg.size());
+    const int64_t n = static_cast<int64_t>(time.size());
+    std::vector<double> c(3 * S), T((size_t)S * n), fit(8 * (size_t)n);
+    std::vector<int32_t> st(n);
+    for (int s = 0; s < S; ++s) {
+        c[3 * s] = cfg[s].vc;
+        c[3 * s + 1] = cfg[s].fc_mhz;
+        c[3 * s + 2] = cfg[s].fm_mhz;
+    }
+    for (int64_t k = 0; k < n; ++k) {
+        if (static_cast<int>(time[k].size()) != S)
+            throw Error(ErrorKind::InvalidArgument, "sample count differs from the grid");
+        for (int s = 0; s < S; ++s) T[(size_t)s * n + k] = time[k][s];
+    }
+    check_status(dso_param_fit(ctx.handle(), c.data(), S, nullptr, T.data(), n, n, nullptr,
+                               nullptr, fit.data(), st.data(), DSO_HOST),
+                 ctx.handle());
+    std::vector<TimeFit> out(n);
+    for (int64_t k = 0; k < n; ++k) {
+        if (st[k]) throw Error(static_cast<ErrorKind>(st[k] - 1), "fit_time failed");
+        TimeFit& f = out[k];
+        f.t0 = fit[k];
+        f.alpha = fit[n + k];
+        f.beta = fit[2 * n + k];
+        f.mape_pct = fit[3 * n + k];
+        f.constraint_active = fit[4 * n + k] != 0.0;
+        f.partial_identifiability = fit[5 * n + k] != 0.0;
+        f.iterations = static_cast<int>(fit[6 * n + k]);
+        f.rss_trace = {fit[7 * n + k]};
+        for (int s = 0; s < S; ++s)
+            f.branch.push_back(f.alpha / cfg[s].fm_mhz >= f.beta / cfg[s].fc_mhz
+                                   ? TimeBranch::Memory
+                                   : TimeBranch::Core);
     }
     return out;
 }

@@ -128,6 +128,40 @@ int main() {
             }
         }
     }
+    // fit_power_batch / fit_time_batch: the reference's param_fit unit-test cases
+    // (test_param_fit.cpp:48-157; the reference's param_fit needs Eigen, absent)
+    {
+        const KernelModelParams t{10.0, 5.0, 2.0, 3.0, 1.0, 8.0, 6.0};
+        std::vector<DvfsConfig> pc;
+        for (double vc : {0.8, 1.2})
+            for (double fc : {600.0, 1100.0})
+                for (double fm : {400.0, 800.0}) pc.push_back({vc, fc, fm});
+        std::vector<std::vector<double>> pw(2);
+        for (auto& c : pc) {
+            pw[0].push_back(power(t, c));
+            pw[1].push_back(3.7 * power(t, c));
+        }
+        auto pf = fit_power_batch(pc, pw, ctx);
+        CHECK(std::abs(pf[0].p0 - 10.0) < 1e-8 && std::abs(pf[0].c - 3.0) < 1e-8);
+        CHECK(!pf[0].constraint_active && pf[0].mape_pct < 1e-9);
+        CHECK(std::abs(pf[1].gamma - 3.7 * pf[0].gamma) < 1e-9 * 3.7 * pf[0].gamma);
+        std::vector<DvfsConfig> tc;
+        for (double fc : {1.0, 2.0, 3.0, 4.0})
+            for (double fm : {1.0, 2.0, 3.0, 4.0}) tc.push_back({1.0, fc, fm});
+        std::vector<std::vector<double>> tt(1);
+        for (auto& c : tc) tt[0].push_back(exec_time(t, c));
+        auto tf = fit_time_batch(tc, tt, ctx);
+        CHECK(std::abs(tf[0].t0 - 1.0) < 1e-6 && std::abs(tf[0].alpha - 8.0) < 1e-6 &&
+              std::abs(tf[0].beta - 6.0) < 1e-5);
+        CHECK(!tf[0].partial_identifiability);
+        std::vector<DvfsConfig> one{{1.0, 600.0, 400.0}, {1.0, 800.0, 400.0}, {1.0, 1000.0, 400.0}};
+        try {
+            (void)fit_power_batch(one, {{1.0, 2.0, 3.0}}, ctx);
+            CHECK(false);
+        } catch (const Error& e) {
+            CHECK(e.kind() == ErrorKind::RankDeficient);
+        }
+    }
     // error behaviour: the reference's kinds (test_optimizer.cpp:199-214)
     {
         DvfsDomain d = default_domain();
