@@ -292,11 +292,11 @@ __device__ __forceinline__ void consumer_tile(const float* W, float* act, float*
         const int n0 = g * 14 + ng * 7;
 #pragma unroll
         for (int t = 0; t < 7; ++t) {
-            const float nbl = neg_bias_log2e(W[B2S + n0 + t]);
-            if (n0 + t < 50) {
-                const float2 s0 = sigmoid2_bias(acc0[t], nbl), s1 = sigmoid2_bias(acc1[t], nbl);
-                act4w[(n0 + t) * RS4] = make_float4(s0.x, s0.y, s1.x, s1.y);
-            }
+            const float bb = W[B2S + n0 + t];
+            if (n0 + t < 50)
+                act4w[(n0 + t) * RS4] =
+                    make_float4(sigmoidf_fast(acc0[t].x + bb), sigmoidf_fast(acc0[t].y + bb),
+                                sigmoidf_fast(acc1[t].x + bb), sigmoidf_fast(acc1[t].y + bb));
         }
         bar_sync(cbar, kGroupThreads);
         PT_END(4, t_e2);

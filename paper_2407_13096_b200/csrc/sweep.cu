@@ -252,7 +252,7 @@ __device__ __noinline__ Best replay_levels(const KParams p, const float4* s_core
 }
 
 template <int CH, int NM>
-__global__ void __launch_bounds__(128, 4) eta_sweep_fast_kernel(
+__global__ void __launch_bounds__(128) eta_sweep_fast_kernel(
     const float* __restrict__ params, int64_t n, int64_t ld, const float4* __restrict__ core4,
     int nc, const float2* __restrict__ mem2, const float2* __restrict__ etaK, int n_eta,
     int32_t* __restrict__ idx, float* __restrict__ cost, int64_t ld_out) {
