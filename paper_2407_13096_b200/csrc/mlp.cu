@@ -709,35 +709,54 @@ __device__ __forceinline__ void csr_features(float* act, float* scr, const Job& 
         }
     }
     bar_sync(BAR_PROD, kProducers);
-    // pass 1: scatter-add counts, category totals
-    uint64_t tot[3] = {0, 0, 0};
-    uint32_t mk0 = 0, mk1 = 0, mk2 = 0, mk3 = 0;  // slots with a non-zero count
-    auto scatter = [&](uint32_t e) {
-        const int slot = (int)(e & 127u);
-        const uint32_t c = e >> 7;
+    // pass 1: scatter-add counts, category totals.  The register-held entries
+    // (<= kCsrRegs per thread, counts < 2^25) sum in 32 bits without overflow,
+    // also across the TPK threads of a kernel (<= 24 * 2^25 < 2^30); entries
+    // beyond those (a kernel listing > 24 categories) sum in 64 bits.
+    uint32_t t32[3] = {0u, 0u, 0u};
+    uint64_t lo_mask = 0, hi_mask = 0;  // slots 0..63 / 64..125 with a non-zero count
+    auto scatter32 = [&](uint32_t e) {
+        const uint32_t slot = e & 127u, c = e >> 7;
         if (slot < DSO_COUNT_ROWS) {
             atomicAdd(acti + (8 + slot) * RS + m, c);
-            const uint32_t bitv = c ? 1u << (slot & 31) : 0u;
-            const int w = slot >> 5;
-            mk0 |= w == 0 ? bitv : 0u;
-            mk1 |= w == 1 ? bitv : 0u;
-            mk2 |= w == 2 ? bitv : 0u;
-            mk3 |= w == 3 ? bitv : 0u;
-            const int cat = cat_of_row(slot);  // selects, not a dynamic index
-            tot[0] += cat == 0 ? c : 0u;
-            tot[1] += cat == 1 ? c : 0u;
-            tot[2] += cat == 2 ? c : 0u;
+            const uint64_t bit = c ? 1ull << (slot & 63u) : 0ull;
+            if (slot < 64u) lo_mask |= bit; else hi_mask |= bit;
+            if (slot < DSO_INSTR_SLOTS) t32[0] += c;
+            else if (slot < DSO_INSTR_SLOTS + DSO_DTYPE_SLOTS) t32[1] += c;
+            else t32[2] += c;
         }
     };
 #pragma unroll
     for (int e = 0; e < kCsrRegs; ++e)
-        if (sub + TPK * e < P.cnt) scatter(P.ent[e]);
-    for (int idx = sub + TPK * kCsrRegs; idx < P.cnt; idx += TPK)
-        scatter(__ldg(J.entries + P.first + idx));
+        if (sub + TPK * e < P.cnt) scatter32(P.ent[e]);
 #pragma unroll
     for (int c = 0; c < 3; ++c)
 #pragma unroll
-        for (int off = 1; off < TPK; off <<= 1) tot[c] += __shfl_xor_sync(0xffffffffu, tot[c], off);
+        for (int off = 1; off < TPK; off <<= 1) t32[c] += __shfl_xor_sync(0xffffffffu, t32[c], off);
+    uint64_t tot[3] = {t32[0], t32[1], t32[2]};
+    if (__any_sync(0xffffffffu, P.cnt > TPK * kCsrRegs)) {
+        uint64_t s64[3] = {0, 0, 0};
+        for (int idx = sub + TPK * kCsrRegs; idx < P.cnt; idx += TPK) {
+            const uint32_t e = __ldg(J.entries + P.first + idx);
+            const uint32_t slot = e & 127u, c = e >> 7;
+            if (slot < DSO_COUNT_ROWS) {
+                atomicAdd(acti + (8 + slot) * RS + m, c);
+                const uint64_t bit = c ? 1ull << (slot & 63u) : 0ull;
+                if (slot < 64u) lo_mask |= bit; else hi_mask |= bit;
+                if (slot < DSO_INSTR_SLOTS) s64[0] += c;
+                else if (slot < DSO_INSTR_SLOTS + DSO_DTYPE_SLOTS) s64[1] += c;
+                else s64[2] += c;
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+#pragma unroll
+            for (int off = 1; off < TPK; off <<= 1) s64[c] += __shfl_xor_sync(0xffffffffu, s64[c], off);
+            tot[c] += s64[c];
+        }
+    }
+    uint32_t mk0 = (uint32_t)lo_mask, mk1 = (uint32_t)(lo_mask >> 32), mk2 = (uint32_t)hi_mask,
+             mk3 = (uint32_t)(hi_mask >> 32);
     mk0 = __reduce_or_sync(0xffffffffu, mk0);
     mk1 = __reduce_or_sync(0xffffffffu, mk1);
     mk2 = __reduce_or_sync(0xffffffffu, mk2);
