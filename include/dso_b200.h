@@ -233,6 +233,31 @@ int64_t dso_model_param_count(const dso_ctx* ctx);
  * FP32-bound kernels): mode 0 = scalar FFMA, 1 = packed FFMA2.  TFLOP/s. */
 int32_t dso_probe_fp32_peak(dso_ctx* ctx, int32_t mode, double* tflops);
 
+/* ---- host feature ingestion (no device; thread-safe) ----------------------
+ * parse_ptx (ptx_features.cpp:238-309): PTX text -> per-kernel category counts
+ * in source order, rows = instr 0..100 | dtype 101..117 | memspace 118..125.
+ * Fails with MalformedPtx (status 1) and a line number in msg on an
+ * unterminated block comment or kernel body. */
+typedef struct dso_ptx dso_ptx;
+int32_t dso_ptx_parse(const char* text, int64_t len, dso_ptx** out, char* msg, int32_t msg_len);
+void dso_ptx_free(dso_ptx* parsed);
+int64_t dso_ptx_kernel_count(const dso_ptx* parsed);
+const char* dso_ptx_kernel_name(const dso_ptx* parsed, int64_t k);
+/* counts126 = kernel k's raw tallies (KernelInstructionCounts maps, ptx_features.hpp:31-37) */
+int32_t dso_ptx_kernel_counts(const dso_ptx* parsed, int64_t k, uint64_t* counts126,
+                              uint64_t* total_instructions);
+/* dense uint32 [126][ld] counts for dso_featurize / dso_pipeline */
+int32_t dso_ptx_counts(const dso_ptx* parsed, uint32_t* counts, int64_t ld);
+/* CSR for dso_pipeline_csr: row_ptr [n+1], entries [nnz] = (count << 7) | row
+ * (InvalidArgument if a count >= 2^25) */
+int64_t dso_ptx_nnz(const dso_ptx* parsed);
+int32_t dso_ptx_csr(const dso_ptx* parsed, uint64_t* row_ptr, uint32_t* entries);
+/* load_dcgm_samples (telemetry.cpp:63-101): header, >= 1 row, 9 fields, values in
+ * [0, 1] (OutOfRange with the row in msg), per-metric mean in double ->
+ * mean8 in DcgmMetricVector order. */
+int32_t dso_load_dcgm_csv(const char* text, int64_t len, double* mean8, char* msg,
+                          int32_t msg_len);
+
 #ifdef __cplusplus
 }
 #endif

@@ -103,6 +103,24 @@ def _declare(L: C.CDLL) -> None:
     L.dso_optimal_config.restype = i32
     L.dso_param_fit.argtypes = [vp, vp, i32, vp, vp, i64, i64, vp, vp, vp, vp, u32]
     L.dso_param_fit.restype = i32
+    L.dso_ptx_parse.argtypes = [C.c_char_p, i64, P(vp), C.c_char_p, i32]
+    L.dso_ptx_parse.restype = i32
+    L.dso_ptx_free.argtypes = [vp]
+    L.dso_ptx_free.restype = None
+    L.dso_ptx_kernel_count.argtypes = [vp]
+    L.dso_ptx_kernel_count.restype = i64
+    L.dso_ptx_kernel_name.argtypes = [vp, i64]
+    L.dso_ptx_kernel_name.restype = C.c_char_p
+    L.dso_ptx_kernel_counts.argtypes = [vp, i64, vp, vp]
+    L.dso_ptx_kernel_counts.restype = i32
+    L.dso_ptx_counts.argtypes = [vp, vp, i64]
+    L.dso_ptx_counts.restype = i32
+    L.dso_ptx_nnz.argtypes = [vp]
+    L.dso_ptx_nnz.restype = i64
+    L.dso_ptx_csr.argtypes = [vp, vp, vp]
+    L.dso_ptx_csr.restype = i32
+    L.dso_load_dcgm_csv.argtypes = [C.c_char_p, i64, vp, C.c_char_p, i32]
+    L.dso_load_dcgm_csv.restype = i32
     L.dso_eta_sweep.argtypes = [vp, vp, i64, i64, P(d), i32, d, vp, vp, i64]
     L.dso_pipeline.argtypes = [vp, vp, vp, i64, i64, d, d, vp, vp, vp, vp, vp, vp, u32]
     L.dso_pipeline_csr.argtypes = [vp, vp, vp, u64, vp, i64, i64, d, d, vp, vp, vp, vp, vp, vp, u32]
@@ -133,4 +151,6 @@ EXPORTED = (
     "dso_pipeline_csr",
     "dso_gen_synthetic", "dso_gen_synthetic_csr",
     "dso_train_grad", "dso_train_apply", "dso_model_param_count", "dso_probe_fp32_peak",
+    "dso_ptx_parse", "dso_ptx_free", "dso_ptx_kernel_count", "dso_ptx_kernel_name",
+    "dso_ptx_kernel_counts", "dso_ptx_counts", "dso_ptx_nnz", "dso_ptx_csr", "dso_load_dcgm_csv",
 )
