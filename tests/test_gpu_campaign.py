@@ -36,6 +36,13 @@ def test_ac6_oracle_predictor(ctx, ref):
     for a, b in zip(rep.rows, rep.rows[1:]):
         assert b["mean_energy_saving_pct"] >= a["mean_energy_saving_pct"] - 1e-9
         assert b["mean_time_loss_pct"] >= a["mean_time_loss_pct"] - 1e-9
+    import json
+
+    from paper_2407_13096_b200.jsonio import campaign_report_to_json
+    doc = json.loads(campaign_report_to_json(rep, default_domain()))
+    assert doc["format_version"] == 1 and len(doc["etas"]) == len(etas)
+    assert set(doc["etas"][0]["apps"][0]) == {"name", "default", "optimized", "energy_saving_pct",
+                                              "time_loss_pct"}
     dom = default_domain()
     root = Rng(0xACCE5506)
     truth = np.array([gen_truth(root.fork(0x7E57000 + i).next_u64()) for i in range(20)])
