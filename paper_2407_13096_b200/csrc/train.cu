@@ -20,6 +20,8 @@
 // second kernel sums the partials in a fixed order (deterministic, no atomics).
 #include <math.h>
 
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace dso_b200 {
@@ -540,8 +542,8 @@ __global__ void __launch_bounds__(WG_THREADS, 1)
 
 // Sum the per-CTA partials in CTA order (deterministic), in double.
 __global__ void reduce_partials(const float* __restrict__ partial, int parts,
-                                const double* __restrict__ loss_partial, float* __restrict__ grad,
-                                double* __restrict__ loss_sum) {
+                                const double* __restrict__ loss_partial, int loss_parts,
+                                float* __restrict__ grad, double* __restrict__ loss_sum) {
     const int e = blockIdx.x * blockDim.x + threadIdx.x;
     if (e < kMasterFloats) {
         double s = 0.0;
@@ -550,7 +552,7 @@ __global__ void reduce_partials(const float* __restrict__ partial, int parts,
     }
     if (e == 0) {
         double s = 0.0;
-        for (int c = 0; c < parts; ++c) s += loss_partial[c];
+        for (int c = 0; c < loss_parts; ++c) s += loss_partial[c];
         *loss_sum = s;
     }
 }
@@ -593,15 +595,21 @@ cudaError_t launch_train_grad(Ctx& cx, const float* x, const float* y, int64_t n
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    // CTAs with no tile / no samples still write their (zero) partials
-    train_fb_kernel<<<parts, kThreads, smem, cx.stream>>>(cx.model.w_master, x, y, n, ld, act,
-                                                          lds, lp);
-    int64_t per = (n + parts - 1) / parts;
+    // grids sized to the batch (small batches launch few CTAs); every launched CTA
+    // writes its partial, and the reduction reads exactly those
+    const int64_t tiles = (n + TM - 1) / TM;
+    const int fb_parts = (int)std::max<int64_t>(1, std::min<int64_t>(parts, tiles));
+    train_fb_kernel<<<fb_parts, kThreads, smem, cx.stream>>>(cx.model.w_master, x, y, n, ld, act,
+                                                             lds, lp);
+    const int64_t chunks = (n + WG_CHUNK - 1) / WG_CHUNK;
+    const int wg_parts = (int)std::max<int64_t>(1, std::min<int64_t>(parts, chunks));
+    int64_t per = (n + wg_parts - 1) / wg_parts;
     per = ((per + WG_CHUNK - 1) / WG_CHUNK) * WG_CHUNK;
     if (per == 0) per = WG_CHUNK;
-    train_wgrad_kernel<<<parts, WG_THREADS, smem_wg, cx.stream>>>(x, ld, act, lds, n, per,
-                                                                  partial);
-    reduce_partials<<<(kMasterFloats + 255) / 256, 256, 0, cx.stream>>>(partial, parts, lp, grad,
+    train_wgrad_kernel<<<wg_parts, WG_THREADS, smem_wg, cx.stream>>>(x, ld, act, lds, n, per,
+                                                                     partial);
+    reduce_partials<<<(kMasterFloats + 255) / 256, 256, 0, cx.stream>>>(partial, wg_parts, lp,
+                                                                        fb_parts, grad,
                                                                         loss_sum_dev);
     cx.launches += 3;
     return cudaGetLastError();

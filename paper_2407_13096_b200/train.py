@@ -142,7 +142,7 @@ def _dev_cols(a):
 
 
 def fit_model(ctx, features, targets, sizes, mean, std, lr: float, batch_size: int,
-              epochs: int, seed: int):
+              epochs: int, seed: int, use_graph: bool = True):
     """fit_model (mlp.cpp:115-130) on the GPU: init_mlp(sizes, seed), per-epoch
     sgd_epoch (mlp.cpp:84-112) with order shuffled_indices(Rng(seed).fork(0x5d0)),
     loss of every batch on the pre-update weights, stop after a NaN epoch.
@@ -161,18 +161,57 @@ def fit_model(ctx, features, targets, sizes, mean, std, lr: float, batch_size: i
     state = fork(seed, 0x5D0)
     grad = torch.empty((ctx.n_model_params,), dtype=torch.float32, device=X.device)
     trace = []
+    batches = list(epoch_batches(n, batch_size))
+    # The epoch's launch sequence is fixed for a given (n, batch size) — only the
+    # shuffled order changes — so it is captured once into a CUDA graph (order
+    # upload, gathers, every batch's gradient + update, the loss sum) and replayed
+    # per epoch; the host writes the next order into a pinned buffer in between.
+    idx_host = torch.empty(n, dtype=torch.int64).pin_memory()
+    idx_dev = torch.empty(n, dtype=torch.int64, device=X.device)
+    Xe, Ye = torch.empty_like(X), torch.empty_like(Y)
+    acc = torch.zeros((), dtype=torch.float64, device=X.device)
+
+    def epoch_body():
+        idx_dev.copy_(idx_host, non_blocking=True)
+        torch.index_select(X, 1, idx_dev, out=Xe)
+        torch.index_select(Y, 1, idx_dev, out=Ye)
+        acc.zero_()
+        for start, b in batches:
+            g, loss = ctx.train_grad_slice(Xe, Ye, start, b, grad=grad)
+            acc.add_(loss[0] / (b * out_dim))
+            ctx.train_apply(g, lr, 1.0 / (b * out_dim))
+
+    graph = None
+    if use_graph and epochs > 2:
+        # warm-up outside capture (allocations, function attributes), on a copy of
+        # the weights that is restored afterwards, then capture on a side stream
+        saved = ctx.get_model()
+        idx_host.copy_(torch.arange(n))
+        epoch_body()
+        torch.cuda.synchronize()
+        ctx.set_model(saved)
+        graph = torch.cuda.CUDAGraph()
+        cap = torch.cuda.Stream()
+        cap.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(cap):
+            ctx.set_stream(cap)
+            try:
+                with torch.cuda.graph(graph, stream=cap):
+                    epoch_body()
+            finally:
+                ctx.set_stream(torch.cuda.current_stream())
+        torch.cuda.current_stream().wait_stream(cap)
+        torch.cuda.synchronize()
+        ctx.set_model(saved)  # the capture does not run the body, but be explicit
     for _ in range(epochs):
         order, state = shuffled_order(n, state)
-        idx = torch.from_numpy(order).to(X.device)
-        Xe, Ye = X.index_select(1, idx), Y.index_select(1, idx)
-        acc = torch.zeros((), dtype=torch.float64, device=X.device)
-        nb = 0
-        for start, b in epoch_batches(n, batch_size):
-            g, loss = ctx.train_grad_slice(Xe, Ye, start, b, grad=grad)
-            acc += loss[0] / (b * out_dim)
-            ctx.train_apply(g, lr, 1.0 / (b * out_dim))
-            nb += 1
-        v = float(acc.item()) / nb
+        torch.cuda.current_stream().synchronize()  # idx_host is read by the previous epoch
+        idx_host.copy_(torch.from_numpy(order))
+        if graph is not None:
+            graph.replay()
+        else:
+            epoch_body()
+        v = float(acc.item()) / len(batches)
         v = v if math.isfinite(v) else float("nan")
         trace.append(v)
         if math.isnan(v):
