@@ -191,16 +191,17 @@ def fit_model(ctx, features, targets, sizes, mean, std, lr: float, batch_size: i
         torch.cuda.synchronize()
         ctx.set_model(saved)
         graph = torch.cuda.CUDAGraph()
+        home = torch.cuda.current_stream()
         cap = torch.cuda.Stream()
-        cap.wait_stream(torch.cuda.current_stream())
+        cap.wait_stream(home)
         with torch.cuda.stream(cap):
             ctx.set_stream(cap)
             try:
                 with torch.cuda.graph(graph, stream=cap):
                     epoch_body()
             finally:
-                ctx.set_stream(torch.cuda.current_stream())
-        torch.cuda.current_stream().wait_stream(cap)
+                ctx.set_stream(home)  # back to the caller's stream (not the capture stream)
+        home.wait_stream(cap)
         torch.cuda.synchronize()
         ctx.set_model(saved)  # the capture does not run the body, but be explicit
     for _ in range(epochs):

@@ -193,3 +193,19 @@ def test_train_errors(ctx):
     with pytest.raises(DsoError) as e:
         cross_validate(ctx, np.random.rand(5, 134), np.random.rand(5, 7), [], 1, 1)
     assert e.value.kind == ErrorKind.InvalidArgument
+
+
+def test_fit_model_restores_context_stream(ctx, port):
+    """fit_model captures its epochs on a side stream; the context must be back on
+    the caller's stream afterwards (later launches race with torch otherwise)."""
+    import ctypes as C
+    from paper_2407_13096_b200.train import canonicalize, fit_model, target_stats as ts
+    f, t = canonicalize(*_corpus(port, 20, 0xACCE5505))
+    mean, std, _ = ts(t)
+    fit_model(ctx, f, t, [134, 100, 50, 25, 7], mean, std, 0.05, 8, 4, 3)
+    x = torch.from_numpy(np.random.default_rng(0).uniform(size=(134, 4096)).astype(np.float32)).cuda()
+    for _ in range(3):
+        p1, _, _ = ctx.predict_params(x)
+        a = p1.cpu().numpy()
+        p2, _, _ = ctx.predict_params(x)
+        np.testing.assert_array_equal(a, p2.cpu().numpy())
