@@ -5,29 +5,30 @@
 // de-standardised (forward_raw mlp.cpp:232-235) and clamped (predict_params
 // mlp.cpp:237-253, kBetaFloor mlp.cpp:15).
 //
-// Execution model — one persistent, warp-specialised CTA per SM (384 threads):
-//   * two CONSUMER groups of 4 warps (one warp per SM sub-partition each) run
-//     the MLP on alternate tiles of 64 kernels held k-major in shared memory
-//     (act[134][64]); each layer is a
-//     register-tiled FP32 GEMM on the FMA pipe with Blackwell's packed FFMA2
-//     (L1: thread = 4 kernels x 13 neurons, 26 FFMA2 per 5 shared loads;
-//     weights are warp-uniform broadcasts; operands of step k+1 in flight
-//     while step k issues); layer outputs overwrite act in place;
-//   * 4 PRODUCER warps, meanwhile, (a) finish the oldest tile: clamp, then
-//     P(f), T(f), the eta objective and the lexicographic argmin over the
-//     whole frequency grid, and (b) run the feature stage of a tile three ahead
-//     (raw PTX counts, dense or sparse -> per-category fractions fused with
-//     DCGM) straight into the buffer it frees;
+// Execution model — one persistent, warp-specialised CTA per SM (512 threads):
+//   * two CONSUMER groups of 4 warps (one warp per SM sub-partition each,
+//     setmaxnreg 160) run the MLP on alternate tiles of 64 kernels held k-major
+//     in shared memory (act[134][64]); each layer is a register-tiled FP32 GEMM
+//     on the FMA pipe with Blackwell's packed FFMA2 (L1: thread = 4 kernels x
+//     13 neurons, 26 FFMA2 per 5 shared loads, only the tile's non-zero input
+//     rows; weights are broadcasts; operands of step k+1 in flight while step
+//     k issues); layer outputs overwrite act in place.  After layer 4 the group
+//     reads its predictions, hands the buffer back (READY), clamps and runs the
+//     grid sweep + eta objective + lexicographic argmin for its tile
+//     (consumer_sweep, sweep_core.cuh) and writes the results;
+//   * 8 PRODUCER warps (setmaxnreg 96) run the feature stage of the next
+//     tiles (sparse CSR or dense PTX counts -> per-category fractions fused with
+//     DCGM, the non-zero row list) straight into the buffer the consumers free;
+//     in predict mode they also write the clamped parameters;
 //   * three activation/output buffers rotate between the roles through named
-//     barriers FULL[b] (producer -> consumer: features in act[b], out[b] free)
-//     and READY[b] (consumer -> producer: predictions in out[b], act[b] free).
-// The MLP (FMA pipe) and the feature/sweep work (LSU/ALU + a little FMA) thus
-// overlap on every SM scheduler.  The model (weights ~100 KB) is staged once per
-// CTA; nothing between a kernel's 536 input bytes and its 16 result bytes
-// touches HBM.
+//     barriers FULL[b] (producer -> consumer: features in act[b]) and READY[b]
+//     (consumer -> producer: act[b] free, predictions in out[b]).
+// The model (weights ~100 KB) is staged once per CTA; nothing between a
+// kernel's input bytes and its 16 result bytes touches HBM.
 //
-// Tensor cores are not used: TF32/BF16 products cannot meet the 1e-5 relative
-// contract on the predicted parameters.
+// Tensor cores are not used: the layer widths are small and TF32 products
+// cannot meet the 1e-5 relative contract on the predicted parameters without
+// 3xTF32 splitting.
 #include <math.h>
 
 #include <cmath>
