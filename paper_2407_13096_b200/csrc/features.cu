@@ -41,17 +41,30 @@ __global__ void __launch_bounds__(256, 2) featurize_kernel(const uint32_t* __res
                         ((reinterpret_cast<uintptr_t>(fused) & 15) == 0);
     const int64_t tiles = (n + kFeatTile - 1) / kFeatTile;
     const int tid = threadIdx.x;
-    for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    auto full = [&](int64_t tile) { return vec_ok && tile * kFeatTile + kFeatTile <= n; };
+    // the next tile's loads are issued before this tile's normalisation and
+    // stores, so every CTA keeps a tile of reads in flight while it computes
+    TileRegs R;
+    int64_t tile = blockIdx.x;
+    if (tile < tiles && full(tile)) tile_load(R, counts, dcgm, tile * kFeatTile, ld);
+    for (; tile < tiles; tile += gridDim.x) {
         const int64_t t0 = tile * kFeatTile;
-        tile_features(act, scratch, counts, dcgm, t0, n, ld, vec_ok);
-        if (vec_ok && t0 + kFeatTile <= n) {
+        if (full(tile))
+            tile_store(act, R);
+        else
+            tile_load_scalar(act, counts, dcgm, t0, n, ld);
+        __syncthreads();
+        const int64_t next = tile + gridDim.x;
+        if (next < tiles && full(next)) tile_load(R, counts, dcgm, next * kFeatTile, ld);
+        tile_normalise(act, scratch);
+        if (full(tile)) {
             const int q = tid & 31, rp = tid >> 5;
 #pragma unroll
             for (int j = 0; j < 17; ++j) {
                 const int r = rp + 8 * j;
                 if (r < DSO_FUSED_ROWS)
-                    reinterpret_cast<float4*>(fused + (int64_t)r * ld + t0)[q] =
-                        reinterpret_cast<const float4*>(act + r * kFeatTile)[q];
+                    __stcs(reinterpret_cast<float4*>(fused + (int64_t)r * ld + t0) + q,
+                           reinterpret_cast<const float4*>(act + r * kFeatTile)[q]);
             }
         } else {
             const int m = tid & (kFeatTile - 1), h = tid >> 7;
@@ -106,7 +119,7 @@ cudaError_t launch_featurize(Ctx& cx, const uint32_t* counts, const float* dcgm,
         attr = true;
     }
     const int64_t tiles = (n + kFeatTile - 1) / kFeatTile;
-    const int grid = (int)std::min<int64_t>(tiles, (int64_t)cx.num_sms * 3);
+    const int grid = (int)std::min<int64_t>(tiles, (int64_t)cx.num_sms * 2);  // 2 CTAs per SM (registers)
     featurize_kernel<<<grid, 256, smem, cx.stream>>>(counts, dcgm, n, ld, fused);
     ++cx.launches;
     return cudaGetLastError();

@@ -26,42 +26,58 @@ constexpr int kFeatTile = 128;
 //   phase 3: every entry becomes count/total, correctly rounded (Markstein).
 // scratch: 1024 floats: tf[3][128], rr[3][128] and the
 // split instr partial sums (u64 [128]).
-__device__ __forceinline__ void tile_features(float* act, float* scratch,
-                                              const uint32_t* __restrict__ counts,
-                                              const float* __restrict__ dcgm, int64_t t0,
-                                              int64_t n, int64_t ld, bool vec_ok) {
+// Registers of one full, aligned tile: 16 x 128-bit count loads + 1 DCGM load
+// per thread (a warp covers one 512-byte row segment).
+struct TileRegs {
+    uint4 v[16];
+    float4 d;
+};
+
+__device__ __forceinline__ void tile_load(TileRegs& R, const uint32_t* __restrict__ counts,
+                                          const float* __restrict__ dcgm, int64_t t0,
+                                          int64_t ld) {
+    const int q = threadIdx.x & 31, rp = threadIdx.x >> 5;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        const int r = rp + 8 * j;
+        if (r < DSO_COUNT_ROWS)
+            R.v[j] = __ldg(reinterpret_cast<const uint4*>(counts + (int64_t)r * ld + t0) + q);
+    }
+    R.d = __ldg(reinterpret_cast<const float4*>(dcgm + (int64_t)rp * ld + t0) + q);
+}
+
+__device__ __forceinline__ void tile_store(float* act, const TileRegs& R) {
+    uint32_t* acti = reinterpret_cast<uint32_t*>(act);
+    const int q = threadIdx.x & 31, rp = threadIdx.x >> 5;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        const int r = rp + 8 * j;
+        if (r < DSO_COUNT_ROWS) reinterpret_cast<uint4*>(acti + (8 + r) * kFeatTile)[q] = R.v[j];
+    }
+    reinterpret_cast<float4*>(act + rp * kFeatTile)[q] = R.d;
+}
+
+// Ragged last tile / unaligned inputs: scalar loads straight into act.
+__device__ __forceinline__ void tile_load_scalar(float* act, const uint32_t* __restrict__ counts,
+                                                 const float* __restrict__ dcgm, int64_t t0,
+                                                 int64_t n, int64_t ld) {
+    uint32_t* acti = reinterpret_cast<uint32_t*>(act);
+    const int m = threadIdx.x & (kFeatTile - 1);
+    const int h = threadIdx.x >> 7;
+    const int64_t k = t0 + m;
+    const bool live = k < n;
+#pragma unroll 9
+    for (int r = h; r < DSO_COUNT_ROWS; r += 2)
+        acti[(8 + r) * kFeatTile + m] = live ? __ldg(counts + (int64_t)r * ld + k) : 0u;
+#pragma unroll
+    for (int r = h; r < 8; r += 2) act[r * kFeatTile + m] = live ? __ldg(dcgm + (int64_t)r * ld + k) : 0.f;
+}
+
+// Normalise a staged tile in place (phases 2 and 3 below); act holds the raw
+// counts in rows 8.. and the DCGM rows 0..7 (the caller synchronised).
+__device__ __forceinline__ void tile_normalise(float* act, float* scratch) {
     uint32_t* acti = reinterpret_cast<uint32_t*>(act);
     const int tid = threadIdx.x;
-    if (vec_ok && t0 + kFeatTile <= n) {
-        const int q = tid & 31;   // kernels 4q .. 4q+3
-        const int rp = tid >> 5;  // row phase = warp index (0..7)
-        uint4 v[16];
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-            const int r = rp + 8 * j;
-            if (r < DSO_COUNT_ROWS)
-                v[j] = __ldg(reinterpret_cast<const uint4*>(counts + (int64_t)r * ld + t0) + q);
-        }
-        const float4 d = __ldg(reinterpret_cast<const float4*>(dcgm + (int64_t)rp * ld + t0) + q);
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-            const int r = rp + 8 * j;
-            if (r < DSO_COUNT_ROWS) reinterpret_cast<uint4*>(acti + (8 + r) * kFeatTile)[q] = v[j];
-        }
-        reinterpret_cast<float4*>(act + rp * kFeatTile)[q] = d;
-    } else {
-        const int m = tid & (kFeatTile - 1);
-        const int h = tid >> 7;
-        const int64_t k = t0 + m;
-        const bool live = k < n;
-#pragma unroll 9
-        for (int r = h; r < DSO_COUNT_ROWS; r += 2)
-            acti[(8 + r) * kFeatTile + m] = live ? __ldg(counts + (int64_t)r * ld + k) : 0u;
-#pragma unroll
-        for (int r = h; r < 8; r += 2)
-            act[r * kFeatTile + m] = live ? __ldg(dcgm + (int64_t)r * ld + k) : 0.f;
-    }
-    __syncthreads();
     // phase 2: exact totals (u64), split so both thread halves sum ~63 rows.
     // scratch (1024 floats): tf[3][128], rr[3][128], part u64[128]
     float* tfv = scratch;
@@ -71,6 +87,7 @@ __device__ __forceinline__ void tile_features(float* act, float* scratch,
     const int m = tid & (kFeatTile - 1);
     uint64_t s_a = 0, s_b = 0, s_c = 0;
     if (tid < kFeatTile) {
+    #pragma unroll 10
         for (int r = 0; r < kSplit; ++r) s_a += acti[(8 + r) * kFeatTile + m];
     } else {
         for (int r = kSplit; r < DSO_INSTR_SLOTS; ++r) s_a += acti[(8 + r) * kFeatTile + m];
