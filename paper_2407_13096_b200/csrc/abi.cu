@@ -189,6 +189,7 @@ int32_t dso_ctx_destroy(dso_ctx* ctx) {
     fit_plan_free(c);
     cudaFree(c.model.wt);
     cudaFree(c.model.w_master);
+    cudaFree(c.model.w_train);
     cudaFree(c.scratch);
     cudaFree(c.train_scratch);
     for (auto& s : c.aux)
@@ -367,6 +368,7 @@ int32_t dso_set_model(dso_ctx* ctx, const int32_t* sizes, int32_t n_sizes, const
     for (int64_t i = 0; i < md.n_biases; ++i) master[md.n_weights + i] = (float)b[i];
     DSO_CUDA(ctx, cudaStreamSynchronize(c.stream));
     if (!md.w_master) DSO_CUDA(ctx, cudaMalloc(&md.w_master, sizeof(float) * master.size()));
+    md.train_dirty = true;
     DSO_CUDA(ctx, cudaMemcpy(md.w_master, master.data(), sizeof(float) * master.size(),
                              cudaMemcpyHostToDevice));
     DSO_CUDA(ctx, model_upload(c, W, b));

@@ -65,6 +65,10 @@ struct ModelDev {
     int64_t wt_floats, bias_floats;
     // master copy in the reference layout (row-major W, concatenated), f32
     float* w_master;  // [n_weights + n_biases]
+    // the training kernel's shared-memory image of the weights (train.cu), rebuilt
+    // from w_master before the next gradient after any change of w_master
+    float* w_train;
+    bool train_dirty;
     int64_t n_weights, n_biases;
 };
 

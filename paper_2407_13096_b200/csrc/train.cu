@@ -34,7 +34,7 @@ constexpr int RS2 = RS / 2;  // in float2 units
 constexpr int kThreads = 256;
 
 // packed weights (floats): layer l stored [K][8 groups][TNP], neuron n = TN*g + t
-constexpr int W1S = 0;                     // [134][8][16], TN 13
+constexpr int W1S = 0;                     // [134][16][8], layer 1: neuron n = 7*g + t
 constexpr int W2S = W1S + 134 * 8 * 16;    // [100][8][8],  TN 7
 constexpr int W3S = W2S + 100 * 8 * 8;     // [50][8][4],   TN 4
 constexpr int W4S = W3S + 50 * 8 * 4;      // [25][8],      TN 1
@@ -64,41 +64,54 @@ constexpr int kMasterFloats = MB4 + 7;  // 20007
 
 __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
 
-__device__ void stage_weights(float* sm, const float* __restrict__ m) {
-    for (int i = threadIdx.x; i < A0S; i += kThreads) sm[i] = 0.f;
-    __syncthreads();
-    for (int e = threadIdx.x; e < 100 * 134; e += kThreads) {
+// The weight image [0, A0S) of the training kernel's shared memory — forward
+// packings per layer, transposed copies for the delta recursion, biases, zero
+// padding — built from the master weights once per update (train_pack_kernel)
+// and copied verbatim into every CTA's shared memory with 128-bit loads.
+// (The image is zeroed by a memset first; the padding stays zero.)
+__global__ void __launch_bounds__(kThreads) train_pack_kernel(const float* __restrict__ m,
+                                                              float* __restrict__ img) {
+    float* sm = img;
+
+    for (int e = blockIdx.x * kThreads + threadIdx.x; e < 100 * 134; e += gridDim.x * kThreads) {
         const int n = e / 134, k = e - n * 134;
-        sm[W1S + (k * 8 + n / 13) * 16 + n % 13] = m[MW1 + e];
+        sm[W1S + (k * 16 + n / 7) * 8 + n % 7] = m[MW1 + e];
     }
-    for (int e = threadIdx.x; e < 50 * 100; e += kThreads) {
+    for (int e = blockIdx.x * kThreads + threadIdx.x; e < 50 * 100; e += gridDim.x * kThreads) {
         const int n = e / 100, k = e - n * 100;
         sm[W2S + (k * 8 + n / 7) * 8 + n % 7] = m[MW2 + e];
     }
-    for (int e = threadIdx.x; e < 25 * 50; e += kThreads) {
+    for (int e = blockIdx.x * kThreads + threadIdx.x; e < 25 * 50; e += gridDim.x * kThreads) {
         const int n = e / 50, k = e - n * 50;
         sm[W3S + (k * 8 + n / 4) * 4 + n % 4] = m[MW3 + e];
     }
-    for (int e = threadIdx.x; e < 7 * 25; e += kThreads) {
+    for (int e = blockIdx.x * kThreads + threadIdx.x; e < 7 * 25; e += gridDim.x * kThreads) {
         const int n = e / 25, k = e - n * 25;
         sm[W4S + k * 8 + n] = m[MW4 + e];
     }
-    for (int i = threadIdx.x; i < 100; i += kThreads) sm[B1S + i] = m[MB1 + i];
-    for (int i = threadIdx.x; i < 50; i += kThreads) sm[B2S + i] = m[MB2 + i];
-    for (int i = threadIdx.x; i < 25; i += kThreads) sm[B3S + i] = m[MB3 + i];
-    for (int i = threadIdx.x; i < 7; i += kThreads) sm[B4S + i] = m[MB4 + i];
-    for (int e = threadIdx.x; e < 50 * 100; e += kThreads) {
+    for (int i = blockIdx.x * kThreads + threadIdx.x; i < 100; i += gridDim.x * kThreads) sm[B1S + i] = m[MB1 + i];
+    for (int i = blockIdx.x * kThreads + threadIdx.x; i < 50; i += gridDim.x * kThreads) sm[B2S + i] = m[MB2 + i];
+    for (int i = blockIdx.x * kThreads + threadIdx.x; i < 25; i += gridDim.x * kThreads) sm[B3S + i] = m[MB3 + i];
+    for (int i = blockIdx.x * kThreads + threadIdx.x; i < 7; i += gridDim.x * kThreads) sm[B4S + i] = m[MB4 + i];
+    for (int e = blockIdx.x * kThreads + threadIdx.x; e < 50 * 100; e += gridDim.x * kThreads) {
         const int n = e / 100, k = e - n * 100;
         sm[T2S + (n * 8 + k / 13) * 16 + k % 13] = m[MW2 + e];
     }
-    for (int e = threadIdx.x; e < 25 * 50; e += kThreads) {
+    for (int e = blockIdx.x * kThreads + threadIdx.x; e < 25 * 50; e += gridDim.x * kThreads) {
         const int n = e / 50, k = e - n * 50;
         sm[T3S + (n * 8 + k / 7) * 8 + k % 7] = m[MW3 + e];
     }
-    for (int e = threadIdx.x; e < 7 * 25; e += kThreads) {
+    for (int e = blockIdx.x * kThreads + threadIdx.x; e < 7 * 25; e += gridDim.x * kThreads) {
         const int n = e / 25, k = e - n * 25;
         sm[T4S + (n * 8 + k / 4) * 4 + k % 4] = m[MW4 + e];
     }
+}
+
+__device__ __forceinline__ void stage_weights(float* sm, const float* __restrict__ img) {
+    static_assert(A0S % 4 == 0, "image is a whole number of float4");
+    const float4* src = reinterpret_cast<const float4*>(img);
+    float4* dst = reinterpret_cast<float4*>(sm);
+    for (int i = threadIdx.x; i < A0S / 4; i += kThreads) dst[i] = __ldg(src + i);
 }
 
 // Dense layer on a 64-sample tile: out[TN*g+t][m] = act(sum_k W[k][g][t] in[k][m] + b).
@@ -154,6 +167,66 @@ __device__ __forceinline__ void dense(const float* sm, int woff, int boff, int i
         float2 z = f2(acc[t].x + bb, acc[t].y + bb);
         if (SIGMOID) z = f2(sigmoidf_fast(z.x), sigmoidf_fast(z.y));
         out2[(TN * g + t) * RS2 + mp] = z;
+    }
+}
+
+// Layer 1 (134 -> 100, half of the forward/backward work): thread = 4 samples
+// (a float4 of A0) x 7 neurons of group g (16 groups, 112 slots); a warp reads
+// 16 sample quads (2 wavefronts) and the weights of 2 groups (2 LDS.128 of 8) per
+// k for 14 FFMA2 — about 1.6x fewer shared-memory wavefronts per FFMA2 than the
+// generic dense<> tile; two k per stage, operands of the next stage in flight.
+__device__ __forceinline__ void dense_l1(float* sm) {
+    const int lane = threadIdx.x & 31;
+    const int sq = lane & 15, g = (threadIdx.x >> 5) * 2 + (lane >> 4);
+    constexpr int RS4 = RS / 4;
+    const float4* a4 = reinterpret_cast<const float4*>(sm + A0S) + sq;
+    const float4* w4 = reinterpret_cast<const float4*>(sm + W1S) + g * 2;
+    float2 acc0[7], acc1[7];
+#pragma unroll
+    for (int t = 0; t < 7; ++t) acc0[t] = acc1[t] = f2(0.f, 0.f);
+    struct Op {
+        float4 a[2], w0[2], w1[2];
+    };
+    auto load = [&](Op& o, int k) {
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            o.a[u] = a4[(k + u) * RS4];
+            o.w0[u] = w4[(k + u) * 32];
+            o.w1[u] = w4[(k + u) * 32 + 1];
+        }
+    };
+    auto math = [&](const Op& o) {
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const float w[7] = {o.w0[u].x, o.w0[u].y, o.w0[u].z, o.w0[u].w,
+                                o.w1[u].x, o.w1[u].y, o.w1[u].z};
+            const float2 a01 = f2(o.a[u].x, o.a[u].y), a23 = f2(o.a[u].z, o.a[u].w);
+#pragma unroll
+            for (int t = 0; t < 7; ++t) {
+                acc0[t] = ffma2(a01, f2(w[t], w[t]), acc0[t]);
+                acc1[t] = ffma2(a23, f2(w[t], w[t]), acc1[t]);
+            }
+        }
+    };
+    Op A, B;
+    load(A, 0);
+#pragma unroll 1
+    for (int k = 0; k < 132; k += 4) {  // 134 = 33 double stages + one trailing pair
+        load(B, k + 2);
+        math(A);
+        load(A, k + 4);
+        math(B);
+    }
+    math(A);  // k = 132, 133
+    float4* out4 = reinterpret_cast<float4*>(sm + A1S) + sq;
+#pragma unroll
+    for (int t = 0; t < 7; ++t) {
+        const int n = 7 * g + t;
+        if (n < 100) {
+            const float bb = sm[B1S + n];
+            out4[n * RS4] = make_float4(sigmoidf_fast(acc0[t].x + bb), sigmoidf_fast(acc0[t].y + bb),
+                                        sigmoidf_fast(acc1[t].x + bb), sigmoidf_fast(acc1[t].y + bb));
+        }
     }
 }
 
@@ -273,13 +346,22 @@ __global__ void __launch_bounds__(kThreads, 1)
                 sm[A0S + r * RS + m] = m < valid ? __ldg(x + (int64_t)r * ld + t0 + m) : 0.f;
             }
         }
-        for (int e = tid; e < 8 * TM; e += kThreads) {
-            const int r = e / TM, m = e - r * TM;
-            sm[YS + r * RS + m] = (r < 7 && m < valid) ? __ldg(y + (int64_t)r * ld + t0 + m) : 0.f;
+        if (valid == TM && (ld & 3) == 0 && (reinterpret_cast<uintptr_t>(y) & 15) == 0) {
+            for (int e = tid; e < 8 * (TM / 4); e += kThreads) {
+                const int r = e / (TM / 4), q = e % (TM / 4);
+                reinterpret_cast<float4*>(sm + YS + r * RS)[q] =
+                    r < 7 ? __ldg(reinterpret_cast<const float4*>(y + (int64_t)r * ld + t0) + q)
+                          : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+        } else {
+            for (int e = tid; e < 8 * TM; e += kThreads) {
+                const int r = e / TM, m = e - r * TM;
+                sm[YS + r * RS + m] = (r < 7 && m < valid) ? __ldg(y + (int64_t)r * ld + t0 + m) : 0.f;
+            }
         }
         __syncthreads();
         // ---- forward (forward_trace) -------------------------------------------------
-        dense<134, 13, 16, true>(sm, W1S, B1S, A0S, A1S);
+        dense_l1(sm);
         __syncthreads();
         const int64_t next = tile + gridDim.x;
         prefetched = next < tiles && xvec && full_tile(next);
@@ -544,16 +626,20 @@ __global__ void __launch_bounds__(WG_THREADS, 1)
 __global__ void reduce_partials(const float* __restrict__ partial, int parts,
                                 const double* __restrict__ loss_partial, int loss_parts,
                                 float* __restrict__ grad, double* __restrict__ loss_sum) {
-    const int e = blockIdx.x * blockDim.x + threadIdx.x;
-    if (e < kMasterFloats) {
-        double s = 0.0;
-        for (int c = 0; c < parts; ++c) s += partial[(int64_t)c * kMasterFloats + e];
-        grad[e] = (float)s;
-    }
-    if (e == 0) {
-        double s = 0.0;
-        for (int c = 0; c < loss_parts; ++c) s += loss_partial[c];
-        *loss_sum = s;
+    // 8 lanes per output: lane j sums parts j, j+8, ... in order, then a fixed
+    // butterfly combines them — deterministic, and 8x the loads in flight
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    const int e = t >> 3, j = t & 7;
+    double s = 0.0;
+    if (e < kMasterFloats)
+        for (int c = j; c < parts; c += 8) s += partial[(int64_t)c * kMasterFloats + e];
+#pragma unroll
+    for (int o = 4; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (e < kMasterFloats && j == 0) grad[e] = (float)s;
+    if (t == 0) {
+        double l = 0.0;
+        for (int c = 0; c < loss_parts; ++c) l += loss_partial[c];
+        *loss_sum = l;
     }
 }
 
@@ -599,7 +685,19 @@ cudaError_t launch_train_grad(Ctx& cx, const float* x, const float* y, int64_t n
     // writes its partial, and the reduction reads exactly those
     const int64_t tiles = (n + TM - 1) / TM;
     const int fb_parts = (int)std::max<int64_t>(1, std::min<int64_t>(parts, tiles));
-    train_fb_kernel<<<fb_parts, kThreads, smem, cx.stream>>>(cx.model.w_master, x, y, n, ld, act,
+    if (!cx.model.w_train) {
+        cudaError_t e = cudaMalloc(&cx.model.w_train, sizeof(float) * A0S);
+        if (e != cudaSuccess) return e;
+        cx.model.train_dirty = true;
+    }
+    if (cx.model.train_dirty) {  // the image is 100 KB: memset + scatter
+        cudaError_t e = cudaMemsetAsync(cx.model.w_train, 0, sizeof(float) * A0S, cx.stream);
+        if (e != cudaSuccess) return e;
+        train_pack_kernel<<<64, kThreads, 0, cx.stream>>>(cx.model.w_master, cx.model.w_train);
+        ++cx.launches;
+        cx.model.train_dirty = false;
+    }
+    train_fb_kernel<<<fb_parts, kThreads, smem, cx.stream>>>(cx.model.w_train, x, y, n, ld, act,
                                                              lds, lp);
     const int64_t chunks = (n + WG_CHUNK - 1) / WG_CHUNK;
     const int wg_parts = (int)std::max<int64_t>(1, std::min<int64_t>(parts, chunks));
@@ -608,7 +706,7 @@ cudaError_t launch_train_grad(Ctx& cx, const float* x, const float* y, int64_t n
     if (per == 0) per = WG_CHUNK;
     train_wgrad_kernel<<<wg_parts, WG_THREADS, smem_wg, cx.stream>>>(x, ld, act, lds, n, per,
                                                                      partial);
-    reduce_partials<<<(kMasterFloats + 255) / 256, 256, 0, cx.stream>>>(partial, wg_parts, lp,
+    reduce_partials<<<(kMasterFloats * 8 + 255) / 256, 256, 0, cx.stream>>>(partial, wg_parts, lp,
                                                                         fb_parts, grad,
                                                                         loss_sum_dev);
     cx.launches += 3;
@@ -616,6 +714,7 @@ cudaError_t launch_train_grad(Ctx& cx, const float* x, const float* y, int64_t n
 }
 
 cudaError_t launch_train_apply(Ctx& cx, const float* grad, float lr_scale) {
+    cx.model.train_dirty = true;
     sgd_apply<<<(kMasterFloats + 255) / 256, 256, 0, cx.stream>>>(cx.model.w_master, grad,
                                                                   lr_scale);
     ++cx.launches;
