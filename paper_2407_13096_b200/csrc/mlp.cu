@@ -117,12 +117,15 @@ constexpr int ROWS = MBAR + 8;              // u32 [3][68]
 constexpr int kRowWords = 68;
 constexpr int ROWCNT = ROWS + kBufs * kRowWords;  // int [3] (+1 pad)
 constexpr int MASKW = ROWCNT + 4;           // u32 [4]: slots 0..125 present in the tile
+#ifndef DSO_PRODUCER_UNROLL
+#define DSO_PRODUCER_UNROLL 2
+#endif
 #ifndef DSO_CSWEEP
 #define DSO_CSWEEP 64
 #endif
 constexpr int kCSweep = DSO_CSWEEP;                 // kernels per tile swept by the consumer group
 constexpr int CSCR = MASKW + 4;             // consumer merge scratch [2 groups][3][4][32]
-constexpr int kCScrFloats = 3 * (kGroupThreads / kCSweep) * kCSweep;
+constexpr int kCScrFloats = kCSweep > 0 ? 3 * (kGroupThreads / kCSweep) * kCSweep : 4;
 constexpr int TABLES = CSCR + 2 * kCScrFloats;  // core4[nc], mem2[nm]
 static_assert(W2S % 4 == 0 && W3S % 4 == 0 && W4S % 4 == 0 && B1S % 4 == 0 &&
                   kModelFloats % 4 == 0 && ACT % 4 == 0 && OUT % 4 == 0 && SCR % 4 == 0 &&
@@ -906,8 +909,9 @@ __device__ __forceinline__ void write_result(const Job& J, int64_t k, int duty, 
 __device__ __forceinline__ void consumer_sweep(const float* sm, const float* out, const Job& J,
                                                int64_t t0, int ct, int cbar, int ready_bar,
                                                float* cs) {
-    constexpr int P = kGroupThreads / kCSweep;
-    const int m = ct % kCSweep, part = ct / kCSweep;
+    constexpr int KC = kCSweep > 0 ? kCSweep : 1;
+    constexpr int P = kGroupThreads / KC;
+    const int m = ct % KC, part = ct / KC;
     bar_sync(cbar, kGroupThreads);  // L4 outputs in out
     float pr[7];
 #pragma unroll
@@ -918,11 +922,11 @@ __device__ __forceinline__ void consumer_sweep(const float* sm, const float* out
     const float4* s_core = reinterpret_cast<const float4*>(sm + TABLES);
     const float2* s_mem = reinterpret_cast<const float2*>(sm + TABLES + 4 * J.nc);
     const Best b = sweep_dispatch<4>(p, s_core, s_mem, J, J.nc * part / P, J.nc * (part + 1) / P);
-    cs[part * kCSweep + m] = b.c;
-    cs[P * kCSweep + part * kCSweep + m] = b.e;
-    reinterpret_cast<int*>(cs)[2 * P * kCSweep + part * kCSweep + m] = b.i;
+    cs[part * KC + m] = b.c;
+    cs[P * KC + part * KC + m] = b.e;
+    reinterpret_cast<int*>(cs)[2 * P * KC + part * KC + m] = b.i;
     bar_sync(cbar, kGroupThreads);
-    const Best r = merge_parts<P, kCSweep>(cs, m);
+    const Best r = merge_parts<P, KC>(cs, m);
 #pragma unroll
     for (int d = 0; d < 4; ++d)  // the four output duties spread over the parts
         if (d * P / 4 == part) write_result(J, t0 + m, d, r, cl, pr, p, s_core, s_mem);
@@ -966,7 +970,8 @@ __device__ __forceinline__ void produce_results(const float* sm, const float* ou
     const KParams p{pr[0], pr[1], pr[2], pr[3], pr[4], pr[5], pr[6]};
     const float4* s_core = reinterpret_cast<const float4*>(sm + TABLES);
     const float2* s_mem = reinterpret_cast<const float2*>(sm + TABLES + 4 * J.nc);
-    const Best b = sweep_dispatch<2>(p, s_core, s_mem, J, J.nc * part / P, J.nc * (part + 1) / P);
+    const Best b = sweep_dispatch<DSO_PRODUCER_UNROLL>(p, s_core, s_mem, J, J.nc * part / P,
+                                                       J.nc * (part + 1) / P);
     float* xc = const_cast<float*>(sm) + SCR;  // [P][NK] cost, energy, index
     xc[part * NK + mm] = b.c;
     xc[P * NK + part * NK + mm] = b.e;
@@ -1041,6 +1046,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (PIPE) {
                 // READY is arrived inside, as soon as the predictions are read
                 PT_BEGIN(t_s);
+                if (kCSweep == 0) {  // the producers sweep the whole tile
+                    bar_sync(BAR_CONS0 + G, kGroupThreads);
+                    bar_arrive(BAR_READY0 + b, kHandoff);
+                } else
                 consumer_sweep(sm, sm + OUT + b * kOutFloats, J,
                                (blockIdx.x + i * gridDim.x) * (int64_t)TM, ct, BAR_CONS0 + G,
                                BAR_READY0 + b, sm + CSCR + G * kCScrFloats);
