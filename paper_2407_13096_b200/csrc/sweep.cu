@@ -30,6 +30,9 @@ namespace dso_b200 {
 namespace {
 
 constexpr int kBlock = 256;
+#ifndef DSO_ETA_CH
+#define DSO_ETA_CH 26
+#endif
 
 __device__ __forceinline__ bool params_invalid(float p0, float kp, float g, float c, float t0,
                                                float a, float b) {
@@ -384,7 +387,7 @@ cudaError_t launch_eta_sweep(Ctx& cx, const float* params, int64_t n, int64_t ld
     const DomainDev& d = cx.dom;
     if (fast && d.nm >= 1 && d.nm <= 4) {
         // chunks of up to 26 etas (101 -> 4 chunks of 26, 3 padding slots)
-        constexpr int CH = 26;
+        constexpr int CH = DSO_ETA_CH;
         const int chunks = (n_eta + CH - 1) / CH;
         const int gx = grid_for(n, 128, cx.num_sms, 16);
         dim3 grid(gx, chunks);
