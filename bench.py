@@ -390,16 +390,19 @@ def run_ours(args, rank, world, local_rank):
     roofline = {
         "bound": "fp32", "achieved": achieved, "peak": pk, "unit": "TFLOP/s",
         "frac": achieved / pk,
-        "traffic": ncu_traffic(args.config, n) if csr else None,
+        "traffic": ncu_traffic(args.config, n) if (csr or args.config == "c4") else None,
         "traffic_unit": "bytes per launch (ncu dram__bytes_read+write, profiles/ncu_summary.json)",
-        "algorithmic_bytes_per_launch": n * ((136 if csr else 536) + 16)
-        if args.config != "c4" else None,
-        "kernel": "pipeline_kernel" if args.config != "c4" else "eta_sweep_kernel",
+        "algorithmic_bytes_per_launch": (n * ((136 if csr else 536) + 16) if args.config != "c4"
+                                         else n * (28 + 101 * 8)),
+        "kernel": "ws_kernel (fused pipeline)" if args.config != "c4" else "eta_sweep_fast_kernel",
         "flops_per_kernel": flops_per_step / n if args.config != "c4" else None,
         "flops_note": ("layer 1 counted on the 8 DCGM + non-zero count rows of each kernel "
                        "(CSR input; all-zero rows are skipped exactly); the dense-input "
                        "count (SURVEY.md §8(d): 39,650 + 14 per pair) is "
-                       "flops_per_kernel_dense" if csr and args.config != "c4" else None),
+                       "flops_per_kernel_dense" if csr and args.config != "c4" else
+                       ("9 flops per (kernel, pair) for P, T, E plus 3 per (kernel, pair, eta); "
+                        "the kernel is bound by the ALU pipe (group min trees and selects: "
+                        "profiles/r1/ncu_eta_sweep_metrics.txt)" if args.config == "c4" else None)),
         "flops_per_kernel_dense": (MLP_FLOPS + PAIR_FLOPS * dom.pairs)
         if args.config != "c4" else None,
         "peak_source": ("measured in this run by dso_probe_fp32_peak (FFMA2 loop, 148x4 CTAs); "
@@ -511,7 +514,9 @@ def run_train(args, rank, world, local_rank, ctx, dom, model, n):
         "config": {"workload": cfg["desc"], "samples_per_gpu": n, "batch_per_gpu": B,
                    "global_batch": B * world, "parallelism": f"dp{world} (NCCL allreduce)"},
         "roofline": {"bound": "fp32", "achieved": achieved, "peak": v.value, "unit": "TFLOP/s",
-                     "frac": achieved / v.value, "traffic": None, "kernel": "train_grad_kernel",
+                     "frac": achieved / v.value, "traffic": ncu_traffic("c5", B),
+                     "traffic_unit": "bytes per dso_train_grad (ncu, profiles/ncu_summary.json)",
+                     "kernel": "train_fb_kernel + train_wgrad_kernel + reduce_partials",
                      "flops_per_sample": TRAIN_FLOPS, "grad_kernel_ms": grad_ms},
         "gpu_launches": ctx.launch_count - launches0, "clocks": clk.summary(),
     }

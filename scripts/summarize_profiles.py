@@ -71,6 +71,29 @@ for rep_name, tag in (("prof_eta.ncu-rep", "eta_sweep"), ("prof_train.ncu-rep", 
             f.write(f"## {d.get('Kernel Name')}\n")
             for k in KEYS[1:]:
                 f.write(f"{k}\t{d.get(k)}\t{u.get(k, '')}\n")
+# DRAM traffic per unit for the C4 (eta sweep, 1M-kernel capture) and C5 (training,
+# 65,536-sample batch: the forward/backward + weight-gradient kernels) roofline lines
+for rep_name, cfg_key, units, unit_name in (("prof_eta.ncu-rep", "c4", 1048576, "kernel"),
+                                            ("prof_train.ncu-rep", "c5", 65536, "sample")):
+    rp = os.path.join(src, rep_name)
+    if not os.path.exists(rp):
+        continue
+    txt = subprocess.run(["ncu", "-i", rp, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
+    rows = list(csv.reader(io.StringIO(txt)))
+    tot, names = 0.0, []
+    for vals in rows[2:]:
+        d = dict(zip(rows[0], vals))
+        u = dict(zip(rows[0], rows[1]))
+        sc = 1e6 if u.get("dram__bytes_read.sum", "").startswith("M") else (
+            1e9 if u.get("dram__bytes_read.sum", "").startswith("G") else 1e3)
+        tot += (float(d["dram__bytes_read.sum"]) + float(d["dram__bytes_write.sum"])) * sc
+        names.append(d["Kernel Name"].split("(")[0])
+    summary[cfg_key] = {"kernel": " + ".join(names), "units_per_capture": units,
+                        f"dram_bytes_per_{unit_name}": tot / units,
+                        "dram_bytes_per_kernel": tot / units,
+                        "source": f"{dst}/ncu_{'eta_sweep' if cfg_key == 'c4' else 'train'}"
+                                  f"_metrics.txt (ncu --set full)"}
 for extra in ("phase_timing.txt", "launches_c5.csv"):
     p = os.path.join(src, extra)
     if os.path.exists(p):
