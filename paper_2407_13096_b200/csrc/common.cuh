@@ -166,7 +166,10 @@ __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
 }
 
 // Packed FP32x2 add / mul (FADD2 / FMUL2): same IEEE round-to-nearest result as
-// the scalar __fadd_rn / __fmul_rn on each lane.
+// the scalar __fadd_rn / __fmul_rn on each lane.  Unlike the scalar forms they
+// are contractable: ptxas fuses an fmul2 feeding an fadd2 into one FFMA2 (.rn
+// is mandatory on f32x2, so it cannot mark the pair), so bit-exact paths never
+// chain the two.
 __device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
     unsigned long long A = *reinterpret_cast<unsigned long long*>(&a);
     unsigned long long B = *reinterpret_cast<unsigned long long*>(&b), D;

@@ -127,6 +127,10 @@ constexpr int kCSweep = DSO_CSWEEP;                 // kernels per tile swept by
 constexpr int CSCR = MASKW + 4;             // consumer merge scratch [2 groups][3][4][32]
 constexpr int kCScrFloats = kCSweep > 0 ? 3 * (kGroupThreads / kCSweep) * kCSweep : 4;
 constexpr int TABLES = CSCR + 2 * kCScrFloats;  // core4[nc], mem2[nm]
+// level-pair table (sweep_core.cuh build_pairs) after core4[nc], mem2[nm]
+__host__ __device__ __forceinline__ int pairs_offset(int nc, int nm) {
+    return (TABLES + 4 * nc + 2 * nm + 3) & ~3;
+}
 static_assert(W2S % 4 == 0 && W3S % 4 == 0 && W4S % 4 == 0 && B1S % 4 == 0 &&
                   kModelFloats % 4 == 0 && ACT % 4 == 0 && OUT % 4 == 0 && SCR % 4 == 0 &&
                   MBAR % 2 == 0 && ROWS % 4 == 0 && TABLES % 4 == 0 && CSCR % 4 == 0,
@@ -601,7 +605,8 @@ struct Job {
     const float2* mem2;
     int nc, nm;
     float eta, K;
-    bool fast;  // fast exact sweep allowed (fast_sweep_ok)
+    bool fast;   // fast exact sweep allowed (fast_sweep_ok)
+    bool pairs;  // level-pair table staged after the level tables (pairs_offset)
     // outputs
     float* params;
     uint8_t* clamped;
@@ -854,11 +859,25 @@ __device__ __forceinline__ Best sweep_dispatch(const KParams& p, const float4* s
     Best b{__int_as_float(0x7fc00000), __int_as_float(0x7fc00000), -1};  // i = -1: empty part
     if (i_lo >= i_hi) return b;
     const int nm = J.nm;
-    if (nm == 4) return sweep_best<4, UNR>(p, s_core, s_mem, 4, i_lo, i_hi, J.eta, J.K, J.fast);
-    if (nm == 1) return sweep_best<1, UNR>(p, s_core, s_mem, 1, i_lo, i_hi, J.eta, J.K, J.fast);
-    if (nm == 3) return sweep_best<3, UNR>(p, s_core, s_mem, 3, i_lo, i_hi, J.eta, J.K, J.fast);
-    if (nm == 2) return sweep_best<2, UNR>(p, s_core, s_mem, 2, i_lo, i_hi, J.eta, J.K, J.fast);
+    const float4* s_pair =
+        J.pairs ? reinterpret_cast<const float4*>(reinterpret_cast<const float*>(s_core) -
+                                                  TABLES + pairs_offset(J.nc, nm))
+                : nullptr;
+    if (nm == 4)
+        return sweep_best<4, UNR>(p, s_core, s_mem, 4, i_lo, i_hi, J.eta, J.K, J.fast, s_pair);
+    if (nm == 1)
+        return sweep_best<1, UNR>(p, s_core, s_mem, 1, i_lo, i_hi, J.eta, J.K, J.fast, s_pair);
+    if (nm == 3)
+        return sweep_best<3, UNR>(p, s_core, s_mem, 3, i_lo, i_hi, J.eta, J.K, J.fast, s_pair);
+    if (nm == 2)
+        return sweep_best<2, UNR>(p, s_core, s_mem, 2, i_lo, i_hi, J.eta, J.K, J.fast, s_pair);
     return sweep_best<0, UNR>(p, s_core, s_mem, nm, i_lo, i_hi, J.eta, J.K, false);
+}
+
+// First level of part `part` of P over nc levels: even, so every part's groups
+// start on a level pair (the last part ends at nc).
+__device__ __forceinline__ int part_lo(int nc, int part, int P) {
+    return part >= P ? nc : (nc * part / P) & ~1;
 }
 
 // Merge P parts [P][NK] of (cost, energy, index) for kernel m (merge_best is
@@ -921,7 +940,8 @@ __device__ __forceinline__ void consumer_sweep(const float* sm, const float* out
     const KParams p{pr[0], pr[1], pr[2], pr[3], pr[4], pr[5], pr[6]};
     const float4* s_core = reinterpret_cast<const float4*>(sm + TABLES);
     const float2* s_mem = reinterpret_cast<const float2*>(sm + TABLES + 4 * J.nc);
-    const Best b = sweep_dispatch<4>(p, s_core, s_mem, J, J.nc * part / P, J.nc * (part + 1) / P);
+    const Best b = sweep_dispatch<4>(p, s_core, s_mem, J, part_lo(J.nc, part, P),
+                                     part_lo(J.nc, part + 1, P));
     cs[part * KC + m] = b.c;
     cs[P * KC + part * KC + m] = b.e;
     reinterpret_cast<int*>(cs)[2 * P * KC + part * KC + m] = b.i;
@@ -970,8 +990,8 @@ __device__ __forceinline__ void produce_results(const float* sm, const float* ou
     const KParams p{pr[0], pr[1], pr[2], pr[3], pr[4], pr[5], pr[6]};
     const float4* s_core = reinterpret_cast<const float4*>(sm + TABLES);
     const float2* s_mem = reinterpret_cast<const float2*>(sm + TABLES + 4 * J.nc);
-    const Best b = sweep_dispatch<DSO_PRODUCER_UNROLL>(p, s_core, s_mem, J, J.nc * part / P,
-                                                       J.nc * (part + 1) / P);
+    const Best b = sweep_dispatch<DSO_PRODUCER_UNROLL>(p, s_core, s_mem, J, part_lo(J.nc, part, P),
+                                                       part_lo(J.nc, part + 1, P));
     float* xc = const_cast<float*>(sm) + SCR;  // [P][NK] cost, energy, index
     xc[part * NK + mm] = b.c;
     xc[P * NK + part * NK + mm] = b.e;
@@ -1009,6 +1029,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             float2* smm = reinterpret_cast<float2*>(sm + TABLES + 4 * J.nc);
             for (int i = threadIdx.x; i < J.nc; i += kThreads) sc[i] = J.core4[i];
             for (int j = threadIdx.x; j < J.nm; j += kThreads) smm[j] = J.mem2[j];
+            if (J.pairs)
+                build_pairs(reinterpret_cast<float4*>(sm + pairs_offset(J.nc, J.nm)), J.core4, J.nc);
         }
     }
     __syncthreads();
@@ -1148,8 +1170,9 @@ __global__ void repack_kernel(const float* __restrict__ master, float* __restric
     }
 }
 
-size_t ws_smem_bytes(int nc, int nm) {
-    return (size_t)(TABLES + 4 * nc + 2 * nm) * sizeof(float);
+size_t ws_smem_bytes(int nc, int nm, bool pairs) {
+    return pairs ? (size_t)(pairs_offset(nc, nm) + 8 * ((nc + 1) / 2)) * sizeof(float)
+                 : (size_t)(TABLES + 4 * nc + 2 * nm) * sizeof(float);
 }
 
 Stats stats_of(const Ctx& cx) {
@@ -1164,7 +1187,9 @@ Stats stats_of(const Ctx& cx) {
 template <int MODE>
 cudaError_t launch_ws(Ctx& cx, const Job& J) {
     constexpr bool PIPE = MODE != MODE_PRED;
-    const size_t smem = ws_smem_bytes(PIPE ? J.nc : 0, PIPE ? J.nm : 0);
+    Job Jl = J;
+    Jl.pairs = PIPE && ws_smem_bytes(J.nc, J.nm, true) <= 227 * 1024;
+    const size_t smem = ws_smem_bytes(PIPE ? J.nc : 0, PIPE ? J.nm : 0, Jl.pairs);
     if (smem > 227 * 1024) return cudaErrorInvalidValue;
     static bool attr = false;
     if (!attr) {
@@ -1176,14 +1201,14 @@ cudaError_t launch_ws(Ctx& cx, const Job& J) {
     }
     const int64_t tiles = (J.n + TM - 1) / TM;
     const int grid = (int)(tiles < cx.num_sms ? tiles : cx.num_sms);
-    ws_kernel<MODE><<<grid, kThreads, smem, cx.stream>>>(cx.model.wt, stats_of(cx), J);
+    ws_kernel<MODE><<<grid, kThreads, smem, cx.stream>>>(cx.model.wt, stats_of(cx), Jl);
     ++cx.launches;
     return cudaGetLastError();
 }
 
 }  // namespace
 
-size_t mlp_smem_bytes() { return ws_smem_bytes(0, 0); }
+size_t mlp_smem_bytes() { return ws_smem_bytes(0, 0, false); }
 
 #ifdef DSO_PHASE_TIMING
 extern "C" int32_t dso_debug_phase_cycles(unsigned long long* out, int reset) {

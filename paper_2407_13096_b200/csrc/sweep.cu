@@ -49,10 +49,12 @@ __global__ void __launch_bounds__(kBlock) sweep_f32_kernel(
     int32_t* __restrict__ idx, float* __restrict__ cost, float* __restrict__ energy,
     float* __restrict__ time, int32_t* __restrict__ kstatus, bool fast) {
     __shared__ float4 s_core[kMaxCore];
+    __shared__ float4 s_pair[kMaxCore + 2];
     __shared__ float2 s_mem[kMaxMem];
     const int nm = NM > 0 ? NM : nm_rt;
     for (int i = threadIdx.x; i < nc; i += blockDim.x) s_core[i] = core4[i];
     for (int j = threadIdx.x; j < nm; j += blockDim.x) s_mem[j] = mem2[j];
+    build_pairs(s_pair, core4, nc);
     __syncthreads();
 
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -73,7 +75,7 @@ __global__ void __launch_bounds__(kBlock) sweep_f32_kernel(
             if (kstatus) kstatus[k] = kInvalidArgument;
             continue;
         }
-        const Best b = sweep_best<NM>(p, s_core, s_mem, nm, 0, nc, eta, K, fast);
+        const Best b = sweep_best<NM>(p, s_core, s_mem, nm, 0, nc, eta, K, fast, s_pair);
         idx[k] = b.i;
         if (cost) cost[k] = b.c;
         if (energy) energy[k] = b.e;
@@ -263,9 +265,11 @@ __global__ void __launch_bounds__(128) eta_sweep_fast_kernel(
     constexpr int GL = FastGroup<NM>::GL;
     constexpr int GH = GL * NM / 2;
     __shared__ float4 s_core[kMaxCore];
+    __shared__ float4 s_pair[kMaxCore + 2];
     __shared__ float2 s_mem[NM];
     for (int i = threadIdx.x; i < nc; i += blockDim.x) s_core[i] = core4[i];
     if (threadIdx.x < NM) s_mem[threadIdx.x] = mem2[threadIdx.x];
+    build_pairs(s_pair, core4, nc);
     __syncthreads();
     const int e0 = blockIdx.y * CH;
     float ev[CH], Kv[CH];
@@ -312,7 +316,10 @@ __global__ void __launch_bounds__(128) eta_sweep_fast_kernel(
             }
             auto group = [&](int i, auto tail) {
                 float pc[GL], tb[GL];
-                group_levels<NM, decltype(tail)::value>(p, s_core, i, nc, pc, tb);
+                if constexpr (decltype(tail)::value)
+                    group_levels<NM, true>(p, s_core, i, nc, pc, tb);
+                else
+                    group_levels_paired<NM>(p, s_pair, i, pc, tb);  // groups start at even i
                 float2 P2[GH], T2[GH];
                 group_pt<NM>(pc, tb, Ta1, G, P2, T2);
 #pragma unroll

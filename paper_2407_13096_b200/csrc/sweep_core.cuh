@@ -246,6 +246,40 @@ __device__ __forceinline__ void group_levels(const KParams& p, const float4* __r
     }
 }
 
+// Level terms from the level-pair table (group start i even): s_pair[2q] =
+// {vc, vc', vc^2 fc, vc'^2 fc'}, s_pair[2q+1] = {1/fc, 1/fc', -, -} of levels
+// 2q, 2q+1, so two levels' Pc take one FFMA2 pair — lane for lane the same
+// roundings as group_levels.
+template <int NM>
+__device__ __forceinline__ void group_levels_paired(const KParams& p,
+                                                    const float4* __restrict__ s_pair, int i,
+                                                    float* pc, float* tb) {
+#pragma unroll
+    for (int l2 = 0; l2 < FastGroup<NM>::GL / 2; ++l2) {
+        const int q = (i >> 1) + l2;
+        const float4 v = s_pair[2 * q], r = s_pair[2 * q + 1];
+        const float2 pc2 = ffma2(make_float2(p.c, p.c), make_float2(v.z, v.w),
+                                 ffma2(make_float2(p.kp, p.kp), make_float2(v.x, v.y),
+                                       make_float2(p.p0, p.p0)));
+        pc[2 * l2] = pc2.x;
+        pc[2 * l2 + 1] = pc2.y;
+        // scalar: ptxas fuses mul.rn.f32x2 + add.rn.f32x2 into FFMA2 (.rn is
+        // mandatory on f32x2, so it does not mark the pair non-contractable)
+        tb[2 * l2] = __fadd_rn(p.t0, __fmul_rn(p.b, r.x));
+        tb[2 * l2 + 1] = __fadd_rn(p.t0, __fmul_rn(p.b, r.y));
+    }
+}
+
+// Builds the level-pair table for nc levels (threads of a block cooperate).
+__device__ __forceinline__ void build_pairs(float4* s_pair, const float4* __restrict__ core4,
+                                            int nc) {
+    for (int q = threadIdx.x; q < (nc + 1) / 2; q += blockDim.x) {
+        const float4 a = core4[2 * q], b = core4[min(2 * q + 1, nc - 1)];
+        s_pair[2 * q] = make_float4(a.x, b.x, a.y, b.y);
+        s_pair[2 * q + 1] = make_float4(a.z, b.z, 0.f, 0.f);
+    }
+}
+
 // P and T of the group's GP = GL*NM pairs, in visit order, two per packed op.
 template <int NM>
 __device__ __forceinline__ void group_pt(const float* pc, const float* tb, const float* Ta1,
@@ -281,13 +315,17 @@ __device__ __forceinline__ float group_min_cost(const float2* P2, const float2* 
     }
 }
 
-template <int NM, bool TAIL>
+template <int NM, bool TAIL, bool PAIRED = false>
 __device__ __forceinline__ float group_min(const KParams& p, const float4* __restrict__ s_core,
                                            const float* Ta1, const float* G, int i, int i_end,
-                                           float eta, float K) {
+                                           float eta, float K,
+                                           const float4* __restrict__ s_pair = nullptr) {
     constexpr int GL = FastGroup<NM>::GL;
     float pc[GL], tb[GL];
-    group_levels<NM, TAIL>(p, s_core, i, i_end, pc, tb);
+    if constexpr (PAIRED)
+        group_levels_paired<NM>(p, s_pair, i, pc, tb);
+    else
+        group_levels<NM, TAIL>(p, s_core, i, i_end, pc, tb);
     float2 P2[GL * NM / 2], T2[GL * NM / 2];
     group_pt<NM>(pc, tb, Ta1, G, P2, T2);
     return group_min_cost<NM>(P2, T2, eta, K);
@@ -298,7 +336,8 @@ __device__ __forceinline__ float group_min(const KParams& p, const float4* __res
 template <int NM, int UNR = 4>
 __device__ __forceinline__ Best sweep_best(const KParams& p, const float4* __restrict__ s_core,
                                            const float2* __restrict__ s_mem, int nm_rt, int i_lo,
-                                           int i_hi, float eta, float K, bool fast) {
+                                           int i_hi, float eta, float K, bool fast,
+                                           const float4* __restrict__ s_pair = nullptr) {
     int lo = i_lo, hi = i_hi;
     if constexpr (NM >= 1 && NM <= 4) {
         constexpr int GL = FastGroup<NM>::GL;
@@ -315,6 +354,22 @@ __device__ __forceinline__ Best sweep_best(const KParams& p, const float4* __res
             int i = i_lo;
             // UNR independent groups per step: their loads and min trees overlap
             // (a single group is a ~80-cycle dependency chain); folded in order
+            if (s_pair && !(i_lo & 1)) {  // groups start on even levels: paired level terms
+#pragma unroll 1
+                for (; i + UNR * GL <= i_hi; i += UNR * GL) {
+                    float m[UNR];
+#pragma unroll
+                    for (int u = 0; u < UNR; ++u)
+                        m[u] = group_min<NM, false, true>(p, s_core, Ta1, G, i + u * GL, i_hi, eta,
+                                                          K, s_pair);
+#pragma unroll
+                    for (int u = 0; u < UNR; ++u) {
+                        tie |= (m[u] == bc);
+                        bg = m[u] < bc ? i + u * GL : bg;
+                        bc = fminf(m[u], bc);
+                    }
+                }
+            }
 #pragma unroll 1
             for (; i + UNR * GL <= i_hi; i += UNR * GL) {
                 float m[UNR];
