@@ -113,7 +113,9 @@ class Context:
         self._raise(self._lib.dso_sync(self._h))
 
     def set_option(self, key: str, value: int) -> None:
-        """dso_set_option: verification/tuning switches (e.g. "fast_sweep")."""
+        """dso_set_option: verification/tuning switches: "fast_sweep" (0/1, exact
+        group-minimum sweep), "mlp_engine" (0 = FMA-pipe predictor kernel, the
+        default; 1 = tcgen05 3xTF32 kernel for predict and the fused pipelines)."""
         self._raise(self._lib.dso_set_option(self._h, key.encode(), int(value)))
 
     @property

@@ -188,6 +188,7 @@ int32_t dso_ctx_destroy(dso_ctx* ctx) {
     cudaFree(c.flag_dev);
     fit_plan_free(c);
     cudaFree(c.model.wt);
+    cudaFree(c.model.wtc);
     cudaFree(c.model.w_master);
     cudaFree(c.model.w_train);
     cudaFree(c.scratch);
@@ -244,6 +245,11 @@ int64_t dso_launch_count(const dso_ctx* ctx) { return ctx ? ctx->c.launches : 0;
 
 int32_t dso_set_option(dso_ctx* ctx, const char* key, int64_t value) {
     if (!ctx || !key) return kInvalidArgument;
+    if (std::string(key) == "mlp_engine") {
+        if (value != 0 && value != 1) return fail(ctx, kInvalidArgument, "mlp_engine is 0 or 1");
+        ctx->c.mlp_engine = value != 0;
+        return 0;
+    }
     if (std::string(key) == "fast_sweep") {
         ctx->c.fast_sweep = value != 0;
         return kOk;

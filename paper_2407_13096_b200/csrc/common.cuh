@@ -69,6 +69,11 @@ struct ModelDev {
     // from w_master before the next gradient after any change of w_master
     float* w_train;
     bool train_dirty;
+    // the tensor-core engine's packed model (mlp_tc.cuh): weights split hi/lo
+    // for 3xTF32; tc_state 1 = finite (host-checked), 0 = non-finite, -1 =
+    // repacked on the device (the kernels read the flag)
+    float* wtc;
+    int tc_state;
     int64_t n_weights, n_biases;
 };
 
@@ -92,6 +97,7 @@ struct Ctx {
     cudaEvent_t ev[8] = {};
     int num_sms = 148;
     bool fast_sweep = true;         // dso_set_option("fast_sweep")
+    bool mlp_engine = false;        // dso_set_option("mlp_engine"): 0 FMA pipe, 1 tensor cores
     float2* eta_dev = nullptr;      // dso_eta_sweep's (eta, K) table
     int eta_cap = 0;
     int* flag_dev = nullptr;        // dso_dcgm_mean's out-of-range flag

@@ -37,6 +37,7 @@
 
 #include "common.cuh"
 #include "sweep_core.cuh"
+#include "tc.cuh"
 
 namespace dso_b200 {
 
@@ -145,7 +146,7 @@ __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b
 
 // Optional per-phase cycle accounting (debug builds only: -DDSO_PHASE_TIMING).
 #ifdef DSO_PHASE_TIMING
-__device__ unsigned long long g_phase_cycles[16];
+__device__ unsigned long long g_phase_cycles[32];
 #define PT_BEGIN(v) long long v = clock64()
 #define PT_END(ph, v)                                                                  \
     do {                                                                              \
@@ -607,6 +608,7 @@ struct Job {
     float eta, K;
     bool fast;   // fast exact sweep allowed (fast_sweep_ok)
     bool pairs;  // level-pair table staged after the level tables (pairs_offset)
+    const int* gate;  // ws_kernel runs only if *gate != 0 (the tc engine's non-finite flag)
     // outputs
     float* params;
     uint8_t* clamped;
@@ -854,15 +856,11 @@ __device__ __forceinline__ void csr_features(float* act, float* scr, const Job& 
 
 template <int UNR>
 __device__ __forceinline__ Best sweep_dispatch(const KParams& p, const float4* s_core,
-                                               const float2* s_mem, const Job& J, int i_lo,
-                                               int i_hi) {
+                                               const float2* s_mem, const float4* s_pair,
+                                               const Job& J, int i_lo, int i_hi) {
     Best b{__int_as_float(0x7fc00000), __int_as_float(0x7fc00000), -1};  // i = -1: empty part
     if (i_lo >= i_hi) return b;
     const int nm = J.nm;
-    const float4* s_pair =
-        J.pairs ? reinterpret_cast<const float4*>(reinterpret_cast<const float*>(s_core) -
-                                                  TABLES + pairs_offset(J.nc, nm))
-                : nullptr;
     if (nm == 4)
         return sweep_best<4, UNR>(p, s_core, s_mem, 4, i_lo, i_hi, J.eta, J.K, J.fast, s_pair);
     if (nm == 1)
@@ -940,7 +938,9 @@ __device__ __forceinline__ void consumer_sweep(const float* sm, const float* out
     const KParams p{pr[0], pr[1], pr[2], pr[3], pr[4], pr[5], pr[6]};
     const float4* s_core = reinterpret_cast<const float4*>(sm + TABLES);
     const float2* s_mem = reinterpret_cast<const float2*>(sm + TABLES + 4 * J.nc);
-    const Best b = sweep_dispatch<4>(p, s_core, s_mem, J, part_lo(J.nc, part, P),
+    const float4* s_pair =
+        J.pairs ? reinterpret_cast<const float4*>(sm + pairs_offset(J.nc, J.nm)) : nullptr;
+    const Best b = sweep_dispatch<4>(p, s_core, s_mem, s_pair, J, part_lo(J.nc, part, P),
                                      part_lo(J.nc, part + 1, P));
     cs[part * KC + m] = b.c;
     cs[P * KC + part * KC + m] = b.e;
@@ -990,7 +990,10 @@ __device__ __forceinline__ void produce_results(const float* sm, const float* ou
     const KParams p{pr[0], pr[1], pr[2], pr[3], pr[4], pr[5], pr[6]};
     const float4* s_core = reinterpret_cast<const float4*>(sm + TABLES);
     const float2* s_mem = reinterpret_cast<const float2*>(sm + TABLES + 4 * J.nc);
-    const Best b = sweep_dispatch<DSO_PRODUCER_UNROLL>(p, s_core, s_mem, J, part_lo(J.nc, part, P),
+    const float4* s_pair =
+        J.pairs ? reinterpret_cast<const float4*>(sm + pairs_offset(J.nc, J.nm)) : nullptr;
+    const Best b = sweep_dispatch<DSO_PRODUCER_UNROLL>(p, s_core, s_mem, s_pair, J,
+                                                       part_lo(J.nc, part, P),
                                                        part_lo(J.nc, part + 1, P));
     float* xc = const_cast<float*>(sm) + SCR;  // [P][NK] cost, energy, index
     xc[part * NK + mm] = b.c;
@@ -1004,11 +1007,14 @@ __device__ __forceinline__ void produce_results(const float* sm, const float* ou
     }
 }
 
+#include "mlp_tc.cuh"
+
 template <int MODE>
 __global__ void __launch_bounds__(kThreads, 1)
     ws_kernel(const float* __restrict__ packed, Stats stats, Job J) {
     constexpr bool PIPE = MODE != MODE_PRED;
     extern __shared__ __align__(16) float sm[];
+    if (J.gate && *J.gate == 0) return;  // the tensor-core engine took this launch
     // ---- stage model, stats, tables (all threads) -----------------------------
     {
         const float4* src = reinterpret_cast<const float4*>(packed);
@@ -1184,9 +1190,47 @@ Stats stats_of(const Ctx& cx) {
     return s;
 }
 
+// Tensor-core engine (mlp_tc.cuh) for predict and CSR-pipeline launches when
+// enabled (dso_set_option "mlp_engine"), the tables fit and the model is known
+// finite on the host; after a device-side repack (training) finiteness lives
+// in a device flag, so both engines are launched and each exits on the flag.
 template <int MODE>
-cudaError_t launch_ws(Ctx& cx, const Job& J) {
+cudaError_t launch_tc(Ctx& cx, const Job& J) {
     constexpr bool PIPE = MODE != MODE_PRED;
+    Job Jl = J;
+    Jl.pairs = PIPE && tce::tc_smem_bytes(J.nc, J.nm, true) <= 227 * 1024;
+    const size_t smem = tce::tc_smem_bytes(PIPE ? J.nc : 0, PIPE ? J.nm : 0, Jl.pairs);
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(tce::tc_kernel<MODE>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             227 * 1024);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    const int64_t tiles = (J.n + tce::TT - 1) / tce::TT;
+    const int grid = (int)(tiles < cx.num_sms ? tiles : cx.num_sms);
+    tce::tc_kernel<MODE><<<grid, tce::kThreadsTC, smem, cx.stream>>>(cx.model.wtc, stats_of(cx), Jl);
+    ++cx.launches;
+    return cudaGetLastError();
+}
+
+template <int MODE>
+bool tc_eligible(const Ctx& cx, const Job& J) {
+    if (!cx.mlp_engine || !cx.model.wtc || cx.model.tc_state == 0) return false;
+    if (MODE == MODE_PRED) return true;
+    return tce::tc_smem_bytes(J.nc, J.nm, false) <= 227 * 1024;
+}
+
+template <int MODE>
+cudaError_t launch_ws(Ctx& cx, const Job& J0) {
+    constexpr bool PIPE = MODE != MODE_PRED;
+    Job J = J0;
+    if (tc_eligible<MODE>(cx, J)) {
+        cudaError_t e = launch_tc<MODE>(cx, J);
+        if (e != cudaSuccess || cx.model.tc_state == 1) return e;
+        J.gate = reinterpret_cast<const int*>(cx.model.wtc) + tce::FLAG;  // unknown: gated fallback
+    }
     Job Jl = J;
     Jl.pairs = PIPE && ws_smem_bytes(J.nc, J.nm, true) <= 227 * 1024;
     const size_t smem = ws_smem_bytes(PIPE ? J.nc : 0, PIPE ? J.nm : 0, Jl.pairs);
@@ -1213,9 +1257,9 @@ size_t mlp_smem_bytes() { return ws_smem_bytes(0, 0, false); }
 #ifdef DSO_PHASE_TIMING
 extern "C" int32_t dso_debug_phase_cycles(unsigned long long* out, int reset) {
     cudaDeviceSynchronize();
-    cudaMemcpyFromSymbol(out, g_phase_cycles, sizeof(unsigned long long) * 16);
+    cudaMemcpyFromSymbol(out, g_phase_cycles, sizeof(unsigned long long) * 32);
     if (reset) {
-        unsigned long long z[16] = {};
+        unsigned long long z[32] = {};
         cudaMemcpyToSymbol(g_phase_cycles, z, sizeof z);
     }
     return 0;
@@ -1250,8 +1294,46 @@ cudaError_t model_upload(Ctx& cx, const double* W, const double* b) {
         if (e != cudaSuccess) return e;
     }
     md.wt_floats = kModelFloats;
-    return cudaMemcpyAsync(md.wt, pk.data(), sizeof(float) * kModelFloats,
-                           cudaMemcpyHostToDevice, cx.stream);
+    cudaError_t e = cudaMemcpyAsync(md.wt, pk.data(), sizeof(float) * kModelFloats,
+                                    cudaMemcpyHostToDevice, cx.stream);
+    if (e != cudaSuccess) return e;
+    // tensor-core model: hi = rna_tf32(w) (cvt.rna.tf32.f32 on the host), lo = w - hi
+    std::vector<float> tp(tce::kModel, 0.f);
+    int bad = 0;
+    auto tf32 = [](float w) {
+        uint32_t u;
+        memcpy(&u, &w, 4);
+        if ((u & 0x7F800000u) != 0x7F800000u) u = (u + 0x1000u) & 0xFFFFE000u;
+        float h;
+        memcpy(&h, &u, 4);
+        return h;
+    };
+    auto put = [&](int hi, int lo, int n, int k, int K, double wd) {
+        const float w = (float)wd, h = tf32(w);
+        tp[hi + tce::cm(n, k, K)] = h;
+        tp[lo + tce::cm(n, k, K)] = std::isfinite(w) ? w - h : 0.f;
+        bad += std::isfinite(w) ? 0 : 1;
+    };
+    for (int n = 0; n < 100; ++n)
+        for (int k = 0; k < 134; ++k) put(tce::W1H, tce::W1L, n, k, tce::K1, W[MW1 + n * 134 + k]);
+    for (int n = 0; n < 50; ++n)
+        for (int k = 0; k < 100; ++k) put(tce::W2H, tce::W2L, n, k, tce::K2, W[MW2 + n * 100 + k]);
+    for (int n = 0; n < 25; ++n)
+        for (int k = 0; k < 50; ++k) put(tce::W3H, tce::W3L, n, k, tce::K3, W[MW3 + n * 50 + k]);
+    for (int n = 0; n < 7; ++n)
+        for (int k = 0; k < 25; ++k) put(tce::W4H, tce::W4L, n, k, tce::K4, W[MW4 + n * 25 + k]);
+    for (int i = 0; i < 100; ++i) tp[tce::NB1 + i] = (float)b[i] * tce::kNL2E;
+    for (int i = 0; i < 50; ++i) tp[tce::NB2 + i] = (float)b[100 + i] * tce::kNL2E;
+    for (int i = 0; i < 25; ++i) tp[tce::NB3 + i] = (float)b[150 + i] * tce::kNL2E;
+    for (int i = 0; i < 7; ++i) tp[tce::B4 + i] = (float)b[175 + i];
+    memcpy(&tp[tce::FLAG], &bad, sizeof(int));
+    if (!md.wtc) {
+        e = cudaMalloc(&md.wtc, sizeof(float) * tce::kModel);
+        if (e != cudaSuccess) return e;
+    }
+    md.tc_state = bad ? 0 : 1;
+    return cudaMemcpyAsync(md.wtc, tp.data(), sizeof(float) * tce::kModel, cudaMemcpyHostToDevice,
+                           cx.stream);
 }
 
 cudaError_t launch_repack(Ctx& cx) {
@@ -1260,6 +1342,14 @@ cudaError_t launch_repack(Ctx& cx) {
     repack_kernel<<<(kMasterFloats + 255) / 256, 256, 0, cx.stream>>>(cx.model.w_master,
                                                                       cx.model.wt);
     ++cx.launches;
+    if (cx.model.wtc) {
+        e = cudaMemsetAsync(cx.model.wtc + tce::FLAG, 0, sizeof(int), cx.stream);
+        if (e != cudaSuccess) return e;
+        tce::tc_repack_kernel<<<(kMasterFloats + 255) / 256, 256, 0, cx.stream>>>(
+            cx.model.w_master, cx.model.wtc);
+        ++cx.launches;
+        cx.model.tc_state = -1;
+    }
     return cudaGetLastError();
 }
 

@@ -1,0 +1,843 @@
+// mlp_tc.cuh — the predictor on the 5th-generation tensor cores (tcgen05),
+// fused with the feature stage and the grid sweep.  Included by mlp.cu inside
+// its anonymous namespace (shares Job, Stats, the sweep and output helpers).
+//
+// Precision: every layer is a 3xTF32 product, D = Ah.Bh + Ah.Bl + Al.Bh with
+// Xh = rna_tf32(X), Xl = X - Xh for activations and weights alike (~22
+// mantissa bits per product, FP32 accumulation in TMEM), which keeps the
+// predicted parameters inside the 1e-5 relative contract (
+// tests/test_gpu_tc.py, test_gpu_mlp.py run both engines).
+//
+// Execution model — one persistent CTA per SM, 13 warps, tiles of 128 kernels
+// (the MMA M: TMEM lane m = kernel m of the tile), two tiles in flight:
+//   * warps 0..3, PRODUCERS (thread = kernel): the feature stage of each tile
+//     (CSR entries / dense counts -> per-category fractions, or fused input),
+//     split hi/lo and written 8 columns at a time into a 3-deep ring of
+//     shared-memory chunks in the UMMA core-matrix layout — the L1 A operand.
+//     CSR tiles skip the 8-column chunks no kernel of the tile touches (their
+//     products are exact zeros);
+//   * warp 12, lane 0: the MMA ISSUER.  L1 (N 112 x K 136) reads A from the
+//     ring (SS), L2 (64 x 104), L3 (32 x 56), L4 (16 x 32) read A from TMEM
+//     (TS); each k-step is three kind::tf32 MMAs and waits only for its own
+//     8-column chunk, so a layer runs while the previous epilogue still
+//     produces later chunks.  Order: L1(t+1), then L2..L4(t);
+//   * warps 4..7 / 8..11, two EPILOGUE GROUPS taking alternate tiles, each
+//     with its own TMEM slot: tcgen05.ld -> bias + sigmoid -> split ->
+//     tcgen05.st as the next layer's A operand (in place over the consumed
+//     accumulator), then the grid sweep of the tile (thread = kernel) — one
+//     group's epilogue overlaps the other's sweep and the next tile's L1.
+// TMEM (512 columns): slot g at 216 g: [0,112) D1 -> A2 hi (in place),
+// [112,216) A2 lo; after L2: [0,56) A3 hi, [56,112) A3 lo, [112,144) D3 -> A4
+// hi, [144,160) D4, [160,192) A4 lo.  [432,496) D2 (shared, guarded by
+// D2FREE), [496 + 8 g, +8) predictions computed on the FMA pipe.
+//
+// Non-finite inputs (a DCGM value, or any predict-mode feature): the producer
+// computes that kernel's prediction on the FMA pipe (tc_forward_x, IEEE
+// semantics like the reference) into the slot's spare TMEM columns and flags
+// the row; a split inf - inf would otherwise turn inf * W into NaN.
+// Non-finite weights never reach this engine (the host or a device flag routes
+// such models to the FFMA engine, ws_kernel).
+
+namespace tce {
+
+constexpr int TT = 128;                            // kernels per tile
+constexpr int kGroupT = 128;                       // threads of a role group (4 warps)
+constexpr int kThreadsTC = 4 * kGroupT;  // producers, 2 epilogue groups, MMA warp (+3 idle)
+constexpr int MMA_WARP = 12;
+// Registers (setmaxnreg): launched at 128 per thread; warpgroup 3 (the MMA warp
+// and three idle warps) releases down to 56, producers grow to 168 and the
+// epilogue groups to 144 (128*168 + 256*144 + 128*56 = 64K).
+constexpr int kRegProd = 168, kRegEpi = 144, kRegMma = 56;
+static_assert(128 * kRegProd + 256 * kRegEpi + 128 * kRegMma <= 65536, "RF budget");
+constexpr int N1 = 112, K1 = 136, N2 = 64, K2 = 104, N3 = 32, K3 = 56, N4 = 16, K4 = 32;
+constexpr int H1 = 100, H2 = 50, H3 = 25, H4 = 7;
+// packed model (floats): weights hi/lo in the SWIZZLE_NONE K-major core-matrix
+// layout (tc.cuh), -b*log2(e) for the hidden layers, b4, the non-finite count
+constexpr int W1H = 0, W1L = W1H + N1 * K1, W2H = W1L + N1 * K1, W2L = W2H + N2 * K2;
+constexpr int W3H = W2L + N2 * K2, W3L = W3H + N3 * K3, W4H = W3L + N3 * K3, W4L = W4H + N4 * K4;
+constexpr int NB1 = W4L + N4 * K4, NB2 = NB1 + N1, NB3 = NB2 + N2, B4 = NB3 + N3;
+constexpr int FLAG = B4 + N4;
+constexpr int kModel = FLAG + 4;
+__host__ __device__ __forceinline__ int cm(int n, int k, int K) {
+    return ((n >> 3) * (K >> 2) + (k >> 2)) * 32 + (n & 7) * 4 + (k & 3);
+}
+// shared memory (floats)
+constexpr int kRing = 3;                     // X chunk buffers
+constexpr int kChunkF = 2 * TT * 8;          // hi [128][8] + lo [128][8] (core-matrix layout)
+constexpr int S_STATS = kModel;              // mean[8] std[8]
+constexpr int S_RING = S_STATS + 16;
+constexpr int S_MISC = S_RING + kRing * kChunkF;  // u32: [0..1] chunk masks, [2..9] slow rows, [10..17] partial masks
+constexpr int S_MBAR = S_MISC + 24;
+enum {
+    MB_XFULL = 0, MB_XEMPTY = 3, MB_D1F = 6, MB_A2R = 8, MB_D2F = 34, MB_D2FREE = 36,
+    MB_A3R = 37, MB_D3F = 51, MB_A4R = 53, MB_D4F = 61, MB_SLOWFREE = 63, kMbars = 65
+};
+constexpr int S_TSLOT = S_MBAR + 2 * kMbars;
+constexpr int S_TABLES = (S_TSLOT + 4 + 3) & ~3;  // core4[nc], mem2[nm], level pairs
+static_assert(kModel % 4 == 0 && S_RING % 4 == 0 && S_MBAR % 2 == 0, "tc smem alignment");
+__host__ __device__ __forceinline__ int tc_pairs_offset(int nc, int nm) {
+    return (S_TABLES + 4 * nc + 2 * nm + 3) & ~3;
+}
+// TMEM columns
+constexpr int SLOT_COLS = 216, TD2 = 432, TSLOW = 496;
+constexpr int A2LO = 112, A3LO = 56, TD3 = 112, TD4 = 144, A4LO = 160;
+constexpr float kNL2E = -1.4426950408889634f;
+
+// phase accounting (debug library only): producer 0, epilogue thread 128, MMA thread
+#ifdef DSO_PHASE_TIMING
+#define TPT_BEGIN(v) long long v = clock64()
+#define TPT_END(ph, v)                                                              \
+    do {                                                                            \
+        if (threadIdx.x == 0 || threadIdx.x == kGroupT || threadIdx.x == 3 * kGroupT) \
+            atomicAdd(&g_phase_cycles[ph], clock64() - (v));                        \
+    } while (0)
+#else
+#define TPT_BEGIN(v) (void)0
+#define TPT_END(ph, v) (void)0
+#endif
+
+__device__ __forceinline__ void mb_init(uint64_t* b, int count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mb_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+// The warp's tcgen05 traffic is complete and ordered before one arrival on b.
+__device__ __forceinline__ void warp_signal(uint64_t* b) {
+    tc::wait_st();
+    tc::fence_before();
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) mb_arrive(b);
+}
+__device__ __forceinline__ bool mbar_test(uint64_t* b, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{ .reg .pred p; mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(ok)
+        : "r"(smem_u32(b)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void wait_acq(uint64_t* b, uint32_t ph) {
+    mbar_wait(b, ph);
+    tc::fence_after();
+}
+
+// hi/lo split of 8 values into two TMEM chunks
+__device__ __forceinline__ void store_split(uint32_t a_hi, uint32_t a_lo, const float (&v)[8]) {
+    float h[8], l[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        h[j] = tc::tf32_hi(v[j]);
+        l[j] = v[j] - h[j];
+    }
+    tc::st8(a_hi, h);
+    tc::st8(a_lo, l);
+}
+
+// Hidden-layer epilogue of one 8-neuron chunk: sigmoid(acc + b) (neurons >=
+// NREAL are padding: 0), split, stored as the next layer's A operand.
+template <int NREAL>
+__device__ __forceinline__ void epi_chunk(uint32_t src, uint32_t dst_hi, uint32_t dst_lo, int c,
+                                          const float* __restrict__ nb, uint64_t* ready) {
+    float v[8];
+    tc::ld8(src, v);
+    tc::wait_ld();
+    float a[8];
+#pragma unroll
+    for (int j = 0; j < 8; j += 2) {
+        const float2 z = ffma2(make_float2(v[j], v[j + 1]), make_float2(kNL2E, kNL2E),
+                               make_float2(nb[8 * c + j], nb[8 * c + j + 1]));
+        float e0, e1, r0, r1;
+        asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e0) : "f"(z.x));
+        asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e1) : "f"(z.y));
+        const float2 d = fadd2(make_float2(1.f, 1.f), make_float2(e0, e1));
+        asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r0) : "f"(d.x));
+        asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r1) : "f"(d.y));
+        a[j] = 8 * c + j < NREAL ? r0 : 0.f;
+        a[j + 1] = 8 * c + j + 1 < NREAL ? r1 : 0.f;
+    }
+    store_split(dst_hi, dst_lo, a);
+    warp_signal(ready);
+}
+
+// FP32 forward of one kernel's features on the FMA pipe: W = Wh + Wl exactly,
+// sequential sums, the same sigmoid as the epilogues.
+__device__ __noinline__ void tc_forward_x(const float* sm, const float* x, float* raw) {
+    float h1[H1], h2[H2], h3[H3];
+    auto w = [&](int hi, int lo, int n, int kk, int K) {
+        return sm[hi + cm(n, kk, K)] + sm[lo + cm(n, kk, K)];
+    };
+    auto sig = [&](float acc, float nbv) {
+        float e, r;
+        asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(fmaf(acc, kNL2E, nbv)));
+        asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(1.f + e));
+        return r;
+    };
+    for (int n = 0; n < H1; ++n) {
+        float z = 0.f;
+        for (int c = 0; c < DSO_FUSED_ROWS; ++c) z = fmaf(w(W1H, W1L, n, c, K1), x[c], z);
+        h1[n] = sig(z, sm[NB1 + n]);
+    }
+    for (int n = 0; n < H2; ++n) {
+        float z = 0.f;
+        for (int c = 0; c < H1; ++c) z = fmaf(w(W2H, W2L, n, c, K2), h1[c], z);
+        h2[n] = sig(z, sm[NB2 + n]);
+    }
+    for (int n = 0; n < H3; ++n) {
+        float z = 0.f;
+        for (int c = 0; c < H2; ++c) z = fmaf(w(W3H, W3L, n, c, K3), h2[c], z);
+        h3[n] = sig(z, sm[NB3 + n]);
+    }
+    for (int n = 0; n < H4; ++n) {
+        float z = 0.f;
+        for (int c = 0; c < H3; ++c) z = fmaf(w(W4H, W4L, n, c, K4), h3[c], z);
+        raw[n] = fmaf(z + sm[B4 + n], sm[S_STATS + 8 + n], sm[S_STATS + n]);
+    }
+}
+
+// CSR row of one kernel (thread = kernel): extent and DCGM prefetched a tile
+// ahead in registers, the entries pulled into L1 ahead and re-read from L1 per
+// chunk (keeping 24 entries live in registers would spill).
+constexpr int kEnt = 24;
+struct Entries {
+    uint64_t first;
+    int cnt;
+    float dg[8];
+};
+
+__device__ __forceinline__ void tc_csr_prefetch(const Job& J, int64_t k, Entries& E) {
+    E.cnt = 0;
+    E.first = 0;
+    if (k < J.n) {
+        const uint64_t a = __ldg(J.row_ptr + k), b = __ldg(J.row_ptr + k + 1);
+        E.first = a - J.ent_base;
+        E.cnt = (int)(b - a);
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) E.dg[j] = k < J.n ? __ldg(J.dcgm + (int64_t)j * J.ld + k) : 0.f;
+}
+
+// The first kEnt entries of a row (0 beyond cnt): 16-byte loads when aligned.
+__device__ __forceinline__ void load_entries(const uint32_t* __restrict__ p, int cnt,
+                                             uint32_t (&en)[kEnt]) {
+    if ((reinterpret_cast<uintptr_t>(p) & 15) == 0 && cnt >= kEnt) {
+#pragma unroll
+        for (int v = 0; v < kEnt / 4; ++v) {
+            const uint4 x = __ldg(reinterpret_cast<const uint4*>(p) + v);
+            en[4 * v] = x.x;
+            en[4 * v + 1] = x.y;
+            en[4 * v + 2] = x.z;
+            en[4 * v + 3] = x.w;
+        }
+    } else {
+#pragma unroll
+        for (int e = 0; e < kEnt; ++e) en[e] = e < cnt ? __ldg(p + e) : 0u;
+    }
+}
+
+// exact per-category totals -> (tf, rr) for normalize_count (see csr_features)
+__device__ __forceinline__ void cat_scales(const uint64_t (&tot)[3], float (&tf)[3], float (&rr)[3]) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        tf[c] = 0.f;
+        rr[c] = 0.f;
+        if (tot[c] != 0 && tot[c] < (1u << 24)) {
+            tf[c] = __uint2float_rn((uint32_t)tot[c]);
+            rr[c] = __frcp_rn(tf[c]);
+        } else if (tot[c] != 0) {
+            tf[c] = -(float)(tot[c] >> 24);
+            rr[c] = (float)(tot[c] & 0xFFFFFFu);
+        }
+    }
+}
+__device__ __forceinline__ float norm_slot(uint32_t cnt, int slot, const float (&tf)[3],
+                                           const float (&rr)[3]) {
+    const int cat = cat_of_row(slot);
+    return normalize_count(cnt, cat == 0 ? tf[0] : (cat == 1 ? tf[1] : tf[2]),
+                           cat == 0 ? rr[0] : (cat == 1 ? rr[1] : rr[2]));
+}
+
+// One 8-column chunk of one kernel into a ring buffer (core-matrix layout).
+__device__ __forceinline__ void put_chunk(float* buf, int row, const float (&v)[8]) {
+    float h[8], l[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        h[j] = tc::tf32_hi(v[j]);
+        l[j] = v[j] - h[j];
+    }
+    const int o = (row >> 3) * 64 + (row & 7) * 4;
+    *reinterpret_cast<float4*>(buf + o) = make_float4(h[0], h[1], h[2], h[3]);
+    *reinterpret_cast<float4*>(buf + o + 32) = make_float4(h[4], h[5], h[6], h[7]);
+    *reinterpret_cast<float4*>(buf + TT * 8 + o) = make_float4(l[0], l[1], l[2], l[3]);
+    *reinterpret_cast<float4*>(buf + TT * 8 + o + 32) = make_float4(l[4], l[5], l[6], l[7]);
+}
+
+// The tensor-core pipeline kernel.  MODE_PRED: fused [134][ld] input, outputs
+// raw/params/clamped; MODE_DENSE: [126][ld] counts + DCGM; MODE_CSR: CSR
+// counts + DCGM; the pipeline modes run the fused sweep.
+template <int MODE>
+__global__ void __launch_bounds__(kThreadsTC, 1)
+    tc_kernel(const float* __restrict__ model, Stats stats, Job J) {
+    constexpr bool PIPE = MODE != MODE_PRED;
+    extern __shared__ __align__(16) float sm[];
+    if (reinterpret_cast<const int*>(model)[FLAG] != 0) return;  // non-finite weights: FFMA engine
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    uint64_t* mb = reinterpret_cast<uint64_t*>(sm + S_MBAR);
+    uint32_t* misc = reinterpret_cast<uint32_t*>(sm + S_MISC);
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(sm + S_TSLOT);
+    {
+        const float4* src = reinterpret_cast<const float4*>(model);
+        float4* dst = reinterpret_cast<float4*>(sm);
+        for (int i = tid; i < kModel / 4; i += kThreadsTC) dst[i] = __ldg(src + i);
+        if (tid < 8) {
+            sm[S_STATS + tid] = stats.mean[tid];
+            sm[S_STATS + 8 + tid] = stats.std_[tid];
+        }
+        if (tid < 24) misc[tid] = 0u;
+        if (PIPE) {
+            float4* sc = reinterpret_cast<float4*>(sm + S_TABLES);
+            float2* smm = reinterpret_cast<float2*>(sm + S_TABLES + 4 * J.nc);
+            for (int i = tid; i < J.nc; i += kThreadsTC) sc[i] = J.core4[i];
+            for (int j = tid; j < J.nm; j += kThreadsTC) smm[j] = J.mem2[j];
+            if (J.pairs)
+                build_pairs(reinterpret_cast<float4*>(sm + tc_pairs_offset(J.nc, J.nm)), J.core4,
+                            J.nc);
+        }
+        if (tid == 0) {
+            for (int b = 0; b < kRing; ++b) {
+                mb_init(mb + MB_XFULL + b, 4);
+                mb_init(mb + MB_XEMPTY + b, 1);
+            }
+            for (int g = 0; g < 2; ++g) {
+                mb_init(mb + MB_D1F + g, 1);
+                mb_init(mb + MB_D2F + g, 1);
+                mb_init(mb + MB_D3F + g, 1);
+                mb_init(mb + MB_D4F + g, 1);
+                mb_init(mb + MB_SLOWFREE + g, 4);
+                for (int c = 0; c < 13; ++c) mb_init(mb + MB_A2R + 13 * g + c, 4);
+                for (int c = 0; c < 7; ++c) mb_init(mb + MB_A3R + 7 * g + c, 4);
+                for (int c = 0; c < 4; ++c) mb_init(mb + MB_A4R + 4 * g + c, 4);
+            }
+            mb_init(mb + MB_D2FREE, 4);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        if (warp == MMA_WARP) tc::tmem_alloc<512>(tslot);
+        // weights written through the generic proxy are read by the tensor core
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t tbase = *tslot;
+    const int64_t tiles = (J.n + TT - 1) / TT;
+    const int64_t my_tiles =
+        (int64_t)blockIdx.x < tiles ? (tiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+    auto t0_of = [&](int64_t i) { return (blockIdx.x + i * gridDim.x) * (int64_t)TT; };
+
+    if (warp >= MMA_WARP) {
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegMma));
+    }
+    if (warp == MMA_WARP) {
+        // ================================ MMA issuer ================================
+        if (lane == 0) {
+            const uint32_t id1 = tc::idesc_tf32(128, N1), id2 = tc::idesc_tf32(128, N2),
+                           id3 = tc::idesc_tf32(128, N3), id4 = tc::idesc_tf32(128, N4);
+            const uint32_t s0 = smem_u32(sm);
+            auto bd = [&](int off, int kk, int K) {
+                return tc::sdesc(s0 + off * 4 + kk * 256, 128, (uint32_t)(K >> 2) * 128);
+            };
+            uint32_t g = 0;  // ring chunks consumed
+            // Event-driven issue: L1 of the next tile and L2..L4 of the current one are
+            // independent streams of k-steps; each is issued as soon as its operand
+            // chunk is ready (non-blocking mbarrier tests), in one tensor-core queue.
+            struct L1S {
+                int64_t t;
+                int c;
+                uint32_t mask;
+                bool active;
+            };
+            auto l1_step = [&](L1S& st) -> bool {
+                const int b = (int)(g % kRing);
+                if (!mbar_test(mb + MB_XFULL + b, (g / kRing) & 1u)) return false;
+                tc::fence_after();
+                if (st.c == 0) st.mask = misc[st.t & 1];  // published before the tile's first chunk
+                const uint32_t D = tbase + (uint32_t)((st.t & 1) * SLOT_COLS);
+                const uint32_t xa = s0 + (uint32_t)(S_RING + b * kChunkF) * 4;
+                const uint64_t ah = tc::sdesc(xa, 128, 256), al = tc::sdesc(xa + TT * 8 * 4, 128, 256);
+                tc::mma_tf32_ss(D, ah, bd(W1H, st.c, K1), id1, st.c == 0 ? 0u : 1u);
+                tc::mma_tf32_ss(D, ah, bd(W1L, st.c, K1), id1, 1u);
+                tc::mma_tf32_ss(D, al, bd(W1H, st.c, K1), id1, 1u);
+                tc::commit(mb + MB_XEMPTY + b);
+                ++g;
+                int nc = st.c + 1;
+                while (nc < 17 && !((st.mask >> nc) & 1u)) ++nc;
+                if (nc >= 17) {
+                    tc::commit(mb + MB_D1F + (st.t & 1));
+                    st.active = false;
+                } else {
+                    st.c = nc;
+                }
+                return true;
+            };
+            if (my_tiles > 0) {
+                L1S s0t{0, 0, 0u, true};
+                while (s0t.active) l1_step(s0t);
+            }
+            for (int64_t t = 0; t < my_tiles; ++t) {
+                L1S st{t + 1, 0, 0u, t + 1 < my_tiles};
+                const int sl = (int)(t & 1);
+                const uint32_t S = tbase + (uint32_t)(sl * SLOT_COLS);
+                const uint32_t ph = (uint32_t)((t >> 1) & 1);
+                bool d2ok = t == 0;
+                int c2 = 0, c3 = 0, c4 = 0;
+                TPT_BEGIN(m_it);
+                while (st.active || c4 < 4) {
+                    while (st.active && l1_step(st)) {
+                    }
+                    if (!d2ok && mbar_test(mb + MB_D2FREE, (uint32_t)((t - 1) & 1))) d2ok = true;
+                    while (d2ok && c2 < 13 && mbar_test(mb + MB_A2R + 13 * sl + c2, ph)) {
+                        tc::fence_after();
+                        tc::mma_tf32_ts(tbase + TD2, S + 8 * c2, bd(W2H, c2, K2), id2, c2 > 0 ? 1u : 0u);
+                        tc::mma_tf32_ts(tbase + TD2, S + 8 * c2, bd(W2L, c2, K2), id2, 1u);
+                        tc::mma_tf32_ts(tbase + TD2, S + A2LO + 8 * c2, bd(W2H, c2, K2), id2, 1u);
+                        if (++c2 == 13) tc::commit(mb + MB_D2F + sl);
+                    }
+                    while (c2 == 13 && c3 < 7 && mbar_test(mb + MB_A3R + 7 * sl + c3, ph)) {
+                        tc::fence_after();
+                        tc::mma_tf32_ts(S + TD3, S + 8 * c3, bd(W3H, c3, K3), id3, c3 > 0 ? 1u : 0u);
+                        tc::mma_tf32_ts(S + TD3, S + 8 * c3, bd(W3L, c3, K3), id3, 1u);
+                        tc::mma_tf32_ts(S + TD3, S + A3LO + 8 * c3, bd(W3H, c3, K3), id3, 1u);
+                        if (++c3 == 7) tc::commit(mb + MB_D3F + sl);
+                    }
+                    while (c3 == 7 && c4 < 4 && mbar_test(mb + MB_A4R + 4 * sl + c4, ph)) {
+                        tc::fence_after();
+                        tc::mma_tf32_ts(S + TD4, S + TD3 + 8 * c4, bd(W4H, c4, K4), id4, c4 > 0 ? 1u : 0u);
+                        tc::mma_tf32_ts(S + TD4, S + TD3 + 8 * c4, bd(W4L, c4, K4), id4, 1u);
+                        tc::mma_tf32_ts(S + TD4, S + A4LO + 8 * c4, bd(W4H, c4, K4), id4, 1u);
+                        if (++c4 == 4) tc::commit(mb + MB_D4F + sl);
+                    }
+                }
+                TPT_END(10, m_it);
+            }
+        }
+        __syncwarp();
+    } else if (warp > MMA_WARP) {
+        // idle warps (they only hand their registers to the other roles)
+    } else if (warp < 4) {
+        // ================================ producers ================================
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegProd));
+        const int row = tid;  // kernel of the tile; TMEM lane quadrant = warp
+        const uint32_t tq = tbase + ((uint32_t)(32 * warp) << 16);
+        uint32_t g = 0;  // ring chunks produced
+        Entries E;
+        if (MODE == MODE_CSR && my_tiles > 0) tc_csr_prefetch(J, t0_of(0) + row, E);
+        for (int64_t t = 0; t < my_tiles; ++t) {
+            const int64_t k = t0_of(t) + row;
+            const int sl = (int)(t & 1);
+            Entries NE;  // next tile's row extents and DCGM, in flight during this tile
+            if (MODE == MODE_CSR && t + 1 < my_tiles) tc_csr_prefetch(J, t0_of(t + 1) + row, NE);
+            if (MODE == MODE_CSR && E.cnt > 0) {
+                // this tile's entries into L1 (read per chunk below)
+                const uint32_t* ep = J.entries + E.first;
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(ep));
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(ep + kEnt - 1));
+            }
+            TPT_BEGIN(p_t);
+            // ---- per-kernel preparation: totals, chunk mask, non-finite rows ----
+            float tf[3] = {0.f, 0.f, 0.f}, rr[3] = {0.f, 0.f, 0.f};
+            uint32_t mask = 1u;   // chunks this kernel touches (chunk 0: DCGM)
+            bool uns = false;     // CSR: entries not strictly increasing, or spilled
+            bool bad = false;     // a non-finite feature: FMA-pipe forward
+            float ef[kEnt];       // CSR (sorted rows): fraction of entry e and its column
+            uint32_t ecp[kEnt / 4];  //   (8 + slot, or 0xFF) packed four per register
+            if (MODE == MODE_CSR) {
+                uint64_t tot[3] = {0, 0, 0};
+                uint32_t t32[3] = {0u, 0u, 0u};
+                int prev = -1;
+                uint32_t en[kEnt];
+                load_entries(J.entries + E.first, E.cnt, en);
+#pragma unroll
+                for (int e = 0; e < kEnt; ++e) {
+                    const int slot = (int)(en[e] & 127u);
+                    const uint32_t cnt = en[e] >> 7;
+                    if (e < E.cnt) {
+                        uns |= slot <= prev;
+                        prev = slot;
+                        if (slot < DSO_COUNT_ROWS) {
+                            const int cat = cat_of_row(slot);
+                            t32[0] += cat == 0 ? cnt : 0u;
+                            t32[1] += cat == 1 ? cnt : 0u;
+                            t32[2] += cat == 2 ? cnt : 0u;
+                            mask |= 1u << ((8 + slot) >> 3);
+                        }
+                    }
+                }
+                if (E.cnt > kEnt) {
+                    uns = true;
+                    for (int idx = kEnt; idx < E.cnt; ++idx) {
+                        const uint32_t en = __ldg(J.entries + E.first + idx);
+                        const int slot = (int)(en & 127u);
+                        if (slot < DSO_COUNT_ROWS) {
+                            const int cat = cat_of_row(slot);
+                            tot[0] += cat == 0 ? (en >> 7) : 0u;
+                            tot[1] += cat == 1 ? (en >> 7) : 0u;
+                            tot[2] += cat == 2 ? (en >> 7) : 0u;
+                            mask |= 1u << ((8 + slot) >> 3);
+                        }
+                    }
+                }
+#pragma unroll
+                for (int c = 0; c < 3; ++c) tot[c] += t32[c];
+                cat_scales(tot, tf, rr);
+#pragma unroll
+                for (int e4 = 0; e4 < kEnt / 4; ++e4) ecp[e4] = 0u;
+#pragma unroll
+                for (int e = 0; e < kEnt; ++e) {
+                    const int slot = (int)(en[e] & 127u);
+                    const bool live = e < E.cnt && slot < DSO_COUNT_ROWS;
+                    ecp[e >> 2] |= (live ? 8u + (uint32_t)slot : 0xFFu) << (8 * (e & 3));
+                    ef[e] = live ? norm_slot(en[e] >> 7, slot, tf, rr) : 0.f;
+                }
+#pragma unroll
+                for (int j = 0; j < 8; ++j) bad |= !isfinite(E.dg[j]);
+            } else if (MODE == MODE_DENSE) {
+                uint64_t tot[3] = {0, 0, 0};
+                if (k < J.n) {
+#pragma unroll 1
+                    for (int r0 = 0; r0 < DSO_COUNT_ROWS; r0 += 42) {
+                        uint32_t cv[42];
+#pragma unroll
+                        for (int u = 0; u < 42; ++u)
+                            cv[u] = __ldg(J.counts + (int64_t)(r0 + u) * J.ld + k);
+#pragma unroll
+                        for (int u = 0; u < 42; ++u) {
+                            const int cat = cat_of_row(r0 + u);
+                            tot[0] += cat == 0 ? cv[u] : 0u;
+                            tot[1] += cat == 1 ? cv[u] : 0u;
+                            tot[2] += cat == 2 ? cv[u] : 0u;
+                        }
+                    }
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) bad |= !isfinite(__ldg(J.dcgm + (int64_t)j * J.ld + k));
+                }
+                cat_scales(tot, tf, rr);
+                mask = 0x1FFFFu;
+            } else {
+                mask = 0x1FFFFu;
+            }
+            // the tile's chunk mask (OR over the 128 kernels), published for the MMA
+            // thread before the tile's first chunk
+            {
+                const uint32_t wm = __reduce_or_sync(0xffffffffu, mask);
+                if (lane == 0) misc[10 + 4 * sl + warp] = wm;
+                bar_sync(1, kGroupT);
+                mask = misc[10 + 4 * sl] | misc[11 + 4 * sl] | misc[12 + 4 * sl] | misc[13 + 4 * sl];
+                if (tid == 0) misc[sl] = mask;
+            }
+            // kernels with a non-finite feature: forward on the FMA pipe, into the
+            // slot's spare TMEM columns (after the epilogue of tile t-2 read them);
+            // runs before the tile's last chunk is handed to the MMA thread
+            auto slow_block = [&]() {
+                if (!__any_sync(0xffffffffu, bad)) return;
+                if (t >= 2) mbar_wait(mb + MB_SLOWFREE + sl, (uint32_t)(((t >> 1) - 1) & 1));
+                float out[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+                if (bad) {
+                    float x[DSO_FUSED_ROWS];
+                    if (MODE == MODE_PRED) {
+                        for (int c = 0; c < DSO_FUSED_ROWS; ++c) x[c] = J.fused[(int64_t)c * J.ld + k];
+                    } else {
+                        for (int j = 0; j < 8; ++j) x[j] = J.dcgm[(int64_t)j * J.ld + k];
+                        for (int r = 0; r < DSO_COUNT_ROWS; ++r) {
+                            uint32_t cnt = 0;
+                            if (MODE == MODE_DENSE) {
+                                cnt = J.counts[(int64_t)r * J.ld + k];
+                            } else {
+                                for (int idx = 0; idx < E.cnt; ++idx) {
+                                    const uint32_t en = J.entries[E.first + idx];
+                                    if ((int)(en & 127u) == r) cnt += en >> 7;
+                                }
+                            }
+                            x[8 + r] = norm_slot(cnt, r, tf, rr);
+                        }
+                    }
+                    tc_forward_x(sm, x, out);
+                    out[7] = 1.f;
+                }
+                tc::fence_after();
+                tc::st8(tq + TSLOW + 8 * sl, out);
+                tc::wait_st();
+                tc::fence_before();
+                const uint32_t bm = __ballot_sync(0xffffffffu, bad);
+                if (lane == 0) misc[2 + 4 * sl + warp] = bm;
+            };
+            if (MODE == MODE_CSR) slow_block();
+            TPT_END(14, p_t);
+            TPT_BEGIN(p_c);
+            // ---- chunks -> ring ----------------------------------------------------
+            auto hand_over = [&](int b) {  // the chunk in ring buffer b is complete
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) mb_arrive(mb + MB_XFULL + b);
+                ++g;
+            };
+            auto claim = [&]() {  // next ring buffer, once the MMAs reading it are done
+                const int b = (int)(g % kRing);
+                TPT_BEGIN(p_w);
+                if (g >= kRing) mbar_wait(mb + MB_XEMPTY + b, ((g / kRing) - 1) & 1u);
+                TPT_END(0, p_w);
+                return b;
+            };
+            const int o = (row >> 3) * 64 + (row & 7) * 4;  // this kernel's core-matrix rows
+            if (MODE == MODE_CSR) {
+                // One in-order pass over the row's entries (sorted by slot): the thread
+                // walks the tile's chunk mask alongside, claiming each chunk buffer,
+                // writing its row (zeros, then its entries in place) and handing the
+                // chunk over when it moves past it.  Every lane visits every chunk of
+                // the mask in order, so the per-chunk warp hand-over lines up.
+                int cur = -1, b = 0;
+                float* buf = sm + S_RING;
+                auto advance_to = [&](int ch) {  // ch in the mask, or 17: past the end
+                    while (cur < ch) {
+                        int nxt = cur + 1;
+                        while (nxt < 17 && !((mask >> nxt) & 1u)) ++nxt;
+                        if (nxt > ch || nxt >= 17) {
+                            if (ch < 17) break;  // (ch is in the mask: unreachable)
+                        }
+                        if (cur >= 0) {
+                            TPT_BEGIN(p_p);
+                            hand_over(b);
+                            TPT_END(1, p_p);
+                        }
+                        if (nxt >= 17) {
+                            cur = 17;
+                            break;
+                        }
+                        cur = nxt;
+                        b = claim();
+                        buf = sm + S_RING + b * kChunkF;
+                        if (cur == 0) {
+                            put_chunk(buf, row, E.dg);
+                        } else {
+                            const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+                            *reinterpret_cast<float4*>(buf + o) = z4;
+                            *reinterpret_cast<float4*>(buf + o + 32) = z4;
+                            *reinterpret_cast<float4*>(buf + TT * 8 + o) = z4;
+                            *reinterpret_cast<float4*>(buf + TT * 8 + o + 32) = z4;
+                        }
+                    }
+                };
+                advance_to(0);
+                if (!uns) {
+#pragma unroll
+                    for (int e = 0; e < kEnt; ++e) {
+                        const uint32_t col = (ecp[e >> 2] >> (8 * (e & 3))) & 0xFFu;
+                        if (col != 0xFFu) {
+                            advance_to((int)(col >> 3));
+                            const float f = ef[e], h = tc::tf32_hi(f);
+                            const int j = (int)(col & 7u), off = o + (j >> 2) * 32 + (j & 3);
+                            buf[off] = h;
+                            buf[TT * 8 + off] = f - h;
+                        }
+                    }
+                } else {
+                    // duplicate / unsorted / long rows: per chunk, sum the counts per slot
+                    for (int c = 1; c < 17; ++c) {
+                        if (!((mask >> c) & 1u)) continue;
+                        advance_to(c);
+                        uint32_t acc[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+                        for (int idx = 0; idx < E.cnt; ++idx) {
+                            const uint32_t en = __ldg(J.entries + E.first + idx);
+                            const int col = 8 + (int)(en & 127u);
+                            if ((col >> 3) == c && col - 8 < DSO_COUNT_ROWS)
+#pragma unroll
+                                for (int j = 0; j < 8; ++j) acc[j] += (col & 7) == j ? (en >> 7) : 0u;
+                        }
+                        float v[8];
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            const int r = 8 * c + j - 8;
+                            v[j] = (r < DSO_COUNT_ROWS) ? norm_slot(acc[j], r, tf, rr) : 0.f;
+                        }
+                        put_chunk(buf, row, v);
+                    }
+                }
+                advance_to(17);  // zero rows of the remaining chunks, hand over the last
+            } else {
+                // predict / dense: chunk values loaded kAhead chunks in advance
+                constexpr int kAhead = 4;
+                float pf[kAhead][8];
+                auto load_chunk = [&](int c, float (&v)[8]) {
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        const int col = 8 * c + j;
+                        float x = 0.f;
+                        if (k < J.n && col < DSO_FUSED_ROWS) {
+                            if (MODE == MODE_PRED) {
+                                x = __ldg(J.fused + (int64_t)col * J.ld + k);
+                            } else if (col < 8) {
+                                x = __ldg(J.dcgm + (int64_t)col * J.ld + k);
+                            } else {
+                                const uint32_t cnt = __ldg(J.counts + (int64_t)(col - 8) * J.ld + k);
+                                x = norm_slot(cnt, col - 8, tf, rr);
+                            }
+                        }
+                        v[j] = x;
+                    }
+                };
+#pragma unroll
+                for (int a = 0; a < kAhead; ++a) load_chunk(a, pf[a]);
+#pragma unroll
+                for (int c = 0; c < 17; ++c) {
+                    float v[8];
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        v[j] = pf[c % kAhead][j];
+                        bad |= !isfinite(v[j]);
+                    }
+                    if (c + kAhead < 17) load_chunk(c + kAhead, pf[c % kAhead]);
+                    if (c == 16) slow_block();
+                    const int b = claim();
+                    put_chunk(sm + S_RING + b * kChunkF, row, v);
+                    TPT_BEGIN(p_p);
+                    hand_over(b);
+                    TPT_END(1, p_p);
+                }
+            }
+            TPT_END(15, p_c);
+            if (MODE == MODE_CSR && t + 1 < my_tiles) E = NE;
+        }
+    } else {
+        // ============================ epilogue groups ============================
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegEpi));
+        const int grp = (warp - 4) >> 2, q = warp & 3;
+        const int row = 32 * q + lane;
+        const uint32_t tq = tbase + ((uint32_t)(32 * q) << 16);
+        const uint32_t S = tq + (uint32_t)(grp * SLOT_COLS);
+        const float4* s_core = reinterpret_cast<const float4*>(sm + S_TABLES);
+        const float2* s_mem = reinterpret_cast<const float2*>(sm + S_TABLES + 4 * J.nc);
+        const float4* s_pair =
+            J.pairs ? reinterpret_cast<const float4*>(sm + tc_pairs_offset(J.nc, J.nm)) : nullptr;
+        for (int64_t t = grp; t < my_tiles; t += 2) {
+            const uint32_t ph = (uint32_t)((t >> 1) & 1);
+            const int64_t k = t0_of(t) + row;
+            TPT_BEGIN(e_w1);
+            wait_acq(mb + MB_D1F + grp, ph);
+            TPT_END(2, e_w1);
+            TPT_BEGIN(e_1);
+            for (int c = 0; c < 13; ++c)
+                epi_chunk<H1>(S + 8 * c, S + 8 * c, S + A2LO + 8 * c, c, sm + NB1,
+                              mb + MB_A2R + 13 * grp + c);
+            TPT_END(3, e_1);
+            TPT_BEGIN(e_w2);
+            wait_acq(mb + MB_D2F + grp, ph);
+            TPT_END(4, e_w2);
+            TPT_BEGIN(e_2);
+            for (int c = 0; c < 7; ++c)
+                epi_chunk<H2>(tq + TD2 + 8 * c, S + 8 * c, S + A3LO + 8 * c, c, sm + NB2,
+                              mb + MB_A3R + 7 * grp + c);
+            __syncwarp();
+            if (lane == 0) mb_arrive(mb + MB_D2FREE);  // D2 read (tcgen05.wait::ld done)
+            TPT_END(5, e_2);
+            TPT_BEGIN(e_w3);
+            wait_acq(mb + MB_D3F + grp, ph);
+            TPT_END(6, e_w3);
+            TPT_BEGIN(e_3);
+            for (int c = 0; c < 4; ++c)
+                epi_chunk<H3>(S + TD3 + 8 * c, S + TD3 + 8 * c, S + A4LO + 8 * c, c, sm + NB3,
+                              mb + MB_A4R + 4 * grp + c);
+            TPT_END(7, e_3);
+            TPT_BEGIN(e_w4);
+            wait_acq(mb + MB_D4F + grp, ph);
+            TPT_END(8, e_w4);
+            TPT_BEGIN(e_4);
+            float raw[8];
+            {
+                float v[8];
+                tc::ld8(S + TD4, v);
+                tc::wait_ld();
+#pragma unroll
+                for (int j = 0; j < 7; ++j)
+                    raw[j] = fmaf(v[j] + sm[B4 + j], sm[S_STATS + 8 + j], sm[S_STATS + j]);
+                const uint32_t bm = *reinterpret_cast<volatile uint32_t*>(misc + 2 + 4 * grp + q);
+                if (bm) {  // kernels predicted on the FMA pipe by the producer
+                    float w[8];
+                    tc::ld8(tq + TSLOW + 8 * grp, w);
+                    tc::wait_ld();
+                    if ((bm >> lane) & 1u)
+#pragma unroll
+                        for (int j = 0; j < 7; ++j) raw[j] = w[j];
+                    __syncwarp();
+                    if (lane == 0) misc[2 + 4 * grp + q] = 0u;
+                }
+                tc::fence_before();
+                __syncwarp();
+                if (lane == 0) mb_arrive(mb + MB_SLOWFREE + grp);
+            }
+            if (MODE == MODE_PRED) {
+                if (k < J.n) {
+                    if (J.raw)
+#pragma unroll
+                        for (int j = 0; j < 7; ++j) J.raw[j * J.ld_out + k] = raw[j];
+                    const bool cl = clamp_params(raw);
+#pragma unroll
+                    for (int j = 0; j < 7; ++j) J.params[j * J.ld_out + k] = raw[j];
+                    if (J.clamped) J.clamped[k] = cl ? 1 : 0;
+                }
+            } else {
+                float pr[7];
+#pragma unroll
+                for (int j = 0; j < 7; ++j) pr[j] = raw[j];
+                const bool cl = clamp_params(pr);
+                const KParams p{pr[0], pr[1], pr[2], pr[3], pr[4], pr[5], pr[6]};
+                const Best r = sweep_dispatch<4>(p, s_core, s_mem, s_pair, J, 0, J.nc);
+#pragma unroll
+                for (int d = 0; d < 4; ++d) write_result(J, k, d, r, cl, pr, p, s_core, s_mem);
+            }
+            TPT_END(9, e_4);
+        }
+    }
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    if (warp == MMA_WARP) tc::tmem_dealloc<512>(tbase);
+}
+
+inline size_t tc_smem_bytes(int nc, int nm, bool pairs) {
+    return pairs ? (size_t)(tc_pairs_offset(nc, nm) + 8 * ((nc + 1) / 2)) * sizeof(float)
+                 : (size_t)(S_TABLES + 4 * nc + 2 * nm) * sizeof(float);
+}
+
+// Packed tc model from the reference-layout master (f32): hi/lo splits with
+// the device's cvt.rna.tf32, padding zero, non-finite weights counted.
+__global__ void tc_repack_kernel(const float* __restrict__ master, float* __restrict__ pk) {
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    auto put = [&](int hi, int lo, int n, int k, int K, float w) {
+        const float h = tc::tf32_hi(w);
+        pk[hi + cm(n, k, K)] = h;
+        pk[lo + cm(n, k, K)] = isfinite(w) ? w - h : 0.f;
+        if (!isfinite(w)) atomicAdd(reinterpret_cast<int*>(pk + FLAG), 1);
+    };
+    if (e < MW2) {
+        put(W1H, W1L, e / 134, e % 134, K1, master[e]);
+    } else if (e < MW3) {
+        const int f = e - MW2;
+        put(W2H, W2L, f / 100, f % 100, K2, master[e]);
+    } else if (e < MW4) {
+        const int f = e - MW3;
+        put(W3H, W3L, f / 50, f % 50, K3, master[e]);
+    } else if (e < MB1) {
+        const int f = e - MW4;
+        put(W4H, W4L, f / 25, f % 25, K4, master[e]);
+    } else if (e < MB2) {
+        pk[NB1 + e - MB1] = master[e] * kNL2E;
+    } else if (e < MB3) {
+        pk[NB2 + e - MB2] = master[e] * kNL2E;
+    } else if (e < MB4) {
+        pk[NB3 + e - MB3] = master[e] * kNL2E;
+    } else if (e < kMasterFloats) {
+        pk[B4 + e - MB4] = master[e];
+    }
+}
+
+}  // namespace tce

@@ -57,3 +57,12 @@ def ctx():
     c = Context(0)
     yield c
     c.close()
+
+
+@pytest.fixture(params=[0, 1], ids=["ffma", "tc"])
+def engine(request, ctx):
+    """Runs a predictor test on both engines: the FMA-pipe kernel (0) and the
+    tcgen05 3xTF32 kernel (1); restores the default afterwards."""
+    ctx.set_option("mlp_engine", request.param)
+    yield request.param
+    ctx.set_option("mlp_engine", 0)

@@ -14,7 +14,7 @@ import torch
 
 from paper_2407_13096_b200 import init_mlp, MlpModel
 
-pytestmark = pytest.mark.gpu
+pytestmark = [pytest.mark.gpu, pytest.mark.usefixtures("engine")]
 
 
 def fused_dev(x):

@@ -9,7 +9,7 @@ import torch
 from helpers import check_argmin, rel_err
 from paper_2407_13096_b200 import config_domain, init_mlp
 
-pytestmark = pytest.mark.gpu
+pytestmark = [pytest.mark.gpu, pytest.mark.usefixtures("engine")]
 
 
 def stats_model(port, seed=424242):
