@@ -75,6 +75,9 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-stages", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=0)
+    ap.add_argument("--engine", default="auto", choices=["auto", "ffma", "tc"],
+                    help="predictor engine: the library's auto choice (tcgen05 for CSR), "
+                         "the FMA-pipe kernel, or the tcgen05 3xTF32 kernel")
     ap.add_argument("--input", default="csr", choices=["csr", "dense"],
                     help="PTX counts as sparse per-kernel lists (the reference's map shape) "
                          "or dense [126][n] rows")
@@ -251,6 +254,7 @@ def run_ours(args, rank, world, local_rank):
     dev = torch.device("cuda", local_rank)
     dom = linear_domain(cfg["nc"], cfg["nm"])
     ctx = Context(local_rank)
+    ctx.set_option("mlp_engine", {"ffma": 0, "tc": 1, "auto": 2}[args.engine])
     ctx.set_domain(dom)
     model = bench_model_device(ctx)
     ctx.set_model(model)
@@ -422,6 +426,7 @@ def run_ours(args, rank, world, local_rank):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (gen_kernel stream generated on device; random-init MLP seed 424242)",
         "config": {"workload": cfg["desc"], "kernels_per_gpu": n, "grid": f"{cfg['nc']}x{cfg['nm']}",
+                   "engine": args.engine,
                    "eta": cfg["eta"] if cfg["eta"] is not None else "0.00..1.00 (101)",
                    "parallelism": f"kernel-sharded x{world}, no collective",
                    "input": ("sparse per-kernel PTX count lists (24 non-zeros/kernel) + DCGM"

@@ -246,8 +246,8 @@ int64_t dso_launch_count(const dso_ctx* ctx) { return ctx ? ctx->c.launches : 0;
 int32_t dso_set_option(dso_ctx* ctx, const char* key, int64_t value) {
     if (!ctx || !key) return kInvalidArgument;
     if (std::string(key) == "mlp_engine") {
-        if (value != 0 && value != 1) return fail(ctx, kInvalidArgument, "mlp_engine is 0 or 1");
-        ctx->c.mlp_engine = value != 0;
+        if (value < 0 || value > 2) return fail(ctx, kInvalidArgument, "mlp_engine is 0, 1 or 2");
+        ctx->c.mlp_engine = (int)value;
         return 0;
     }
     if (std::string(key) == "fast_sweep") {

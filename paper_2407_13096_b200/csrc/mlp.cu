@@ -464,6 +464,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t* mbar, uint32_t parity) {
 }
 
 // count / total, correctly rounded (Markstein), totals >= 2^24 in FP64
+// totals >= 2^24 (tf = -hi, rr = lo): FP64 quotient, out of line so the
+// common path never carries (or if-converts) the double division
+__device__ __noinline__ float normalize_count_wide(uint32_t c, float tf, float rr) {
+    return (float)((double)c / fma((double)-tf, 16777216.0, (double)rr));
+}
 __device__ __forceinline__ float normalize_count(uint32_t c, float tf, float rr) {
     if (tf > 0.f) {
         const float cf = (__int_as_float(0x4B000000u | (c & 0x7FFFFFu)) - 8388608.f) +
@@ -472,7 +477,7 @@ __device__ __forceinline__ float normalize_count(uint32_t c, float tf, float rr)
         return fmaf(fmaf(-qq, tf, cf), rr, qq);
     }
     if (tf == 0.f) return 0.f;
-    return (float)((double)c / fma((double)-tf, 16777216.0, (double)rr));
+    return normalize_count_wide(c, tf, rr);
 }
 
 __device__ __forceinline__ void produce_features(float* act, float* scr,
@@ -1190,10 +1195,10 @@ Stats stats_of(const Ctx& cx) {
     return s;
 }
 
-// Tensor-core engine (mlp_tc.cuh) for predict and CSR-pipeline launches when
-// enabled (dso_set_option "mlp_engine"), the tables fit and the model is known
-// finite on the host; after a device-side repack (training) finiteness lives
-// in a device flag, so both engines are launched and each exits on the flag.
+// Tensor-core engine (mlp_tc.cuh) when selected (dso_set_option "mlp_engine":
+// 1, or 2 = auto for predict and the CSR pipeline), the tables fit and the model
+// is known finite on the host; after a device-side repack (training) finiteness
+// lives in a device flag, so both engines are launched and each exits on the flag.
 template <int MODE>
 cudaError_t launch_tc(Ctx& cx, const Job& J) {
     constexpr bool PIPE = MODE != MODE_PRED;
@@ -1217,7 +1222,10 @@ cudaError_t launch_tc(Ctx& cx, const Job& J) {
 
 template <int MODE>
 bool tc_eligible(const Ctx& cx, const Job& J) {
-    if (!cx.mlp_engine || !cx.model.wtc || cx.model.tc_state == 0) return false;
+    if (cx.mlp_engine == 0 || !cx.model.wtc || cx.model.tc_state == 0) return false;
+    // auto: the dense-count producer re-reads 126 strided rows per kernel and is
+    // latency-bound on this engine; the FMA-pipe kernel's bulk copies win there
+    if (cx.mlp_engine == 2 && MODE == MODE_DENSE) return false;
     if (MODE == MODE_PRED) return true;
     return tce::tc_smem_bytes(J.nc, J.nm, false) <= 227 * 1024;
 }
@@ -1319,9 +1327,17 @@ cudaError_t model_upload(Ctx& cx, const double* W, const double* b) {
     for (int n = 0; n < 50; ++n)
         for (int k = 0; k < 100; ++k) put(tce::W2H, tce::W2L, n, k, tce::K2, W[MW2 + n * 100 + k]);
     for (int n = 0; n < 25; ++n)
-        for (int k = 0; k < 50; ++k) put(tce::W3H, tce::W3L, n, k, tce::K3, W[MW3 + n * 50 + k]);
+        for (int k = 0; k < 50; ++k) {
+            const float w = (float)W[MW3 + n * 50 + k];
+            tp[tce::W3T + k * 28 + n] = w;
+            bad += std::isfinite(w) ? 0 : 1;
+        }
     for (int n = 0; n < 7; ++n)
-        for (int k = 0; k < 25; ++k) put(tce::W4H, tce::W4L, n, k, tce::K4, W[MW4 + n * 25 + k]);
+        for (int k = 0; k < 25; ++k) {
+            const float w = (float)W[MW4 + n * 25 + k];
+            tp[tce::W4T + k * 8 + n] = w;
+            bad += std::isfinite(w) ? 0 : 1;
+        }
     for (int i = 0; i < 100; ++i) tp[tce::NB1 + i] = (float)b[i] * tce::kNL2E;
     for (int i = 0; i < 50; ++i) tp[tce::NB2 + i] = (float)b[100 + i] * tce::kNL2E;
     for (int i = 0; i < 25; ++i) tp[tce::NB3 + i] = (float)b[150 + i] * tce::kNL2E;

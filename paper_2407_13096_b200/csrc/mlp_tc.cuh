@@ -49,28 +49,34 @@ constexpr int MMA_WARP = 12;
 // epilogue groups to 144 (128*168 + 256*144 + 128*56 = 64K).
 constexpr int kRegProd = 168, kRegEpi = 144, kRegMma = 56;
 static_assert(128 * kRegProd + 256 * kRegEpi + 128 * kRegMma <= 65536, "RF budget");
-constexpr int N1 = 112, K1 = 136, N2 = 64, K2 = 104, N3 = 32, K3 = 56, N4 = 16, K4 = 32;
+constexpr int N1 = 112, K1 = 136, N2 = 64, K2 = 104;
 constexpr int H1 = 100, H2 = 50, H3 = 25, H4 = 7;
-// packed model (floats): weights hi/lo in the SWIZZLE_NONE K-major core-matrix
-// layout (tc.cuh), -b*log2(e) for the hidden layers, b4, the non-finite count
+// packed model (floats): L1/L2 weights hi/lo in the SWIZZLE_NONE K-major
+// core-matrix layout (tc.cuh); L3/L4 (1,425 weights) stay FP32 for the FMA
+// pipe, transposed [k][n] with n padded to 28 / 8 (FFMA2 neuron pairs);
+// -b*log2(e) for the hidden layers, b4, the non-finite count
 constexpr int W1H = 0, W1L = W1H + N1 * K1, W2H = W1L + N1 * K1, W2L = W2H + N2 * K2;
-constexpr int W3H = W2L + N2 * K2, W3L = W3H + N3 * K3, W4H = W3L + N3 * K3, W4L = W4H + N4 * K4;
-constexpr int NB1 = W4L + N4 * K4, NB2 = NB1 + N1, NB3 = NB2 + N2, B4 = NB3 + N3;
-constexpr int FLAG = B4 + N4;
+constexpr int W3T = W2L + N2 * K2, W4T = W3T + H2 * 28;
+constexpr int NB1 = W4T + H3 * 8, NB2 = NB1 + N1, NB3 = NB2 + N2, B4 = NB3 + 32;
+constexpr int FLAG = B4 + 16;
 constexpr int kModel = FLAG + 4;
 __host__ __device__ __forceinline__ int cm(int n, int k, int K) {
     return ((n >> 3) * (K >> 2) + (k >> 2)) * 32 + (n & 7) * 4 + (k & 3);
 }
 // shared memory (floats)
-constexpr int kRing = 3;                     // X chunk buffers
+constexpr int kRing = 2;                     // X chunk buffers
 constexpr int kChunkF = 2 * TT * 8;          // hi [128][8] + lo [128][8] (core-matrix layout)
 constexpr int S_STATS = kModel;              // mean[8] std[8]
 constexpr int S_RING = S_STATS + 16;
-constexpr int S_MISC = S_RING + kRing * kChunkF;  // u32: [0..1] chunk masks, [2..9] slow rows, [10..17] partial masks
+// CSR: per-kernel entry lists of the tile being produced, entry-major so a warp's
+// 32 kernels hit 32 banks: fraction [24][128] f32 and column [24][128] u8
+constexpr int S_ELIST = S_RING + kRing * kChunkF;
+constexpr int S_ECOL = S_ELIST + 24 * TT;
+constexpr int S_MISC = S_ECOL + 24 * TT / 4;  // u32: [0..1] chunk masks, [2..9] slow rows, [10..17] partial masks
 constexpr int S_MBAR = S_MISC + 24;
 enum {
     MB_XFULL = 0, MB_XEMPTY = 3, MB_D1F = 6, MB_A2R = 8, MB_D2F = 34, MB_D2FREE = 36,
-    MB_A3R = 37, MB_D3F = 51, MB_A4R = 53, MB_D4F = 61, MB_SLOWFREE = 63, kMbars = 65
+    MB_SLOWFREE = 37, kMbars = 39
 };
 constexpr int S_TSLOT = S_MBAR + 2 * kMbars;
 constexpr int S_TABLES = (S_TSLOT + 4 + 3) & ~3;  // core4[nc], mem2[nm], level pairs
@@ -80,7 +86,7 @@ __host__ __device__ __forceinline__ int tc_pairs_offset(int nc, int nm) {
 }
 // TMEM columns
 constexpr int SLOT_COLS = 216, TD2 = 432, TSLOW = 496;
-constexpr int A2LO = 112, A3LO = 56, TD3 = 112, TD4 = 144, A4LO = 160;
+constexpr int A2LO = 112;
 constexpr float kNL2E = -1.4426950408889634f;
 
 // phase accounting (debug library only): producer 0, epilogue thread 128, MMA thread
@@ -186,12 +192,12 @@ __device__ __noinline__ void tc_forward_x(const float* sm, const float* x, float
     }
     for (int n = 0; n < H3; ++n) {
         float z = 0.f;
-        for (int c = 0; c < H2; ++c) z = fmaf(w(W3H, W3L, n, c, K3), h2[c], z);
+        for (int c = 0; c < H2; ++c) z = fmaf(sm[W3T + c * 28 + n], h2[c], z);
         h3[n] = sig(z, sm[NB3 + n]);
     }
     for (int n = 0; n < H4; ++n) {
         float z = 0.f;
-        for (int c = 0; c < H3; ++c) z = fmaf(w(W4H, W4L, n, c, K4), h3[c], z);
+        for (int c = 0; c < H3; ++c) z = fmaf(sm[W4T + c * 8 + n], h3[c], z);
         raw[n] = fmaf(z + sm[B4 + n], sm[S_STATS + 8 + n], sm[S_STATS + n]);
     }
 }
@@ -312,12 +318,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
             for (int g = 0; g < 2; ++g) {
                 mb_init(mb + MB_D1F + g, 1);
                 mb_init(mb + MB_D2F + g, 1);
-                mb_init(mb + MB_D3F + g, 1);
-                mb_init(mb + MB_D4F + g, 1);
                 mb_init(mb + MB_SLOWFREE + g, 4);
                 for (int c = 0; c < 13; ++c) mb_init(mb + MB_A2R + 13 * g + c, 4);
-                for (int c = 0; c < 7; ++c) mb_init(mb + MB_A3R + 7 * g + c, 4);
-                for (int c = 0; c < 4; ++c) mb_init(mb + MB_A4R + 4 * g + c, 4);
             }
             mb_init(mb + MB_D2FREE, 4);
             asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -341,8 +343,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     if (warp == MMA_WARP) {
         // ================================ MMA issuer ================================
         if (lane == 0) {
-            const uint32_t id1 = tc::idesc_tf32(128, N1), id2 = tc::idesc_tf32(128, N2),
-                           id3 = tc::idesc_tf32(128, N3), id4 = tc::idesc_tf32(128, N4);
+            const uint32_t id1 = tc::idesc_tf32(128, N1), id2 = tc::idesc_tf32(128, N2);
             const uint32_t s0 = smem_u32(sm);
             auto bd = [&](int off, int kk, int K) {
                 return tc::sdesc(s0 + off * 4 + kk * 256, 128, (uint32_t)(K >> 2) * 128);
@@ -380,45 +381,34 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
                 }
                 return true;
             };
-            if (my_tiles > 0) {
-                L1S s0t{0, 0, 0u, true};
-                while (s0t.active) l1_step(s0t);
-            }
-            for (int64_t t = 0; t < my_tiles; ++t) {
-                L1S st{t + 1, 0, 0u, t + 1 < my_tiles};
-                const int sl = (int)(t & 1);
+            // One scheduler loop: L1 runs one tile ahead of L2 (tile b + 2 reuses tile
+            // b's slot once L2(b) is issued: the tensor core executes in issue order).
+            L1S st{0, 0, 0u, my_tiles > 0};
+            int64_t b = 0;
+            bool d2ok = true;
+            int c2 = 0;
+            while (b < my_tiles) {
+                if (!st.active && st.t + 1 < my_tiles && st.t + 1 <= b + 1) st = L1S{st.t + 1, 0, 0u, true};
+                while (st.active && l1_step(st)) {
+                }
+                if (st.t <= b && st.active) continue;  // L1(b) not fully issued yet
+                const int sl = (int)(b & 1);
                 const uint32_t S = tbase + (uint32_t)(sl * SLOT_COLS);
-                const uint32_t ph = (uint32_t)((t >> 1) & 1);
-                bool d2ok = t == 0;
-                int c2 = 0, c3 = 0, c4 = 0;
-                TPT_BEGIN(m_it);
-                while (st.active || c4 < 4) {
-                    while (st.active && l1_step(st)) {
-                    }
-                    if (!d2ok && mbar_test(mb + MB_D2FREE, (uint32_t)((t - 1) & 1))) d2ok = true;
-                    while (d2ok && c2 < 13 && mbar_test(mb + MB_A2R + 13 * sl + c2, ph)) {
-                        tc::fence_after();
-                        tc::mma_tf32_ts(tbase + TD2, S + 8 * c2, bd(W2H, c2, K2), id2, c2 > 0 ? 1u : 0u);
-                        tc::mma_tf32_ts(tbase + TD2, S + 8 * c2, bd(W2L, c2, K2), id2, 1u);
-                        tc::mma_tf32_ts(tbase + TD2, S + A2LO + 8 * c2, bd(W2H, c2, K2), id2, 1u);
-                        if (++c2 == 13) tc::commit(mb + MB_D2F + sl);
-                    }
-                    while (c2 == 13 && c3 < 7 && mbar_test(mb + MB_A3R + 7 * sl + c3, ph)) {
-                        tc::fence_after();
-                        tc::mma_tf32_ts(S + TD3, S + 8 * c3, bd(W3H, c3, K3), id3, c3 > 0 ? 1u : 0u);
-                        tc::mma_tf32_ts(S + TD3, S + 8 * c3, bd(W3L, c3, K3), id3, 1u);
-                        tc::mma_tf32_ts(S + TD3, S + A3LO + 8 * c3, bd(W3H, c3, K3), id3, 1u);
-                        if (++c3 == 7) tc::commit(mb + MB_D3F + sl);
-                    }
-                    while (c3 == 7 && c4 < 4 && mbar_test(mb + MB_A4R + 4 * sl + c4, ph)) {
-                        tc::fence_after();
-                        tc::mma_tf32_ts(S + TD4, S + TD3 + 8 * c4, bd(W4H, c4, K4), id4, c4 > 0 ? 1u : 0u);
-                        tc::mma_tf32_ts(S + TD4, S + TD3 + 8 * c4, bd(W4L, c4, K4), id4, 1u);
-                        tc::mma_tf32_ts(S + TD4, S + A4LO + 8 * c4, bd(W4H, c4, K4), id4, 1u);
-                        if (++c4 == 4) tc::commit(mb + MB_D4F + sl);
+                const uint32_t ph = (uint32_t)((b >> 1) & 1);
+                if (!d2ok && mbar_test(mb + MB_D2FREE, (uint32_t)((b - 1) & 1))) d2ok = true;
+                while (d2ok && c2 < 13 && mbar_test(mb + MB_A2R + 13 * sl + c2, ph)) {
+                    tc::fence_after();
+                    tc::mma_tf32_ts(tbase + TD2, S + 8 * c2, bd(W2H, c2, K2), id2, c2 > 0 ? 1u : 0u);
+                    tc::mma_tf32_ts(tbase + TD2, S + 8 * c2, bd(W2L, c2, K2), id2, 1u);
+                    tc::mma_tf32_ts(tbase + TD2, S + A2LO + 8 * c2, bd(W2H, c2, K2), id2, 1u);
+                    if (++c2 == 13) {
+                        tc::commit(mb + MB_D2F + sl);
+                        ++b;
+                        c2 = 0;
+                        d2ok = false;
+                        break;
                     }
                 }
-                TPT_END(10, m_it);
             }
         }
         __syncwarp();
@@ -435,7 +425,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         for (int64_t t = 0; t < my_tiles; ++t) {
             const int64_t k = t0_of(t) + row;
             const int sl = (int)(t & 1);
-            Entries NE;  // next tile's row extents and DCGM, in flight during this tile
+            Entries NE;  // next tile's row extent and DCGM, in flight during this tile
             if (MODE == MODE_CSR && t + 1 < my_tiles) tc_csr_prefetch(J, t0_of(t + 1) + row, NE);
             if (MODE == MODE_CSR && E.cnt > 0) {
                 // this tile's entries into L1 (read per chunk below)
@@ -449,8 +439,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
             uint32_t mask = 1u;   // chunks this kernel touches (chunk 0: DCGM)
             bool uns = false;     // CSR: entries not strictly increasing, or spilled
             bool bad = false;     // a non-finite feature: FMA-pipe forward
-            float ef[kEnt];       // CSR (sorted rows): fraction of entry e and its column
-            uint32_t ecp[kEnt / 4];  //   (8 + slot, or 0xFF) packed four per register
+            uint64_t nib = 0;     // CSR (sorted rows): entries per chunk 1..16, 4 bits each
             if (MODE == MODE_CSR) {
                 uint64_t tot[3] = {0, 0, 0};
                 uint32_t t32[3] = {0u, 0u, 0u};
@@ -490,14 +479,20 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
 #pragma unroll
                 for (int c = 0; c < 3; ++c) tot[c] += t32[c];
                 cat_scales(tot, tf, rr);
-#pragma unroll
-                for (int e4 = 0; e4 < kEnt / 4; ++e4) ecp[e4] = 0u;
+                // this kernel's entry list (fraction, column) in slot order, and how
+                // many entries fall in each 8-column chunk
+                float* el = sm + S_ELIST;
+                uint8_t* ecl = reinterpret_cast<uint8_t*>(sm + S_ECOL);
+                int ne = 0;
 #pragma unroll
                 for (int e = 0; e < kEnt; ++e) {
                     const int slot = (int)(en[e] & 127u);
-                    const bool live = e < E.cnt && slot < DSO_COUNT_ROWS;
-                    ecp[e >> 2] |= (live ? 8u + (uint32_t)slot : 0xFFu) << (8 * (e & 3));
-                    ef[e] = live ? norm_slot(en[e] >> 7, slot, tf, rr) : 0.f;
+                    if (e < E.cnt && slot < DSO_COUNT_ROWS) {
+                        el[ne * TT + row] = norm_slot(en[e] >> 7, slot, tf, rr);
+                        ecl[ne * TT + row] = (uint8_t)(8 + slot);
+                        nib += 1ull << (4 * (((8 + slot) >> 3) - 1));
+                        ++ne;
+                    }
                 }
 #pragma unroll
                 for (int j = 0; j < 8; ++j) bad |= !isfinite(E.dg[j]);
@@ -590,61 +585,33 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
             };
             const int o = (row >> 3) * 64 + (row & 7) * 4;  // this kernel's core-matrix rows
             if (MODE == MODE_CSR) {
-                // One in-order pass over the row's entries (sorted by slot): the thread
-                // walks the tile's chunk mask alongside, claiming each chunk buffer,
-                // writing its row (zeros, then its entries in place) and handing the
-                // chunk over when it moves past it.  Every lane visits every chunk of
-                // the mask in order, so the per-chunk warp hand-over lines up.
-                int cur = -1, b = 0;
-                float* buf = sm + S_RING;
-                auto advance_to = [&](int ch) {  // ch in the mask, or 17: past the end
-                    while (cur < ch) {
-                        int nxt = cur + 1;
-                        while (nxt < 17 && !((mask >> nxt) & 1u)) ++nxt;
-                        if (nxt > ch || nxt >= 17) {
-                            if (ch < 17) break;  // (ch is in the mask: unreachable)
-                        }
-                        if (cur >= 0) {
-                            TPT_BEGIN(p_p);
-                            hand_over(b);
-                            TPT_END(1, p_p);
-                        }
-                        if (nxt >= 17) {
-                            cur = 17;
-                            break;
-                        }
-                        cur = nxt;
-                        b = claim();
-                        buf = sm + S_RING + b * kChunkF;
-                        if (cur == 0) {
-                            put_chunk(buf, row, E.dg);
-                        } else {
-                            const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
-                            *reinterpret_cast<float4*>(buf + o) = z4;
-                            *reinterpret_cast<float4*>(buf + o + 32) = z4;
-                            *reinterpret_cast<float4*>(buf + TT * 8 + o) = z4;
-                            *reinterpret_cast<float4*>(buf + TT * 8 + o + 32) = z4;
-                        }
-                    }
-                };
-                advance_to(0);
-                if (!uns) {
-#pragma unroll
-                    for (int e = 0; e < kEnt; ++e) {
-                        const uint32_t col = (ecp[e >> 2] >> (8 * (e & 3))) & 0xFFu;
-                        if (col != 0xFFu) {
-                            advance_to((int)(col >> 3));
-                            const float f = ef[e], h = tc::tf32_hi(f);
-                            const int j = (int)(col & 7u), off = o + (j >> 2) * 32 + (j & 3);
+                const float* el = sm + S_ELIST;
+                const uint8_t* ecl = reinterpret_cast<const uint8_t*>(sm + S_ECOL);
+                int ep = 0;  // first list entry of the current chunk
+#pragma unroll 1
+                for (int c = 0; c < 17; ++c) {
+                    if (!((mask >> c) & 1u)) continue;
+                    const int b = claim();
+                    float* buf = sm + S_RING + b * kChunkF;
+                    if (c == 0) {
+                        put_chunk(buf, row, E.dg);
+                    } else if (!uns) {
+                        // zeros, then this chunk's entries in place (predicated scan)
+                        const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+                        *reinterpret_cast<float4*>(buf + o) = z4;
+                        *reinterpret_cast<float4*>(buf + o + 32) = z4;
+                        *reinterpret_cast<float4*>(buf + TT * 8 + o) = z4;
+                        *reinterpret_cast<float4*>(buf + TT * 8 + o + 32) = z4;
+                        const int n_c = (int)((nib >> (4 * (c - 1))) & 15u);
+                        for (int i = ep; i < ep + n_c; ++i) {
+                            const float f = el[i * TT + row], h = tc::tf32_hi(f);
+                            const int j = ecl[i * TT + row] & 7, off = o + (j >> 2) * 32 + (j & 3);
                             buf[off] = h;
                             buf[TT * 8 + off] = f - h;
                         }
-                    }
-                } else {
-                    // duplicate / unsorted / long rows: per chunk, sum the counts per slot
-                    for (int c = 1; c < 17; ++c) {
-                        if (!((mask >> c) & 1u)) continue;
-                        advance_to(c);
+                        ep += n_c;
+                    } else {
+                        // duplicate / unsorted / long rows: sum the counts per slot
                         uint32_t acc[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
                         for (int idx = 0; idx < E.cnt; ++idx) {
                             const uint32_t en = __ldg(J.entries + E.first + idx);
@@ -661,8 +628,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
                         }
                         put_chunk(buf, row, v);
                     }
+                    TPT_BEGIN(p_p);
+                    hand_over(b);
+                    TPT_END(1, p_p);
                 }
-                advance_to(17);  // zero rows of the remaining chunks, hand over the last
             } else {
                 // predict / dense: chunk values loaded kAhead chunks in advance
                 constexpr int kAhead = 4;
@@ -733,32 +702,84 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
             wait_acq(mb + MB_D2F + grp, ph);
             TPT_END(4, e_w2);
             TPT_BEGIN(e_2);
-            for (int c = 0; c < 7; ++c)
-                epi_chunk<H2>(tq + TD2 + 8 * c, S + 8 * c, S + A3LO + 8 * c, c, sm + NB2,
-                              mb + MB_A3R + 7 * grp + c);
-            __syncwarp();
-            if (lane == 0) mb_arrive(mb + MB_D2FREE);  // D2 read (tcgen05.wait::ld done)
-            TPT_END(5, e_2);
-            TPT_BEGIN(e_w3);
-            wait_acq(mb + MB_D3F + grp, ph);
-            TPT_END(6, e_w3);
-            TPT_BEGIN(e_3);
-            for (int c = 0; c < 4; ++c)
-                epi_chunk<H3>(S + TD3 + 8 * c, S + TD3 + 8 * c, S + A4LO + 8 * c, c, sm + NB3,
-                              mb + MB_A4R + 4 * grp + c);
-            TPT_END(7, e_3);
-            TPT_BEGIN(e_w4);
-            wait_acq(mb + MB_D4F + grp, ph);
-            TPT_END(8, e_w4);
-            TPT_BEGIN(e_4);
-            float raw[8];
-            {
+            // L2 outputs: sigmoid of D2 into registers; D2 is then free for the next tile
+            float h2[56];
+#pragma unroll
+            for (int c = 0; c < 7; ++c) {
                 float v[8];
-                tc::ld8(S + TD4, v);
+                tc::ld8(tq + TD2 + 8 * c, v);
                 tc::wait_ld();
 #pragma unroll
+                for (int j = 0; j < 8; j += 2) {
+                    const float2 z = ffma2(make_float2(v[j], v[j + 1]), make_float2(kNL2E, kNL2E),
+                                           make_float2(sm[NB2 + 8 * c + j], sm[NB2 + 8 * c + j + 1]));
+                    float e0, e1, r0, r1;
+                    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e0) : "f"(z.x));
+                    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e1) : "f"(z.y));
+                    const float2 d = fadd2(make_float2(1.f, 1.f), make_float2(e0, e1));
+                    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r0) : "f"(d.x));
+                    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r1) : "f"(d.y));
+                    h2[8 * c + j] = r0;
+                    h2[8 * c + j + 1] = r1;
+                }
+            }
+            tc::fence_before();
+            __syncwarp();
+            if (lane == 0) mb_arrive(mb + MB_D2FREE);
+            TPT_END(5, e_2);
+            TPT_BEGIN(e_3);
+            // L3 (50 -> 25, sigmoid) and L4 (25 -> 7) on the FMA pipe, FP32, neuron
+            // pairs per FFMA2, weights as shared-memory broadcasts
+            float raw[8];
+            {
+                float2 a3[14];
+#pragma unroll
+                for (int u = 0; u < 14; ++u) a3[u] = make_float2(0.f, 0.f);
+#pragma unroll 5
+                for (int kk = 0; kk < H2; ++kk) {
+                    const float4* wr = reinterpret_cast<const float4*>(sm + W3T + kk * 28);
+                    const float2 x2 = make_float2(h2[kk], h2[kk]);
+#pragma unroll
+                    for (int u = 0; u < 7; ++u) {
+                        const float4 w4 = wr[u];
+                        a3[2 * u] = ffma2(x2, make_float2(w4.x, w4.y), a3[2 * u]);
+                        a3[2 * u + 1] = ffma2(x2, make_float2(w4.z, w4.w), a3[2 * u + 1]);
+                    }
+                }
+                float h3[28];
+#pragma unroll
+                for (int u = 0; u < 14; ++u) {
+                    const float2 z = ffma2(a3[u], make_float2(kNL2E, kNL2E),
+                                           make_float2(sm[NB3 + 2 * u], sm[NB3 + 2 * u + 1]));
+                    float e0, e1, r0, r1;
+                    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e0) : "f"(z.x));
+                    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e1) : "f"(z.y));
+                    const float2 d = fadd2(make_float2(1.f, 1.f), make_float2(e0, e1));
+                    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r0) : "f"(d.x));
+                    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r1) : "f"(d.y));
+                    h3[2 * u] = r0;
+                    h3[2 * u + 1] = r1;
+                }
+                float2 a4[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                                make_float2(0.f, 0.f)};
+#pragma unroll
+                for (int kk = 0; kk < H3; ++kk) {
+                    const float4* wr = reinterpret_cast<const float4*>(sm + W4T + kk * 8);
+                    const float2 x2 = make_float2(h3[kk], h3[kk]);
+                    const float4 w0 = wr[0], w1 = wr[1];
+                    a4[0] = ffma2(x2, make_float2(w0.x, w0.y), a4[0]);
+                    a4[1] = ffma2(x2, make_float2(w0.z, w0.w), a4[1]);
+                    a4[2] = ffma2(x2, make_float2(w1.x, w1.y), a4[2]);
+                    a4[3] = ffma2(x2, make_float2(w1.z, w1.w), a4[3]);
+                }
+                const float z4[8] = {a4[0].x, a4[0].y, a4[1].x, a4[1].y, a4[2].x, a4[2].y, a4[3].x, a4[3].y};
+#pragma unroll
                 for (int j = 0; j < 7; ++j)
-                    raw[j] = fmaf(v[j] + sm[B4 + j], sm[S_STATS + 8 + j], sm[S_STATS + j]);
+                    raw[j] = fmaf(z4[j] + sm[B4 + j], sm[S_STATS + 8 + j], sm[S_STATS + j]);
+            }
+            TPT_END(7, e_3);
+            TPT_BEGIN(e_4);
+            {
                 const uint32_t bm = *reinterpret_cast<volatile uint32_t*>(misc + 2 + 4 * grp + q);
                 if (bm) {  // kernels predicted on the FMA pipe by the producer
                     float w[8];
@@ -825,10 +846,12 @@ __global__ void tc_repack_kernel(const float* __restrict__ master, float* __rest
         put(W2H, W2L, f / 100, f % 100, K2, master[e]);
     } else if (e < MW4) {
         const int f = e - MW3;
-        put(W3H, W3L, f / 50, f % 50, K3, master[e]);
+        pk[W3T + (f % 50) * 28 + f / 50] = master[e];
+        if (!isfinite(master[e])) atomicAdd(reinterpret_cast<int*>(pk + FLAG), 1);
     } else if (e < MB1) {
         const int f = e - MW4;
-        put(W4H, W4L, f / 25, f % 25, K4, master[e]);
+        pk[W4T + (f % 25) * 8 + f / 25] = master[e];
+        if (!isfinite(master[e])) atomicAdd(reinterpret_cast<int*>(pk + FLAG), 1);
     } else if (e < MB2) {
         pk[NB1 + e - MB1] = master[e] * kNL2E;
     } else if (e < MB3) {

@@ -16,6 +16,7 @@ L.dso_debug_phase_cycles.argtypes = [C.c_void_p, C.c_int]
 names = ["c.wait_full", "c.L1", "c.L1_epi", "c.L2", "c.L2_epi", "c.L3", "c.L3_epi", "c.L4",
          "p.wait_ready", "p.results", "p.features", "c.sweep", "", "", "", ""]
 ctx = Context(0)
+ctx.set_option("mlp_engine", 0)  # the FMA-pipe kernel's phases
 n = 1 << 22
 for mode in ("pipeline_csr", "pipeline", "predict"):
     ctx.set_domain(config_domain("c3"))

@@ -19,6 +19,7 @@ names = ["p.wait_XEMPTY", "p.put+arrive", "e.wait_D1", "e.epi1", "e.wait_D2", "e
          "e.epi3", "e.wait_D4", "e.epi4+sweep", "m.L1(waits X)", "m.L2", "m.L3", "m.L4",
          "p.prep", "p.chunks", "m.wait_XFULL"]
 ctx = Context(0)
+ctx.set_option("mlp_engine", 1)
 n = 1 << 22
 for mode in ("pipeline_csr", "predict", "pipeline"):
     ctx.set_domain(config_domain("c3"))

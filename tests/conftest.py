@@ -65,4 +65,4 @@ def engine(request, ctx):
     tcgen05 3xTF32 kernel (1); restores the default afterwards."""
     ctx.set_option("mlp_engine", request.param)
     yield request.param
-    ctx.set_option("mlp_engine", 0)
+    ctx.set_option("mlp_engine", 2)

@@ -76,7 +76,7 @@ def _both(ctx, fn):
             r = fn()
             out.append({k: (v.cpu().numpy() if hasattr(v, "cpu") else v) for k, v in r.items()})
         finally:
-            ctx.set_option("mlp_engine", 0)
+            ctx.set_option("mlp_engine", 2)
     return out
 
 
@@ -157,4 +157,4 @@ def test_tc_after_device_repack(ctx):
 def test_tc_engine_option_errors(ctx):
     from paper_2407_13096_b200 import DsoError
     with pytest.raises(DsoError):
-        ctx.set_option("mlp_engine", 2)
+        ctx.set_option("mlp_engine", 3)
