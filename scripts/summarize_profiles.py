@@ -26,8 +26,30 @@ KEYS = ["Kernel Name", "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__
         "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
         "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "smsp__inst_executed.sum",
         "launch__registers_per_thread", "launch__block_size", "launch__grid_size",
-        "launch__shared_mem_per_block_dynamic"]
+        "launch__shared_mem_per_block_dynamic",
+        "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed"]
 summary = {}
+def dump_metrics(rep, out):
+    txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
+    rows = list(csv.reader(io.StringIO(txt)))
+    if len(rows) < 3:
+        return None, None
+    hdr, units, vals = rows[0], rows[1], rows[2]
+    d, u = dict(zip(hdr, vals)), dict(zip(hdr, units))
+    with open(out, "w") as f:
+        f.write(f"# ncu --set full --clock-control none capture of {rep}\n")
+        for k in KEYS:
+            if k in d:
+                f.write(f"{k}\t{d.get(k)}\t{u.get(k, '')}\n")
+    return d, u
+
+
+# the FMA-pipe engine's kernel on the same workload (bench --engine ffma)
+rp = os.path.join(src, "prof_pipeline_ffma.ncu-rep")
+if os.path.exists(rp):
+    dump_metrics(rp, os.path.join(dst, "ncu_ws_kernel_ffma_metrics.txt"))
 rep = os.path.join(src, "prof_pipeline.ncu-rep")
 if os.path.exists(rep):
     txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
@@ -36,7 +58,7 @@ if os.path.exists(rep):
     hdr, units, vals = rows[0], rows[1], rows[2]
     d = dict(zip(hdr, vals))
     u = dict(zip(hdr, units))
-    with open(os.path.join(dst, "ncu_ws_kernel_metrics.txt"), "w") as f:
+    with open(os.path.join(dst, "ncu_c3_kernel_metrics.txt"), "w") as f:
         f.write(f"# ncu --set full --clock-control none capture of {rep}\n")
         for k in KEYS:
             f.write(f"{k}\t{d.get(k)}\t{u.get(k, '')}\n")
@@ -47,11 +69,11 @@ if os.path.exists(rep):
     summary["c3"] = {"kernel": d["Kernel Name"], "kernels_per_launch": n_kernels,
                      "dram_bytes_per_launch": mb * scale,
                      "dram_bytes_per_kernel": mb * scale / n_kernels,
-                     "source": f"{dst}/ncu_ws_kernel_metrics.txt (ncu --set full, "
+                     "source": f"{dst}/ncu_c3_kernel_metrics.txt (ncu --set full, "
                                f"{n_kernels} kernels, CSR input)"}
     lines = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source",
                             "cuda,sass"], capture_output=True, text=True).stdout
-    with open(os.path.join(dst, "ncu_ws_kernel_source_hot_lines.txt"), "w") as f:
+    with open(os.path.join(dst, "ncu_c3_kernel_source_hot_lines.txt"), "w") as f:
         out = subprocess.run([sys.executable, "scripts/ncu_lines.py", rep, "40"],
                              capture_output=True, text=True).stdout
         f.write(out)
@@ -116,13 +138,14 @@ if os.path.exists(lc):
         for k, (c, t) in sorted(agg.items(), key=lambda x: -x[1][1]):
             f.write(f"{c}\t{t / 1e6:.3f}\t{k}\n")
     shutil.copy(lc, os.path.join(dst, "launches.csv"))
-for name in ("bench", "bench_c2", "bench_c4", "bench_c5"):
+for name in ("bench", "bench_c2", "bench_c4", "bench_c5", "bench_ffma", "bench_dense"):
     p = os.path.join(src, name + ".log")
     if os.path.exists(p):
         line = open(p).readline().strip()
         if line.startswith("{"):
             open(os.path.join(dst, name + ".json"), "w").write(line + "\n")
-for extra in ("pytest_gpu.log", "memcheck.log", "smoke.log", "nvidia-smi.txt"):
+for extra in ("pytest_gpu.log", "memcheck.log", "smoke.log", "nvidia-smi.txt", "tc_phase.txt",
+              "phase_timing.txt"):
     p = os.path.join(src, extra)
     if os.path.exists(p):
         shutil.copy(p, os.path.join(dst, extra))
