@@ -1323,7 +1323,9 @@ cudaError_t model_upload(Ctx& cx, const double* W, const double* b) {
         bad += std::isfinite(w) ? 0 : 1;
     };
     for (int n = 0; n < 100; ++n)
-        for (int k = 0; k < 134; ++k) put(tce::W1H, tce::W1L, n, k, tce::K1, W[MW1 + n * 134 + k]);
+        for (int k = 0; k < 134; ++k)
+            put(tce::W1H, tce::W1L, n, k < 8 ? k : 8 + tce::tc_pos(k - 8), tce::K1,
+                W[MW1 + n * 134 + k]);
     for (int n = 0; n < 50; ++n)
         for (int k = 0; k < 100; ++k) put(tce::W2H, tce::W2L, n, k, tce::K2, W[MW2 + n * 100 + k]);
     for (int n = 0; n < 25; ++n)

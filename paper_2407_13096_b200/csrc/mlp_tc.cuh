@@ -63,6 +63,27 @@ constexpr int kModel = FLAG + 4;
 __host__ __device__ __forceinline__ int cm(int n, int k, int K) {
     return ((n >> 3) * (K >> 2) + (k >> 2)) * 32 + (n & 7) * 4 + (k & 3);
 }
+// Layer-1 K order of the count slots: the 24 categories every PTX kernel tends to
+// list first (the set the reference's own synthetic kernels fill,
+// ptx_features.cpp:18-49 / sim_harness.cpp:70-95: add mul fma setp mov ld st cvt
+// bra ret bar | s32 u32 u64 f32 f64 b32 b64 | reg const global local param
+// shared), then the other 102 in slot order.  A fixed relabelling of the K axis
+// (weights packed to match), so the 8-column chunks of layer 1 that a tile leaves
+// all-zero — skipped exactly — are as many as possible: 3 count chunks instead of
+// up to 16 for such kernels.
+__host__ __device__ __forceinline__ int common_slot(int i) {
+    constexpr int kCommon[24] = {0,   4,   37,  39,  51,  54,  56,  61,  71,  74,  76,  103,
+                                 107, 108, 111, 112, 115, 116, 118, 120, 121, 122, 123, 124};
+    return kCommon[i];
+}
+__host__ __device__ inline int tc_pos(int slot) {  // slot -> position on the K axis (- 8)
+    int below = 0;
+    for (int i = 0; i < 24; ++i) {
+        if (common_slot(i) == slot) return i;
+        below += common_slot(i) < slot ? 1 : 0;
+    }
+    return 24 + slot - below;
+}
 // shared memory (floats)
 constexpr int kRing = 2;                     // X chunk buffers
 constexpr int kChunkF = 2 * TT * 8;          // hi [128][8] + lo [128][8] (core-matrix layout)
@@ -73,10 +94,16 @@ constexpr int S_RING = S_STATS + 16;
 constexpr int S_ELIST = S_RING + kRing * kChunkF;
 constexpr int S_ECOL = S_ELIST + 24 * TT;
 constexpr int S_MISC = S_ECOL + 24 * TT / 4;  // u32: [0..1] chunk masks, [2..9] slow rows, [10..17] partial masks
-constexpr int S_MBAR = S_MISC + 24;
+constexpr int S_PERM = S_MISC + 24;  // u8 pos_of[128] (slot -> K position), slot_at[128]
+// CSR: the tile's entries, bulk-copied from global a tile ahead (when the tile's
+// entry range is 16-byte aligned and fits), [0] base entry index, [2] staged flag
+constexpr int kStageEnt = 24 * TT;
+constexpr int S_ESTAGE = S_PERM + 64;
+constexpr int S_EMETA = S_ESTAGE + kStageEnt;
+constexpr int S_MBAR = S_EMETA + 4;
 enum {
     MB_XFULL = 0, MB_XEMPTY = 3, MB_D1F = 6, MB_A2R = 8, MB_D2F = 34, MB_D2FREE = 36,
-    MB_SLOWFREE = 37, kMbars = 39
+    MB_SLOWFREE = 37, MB_ESTAGE = 39, kMbars = 40
 };
 constexpr int S_TSLOT = S_MBAR + 2 * kMbars;
 constexpr int S_TABLES = (S_TSLOT + 4 + 3) & ~3;  // core4[nc], mem2[nm], level pairs
@@ -171,6 +198,7 @@ __device__ __forceinline__ void epi_chunk(uint32_t src, uint32_t dst_hi, uint32_
 // sequential sums, the same sigmoid as the epilogues.
 __device__ __noinline__ void tc_forward_x(const float* sm, const float* x, float* raw) {
     float h1[H1], h2[H2], h3[H3];
+    const uint8_t* pos_of = reinterpret_cast<const uint8_t*>(sm + S_PERM);
     auto w = [&](int hi, int lo, int n, int kk, int K) {
         return sm[hi + cm(n, kk, K)] + sm[lo + cm(n, kk, K)];
     };
@@ -182,7 +210,8 @@ __device__ __noinline__ void tc_forward_x(const float* sm, const float* x, float
     };
     for (int n = 0; n < H1; ++n) {
         float z = 0.f;
-        for (int c = 0; c < DSO_FUSED_ROWS; ++c) z = fmaf(w(W1H, W1L, n, c, K1), x[c], z);
+        for (int c = 0; c < DSO_FUSED_ROWS; ++c)
+            z = fmaf(w(W1H, W1L, n, c < 8 ? c : 8 + pos_of[c - 8], K1), x[c], z);
         h1[n] = sig(z, sm[NB1 + n]);
     }
     for (int n = 0; n < H2; ++n) {
@@ -301,6 +330,12 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
             sm[S_STATS + 8 + tid] = stats.std_[tid];
         }
         if (tid < 24) misc[tid] = 0u;
+        if (tid < DSO_COUNT_ROWS) {
+            uint8_t* pm = reinterpret_cast<uint8_t*>(sm + S_PERM);
+            const int ps = tc_pos(tid);
+            pm[tid] = (uint8_t)ps;
+            pm[128 + ps] = (uint8_t)tid;
+        }
         if (PIPE) {
             float4* sc = reinterpret_cast<float4*>(sm + S_TABLES);
             float2* smm = reinterpret_cast<float2*>(sm + S_TABLES + 4 * J.nc);
@@ -322,6 +357,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
                 for (int c = 0; c < 13; ++c) mb_init(mb + MB_A2R + 13 * g + c, 4);
             }
             mb_init(mb + MB_D2FREE, 4);
+            mb_init(mb + MB_ESTAGE, 1);
             asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         }
         if (warp == MMA_WARP) tc::tmem_alloc<512>(tslot);
@@ -417,11 +453,46 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     } else if (warp < 4) {
         // ================================ producers ================================
         asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegProd));
+        const uint8_t* pos_of = reinterpret_cast<const uint8_t*>(sm + S_PERM);
+        const uint8_t* slot_at = pos_of + 128;
         const int row = tid;  // kernel of the tile; TMEM lane quadrant = warp
         const uint32_t tq = tbase + ((uint32_t)(32 * warp) << 16);
         uint32_t g = 0;  // ring chunks produced
         Entries E;
         if (MODE == MODE_CSR && my_tiles > 0) tc_csr_prefetch(J, t0_of(0) + row, E);
+        // CSR: thread 0 bulk-copies tile i's entry range into shared memory (one
+        // cp.async.bulk, completing on MB_ESTAGE) when it is 16-byte aligned and fits;
+        // otherwise it only arrives, and the kernels read their entries from global
+        auto stage = [&](int64_t i) {
+            if (MODE != MODE_CSR || tid != 0) return;
+            const int64_t t0i = t0_of(i), t1i = t0i + TT < J.n ? t0i + TT : J.n;
+            const uint64_t a = __ldg(J.row_ptr + t0i) - J.ent_base, b = __ldg(J.row_ptr + t1i) - J.ent_base;
+            const uint64_t bytes = (b - a) * 4;
+            const uint32_t* src = J.entries + a;
+            uint32_t* meta = reinterpret_cast<uint32_t*>(sm + S_EMETA);
+            const bool ok = bytes > 0 && bytes <= (uint64_t)kStageEnt * 4 && (bytes & 15) == 0 &&
+                            (reinterpret_cast<uintptr_t>(src) & 15) == 0;
+            meta[0] = (uint32_t)a;
+            meta[1] = (uint32_t)(a >> 32);
+            meta[2] = ok ? 1u : 0u;
+            const uint32_t bar = smem_u32(mb + MB_ESTAGE);
+            if (ok) {
+                // the buffer was last read through the generic proxy (the barrier before
+                // this call ordered every producer's reads); the bulk copy writes it
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                             "r"((uint32_t)bytes)
+                             : "memory");
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                        smem_u32(sm + S_ESTAGE)),
+                    "l"(src), "r"((uint32_t)bytes), "r"(bar)
+                    : "memory");
+            } else {
+                mb_arrive(mb + MB_ESTAGE);
+            }
+        };
+        if (my_tiles > 0) stage(0);
         for (int64_t t = 0; t < my_tiles; ++t) {
             const int64_t k = t0_of(t) + row;
             const int sl = (int)(t & 1);
@@ -445,22 +516,41 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
                 uint32_t t32[3] = {0u, 0u, 0u};
                 int prev = -1;
                 uint32_t en[kEnt];
-                load_entries(J.entries + E.first, E.cnt, en);
+                TPT_BEGIN(p_l);
+                mbar_wait(mb + MB_ESTAGE, (uint32_t)(t & 1));
+                {
+                    const uint32_t* meta = reinterpret_cast<const uint32_t*>(sm + S_EMETA);
+                    if (meta[2]) {  // staged: this kernel's entries from shared memory
+                        const uint64_t base = meta[0] | ((uint64_t)meta[1] << 32);
+                        const uint32_t* sp = reinterpret_cast<const uint32_t*>(sm + S_ESTAGE) +
+                                             (E.first - base);
+#pragma unroll
+                        for (int e = 0; e < kEnt; ++e) en[e] = e < E.cnt ? sp[e] : 0u;
+                    } else {
+                        load_entries(J.entries + E.first, E.cnt, en);
+                    }
+                }
+                // one branch-free pass: liveness, K column, category totals, chunk
+                // mask and counts per chunk (the column lookup done once per entry)
+                uint32_t colp[kEnt / 4];  // K columns, four per register (0 = dead entry)
+#pragma unroll
+                for (int e4 = 0; e4 < kEnt / 4; ++e4) colp[e4] = 0u;
 #pragma unroll
                 for (int e = 0; e < kEnt; ++e) {
                     const int slot = (int)(en[e] & 127u);
                     const uint32_t cnt = en[e] >> 7;
-                    if (e < E.cnt) {
-                        uns |= slot <= prev;
-                        prev = slot;
-                        if (slot < DSO_COUNT_ROWS) {
-                            const int cat = cat_of_row(slot);
-                            t32[0] += cat == 0 ? cnt : 0u;
-                            t32[1] += cat == 1 ? cnt : 0u;
-                            t32[2] += cat == 2 ? cnt : 0u;
-                            mask |= 1u << ((8 + slot) >> 3);
-                        }
-                    }
+                    const bool inrow = e < E.cnt;
+                    const bool live = inrow && slot < DSO_COUNT_ROWS;
+                    uns |= inrow && slot <= prev;
+                    prev = inrow ? slot : prev;
+                    const int col = 8 + pos_of[live ? slot : 0];
+                    const int cat = cat_of_row(slot);
+                    t32[0] += (live && cat == 0) ? cnt : 0u;
+                    t32[1] += (live && cat == 1) ? cnt : 0u;
+                    t32[2] += (live && cat == 2) ? cnt : 0u;
+                    mask |= live ? 1u << (col >> 3) : 0u;
+                    nib += live ? 1ull << (4 * ((col >> 3) - 1)) : 0ull;
+                    colp[e >> 2] |= (live ? (uint32_t)col : 0u) << (8 * (e & 3));
                 }
                 if (E.cnt > kEnt) {
                     uns = true;
@@ -472,13 +562,15 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
                             tot[0] += cat == 0 ? (en >> 7) : 0u;
                             tot[1] += cat == 1 ? (en >> 7) : 0u;
                             tot[2] += cat == 2 ? (en >> 7) : 0u;
-                            mask |= 1u << ((8 + slot) >> 3);
+                            mask |= 1u << ((8 + pos_of[slot]) >> 3);
                         }
                     }
                 }
 #pragma unroll
                 for (int c = 0; c < 3; ++c) tot[c] += t32[c];
                 cat_scales(tot, tf, rr);
+                TPT_END(16, p_l);
+                TPT_BEGIN(p_f);
                 // this kernel's entry list (fraction, column) in slot order, and how
                 // many entries fall in each 8-column chunk
                 float* el = sm + S_ELIST;
@@ -486,16 +578,16 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
                 int ne = 0;
 #pragma unroll
                 for (int e = 0; e < kEnt; ++e) {
-                    const int slot = (int)(en[e] & 127u);
-                    if (e < E.cnt && slot < DSO_COUNT_ROWS) {
-                        el[ne * TT + row] = norm_slot(en[e] >> 7, slot, tf, rr);
-                        ecl[ne * TT + row] = (uint8_t)(8 + slot);
-                        nib += 1ull << (4 * (((8 + slot) >> 3) - 1));
-                        ++ne;
+                    const uint32_t col = (colp[e >> 2] >> (8 * (e & 3))) & 0xFFu;
+                    if (col) {
+                        el[ne * TT + row] = norm_slot(en[e] >> 7, (int)(en[e] & 127u), tf, rr);
+                        ecl[ne * TT + row] = (uint8_t)col;
                     }
+                    ne += col ? 1 : 0;
                 }
 #pragma unroll
                 for (int j = 0; j < 8; ++j) bad |= !isfinite(E.dg[j]);
+                TPT_END(17, p_f);
             } else if (MODE == MODE_DENSE) {
                 uint64_t tot[3] = {0, 0, 0};
                 if (k < J.n) {
@@ -521,14 +613,16 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
             } else {
                 mask = 0x1FFFFu;
             }
+            TPT_BEGIN(p_m);
             // the tile's chunk mask (OR over the 128 kernels), published for the MMA
             // thread before the tile's first chunk
             {
                 const uint32_t wm = __reduce_or_sync(0xffffffffu, mask);
                 if (lane == 0) misc[10 + 4 * sl + warp] = wm;
-                bar_sync(1, kGroupT);
+                bar_sync(1, kGroupT);  // (also: every producer has read this tile's stage)
                 mask = misc[10 + 4 * sl] | misc[11 + 4 * sl] | misc[12 + 4 * sl] | misc[13 + 4 * sl];
                 if (tid == 0) misc[sl] = mask;
+                if (t + 1 < my_tiles) stage(t + 1);
             }
             // kernels with a non-finite feature: forward on the FMA pipe, into the
             // slot's spare TMEM columns (after the epilogue of tile t-2 read them);
@@ -566,8 +660,18 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
                 const uint32_t bm = __ballot_sync(0xffffffffu, bad);
                 if (lane == 0) misc[2 + 4 * sl + warp] = bm;
             };
+            TPT_END(18, p_m);
+            TPT_BEGIN(p_s);
             if (MODE == MODE_CSR) slow_block();
+            TPT_END(19, p_s);
             TPT_END(14, p_t);
+            // the next tile's entries into L2 while this tile's chunks are produced
+            // (its row extent, loaded at this tile's start, has arrived by now)
+            if (MODE == MODE_CSR && t + 1 < my_tiles && NE.cnt > 0) {
+                const uint32_t* ep = J.entries + NE.first;
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(ep));
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(ep + kEnt - 1));
+            }
             TPT_BEGIN(p_c);
             // ---- chunks -> ring ----------------------------------------------------
             auto hand_over = [&](int b) {  // the chunk in ring buffer b is complete
@@ -615,16 +719,18 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
                         uint32_t acc[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
                         for (int idx = 0; idx < E.cnt; ++idx) {
                             const uint32_t en = __ldg(J.entries + E.first + idx);
-                            const int col = 8 + (int)(en & 127u);
-                            if ((col >> 3) == c && col - 8 < DSO_COUNT_ROWS)
+                            const int slot = (int)(en & 127u);
+                            if (slot >= DSO_COUNT_ROWS) continue;
+                            const int col = 8 + pos_of[slot];
+                            if ((col >> 3) == c)
 #pragma unroll
                                 for (int j = 0; j < 8; ++j) acc[j] += (col & 7) == j ? (en >> 7) : 0u;
                         }
                         float v[8];
 #pragma unroll
                         for (int j = 0; j < 8; ++j) {
-                            const int r = 8 * c + j - 8;
-                            v[j] = (r < DSO_COUNT_ROWS) ? norm_slot(acc[j], r, tf, rr) : 0.f;
+                            const int p = 8 * c + j - 8;
+                            v[j] = (p < DSO_COUNT_ROWS) ? norm_slot(acc[j], slot_at[p], tf, rr) : 0.f;
                         }
                         put_chunk(buf, row, v);
                     }
@@ -642,13 +748,14 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
                         const int col = 8 * c + j;
                         float x = 0.f;
                         if (k < J.n && col < DSO_FUSED_ROWS) {
+                            const int sl8 = col < 8 ? col : 8 + slot_at[col - 8];  // feature row
                             if (MODE == MODE_PRED) {
-                                x = __ldg(J.fused + (int64_t)col * J.ld + k);
+                                x = __ldg(J.fused + (int64_t)sl8 * J.ld + k);
                             } else if (col < 8) {
                                 x = __ldg(J.dcgm + (int64_t)col * J.ld + k);
                             } else {
-                                const uint32_t cnt = __ldg(J.counts + (int64_t)(col - 8) * J.ld + k);
-                                x = norm_slot(cnt, col - 8, tf, rr);
+                                const uint32_t cnt = __ldg(J.counts + (int64_t)(sl8 - 8) * J.ld + k);
+                                x = norm_slot(cnt, sl8 - 8, tf, rr);
                             }
                         }
                         v[j] = x;
@@ -840,7 +947,8 @@ __global__ void tc_repack_kernel(const float* __restrict__ master, float* __rest
         if (!isfinite(w)) atomicAdd(reinterpret_cast<int*>(pk + FLAG), 1);
     };
     if (e < MW2) {
-        put(W1H, W1L, e / 134, e % 134, K1, master[e]);
+        const int c = e % 134;
+        put(W1H, W1L, e / 134, c < 8 ? c : 8 + tc_pos(c - 8), K1, master[e]);
     } else if (e < MW3) {
         const int f = e - MW2;
         put(W2H, W2L, f / 100, f % 100, K2, master[e]);
