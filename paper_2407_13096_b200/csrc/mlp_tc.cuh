@@ -533,6 +533,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
                 // one branch-free pass: liveness, K column, category totals, chunk
                 // mask and counts per chunk (the column lookup done once per entry)
                 uint32_t colp[kEnt / 4];  // K columns, four per register (0 = dead entry)
+                int ncommon = 0;          // live entries in the common-category columns
 #pragma unroll
                 for (int e4 = 0; e4 < kEnt / 4; ++e4) colp[e4] = 0u;
 #pragma unroll
@@ -551,6 +552,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
                     mask |= live ? 1u << (col >> 3) : 0u;
                     nib += live ? 1ull << (4 * ((col >> 3) - 1)) : 0ull;
                     colp[e >> 2] |= (live ? (uint32_t)col : 0u) << (8 * (e & 3));
+                    ncommon += (live && col < 32) ? 1 : 0;
                 }
                 if (E.cnt > kEnt) {
                     uns = true;
@@ -573,17 +575,21 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
                 TPT_BEGIN(p_f);
                 // this kernel's entry list (fraction, column) in slot order, and how
                 // many entries fall in each 8-column chunk
+                // list order = K order: the common categories (columns < 32, increasing
+                // with the slot) first, then the others (also increasing with the slot)
                 float* el = sm + S_ELIST;
                 uint8_t* ecl = reinterpret_cast<uint8_t*>(sm + S_ECOL);
-                int ne = 0;
+                int nlo = 0, nhi = ncommon;
 #pragma unroll
                 for (int e = 0; e < kEnt; ++e) {
                     const uint32_t col = (colp[e >> 2] >> (8 * (e & 3))) & 0xFFu;
+                    const int at = col < 32u ? nlo : nhi;
                     if (col) {
-                        el[ne * TT + row] = norm_slot(en[e] >> 7, (int)(en[e] & 127u), tf, rr);
-                        ecl[ne * TT + row] = (uint8_t)col;
+                        el[at * TT + row] = norm_slot(en[e] >> 7, (int)(en[e] & 127u), tf, rr);
+                        ecl[at * TT + row] = (uint8_t)col;
                     }
-                    ne += col ? 1 : 0;
+                    nlo += (col && col < 32u) ? 1 : 0;
+                    nhi += (col >= 32u) ? 1 : 0;
                 }
 #pragma unroll
                 for (int j = 0; j < 8; ++j) bad |= !isfinite(E.dg[j]);

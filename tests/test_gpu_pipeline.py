@@ -183,6 +183,30 @@ def test_pipeline_csr_irregular(ctx, port):
     del ent_pad
 
 
+def test_pipeline_csr_sorted_random_slots(ctx, port):
+    """Slot-sorted entries over all 126 categories (each engine's fast path, incl.
+    the tcgen05 engine's reordered layer-1 columns), equal to the dense pipeline."""
+    dom = config_domain("c3")
+    ctx.set_domain(dom)
+    ctx.set_model(stats_model(port))
+    rng = np.random.default_rng(8)
+    n = 4096 + 5
+    counts = np.zeros((n, 126), np.uint32)
+    for k in range(n):
+        nnz = int(rng.integers(1, 25))
+        slots = rng.choice(126, size=nnz, replace=False)
+        counts[k, slots] = rng.integers(1, 300_000, size=nnz)
+    dcgm = rng.uniform(0, 1, size=(n, 8)).astype(np.float32)
+    rp, ent = csr_from_dense(counts)
+    dc_t = torch.from_numpy(np.ascontiguousarray(dcgm.T)).cuda()
+    b = ctx.pipeline_csr(torch.from_numpy(rp).cuda(), torch.from_numpy(ent.view(np.int32)).cuda(),
+                         dc_t, 0.5, want_params=True)
+    a = ctx.pipeline(torch.from_numpy(np.ascontiguousarray(counts.T).view(np.int32)).cuda(), dc_t,
+                     0.5, want_params=True)
+    for f in ("idx", "cost", "energy", "time", "params", "clamped"):
+        np.testing.assert_array_equal(a[f].cpu().numpy(), b[f].cpu().numpy())
+
+
 def test_pipeline_csr_host_large(ctx, port):
     dom = config_domain("c3")
     ctx.set_domain(dom)
