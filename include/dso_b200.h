@@ -72,7 +72,11 @@ int64_t dso_launch_count(const dso_ctx* ctx);
 /* Tuning / verification switches (no reference counterpart; results never
  * depend on them).  key "fast_sweep": 1 (default) lets the FP32 sweeps use the
  * group-minimum argmin (bit-identical, see sweep_core.cuh), 0 forces the
- * pair-by-pair lexicographic scan.  Unknown key -> InvalidArgument. */
+ * pair-by-pair lexicographic scan.  key "mlp_engine": the predictor engine of
+ * dso_predict / dso_pipeline / dso_pipeline_csr: 0 = FP32 FMA-pipe kernel,
+ * 1 = tcgen05 3xTF32 tensor-core kernel, 2 = auto (default: tensor cores for
+ * predict and CSR input, FMA pipe for dense counts).  Unknown key or value ->
+ * InvalidArgument. */
 int32_t dso_set_option(dso_ctx* ctx, const char* key, int64_t value);
 
 /* ---- domain: replaces the DvfsDomain argument + validate(DvfsDomain) ------
