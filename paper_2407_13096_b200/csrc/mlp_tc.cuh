@@ -579,17 +579,36 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
                 // with the slot) first, then the others (also increasing with the slot)
                 float* el = sm + S_ELIST;
                 uint8_t* ecl = reinterpret_cast<uint8_t*>(sm + S_ECOL);
-                int nlo = 0, nhi = ncommon;
+                int nlive = 0;
 #pragma unroll
-                for (int e = 0; e < kEnt; ++e) {
-                    const uint32_t col = (colp[e >> 2] >> (8 * (e & 3))) & 0xFFu;
-                    const int at = col < 32u ? nlo : nhi;
-                    if (col) {
-                        el[at * TT + row] = norm_slot(en[e] >> 7, (int)(en[e] & 127u), tf, rr);
-                        ecl[at * TT + row] = (uint8_t)col;
+                for (int e4 = 0; e4 < kEnt / 4; ++e4)
+                    nlive += (colp[e4] & 0xFFu ? 1 : 0) + (colp[e4] & 0xFF00u ? 1 : 0) +
+                             (colp[e4] & 0xFF0000u ? 1 : 0) + (colp[e4] & 0xFF000000u ? 1 : 0);
+                if (ncommon == nlive) {
+                    // only common categories: slot order is already K order
+                    int ne = 0;
+#pragma unroll
+                    for (int e = 0; e < kEnt; ++e) {
+                        const uint32_t col = (colp[e >> 2] >> (8 * (e & 3))) & 0xFFu;
+                        if (col) {
+                            el[ne * TT + row] = norm_slot(en[e] >> 7, (int)(en[e] & 127u), tf, rr);
+                            ecl[ne * TT + row] = (uint8_t)col;
+                        }
+                        ne += col ? 1 : 0;
                     }
-                    nlo += (col && col < 32u) ? 1 : 0;
-                    nhi += (col >= 32u) ? 1 : 0;
+                } else {
+                    int nlo = 0, nhi = ncommon;
+#pragma unroll
+                    for (int e = 0; e < kEnt; ++e) {
+                        const uint32_t col = (colp[e >> 2] >> (8 * (e & 3))) & 0xFFu;
+                        const int at = col < 32u ? nlo : nhi;
+                        if (col) {
+                            el[at * TT + row] = norm_slot(en[e] >> 7, (int)(en[e] & 127u), tf, rr);
+                            ecl[at * TT + row] = (uint8_t)col;
+                        }
+                        nlo += (col && col < 32u) ? 1 : 0;
+                        nhi += (col >= 32u) ? 1 : 0;
+                    }
                 }
 #pragma unroll
                 for (int j = 0; j < 8; ++j) bad |= !isfinite(E.dg[j]);
