@@ -158,3 +158,17 @@ def test_tc_engine_option_errors(ctx):
     from paper_2407_13096_b200 import DsoError
     with pytest.raises(DsoError):
         ctx.set_option("mlp_engine", 3)
+
+
+def test_tc_large_domain_falls_back(ctx):
+    """A domain whose level tables do not fit next to the split weights (nc = 600)
+    runs the FMA-pipe kernel under mlp_engine = 1: identical to engine 0."""
+    from paper_2407_13096_b200 import linear_domain
+    ctx.set_domain(linear_domain(600, 4))
+    m = _model()
+    ctx.set_model(m)
+    g = ctx.gen_synthetic_csr(3000, root=9)
+    a, b = _both(ctx, lambda: ctx.pipeline_csr(g["row_ptr"], g["entries"], g["dcgm"], 0.8,
+                                               want_params=True))
+    for f in ("idx", "cost", "energy", "time", "params", "clamped"):
+        np.testing.assert_array_equal(a[f], b[f])
