@@ -286,6 +286,19 @@ __device__ __forceinline__ void cat_scales(const uint64_t (&tot)[3], float (&tf)
         }
     }
 }
+// normalize_count without the wide-total branch: valid for tf >= 0 (a zero
+// total has only zero counts: 0 * 0 -> 0); kernels with a total >= 2^24 take
+// the general path
+__device__ __forceinline__ float norm_fast(uint32_t c, int slot, const float (&tf)[3],
+                                           const float (&rr)[3]) {
+    const int cat = cat_of_row(slot);
+    const float t = cat == 0 ? tf[0] : (cat == 1 ? tf[1] : tf[2]);
+    const float r = cat == 0 ? rr[0] : (cat == 1 ? rr[1] : rr[2]);
+    const float cf = (__int_as_float(0x4B000000u | (c & 0x7FFFFFu)) - 8388608.f) +
+                     ((c & 0x800000u) ? 8388608.f : 0.f);
+    const float qq = __fmul_rn(cf, r);
+    return fmaf(fmaf(-qq, t, cf), r, qq);
+}
 __device__ __forceinline__ float norm_slot(uint32_t cnt, int slot, const float (&tf)[3],
                                            const float (&rr)[3]) {
     const int cat = cat_of_row(slot);
@@ -571,6 +584,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
 #pragma unroll
                 for (int c = 0; c < 3; ++c) tot[c] += t32[c];
                 cat_scales(tot, tf, rr);
+                uns |= tf[0] < 0.f || tf[1] < 0.f || tf[2] < 0.f;  // a total >= 2^24
                 TPT_END(16, p_l);
                 TPT_BEGIN(p_f);
                 // this kernel's entry list (fraction, column) in slot order, and how
@@ -591,7 +605,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
                     for (int e = 0; e < kEnt; ++e) {
                         const uint32_t col = (colp[e >> 2] >> (8 * (e & 3))) & 0xFFu;
                         if (col) {
-                            el[ne * TT + row] = norm_slot(en[e] >> 7, (int)(en[e] & 127u), tf, rr);
+                            el[ne * TT + row] = norm_fast(en[e] >> 7, (int)(en[e] & 127u), tf, rr);
                             ecl[ne * TT + row] = (uint8_t)col;
                         }
                         ne += col ? 1 : 0;
@@ -603,7 +617,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
                         const uint32_t col = (colp[e >> 2] >> (8 * (e & 3))) & 0xFFu;
                         const int at = col < 32u ? nlo : nhi;
                         if (col) {
-                            el[at * TT + row] = norm_slot(en[e] >> 7, (int)(en[e] & 127u), tf, rr);
+                            el[at * TT + row] = norm_fast(en[e] >> 7, (int)(en[e] & 127u), tf, rr);
                             ecl[at * TT + row] = (uint8_t)col;
                         }
                         nlo += (col && col < 32u) ? 1 : 0;
