@@ -26,9 +26,8 @@
 // The model (weights ~100 KB) is staged once per CTA; nothing between a
 // kernel's input bytes and its 16 result bytes touches HBM.
 //
-// Tensor cores are not used: the layer widths are small and TF32 products
-// cannot meet the 1e-5 relative contract on the predicted parameters without
-// 3xTF32 splitting.
+// This is the FMA-pipe engine.  The tcgen05 engine (3xTF32 MMAs, TMEM) is in
+// mlp_tc.cuh; launch_ws picks the engine (dso_set_option "mlp_engine").
 #include <math.h>
 
 #include <cmath>

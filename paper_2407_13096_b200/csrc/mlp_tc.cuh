@@ -2,34 +2,40 @@
 // fused with the feature stage and the grid sweep.  Included by mlp.cu inside
 // its anonymous namespace (shares Job, Stats, the sweep and output helpers).
 //
-// Precision: every layer is a 3xTF32 product, D = Ah.Bh + Ah.Bl + Al.Bh with
+// Precision: layers 1-2 are 3xTF32 products, D = Ah.Bh + Ah.Bl + Al.Bh with
 // Xh = rna_tf32(X), Xl = X - Xh for activations and weights alike (~22
-// mantissa bits per product, FP32 accumulation in TMEM), which keeps the
-// predicted parameters inside the 1e-5 relative contract (
-// tests/test_gpu_tc.py, test_gpu_mlp.py run both engines).
+// mantissa bits per product, FP32 accumulation in TMEM); layers 3-4 run in
+// FP32 on the FMA pipe.  Inside the 1e-5 relative contract on the predicted
+// parameters (tests/test_gpu_tc.py, and test_gpu_mlp.py /
+// test_gpu_pipeline.py run on both engines).
 //
-// Execution model — one persistent CTA per SM, 13 warps, tiles of 128 kernels
-// (the MMA M: TMEM lane m = kernel m of the tile), two tiles in flight:
+// Execution model — one persistent CTA per SM, 13 working warps (16 launched:
+// setmaxnreg moves the idle warps' registers to the producers and epilogues),
+// tiles of 128 kernels (the MMA M: TMEM lane m = kernel m of the tile), two
+// tiles in flight:
 //   * warps 0..3, PRODUCERS (thread = kernel): the feature stage of each tile
-//     (CSR entries / dense counts -> per-category fractions, or fused input),
-//     split hi/lo and written 8 columns at a time into a 3-deep ring of
+//     (CSR entries -> exact per-category fractions in a per-kernel list in
+//     layer-1 K order; dense counts or fused input loaded a few chunks ahead),
+//     split hi/lo and written 8 columns at a time into a 2-deep ring of
 //     shared-memory chunks in the UMMA core-matrix layout — the L1 A operand.
 //     CSR tiles skip the 8-column chunks no kernel of the tile touches (their
-//     products are exact zeros);
+//     products are exact zeros); the K axis puts the 24 common PTX categories
+//     first (tc_pos) so typical kernels touch 4 of 17 chunks;
 //   * warp 12, lane 0: the MMA ISSUER.  L1 (N 112 x K 136) reads A from the
-//     ring (SS), L2 (64 x 104), L3 (32 x 56), L4 (16 x 32) read A from TMEM
-//     (TS); each k-step is three kind::tf32 MMAs and waits only for its own
-//     8-column chunk, so a layer runs while the previous epilogue still
-//     produces later chunks.  Order: L1(t+1), then L2..L4(t);
+//     ring (SS), L2 (64 x 104) reads A from TMEM (TS); each k-step is three
+//     kind::tf32 MMAs issued as soon as its 8-column chunk is ready (an event
+//     loop over non-blocking mbarrier tests: L1 of the next tile interleaved
+//     with L2 of the current one); tcgen05.commit frees ring buffers and
+//     signals finished layers;
 //   * warps 4..7 / 8..11, two EPILOGUE GROUPS taking alternate tiles, each
 //     with its own TMEM slot: tcgen05.ld -> bias + sigmoid -> split ->
-//     tcgen05.st as the next layer's A operand (in place over the consumed
-//     accumulator), then the grid sweep of the tile (thread = kernel) — one
-//     group's epilogue overlaps the other's sweep and the next tile's L1.
+//     tcgen05.st of A2 in place over the consumed D1; then D2 -> sigmoid into
+//     registers, layers 3-4 on the FMA pipe, clamp, the grid sweep of the tile
+//     (thread = kernel) and the outputs — one group's tail overlaps the other
+//     group's tile on the tensor core.
 // TMEM (512 columns): slot g at 216 g: [0,112) D1 -> A2 hi (in place),
-// [112,216) A2 lo; after L2: [0,56) A3 hi, [56,112) A3 lo, [112,144) D3 -> A4
-// hi, [144,160) D4, [160,192) A4 lo.  [432,496) D2 (shared, guarded by
-// D2FREE), [496 + 8 g, +8) predictions computed on the FMA pipe.
+// [112,216) A2 lo; [432,496) D2 (shared, guarded by D2FREE); [496 + 8 g, +8)
+// predictions computed on the FMA pipe.
 //
 // Non-finite inputs (a DCGM value, or any predict-mode feature): the producer
 // computes that kernel's prediction on the FMA pipe (tc_forward_x, IEEE
