@@ -16,9 +16,16 @@ for cfg in ("c1", "c3"):
     m.target_mean = np.array([60, 10, 0.01, 0.004, 0.15, 200, 200.0])
     m.target_std = np.array([15, 3, 0.005, 0.001, 0.07, 100, 100.0])
     ctx.set_model(m)
-    for n in (1, 63, 64, 65, 1000, 4099):
+    for n in (1, 63, 64, 65, 127, 128, 129, 1000, 4099):
         g = ctx.gen_synthetic(n, root=n)
         f = ctx.featurize(g["counts"], g["dcgm"])
+        for eng in (0, 1):  # both predictor engines (FMA pipe, tcgen05)
+            ctx.set_option("mlp_engine", eng)
+            ctx.predict_params(f, want_raw=True)
+            ctx.pipeline(g["counts"], g["dcgm"], 0.8, want_params=True)
+            gc = ctx.gen_synthetic_csr(n, root=n)
+            ctx.pipeline_csr(gc["row_ptr"], gc["entries"], gc["dcgm"], 0.8, want_params=True)
+        ctx.set_option("mlp_engine", 2)
         p, cl, raw = ctx.predict_params(f, want_raw=True)
         ctx.brute_force_config(p, 0.8)
         ctx.brute_force_config_exact(p.double().t().contiguous(), 0.8)
