@@ -523,6 +523,33 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
                 asm volatile("prefetch.global.L1 [%0];" ::"l"(ep));
                 asm volatile("prefetch.global.L1 [%0];" ::"l"(ep + kEnt - 1));
             }
+            // predict / dense: the input rows of tile t+2 into L2 (bulk prefetches, one
+            // 512-byte row segment per thread, no registers or shared memory held), so
+            // the chunk loads below hit L2 rather than HBM
+            if (MODE != MODE_CSR && t + 2 < my_tiles) {
+                const int64_t tp = t0_of(t + 2);
+                const int nrows = MODE == MODE_PRED ? DSO_FUSED_ROWS : DSO_COUNT_ROWS + 8;
+                if (tp + TT <= J.n && (J.ld & 3) == 0 && row < nrows) {
+                    const void* src = MODE == MODE_PRED
+                                          ? (const void*)(J.fused + (int64_t)row * J.ld + tp)
+                                      : row < 8 ? (const void*)(J.dcgm + (int64_t)row * J.ld + tp)
+                                                : (const void*)(J.counts + (int64_t)(row - 8) * J.ld + tp);
+                    if ((reinterpret_cast<uintptr_t>(src) & 15) == 0)
+                        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src),
+                                     "r"((uint32_t)(TT * 4))
+                                     : "memory");
+                }
+                if (row + kGroupT < nrows) {  // (rows 128..133 of the fused input)
+                    const int r2 = row + kGroupT;
+                    const void* src2 = MODE == MODE_PRED
+                                           ? (const void*)(J.fused + (int64_t)r2 * J.ld + tp)
+                                           : (const void*)(J.counts + (int64_t)(r2 - 8) * J.ld + tp);
+                    if (tp + TT <= J.n && (J.ld & 3) == 0 && (reinterpret_cast<uintptr_t>(src2) & 15) == 0)
+                        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src2),
+                                     "r"((uint32_t)(TT * 4))
+                                     : "memory");
+                }
+            }
             TPT_BEGIN(p_t);
             // ---- per-kernel preparation: totals, chunk mask, non-finite rows ----
             float tf[3] = {0.f, 0.f, 0.f}, rr[3] = {0.f, 0.f, 0.f};
