@@ -88,6 +88,12 @@ public:
                      ctx_);
     }
 
+    // dso_set_option: "mlp_engine" (0 FMA pipe, 1 tcgen05, 2 auto = default),
+    // "fast_sweep" (1 default, 0 pair-by-pair scan); InvalidArgument otherwise
+    void set_option(const char* key, int64_t value) {
+        check_status(dso_set_option(ctx_, key, value), ctx_);
+    }
+
     const std::vector<double>& core() const { return core_; }
     const std::vector<double>& mem() const { return mem_; }
     const DeviceConstants& dev() const { return dev_; }

@@ -209,17 +209,27 @@ int main() {
                 counts[k].entries.push_back({s, static_cast<uint32_t>(rng.below(100000))});
             for (int m = 0; m < 8; ++m) dcgm[k][m] = rng.uniform01();
         }
-        auto dec = optimize_kernels(counts, dcgm, 0.8, 300.0, ctx);
-        int worse = 0;
-        for (std::size_t k = 0; k < dec.size(); ++k) {
-            KernelModelParams p = dec[k].params;
-            CHECK(p.p0 >= 0 && p.alpha + p.beta > 0);
-            const OptimizationResult r = brute_force_config(p, d, 0.8, 300.0);
-            const double fc = d.core_freqs_mhz[dec[k].fc_idx], fm = d.mem_freqs_mhz[dec[k].fm_idx];
-            const double c = cost(p, DvfsConfig{required_voltage_mhz(fc, d.dev), fc, fm}, 0.8, 300.0);
-            worse += c > r.cost * (1.0 + 1e-6);
+        for (int engine : {0, 1}) {  // FMA-pipe and tcgen05 predictor engines
+            ctx.set_option("mlp_engine", engine);
+            auto dec = optimize_kernels(counts, dcgm, 0.8, 300.0, ctx);
+            int worse = 0;
+            for (std::size_t k = 0; k < dec.size(); ++k) {
+                KernelModelParams p = dec[k].params;
+                CHECK(p.p0 >= 0 && p.alpha + p.beta > 0);
+                const OptimizationResult r = brute_force_config(p, d, 0.8, 300.0);
+                const double fc = d.core_freqs_mhz[dec[k].fc_idx], fm = d.mem_freqs_mhz[dec[k].fm_idx];
+                const double c = cost(p, DvfsConfig{required_voltage_mhz(fc, d.dev), fc, fm}, 0.8, 300.0);
+                worse += c > r.cost * (1.0 + 1e-6);
+            }
+            CHECK(worse == 0);
         }
-        CHECK(worse == 0);
+        ctx.set_option("mlp_engine", 2);
+        try {
+            ctx.set_option("mlp_engine", 3);
+            CHECK(false);
+        } catch (const Error& e) {
+            CHECK(e.kind() == ErrorKind::InvalidArgument);
+        }
     }
     std::printf("%s: %d failure(s)\n", failures ? "FAIL" : "PASS", failures);
     return failures ? 1 : 0;
