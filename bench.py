@@ -35,6 +35,7 @@ sys.path.insert(0, ROOT)
 METRIC = "(kernel×freq-pair) evals/sec, 1/2/4/8 B200, % roofline vs host-CPU ref"
 UNIT = "(kernel, freq-pair) evals/s"
 ROOT_SEED = 0xD50B203
+DSO_COUNT_ROWS = 126
 MLP_FLOPS = 2 * (134 * 100 + 100 * 50 + 50 * 25 + 25 * 7)  # 39,650 per kernel
 PAIR_FLOPS = 14
 
@@ -74,6 +75,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-stages", action="store_true")
+    ap.add_argument("--no-extra", action="store_true",
+                    help="skip the other configs (C2, C4, C5) measured after the headline")
     ap.add_argument("--cpu-sample", type=int, default=0)
     ap.add_argument("--engine", default="auto", choices=["auto", "ffma", "tc"],
                     help="predictor engine: the library's auto choice (tcgen05 for CSR), "
@@ -163,13 +166,20 @@ def ncu_traffic(config, n):
 
 
 # ---------------------------------------------------------------------------------------
+def ref_domain(nc, nm):
+    """The benchmark grid without the product package: fc = 705 +
+    675 i/(nc-1), fm = 438 + 439 j/(nm-1) or {877}; default_device (sim_harness.cpp:103-106)
+    as [kappa_vf, pmax, vmin, vmax, mhz_per_unit]."""
+    core = 705.0 + (1380.0 - 705.0) * np.arange(nc) / max(nc - 1, 1)
+    mem = np.array([877.0]) if nm == 1 else 438.0 + 439.0 * np.arange(nm) / (nm - 1)
+    return core, mem, np.array([0.5, 300.0, 0.55, 2.10, 1000.0])
+
+
 def cpu_pipeline_rate(port, ref, n, cfg, model, threads):
     """Host-CPU reference path on n kernels: features + MLP (C restatement; the
     reference needs Eigen, absent) and brute_force_config (the reference's own
     optimizer.cpp, oracle/_ref).  Returns (pairs/s, seconds, detail)."""
-    from paper_2407_13096_b200 import linear_domain
-    dom = linear_domain(cfg["nc"], cfg["nm"])
-    dev = dom.dev.as_array()
+    core, mem, dev = ref_domain(cfg["nc"], cfg["nm"])
     g = port.gen_stream(ROOT_SEED, n, want=("counts", "dcgm"), threads=threads)
     t0 = time.perf_counter()
     fused = port.fuse(g["counts"], g["dcgm"])
@@ -177,29 +187,34 @@ def cpu_pipeline_rate(port, ref, n, cfg, model, threads):
     t1 = time.perf_counter()
     eta = cfg["eta"] if cfg["eta"] is not None else 0.8
     if ref is not None:
-        ref.brute_force_config(params, dom.core_freqs_mhz, dom.mem_freqs_mhz, dev, eta,
-                               dom.dev.pmax_w, threads=threads)
+        ref.brute_force_config(params, core, mem, dev, eta, dev[1], threads=threads)
         sweep_kind = "reference optimizer.cpp (oracle/_ref)"
     else:
-        port.brute_force(params, dom.core_freqs_mhz, dom.mem_freqs_mhz, dev, eta,
-                         dom.dev.pmax_w, threads=threads)
+        port.brute_force(params, core, mem, dev, eta, dev[1], threads=threads)
         sweep_kind = "C restatement (oracle/liboracle.so)"
     t2 = time.perf_counter()
-    pairs = n * dom.pairs
+    pairs = n * len(core) * len(mem)
     return pairs / (t2 - t0), t2 - t0, {"features_mlp_s": t1 - t0, "sweep_s": t2 - t1,
                                          "sweep_impl": sweep_kind}
 
 
-def bench_model(port=None):
-    """Model for the benchmark: Glorot init (seed 424242, the golden seed) with
-    target stats of the synthetic truth parameters so outputs are DVFS-scaled."""
-    from paper_2407_13096_b200 import init_mlp
-    m = init_mlp(seed=424242)
-    # population mean / std of the generator's parameter ranges, from 65,536 draws
-    if port is not None:
-        p = port.gen_stream(0xC0FFEE, 65536, want=("params",))["params"]
-        m.target_mean, m.target_std = p.mean(0), p.std(0)
-    return m
+class OracleModel:
+    """A model object in the layout the oracle reads (layer_sizes, weights, biases,
+    target_mean, target_std) — the reference arm never touches the product library."""
+
+    def __init__(self, layer_sizes, weights, biases, target_mean, target_std):
+        self.layer_sizes, self.weights, self.biases = layer_sizes, weights, biases
+        self.target_mean, self.target_std = target_mean, target_std
+
+
+def bench_model(port):
+    """Model for the CPU legs: init_mlp(default_layer_sizes, 424242) by the oracle's
+    restatement of mlp.cpp:184-207 (identical draws to the device model), with the
+    population mean / std of 65,536 synthetic truth parameters as target stats."""
+    sizes = [134, 100, 50, 25, 7]
+    ws, bs = port.init_mlp(sizes, 424242)
+    p = port.gen_stream(0xC0FFEE, 65536, want=("params",))["params"]
+    return OracleModel(sizes, ws, bs, p.mean(0), p.std(0))
 
 
 def run_reference(args, rank, world):
@@ -240,243 +255,251 @@ def run_reference(args, rank, world):
 
 
 # ---------------------------------------------------------------------------------------
-def run_ours(args, rank, world, local_rank):
+TC_L1_FLOPS = 3 * 2 * 128 * 112 * 8   # one tcgen05 layer-1 k-step: 3 kind::tf32 MMAs M128 N112 K8
+TC_L2_FLOPS = 3 * 2 * 128 * 64 * 8    # one layer-2 k-step: 3 MMAs M128 N64 K8
+
+
+def cuda_time(stream, fn, reps):
+    """Mean ms per call of fn over reps calls, CUDA events on the launching stream."""
     import torch
-    import torch.distributed as dist
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    a.record(stream)
+    for _ in range(reps):
+        fn()
+    b.record(stream)
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / reps
 
-    from paper_2407_13096_b200 import linear_domain
-    from paper_2407_13096_b200.api import Context, _ptr
-    from paper_2407_13096_b200 import _lib
 
-    cfg = CONFIGS[args.config]
-    n = args.kernels or cfg["n"]
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
-    dom = linear_domain(cfg["nc"], cfg["nm"])
-    ctx = Context(local_rank)
-    ctx.set_option("mlp_engine", {"ffma": 0, "tc": 1, "auto": 2}[args.engine])
-    ctx.set_domain(dom)
-    model = bench_model_device(ctx)
-    ctx.set_model(model)
-    stream = torch.cuda.current_stream(dev)
+class Timed:
+    """W warm-up steps, then K steps between barrier + synchronize, CUDA events on
+    the launching stream, max over ranks (the contract's timing rule)."""
 
-    if args.config == "c5":
-        return run_train(args, rank, world, local_rank, ctx, dom, model, n)
-    # inputs: this rank's shard [rank*n, (rank+1)*n) of the global synthetic stream
-    csr = args.input == "csr" and args.config != "c4"
-    if csr:
-        gen = ctx.gen_synthetic_csr(n, root=ROOT_SEED, first=rank * n)
-        counts = None
-        dcgm = gen["dcgm"]
-    else:
-        gen = ctx.gen_synthetic(n, root=ROOT_SEED, first=rank * n, params=(args.config == "c4"))
-        counts, dcgm = gen["counts"], gen["dcgm"]
-    etas = np.arange(101) / 100.0
-    if args.config == "c4":
-        params = gen["params"]
-        idx_o = torch.empty((101, n), dtype=torch.int32, device=dev)
-        cost_o = torch.empty((101, n), dtype=torch.float32, device=dev)
-        eta_arr = np.ascontiguousarray(etas)
-        dp = __import__("ctypes").POINTER(__import__("ctypes").c_double)
+    def __init__(self, world, dev, stream):
+        self.world, self.dev, self.stream = world, dev, stream
 
-        def step():
-            ctx._raise(ctx._lib.dso_eta_sweep(ctx._h, _ptr(params), n, n,
-                                              eta_arr.ctypes.data_as(dp), 101, dom.dev.pmax_w,
-                                              _ptr(idx_o), _ptr(cost_o), n))
-        units_per_step = n * dom.pairs  # (kernel, pair) evals; x101 etas reported separately
-        flops_per_step = n * dom.pairs * (9 + 3 * 101)  # P,T,E once + 3 per (pair, eta)
-    else:
-        out = ctx.alloc_pipeline_out(n)
-        if csr:
-            def step():
-                ctx.pipeline_csr(gen["row_ptr"], gen["entries"], dcgm, cfg["eta"], out=out)
-        else:
-            def step():
-                ctx.pipeline(counts, dcgm, cfg["eta"], out=out)
-        units_per_step = n * dom.pairs
-        flops_per_step = n * (MLP_FLOPS + PAIR_FLOPS * dom.pairs)
-        if csr:
-            # Sparse input: layer 1 only needs the rows a kernel lists (8 DCGM rows +
-            # its non-zero count slots; the kernel skips all-zero rows exactly), so
-            # the algorithmic work is 2*100*(8 + nnz) there, not 2*100*134.
-            nnz = float((gen["row_ptr"][n] - gen["row_ptr"][0]).item()) / n
-            flops_per_step = n * (mlp_flops_sparse(8 + nnz) + PAIR_FLOPS * dom.pairs)
-
-    # measured FP32 peak (roofline denominator for the FP32-pipe-bound kernels)
-    peak = {}
-    for mode, name in ((1, "ffma2"), (0, "ffma")):
-        v = __import__("ctypes").c_double()
-        ctx._raise(_lib.lib().dso_probe_fp32_peak(ctx._h, mode, __import__("ctypes").byref(v)))
-        peak[name] = v.value
-
-    def barrier():
-        if world > 1:
+    def barrier(self):
+        if self.world > 1:
+            import torch.distributed as dist
             dist.barrier()
 
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    barrier()
-    launches0 = ctx.launch_count
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    with ClockSampler(list(range(world)) if world > 1 else [local_rank]) as clk:
+    def max_over_ranks(self, v):
+        import torch
+        import torch.distributed as dist
+        t = torch.tensor([v], dtype=torch.float64, device=self.dev)
+        if self.world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def run(self, step, steps, warmup, clocks=None):
+        import torch
+        for i in range(warmup):
+            step(i)
         torch.cuda.synchronize()
-        e0.record(stream)
-        for _ in range(args.steps):
-            step()
-        e1.record(stream)
+        self.barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
-    barrier()
-    launches = ctx.launch_count - launches0
-    ms = e0.elapsed_time(e1) / args.steps
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
-    value = units_per_step * world / (ms_max * 1e-3)
-
-    # ---- per-stage breakdown (same data, separate kernels) ---------------------------
-    stages = None
-    if not args.no_stages and args.config != "c4":
-        dense = ctx.gen_synthetic(n, root=ROOT_SEED, first=rank * n, params=False)
-        stages = stage_times(ctx, dense["counts"], dense["dcgm"], cfg, dom, n, stream)
-        if csr:
-            a = torch.cuda.Event(enable_timing=True)
-            bb = torch.cuda.Event(enable_timing=True)
-            ctx.pipeline(dense["counts"], dense["dcgm"], cfg["eta"], out=out)
-            a.record(stream)
-            for _ in range(3):
-                ctx.pipeline(dense["counts"], dense["dcgm"], cfg["eta"], out=out)
-            bb.record(stream)
-            torch.cuda.synchronize()
-            stages["pipeline_dense_input_ms"] = a.elapsed_time(bb) / 3
-        del dense
-
-    # ---- end to end through the C-ABI with pinned host buffers --------------------------
-    e2e = None
-    if not args.no_e2e and args.config != "c4":
-        hd = dcgm.cpu().pin_memory()
-        if csr:
-            hrp = gen["row_ptr"].cpu().pin_memory()
-            hent = gen["entries"].cpu().pin_memory()
-            h2d = (n + 1) * 8 + hent.numel() * 4 + n * 8 * 4
-            run_e2e = lambda o: ctx.pipeline_csr(hrp, hent, hd, cfg["eta"], out=o)  # noqa: E731
-        else:
-            hc = counts.cpu().pin_memory()
-            h2d = n * (126 * 4 + 8 * 4)
-            run_e2e = lambda o: ctx.pipeline(hc, hd, cfg["eta"], out=o)  # noqa: E731
-        hout = ctx.alloc_pipeline_out(n, host=True, like=hd)
-        run_e2e(hout)  # warm-up (staging buffers)
-        k = max(1, min(args.steps, 5))
-        barrier()
-        t0 = time.perf_counter()
-        for _ in range(k):
-            run_e2e(hout)
-        el = (time.perf_counter() - t0) / k
-        te = torch.tensor([el], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        el = float(te.item())
-        e2e = {"value": units_per_step * world / el, "unit": UNIT,
-               "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(n * 16), "ms_per_step": el * 1e3,
-               "steps": k, "timing": "host wall clock around synchronous C-ABI calls "
-                                     "(dso_pipeline%s with DSO_HOST, pinned buffers)"
-                                     % ("_csr" if csr else "")}
-        del hd, hout
-
-    if rank != 0:
-        return
-    achieved = flops_per_step / (ms * 1e-3) / 1e12
-    peaks = measured_peaks()
-    pk = peak["ffma2"]
-    # which predictor engine ran (the library's auto policy: tcgen05 for CSR input)
-    engine_used = ("tc" if args.config != "c4" and (args.engine == "tc" or
-                                                      (args.engine == "auto" and csr))
-                   else ("ffma" if args.config != "c4" else None))
-    roofline = {
-        "bound": "fp32", "achieved": achieved, "peak": pk, "unit": "TFLOP/s",
-        "frac": achieved / pk,
-        "traffic": ncu_traffic(args.config, n) if (csr or args.config == "c4") else None,
-        "traffic_unit": "bytes per launch (ncu dram__bytes_read+write, profiles/ncu_summary.json)",
-        "algorithmic_bytes_per_launch": (n * ((136 if csr else 536) + 16) if args.config != "c4"
-                                         else n * (28 + 101 * 8)),
-        "kernel": "ws_kernel (fused pipeline)" if args.config != "c4" else "eta_sweep_fast_kernel",
-        "flops_per_kernel": flops_per_step / n if args.config != "c4" else None,
-        "flops_note": ("layer 1 counted on the 8 DCGM + non-zero count rows of each kernel "
-                       "(CSR input; all-zero rows are skipped exactly); the dense-input "
-                       "count (SURVEY.md §8(d): 39,650 + 14 per pair) is "
-                       "flops_per_kernel_dense" if csr and args.config != "c4" else
-                       ("9 flops per (kernel, pair) for P, T, E plus 3 per (kernel, pair, eta); "
-                        "the kernel is bound by the ALU pipe (group min trees and selects: "
-                        "profiles/r1/ncu_eta_sweep_metrics.txt)" if args.config == "c4" else None)),
-        "flops_per_kernel_dense": (MLP_FLOPS + PAIR_FLOPS * dom.pairs)
-        if args.config != "c4" else None,
-        "peak_source": ("measured in this run by dso_probe_fp32_peak (FFMA2 loop, 148x4 CTAs); "
-                        "MEASURED_PEAKS.json has no FP32 figure"),
-        "peak_ffma_scalar": peak["ffma"],
-        "nominal_peak": 148 * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12,
-        "hbm_gbs_measured": peaks.get("hbm_gbs"),
-        "achieved_input_gbs": (n * (136 if csr else 536) / (ms * 1e-3) / 1e9
-                               if args.config != "c4" else None),
-    }
-    if engine_used == "tc":
-        # the tcgen05 engine: layers 1-2 as 3xTF32 MMAs (3 TF32 products per
-        # multiply-add), layers 3-4 and the sweep on the FMA pipe; roofline against
-        # the dense TF32 tensor peak (half the measured dense bf16 figure)
-        tc_flops = n * 3 * 2 * (134 * 100 + 100 * 50)
-        tc_peak = peaks.get("bf16_tflops", 2250.0) / 2
-        fp32_view = dict(roofline)
-        roofline = {
-            "bound": "tensor", "achieved": tc_flops / (ms * 1e-3) / 1e12, "peak": tc_peak,
-            "unit": "TFLOP/s", "frac": tc_flops / (ms * 1e-3) / 1e12 / tc_peak,
-            "traffic": fp32_view["traffic"], "traffic_unit": fp32_view["traffic_unit"],
-            "algorithmic_bytes_per_launch": fp32_view["algorithmic_bytes_per_launch"],
-            "kernel": "tc_kernel (fused pipeline, tcgen05 kind::tf32)",
-            "tensor_flops_per_kernel": 3 * 2 * (134 * 100 + 100 * 50),
-            "flops_note": "TF32 tensor products issued for layers 1-2 (3xTF32: hi.hi + hi.lo + "
-                          "lo.hi per multiply-add, dense K = 134 / 100); CSR tiles skip all-zero "
-                          "8-column chunks of layer 1, so the issued count is lower than this",
-            "peak_source": "MEASURED_PEAKS.json bf16_tflops / 2 (dense TF32 = half the bf16 rate)",
-            "fp32_equivalent": {"achieved": achieved, "peak": pk, "frac": achieved / pk,
-                                "flops_per_kernel": fp32_view["flops_per_kernel"]},
-            "hbm_gbs_measured": peaks.get("hbm_gbs"),
-            "achieved_input_gbs": fp32_view["achieved_input_gbs"],
-        }
-    cpu = None
-    if not args.no_cpu and world == 1:
-        cpu = cpu_baseline(args, cfg, model)
-    line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic (gen_kernel stream generated on device; random-init MLP seed 424242)",
-        "config": {"workload": cfg["desc"], "kernels_per_gpu": n, "grid": f"{cfg['nc']}x{cfg['nm']}",
-                   "engine": engine_used or args.engine,
-                   "eta": cfg["eta"] if cfg["eta"] is not None else "0.00..1.00 (101)",
-                   "parallelism": f"kernel-sharded x{world}, no collective",
-                   "input": ("sparse per-kernel PTX count lists (24 non-zeros/kernel) + DCGM"
-                             if csr else "dense [126][n] PTX counts + DCGM"),
-                   "l2": "inputs > 126 MB L2 per step (no flush needed)"},
-        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-        "clocks": clk.summary(), "stages": stages,
-    }
-    if args.config == "c4":
-        line["triples_per_s"] = value * 101
-    print(json.dumps(line), flush=True)
+        e0.record(self.stream)
+        for i in range(steps):
+            step(warmup + i)
+        e1.record(self.stream)
+        torch.cuda.synchronize()
+        self.barrier()
+        ms = e0.elapsed_time(e1) / steps
+        return ms, self.max_over_ranks(ms)
 
 
-def run_train(args, rank, world, local_rank, ctx, dom, model, n):
-    """C5: synchronous data-parallel SGD steps (device grad -> NCCL allreduce ->
-    device update) over a device-resident 10M-sample shard per GPU."""
+def fp32_peak(ctx):
+    """Builder-measured FP32 peaks (dso_probe_fp32_peak: FFMA2 / FFMA loops on
+    148 x 4 CTAs). MEASURED_PEAKS.json has no FP32 figure."""
+    import ctypes as C
+    from paper_2407_13096_b200 import _lib
+    out = {}
+    for mode, name in ((1, "ffma2"), (0, "ffma")):
+        v = C.c_double()
+        ctx._raise(_lib.lib().dso_probe_fp32_peak(ctx._h, mode, C.byref(v)))
+        out[name] = v.value
+    return out
+
+
+PEAK_NOTE = ("builder-measured in this run: dso_probe_fp32_peak (FFMA2 loop on 148x4 CTAs); "
+             "MEASURED_PEAKS.json has no FP32 figure")
+
+
+def measure_pipeline(ctx, name, args, rank, world, tm, peak, steps, warmup, csr=True,
+                     with_e2e=False, clocks=None):
+    """C2 / C3: the fused pipeline (features -> MLP -> sweep -> argmin) over this rank's
+    shard of the synthetic stream.  Returns (line fields, inputs)."""
     import torch
-    import torch.distributed as dist
+    from paper_2407_13096_b200 import linear_domain
+    cfg = CONFIGS[name]
+    n = args.kernels if (args.kernels and name == args.config) else cfg["n"]
+    dom = linear_domain(cfg["nc"], cfg["nm"])
+    ctx.set_domain(dom)
+    if csr:
+        gen = ctx.gen_synthetic_csr(n, root=ROOT_SEED, first=rank * n)
+        dcgm = gen["dcgm"]
+        nnz = float((gen["row_ptr"][n] - gen["row_ptr"][0]).item()) / n
+    else:
+        gen = ctx.gen_synthetic(n, root=ROOT_SEED, first=rank * n, params=False)
+        dcgm = gen["dcgm"]
+        nnz = DSO_COUNT_ROWS
+    out = ctx.alloc_pipeline_out(n)
+    if csr:
+        step = lambda i: ctx.pipeline_csr(gen["row_ptr"], gen["entries"], dcgm, cfg["eta"], out=out)  # noqa: E731
+    else:
+        step = lambda i: ctx.pipeline(gen["counts"], dcgm, cfg["eta"], out=out)  # noqa: E731
+    launches0 = ctx.launch_count
+    ctx.counters(reset=True)
+    for i in range(warmup):
+        step(i)
+    ctx.counters(reset=True)
+    launches0 = ctx.launch_count
+    if clocks is not None:
+        with clocks:
+            ms, ms_max = tm.run(step, steps, 0)
+    else:
+        ms, ms_max = tm.run(step, steps, 0)
+    ctr = ctx.counters(reset=True)
+    launches = ctx.launch_count - launches0
+    pairs = dom.pairs
+    units = n * pairs
+    value = units * world / (ms_max * 1e-3)
+    # FP32-equivalent algorithmic work (SURVEY.md §8(d)), layer 1 on the rows a
+    # kernel lists (8 DCGM + its non-zero count slots; all-zero rows are exact zeros)
+    fpk = mlp_flops_sparse(8 + nnz) + PAIR_FLOPS * pairs
+    fpk_dense = MLP_FLOPS + PAIR_FLOPS * pairs
+    achieved = n * fpk / (ms * 1e-3) / 1e12
+    peaks = measured_peaks()
+    engine = "tc" if ctr["tc_tiles"] > 0 else "ffma"
+    roofline = {
+        "bound": "fp32", "achieved": achieved, "peak": peak["ffma2"], "unit": "TFLOP/s",
+        "frac": achieved / peak["ffma2"],
+        "traffic": ncu_traffic(name, n) if csr else None,
+        "traffic_unit": "bytes per launch (ncu dram__bytes_read+write, profiles/ncu_summary.json)",
+        "algorithmic_bytes_per_launch": n * ((8 + 4 * nnz + 32) if csr else (126 * 4 + 32)) + n * 16,
+        "kernel": ("tc_kernel<MODE_CSR> (fused pipeline; layers 1-2 on tcgen05 kind::tf32)"
+                   if engine == "tc" else "ws_kernel (fused pipeline, FFMA2)"),
+        "flops_per_kernel": fpk,
+        "flops_note": ("FP32-equivalent algorithmic flops per kernel: MLP with layer 1 on the 8 + "
+                       f"{nnz:g} listed input rows (2*100*(8+nnz) + 2*(5000+1250+175)) + "
+                       f"{PAIR_FLOPS} per (kernel, pair) x {pairs} pairs; the dense-input count "
+                       "(SURVEY.md §8(d)) is flops_per_kernel_dense"),
+        "flops_per_kernel_dense": fpk_dense,
+        "peak_source": PEAK_NOTE, "peak_ffma_scalar": peak["ffma"],
+        "nominal_peak": 148 * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12,
+        "binding_unit": "CUDA-core issue (FP32/ALU pipes): producers' CSR feature stage and the "
+                        "epilogues' layers 3-4 + grid sweep; the tensor pipe is not the limiter "
+                        "(tensor_view)",
+    }
+    if engine == "tc":
+        issued = ctr["tc_l1_ksteps"] * TC_L1_FLOPS + ctr["tc_l2_ksteps"] * TC_L2_FLOPS
+        tflops = issued / steps / (ms * 1e-3) / 1e12
+        tpk = peaks.get("bf16_tflops", 2250.0) / 2
+        roofline["tensor_view"] = {
+            "achieved": tflops, "peak": tpk, "frac": tflops / tpk, "unit": "TFLOP/s",
+            "issued_flops_per_step": issued / steps,
+            "l1_ksteps_per_tile": ctr["tc_l1_ksteps"] / max(ctr["tc_tiles"], 1),
+            "l2_ksteps_per_tile": ctr["tc_l2_ksteps"] / max(ctr["tc_tiles"], 1),
+            "source": "device counters (dso_get_counters) over the timed steps: k-steps the MMA "
+                      "thread issued x 3 kind::tf32 MMAs (M128 x N112 x K8 layer 1, "
+                      "M128 x N64 x K8 layer 2; padded shapes)",
+            "peak_source": "MEASURED_PEAKS.json bf16_tflops / 2 (dense TF32 = half the bf16 rate)",
+        }
+    res = {"value": value, "unit": UNIT, "ms_per_step": ms_max, "steps": steps,
+           "kernels_per_gpu": n, "grid": f"{cfg['nc']}x{cfg['nm']}", "engine": engine,
+           "roofline": roofline, "gpu_launches": launches,
+           "input": ("sparse per-kernel PTX count lists (%g non-zeros/kernel) + DCGM" % nnz
+                     if csr else "dense [126][n] PTX counts + DCGM")}
+    if with_e2e:
+        res["e2e"] = measure_e2e(ctx, gen, dcgm, cfg, n, csr, steps, tm, world, units)
+    return res, gen
 
+
+def measure_e2e(ctx, gen, dcgm, cfg, n, csr, steps, tm, world, units):
+    """The same metric through the C-ABI with pinned HOST buffers (H2D + kernel + D2H
+    inside each timed call)."""
+    hd = dcgm.cpu().pin_memory()
+    if csr:
+        hrp = gen["row_ptr"].cpu().pin_memory()
+        hent = gen["entries"].cpu().pin_memory()
+        h2d = (n + 1) * 8 + hent.numel() * 4 + n * 8 * 4
+        run = lambda o: ctx.pipeline_csr(hrp, hent, hd, cfg["eta"], out=o)  # noqa: E731
+    else:
+        hc = gen["counts"].cpu().pin_memory()
+        h2d = n * (126 * 4 + 8 * 4)
+        run = lambda o: ctx.pipeline(hc, hd, cfg["eta"], out=o)  # noqa: E731
+    hout = ctx.alloc_pipeline_out(n, host=True, like=hd)
+    run(hout)  # warm-up (staging buffers)
+    k = max(1, min(steps, 5))
+    tm.barrier()
+    t0 = time.perf_counter()
+    for _ in range(k):
+        run(hout)
+    el = tm.max_over_ranks((time.perf_counter() - t0) / k)
+    return {"value": units * world / el, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(n * 16), "ms_per_step": el * 1e3, "steps": k,
+            "timing": "host wall clock around synchronous C-ABI calls (dso_pipeline%s with "
+                      "DSO_HOST, pinned buffers), max over ranks" % ("_csr" if csr else "")}
+
+
+def measure_eta(ctx, args, rank, world, tm, peak, steps, warmup):
+    """C4: brute_force_config at 101 etas (dso_eta_sweep) over 4M kernels' params."""
+    import ctypes as C
+
+    import torch
+    from paper_2407_13096_b200 import linear_domain
+    from paper_2407_13096_b200.api import _ptr
+    cfg = CONFIGS["c4"]
+    n = args.kernels if (args.kernels and args.config == "c4") else cfg["n"]
+    dom = linear_domain(cfg["nc"], cfg["nm"])
+    ctx.set_domain(dom)
+    params = ctx.gen_synthetic(n, root=ROOT_SEED, first=rank * n, counts=False, dcgm=False)["params"]
+    dev = params.device
+    idx_o = torch.empty((101, n), dtype=torch.int32, device=dev)
+    cost_o = torch.empty((101, n), dtype=torch.float32, device=dev)
+    etas = np.ascontiguousarray(np.arange(101) / 100.0)
+    dp = C.POINTER(C.c_double)
+
+    def step(i):
+        ctx._raise(ctx._lib.dso_eta_sweep(ctx._h, _ptr(params), n, n, etas.ctypes.data_as(dp),
+                                          101, dom.dev.pmax_w, _ptr(idx_o), _ptr(cost_o), n))
+    for i in range(warmup):
+        step(i)
+    l0 = ctx.launch_count
+    ms, ms_max = tm.run(step, steps, 0)
+    units = n * dom.pairs
+    fl = units * (9 + 3 * 101)
+    achieved = fl / (ms * 1e-3) / 1e12
+    return {"value": units * world / (ms_max * 1e-3), "unit": UNIT, "ms_per_step": ms_max,
+            "steps": steps, "triples_per_s": units * 101 * world / (ms_max * 1e-3),
+            "kernels_per_gpu": n, "grid": f"{cfg['nc']}x{cfg['nm']}", "gpu_launches": ctx.launch_count - l0,
+            "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak["ffma2"],
+                         "frac": achieved / peak["ffma2"], "unit": "TFLOP/s",
+                         "kernel": "eta_sweep_fast_kernel",
+                         "flops_per_pair": 9 + 3 * 101,
+                         "flops_note": "P (3 FMA), T (mul, max, add), E (mul) once per (kernel, pair) "
+                                       "= 9, plus C = (eta*P + K)*T = 3 per (kernel, pair, eta)",
+                         "peak_source": PEAK_NOTE,
+                         "traffic": ncu_traffic("c4", n),
+                         "algorithmic_bytes_per_launch": n * (28 + 101 * 8)}}
+
+
+def measure_train(ctx, args, rank, world, tm, peak, steps, warmup, model):
+    """C5: synchronous data-parallel SGD steps (device gradient -> NCCL allreduce of
+    the 20,007-float gradient -> identical device update) over a device-resident
+    shard of synthetic samples per GPU."""
+    import torch
+    from paper_2407_13096_b200 import linear_domain
     from paper_2407_13096_b200.train import DataParallelTrainer
     cfg = CONFIGS["c5"]
-    dev = torch.device("cuda", local_rank)
-    stream = torch.cuda.current_stream(dev)
+    n = args.kernels if (args.kernels and args.config == "c5") else cfg["n"]
+    ctx.set_domain(linear_domain(cfg["nc"], cfg["nm"]))
+    ctx.set_model(model)
+    dev = torch.device("cuda", ctx.device)
     B = cfg["batch"]
     gen = ctx.gen_synthetic(n, root=0xACCE5505, first=rank * n)
     x = ctx.featurize(gen["counts"], gen["dcgm"])
@@ -491,67 +514,133 @@ def run_train(args, rank, world, local_rank, ctx, dom, model, n):
     grad = torch.empty((ctx.n_model_params,), dtype=torch.float32, device=dev)
 
     def step(i):
-        s = (i % nb) * B
-        g, loss = ctx.train_grad_slice(x, y, s, B, grad=grad)
+        s0 = (i % nb) * B
+        g, loss = ctx.train_grad_slice(x, y, s0, B, grad=grad)
         tr.allreduce(g)
         tr.allreduce(loss)
         ctx.train_apply(g, tr.lr, 1.0 / (B * world * 7))
-        return loss
 
-    def barrier():
-        if world > 1:
-            dist.barrier()
-
-    for i in range(args.warmup):
+    for i in range(warmup):
         step(i)
-    torch.cuda.synchronize()
-    barrier()
-    launches0 = ctx.launch_count
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    with ClockSampler(list(range(world)) if world > 1 else [local_rank]) as clk:
-        e0.record(stream)
-        for i in range(args.steps):
-            step(args.warmup + i)
-        e1.record(stream)
-        torch.cuda.synchronize()
-    barrier()
-    ms = e0.elapsed_time(e1) / args.steps
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
-    # grad kernel alone (share of the step)
-    a = torch.cuda.Event(enable_timing=True)
-    bb = torch.cuda.Event(enable_timing=True)
-    a.record(stream)
-    for i in range(5):
-        ctx.train_grad_slice(x, y, (i % nb) * B, B, grad=grad)
-    bb.record(stream)
-    torch.cuda.synchronize()
-    grad_ms = a.elapsed_time(bb) / 5
+    l0 = ctx.launch_count
+    ms, ms_max = tm.run(step, steps, 0)
+    launches = ctx.launch_count - l0
+    grad_ms = cuda_time(tm.stream, lambda: ctx.train_grad_slice(x, y, 0, B, grad=grad), 5)
+    achieved = B * TRAIN_FLOPS / (grad_ms * 1e-3) / 1e12
+    step_tflops = B * TRAIN_FLOPS / (ms * 1e-3) / 1e12
+    ctx.set_model(model)  # training moved the weights
+    del x, y
+    return {"metric": "predictor training sample-steps/s (C5)", "value": B * world / (ms_max * 1e-3),
+            "unit": "samples/s", "ms_per_step": ms_max, "steps": steps,
+            "samples_per_gpu": n, "batch_per_gpu": B, "global_batch": B * world,
+            "parallelism": f"dp{world} (%s allreduce)" % ("NCCL" if world > 1 else "no"),
+            "gpu_launches": launches,
+            "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak["ffma2"],
+                         "frac": achieved / peak["ffma2"], "unit": "TFLOP/s",
+                         "step_view": {"achieved": step_tflops, "frac": step_tflops / peak["ffma2"],
+                                       "note": "whole step incl. update and allreduce"},
+                         "traffic": ncu_traffic("c5", B),
+                         "traffic_unit": "bytes per dso_train_grad (ncu, profiles/ncu_summary.json)",
+                         "kernel": "dso_train_grad kernels", "flops_per_sample": TRAIN_FLOPS,
+                         "grad_kernel_ms": grad_ms, "peak_source": PEAK_NOTE}}
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+
+    from paper_2407_13096_b200.api import Context
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    ctx = Context(local_rank)
+    ctx.set_option("mlp_engine", {"ffma": 0, "tc": 1, "auto": 2}[args.engine])
+    model = bench_model_device(ctx)
+    ctx.set_model(model)
+    stream = torch.cuda.current_stream(dev)
+    tm = Timed(world, dev, stream)
+    peak = fp32_peak(ctx)
+    clk = ClockSampler(list(range(world)) if world > 1 else [local_rank])
+    csr = args.input == "csr"
+
+    if args.config in ("c2", "c3"):
+        head, gen = measure_pipeline(ctx, args.config, args, rank, world, tm, peak, args.steps,
+                                     args.warmup, csr=csr, with_e2e=not args.no_e2e, clocks=clk)
+        cfg = CONFIGS[args.config]
+        stages = None
+        if not args.no_stages:
+            del gen
+            n = head["kernels_per_gpu"]
+            dense = ctx.gen_synthetic(n, root=ROOT_SEED, first=rank * n, params=False)
+            from paper_2407_13096_b200 import linear_domain
+            stages = stage_times(ctx, dense["counts"], dense["dcgm"], cfg,
+                                 linear_domain(cfg["nc"], cfg["nm"]), n, stream)
+            if csr:
+                o = ctx.alloc_pipeline_out(n)
+                stages["pipeline_dense_input_ms"] = cuda_time(
+                    stream, lambda: ctx.pipeline(dense["counts"], dense["dcgm"], cfg["eta"], out=o), 3)
+            del dense
+        else:
+            del gen
+        e2e = head.pop("e2e", None)
+        line = {
+            "metric": METRIC, "value": head["value"], "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": head["ms_per_step"],
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (gen_kernel stream generated on device; random-init MLP seed 424242)",
+            "config": {"workload": cfg["desc"], "kernels_per_gpu": head["kernels_per_gpu"],
+                       "grid": head["grid"], "engine": head["engine"], "eta": cfg["eta"],
+                       "parallelism": f"kernel-sharded x{world}, no collective",
+                       "input": head["input"],
+                       "l2": "inputs > 126 MB L2 per step (no flush needed)"},
+            "roofline": head["roofline"], "e2e": e2e, "gpu_launches": head["gpu_launches"],
+            "clocks": clk.summary(), "stages": stages,
+        }
+    elif args.config == "c4":
+        with clk:
+            r = measure_eta(ctx, args, rank, world, tm, peak, args.steps, args.warmup)
+        line = {"metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["ms_per_step"],
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+                "data": "synthetic (gen_kernel stream generated on device)",
+                "config": {"workload": CONFIGS["c4"]["desc"], "kernels_per_gpu": r["kernels_per_gpu"],
+                           "parallelism": f"kernel-sharded x{world}, no collective",
+                           "l2": "outputs 3.2 GB per step (> L2)"},
+                "roofline": r["roofline"], "triples_per_s": r["triples_per_s"],
+                "gpu_launches": r["gpu_launches"], "clocks": clk.summary(), "e2e": None}
+    else:  # c5
+        with clk:
+            r = measure_train(ctx, args, rank, world, tm, peak, args.steps, args.warmup, model)
+        line = {"metric": r["metric"], "value": r["value"], "unit": r["unit"], "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["ms_per_step"],
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+                "data": "synthetic (gen_kernel stream generated on device)",
+                "config": {"workload": CONFIGS["c5"]["desc"], "samples_per_gpu": r["samples_per_gpu"],
+                           "batch_per_gpu": r["batch_per_gpu"], "global_batch": r["global_batch"],
+                           "parallelism": r["parallelism"],
+                           "l2": "batches stream through a 5.6 GB device-resident shard"},
+                "roofline": r["roofline"], "gpu_launches": r["gpu_launches"],
+                "clocks": clk.summary(), "e2e": None}
+
+    # ---- the other BASELINE configs, measured in the same run (driver-visible) --------
+    others = {}
+    if not args.no_extra and args.config == "c3":
+        ks, kw = max(3, min(args.steps, 10)), 3
+        try:
+            r, g = measure_pipeline(ctx, "c2", args, rank, world, tm, peak, max(args.steps, 20),
+                                    kw, csr=True)
+            del g
+            others["c2"] = r
+            others["c4"] = measure_eta(ctx, args, rank, world, tm, peak, ks, kw)
+            others["c5"] = measure_train(ctx, args, rank, world, tm, peak, max(args.steps, 20), kw,
+                                         model)
+        except Exception as exc:  # reported, never silently dropped
+            others["error"] = repr(exc)
+        line["configs"] = others
     if rank != 0:
         return
-    value = B * world / (ms_max * 1e-3)
-    achieved = B * TRAIN_FLOPS / (grad_ms * 1e-3) / 1e12
-    v = __import__("ctypes").c_double()
-    from paper_2407_13096_b200 import _lib
-    ctx._raise(_lib.lib().dso_probe_fp32_peak(ctx._h, 1, __import__("ctypes").byref(v)))
-    line = {
-        "metric": "predictor training sample-steps/s (C5)", "value": value,
-        "unit": "samples/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic (gen_kernel stream generated on device)",
-        "config": {"workload": cfg["desc"], "samples_per_gpu": n, "batch_per_gpu": B,
-                   "global_batch": B * world, "parallelism": f"dp{world} (NCCL allreduce)"},
-        "roofline": {"bound": "fp32", "achieved": achieved, "peak": v.value, "unit": "TFLOP/s",
-                     "frac": achieved / v.value, "traffic": ncu_traffic("c5", B),
-                     "traffic_unit": "bytes per dso_train_grad (ncu, profiles/ncu_summary.json)",
-                     "kernel": "train_fb_kernel + train_wgrad_kernel + reduce_partials",
-                     "flops_per_sample": TRAIN_FLOPS, "grad_kernel_ms": grad_ms},
-        "gpu_launches": ctx.launch_count - launches0, "clocks": clk.summary(),
-    }
+    line["cpu_baseline"] = None
+    if not args.no_cpu and world == 1 and args.config in ("c2", "c3"):
+        line["cpu_baseline"] = cpu_baseline(args, CONFIGS[args.config], model)
     print(json.dumps(line), flush=True)
 
 
@@ -633,8 +722,30 @@ def cpu_baseline(args, cfg, model):
                        f"{det['sweep_s']:.2f} s")}
 
 
+def self_launch(args):
+    """`--gpus N` without a launcher: start N ranks of this script on this node (one
+    process per GPU), with the torchrun environment (RANK, LOCAL_RANK, WORLD_SIZE,
+    MASTER_ADDR=127.0.0.1, MASTER_PORT) and NCCL_DEBUG=INFO so NCCL's communicator
+    lines (nranks) land in stderr.  Returns the worst exit code."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    procs = []
+    for r in range(args.gpus):
+        env = dict(os.environ, RANK=str(r), LOCAL_RANK=str(r), WORLD_SIZE=str(args.gpus),
+                   LOCAL_WORLD_SIZE=str(args.gpus), MASTER_ADDR="127.0.0.1",
+                   MASTER_PORT=str(port))
+        env.setdefault("NCCL_DEBUG", "INFO")
+        procs.append(subprocess.Popen([sys.executable, os.path.abspath(__file__)] + sys.argv[1:],
+                                      env=env))
+    return max(p.wait() for p in procs)
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args))
     world = env_int("WORLD_SIZE", 1)
     rank = env_int("RANK", 0)
     local_rank = env_int("LOCAL_RANK", 0)
@@ -643,6 +754,7 @@ def main():
         import torch.distributed as dist
         if args.impl == "ours":
             torch.cuda.set_device(local_rank)
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
         dist.init_process_group("nccl" if args.impl == "ours" else "gloo")
     try:
         if args.impl == "reference":

@@ -29,6 +29,7 @@
 // as a scalar loop over brute_force_config would.
 #pragma once
 
+#include <array>
 #include <cstdint>
 #include <span>
 #include <string>
@@ -262,7 +263,9 @@ inline std::vector<TimeFit> fit_time_batch(const std::vector<DvfsConfig>& cfg,
         f.iterations = static_cast<int>(fit[6 * n + k]);
         f.rss_trace = {fit[7 * n + k]};
         for (int s = 0; s < S; ++s)
-            f.branch.push_back(f.alpha / cfg[s].fm_mhz >= f.beta / cfg[s].fc_mhz
+            // the reference's reassignment test (param_fit.cpp:93-94,212-213): the
+            // final branch is the last reassignment, alpha * (1/fm) >= beta * (1/fc)
+            f.branch.push_back(f.alpha * (1.0 / cfg[s].fm_mhz) >= f.beta * (1.0 / cfg[s].fc_mhz)
                                    ? TimeBranch::Memory
                                    : TimeBranch::Core);
     }

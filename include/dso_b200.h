@@ -69,6 +69,20 @@ const char* dso_last_error(const dso_ctx* ctx);
 const char* dso_status_name(int32_t status);
 /* Number of device kernel launches issued on ctx so far (evidence counter). */
 int64_t dso_launch_count(const dso_ctx* ctx);
+
+/* Device evidence counters: the work the kernels actually issued (accumulated
+ * per context; the call synchronises the context stream).  Indices:
+ *   DSO_CTR_TC_L1_KSTEPS  tcgen05 layer-1 k-steps (3 kind::tf32 MMAs of
+ *                         M128 x N112 x K8 each; CSR tiles skip all-zero chunks)
+ *   DSO_CTR_TC_L2_KSTEPS  tcgen05 layer-2 k-steps (3 MMAs of M128 x N64 x K8)
+ *   DSO_CTR_TC_TILES      128-kernel tiles processed by the tcgen05 engine
+ * reset != 0 zeroes them after the read.  Not a reference interface (bench
+ * evidence for roofline.achieved). */
+#define DSO_CTR_TC_L1_KSTEPS 0
+#define DSO_CTR_TC_L2_KSTEPS 1
+#define DSO_CTR_TC_TILES 2
+#define DSO_N_COUNTERS 8
+int32_t dso_get_counters(dso_ctx* ctx, uint64_t* out, int32_t n, int32_t reset);
 /* Tuning / verification switches (no reference counterpart; results never
  * depend on them).  key "fast_sweep": 1 (default) lets the FP32 sweeps use the
  * group-minimum argmin (bit-identical, see sweep_core.cuh), 0 forces the

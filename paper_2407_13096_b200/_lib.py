@@ -85,6 +85,8 @@ def _declare(L: C.CDLL) -> None:
     L.dso_status_name.restype = C.c_char_p
     L.dso_launch_count.argtypes = [vp]
     L.dso_launch_count.restype = i64
+    L.dso_get_counters.argtypes = [vp, P(u64), i32, i32]
+    L.dso_get_counters.restype = i32
     L.dso_set_option.argtypes = [vp, C.c_char_p, i64]
     L.dso_set_option.restype = i32
     L.dso_set_domain.argtypes = [vp, P(d), i32, P(d), i32, P(d)]
@@ -145,7 +147,7 @@ def _declare(L: C.CDLL) -> None:
 # Every symbol include/dso_b200.h declares (checked by tests/test_abi.py).
 EXPORTED = (
     "dso_ctx_create", "dso_ctx_destroy", "dso_ctx_set_stream", "dso_sync", "dso_last_error",
-    "dso_status_name", "dso_launch_count", "dso_set_option", "dso_set_domain", "dso_validate_domain", "dso_set_model", "dso_get_model",
+    "dso_status_name", "dso_launch_count", "dso_get_counters", "dso_set_option", "dso_set_domain", "dso_validate_domain", "dso_set_model", "dso_get_model",
     "dso_init_mlp", "dso_shuffled_indices", "dso_featurize", "dso_dcgm_mean", "dso_predict",
     "dso_sweep", "dso_sweep_f64", "dso_optimal_config", "dso_param_fit", "dso_eta_sweep", "dso_pipeline",
     "dso_pipeline_csr",

@@ -63,6 +63,39 @@ def _check(t, dtype, rows: int | None, name: str):
                        f"{name} must have shape [{rows}, ld], got {tuple(t.shape)}")
 
 
+_TORCH_OF = {}
+if torch is not None:
+    _TORCH_OF = {np.int32: (torch.int32,), np.uint32: (torch.int32,), np.float32: (torch.float32,),
+                 np.int64: (torch.int64,), np.float64: (torch.float64,)}
+
+
+def _check_host(t, dtypes, rows: int | None, name: str, dim: int = 2):
+    """Host-buffer (numpy / CPU tensor) twin of _check: the library reads these
+    through raw pointers, so dtype, rank, row count and contiguity must be exact."""
+    if _is_cuda(t):
+        raise DsoError(ErrorKind.InvalidArgument, f"{name}: mixed host and device buffers")
+    if torch is not None and isinstance(t, torch.Tensor):
+        ok = t.dtype in sum((_TORCH_OF[d] for d in dtypes), ())
+        contiguous = t.is_contiguous()
+        shape = tuple(t.shape)
+        got = t.dtype
+    elif isinstance(t, np.ndarray):
+        ok = t.dtype.type in dtypes
+        contiguous = t.flags.c_contiguous
+        shape = t.shape
+        got = t.dtype
+    else:
+        raise DsoError(ErrorKind.InvalidArgument, f"{name}: unsupported array type {type(t)}")
+    if not ok:
+        raise DsoError(ErrorKind.InvalidArgument,
+                       f"{name} must be {'/'.join(d.__name__ for d in dtypes)}, got {got}")
+    if not contiguous:
+        raise DsoError(ErrorKind.InvalidArgument, f"{name} must be contiguous")
+    if len(shape) != dim or (rows is not None and shape[0] != rows):
+        want = f"[{rows}, ld]" if dim == 2 else "1-D"
+        raise DsoError(ErrorKind.InvalidArgument, f"{name} must have shape {want}, got {shape}")
+
+
 class Context:
     """One device's state (stream, domain tables, model); dso_ctx in the C-ABI."""
 
@@ -123,6 +156,13 @@ class Context:
     def launch_count(self) -> int:
         """Device kernels launched through this context (evidence counter)."""
         return int(self._lib.dso_launch_count(self._h))
+
+    def counters(self, reset: bool = False) -> dict:
+        """dso_get_counters: work the kernels actually issued on this context
+        (tcgen05 layer-1 / layer-2 k-steps, 128-kernel tiles)."""
+        buf = (C.c_uint64 * 3)()
+        self._raise(self._lib.dso_get_counters(self._h, buf, 3, 1 if reset else 0))
+        return {"tc_l1_ksteps": int(buf[0]), "tc_l2_ksteps": int(buf[1]), "tc_tiles": int(buf[2])}
 
     def _empty(self, shape, dtype):
         return torch.empty(shape, dtype=dtype, device=f"cuda:{self.device}")
@@ -219,7 +259,10 @@ class Context:
                                      _ptr(out), _ptr(bad))
         if st and status_kind(st) == ErrorKind.OutOfRange:
             rowk = bad[:n].cpu().numpy()
-            first = int(np.flatnonzero(rowk)[0])
+            nz = np.flatnonzero(rowk)
+            if len(nz) == 0:
+                self._raise(st)
+            first = int(nz[0])
             raise DsoError(ErrorKind.OutOfRange,
                            f"kernel {first}: row {int(rowk[first])}: metric value outside [0, 1]")
         self._raise(st)
@@ -376,6 +419,13 @@ class Context:
         if not host:
             _check(counts, torch.int32, 126, "counts")
             _check(dcgm, torch.float32, 8, "dcgm")
+        else:
+            _check_host(counts, (np.uint32, np.int32), 126, "counts")
+            _check_host(dcgm, (np.float32,), 8, "dcgm")
+        if dcgm.shape[1] != ld:
+            raise DsoError(ErrorKind.InvalidArgument, "counts and dcgm must share ld")
+        if not 0 <= n <= ld:
+            raise DsoError(ErrorKind.InvalidArgument, "batch requires 0 <= n <= ld")
         self._raise(self._lib.dso_pipeline(
             self._h, _ptr(counts), _ptr(dcgm), n, ld, eta, pmax, _ptr(out.get("params")),
             _ptr(out.get("clamped")), _ptr(out["idx"]), _ptr(out.get("cost")),
@@ -390,14 +440,24 @@ class Context:
         on the device; CPU (pinned) tensors / numpy go through the chunked host path."""
         pmax = self.domain.dev.pmax_w if pmax_w is None else pmax_w
         host = not _is_cuda(row_ptr)
+        if host:
+            _check_host(row_ptr, (np.int64,), None, "row_ptr", dim=1)
+            _check_host(entries, (np.int32, np.uint32), None, "entries", dim=1)
+            _check_host(dcgm, (np.float32,), 8, "dcgm")
+        else:
+            for t, dt, name in ((row_ptr, torch.int64, "row_ptr"), (entries, torch.int32, "entries")):
+                if not _is_cuda(t) or t.dtype != dt or t.dim() != 1 or not t.is_contiguous():
+                    raise DsoError(ErrorKind.InvalidArgument,
+                                   f"{name} must be a contiguous 1-D CUDA {dt} tensor")
+            _check(dcgm, torch.float32, 8, "dcgm")
         ld = dcgm.shape[1]
         n = ld if n is None else n
+        if not 0 <= n <= ld:
+            raise DsoError(ErrorKind.InvalidArgument, "batch requires 0 <= n <= ld")
         if row_ptr.shape[0] < n + 1:
             raise DsoError(ErrorKind.InvalidArgument, "row_ptr needs n + 1 entries")
         if out is None:
             out = self.alloc_pipeline_out(ld, host=host, want_params=want_params, like=dcgm)
-        if not host:
-            _check(dcgm, torch.float32, 8, "dcgm")
         self._raise(self._lib.dso_pipeline_csr(
             self._h, _ptr(row_ptr), _ptr(entries), C.c_uint64(ent_base), _ptr(dcgm), n, ld, eta,
             pmax, _ptr(out.get("params")), _ptr(out.get("clamped")), _ptr(out["idx"]),

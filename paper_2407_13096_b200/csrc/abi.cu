@@ -166,6 +166,14 @@ int32_t dso_ctx_create(int32_t device, dso_ctx** out) {
     ctx->c.stream = ctx->c.own_stream;
     for (auto& s : ctx->c.aux) cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
     for (auto& ev : ctx->c.ev) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+    e = cudaMalloc(&ctx->c.counters_dev, sizeof(unsigned long long) * DSO_N_COUNTERS);
+    if (e == cudaSuccess)
+        e = cudaMemset(ctx->c.counters_dev, 0, sizeof(unsigned long long) * DSO_N_COUNTERS);
+    if (e != cudaSuccess) {
+        cudaStreamDestroy(ctx->c.own_stream);
+        delete ctx;
+        return kCuda;
+    }
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     ctx->c.num_sms = sms > 0 ? sms : 148;
@@ -193,6 +201,7 @@ int32_t dso_ctx_destroy(dso_ctx* ctx) {
     cudaFree(c.model.w_train);
     cudaFree(c.scratch);
     cudaFree(c.train_scratch);
+    cudaFree(c.counters_dev);
     for (auto& s : c.aux)
         if (s) cudaStreamDestroy(s);
     for (auto& ev : c.ev)
@@ -242,6 +251,19 @@ const char* dso_status_name(int32_t st) {
 }
 
 int64_t dso_launch_count(const dso_ctx* ctx) { return ctx ? ctx->c.launches : 0; }
+
+int32_t dso_get_counters(dso_ctx* ctx, uint64_t* out, int32_t n, int32_t reset) {
+    if (!ctx || n < 0 || (n > 0 && !out)) return kInvalidArgument;
+    if (n > DSO_N_COUNTERS) return fail(ctx, kInvalidArgument, "more counters requested than exist");
+    Ctx& c = ctx->c;
+    DSO_CUDA(ctx, cudaSetDevice(c.device));
+    DSO_CUDA(ctx, cudaStreamSynchronize(c.stream));
+    unsigned long long h[DSO_N_COUNTERS] = {};
+    DSO_CUDA(ctx, cudaMemcpy(h, c.counters_dev, sizeof(h), cudaMemcpyDeviceToHost));
+    for (int i = 0; i < n; ++i) out[i] = h[i];
+    if (reset) DSO_CUDA(ctx, cudaMemset(c.counters_dev, 0, sizeof(h)));
+    return kOk;
+}
 
 int32_t dso_set_option(dso_ctx* ctx, const char* key, int64_t value) {
     if (!ctx || !key) return kInvalidArgument;
@@ -662,8 +684,6 @@ int32_t dso_eta_sweep(dso_ctx* ctx, const float* params, int64_t n, int64_t ld,
     if (c.eta_cap < n_eta) {
         DSO_CUDA(ctx, cudaStreamSynchronize(c.stream));
         cudaFree(c.eta_dev);
-    cudaFree(c.flag_dev);
-    fit_plan_free(c);
         c.eta_dev = nullptr;
         c.eta_cap = 0;
         DSO_CUDA(ctx, cudaMalloc(&c.eta_dev, sizeof(float2) * n_eta));

@@ -4,11 +4,27 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <mutex>
+#include <set>
 #include <string>
+#include <utility>
 
 #include "../../include/dso_b200.h"
 
 namespace dso_b200 {
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) is per device: remember, per
+// (kernel, device), that it has been applied. Thread-safe; contexts on several
+// devices of one process each get the attribute on their own device.
+inline cudaError_t ensure_smem_attr(const void* func, int device, int bytes) {
+    static std::mutex mu;
+    static std::set<std::pair<const void*, int>> done;
+    std::lock_guard<std::mutex> lock(mu);
+    if (done.count({func, device})) return cudaSuccess;
+    cudaError_t e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess) done.insert({func, device});
+    return e;
+}
 
 // 1 + dso::ErrorKind (reference proj/include/dso/error.hpp:10-25)
 enum Status : int32_t {
@@ -105,6 +121,8 @@ struct Ctx {
     void* fit_plan = nullptr;       // dso_param_fit's factored designs (fit.cu)
     void* train_scratch = nullptr;  // per-CTA partial gradients
     size_t train_scratch_bytes = 0;
+    // device evidence counters (dso_get_counters): work the kernels actually issued
+    unsigned long long* counters_dev = nullptr;
 };
 
 }  // namespace dso_b200

@@ -111,12 +111,9 @@ cudaError_t launch_featurize(Ctx& cx, const uint32_t* counts, const float* dcgm,
                              int64_t ld, float* fused) {
     if (n <= 0) return cudaSuccess;
     const size_t smem = (size_t)(DSO_FUSED_ROWS * kFeatTile + 1024) * sizeof(float);
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(featurize_kernel,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    {
+        cudaError_t e = ensure_smem_attr((const void*)featurize_kernel, cx.device, (int)smem);
         if (e != cudaSuccess) return e;
-        attr = true;
     }
     const int64_t tiles = (n + kFeatTile - 1) / kFeatTile;
     const int grid = (int)std::min<int64_t>(tiles, (int64_t)cx.num_sms * 2);  // 2 CTAs per SM (registers)

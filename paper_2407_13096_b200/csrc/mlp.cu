@@ -622,6 +622,9 @@ struct Job {
     float* energy;
     float* time;
     int64_t ld_out;
+    // evidence counters (Ctx::counters_dev): [0] tcgen05 layer-1 k-steps issued,
+    // [1] layer-2 k-steps issued, [2] 128-kernel tiles; NULL = not counted
+    unsigned long long* counters;
 };
 
 // OR of a predicate over the producer warps (named-barrier reduction).
@@ -1204,16 +1207,13 @@ cudaError_t launch_tc(Ctx& cx, const Job& J) {
     Job Jl = J;
     Jl.pairs = PIPE && tce::tc_smem_bytes(J.nc, J.nm, true) <= 227 * 1024;
     const size_t smem = tce::tc_smem_bytes(PIPE ? J.nc : 0, PIPE ? J.nm : 0, Jl.pairs);
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(tce::tc_kernel<MODE>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             227 * 1024);
+    {
+        cudaError_t e = ensure_smem_attr((const void*)tce::tc_kernel<MODE>, cx.device, 227 * 1024);
         if (e != cudaSuccess) return e;
-        attr = true;
     }
     const int64_t tiles = (J.n + tce::TT - 1) / tce::TT;
     const int grid = (int)(tiles < cx.num_sms ? tiles : cx.num_sms);
+    Jl.counters = cx.counters_dev;
     tce::tc_kernel<MODE><<<grid, tce::kThreadsTC, smem, cx.stream>>>(cx.model.wtc, stats_of(cx), Jl);
     ++cx.launches;
     return cudaGetLastError();
@@ -1242,13 +1242,9 @@ cudaError_t launch_ws(Ctx& cx, const Job& J0) {
     Jl.pairs = PIPE && ws_smem_bytes(J.nc, J.nm, true) <= 227 * 1024;
     const size_t smem = ws_smem_bytes(PIPE ? J.nc : 0, PIPE ? J.nm : 0, Jl.pairs);
     if (smem > 227 * 1024) return cudaErrorInvalidValue;
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(ws_kernel<MODE>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             227 * 1024);
+    {
+        cudaError_t e = ensure_smem_attr((const void*)ws_kernel<MODE>, cx.device, 227 * 1024);
         if (e != cudaSuccess) return e;
-        attr = true;
     }
     const int64_t tiles = (J.n + TM - 1) / TM;
     const int grid = (int)(tiles < cx.num_sms ? tiles : cx.num_sms);

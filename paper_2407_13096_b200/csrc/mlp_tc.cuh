@@ -404,6 +404,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
                 return tc::sdesc(s0 + off * 4 + kk * 256, 128, (uint32_t)(K >> 2) * 128);
             };
             uint32_t g = 0;  // ring chunks consumed
+            unsigned long long n_l1 = 0, n_l2 = 0;  // k-steps issued (evidence counters)
             // Event-driven issue: L1 of the next tile and L2..L4 of the current one are
             // independent streams of k-steps; each is issued as soon as its operand
             // chunk is ready (non-blocking mbarrier tests), in one tensor-core queue.
@@ -426,6 +427,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
                 tc::mma_tf32_ss(D, al, bd(W1H, st.c, K1), id1, 1u);
                 tc::commit(mb + MB_XEMPTY + b);
                 ++g;
+                ++n_l1;
                 int nc = st.c + 1;
                 while (nc < 17 && !((st.mask >> nc) & 1u)) ++nc;
                 if (nc >= 17) {
@@ -456,6 +458,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
                     tc::mma_tf32_ts(tbase + TD2, S + 8 * c2, bd(W2H, c2, K2), id2, c2 > 0 ? 1u : 0u);
                     tc::mma_tf32_ts(tbase + TD2, S + 8 * c2, bd(W2L, c2, K2), id2, 1u);
                     tc::mma_tf32_ts(tbase + TD2, S + A2LO + 8 * c2, bd(W2H, c2, K2), id2, 1u);
+                    ++n_l2;
                     if (++c2 == 13) {
                         tc::commit(mb + MB_D2F + sl);
                         ++b;
@@ -464,6 +467,11 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
                         break;
                     }
                 }
+            }
+            if (J.counters) {
+                atomicAdd(J.counters + 0, n_l1);
+                atomicAdd(J.counters + 1, n_l2);
+                atomicAdd(J.counters + 2, (unsigned long long)my_tiles);
             }
         }
         __syncwarp();

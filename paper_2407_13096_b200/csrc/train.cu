@@ -669,17 +669,13 @@ cudaError_t launch_train_grad(Ctx& cx, const float* x, const float* y, int64_t n
     float* partial = (float*)cx.train_scratch;
     double* lp = (double*)(partial + (size_t)parts * kMasterFloats);
     float* act = (float*)(((uintptr_t)(lp + parts) + 255) & ~(uintptr_t)255);
-    static bool attr = false;
     const size_t smem = (size_t)kSmemFloats * sizeof(float);
     const size_t smem_wg = (size_t)2 * WG_CHUNK * WG_REC * sizeof(float);
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(train_fb_kernel,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    {
+        cudaError_t e = ensure_smem_attr((const void*)train_fb_kernel, cx.device, (int)smem);
         if (e != cudaSuccess) return e;
-        e = cudaFuncSetAttribute(train_wgrad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem_wg);
+        e = ensure_smem_attr((const void*)train_wgrad_kernel, cx.device, (int)smem_wg);
         if (e != cudaSuccess) return e;
-        attr = true;
     }
     // grids sized to the batch (small batches launch few CTAs); every launched CTA
     // writes its partial, and the reduction reads exactly those

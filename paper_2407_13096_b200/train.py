@@ -275,9 +275,12 @@ def cross_validate(ctx, features, targets, grid, seed: int, epochs: int, sizes=N
     return {"table": table, "best": (best[0], best[1])}
 
 
-def train(ctx, features, targets, grid, seed: int, epochs: int, sizes=None):
+def train(ctx, features, targets, grid, seed: int, epochs: int, sizes=None,
+          learning_rate: float = 0.1, batch_size: int = 16):
     """train (mlp.cpp:413-437): checks, cross-validation over grid, then a final
-    fit_model on the whole canonical dataset with the winning cell.
+    fit_model on the whole canonical dataset with the winning cell. An empty grid
+    means the single cell (learning_rate, batch_size), as TrainConfig's defaults
+    (mlp.hpp:75-89, mlp.cpp:424-427).
     Returns {"model", "cv", "epoch_loss", "degenerate_targets"}."""
     from ._lib import DsoError, ErrorKind
     f = np.asarray(features, np.float64)
@@ -290,6 +293,8 @@ def train(ctx, features, targets, grid, seed: int, epochs: int, sizes=None):
     f, t = canonicalize(f, t)
     sizes = list(sizes) if sizes else [f.shape[1], 100, 50, 25, t.shape[1]]
     sizes[0], sizes[-1] = f.shape[1], t.shape[1]
+    if not grid:
+        grid = [(float(learning_rate), int(batch_size))]
     cv = cross_validate(ctx, f, t, grid, seed, epochs, sizes)
     mean, std, degenerate = target_stats(t)
     lr, bs = cv["best"]

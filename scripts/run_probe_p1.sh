@@ -1,5 +1,6 @@
 set -u
 OUT=gpurun_out/p1; mkdir -p $OUT
+nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o scripts/probes/lds_probe scripts/probes/lds_probe.cu
 ncu --metrics l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum,smsp__inst_executed_op_shared_ld.sum --csv scripts/probes/lds_probe > $OUT/lds_probe.csv 2>&1
 timeout 900 python -m pytest tests/test_gpu_pipeline.py tests/test_gpu_mlp.py tests/test_gpu_cpp.py -q -x > $OUT/pytest.log 2>&1; echo rc=$? >> $OUT/pytest.log
 timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu --no-e2e > $OUT/bench.log 2>&1

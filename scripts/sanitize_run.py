@@ -35,5 +35,17 @@ for cfg in ("c1", "c3"):
         gr, loss = ctx.train_grad(f, y)
         ctx.train_apply(gr, 0.01, 1.0 / n)
         ctx.dcgm_mean(torch.rand((3, 8, n), device="cuda", dtype=torch.float64))
+# per-context scratch in any call order (regression: the eta table's growth once
+# freed the dcgm_mean flag), then destroy
+c2 = Context(0)
+c2.set_domain(config_domain("c3"))
+s = torch.rand((4, 8, 257), device="cuda", dtype=torch.float64)
+c2.dcgm_mean(s)
+pp = c2.gen_synthetic(1000, root=5, counts=False, dcgm=False)["params"]
+c2.eta_sweep(pp, np.arange(5) / 4.0)
+c2.dcgm_mean(s)
+c2.eta_sweep(pp, np.arange(101) / 100.0)
+c2.dcgm_mean(s)
+c2.close()
 torch.cuda.synchronize()
 print("sanitize run ok")

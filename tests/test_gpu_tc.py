@@ -16,9 +16,20 @@ from paper_2407_13096_b200 import _lib
 pytestmark = pytest.mark.gpu
 
 
+_PROBE = None
+
+
+def probe_lib():
+    """The test-only probe library (csrc/tcprobe.cu, not part of libdso_b200.so)."""
+    global _PROBE
+    if _PROBE is None:
+        import os
+        _PROBE = C.CDLL(os.path.join(os.path.dirname(_lib.LIB_PATH), "libdso_tcprobe.so"))
+    return _PROBE
+
+
 def tc_gemm(a, b, passes, reps=1):
-    L = _lib.lib()
-    f = L.dso_debug_tc_gemm
+    f = probe_lib().dso_debug_tc_gemm
     f.argtypes = [C.c_void_p] * 3 + [C.c_int32] * 4 + [C.c_void_p]
     f.restype = C.c_int32
     A = torch.from_numpy(np.ascontiguousarray(a, np.float32)).cuda()
