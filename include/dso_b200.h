@@ -243,6 +243,43 @@ int32_t dso_train_grad(dso_ctx* ctx, const float* x, const float* y_std, int64_t
                        int64_t ld, float* grad, double* loss_sum);
 /* W -= lr * scale * grad  (sgd update, mlp.cpp:105-108). */
 int32_t dso_train_apply(dso_ctx* ctx, const float* grad, double lr, double scale);
+
+/* One synchronous data-parallel SGD step inside the library (SURVEY.md §8(b),
+ * §8(e)): the batch-sum gradient of this rank's n samples -> ncclAllReduce(sum)
+ * of the gradient and the loss over `nccl_comm` (an ncclComm_t; NULL = one
+ * process) -> W -= lr / (global_batch * out) * g on every rank (mse_loss's
+ * 1/(B*out), mlp.cpp:259-289; update mlp.cpp:105-108).  loss (host, optional:
+ * NULL keeps the call asynchronous) receives mse_loss of the global batch on
+ * the pre-update weights. */
+int32_t dso_train_step(dso_ctx* ctx, const float* x, const float* y_std, int64_t n, int64_t ld,
+                       double lr, int64_t global_batch, void* nccl_comm, double* loss);
+
+/* fit_model's epoch loop (mlp.cpp:84-130) on the device model set with
+ * dso_set_model (the caller does init_mlp + target stats, as fit_model does):
+ * per epoch the order shuffled_indices(Rng(seed).fork(0x5d0)) (rng.hpp:58-64,
+ * mlp.cpp:87,123), contiguous batches of `batch` (last one partial), each
+ * batch's mse_loss on the pre-update weights, W -= lr * g; epoch_loss[e]
+ * (host, optional, >= epochs entries) = the mean batch loss; stops after a
+ * NaN epoch (mlp.cpp:126), *epochs_run = epochs completed.  x [in][ld],
+ * y_std [out][ld] device, the WHOLE dataset on every rank; with nranks > 1 each
+ * rank takes the contiguous share [b*rank/nranks, b*(rank+1)/nranks) of every
+ * batch and the gradients are summed over nccl_comm, so replicas stay
+ * identical and equal the single-device run up to FP32 summation order.
+ * Single-process epochs run as one CUDA graph replay each. */
+int32_t dso_fit_model(dso_ctx* ctx, const float* x, const float* y_std, int64_t n, int64_t ld,
+                      double lr, int32_t batch, int32_t epochs, uint64_t seed, void* nccl_comm,
+                      int32_t rank, int32_t nranks, double* epoch_loss, int32_t* epochs_run);
+
+/* NCCL, reached through dlopen (the copy already loaded in the process if any):
+ * a unique id (DSO_NCCL_ID_BYTES bytes, broadcast by the host over any channel),
+ * a communicator for (nranks, rank) on `device`, its destruction, the version.
+ * IoError when no libnccl.so.2 is available. */
+#define DSO_NCCL_ID_BYTES 128
+int32_t dso_nccl_unique_id(uint8_t* id);
+int32_t dso_nccl_comm_init(int32_t nranks, const uint8_t* id, int32_t rank, int32_t device,
+                           void** comm);
+int32_t dso_nccl_comm_destroy(void* comm);
+int32_t dso_nccl_version(int32_t* version);
 /* Number of parameters (weights + biases) of the device model. */
 int64_t dso_model_param_count(const dso_ctx* ctx);
 

@@ -132,6 +132,18 @@ def _declare(L: C.CDLL) -> None:
     L.dso_gen_synthetic.argtypes = [vp, u64, u64, i64, i64, i64, vp, vp, vp]
     L.dso_train_grad.argtypes = [vp, vp, vp, i64, i64, vp, vp]
     L.dso_train_apply.argtypes = [vp, vp, d, d]
+    L.dso_train_step.argtypes = [vp, vp, vp, i64, i64, d, i64, vp, P(d)]
+    L.dso_train_step.restype = i32
+    L.dso_fit_model.argtypes = [vp, vp, vp, i64, i64, d, i32, i32, u64, vp, i32, i32, P(d), P(i32)]
+    L.dso_fit_model.restype = i32
+    L.dso_nccl_unique_id.argtypes = [vp]
+    L.dso_nccl_unique_id.restype = i32
+    L.dso_nccl_comm_init.argtypes = [i32, vp, i32, i32, P(vp)]
+    L.dso_nccl_comm_init.restype = i32
+    L.dso_nccl_comm_destroy.argtypes = [vp]
+    L.dso_nccl_comm_destroy.restype = i32
+    L.dso_nccl_version.argtypes = [P(i32)]
+    L.dso_nccl_version.restype = i32
     L.dso_probe_fp32_peak.argtypes = [vp, i32, P(d)]
     L.dso_probe_fp32_peak.restype = i32
     L.dso_model_param_count.argtypes = [vp]
@@ -152,7 +164,9 @@ EXPORTED = (
     "dso_sweep", "dso_sweep_f64", "dso_optimal_config", "dso_param_fit", "dso_eta_sweep", "dso_pipeline",
     "dso_pipeline_csr",
     "dso_gen_synthetic", "dso_gen_synthetic_csr",
-    "dso_train_grad", "dso_train_apply", "dso_model_param_count", "dso_probe_fp32_peak",
+    "dso_train_grad", "dso_train_apply", "dso_train_step", "dso_fit_model",
+    "dso_nccl_unique_id", "dso_nccl_comm_init", "dso_nccl_comm_destroy", "dso_nccl_version",
+    "dso_model_param_count", "dso_probe_fp32_peak",
     "dso_ptx_parse", "dso_ptx_free", "dso_ptx_kernel_count", "dso_ptx_kernel_name",
     "dso_ptx_kernel_counts", "dso_ptx_counts", "dso_ptx_nnz", "dso_ptx_csr", "dso_load_dcgm_csv",
 )

@@ -521,3 +521,71 @@ class Context:
     def train_apply(self, grad, lr: float, scale: float) -> None:
         """W -= lr * scale * grad on the device model (mlp.cpp:105-108)."""
         self._raise(self._lib.dso_train_apply(self._h, _ptr(grad), lr, scale))
+
+    def train_step(self, x, y_std, lr: float, global_batch: int, n: int | None = None,
+                   comm=None, want_loss: bool = True):
+        """dso_train_step: one data-parallel SGD step inside the library (gradient ->
+        NCCL allreduce over `comm` (NcclComm or None) -> update).  Returns the global
+        batch's mse_loss on the pre-update weights (float) or None."""
+        _check(x, torch.float32, None, "x")
+        _check(y_std, torch.float32, None, "y_std")
+        ld = x.shape[1]
+        n = ld if n is None else n
+        loss = C.c_double()
+        self._raise(self._lib.dso_train_step(self._h, _ptr(x), _ptr(y_std), n, ld, float(lr),
+                                             int(global_batch), None if comm is None else comm.handle,
+                                             C.byref(loss) if want_loss else None))
+        return loss.value if want_loss else None
+
+    def fit_model(self, x, y_std, lr: float, batch: int, epochs: int, seed: int, comm=None,
+                  rank: int = 0, nranks: int = 1):
+        """dso_fit_model: fit_model's epoch loop (mlp.cpp:84-130) on the device model
+        (set beforehand); x [in, n], y_std [out, n] CUDA float32.  Returns the
+        epoch-loss trace (list, NaN-terminated on divergence)."""
+        _check(x, torch.float32, None, "x")
+        _check(y_std, torch.float32, None, "y_std")
+        n = x.shape[1]
+        trace = (C.c_double * max(epochs, 1))()
+        ran = C.c_int32()
+        self._raise(self._lib.dso_fit_model(self._h, _ptr(x), _ptr(y_std), n, n, float(lr),
+                                            int(batch), int(epochs), C.c_uint64(seed),
+                                            None if comm is None else comm.handle, rank, nranks,
+                                            trace, C.byref(ran)))
+        return [float(trace[i]) for i in range(ran.value)]
+
+
+class NcclComm:
+    """An NCCL communicator created by the library (dso_nccl_comm_init) for the
+    ranks of a torch.distributed group: rank 0's unique id is broadcast over the
+    group (any backend), then every rank joins on its device."""
+
+    def __init__(self, device: int, group=None):
+        import torch.distributed as dist
+        L = lib()
+        self._lib = L
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        uid = (C.c_uint8 * 128)()
+        if rank == 0:
+            st = L.dso_nccl_unique_id(uid)
+            if st:
+                raise DsoError(status_kind(st), "dso_nccl_unique_id failed (is libnccl.so.2 loadable?)")
+        obj = [bytes(uid)]
+        dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group else 0,
+                                   group=group)
+        uid = (C.c_uint8 * 128).from_buffer_copy(obj[0])
+        h = C.c_void_p()
+        st = L.dso_nccl_comm_init(world, uid, rank, device, C.byref(h))
+        if st:
+            raise DsoError(status_kind(st), "dso_nccl_comm_init failed")
+        self.handle, self.rank, self.world = h, rank, world
+
+    def close(self):
+        if getattr(self, "handle", None):
+            self._lib.dso_nccl_comm_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

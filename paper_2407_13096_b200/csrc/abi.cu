@@ -202,6 +202,8 @@ int32_t dso_ctx_destroy(dso_ctx* ctx) {
     cudaFree(c.scratch);
     cudaFree(c.train_scratch);
     cudaFree(c.counters_dev);
+    cudaFree(c.dp_grad);
+    cudaFree(c.dp_dbl);
     for (auto& s : c.aux)
         if (s) cudaStreamDestroy(s);
     for (auto& ev : c.ev)
@@ -385,6 +387,7 @@ int32_t dso_set_model(dso_ctx* ctx, const int32_t* sizes, int32_t n_sizes, const
     DSO_CUDA(ctx, cudaSetDevice(c.device));
     ModelDev& md = c.model;
     for (int i = 0; i < 5; ++i) md.sizes[i] = sizes[i];
+    md.n_layers = n_sizes;
     for (int i = 0; i < 8; ++i) {
         md.mean[i] = i < out ? (float)mean[i] : 0.f;
         md.std_[i] = i < out ? (float)std_[i] : 1.f;

@@ -75,6 +75,7 @@ struct DomainDev {
 // for the device path (the reference trains probe nets only in unit tests).
 struct ModelDev {
     int sizes[5];
+    int n_layers = 5;  // entries of sizes (layers + 1)
     float* wt;       // packed per-layer transposed weights (see mlp.cu layout)
     float* bias;     // packed biases (padded)
     float mean[8], std_[8];
@@ -123,6 +124,10 @@ struct Ctx {
     size_t train_scratch_bytes = 0;
     // device evidence counters (dso_get_counters): work the kernels actually issued
     unsigned long long* counters_dev = nullptr;
+    // dso_train_step / dso_fit_model (dp.cu): gradient and loss buffers
+    float* dp_grad = nullptr;
+    double* dp_dbl = nullptr;
+    int64_t dp_np = 0;
 };
 
 }  // namespace dso_b200
@@ -174,7 +179,12 @@ cudaError_t launch_gen_csr(Ctx& c, uint64_t root, uint64_t salt_base, int64_t fi
 cudaError_t model_upload(Ctx& c, const double* W, const double* b);
 cudaError_t launch_train_grad(Ctx& c, const float* x, const float* y, int64_t n, int64_t ld,
                               float* grad, double* loss_sum_dev);
-cudaError_t launch_train_apply(Ctx& c, const float* grad, float lr_scale);
+// repack = false leaves the inference kernels' packed weights stale (training
+// loops repack once at the end, dp.cu)
+cudaError_t launch_train_apply(Ctx& c, const float* grad, float lr_scale, bool repack = true);
+// allocations (scratch, weight image) and kernel attributes for batches of up to
+// n samples, without launching: makes the next gradients capturable
+cudaError_t train_prepare(Ctx& c, int64_t n);
 cudaError_t launch_repack(Ctx& c);  // w_master (f32, reference layout) -> packed wt
 size_t mlp_smem_bytes();
 

@@ -650,6 +650,31 @@ __global__ void sgd_apply(float* __restrict__ master, const float* __restrict__ 
 
 }  // namespace
 
+cudaError_t train_prepare(Ctx& cx, int64_t n) {
+    const int parts = cx.num_sms;
+    const int64_t lds = ((n + TM - 1) / TM) * TM;
+    const size_t need = (size_t)parts * kMasterFloats * sizeof(float) + (size_t)parts * sizeof(double) +
+                        (size_t)kScratchRows * (size_t)(lds > 0 ? lds : TM) * sizeof(float) + 256;
+    if (cx.train_scratch_bytes < need) {
+        cudaFree(cx.train_scratch);
+        cx.train_scratch = nullptr;
+        cx.train_scratch_bytes = 0;
+        cudaError_t e = cudaMalloc(&cx.train_scratch, need);
+        if (e != cudaSuccess) return e;
+        cx.train_scratch_bytes = need;
+    }
+    if (!cx.model.w_train) {
+        cudaError_t e = cudaMalloc(&cx.model.w_train, sizeof(float) * A0S);
+        if (e != cudaSuccess) return e;
+        cx.model.train_dirty = true;
+    }
+    cudaError_t e = ensure_smem_attr((const void*)train_fb_kernel, cx.device,
+                                     (int)((size_t)kSmemFloats * sizeof(float)));
+    if (e != cudaSuccess) return e;
+    return ensure_smem_attr((const void*)train_wgrad_kernel, cx.device,
+                            (int)((size_t)2 * WG_CHUNK * WG_REC * sizeof(float)));
+}
+
 cudaError_t launch_train_grad(Ctx& cx, const float* x, const float* y, int64_t n, int64_t ld,
                               float* grad, double* loss_sum_dev) {
     const int parts = cx.num_sms;
@@ -709,13 +734,13 @@ cudaError_t launch_train_grad(Ctx& cx, const float* x, const float* y, int64_t n
     return cudaGetLastError();
 }
 
-cudaError_t launch_train_apply(Ctx& cx, const float* grad, float lr_scale) {
+cudaError_t launch_train_apply(Ctx& cx, const float* grad, float lr_scale, bool repack) {
     cx.model.train_dirty = true;
     sgd_apply<<<(kMasterFloats + 255) / 256, 256, 0, cx.stream>>>(cx.model.w_master, grad,
                                                                   lr_scale);
     ++cx.launches;
     cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
+    if (e != cudaSuccess || !repack) return e;
     return launch_repack(cx);  // inference kernels see the updated weights
 }
 

@@ -142,13 +142,12 @@ def _dev_cols(a):
 
 
 def fit_model(ctx, features, targets, sizes, mean, std, lr: float, batch_size: int,
-              epochs: int, seed: int, use_graph: bool = True):
-    """fit_model (mlp.cpp:115-130) on the GPU: init_mlp(sizes, seed), per-epoch
-    sgd_epoch (mlp.cpp:84-112) with order shuffled_indices(Rng(seed).fork(0x5d0)),
-    loss of every batch on the pre-update weights, stop after a NaN epoch.
-    Returns (model, epoch_loss_trace)."""
-    import torch
-
+              epochs: int, seed: int, comm=None, rank: int = 0, nranks: int = 1):
+    """fit_model (mlp.cpp:115-130) on the GPU: init_mlp(sizes, seed) with the given
+    target stats, then the library's native epoch loop (dso_fit_model: per-epoch
+    order shuffled_indices(Rng(seed).fork(0x5d0)), contiguous batches, the loss of
+    every batch on the pre-update weights, stop after a NaN epoch; one CUDA graph
+    replay per epoch).  Returns (model, epoch_loss_trace)."""
     from .model import init_mlp
     m = init_mlp(list(sizes), seed=seed)
     m.target_mean, m.target_std = np.array(mean, np.float64), np.array(std, np.float64)
@@ -156,67 +155,8 @@ def fit_model(ctx, features, targets, sizes, mean, std, lr: float, batch_size: i
     f = np.asarray(features, np.float64)
     y = (np.asarray(targets, np.float64) - m.target_mean) / m.target_std
     X, Y = _dev_cols(f), _dev_cols(y)
-    n = X.shape[1]
-    out_dim = Y.shape[0]
-    state = fork(seed, 0x5D0)
-    grad = torch.empty((ctx.n_model_params,), dtype=torch.float32, device=X.device)
-    trace = []
-    batches = list(epoch_batches(n, batch_size))
-    # The epoch's launch sequence is fixed for a given (n, batch size) — only the
-    # shuffled order changes — so it is captured once into a CUDA graph (order
-    # upload, gathers, every batch's gradient + update, the loss sum) and replayed
-    # per epoch; the host writes the next order into a pinned buffer in between.
-    idx_host = torch.empty(n, dtype=torch.int64).pin_memory()
-    idx_dev = torch.empty(n, dtype=torch.int64, device=X.device)
-    Xe, Ye = torch.empty_like(X), torch.empty_like(Y)
-    acc = torch.zeros((), dtype=torch.float64, device=X.device)
-
-    def epoch_body():
-        idx_dev.copy_(idx_host, non_blocking=True)
-        torch.index_select(X, 1, idx_dev, out=Xe)
-        torch.index_select(Y, 1, idx_dev, out=Ye)
-        acc.zero_()
-        for start, b in batches:
-            g, loss = ctx.train_grad_slice(Xe, Ye, start, b, grad=grad)
-            acc.add_(loss[0] / (b * out_dim))
-            ctx.train_apply(g, lr, 1.0 / (b * out_dim))
-
-    graph = None
-    if use_graph and epochs > 2:
-        # warm-up outside capture (allocations, function attributes), on a copy of
-        # the weights that is restored afterwards, then capture on a side stream
-        saved = ctx.get_model()
-        idx_host.copy_(torch.arange(n))
-        epoch_body()
-        torch.cuda.synchronize()
-        ctx.set_model(saved)
-        graph = torch.cuda.CUDAGraph()
-        home = torch.cuda.current_stream()
-        cap = torch.cuda.Stream()
-        cap.wait_stream(home)
-        with torch.cuda.stream(cap):
-            ctx.set_stream(cap)
-            try:
-                with torch.cuda.graph(graph, stream=cap):
-                    epoch_body()
-            finally:
-                ctx.set_stream(home)  # back to the caller's stream (not the capture stream)
-        home.wait_stream(cap)
-        torch.cuda.synchronize()
-        ctx.set_model(saved)  # the capture does not run the body, but be explicit
-    for _ in range(epochs):
-        order, state = shuffled_order(n, state)
-        torch.cuda.current_stream().synchronize()  # idx_host is read by the previous epoch
-        idx_host.copy_(torch.from_numpy(order))
-        if graph is not None:
-            graph.replay()
-        else:
-            epoch_body()
-        v = float(acc.item()) / len(batches)
-        v = v if math.isfinite(v) else float("nan")
-        trace.append(v)
-        if math.isnan(v):
-            break
+    trace = ctx.fit_model(X, Y, lr, batch_size, epochs, seed, comm=comm, rank=rank,
+                          nranks=nranks)
     return ctx.get_model(), trace
 
 
