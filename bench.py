@@ -494,7 +494,6 @@ def measure_train(ctx, args, rank, world, tm, peak, steps, warmup, model):
     shard of synthetic samples per GPU."""
     import torch
     from paper_2407_13096_b200 import linear_domain
-    from paper_2407_13096_b200.train import DataParallelTrainer
     cfg = CONFIGS["c5"]
     n = args.kernels if (args.kernels and args.config == "c5") else cfg["n"]
     ctx.set_domain(linear_domain(cfg["nc"], cfg["nm"]))
@@ -509,16 +508,14 @@ def measure_train(ctx, args, rank, world, tm, peak, steps, warmup, model):
     std = torch.tensor(model.target_std, dtype=torch.float64, device=dev)
     y = ((p - mean[:, None]) / std[:, None]).float().contiguous()
     del p, gen
-    tr = DataParallelTrainer(ctx, lr=0.1)
+    from paper_2407_13096_b200.api import NcclComm
+    comm = NcclComm(ctx.device) if world > 1 else None  # the library's own NCCL communicator
     nb = n // B
     grad = torch.empty((ctx.n_model_params,), dtype=torch.float32, device=dev)
 
     def step(i):
-        s0 = (i % nb) * B
-        g, loss = ctx.train_grad_slice(x, y, s0, B, grad=grad)
-        tr.allreduce(g)
-        tr.allreduce(loss)
-        ctx.train_apply(g, tr.lr, 1.0 / (B * world * 7))
+        # dso_train_step: gradient -> ncclAllReduce (in the library) -> update
+        ctx.train_step(x, y, 0.1, B * world, n=B, start=(i % nb) * B, comm=comm, want_loss=False)
 
     for i in range(warmup):
         step(i)
@@ -530,6 +527,8 @@ def measure_train(ctx, args, rank, world, tm, peak, steps, warmup, model):
     step_tflops = B * TRAIN_FLOPS / (ms * 1e-3) / 1e12
     ctx.set_model(model)  # training moved the weights
     del x, y
+    if comm is not None:
+        comm.close()
     return {"metric": "predictor training sample-steps/s (C5)", "value": B * world / (ms_max * 1e-3),
             "unit": "samples/s", "ms_per_step": ms_max, "steps": steps,
             "samples_per_gpu": n, "batch_per_gpu": B, "global_batch": B * world,
@@ -541,7 +540,7 @@ def measure_train(ctx, args, rank, world, tm, peak, steps, warmup, model):
                                        "note": "whole step incl. update and allreduce"},
                          "traffic": ncu_traffic("c5", B),
                          "traffic_unit": "bytes per dso_train_grad (ncu, profiles/ncu_summary.json)",
-                         "kernel": "dso_train_grad kernels", "flops_per_sample": TRAIN_FLOPS,
+                         "kernel": "dso_train_grad kernels (step: dso_train_step)", "flops_per_sample": TRAIN_FLOPS,
                          "grad_kernel_ms": grad_ms, "peak_source": PEAK_NOTE}}
 
 

@@ -133,6 +133,14 @@ int32_t dso_featurize(dso_ctx* ctx, const uint32_t* counts, const float* dcgm, i
 /* load_dcgm_samples mean (telemetry.cpp:73-89) over parsed rows:
  * samples double [rows][8][ld] -> out float [8][ld].  bad_row[k] = first
  * 1-based row with a value outside [0,1] (0 if none); status OutOfRange if any. */
+/* featurize + as_vector on the reference's 64-bit counts (KernelInstructionCounts
+ * maps are std::uint64_t, ptx_features.hpp:31-37): counts uint64 [126][ld], dcgm
+ * float [8][ld] -> fused float [134][ld].  Exact integer category totals, one
+ * FP64 division per count (the reference's double quotient), rounded once to
+ * float; equal to the reference for totals < 2^53. */
+int32_t dso_featurize_u64(dso_ctx* ctx, const uint64_t* counts, const float* dcgm, int64_t n,
+                          int64_t ld, float* fused);
+
 int32_t dso_dcgm_mean(dso_ctx* ctx, const double* samples, int64_t rows, int64_t n,
                       int64_t ld, float* out, int64_t* bad_row);
 

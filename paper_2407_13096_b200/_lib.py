@@ -97,6 +97,8 @@ def _declare(L: C.CDLL) -> None:
     L.dso_init_mlp.argtypes = [P(i32), i32, u64, P(d), P(d)]
     L.dso_shuffled_indices.argtypes = [u64, P(u64), P(u64)]
     L.dso_featurize.argtypes = [vp, vp, vp, i64, i64, vp]
+    L.dso_featurize_u64.argtypes = [vp, vp, vp, i64, i64, vp]
+    L.dso_featurize_u64.restype = i32
     L.dso_dcgm_mean.argtypes = [vp, vp, i64, i64, i64, vp, vp]
     L.dso_predict.argtypes = [vp, vp, i64, i64, vp, vp, vp]
     L.dso_sweep.argtypes = [vp, vp, i64, i64, d, d, vp, vp, vp, vp, vp]
@@ -160,7 +162,7 @@ def _declare(L: C.CDLL) -> None:
 EXPORTED = (
     "dso_ctx_create", "dso_ctx_destroy", "dso_ctx_set_stream", "dso_sync", "dso_last_error",
     "dso_status_name", "dso_launch_count", "dso_get_counters", "dso_set_option", "dso_set_domain", "dso_validate_domain", "dso_set_model", "dso_get_model",
-    "dso_init_mlp", "dso_shuffled_indices", "dso_featurize", "dso_dcgm_mean", "dso_predict",
+    "dso_init_mlp", "dso_shuffled_indices", "dso_featurize", "dso_featurize_u64", "dso_dcgm_mean", "dso_predict",
     "dso_sweep", "dso_sweep_f64", "dso_optimal_config", "dso_param_fit", "dso_eta_sweep", "dso_pipeline",
     "dso_pipeline_csr",
     "dso_gen_synthetic", "dso_gen_synthetic_csr",

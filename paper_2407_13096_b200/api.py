@@ -246,6 +246,20 @@ class Context:
                                             _ptr(fused)))
         return fused
 
+    def featurize_u64(self, counts, dcgm, n: int | None = None, out=None):
+        """featurize + as_vector on the reference's 64-bit counts: counts CUDA int64
+        [126, ld] (uint64 bit patterns), dcgm float32 [8, ld] -> fused [134, ld]."""
+        _check(counts, torch.int64, 126, "counts")
+        _check(dcgm, torch.float32, 8, "dcgm")
+        ld = counts.shape[1]
+        n = ld if n is None else n
+        if dcgm.shape[1] != ld:
+            raise DsoError(ErrorKind.InvalidArgument, "counts and dcgm must share ld")
+        fused = self._empty((134, ld), torch.float32) if out is None else out
+        self._raise(self._lib.dso_featurize_u64(self._h, _ptr(counts), _ptr(dcgm), n, ld,
+                                                _ptr(fused)))
+        return fused
+
     def dcgm_mean(self, samples, n: int | None = None):
         """samples: float64 [rows, 8, ld] -> (mean float32 [8, ld], bad_row int64 [ld])."""
         if not _is_cuda(samples) or samples.dtype != torch.float64 or samples.dim() != 3 \
@@ -270,16 +284,22 @@ class Context:
 
     # -- predictor ------------------------------------------------------------------
     def predict_params(self, fused, n: int | None = None, want_raw: bool = False):
-        """predict_params for every column: (params [7, ld], clamped [ld] bool, raw|None)."""
-        _check(fused, torch.float32, 134, "fused")
+        """predict_params for every column: (params [7, ld], clamped [ld] bool, raw|None).
+        A model with another chain (TrainConfig.layer_sizes) reads [sizes[0], ld] and
+        returns raw [sizes[-1], ld] (forward_raw); params / clamped need 7 outputs."""
+        sizes = self._sizes()
+        _check(fused, torch.float32, sizes[0], "fused")
         ld = fused.shape[1]
         n = ld if n is None else n
-        params = self._empty((7, ld), torch.float32)
-        clamped = self._empty((ld,), torch.uint8)
-        raw = self._empty((7, ld), torch.float32) if want_raw else None
+        params = self._empty((7, ld), torch.float32) if sizes[-1] == 7 else None
+        clamped = self._empty((ld,), torch.uint8) if sizes[-1] == 7 else None
+        raw = self._empty((sizes[-1], ld), torch.float32) if want_raw else None
         self._raise(self._lib.dso_predict(self._h, _ptr(fused), n, ld, _ptr(params),
                                           _ptr(clamped), _ptr(raw)))
-        return params, clamped.bool(), raw
+        return params, (clamped.bool() if clamped is not None else None), raw
+
+    def _sizes(self):
+        return list(self.model.layer_sizes) if self.model is not None else [134, 100, 50, 25, 7]
 
     # -- sweep ----------------------------------------------------------------------
     def brute_force_config(self, params, eta: float, pmax_w: float | None = None,
@@ -492,8 +512,9 @@ class Context:
     def train_grad(self, x, y_std, n: int | None = None, grad=None):
         """Sum over the batch of per-sample gradients of 0.5*||out - y||^2 (device model).
         Returns (grad float32 [n_params], loss_sum float)."""
-        _check(x, torch.float32, 134, "x")
-        _check(y_std, torch.float32, 7, "y_std")
+        sizes = self._sizes()
+        _check(x, torch.float32, sizes[0], "x")
+        _check(y_std, torch.float32, sizes[-1], "y_std")
         ld = x.shape[1]
         n = ld if n is None else n
         if grad is None:
@@ -506,8 +527,9 @@ class Context:
     def train_grad_slice(self, x, y_std, start: int, count: int, grad=None):
         """train_grad on columns [start, start+count) of [134, ld] / [7, ld] tensors
         (a batch of a device-resident dataset, no copy)."""
-        _check(x, torch.float32, 134, "x")
-        _check(y_std, torch.float32, 7, "y_std")
+        sizes = self._sizes()
+        _check(x, torch.float32, sizes[0], "x")
+        _check(y_std, torch.float32, sizes[-1], "y_std")
         ld = x.shape[1]
         if y_std.shape[1] != ld or start < 0 or start + count > ld:
             raise DsoError(ErrorKind.InvalidArgument, "slice outside the dataset")
@@ -523,16 +545,20 @@ class Context:
         self._raise(self._lib.dso_train_apply(self._h, _ptr(grad), lr, scale))
 
     def train_step(self, x, y_std, lr: float, global_batch: int, n: int | None = None,
-                   comm=None, want_loss: bool = True):
-        """dso_train_step: one data-parallel SGD step inside the library (gradient ->
-        NCCL allreduce over `comm` (NcclComm or None) -> update).  Returns the global
-        batch's mse_loss on the pre-update weights (float) or None."""
+                   comm=None, want_loss: bool = True, start: int = 0):
+        """dso_train_step: one data-parallel SGD step inside the library (gradient of
+        columns [start, start + n) -> NCCL allreduce over `comm` (NcclComm or None) ->
+        update).  Returns the global batch's mse_loss on the pre-update weights
+        (float) or None."""
         _check(x, torch.float32, None, "x")
         _check(y_std, torch.float32, None, "y_std")
         ld = x.shape[1]
-        n = ld if n is None else n
+        n = ld - start if n is None else n
+        if y_std.shape[1] != ld or start < 0 or n < 0 or start + n > ld:
+            raise DsoError(ErrorKind.InvalidArgument, "slice outside the dataset")
         loss = C.c_double()
-        self._raise(self._lib.dso_train_step(self._h, _ptr(x), _ptr(y_std), n, ld, float(lr),
+        self._raise(self._lib.dso_train_step(self._h, _ptr(x) + 4 * start,
+                                             _ptr(y_std) + 4 * start, n, ld, float(lr),
                                              int(global_batch), None if comm is None else comm.handle,
                                              C.byref(loss) if want_loss else None))
         return loss.value if want_loss else None

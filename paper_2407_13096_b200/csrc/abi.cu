@@ -204,6 +204,8 @@ int32_t dso_ctx_destroy(dso_ctx* ctx) {
     cudaFree(c.counters_dev);
     cudaFree(c.dp_grad);
     cudaFree(c.dp_dbl);
+    cudaFree(c.gen_scratch);
+    cudaFree(c.model.gstats);
     for (auto& s : c.aux)
         if (s) cudaStreamDestroy(s);
     for (auto& ev : c.ev)
@@ -379,30 +381,60 @@ int32_t dso_set_model(dso_ctx* ctx, const int32_t* sizes, int32_t n_sizes, const
     static const int kDefault[5] = {134, 100, 50, 25, 7};
     bool is_default = n_sizes == 5;
     for (int i = 0; is_default && i < 5; ++i) is_default = sizes[i] == kDefault[i];
-    if (!is_default)
+    // any other chain: the generic engine (mlp_gen.cu), within its limits
+    int sum_w = 0, max_w = 0;
+    for (int i = 0; i < n_sizes; ++i) {
+        sum_w += sizes[i];
+        max_w = std::max(max_w, sizes[i]);
+    }
+    if (!is_default && (n_sizes - 1 > kGenMaxLayers || max_w > kGenMaxWidth || sum_w > kGenMaxSumWidths))
         return fail(ctx, kInvalidModel,
-                    "device kernels implement the default topology 134-100-50-25-7 "
-                    "(default_layer_sizes, mlp.cpp:177) only");
+                    "the device engine for non-default chains supports <= 8 layers, widths <= 256 "
+                    "and a sum of widths <= 700");
     Ctx& c = ctx->c;
     DSO_CUDA(ctx, cudaSetDevice(c.device));
     ModelDev& md = c.model;
-    for (int i = 0; i < 5; ++i) md.sizes[i] = sizes[i];
+    for (int i = 0; i < n_sizes; ++i) md.sizes[i] = sizes[i];
     md.n_layers = n_sizes;
+    md.generic = !is_default;
     for (int i = 0; i < 8; ++i) {
         md.mean[i] = i < out ? (float)mean[i] : 0.f;
         md.std_[i] = i < out ? (float)std_[i] : 1.f;
     }
-    md.n_weights = 134 * 100 + 100 * 50 + 50 * 25 + 25 * 7;
-    md.n_biases = 100 + 50 + 25 + 7;
+    md.n_weights = 0;
+    md.n_biases = 0;
+    for (int l = 0; l + 1 < n_sizes; ++l) {
+        md.n_weights += (int64_t)sizes[l] * sizes[l + 1];
+        md.n_biases += sizes[l + 1];
+    }
     std::vector<float> master(md.n_weights + md.n_biases);
     for (int64_t i = 0; i < md.n_weights; ++i) master[i] = (float)W[i];
     for (int64_t i = 0; i < md.n_biases; ++i) master[md.n_weights + i] = (float)b[i];
     DSO_CUDA(ctx, cudaStreamSynchronize(c.stream));
-    if (!md.w_master) DSO_CUDA(ctx, cudaMalloc(&md.w_master, sizeof(float) * master.size()));
+    if (md.w_master_cap < (int64_t)master.size()) {
+        cudaFree(md.w_master);
+        md.w_master = nullptr;
+        md.w_master_cap = 0;
+        DSO_CUDA(ctx, cudaMalloc(&md.w_master, sizeof(float) * master.size()));
+        md.w_master_cap = (int64_t)master.size();
+    }
     md.train_dirty = true;
     DSO_CUDA(ctx, cudaMemcpy(md.w_master, master.data(), sizeof(float) * master.size(),
                              cudaMemcpyHostToDevice));
-    DSO_CUDA(ctx, model_upload(c, W, b));
+    if (md.generic) {
+        std::vector<float> st(2 * out);
+        for (int i = 0; i < out; ++i) {
+            st[i] = (float)mean[i];
+            st[out + i] = (float)std_[i];
+        }
+        cudaFree(md.gstats);
+        md.gstats = nullptr;
+        DSO_CUDA(ctx, cudaMalloc(&md.gstats, sizeof(float) * st.size()));
+        DSO_CUDA(ctx, cudaMemcpy(md.gstats, st.data(), sizeof(float) * st.size(),
+                                 cudaMemcpyHostToDevice));
+    } else {
+        DSO_CUDA(ctx, model_upload(c, W, b));
+    }
     DSO_CUDA(ctx, cudaStreamSynchronize(c.stream));
     c.has_model = true;
     return kOk;
@@ -462,6 +494,15 @@ int32_t dso_featurize(dso_ctx* ctx, const uint32_t* counts, const float* dcgm, i
     if (st) return st;
     if ((st = check_batch(ctx, n, ld))) return st;
     DSO_CUDA(ctx, launch_featurize(ctx->c, counts, dcgm, n, ld, fused));
+    return kOk;
+}
+
+int32_t dso_featurize_u64(dso_ctx* ctx, const uint64_t* counts, const float* dcgm, int64_t n,
+                          int64_t ld, float* fused) {
+    int32_t st = check_ctx(ctx, false, false);
+    if (st) return st;
+    if ((st = check_batch(ctx, n, ld))) return st;
+    DSO_CUDA(ctx, launch_featurize_u64(ctx->c, counts, dcgm, n, ld, fused));
     return kOk;
 }
 

@@ -73,15 +73,22 @@ struct DomainDev {
 // Only the default topology 134-100-50-25-7 (mlp.cpp:177) runs on the fused
 // kernels; other topologies are rejected by dso_set_model with InvalidModel
 // for the device path (the reference trains probe nets only in unit tests).
+constexpr int kGenMaxLayers = 8, kGenMaxWidth = 256, kGenMaxSumWidths = 700;
+
 struct ModelDev {
-    int sizes[5];
+    int sizes[kGenMaxLayers + 1];
     int n_layers = 5;  // entries of sizes (layers + 1)
+    // any chain other than 134-100-50-25-7 runs on the generic engine (mlp_gen.cu)
+    // from w_master; gstats = target mean[out] then std[out] (device)
+    bool generic = false;
+    float* gstats = nullptr;
     float* wt;       // packed per-layer transposed weights (see mlp.cu layout)
     float* bias;     // packed biases (padded)
     float mean[8], std_[8];
     int64_t wt_floats, bias_floats;
     // master copy in the reference layout (row-major W, concatenated), f32
     float* w_master;  // [n_weights + n_biases]
+    int64_t w_master_cap = 0;
     // the training kernel's shared-memory image of the weights (train.cu), rebuilt
     // from w_master before the next gradient after any change of w_master
     float* w_train;
@@ -92,6 +99,16 @@ struct ModelDev {
     float* wtc;
     int tc_state;
     int64_t n_weights, n_biases;
+};
+
+// Layer chain of a generic model (mlp_gen.cu): offsets into the master layout.
+struct GenNet {
+    int layers;                     // weight layers
+    int sizes[kGenMaxLayers + 1];
+    int woff[kGenMaxLayers], boff[kGenMaxLayers];
+    int aoff[kGenMaxLayers + 1];    // activation rows of layer l in the grad kernel
+    int maxw, sum_widths;
+    int64_t nw, nb;
 };
 
 struct Ctx {
@@ -128,6 +145,9 @@ struct Ctx {
     float* dp_grad = nullptr;
     double* dp_dbl = nullptr;
     int64_t dp_np = 0;
+    // the generic-chain pipeline's staging (mlp_gen.cu)
+    void* gen_scratch = nullptr;
+    size_t gen_scratch_bytes = 0;
 };
 
 }  // namespace dso_b200
@@ -185,7 +205,23 @@ cudaError_t launch_train_apply(Ctx& c, const float* grad, float lr_scale, bool r
 // allocations (scratch, weight image) and kernel attributes for batches of up to
 // n samples, without launching: makes the next gradients capturable
 cudaError_t train_prepare(Ctx& c, int64_t n);
-cudaError_t launch_repack(Ctx& c);  // w_master (f32, reference layout) -> packed wt
+cudaError_t launch_repack(Ctx& c);
+// generic-chain engine and 64-bit-count features (mlp_gen.cu)
+GenNet gen_net_of(const ModelDev& md);
+cudaError_t launch_gen_forward(Ctx& c, const float* x, int64_t n, int64_t ld, float* raw,
+                               float* params, uint8_t* clamped, int64_t ld_out);
+cudaError_t launch_gen_grad(Ctx& c, const float* x, const float* y, int64_t n, int64_t ld,
+                            float* grad, double* loss_sum_dev);
+cudaError_t launch_gen_apply(Ctx& c, const float* grad, float lr_scale);
+cudaError_t launch_featurize_u64(Ctx& c, const uint64_t* counts, const float* dcgm, int64_t n,
+                                 int64_t ld, float* fused);
+cudaError_t launch_csr_to_dense(Ctx& c, const uint64_t* row_ptr, const uint32_t* entries,
+                                uint64_t ent_base, int64_t n, int64_t ld, uint32_t* counts);
+cudaError_t launch_gen_pipeline(Ctx& c, const uint32_t* counts, const uint64_t* row_ptr,
+                                const uint32_t* entries, uint64_t ent_base, const float* dcgm,
+                                int64_t n, int64_t ld, float eta, float K, float* params,
+                                uint8_t* clamped, int32_t* idx, float* cost, float* energy,
+                                float* time, int64_t ld_out);  // w_master (f32, reference layout) -> packed wt
 size_t mlp_smem_bytes();
 
 // ---- device helpers ---------------------------------------------------------

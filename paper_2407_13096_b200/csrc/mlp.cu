@@ -1350,6 +1350,7 @@ cudaError_t model_upload(Ctx& cx, const double* W, const double* b) {
 }
 
 cudaError_t launch_repack(Ctx& cx) {
+    if (cx.model.generic) return cudaSuccess;  // the generic engine reads w_master
     cudaError_t e = cudaMemsetAsync(cx.model.wt + FLAGW, 0, sizeof(int), cx.stream);
     if (e != cudaSuccess) return e;
     repack_kernel<<<(kMasterFloats + 255) / 256, 256, 0, cx.stream>>>(cx.model.w_master,
@@ -1369,6 +1370,7 @@ cudaError_t launch_repack(Ctx& cx) {
 cudaError_t launch_predict(Ctx& cx, const float* fused, int64_t n, int64_t ld, float* params,
                            uint8_t* clamped, float* raw) {
     if (n <= 0) return cudaSuccess;
+    if (cx.model.generic) return launch_gen_forward(cx, fused, n, ld, raw, params, clamped, ld);
     Job J{};
     J.fused = fused;
     J.n = n;
@@ -1385,6 +1387,9 @@ cudaError_t launch_pipeline(Ctx& cx, const uint32_t* counts, const float* dcgm, 
                             int32_t* idx, float* cost, float* energy, float* time,
                             int64_t ld_out) {
     if (n <= 0) return cudaSuccess;
+    if (cx.model.generic)
+        return launch_gen_pipeline(cx, counts, nullptr, nullptr, 0, dcgm, n, ld, eta, K, params,
+                                   clamped, idx, cost, energy, time, ld_out);
     Job J{};
     J.counts = counts;
     J.dcgm = dcgm;
@@ -1412,6 +1417,9 @@ cudaError_t launch_pipeline_csr(Ctx& cx, const uint64_t* row_ptr, const uint32_t
                                 float eta, float K, float* params, uint8_t* clamped, int32_t* idx,
                                 float* cost, float* energy, float* time, int64_t ld_out) {
     if (n <= 0) return cudaSuccess;
+    if (cx.model.generic)
+        return launch_gen_pipeline(cx, nullptr, row_ptr, entries, ent_base, dcgm, n, ld, eta, K,
+                                   params, clamped, idx, cost, energy, time, ld_out);
     Job J{};
     J.row_ptr = row_ptr;
     J.entries = entries;

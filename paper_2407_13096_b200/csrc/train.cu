@@ -651,6 +651,20 @@ __global__ void sgd_apply(float* __restrict__ master, const float* __restrict__ 
 }  // namespace
 
 cudaError_t train_prepare(Ctx& cx, int64_t n) {
+    if (cx.model.generic) {  // sized by launch_gen_grad's first call: reserve it here
+        const GenNet g = gen_net_of(cx.model);
+        const int64_t parts = std::max<int64_t>(1, std::min<int64_t>((n + 63) / 64, 2 * cx.num_sms));
+        const size_t need = (size_t)parts * (g.nw + g.nb) * sizeof(float) + (size_t)parts * 8 + 256;
+        if (cx.train_scratch_bytes < need) {
+            cudaFree(cx.train_scratch);
+            cx.train_scratch = nullptr;
+            cx.train_scratch_bytes = 0;
+            cudaError_t e = cudaMalloc(&cx.train_scratch, need);
+            if (e != cudaSuccess) return e;
+            cx.train_scratch_bytes = need;
+        }
+        return cudaSuccess;
+    }
     const int parts = cx.num_sms;
     const int64_t lds = ((n + TM - 1) / TM) * TM;
     const size_t need = (size_t)parts * kMasterFloats * sizeof(float) + (size_t)parts * sizeof(double) +
@@ -677,6 +691,7 @@ cudaError_t train_prepare(Ctx& cx, int64_t n) {
 
 cudaError_t launch_train_grad(Ctx& cx, const float* x, const float* y, int64_t n, int64_t ld,
                               float* grad, double* loss_sum_dev) {
+    if (cx.model.generic) return launch_gen_grad(cx, x, y, n, ld, grad, loss_sum_dev);
     const int parts = cx.num_sms;
     const int64_t lds = ((n + TM - 1) / TM) * TM;  // scratch row length (whole tiles)
     const size_t part_b = (size_t)parts * kMasterFloats * sizeof(float);
@@ -735,6 +750,7 @@ cudaError_t launch_train_grad(Ctx& cx, const float* x, const float* y, int64_t n
 }
 
 cudaError_t launch_train_apply(Ctx& cx, const float* grad, float lr_scale, bool repack) {
+    if (cx.model.generic) return launch_gen_apply(cx, grad, lr_scale);
     cx.model.train_dirty = true;
     sgd_apply<<<(kMasterFloats + 255) / 256, 256, 0, cx.stream>>>(cx.model.w_master, grad,
                                                                   lr_scale);
