@@ -92,6 +92,10 @@ def test_set_model_validation(ctx):
     with pytest.raises(DsoError) as e:
         ctx.set_model(m)
     assert e.value.kind == ErrorKind.InvalidModel
+    # any chain within the generic engine's limits is accepted (mlp_gen.cu) ...
+    ctx.set_model(init_mlp([4, 3, 2], seed=1))
+    assert ctx.n_model_params == 4 * 3 + 3 * 2 + 3 + 2
+    # ... wider chains are not
     with pytest.raises(DsoError) as e:
-        ctx.set_model(init_mlp([4, 3, 2], seed=1))
+        ctx.set_model(init_mlp([4, 300, 2], seed=1))
     assert e.value.kind == ErrorKind.InvalidModel
