@@ -315,6 +315,9 @@ int32_t dso_ptx_counts(const dso_ptx* parsed, uint32_t* counts, int64_t ld);
  * (InvalidArgument if a count >= 2^25) */
 int64_t dso_ptx_nnz(const dso_ptx* parsed);
 int32_t dso_ptx_csr(const dso_ptx* parsed, uint64_t* row_ptr, uint32_t* entries);
+/* Canonical category name of count row r (ptx_features.cpp:18-49 lists; the last
+ * entry of each category is "other"), NULL outside 0..125. */
+const char* dso_category_name(int32_t row);
 /* load_dcgm_samples (telemetry.cpp:63-101): header, >= 1 row, 9 fields, values in
  * [0, 1] (OutOfRange with the row in msg), per-metric mean in double ->
  * mean8 in DcgmMetricVector order. */

@@ -123,6 +123,8 @@ def _declare(L: C.CDLL) -> None:
     L.dso_ptx_nnz.restype = i64
     L.dso_ptx_csr.argtypes = [vp, vp, vp]
     L.dso_ptx_csr.restype = i32
+    L.dso_category_name.argtypes = [i32]
+    L.dso_category_name.restype = C.c_char_p
     L.dso_load_dcgm_csv.argtypes = [C.c_char_p, i64, vp, C.c_char_p, i32]
     L.dso_load_dcgm_csv.restype = i32
     L.dso_eta_sweep.argtypes = [vp, vp, i64, i64, P(d), i32, d, vp, vp, i64]
@@ -170,5 +172,6 @@ EXPORTED = (
     "dso_nccl_unique_id", "dso_nccl_comm_init", "dso_nccl_comm_destroy", "dso_nccl_version",
     "dso_model_param_count", "dso_probe_fp32_peak",
     "dso_ptx_parse", "dso_ptx_free", "dso_ptx_kernel_count", "dso_ptx_kernel_name",
-    "dso_ptx_kernel_counts", "dso_ptx_counts", "dso_ptx_nnz", "dso_ptx_csr", "dso_load_dcgm_csv",
+    "dso_ptx_kernel_counts", "dso_ptx_counts", "dso_ptx_nnz", "dso_ptx_csr", "dso_category_name",
+    "dso_load_dcgm_csv",
 )

@@ -315,6 +315,18 @@ int32_t dso_ptx_csr(const dso_ptx* p, uint64_t* row_ptr, uint32_t* entries) {
     return 0;
 }
 
+// Canonical category name of count row r (instruction_categories /
+// data_type_categories / memory_space_categories, ptx_features.hpp:39-41): rows
+// 0..100, 101..117, 118..125; the last of each list is "other".
+const char* dso_category_name(int32_t row) {
+    if (row < 0 || row >= kInstr + kDtype + kMem) return nullptr;
+    if (row < kInstr) return row < kInstr - 1 ? kOps[row] : "other";
+    row -= kInstr;
+    if (row < kDtype) return row < kDtype - 1 ? kTypes[row] : "other";
+    row -= kDtype;
+    return row < kMem - 1 ? kSpaces[row] : "other";
+}
+
 // load_dcgm_samples (telemetry.cpp:63-101): header check, >= 1 data row, 9 fields
 // per row, every metric in [0, 1], per-metric mean in double (row order).
 int32_t dso_load_dcgm_csv(const char* text, int64_t len, double* mean8, char* msg,
