@@ -578,6 +578,8 @@ def run_ours(args, rank, world, local_rank):
                 stages["pipeline_dense_input_ms"] = cuda_time(
                     stream, lambda: ctx.pipeline(dense["counts"], dense["dcgm"], cfg["eta"], out=o), 3)
             del dense
+            if csr:
+                stages["realistic_mix"] = realistic_stage(ctx, cfg, stream)
         else:
             del gen
         e2e = head.pop("e2e", None)
@@ -652,6 +654,61 @@ def bench_model_device(ctx):
     p = p.double().cpu().numpy()
     m.target_mean, m.target_std = p.mean(1), p.std(1)
     return m
+
+
+def realistic_counts_csr(n, seed=2407, chunk=1 << 19):
+    """A realistic PTX category mix, not the generator's fixed 24 slots: every kernel
+    lists each of the 126 categories independently with a Zipf-like probability
+    (~25 listed categories per kernel, every slot used somewhere), counts log-uniform
+    in [1, 2e6].  Returns CSR (row_ptr int64, entries int32 = (count << 7) | slot),
+    slot-sorted per kernel."""
+    rng = np.random.default_rng(seed)
+    w = 1.0 / (1.0 + np.arange(126)) ** 0.8
+    w = w[rng.permutation(126)]
+    p = np.minimum(w * (25.0 / w.sum()), 0.95)
+    rows, ents = [np.zeros(1, np.int64)], []
+    total = 0
+    for a in range(0, n, chunk):
+        m = min(chunk, n - a)
+        mask = rng.random((m, 126), dtype=np.float32) < p
+        k, sl = np.nonzero(mask)
+        cnt = np.exp(rng.random(len(k), dtype=np.float32) * np.float32(np.log(2e6))).astype(np.int64) + 1
+        ents.append(((cnt << 7) | sl).astype(np.int32))
+        rows.append(total + np.cumsum(mask.sum(1)))
+        total += len(k)
+    return np.concatenate(rows), np.concatenate(ents)
+
+
+def realistic_stage(ctx, cfg, stream, n=1 << 22):
+    """The CSR pipeline on the realistic mix (4M kernels, same grid / eta), both
+    predictor engines, plus the same kernels as dense [126][n] counts."""
+    import torch
+    rp, ent = realistic_counts_csr(n)
+    rp_t, ent_t = torch.from_numpy(rp).cuda(), torch.from_numpy(ent).cuda()
+    dcgm = torch.rand((8, n), device="cuda", dtype=torch.float32)
+    o = ctx.alloc_pipeline_out(n)
+    pairs = cfg["nc"] * cfg["nm"]
+    res = {"kernels": n, "nnz_per_kernel": float(len(ent)) / n,
+           "slots_used": int(len(np.unique(ent & 127)))}
+    for name, eng in (("tc", 1), ("ffma", 0)):
+        ctx.set_option("mlp_engine", eng)
+        ctx.counters(reset=True)
+        ms = cuda_time(stream, lambda: ctx.pipeline_csr(rp_t, ent_t, dcgm, cfg["eta"], out=o), 3)
+        c = ctx.counters(reset=True)
+        res[f"{name}_ms"] = ms
+        res[f"{name}_pairs_per_s"] = n * pairs / (ms * 1e-3)
+        if c["tc_tiles"]:
+            res["tc_l1_ksteps_per_tile"] = c["tc_l1_ksteps"] / c["tc_tiles"]
+    ctx.set_option("mlp_engine", 2)
+    dense = torch.zeros((126, n), dtype=torch.int32, device="cuda")
+    kk = np.repeat(np.arange(n), np.diff(rp))
+    dense[torch.from_numpy(ent & 127).cuda().long(), torch.from_numpy(kk).cuda()] = \
+        torch.from_numpy(ent >> 7).cuda()
+    res["dense_input_ms"] = cuda_time(stream, lambda: ctx.pipeline(dense, dcgm, cfg["eta"], out=o), 3)
+    res["note"] = ("Zipf-like inclusion probabilities over all 126 categories "
+                   "(bench.realistic_counts_csr); ms per 4M-kernel call, CUDA events")
+    del dense, rp_t, ent_t
+    return res
 
 
 def stage_times(ctx, counts, dcgm, cfg, dom, n, stream):

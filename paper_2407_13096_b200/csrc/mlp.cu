@@ -144,6 +144,9 @@ constexpr int kMasterFloats = MB4 + 7;
 __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
 
 // Optional per-phase cycle accounting (debug builds only: -DDSO_PHASE_TIMING).
+#ifdef DSO_TC_TRACE
+__device__ unsigned long long g_trace[16 * 64];
+#endif
 #ifdef DSO_PHASE_TIMING
 __device__ unsigned long long g_phase_cycles[32];
 #define PT_BEGIN(v) long long v = clock64()
@@ -1265,6 +1268,14 @@ extern "C" int32_t dso_debug_phase_cycles(unsigned long long* out, int reset) {
         unsigned long long z[32] = {};
         cudaMemcpyToSymbol(g_phase_cycles, z, sizeof z);
     }
+    return 0;
+}
+#endif
+
+#ifdef DSO_TC_TRACE
+extern "C" int32_t dso_debug_trace(unsigned long long* out) {
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(out, g_trace, sizeof(unsigned long long) * 16 * 64);
     return 0;
 }
 #endif

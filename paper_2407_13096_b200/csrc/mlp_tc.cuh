@@ -50,6 +50,14 @@ constexpr int TT = 128;                            // kernels per tile
 constexpr int kGroupT = 128;                       // threads of a role group (4 warps)
 constexpr int kThreadsTC = 4 * kGroupT;  // producers, 2 epilogue groups, MMA warp (+3 idle)
 constexpr int MMA_WARP = 12;
+#ifndef DSO_MMA_SLEEP_NS
+#define DSO_MMA_SLEEP_NS 32
+#endif
+constexpr unsigned kMmaSleepNs = DSO_MMA_SLEEP_NS;  // idle back-off of the MMA issuer's poll
+#ifndef DSO_EPI1_BATCH
+#define DSO_EPI1_BATCH 4
+#endif
+constexpr int kEpi1Batch = DSO_EPI1_BATCH;  // layer-1 epilogue chunks per TMEM load/store wait
 // Registers (setmaxnreg): launched at 128 per thread; warpgroup 3 (the MMA warp
 // and three idle warps) releases down to 56, producers grow to 168 and the
 // epilogue groups to 144 (128*168 + 256*144 + 128*56 = 64K).
@@ -135,6 +143,16 @@ constexpr float kNL2E = -1.4426950408889634f;
 #define TPT_END(ph, v) (void)0
 #endif
 
+// event timeline of CTA 0 (debug builds with -DDSO_TC_TRACE; dso_debug_trace)
+#ifdef DSO_TC_TRACE
+#define TRACE(ev, t)                                                   \
+    do {                                                               \
+        if (blockIdx.x == 0 && (t) < 64) g_trace[(ev) * 64 + (t)] = clock64(); \
+    } while (0)
+#else
+#define TRACE(ev, t) (void)0
+#endif
+
 __device__ __forceinline__ void mb_init(uint64_t* b, int count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
 }
@@ -172,6 +190,29 @@ __device__ __forceinline__ void store_split(uint32_t a_hi, uint32_t a_lo, const 
     }
     tc::st8(a_hi, h);
     tc::st8(a_lo, l);
+}
+
+// Activation of one loaded 8-neuron chunk: sigmoid(acc + b) (neurons >= NREAL are
+// padding: 0), split, stored as the next layer's A operand (not yet waited on).
+template <int NREAL>
+__device__ __forceinline__ void epi_act_store(const float (&v)[8], int c,
+                                              const float* __restrict__ nb, uint32_t dst_hi,
+                                              uint32_t dst_lo) {
+    float a[8];
+#pragma unroll
+    for (int j = 0; j < 8; j += 2) {
+        const float2 z = ffma2(make_float2(v[j], v[j + 1]), make_float2(kNL2E, kNL2E),
+                               make_float2(nb[8 * c + j], nb[8 * c + j + 1]));
+        float e0, e1, r0, r1;
+        asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e0) : "f"(z.x));
+        asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e1) : "f"(z.y));
+        const float2 d = fadd2(make_float2(1.f, 1.f), make_float2(e0, e1));
+        asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r0) : "f"(d.x));
+        asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r1) : "f"(d.y));
+        a[j] = 8 * c + j < NREAL ? r0 : 0.f;
+        a[j + 1] = 8 * c + j + 1 < NREAL ? r1 : 0.f;
+    }
+    store_split(dst_hi, dst_lo, a);
 }
 
 // Hidden-layer epilogue of one 8-neuron chunk: sigmoid(acc + b) (neurons >=
@@ -423,6 +464,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
                 const uint32_t xa = s0 + (uint32_t)(S_RING + b * kChunkF) * 4;
                 const uint64_t ah = tc::sdesc(xa, 128, 256), al = tc::sdesc(xa + TT * 8 * 4, 128, 256);
                 tc::mma_tf32_ss(D, ah, bd(W1H, st.c, K1), id1, st.c == 0 ? 0u : 1u);
+                if (st.c == 0) TRACE(0, st.t);
                 tc::mma_tf32_ss(D, ah, bd(W1L, st.c, K1), id1, 1u);
                 tc::mma_tf32_ss(D, al, bd(W1H, st.c, K1), id1, 1u);
                 tc::commit(mb + MB_XEMPTY + b);
@@ -432,6 +474,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
                 while (nc < 17 && !((st.mask >> nc) & 1u)) ++nc;
                 if (nc >= 17) {
                     tc::commit(mb + MB_D1F + (st.t & 1));
+                    TRACE(1, st.t);
                     st.active = false;
                 } else {
                     st.c = nc;
@@ -446,9 +489,14 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
             int c2 = 0;
             while (b < my_tiles) {
                 if (!st.active && st.t + 1 < my_tiles && st.t + 1 <= b + 1) st = L1S{st.t + 1, 0, 0u, true};
-                while (st.active && l1_step(st)) {
+                bool prog = false;
+                while (st.active && l1_step(st)) prog = true;
+                if (st.t <= b && st.active) {  // L1(b) not fully issued yet
+                    // nothing ready: yield the issue slots to this SMSP's producer and
+                    // epilogue warps for a moment instead of spinning
+                    if (!prog && kMmaSleepNs) __nanosleep(kMmaSleepNs);
+                    continue;
                 }
-                if (st.t <= b && st.active) continue;  // L1(b) not fully issued yet
                 const int sl = (int)(b & 1);
                 const uint32_t S = tbase + (uint32_t)(sl * SLOT_COLS);
                 const uint32_t ph = (uint32_t)((b >> 1) & 1);
@@ -456,17 +504,21 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
                 while (d2ok && c2 < 13 && mbar_test(mb + MB_A2R + 13 * sl + c2, ph)) {
                     tc::fence_after();
                     tc::mma_tf32_ts(tbase + TD2, S + 8 * c2, bd(W2H, c2, K2), id2, c2 > 0 ? 1u : 0u);
+                    if (c2 == 0) TRACE(2, b);
                     tc::mma_tf32_ts(tbase + TD2, S + 8 * c2, bd(W2L, c2, K2), id2, 1u);
                     tc::mma_tf32_ts(tbase + TD2, S + A2LO + 8 * c2, bd(W2H, c2, K2), id2, 1u);
                     ++n_l2;
+                    prog = true;
                     if (++c2 == 13) {
                         tc::commit(mb + MB_D2F + sl);
+                        TRACE(3, b);
                         ++b;
                         c2 = 0;
                         d2ok = false;
                         break;
                     }
                 }
+                if (!prog && kMmaSleepNs) __nanosleep(kMmaSleepNs);
             }
             if (J.counters) {
                 atomicAdd(J.counters + 0, n_l1);
@@ -559,15 +611,23 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
                 }
             }
             TPT_BEGIN(p_t);
+            if (tid == 0) TRACE(4, t);
             // ---- per-kernel preparation: totals, chunk mask, non-finite rows ----
             float tf[3] = {0.f, 0.f, 0.f}, rr[3] = {0.f, 0.f, 0.f};
             uint32_t mask = 1u;   // chunks this kernel touches (chunk 0: DCGM)
             bool uns = false;     // CSR: entries not strictly increasing, or spilled
             bool bad = false;     // a non-finite feature: FMA-pipe forward
-            uint64_t nib = 0;     // CSR (sorted rows): entries per chunk 1..16, 4 bits each
+            int nlive = 0;        // CSR: live entries (the K-ordered list's length)
+#ifdef DSO_TCV_NOPROD
+            if (MODE == MODE_CSR) mbar_wait(mb + MB_ESTAGE, (uint32_t)(t & 1));
+            if (MODE == MODE_CSR && false) {
+#else
             if (MODE == MODE_CSR) {
+#endif
                 uint64_t tot[3] = {0, 0, 0};
-                uint32_t t32[3] = {0u, 0u, 0u};
+                // category totals as suffix sums over the slot order: all, dtype +
+                // memspace (slot >= 101), memspace (slot >= 118)
+                uint32_t ta = 0u, t12 = 0u, t2 = 0u;
                 int prev = -1;
                 uint32_t en[kEnt];
                 TPT_BEGIN(p_l);
@@ -599,15 +659,16 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
                     uns |= inrow && slot <= prev;
                     prev = inrow ? slot : prev;
                     const int col = 8 + pos_of[live ? slot : 0];
-                    const int cat = cat_of_row(slot);
-                    t32[0] += (live && cat == 0) ? cnt : 0u;
-                    t32[1] += (live && cat == 1) ? cnt : 0u;
-                    t32[2] += (live && cat == 2) ? cnt : 0u;
+                    const uint32_t cl = live ? cnt : 0u;
+                    ta += cl;
+                    t12 += slot >= DSO_INSTR_SLOTS ? cl : 0u;
+                    t2 += slot >= DSO_INSTR_SLOTS + DSO_DTYPE_SLOTS ? cl : 0u;
                     mask |= live ? 1u << (col >> 3) : 0u;
-                    nib += live ? 1ull << (4 * ((col >> 3) - 1)) : 0ull;
                     colp[e >> 2] |= (live ? (uint32_t)col : 0u) << (8 * (e & 3));
                     ncommon += (live && col < 32) ? 1 : 0;
+                    nlive += live ? 1 : 0;
                 }
+                const uint32_t t32[3] = {ta - t12, t12 - t2, t2};
                 if (E.cnt > kEnt) {
                     uns = true;
                     for (int idx = kEnt; idx < E.cnt; ++idx) {
@@ -634,11 +695,6 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
                 // with the slot) first, then the others (also increasing with the slot)
                 float* el = sm + S_ELIST;
                 uint8_t* ecl = reinterpret_cast<uint8_t*>(sm + S_ECOL);
-                int nlive = 0;
-#pragma unroll
-                for (int e4 = 0; e4 < kEnt / 4; ++e4)
-                    nlive += (colp[e4] & 0xFFu ? 1 : 0) + (colp[e4] & 0xFF00u ? 1 : 0) +
-                             (colp[e4] & 0xFF0000u ? 1 : 0) + (colp[e4] & 0xFF000000u ? 1 : 0);
                 if (ncommon == nlive) {
                     // only common categories: slot order is already K order
                     int ne = 0;
@@ -741,6 +797,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
                 if (lane == 0) misc[2 + 4 * sl + warp] = bm;
             };
             TPT_END(18, p_m);
+            if (tid == 0) TRACE(5, t);
             TPT_BEGIN(p_s);
             if (MODE == MODE_CSR) slow_block();
             TPT_END(19, p_s);
@@ -786,14 +843,16 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
                         *reinterpret_cast<float4*>(buf + o + 32) = z4;
                         *reinterpret_cast<float4*>(buf + TT * 8 + o) = z4;
                         *reinterpret_cast<float4*>(buf + TT * 8 + o + 32) = z4;
-                        const int n_c = (int)((nib >> (4 * (c - 1))) & 15u);
-                        for (int i = ep; i < ep + n_c; ++i) {
-                            const float f = el[i * TT + row], h = tc::tf32_hi(f);
-                            const int j = ecl[i * TT + row] & 7, off = o + (j >> 2) * 32 + (j & 3);
+                        // this chunk's entries: contiguous in the K-ordered list
+                        for (; ep < nlive; ++ep) {
+                            const uint32_t cc = ecl[ep * TT + row];
+                            const float f = el[ep * TT + row];
+                            if ((int)(cc >> 3) != c) break;
+                            const float h = tc::tf32_hi(f);
+                            const int j = cc & 7, off = o + (j >> 2) * 32 + (j & 3);
                             buf[off] = h;
                             buf[TT * 8 + off] = f - h;
                         }
-                        ep += n_c;
                     } else {
                         // duplicate / unsorted / long rows: sum the counts per slot
                         uint32_t acc[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
@@ -861,6 +920,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
                 }
             }
             TPT_END(15, p_c);
+            if (tid == 0) TRACE(7, t);
             if (MODE == MODE_CSR && t + 1 < my_tiles) E = NE;
         }
     } else {
@@ -878,24 +938,71 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
             const uint32_t ph = (uint32_t)((t >> 1) & 1);
             const int64_t k = t0_of(t) + row;
             TPT_BEGIN(e_w1);
+            if (q == 0 && lane == 0) TRACE(8, t);
             wait_acq(mb + MB_D1F + grp, ph);
             TPT_END(2, e_w1);
+            if (q == 0 && lane == 0) TRACE(9, t);
             TPT_BEGIN(e_1);
-            for (int c = 0; c < 13; ++c)
-                epi_chunk<H1>(S + 8 * c, S + 8 * c, S + A2LO + 8 * c, c, sm + NB1,
-                              mb + MB_A2R + 13 * grp + c);
+            {
+                // batches of kEpi1Batch chunks: the batch's TMEM loads back to back, one
+                // wait, activations split and stored as A2, one store wait, then the
+                // batch's chunks are signalled (tcgen05 load / store latencies paid once
+                // per batch instead of once per chunk)
+#pragma unroll 1
+                for (int c0 = 0; c0 < 13; c0 += kEpi1Batch) {
+                    float v[kEpi1Batch][8];
+#pragma unroll
+                    for (int u = 0; u < kEpi1Batch; ++u)
+                        if (c0 + u < 13) tc::ld8(S + 8 * (c0 + u), v[u]);
+                    tc::wait_ld_tie(v[0]);
+#pragma unroll
+                    for (int u = 1; u < kEpi1Batch; ++u) tc::tie8(v[u]);
+#pragma unroll
+                    for (int u = 0; u < kEpi1Batch; ++u)
+                        if (c0 + u < 13)
+                            epi_act_store<H1>(v[u], c0 + u, sm + NB1, S + 8 * (c0 + u),
+                                              S + A2LO + 8 * (c0 + u));
+                    tc::wait_st();
+                    tc::fence_before();
+                    __syncwarp();
+                    if (lane == 0)
+#pragma unroll
+                        for (int u = 0; u < kEpi1Batch; ++u)
+                            if (c0 + u < 13) mb_arrive(mb + MB_A2R + 13 * grp + c0 + u);
+                }
+            }
             TPT_END(3, e_1);
+            if (q == 0 && lane == 0) TRACE(10, t);
             TPT_BEGIN(e_w2);
             wait_acq(mb + MB_D2F + grp, ph);
             TPT_END(4, e_w2);
+            if (q == 0 && lane == 0) TRACE(11, t);
             TPT_BEGIN(e_2);
             // L2 outputs: sigmoid of D2 into registers; D2 is then free for the next tile
             float h2[56];
+            {
+                // all of D2 into registers with one wait, then D2 is released at once
+                // (the next tile's layer 2 may start) and the activations follow
+                float v[7][8];
+#pragma unroll
+                for (int c = 0; c < 7; ++c) tc::ld8(tq + TD2 + 8 * c, v[c]);
+                tc::wait_ld_tie(v[0]);
+#pragma unroll
+                for (int c = 1; c < 7; ++c) tc::tie8(v[c]);
+                tc::fence_before();
+                __syncwarp();
+                if (lane == 0) mb_arrive(mb + MB_D2FREE);
+                if (q == 0 && lane == 0) TRACE(12, t);
+#pragma unroll
+                for (int c = 0; c < 7; ++c)
+#pragma unroll
+                for (int j = 0; j < 8; ++j) h2[8 * c + j] = v[c][j];
+            }
 #pragma unroll
             for (int c = 0; c < 7; ++c) {
                 float v[8];
-                tc::ld8(tq + TD2 + 8 * c, v);
-                tc::wait_ld();
+#pragma unroll
+                for (int j = 0; j < 8; ++j) v[j] = h2[8 * c + j];
 #pragma unroll
                 for (int j = 0; j < 8; j += 2) {
                     const float2 z = ffma2(make_float2(v[j], v[j + 1]), make_float2(kNL2E, kNL2E),
@@ -910,14 +1017,16 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
                     h2[8 * c + j + 1] = r1;
                 }
             }
-            tc::fence_before();
-            __syncwarp();
-            if (lane == 0) mb_arrive(mb + MB_D2FREE);
             TPT_END(5, e_2);
             TPT_BEGIN(e_3);
             // L3 (50 -> 25, sigmoid) and L4 (25 -> 7) on the FMA pipe, FP32, neuron
             // pairs per FFMA2, weights as shared-memory broadcasts
             float raw[8];
+#ifdef DSO_TCV_NOL34
+#pragma unroll
+            for (int j = 0; j < 8; ++j) raw[j] = h2[j] * sm[S_STATS + 8 + (j & 7)] + h2[8 + j];
+            if (false)
+#endif
             {
                 float2 a3[14];
 #pragma unroll
@@ -965,6 +1074,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
                     raw[j] = fmaf(z4[j] + sm[B4 + j], sm[S_STATS + 8 + j], sm[S_STATS + j]);
             }
             TPT_END(7, e_3);
+            if (q == 0 && lane == 0) TRACE(13, t);
             TPT_BEGIN(e_4);
             {
                 const uint32_t bm = *reinterpret_cast<volatile uint32_t*>(misc + 2 + 4 * grp + q);
@@ -998,11 +1108,16 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
                 for (int j = 0; j < 7; ++j) pr[j] = raw[j];
                 const bool cl = clamp_params(pr);
                 const KParams p{pr[0], pr[1], pr[2], pr[3], pr[4], pr[5], pr[6]};
+#ifdef DSO_TCV_NOSWEEP
+                const Best r{pr[0], pr[1], (int)(pr[2] > 1.f)};
+#else
                 const Best r = sweep_dispatch<4>(p, s_core, s_mem, s_pair, J, 0, J.nc);
+#endif
 #pragma unroll
                 for (int d = 0; d < 4; ++d) write_result(J, k, d, r, cl, pr, p, s_core, s_mem);
             }
             TPT_END(9, e_4);
+            if (q == 0 && lane == 0) TRACE(14, t);
         }
     }
     tc::fence_before();

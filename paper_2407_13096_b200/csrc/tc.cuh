@@ -78,6 +78,20 @@ __device__ __forceinline__ void ld16(uint32_t a, float (&v)[16]) {
 #pragma unroll
     for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
+// tcgen05.wait::ld with the loaded registers tied through it: no use of v can be
+// scheduled before the wait (the asm's outputs are the completed values)
+__device__ __forceinline__ void wait_ld_tie(float (&v)[8]) {
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+f"(v[0]), "+f"(v[1]), "+f"(v[2]), "+f"(v[3]), "+f"(v[4]), "+f"(v[5]),
+                   "+f"(v[6]), "+f"(v[7])
+                 :
+                 : "memory");
+}
+// zero-cost ordering point: v is (re)defined here, after every earlier volatile asm
+__device__ __forceinline__ void tie8(float (&v)[8]) {
+    asm volatile("" : "+f"(v[0]), "+f"(v[1]), "+f"(v[2]), "+f"(v[3]), "+f"(v[4]), "+f"(v[5]),
+                 "+f"(v[6]), "+f"(v[7]));
+}
 __device__ __forceinline__ void st8(uint32_t a, const float (&v)[8]) {
     asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(a),
                  "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])),

@@ -4,7 +4,7 @@ import os
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-os.environ["DSO_B200_LIB"] = os.path.join(ROOT, "paper_2407_13096_b200", "lib", "libdso_b200_phase.so")
+os.environ.setdefault("DSO_B200_LIB", os.path.join(ROOT, "paper_2407_13096_b200", "lib", "libdso_b200_phase.so"))
 sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
@@ -22,7 +22,7 @@ names = ["p.wait_XEMPTY", "p.put+arrive", "e.wait_D1", "e.epi1", "e.wait_D2", "e
 ctx = Context(0)
 ctx.set_option("mlp_engine", 1)
 n = 1 << 22
-for mode in ("pipeline_csr", "predict", "pipeline"):
+for mode in os.environ.get("TC_PHASE_MODES", "pipeline_csr,predict,pipeline").split(","):
     ctx.set_domain(config_domain("c3"))
     m = init_mlp(seed=424242)
     m.target_mean = np.array([60, 10, 0.01, 0.004, 0.15, 200, 200.0])
