@@ -146,6 +146,7 @@ __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b
 // Optional per-phase cycle accounting (debug builds only: -DDSO_PHASE_TIMING).
 #ifdef DSO_TC_TRACE
 __device__ unsigned long long g_trace[16 * 64];
+__device__ unsigned long long g_trace2[64 * 6 * 4];
 #endif
 #ifdef DSO_PHASE_TIMING
 __device__ unsigned long long g_phase_cycles[32];
@@ -1276,6 +1277,7 @@ extern "C" int32_t dso_debug_phase_cycles(unsigned long long* out, int reset) {
 extern "C" int32_t dso_debug_trace(unsigned long long* out) {
     cudaDeviceSynchronize();
     cudaMemcpyFromSymbol(out, g_trace, sizeof(unsigned long long) * 16 * 64);
+    cudaMemcpyFromSymbol(out + 16 * 64, g_trace2, sizeof(unsigned long long) * 64 * 6 * 4);
     return 0;
 }
 #endif

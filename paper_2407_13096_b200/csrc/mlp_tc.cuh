@@ -287,17 +287,28 @@ struct Entries {
     int cnt;
     float dg[8];
 };
+// The next tile's row extent and DCGM as raw loads: nothing consumes them until
+// the tile changes (tc_csr_take), so their HBM latency hides behind this tile
+// (deriving first / cnt at load time stalled the producer on every tile).
+struct EntriesRaw {
+    uint64_t a, b;
+    float dg[8];
+};
 
-__device__ __forceinline__ void tc_csr_prefetch(const Job& J, int64_t k, Entries& E) {
-    E.cnt = 0;
-    E.first = 0;
-    if (k < J.n) {
-        const uint64_t a = __ldg(J.row_ptr + k), b = __ldg(J.row_ptr + k + 1);
-        E.first = a - J.ent_base;
-        E.cnt = (int)(b - a);
-    }
+__device__ __forceinline__ void tc_csr_prefetch(const Job& J, int64_t k, EntriesRaw& R) {
+    const int64_t kk = k < J.n ? k : J.n - 1;  // in bounds; tail rows are zeroed on take
+    R.a = __ldg(J.row_ptr + kk);
+    R.b = __ldg(J.row_ptr + kk + 1);
 #pragma unroll
-    for (int j = 0; j < 8; ++j) E.dg[j] = k < J.n ? __ldg(J.dcgm + (int64_t)j * J.ld + k) : 0.f;
+    for (int j = 0; j < 8; ++j) R.dg[j] = __ldg(J.dcgm + (int64_t)j * J.ld + kk);
+}
+__device__ __forceinline__ void tc_csr_take(const Job& J, int64_t k, const EntriesRaw& R,
+                                            Entries& E) {
+    const bool in = k < J.n;
+    E.first = in ? R.a - J.ent_base : 0;
+    E.cnt = in ? (int)(R.b - R.a) : 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) E.dg[j] = in ? R.dg[j] : 0.f;
 }
 
 // The first kEnt entries of a row (0 beyond cnt): 16-byte loads when aligned.
@@ -538,7 +549,11 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         const uint32_t tq = tbase + ((uint32_t)(32 * warp) << 16);
         uint32_t g = 0;  // ring chunks produced
         Entries E;
-        if (MODE == MODE_CSR && my_tiles > 0) tc_csr_prefetch(J, t0_of(0) + row, E);
+        if (MODE == MODE_CSR && my_tiles > 0) {
+            EntriesRaw R0;
+            tc_csr_prefetch(J, t0_of(0) + row, R0);
+            tc_csr_take(J, t0_of(0) + row, R0, E);
+        }
         // CSR: thread 0 bulk-copies tile i's entry range into shared memory (one
         // cp.async.bulk, completing on MB_ESTAGE) when it is 16-byte aligned and fits;
         // otherwise it only arrives, and the kernels read their entries from global
@@ -575,7 +590,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         for (int64_t t = 0; t < my_tiles; ++t) {
             const int64_t k = t0_of(t) + row;
             const int sl = (int)(t & 1);
-            Entries NE;  // next tile's row extent and DCGM, in flight during this tile
+            EntriesRaw NE;  // next tile's row extent and DCGM, in flight during this tile
             if (MODE == MODE_CSR && t + 1 < my_tiles) tc_csr_prefetch(J, t0_of(t + 1) + row, NE);
             if (MODE == MODE_CSR && E.cnt > 0) {
                 // this tile's entries into L1 (read per chunk below)
@@ -618,6 +633,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
             bool uns = false;     // CSR: entries not strictly increasing, or spilled
             bool bad = false;     // a non-finite feature: FMA-pipe forward
             int nlive = 0;        // CSR: live entries (the K-ordered list's length)
+            uint64_t nib = 0;     // CSR: live entries per chunk 1..16, 4 bits each
 #ifdef DSO_TCV_NOPROD
             if (MODE == MODE_CSR) mbar_wait(mb + MB_ESTAGE, (uint32_t)(t & 1));
             if (MODE == MODE_CSR && false) {
@@ -667,6 +683,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
                     colp[e >> 2] |= (live ? (uint32_t)col : 0u) << (8 * (e & 3));
                     ncommon += (live && col < 32) ? 1 : 0;
                     nlive += live ? 1 : 0;
+                    nib += live ? 1ull << (4 * ((col >> 3) - 1)) : 0ull;
                 }
                 const uint32_t t32[3] = {ta - t12, t12 - t2, t2};
                 if (E.cnt > kEnt) {
@@ -804,8 +821,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
             TPT_END(14, p_t);
             // the next tile's entries into L2 while this tile's chunks are produced
             // (its row extent, loaded at this tile's start, has arrived by now)
-            if (MODE == MODE_CSR && t + 1 < my_tiles && NE.cnt > 0) {
-                const uint32_t* ep = J.entries + NE.first;
+            if (MODE == MODE_CSR && t + 1 < my_tiles && t0_of(t + 1) + row < J.n && NE.b > NE.a) {
+                const uint32_t* ep = J.entries + (NE.a - J.ent_base);
                 asm volatile("prefetch.global.L2 [%0];" ::"l"(ep));
                 asm volatile("prefetch.global.L2 [%0];" ::"l"(ep + kEnt - 1));
             }
@@ -843,16 +860,21 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
                         *reinterpret_cast<float4*>(buf + o + 32) = z4;
                         *reinterpret_cast<float4*>(buf + TT * 8 + o) = z4;
                         *reinterpret_cast<float4*>(buf + TT * 8 + o + 32) = z4;
-                        // this chunk's entries: contiguous in the K-ordered list
-                        for (; ep < nlive; ++ep) {
-                            const uint32_t cc = ecl[ep * TT + row];
-                            const float f = el[ep * TT + row];
-                            if ((int)(cc >> 3) != c) break;
-                            const float h = tc::tf32_hi(f);
-                            const int j = cc & 7, off = o + (j >> 2) * 32 + (j & 3);
-                            buf[off] = h;
-                            buf[TT * 8 + off] = f - h;
+                        // this chunk's entries: contiguous in the K-ordered list, their
+                        // number known up front (independent reads, no data-dependent exit)
+                        const int n_c = (int)((nib >> (4 * (c - 1))) & 15u);
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) {
+                            if (i < n_c) {
+                                const uint32_t cc = ecl[(ep + i) * TT + row];
+                                const float f = el[(ep + i) * TT + row];
+                                const float h = tc::tf32_hi(f);
+                                const int j = cc & 7, off = o + (j >> 2) * 32 + (j & 3);
+                                buf[off] = h;
+                                buf[TT * 8 + off] = f - h;
+                            }
                         }
+                        ep += n_c;
                     } else {
                         // duplicate / unsorted / long rows: sum the counts per slot
                         uint32_t acc[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
@@ -921,7 +943,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
             }
             TPT_END(15, p_c);
             if (tid == 0) TRACE(7, t);
-            if (MODE == MODE_CSR && t + 1 < my_tiles) E = NE;
+            if (MODE == MODE_CSR && t + 1 < my_tiles) tc_csr_take(J, t0_of(t + 1) + row, NE, E);
         }
     } else {
         // ============================ epilogue groups ============================

@@ -28,9 +28,11 @@ g = ctx.gen_synthetic_csr(n, root=3)
 for _ in range(2):
     ctx.pipeline_csr(g["row_ptr"], g["entries"], g["dcgm"], 0.8)
 ctx.sync()
-buf = (C.c_ulonglong * (16 * 64))()
+buf = (C.c_ulonglong * (16 * 64 + 64 * 24))()
 L.dso_debug_trace(buf)
-tr = np.array(buf, dtype=np.int64).reshape(16, 64)
+allv = np.array(buf, dtype=np.int64)
+tr = allv[:1024].reshape(16, 64)
+tr2 = allv[1024:].reshape(64, 6, 4)
 names = ["L1 first", "L1 last", "L2 first", "L2 last", "P start", "P mask", "-", "P done",
          "E wD1 beg", "E D1 got", "E epi1 end", "E D2 got", "E D2 read", "E epi3 end", "E done"]
 t0 = tr[4, 8]
@@ -38,3 +40,13 @@ print("tile " + " ".join(f"{x:>10s}" for x in names if x != "-"))
 for t in range(8, 30):
     row = [tr[e, t] - t0 for e in range(15) if e != 6]
     print(f"{t:4d} " + " ".join(f"{v:10d}" for v in row))
+
+print("\nproducer thread 0, per chunk: claim begin / claim end / written / handed over (rel. to P mask)")
+for t in range(8, 14):
+    base = tr[5, t]
+    print(f"{t:4d} " + "  ".join("/".join(str(int(v - base)) for v in tr2[t, c]) for c in range(5) if tr2[t, c, 0]))
+
+print("\nproducer thread 0, prep: entries loaded / decoded / exchanged / list written (rel. to P start)")
+for t in range(8, 14):
+    base = tr[4, t]
+    print(f"{t:4d} " + " / ".join(str(int(v - base)) for v in tr2[t, 5]) + f"   mask at {int(tr[5, t] - base)}")
