@@ -103,22 +103,21 @@ constexpr int kRing = 2;                     // X chunk buffers
 constexpr int kChunkF = 2 * TT * 8;          // hi [128][8] + lo [128][8] (core-matrix layout)
 constexpr int S_STATS = kModel;              // mean[8] std[8]
 constexpr int S_RING = S_STATS + 16;
-// CSR: per-kernel entry lists of the tile being produced, entry-major so a warp's
-// 32 kernels hit 32 banks: fraction [24][128] f32 and column [24][128] u8
-constexpr int S_ELIST = S_RING + kRing * kChunkF;
-constexpr int S_ECOL = S_ELIST + 24 * TT;
-constexpr int S_MISC = S_ECOL + 24 * TT / 4;  // u32: [0..1] chunk masks, [2..9] slow rows, [10..17] partial masks
+constexpr int S_MISC = S_RING + kRing * kChunkF;  // u32: [0..1] chunk masks, [2..9] slow rows, [10..17] partial masks
 constexpr int S_PERM = S_MISC + 24;  // u8 pos_of[128] (slot -> K position), slot_at[128]
-// CSR: the tile's entries, bulk-copied from global a tile ahead (when the tile's
-// entry range is 16-byte aligned and fits), [0] base entry index, [2] staged flag
-constexpr int kStageEnt = 24 * TT;
+// CSR: the entries of tiles t and t+1, each bulk-copied a tile ahead into its own
+// buffer (the tile's entry range widened to 16-byte boundaries; 27.5 entries per
+// kernel on average fit).  Per buffer meta: [0,1] first staged entry index, [2]
+// staged flag.  A tile whose range does not fit reads its entries from global.
+constexpr int kStageEnt = 3520;
 constexpr int S_ESTAGE = S_PERM + 64;
-constexpr int S_EMETA = S_ESTAGE + kStageEnt;
-constexpr int S_MBAR = S_EMETA + 4;
+constexpr int S_EMETA = S_ESTAGE + 2 * kStageEnt;
+constexpr int S_MBAR = S_EMETA + 8;
 enum {
     MB_XFULL = 0, MB_XEMPTY = 3, MB_D1F = 6, MB_A2R = 8, MB_D2F = 34, MB_D2FREE = 36,
-    MB_SLOWFREE = 37, MB_ESTAGE = 39, kMbars = 40
+    MB_SLOWFREE = 37, MB_ESTAGE = 39, kMbars = 41
 };
+static_assert(S_ESTAGE % 4 == 0 && kStageEnt % 4 == 0, "bulk-copy destinations are 16-byte aligned");
 constexpr int S_TSLOT = S_MBAR + 2 * kMbars;
 constexpr int S_TABLES = (S_TSLOT + 4 + 3) & ~3;  // core4[nc], mem2[nm], level pairs
 static_assert(kModel % 4 == 0 && S_RING % 4 == 0 && S_MBAR % 2 == 0, "tc smem alignment");
@@ -279,9 +278,8 @@ __device__ __noinline__ void tc_forward_x(const float* sm, const float* x, float
 }
 
 // CSR row of one kernel (thread = kernel): extent and DCGM prefetched a tile
-// ahead in registers, the entries pulled into L1 ahead and re-read from L1 per
-// chunk (keeping 24 entries live in registers would spill).
-constexpr int kEnt = 24;
+// ahead in registers; the entries themselves are read from the tile's staged copy
+// in shared memory (or from global when the tile was not staged).
 struct Entries {
     uint64_t first;
     int cnt;
@@ -309,24 +307,6 @@ __device__ __forceinline__ void tc_csr_take(const Job& J, int64_t k, const Entri
     E.cnt = in ? (int)(R.b - R.a) : 0;
 #pragma unroll
     for (int j = 0; j < 8; ++j) E.dg[j] = in ? R.dg[j] : 0.f;
-}
-
-// The first kEnt entries of a row (0 beyond cnt): 16-byte loads when aligned.
-__device__ __forceinline__ void load_entries(const uint32_t* __restrict__ p, int cnt,
-                                             uint32_t (&en)[kEnt]) {
-    if ((reinterpret_cast<uintptr_t>(p) & 15) == 0 && cnt >= kEnt) {
-#pragma unroll
-        for (int v = 0; v < kEnt / 4; ++v) {
-            const uint4 x = __ldg(reinterpret_cast<const uint4*>(p) + v);
-            en[4 * v] = x.x;
-            en[4 * v + 1] = x.y;
-            en[4 * v + 2] = x.z;
-            en[4 * v + 3] = x.w;
-        }
-    } else {
-#pragma unroll
-        for (int e = 0; e < kEnt; ++e) en[e] = e < cnt ? __ldg(p + e) : 0u;
-    }
 }
 
 // exact per-category totals -> (tf, rr) for normalize_count (see csr_features)
@@ -362,6 +342,13 @@ __device__ __forceinline__ float norm_slot(uint32_t cnt, int slot, const float (
     const int cat = cat_of_row(slot);
     return normalize_count(cnt, cat == 0 ? tf[0] : (cat == 1 ? tf[1] : tf[2]),
                            cat == 0 ? rr[0] : (cat == 1 ? rr[1] : rr[2]));
+}
+
+// st.shared.f32 under a predicate (no branch around the store)
+__device__ __forceinline__ void sts_pred(uint32_t a, float v, bool p) {
+    asm volatile("{ .reg .pred q; setp.ne.u32 q, %2, 0; @q st.shared.f32 [%0], %1; }" ::"r"(a), "f"(v),
+                 "r"((uint32_t)p)
+                 : "memory");
 }
 
 // One 8-column chunk of one kernel into a ring buffer (core-matrix layout).
@@ -429,6 +416,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
             }
             mb_init(mb + MB_D2FREE, 4);
             mb_init(mb + MB_ESTAGE, 1);
+            mb_init(mb + MB_ESTAGE + 1, 1);
             asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         }
         if (warp == MMA_WARP) tc::tmem_alloc<512>(tslot);
@@ -554,36 +542,40 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
             tc_csr_prefetch(J, t0_of(0) + row, R0);
             tc_csr_take(J, t0_of(0) + row, R0, E);
         }
-        // CSR: thread 0 bulk-copies tile i's entry range into shared memory (one
-        // cp.async.bulk, completing on MB_ESTAGE) when it is 16-byte aligned and fits;
-        // otherwise it only arrives, and the kernels read their entries from global
+        // CSR: thread 0 bulk-copies tile i's entry range, widened to 16-byte boundaries,
+        // into stage buffer i & 1 (one cp.async.bulk completing on MB_ESTAGE + (i & 1));
+        // when the widened range does not fit, or would leave the batch's entry array,
+        // it only arrives and the tile reads its entries from global
+        uint64_t ent_total = 0;  // entries of the batch (thread 0)
+        if (MODE == MODE_CSR && tid == 0) ent_total = __ldg(J.row_ptr + J.n) - J.ent_base;
         auto stage = [&](int64_t i) {
             if (MODE != MODE_CSR || tid != 0) return;
+            const int sb = (int)(i & 1);
             const int64_t t0i = t0_of(i), t1i = t0i + TT < J.n ? t0i + TT : J.n;
             const uint64_t a = __ldg(J.row_ptr + t0i) - J.ent_base, b = __ldg(J.row_ptr + t1i) - J.ent_base;
-            const uint64_t bytes = (b - a) * 4;
-            const uint32_t* src = J.entries + a;
-            uint32_t* meta = reinterpret_cast<uint32_t*>(sm + S_EMETA);
-            const bool ok = bytes > 0 && bytes <= (uint64_t)kStageEnt * 4 && (bytes & 15) == 0 &&
-                            (reinterpret_cast<uintptr_t>(src) & 15) == 0;
-            meta[0] = (uint32_t)a;
-            meta[1] = (uint32_t)(a >> 32);
+            const uint64_t mis = (reinterpret_cast<uintptr_t>(J.entries + a) & 15) >> 2;
+            const uint64_t a4 = a - mis, b4 = a4 + ((b - a4 + 3) & ~3ull);
+            uint32_t* meta = reinterpret_cast<uint32_t*>(sm + S_EMETA) + 4 * sb;
+            const bool ok = b > a && a >= mis && b4 <= ent_total && b4 - a4 <= (uint64_t)kStageEnt;
+            meta[0] = (uint32_t)a4;
+            meta[1] = (uint32_t)(a4 >> 32);
             meta[2] = ok ? 1u : 0u;
-            const uint32_t bar = smem_u32(mb + MB_ESTAGE);
+            const uint32_t bar = smem_u32(mb + MB_ESTAGE + sb);
             if (ok) {
+                const uint32_t bytes = (uint32_t)(b4 - a4) * 4u;
                 // the buffer was last read through the generic proxy (the barrier before
                 // this call ordered every producer's reads); the bulk copy writes it
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
-                             "r"((uint32_t)bytes)
+                             "r"(bytes)
                              : "memory");
                 asm volatile(
                     "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                        smem_u32(sm + S_ESTAGE)),
-                    "l"(src), "r"((uint32_t)bytes), "r"(bar)
+                        smem_u32(sm + S_ESTAGE + sb * kStageEnt)),
+                    "l"(J.entries + a4), "r"(bytes), "r"(bar)
                     : "memory");
             } else {
-                mb_arrive(mb + MB_ESTAGE);
+                mb_arrive(mb + MB_ESTAGE + sb);
             }
         };
         if (my_tiles > 0) stage(0);
@@ -592,12 +584,6 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
             const int sl = (int)(t & 1);
             EntriesRaw NE;  // next tile's row extent and DCGM, in flight during this tile
             if (MODE == MODE_CSR && t + 1 < my_tiles) tc_csr_prefetch(J, t0_of(t + 1) + row, NE);
-            if (MODE == MODE_CSR && E.cnt > 0) {
-                // this tile's entries into L1 (read per chunk below)
-                const uint32_t* ep = J.entries + E.first;
-                asm volatile("prefetch.global.L1 [%0];" ::"l"(ep));
-                asm volatile("prefetch.global.L1 [%0];" ::"l"(ep + kEnt - 1));
-            }
             // predict / dense: the input rows of tile t+2 into L2 (bulk prefetches, one
             // 512-byte row segment per thread, no registers or shared memory held), so
             // the chunk loads below hit L2 rather than HBM
@@ -630,65 +616,83 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
             // ---- per-kernel preparation: totals, chunk mask, non-finite rows ----
             float tf[3] = {0.f, 0.f, 0.f}, rr[3] = {0.f, 0.f, 0.f};
             uint32_t mask = 1u;   // chunks this kernel touches (chunk 0: DCGM)
-            bool uns = false;     // CSR: entries not strictly increasing, or spilled
+            bool uns = false;     // CSR: general path (unsorted / duplicate slots, > 64
+                                  // entries, a category total >= 2^24)
             bool bad = false;     // a non-finite feature: FMA-pipe forward
-            int nlive = 0;        // CSR: live entries (the K-ordered list's length)
             uint64_t nib = 0;     // CSR: live entries per chunk 1..16, 4 bits each
-#ifdef DSO_TCV_NOPROD
-            if (MODE == MODE_CSR) mbar_wait(mb + MB_ESTAGE, (uint32_t)(t & 1));
-            if (MODE == MODE_CSR && false) {
-#else
+            uint64_t cbits = 0;   // CSR: row positions of the entries in the common
+            uint64_t obits = 0;   //   categories (chunks 1-3) and of the others (4-16)
+            const int sb = (int)(t & 1);
+            bool staged = false;
+            const uint32_t* s_row = nullptr;  // CSR: this kernel's staged entries
             if (MODE == MODE_CSR) {
-#endif
-                uint64_t tot[3] = {0, 0, 0};
-                // category totals as suffix sums over the slot order: all, dtype +
-                // memspace (slot >= 101), memspace (slot >= 118)
+                TPT_BEGIN(p_l);
+                mbar_wait(mb + MB_ESTAGE + sb, (uint32_t)((t >> 1) & 1));
+                {
+                    const uint32_t* meta = reinterpret_cast<const uint32_t*>(sm + S_EMETA) + 4 * sb;
+                    staged = meta[2] != 0;
+                    const uint64_t base = meta[0] | ((uint64_t)meta[1] << 32);
+                    // (an empty row, e.g. past the batch end, points at the buffer start:
+                    // pass B reads a valid word for its predicated-off slots)
+                    s_row = reinterpret_cast<const uint32_t*>(sm + S_ESTAGE + sb * kStageEnt) +
+                            (E.cnt > 0 ? E.first - base : 0);
+                }
+                // pass A, one visit per entry: category totals (suffix sums over the slot
+                // order: all, dtype + memspace (slot >= 101), memspace (slot >= 118)),
+                // chunk mask, live entries per chunk, and which entries are common-
+                // category ones (their K positions 0..23 come first, in slot order; the
+                // others follow, also in slot order)
                 uint32_t ta = 0u, t12 = 0u, t2 = 0u;
                 int prev = -1;
-                uint32_t en[kEnt];
-                TPT_BEGIN(p_l);
-                mbar_wait(mb + MB_ESTAGE, (uint32_t)(t & 1));
-                {
-                    const uint32_t* meta = reinterpret_cast<const uint32_t*>(sm + S_EMETA);
-                    if (meta[2]) {  // staged: this kernel's entries from shared memory
-                        const uint64_t base = meta[0] | ((uint64_t)meta[1] << 32);
-                        const uint32_t* sp = reinterpret_cast<const uint32_t*>(sm + S_ESTAGE) +
-                                             (E.first - base);
-#pragma unroll
-                        for (int e = 0; e < kEnt; ++e) en[e] = e < E.cnt ? sp[e] : 0u;
-                    } else {
-                        load_entries(J.entries + E.first, E.cnt, en);
-                    }
-                }
-                // one branch-free pass: liveness, K column, category totals, chunk
-                // mask and counts per chunk (the column lookup done once per entry)
-                uint32_t colp[kEnt / 4];  // K columns, four per register (0 = dead entry)
-                int ncommon = 0;          // live entries in the common-category columns
-#pragma unroll
-                for (int e4 = 0; e4 < kEnt / 4; ++e4) colp[e4] = 0u;
-#pragma unroll
-                for (int e = 0; e < kEnt; ++e) {
-                    const int slot = (int)(en[e] & 127u);
-                    const uint32_t cnt = en[e] >> 7;
-                    const bool inrow = e < E.cnt;
+                auto visit = [&](uint32_t en, int e, bool inrow) {
+                    const int slot = (int)(en & 127u);
+                    const uint32_t c = en >> 7;
                     const bool live = inrow && slot < DSO_COUNT_ROWS;
                     uns |= inrow && slot <= prev;
                     prev = inrow ? slot : prev;
-                    const int col = 8 + pos_of[live ? slot : 0];
-                    const uint32_t cl = live ? cnt : 0u;
+                    const int pos = pos_of[slot];
+                    const uint32_t cl = live ? c : 0u;
                     ta += cl;
                     t12 += slot >= DSO_INSTR_SLOTS ? cl : 0u;
                     t2 += slot >= DSO_INSTR_SLOTS + DSO_DTYPE_SLOTS ? cl : 0u;
-                    mask |= live ? 1u << (col >> 3) : 0u;
-                    colp[e >> 2] |= (live ? (uint32_t)col : 0u) << (8 * (e & 3));
-                    ncommon += (live && col < 32) ? 1 : 0;
-                    nlive += live ? 1 : 0;
-                    nib += live ? 1ull << (4 * ((col >> 3) - 1)) : 0ull;
-                }
-                const uint32_t t32[3] = {ta - t12, t12 - t2, t2};
-                if (E.cnt > kEnt) {
+                    const int ch = (pos + 8) >> 3;
+                    mask |= live ? 1u << ch : 0u;
+                    nib += live ? 1ull << (4 * ch - 4) : 0ull;
+                    const uint64_t bit = 1ull << e;
+                    cbits |= (live && pos < 24) ? bit : 0ull;
+                    obits |= (live && pos >= 24) ? bit : 0ull;
+                };
+                const int ce = E.cnt;
+                if (ce <= 64) {
+                    // branch-free: out-of-row slots load a valid word and are ignored
+                    if (staged) {
+#pragma unroll 1
+                        for (int e0 = 0; e0 < ce; e0 += 4) {
+                            uint32_t en[4];
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) en[u] = s_row[e0 + u < ce ? e0 + u : 0];
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) visit(en[u], e0 + u, e0 + u < ce);
+                        }
+                    } else {
+                        const uint32_t* gp = J.entries + E.first;
+#pragma unroll 1
+                        for (int e0 = 0; e0 < ce; e0 += 4) {
+                            uint32_t en[4];
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) en[u] = __ldg(gp + (e0 + u < ce ? e0 + u : 0));
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) visit(en[u], e0 + u, e0 + u < ce);
+                        }
+                    }
+                    const uint64_t tot[3] = {ta - t12, t12 - t2, t2};
+                    cat_scales(tot, tf, rr);
+                    uns |= tf[0] < 0.f || tf[1] < 0.f || tf[2] < 0.f;  // a total >= 2^24
+                } else {
+                    // a long row: totals and mask by the general path
                     uns = true;
-                    for (int idx = kEnt; idx < E.cnt; ++idx) {
+                    uint64_t tot[3] = {0, 0, 0};
+                    for (int idx = 0; idx < ce; ++idx) {
                         const uint32_t en = __ldg(J.entries + E.first + idx);
                         const int slot = (int)(en & 127u);
                         if (slot < DSO_COUNT_ROWS) {
@@ -699,48 +703,11 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
                             mask |= 1u << ((8 + pos_of[slot]) >> 3);
                         }
                     }
-                }
-#pragma unroll
-                for (int c = 0; c < 3; ++c) tot[c] += t32[c];
-                cat_scales(tot, tf, rr);
-                uns |= tf[0] < 0.f || tf[1] < 0.f || tf[2] < 0.f;  // a total >= 2^24
-                TPT_END(16, p_l);
-                TPT_BEGIN(p_f);
-                // this kernel's entry list (fraction, column) in slot order, and how
-                // many entries fall in each 8-column chunk
-                // list order = K order: the common categories (columns < 32, increasing
-                // with the slot) first, then the others (also increasing with the slot)
-                float* el = sm + S_ELIST;
-                uint8_t* ecl = reinterpret_cast<uint8_t*>(sm + S_ECOL);
-                if (ncommon == nlive) {
-                    // only common categories: slot order is already K order
-                    int ne = 0;
-#pragma unroll
-                    for (int e = 0; e < kEnt; ++e) {
-                        const uint32_t col = (colp[e >> 2] >> (8 * (e & 3))) & 0xFFu;
-                        if (col) {
-                            el[ne * TT + row] = norm_fast(en[e] >> 7, (int)(en[e] & 127u), tf, rr);
-                            ecl[ne * TT + row] = (uint8_t)col;
-                        }
-                        ne += col ? 1 : 0;
-                    }
-                } else {
-                    int nlo = 0, nhi = ncommon;
-#pragma unroll
-                    for (int e = 0; e < kEnt; ++e) {
-                        const uint32_t col = (colp[e >> 2] >> (8 * (e & 3))) & 0xFFu;
-                        const int at = col < 32u ? nlo : nhi;
-                        if (col) {
-                            el[at * TT + row] = norm_fast(en[e] >> 7, (int)(en[e] & 127u), tf, rr);
-                            ecl[at * TT + row] = (uint8_t)col;
-                        }
-                        nlo += (col && col < 32u) ? 1 : 0;
-                        nhi += (col >= 32u) ? 1 : 0;
-                    }
+                    cat_scales(tot, tf, rr);
                 }
 #pragma unroll
                 for (int j = 0; j < 8; ++j) bad |= !isfinite(E.dg[j]);
-                TPT_END(17, p_f);
+                TPT_END(16, p_l);
             } else if (MODE == MODE_DENSE) {
                 uint64_t tot[3] = {0, 0, 0};
                 if (k < J.n) {
@@ -772,7 +739,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
             {
                 const uint32_t wm = __reduce_or_sync(0xffffffffu, mask);
                 if (lane == 0) misc[10 + 4 * sl + warp] = wm;
-                bar_sync(1, kGroupT);  // (also: every producer has read this tile's stage)
+                // (also: every producer has finished tile t-1, whose stage buffer the
+                // copy for tile t+1 reuses)
+                bar_sync(1, kGroupT);
                 mask = misc[10 + 4 * sl] | misc[11 + 4 * sl] | misc[12 + 4 * sl] | misc[13 + 4 * sl];
                 if (tid == 0) misc[sl] = mask;
                 if (t + 1 < my_tiles) stage(t + 1);
@@ -824,7 +793,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
             if (MODE == MODE_CSR && t + 1 < my_tiles && t0_of(t + 1) + row < J.n && NE.b > NE.a) {
                 const uint32_t* ep = J.entries + (NE.a - J.ent_base);
                 asm volatile("prefetch.global.L2 [%0];" ::"l"(ep));
-                asm volatile("prefetch.global.L2 [%0];" ::"l"(ep + kEnt - 1));
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(ep + (NE.b - NE.a) - 1));
             }
             TPT_BEGIN(p_c);
             // ---- chunks -> ring ----------------------------------------------------
@@ -843,38 +812,82 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
             };
             const int o = (row >> 3) * 64 + (row & 7) * 4;  // this kernel's core-matrix rows
             if (MODE == MODE_CSR) {
-                const float* el = sm + S_ELIST;
-                const uint8_t* ecl = reinterpret_cast<const uint8_t*>(sm + S_ECOL);
-                int ep = 0;  // first list entry of the current chunk
+                // pass B: chunk c's entries are the next n_c common-category entries
+                // (c = 1..3) or the next n_c others (c = 4..16) in row order: their
+                // positions are popped off cbits / obits, four per step
+                const float tf0 = tf[0], tf1 = tf[1], tf2 = tf[2], rr0 = rr[0], rr1 = rr[1],
+                            rr2 = rr[2];
+                const uint32_t buf_row = smem_u32(sm + S_RING) + 4u * (uint32_t)o;
+                // global reads of an empty row go to entry 0 (some kernel of the tile has
+                // entries whenever pass B runs, so the array is not empty)
+                const uint64_t g_first = E.cnt > 0 ? E.first : 0;
+                // branch-free: entries beyond n_c load a valid word (position 0) and
+                // their stores are predicated off
+                auto take = [&](auto stg, uint64_t& rem, int n_c, int nmax, uint32_t bufa) {
+#pragma unroll 1
+                    for (int i0 = 0; i0 < nmax; i0 += 4) {
+                        uint32_t en[4];
+                        bool on[4];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            on[u] = i0 + u < n_c;
+                            const uint32_t lo = (uint32_t)rem, hi = (uint32_t)(rem >> 32);
+                            int e = lo ? __ffs(lo) - 1 : 31 + __ffs(hi);
+                            e = on[u] ? e : 0;
+                            rem = on[u] ? rem & (rem - 1) : rem;
+                            if constexpr (decltype(stg)::value)
+                                en[u] = s_row[e];
+                            else
+                                en[u] = __ldg(J.entries + g_first + e);
+                        }
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const int slot = (int)(en[u] & 127u);
+                            float t = tf0, r = rr0;
+                            t = slot >= DSO_INSTR_SLOTS ? tf1 : t;
+                            r = slot >= DSO_INSTR_SLOTS ? rr1 : r;
+                            t = slot >= DSO_INSTR_SLOTS + DSO_DTYPE_SLOTS ? tf2 : t;
+                            r = slot >= DSO_INSTR_SLOTS + DSO_DTYPE_SLOTS ? rr2 : r;
+                            const uint32_t c = en[u] >> 7;
+                            const float cf = (__int_as_float(0x4B000000u | (c & 0x7FFFFFu)) - 8388608.f) +
+                                             ((c & 0x800000u) ? 8388608.f : 0.f);
+                            const float qq = __fmul_rn(cf, r);
+                            const float f = fmaf(fmaf(-qq, t, cf), r, qq);
+                            const float h = tc::tf32_hi(f);
+                            const int j = pos_of[slot] & 7;
+                            const uint32_t a = bufa + 4u * (uint32_t)((j >> 2) * 32 + (j & 3));
+                            sts_pred(a, h, on[u]);
+                            sts_pred(a + 4u * TT * 8, f - h, on[u]);
+                        }
+                    }
+                };
 #pragma unroll 1
                 for (int c = 0; c < 17; ++c) {
                     if (!((mask >> c) & 1u)) continue;
                     const int b = claim();
                     float* buf = sm + S_RING + b * kChunkF;
+                    const int n_c = (c == 0 || uns) ? 0 : (int)((nib >> (4 * (c - 1))) & 15u);
+                    const int nmax = __reduce_max_sync(0xffffffffu, n_c);
                     if (c == 0) {
                         put_chunk(buf, row, E.dg);
                     } else if (!uns) {
-                        // zeros, then this chunk's entries in place (predicated scan)
+                        // zeros, then this chunk's entries in place
                         const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
                         *reinterpret_cast<float4*>(buf + o) = z4;
                         *reinterpret_cast<float4*>(buf + o + 32) = z4;
                         *reinterpret_cast<float4*>(buf + TT * 8 + o) = z4;
                         *reinterpret_cast<float4*>(buf + TT * 8 + o + 32) = z4;
-                        // this chunk's entries: contiguous in the K-ordered list, their
-                        // number known up front (independent reads, no data-dependent exit)
-                        const int n_c = (int)((nib >> (4 * (c - 1))) & 15u);
-#pragma unroll
-                        for (int i = 0; i < 8; ++i) {
-                            if (i < n_c) {
-                                const uint32_t cc = ecl[(ep + i) * TT + row];
-                                const float f = el[(ep + i) * TT + row];
-                                const float h = tc::tf32_hi(f);
-                                const int j = cc & 7, off = o + (j >> 2) * 32 + (j & 3);
-                                buf[off] = h;
-                                buf[TT * 8 + off] = f - h;
-                            }
+                        if (c < 4) {
+                            if (staged)
+                                take(std::true_type{}, cbits, n_c, nmax, buf_row + 4u * b * kChunkF);
+                            else
+                                take(std::false_type{}, cbits, n_c, nmax, buf_row + 4u * b * kChunkF);
+                        } else {
+                            if (staged)
+                                take(std::true_type{}, obits, n_c, nmax, buf_row + 4u * b * kChunkF);
+                            else
+                                take(std::false_type{}, obits, n_c, nmax, buf_row + 4u * b * kChunkF);
                         }
-                        ep += n_c;
                     } else {
                         // duplicate / unsorted / long rows: sum the counts per slot
                         uint32_t acc[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};

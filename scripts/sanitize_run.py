@@ -35,6 +35,26 @@ for cfg in ("c1", "c3"):
         gr, loss = ctx.train_grad(f, y)
         ctx.train_apply(gr, 0.01, 1.0 / n)
         ctx.dcgm_mean(torch.rand((3, 8, n), device="cuda", dtype=torch.float64))
+# the tcgen05 engine's CSR producer on irregular rows: 0..70 slot-sorted entries
+# (staged / global / general paths), empty rows at the end, misaligned entry arrays
+rng = np.random.default_rng(3)
+ctx.set_domain(config_domain("c3"))
+for n in (5, 300, 1500):
+    lens = rng.integers(0, 71, size=n)
+    lens[-3:] = 0
+    ents, rp = [], [0]
+    for L in lens:
+        sl = np.sort(rng.choice(126, size=int(L), replace=False))
+        ents.extend(((rng.integers(1, 5000, size=int(L)) << 7) | sl).tolist())
+        rp.append(len(ents))
+    ent = np.array(ents, np.int64).astype(np.int32)
+    for shift in (0, 1, 3):
+        buf = torch.zeros(len(ent) + 4, dtype=torch.int32, device="cuda")
+        buf[shift:shift + len(ent)] = torch.from_numpy(ent).cuda()
+        ctx.set_option("mlp_engine", 1)
+        ctx.pipeline_csr(torch.tensor(rp, dtype=torch.int64, device="cuda"), buf[shift:shift + len(ent)],
+                         torch.rand((8, n), device="cuda"), 0.8, want_params=True)
+ctx.set_option("mlp_engine", 2)
 # per-context scratch in any call order (regression: the eta table's growth once
 # freed the dcgm_mean flag), then destroy
 c2 = Context(0)

@@ -209,6 +209,35 @@ def test_pipeline_csr_sorted_random_slots(ctx, port):
         np.testing.assert_array_equal(a[f].cpu().numpy(), b[f].cpu().numpy())
 
 
+def test_pipeline_csr_long_sorted_rows(ctx, port):
+    """Slot-sorted rows of 20..70 entries (the tcgen05 engine's two-pass producer for
+    any row up to 64 entries, the general path beyond; tiles over the shared-memory
+    stage read from global), entry arrays starting 1..3 words past a 16-byte
+    boundary — equal to the dense pipeline bit for bit."""
+    dom = config_domain("c3")
+    ctx.set_domain(dom)
+    ctx.set_model(stats_model(port))
+    rng = np.random.default_rng(9)
+    n = 6000 + 7
+    counts = np.zeros((n, 126), np.uint32)
+    for k in range(n):
+        nnz = int(rng.integers(20, 71)) if k < 3000 else int(rng.integers(20, 31))
+        slots = rng.choice(126, size=nnz, replace=False)
+        counts[k, slots] = rng.integers(1, 120_000, size=nnz)
+    dcgm = rng.uniform(0, 1, size=(n, 8)).astype(np.float32)
+    rp, ent = csr_from_dense(counts)
+    dc_t = torch.from_numpy(np.ascontiguousarray(dcgm.T)).cuda()
+    a = ctx.pipeline(torch.from_numpy(np.ascontiguousarray(counts.T).view(np.int32)).cuda(), dc_t,
+                     0.5, want_params=True)
+    for shift in (0, 1, 2, 3):
+        buf = torch.zeros(len(ent) + 8, dtype=torch.int32, device="cuda")
+        buf[shift:shift + len(ent)] = torch.from_numpy(ent.view(np.int32)).cuda()
+        b = ctx.pipeline_csr(torch.from_numpy(rp).cuda(), buf[shift:shift + len(ent)], dc_t, 0.5,
+                             want_params=True)
+        for f in ("idx", "cost", "energy", "time", "params", "clamped"):
+            np.testing.assert_array_equal(a[f].cpu().numpy(), b[f].cpu().numpy())
+
+
 def test_pipeline_csr_host_large(ctx, port):
     dom = config_domain("c3")
     ctx.set_domain(dom)
