@@ -149,6 +149,11 @@ __device__ __forceinline__ void commit(uint64_t* mbar) {
 
 // TF32 split for 3xTF32: hi = rna(x) to 10 mantissa bits, lo = x - hi (the MMA
 // reads lo's top 10 mantissa bits).  hi*hi + hi*lo + lo*hi carries ~22 bits.
+// cvt.rna.tf32's rounding for finite x by integer arithmetic (2 instructions
+// instead of ptxas's expansion with special-value handling)
+__device__ __forceinline__ float tf32_hi_finite(float x) {
+    return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
+}
 __device__ __forceinline__ float tf32_hi(float x) {
     uint32_t r;
     asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
