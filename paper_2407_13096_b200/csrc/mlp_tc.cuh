@@ -204,7 +204,7 @@ __device__ __forceinline__ void store_split(uint32_t a_hi, uint32_t a_lo, const 
     float h[8], l[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-        h[j] = tc::tf32_hi(v[j]);
+        h[j] = tc::tf32_hi_finite(v[j]);  // sigmoid outputs: finite
         l[j] = v[j] - h[j];
     }
     tc::st8(a_hi, h);
@@ -1028,6 +1028,24 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         const float2* s_mem = reinterpret_cast<const float2*>(sm + S_TABLES + 4 * J.nc);
         const float4* s_pair =
             J.pairs ? reinterpret_cast<const float4*>(sm + tc_pairs_offset(J.nc, J.nm)) : nullptr;
+        // pipeline modes: clamped parameters of the tile's kernels -> grid sweep
+        // (a sweep of the previous tile placed in this tile's layer-2 wait measured
+        // slower: the producers, not the layer-2 hand-off, bound the engine)
+        struct Pending {
+            int64_t k;
+            float pr[7];
+            bool cl;
+        } pend;
+        auto sweep_out = [&](const Pending& P) {
+            const KParams p{P.pr[0], P.pr[1], P.pr[2], P.pr[3], P.pr[4], P.pr[5], P.pr[6]};
+#ifdef DSO_TCV_NOSWEEP
+            const Best r{P.pr[0], P.pr[1], (int)(P.pr[2] > 1.f)};
+#else
+            const Best r = sweep_dispatch<4>(p, s_core, s_mem, s_pair, J, 0, J.nc);
+#endif
+#pragma unroll
+            for (int d = 0; d < 4; ++d) write_result(J, P.k, d, r, P.cl, P.pr, p, s_core, s_mem);
+        };
         for (int64_t t = grp; t < my_tiles; t += 2) {
             const uint32_t ph = (uint32_t)((t >> 1) & 1);
             const int64_t k = t0_of(t) + row;
@@ -1197,20 +1215,15 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
                     if (J.clamped) J.clamped[k] = cl ? 1 : 0;
                 }
             } else {
-                float pr[7];
 #pragma unroll
-                for (int j = 0; j < 7; ++j) pr[j] = raw[j];
-                const bool cl = clamp_params(pr);
-                const KParams p{pr[0], pr[1], pr[2], pr[3], pr[4], pr[5], pr[6]};
-#ifdef DSO_TCV_NOSWEEP
-                const Best r{pr[0], pr[1], (int)(pr[2] > 1.f)};
-#else
-                const Best r = sweep_dispatch<4>(p, s_core, s_mem, s_pair, J, 0, J.nc);
-#endif
-#pragma unroll
-                for (int d = 0; d < 4; ++d) write_result(J, k, d, r, cl, pr, p, s_core, s_mem);
+                for (int j = 0; j < 7; ++j) pend.pr[j] = raw[j];
+                pend.cl = clamp_params(pend.pr);
+                pend.k = k;
+                TPT_END(10, e_4);
+                TPT_BEGIN(e_s);
+                sweep_out(pend);
+                TPT_END(9, e_s);
             }
-            TPT_END(9, e_4);
             if (q == 0 && lane == 0) TRACE(14, t);
         }
     }

@@ -15,10 +15,9 @@ from paper_2407_13096_b200.api import Context  # noqa: E402
 L = _lib.lib()
 L.dso_debug_phase_cycles.argtypes = [C.c_void_p, C.c_int]
 # epilogue phases are recorded by group 0 only (every other tile): scaled x2 below
-names = ["p.wait_XEMPTY", "p.put+arrive", "e.wait_D1", "e.epi1", "e.wait_D2", "e.epi2", "e.wait_D3",
-         "e.epi3", "e.wait_D4", "e.epi4+sweep", "m.L1(waits X)", "m.L2", "m.L3", "m.L4",
-         "p.prep", "p.chunks", "m.wait_XFULL", "p.prep.load+totals", "p.prep.lists",
-         "p.prep.mask", "p.prep.slow"]
+names = ["p.wait_XEMPTY", "p.put+arrive", "e.wait_D1", "e.epi1", "e.wait_D2", "e.epi2", "-",
+         "e.epi3", "-", "e.sweep(prev tile)", "e.clamp+slow", "-", "-", "-",
+         "p.prep", "p.chunks", "p.passA", "-", "p.mask", "p.slow"]
 ctx = Context(0)
 ctx.set_option("mlp_engine", 1)
 n = 1 << 22
