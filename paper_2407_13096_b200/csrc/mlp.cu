@@ -1216,6 +1216,17 @@ cudaError_t launch_tc(Ctx& cx, const Job& J) {
         cudaError_t e = ensure_smem_attr((const void*)tce::tc_kernel<MODE>, cx.device, 227 * 1024);
         if (e != cudaSuccess) return e;
     }
+    {
+        // the per-role setmaxnreg plan assumes the launch allocation kRegLaunch
+        // (releases must cover increases, or the kernel would block forever)
+        static const int regs = [] {
+            cudaFuncAttributes a{};
+            return cudaFuncGetAttributes(&a, (const void*)tce::tc_kernel<MODE>) == cudaSuccess
+                       ? a.numRegs
+                       : -1;
+        }();
+        if (regs != tce::kRegLaunch) return cudaErrorInvalidKernelImage;
+    }
     const int64_t tiles = (J.n + tce::TT - 1) / tce::TT;
     const int grid = (int)(tiles < cx.num_sms ? tiles : cx.num_sms);
     Jl.counters = cx.counters_dev;

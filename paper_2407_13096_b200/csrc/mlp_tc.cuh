@@ -65,8 +65,10 @@ constexpr int kEpi1Batch = DSO_EPI1_BATCH;  // layer-1 epilogue chunks per TMEM 
 // Registers (setmaxnreg): launched at 128 per thread; the MMA warpgroup (the MMA
 // warp and three idle warps) releases down to 56, producers grow to 168 and the
 // epilogue groups to 144 (128*168 + 256*144 + 128*56 = 64K).
+constexpr int kRegLaunch = 128;  // ptxas allocation at launch (checked by launch_tc)
 constexpr int kRegProd = 168, kRegEpi = 144, kRegMma = 56;
-static_assert(128 * kRegProd + 256 * kRegEpi + 128 * kRegMma <= 65536, "RF budget");
+static_assert(128 * (kRegLaunch - kRegMma) >= 128 * (kRegProd - kRegLaunch) + 256 * (kRegEpi - kRegLaunch),
+              "setmaxnreg: increases must be covered by releases");
 constexpr int N1 = 112, K1 = 136, N2 = 64, K2 = 104;
 constexpr int H1 = 100, H2 = 50, H3 = 25, H4 = 7;
 // packed model (floats): L1/L2 weights hi/lo in the SWIZZLE_NONE K-major

@@ -5,9 +5,9 @@
 set -u
 TAG=$1; shift
 OUT=gpurun_out/$TAG; mkdir -p $OUT
-( timeout 900 python -m pytest "$@" -q -m gpu --timeout 600 -rf -x -s > $OUT/pytest.log 2>&1; echo "rc=$?" >> $OUT/pytest.log )
-( timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu --no-e2e --no-extra > $OUT/bench.log 2>&1; echo "rc=$?" >> $OUT/bench.log )
-if [ "${PHASE:-0}" = "1" ]; then ( timeout 300 python scripts/tc_phase.py > $OUT/tc_phase.txt 2>&1 ); fi
+( timeout -s KILL 420 python -m pytest "$@" -q -m gpu --timeout 120 -rf -x -s > $OUT/pytest.log 2>&1; echo "rc=$?" >> $OUT/pytest.log )
+( timeout -s KILL 300 python bench.py --steps 10 --warmup 3 --no-cpu --no-e2e --no-extra > $OUT/bench.log 2>&1; echo "rc=$?" >> $OUT/bench.log )
+if [ "${PHASE:-0}" = "1" ]; then ( timeout -s KILL 200 python scripts/tc_phase.py > $OUT/tc_phase.txt 2>&1 ); fi
 tail -3 $OUT/pytest.log
 python - <<'PY' "$OUT/bench.log"
 import json, sys
