@@ -534,10 +534,12 @@ def measure_train(ctx, args, rank, world, tm, peak, steps, warmup, model):
             "samples_per_gpu": n, "batch_per_gpu": B, "global_batch": B * world,
             "parallelism": f"dp{world} (%s allreduce)" % ("NCCL" if world > 1 else "no"),
             "gpu_launches": launches,
-            "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak["ffma2"],
-                         "frac": achieved / peak["ffma2"], "unit": "TFLOP/s",
-                         "step_view": {"achieved": step_tflops, "frac": step_tflops / peak["ffma2"],
-                                       "note": "whole step incl. update and allreduce"},
+            "roofline": {"bound": "fp32", "achieved": step_tflops, "peak": peak["ffma2"],
+                         "frac": step_tflops / peak["ffma2"], "unit": "TFLOP/s",
+                         "note": "whole step (gradient kernels, allreduce when N > 1, update)",
+                         "grad_call_view": {"achieved": achieved, "frac": achieved / peak["ffma2"],
+                                            "note": "dso_train_grad alone, back-to-back calls "
+                                                    "(includes per-call host overhead)"},
                          "traffic": ncu_traffic("c5", B),
                          "traffic_unit": "bytes per dso_train_grad (ncu, profiles/ncu_summary.json)",
                          "kernel": "dso_train_grad kernels (step: dso_train_step)", "flops_per_sample": TRAIN_FLOPS,

@@ -98,6 +98,9 @@ struct ModelDev {
     // repacked on the device (the kernels read the flag)
     float* wtc;
     int tc_state;
+    // wt / wtc are rebuilt from w_master lazily: a training update only marks
+    // them stale, the next inference launch repacks (launch_ws)
+    bool infer_dirty = false;
     int64_t n_weights, n_biases;
 };
 

@@ -1248,6 +1248,11 @@ bool tc_eligible(const Ctx& cx, const Job& J) {
 template <int MODE>
 cudaError_t launch_ws(Ctx& cx, const Job& J0) {
     constexpr bool PIPE = MODE != MODE_PRED;
+    if (cx.model.infer_dirty) {  // weights updated by training since the last pack
+        cudaError_t e = launch_repack(cx);
+        if (e != cudaSuccess) return e;
+        cx.model.infer_dirty = false;
+    }
     Job J = J0;
     if (tc_eligible<MODE>(cx, J)) {
         cudaError_t e = launch_tc<MODE>(cx, J);
@@ -1370,6 +1375,7 @@ cudaError_t model_upload(Ctx& cx, const double* W, const double* b) {
         if (e != cudaSuccess) return e;
     }
     md.tc_state = bad ? 0 : 1;
+    md.infer_dirty = false;  // packed from the host copy just uploaded
     return cudaMemcpyAsync(md.wtc, tp.data(), sizeof(float) * tce::kModel, cudaMemcpyHostToDevice,
                            cx.stream);
 }

@@ -648,6 +648,41 @@ __global__ void sgd_apply(float* __restrict__ master, const float* __restrict__ 
     if (e < kMasterFloats) master[e] = fmaf(-s, grad[e], master[e]);
 }
 
+// sgd_apply that also writes the updated weight into the training kernel's
+// image (the positions train_pack_kernel uses), so the next gradient needs no
+// repack; the image's zero padding is never touched.
+__global__ void sgd_apply_pack(float* __restrict__ master, const float* __restrict__ grad,
+                               float s, float* __restrict__ img) {
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= kMasterFloats) return;
+    const float w = fmaf(-s, grad[e], master[e]);
+    master[e] = w;
+    if (e < MW2) {
+        const int n = e / 134, k = e - n * 134;
+        img[W1S + (k * 16 + n / 7) * 8 + n % 7] = w;
+    } else if (e < MW3) {
+        const int i = e - MW2, n = i / 100, k = i - n * 100;
+        img[W2S + (k * 8 + n / 7) * 8 + n % 7] = w;
+        img[T2S + (n * 8 + k / 13) * 16 + k % 13] = w;
+    } else if (e < MW4) {
+        const int i = e - MW3, n = i / 50, k = i - n * 50;
+        img[W3S + (k * 8 + n / 4) * 4 + n % 4] = w;
+        img[T3S + (n * 8 + k / 7) * 8 + k % 7] = w;
+    } else if (e < MB1) {
+        const int i = e - MW4, n = i / 25, k = i - n * 25;
+        img[W4S + k * 8 + n] = w;
+        img[T4S + (n * 8 + k / 4) * 4 + k % 4] = w;
+    } else if (e < MB2) {
+        img[B1S + (e - MB1)] = w;
+    } else if (e < MB3) {
+        img[B2S + (e - MB2)] = w;
+    } else if (e < MB4) {
+        img[B3S + (e - MB3)] = w;
+    } else {
+        img[B4S + (e - MB4)] = w;
+    }
+}
+
 }  // namespace
 
 cudaError_t train_prepare(Ctx& cx, int64_t n) {
@@ -751,13 +786,21 @@ cudaError_t launch_train_grad(Ctx& cx, const float* x, const float* y, int64_t n
 
 cudaError_t launch_train_apply(Ctx& cx, const float* grad, float lr_scale, bool repack) {
     if (cx.model.generic) return launch_gen_apply(cx, grad, lr_scale);
-    cx.model.train_dirty = true;
-    sgd_apply<<<(kMasterFloats + 255) / 256, 256, 0, cx.stream>>>(cx.model.w_master, grad,
-                                                                  lr_scale);
+    if (cx.model.w_train && !cx.model.train_dirty) {
+        // update master and the training image together (no repack before the
+        // next gradient)
+        sgd_apply_pack<<<(kMasterFloats + 255) / 256, 256, 0, cx.stream>>>(
+            cx.model.w_master, grad, lr_scale, cx.model.w_train);
+    } else {
+        cx.model.train_dirty = true;
+        sgd_apply<<<(kMasterFloats + 255) / 256, 256, 0, cx.stream>>>(cx.model.w_master, grad,
+                                                                      lr_scale);
+    }
     ++cx.launches;
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess || !repack) return e;
-    return launch_repack(cx);  // inference kernels see the updated weights
+    cx.model.infer_dirty = true;  // the next inference launch repacks (launch_ws)
+    return cudaSuccess;
 }
 
 }  // namespace dso_b200
