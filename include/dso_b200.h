@@ -86,7 +86,9 @@ int32_t dso_get_counters(dso_ctx* ctx, uint64_t* out, int32_t n, int32_t reset);
 /* Tuning / verification switches (no reference counterpart; results never
  * depend on them).  key "fast_sweep": 1 (default) lets the FP32 sweeps use the
  * group-minimum argmin (bit-identical, see sweep_core.cuh), 0 forces the
- * pair-by-pair lexicographic scan.  key "mlp_engine": the predictor engine of
+ * pair-by-pair lexicographic scan.  key "train_tc": 1 (default) computes the
+ * training weight gradients on the tensor cores (3xTF32, tcgen05), 0 on the
+ * FMA pipe.  key "mlp_engine": the predictor engine of
  * dso_predict / dso_pipeline / dso_pipeline_csr: 0 = FP32 FMA-pipe kernel,
  * 1 = tcgen05 3xTF32 tensor-core kernel, 2 = auto (default: tensor cores for
  * predict and CSR input, FMA pipe for dense counts).  Unknown key or value ->

@@ -280,6 +280,10 @@ int32_t dso_set_option(dso_ctx* ctx, const char* key, int64_t value) {
         ctx->c.fast_sweep = value != 0;
         return kOk;
     }
+    if (std::string(key) == "train_tc") {
+        ctx->c.train_tc = value != 0;
+        return kOk;
+    }
     return fail(ctx, kInvalidArgument, std::string("unknown option: ") + key);
 }
 

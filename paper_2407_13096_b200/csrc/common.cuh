@@ -134,6 +134,7 @@ struct Ctx {
     cudaEvent_t ev[8] = {};
     int num_sms = 148;
     bool fast_sweep = true;         // dso_set_option("fast_sweep")
+    bool train_tc = true;           // dso_set_option("train_tc"): weight gradients on tcgen05
     int mlp_engine = 2;             // dso_set_option("mlp_engine"): 0 FMA pipe, 1 tensor cores,
                                     // 2 auto (tensor cores for predict / CSR, FMA pipe for dense)
     float2* eta_dev = nullptr;      // dso_eta_sweep's (eta, K) table

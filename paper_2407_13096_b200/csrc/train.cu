@@ -23,6 +23,7 @@
 #include <algorithm>
 
 #include "common.cuh"
+#include "tc.cuh"
 
 namespace dso_b200 {
 
@@ -623,6 +624,247 @@ __global__ void __launch_bounds__(WG_THREADS, 1)
 }
 
 // Sum the per-CTA partials in CTA order (deterministic), in double.
+// ---------------------------------------------------------------------------
+// Weight gradients on the 5th-generation tensor cores (train_wgrad_tc_kernel).
+// Per CTA a contiguous range of samples (split-K, partials reduced by
+// reduce_partials as for train_wgrad_kernel).  For layer l the contraction over
+// samples  gW_l[n][k] = sum_s delta_l[n][s] a_{l-1}[k][s]  is one MMA chain
+// D_l[M=128 x N_l] += A[128 x 16] . B[N_l x 16]^T per stage of 16 samples, with
+// A = the deltas (rows = output neurons, zero-padded to 128) and B = the layer's
+// inputs (rows = input features, zero-padded to N_l = 144 / 112 / 64 / 32, plus
+// one row of ones whose column gives the bias gradient sum_s delta_l[n][s]).
+// 3xTF32 (hi.hi + hi.lo + lo.hi, FP32 accumulation in TMEM: 352 columns) keeps
+// the FP32 result.  Eight loader warps read a stage's 491 operand rows from the
+// scratch rows train_fb_kernel wrote (and x), split them hi/lo into the SWIZZLE_NONE
+// K-major core-matrix layout (two stage buffers), one thread issues the MMAs,
+// and four warps read the accumulators out at the end.
+namespace twg {
+constexpr int KS = 16;                      // samples per stage
+constexpr int kLoadWarps = 16, kThreadsWG = (kLoadWarps + 1) * 32;
+__host__ __device__ constexpr int NOUT(int l) { return l == 0 ? 100 : l == 1 ? 50 : l == 2 ? 25 : 7; }
+__host__ __device__ constexpr int NIN(int l) { return l == 0 ? 134 : l == 1 ? 100 : l == 2 ? 50 : 25; }
+// MMA N per layer (multiple of 16, > NIN for the ones row) and D's TMEM column
+__host__ __device__ constexpr int NPAD(int l) { return l == 0 ? 144 : l == 1 ? 112 : l == 2 ? 64 : 32; }
+__host__ __device__ constexpr int TCOL(int l) { return l == 0 ? 0 : l == 1 ? 144 : l == 2 ? 256 : 320; }
+// stage layout (floats): A_l [128][KS] at 2048 l, then B_1..B_4; hi part, then lo part
+constexpr int AOFF = 0, BOFF = 4 * 128 * KS;
+__host__ __device__ constexpr int BREG(int l) { return BOFF + TCOL(l) * KS; }
+constexpr int HALF = BOFF + 352 * KS;         // floats of one hi (or lo) part
+constexpr int STAGE = 2 * HALF;               // hi + lo
+constexpr int SMEM_FLOATS = 2 * STAGE + 16;   // two stages + barriers
+constexpr int ROWS = 491;                     // operand rows loaded per stage
+constexpr int ITEMS = ROWS * (KS / 4);        // float4 items per stage
+constexpr int PER_T = (ITEMS + kLoadWarps * 32 - 1) / (kLoadWarps * 32);
+// master offsets of layer l's weights / biases
+__host__ __device__ constexpr int MWL(int l) { return l == 0 ? MW1 : l == 1 ? MW2 : l == 2 ? MW3 : MW4; }
+__host__ __device__ constexpr int MBL(int l) { return l == 0 ? MB1 : l == 1 ? MB2 : l == 2 ? MB3 : MB4; }
+
+// element (r, k) of an [R][KS] K-major core-matrix operand
+__host__ __device__ constexpr int cm_off(int r, int k) {
+    return ((r >> 3) * (KS / 4) + (k >> 2)) * 32 + (r & 7) * 4 + (k & 3);
+}
+// operand row r (0..490) of a stage -> (smem float offset of its row in the hi part,
+// global source row, from x?)
+__device__ __forceinline__ void row_map(int r, int& base, int& src, bool& from_x) {
+    from_x = false;
+    if (r < 134) { base = BREG(0) + cm_off(r, 0); src = r; from_x = true; return; }
+    r -= 134;
+    if (r < 100) { base = AOFF + 0 * 128 * KS + cm_off(r, 0); src = SD1 + r; return; }
+    r -= 100;
+    if (r < 100) { base = BREG(1) + cm_off(r, 0); src = SA1 + r; return; }
+    r -= 100;
+    if (r < 50) { base = AOFF + 1 * 128 * KS + cm_off(r, 0); src = SD2 + r; return; }
+    r -= 50;
+    if (r < 50) { base = BREG(2) + cm_off(r, 0); src = SA2 + r; return; }
+    r -= 50;
+    if (r < 25) { base = AOFF + 2 * 128 * KS + cm_off(r, 0); src = SD3 + r; return; }
+    r -= 25;
+    if (r < 25) { base = BREG(3) + cm_off(r, 0); src = SA3 + r; return; }
+    r -= 25;
+    base = AOFF + 3 * 128 * KS + cm_off(r, 0);  // r < 7
+    src = SD4 + r;
+}
+__device__ __forceinline__ void mb_init(uint64_t* b, int count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(tc::smem_addr(b)), "r"(count)
+                 : "memory");
+}
+__device__ __forceinline__ void mb_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(tc::smem_addr(b))
+                 : "memory");
+}
+__device__ __forceinline__ void mb_wait(uint64_t* b, uint32_t parity) {
+    uint32_t done = 0;
+    while (!done)
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3; selp.u32 %0, 1, 0, p; }"
+            : "=r"(done)
+            : "r"(tc::smem_addr(b)), "r"(parity), "r"(100000u)
+            : "memory");
+}
+}  // namespace twg
+
+__global__ void __launch_bounds__(twg::kThreadsWG, 1)
+    train_wgrad_tc_kernel(const float* __restrict__ x, int64_t ld, const float* __restrict__ act,
+                          int64_t lds, int64_t n, int64_t per, float* __restrict__ partial) {
+    using namespace twg;
+    extern __shared__ __align__(16) float sm[];
+    uint64_t* mb = reinterpret_cast<uint64_t*>(sm + 2 * STAGE);  // FULL[2] EMPTY[2] DONE
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(sm + 2 * STAGE + 10);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int64_t s_lo = (int64_t)blockIdx.x * per, s_hi = min(n, s_lo + per);
+    const int stages = s_hi > s_lo ? (int)((s_hi - s_lo + KS - 1) / KS) : 0;
+    // zero both stages (padding rows stay zero), then the ones rows (bias columns)
+    for (int i = tid; i < 2 * STAGE / 4; i += kThreadsWG)
+        reinterpret_cast<float4*>(sm)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    __syncthreads();
+    for (int i = tid; i < 2 * 4 * KS; i += kThreadsWG) {
+        const int st = i / (4 * KS), l = (i / KS) & 3, k = i % KS;
+        sm[st * STAGE + BREG(l) + cm_off(NIN(l), k)] = 1.0f;  // hi = 1, lo = 0
+    }
+    if (tid == 0) {
+        for (int i = 0; i < 2; ++i) {
+            mb_init(mb + i, kLoadWarps);      // FULL
+            mb_init(mb + 2 + i, 1);           // EMPTY (MMA commit)
+        }
+        mb_init(mb + 4, 1);                   // DONE
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == kLoadWarps) tc::tmem_alloc<512>(tslot);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t tbase = *tslot;
+
+    if (warp < kLoadWarps) {
+        // ---- loaders: each thread's float4 items (row, sample quad) are fixed ----
+        const bool vec = ((ld | lds) & 3) == 0 && ((reinterpret_cast<uintptr_t>(x) |
+                                                    reinterpret_cast<uintptr_t>(act)) & 15) == 0 &&
+                         (s_lo & 3) == 0;
+        int soff[PER_T];
+        const float* gsrc[PER_T];
+        int qd[PER_T];
+#pragma unroll
+        for (int i = 0; i < PER_T; ++i) {
+            const int it = tid + i * kLoadWarps * 32;
+            const int r = it < ITEMS ? it / (KS / 4) : 0;
+            qd[i] = it < ITEMS ? it % (KS / 4) : -1;
+            int base, src;
+            bool fx;
+            row_map(r, base, src, fx);
+            soff[i] = base + qd[i] * 32;  // sample quad q: core matrix k4 = q
+            gsrc[i] = fx ? x + (int64_t)src * ld : act + (int64_t)src * lds;
+        }
+        // a stage's loads are issued one stage ahead (registers), so their latency
+        // overlaps the current stage's split / store and the wait for its buffer
+        auto load = [&](int it, float4 (&v)[PER_T]) {
+            const int64_t s0 = s_lo + (int64_t)it * KS;
+#pragma unroll
+            for (int i = 0; i < PER_T; ++i) {
+                v[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (qd[i] < 0) continue;
+                const int64_t s = s0 + 4 * qd[i];
+                if (vec && s + 3 < s_hi) {
+                    v[i] = __ldg(reinterpret_cast<const float4*>(gsrc[i] + s));
+                } else {
+                    v[i].x = s < s_hi ? __ldg(gsrc[i] + s) : 0.f;
+                    v[i].y = s + 1 < s_hi ? __ldg(gsrc[i] + s + 1) : 0.f;
+                    v[i].z = s + 2 < s_hi ? __ldg(gsrc[i] + s + 2) : 0.f;
+                    v[i].w = s + 3 < s_hi ? __ldg(gsrc[i] + s + 3) : 0.f;
+                }
+            }
+        };
+        float4 nxt[PER_T];
+        if (stages > 0) load(0, nxt);
+        for (int it = 0; it < stages; ++it) {
+            const int b = it & 1;
+            float4 cur[PER_T];
+#pragma unroll
+            for (int i = 0; i < PER_T; ++i) cur[i] = nxt[i];
+            if (it + 1 < stages) load(it + 1, nxt);
+            if (it >= 2) mb_wait(mb + 2 + b, (uint32_t)(((it >> 1) - 1) & 1));
+            float* hi = sm + b * STAGE;
+            float* lo = hi + HALF;
+#pragma unroll
+            for (int i = 0; i < PER_T; ++i) {
+                if (qd[i] < 0) continue;
+                const float4 v = cur[i];
+                const float4 h = make_float4(tc::tf32_hi_finite(v.x), tc::tf32_hi_finite(v.y),
+                                             tc::tf32_hi_finite(v.z), tc::tf32_hi_finite(v.w));
+                *reinterpret_cast<float4*>(hi + soff[i]) = h;
+                *reinterpret_cast<float4*>(lo + soff[i]) =
+                    make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mb_arrive(mb + b);
+        }
+    } else if (lane == 0) {
+        // ---- MMA issuer ----------------------------------------------------------
+        const uint32_t s0 = tc::smem_addr(sm);
+        for (int it = 0; it < stages; ++it) {
+            const int b = it & 1;
+            mb_wait(mb + b, (uint32_t)((it >> 1) & 1));
+            tc::fence_after();
+            const uint32_t hi = s0 + (uint32_t)(b * STAGE) * 4, lo = hi + HALF * 4;
+#pragma unroll
+            for (int l = 0; l < 4; ++l) {
+                const uint32_t id = tc::idesc_tf32(128, NPAD(l));
+                const uint32_t d = tbase + (uint32_t)TCOL(l);
+#pragma unroll
+                for (int kk = 0; kk < KS / 8; ++kk) {
+                    const uint32_t ao = (uint32_t)(AOFF + l * 128 * KS) * 4 + kk * 256,
+                                   bo = (uint32_t)BREG(l) * 4 + kk * 256;
+                    const uint64_t ah = tc::sdesc(hi + ao, 128, (KS / 4) * 128),
+                                   al = tc::sdesc(lo + ao, 128, (KS / 4) * 128),
+                                   bh = tc::sdesc(hi + bo, 128, (KS / 4) * 128),
+                                   bl = tc::sdesc(lo + bo, 128, (KS / 4) * 128);
+                    tc::mma_tf32_ss(d, ah, bh, id, (it > 0 || kk > 0) ? 1u : 0u);
+                    tc::mma_tf32_ss(d, ah, bl, id, 1u);
+                    tc::mma_tf32_ss(d, al, bh, id, 1u);
+                }
+            }
+            tc::commit(mb + 2 + b);
+        }
+        tc::commit(mb + 4);
+    }
+    __syncwarp();
+    // ---- accumulators -> this CTA's partial gradient (master layout) ------------
+    if (warp < 4) {
+        float* out = partial + (int64_t)blockIdx.x * kMasterFloats;
+        const int row = 32 * warp + lane;  // output neuron
+        if (stages > 0) {
+            mb_wait(mb + 4, 0);
+            tc::fence_after();
+        }
+#pragma unroll 1
+        for (int l = 0; l < 4; ++l) {
+            for (int c0 = 0; c0 < NPAD(l); c0 += 8) {
+                float v[8];
+                if (stages > 0) {
+                    tc::ld8(tbase + ((uint32_t)(32 * warp) << 16) + (uint32_t)(TCOL(l) + c0), v);
+                    tc::wait_ld();
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) v[j] = 0.f;
+                }
+                if (row < NOUT(l)) {
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        const int k = c0 + j;
+                        if (k < NIN(l)) out[MWL(l) + row * NIN(l) + k] = v[j];
+                        else if (k == NIN(l)) out[MBL(l) + row] = v[j];
+                    }
+                }
+            }
+        }
+    }
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    if (warp == kLoadWarps) tc::tmem_dealloc<512>(tbase);
+}
+
 __global__ void reduce_partials(const float* __restrict__ partial, int parts,
                                 const double* __restrict__ loss_partial, int loss_parts,
                                 float* __restrict__ grad, double* __restrict__ loss_sum) {
@@ -775,8 +1017,16 @@ cudaError_t launch_train_grad(Ctx& cx, const float* x, const float* y, int64_t n
     int64_t per = (n + wg_parts - 1) / wg_parts;
     per = ((per + WG_CHUNK - 1) / WG_CHUNK) * WG_CHUNK;
     if (per == 0) per = WG_CHUNK;
-    train_wgrad_kernel<<<wg_parts, WG_THREADS, smem_wg, cx.stream>>>(x, ld, act, lds, n, per,
-                                                                     partial);
+    if (cx.train_tc) {
+        const size_t smem_tc = (size_t)twg::SMEM_FLOATS * sizeof(float);
+        cudaError_t e = ensure_smem_attr((const void*)train_wgrad_tc_kernel, cx.device, (int)smem_tc);
+        if (e != cudaSuccess) return e;
+        train_wgrad_tc_kernel<<<wg_parts, twg::kThreadsWG, smem_tc, cx.stream>>>(x, ld, act, lds, n,
+                                                                             per, partial);
+    } else {
+        train_wgrad_kernel<<<wg_parts, WG_THREADS, smem_wg, cx.stream>>>(x, ld, act, lds, n, per,
+                                                                         partial);
+    }
     reduce_partials<<<(kMasterFloats * 8 + 255) / 256, 256, 0, cx.stream>>>(partial, wg_parts, lp,
                                                                         fb_parts, grad,
                                                                         loss_sum_dev);
