@@ -463,102 +463,75 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     if ((warp >> 2) == MMA_WG) {
         asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegMma));
     }
-    if (warp == MMA_WARP) {
-        // ================================ MMA issuer ================================
+    if (warp == MMA_WARP || warp == MMA_WARP + 1) {
+        // ============================== MMA issuers ===============================
+        // Two threads in two warps (two SMSPs), each sleeping in the mbarrier of its
+        // own next event, no polling: warp MMA_WARP issues layer 1 (chunk by chunk
+        // as the producers hand them over), warp MMA_WARP + 1 layer 2 (chunk by
+        // chunk as the epilogue group stores A2).  Tile t's layer 1 reuses the TMEM
+        // slot of tile t-2, so it starts once layer 2 of tile t-2 has completed
+        // (its commit barrier MB_D2F): no ordering between the two issuers' MMAs
+        // is assumed.
         if (lane == 0) {
             const uint32_t id1 = tc::idesc_tf32(128, N1), id2 = tc::idesc_tf32(128, N2);
             const uint32_t s0 = smem_u32(sm);
             auto bd = [&](int off, int kk, int K) {
                 return tc::sdesc(s0 + off * 4 + kk * 256, 128, (uint32_t)(K >> 2) * 128);
             };
-            uint32_t g = 0;  // ring chunks consumed
-            unsigned long long n_l1 = 0, n_l2 = 0;  // k-steps issued (evidence counters)
-            // Event-driven issue: L1 of the next tile and L2..L4 of the current one are
-            // independent streams of k-steps; each is issued as soon as its operand
-            // chunk is ready (non-blocking mbarrier tests), in one tensor-core queue.
-            struct L1S {
-                int64_t t;
-                int c;
-                uint32_t mask;
-                bool active;
-            };
-            auto l1_step = [&](L1S& st) -> bool {
-                const int b = (int)(g % kRing);
-                if (!mbar_test(mb + MB_XFULL + b, (g / kRing) & 1u)) return false;
-                tc::fence_after();
-                if (st.c == 0) st.mask = misc[st.t & 1];  // published before the tile's first chunk
-                const uint32_t D = tbase + (uint32_t)((st.t & 1) * SLOT_COLS);
-                const uint32_t xa = s0 + (uint32_t)(S_RING + b * kChunkF) * 4;
-                const uint64_t ah = tc::sdesc(xa, 128, 256), al = tc::sdesc(xa + TT * 8 * 4, 128, 256);
-                tc::mma_tf32_ss(D, ah, bd(W1H, st.c, K1), id1, st.c == 0 ? 0u : 1u);
-                if (st.c == 0) TRACE(0, st.t);
-                tc::mma_tf32_ss(D, ah, bd(W1L, st.c, K1), id1, 1u);
-                tc::mma_tf32_ss(D, al, bd(W1H, st.c, K1), id1, 1u);
-                tc::commit(mb + MB_XEMPTY + b);
-                ++g;
-                ++n_l1;
-                int nc = st.c + 1;
-                while (nc < 17 && !((st.mask >> nc) & 1u)) ++nc;
-                if (nc >= 17) {
-                    tc::commit(mb + MB_D1F + (st.t & 1));
-                    TRACE(1, st.t);
-                    st.active = false;
-                } else {
-                    st.c = nc;
-                }
-                return true;
-            };
-            // One scheduler loop: L1 runs one tile ahead of L2 (tile b + 2 reuses tile
-            // b's slot once L2(b) is issued: the tensor core executes in issue order).
-            L1S st{0, 0, 0u, my_tiles > 0};
-            int64_t b = 0;
-            bool d2ok = true;
-            int c2 = 0;
-            while (b < my_tiles) {
-                if (!st.active && st.t + 1 < my_tiles && st.t + 1 <= b + 1) st = L1S{st.t + 1, 0, 0u, true};
-                bool prog = false;
-                while (st.active && l1_step(st)) prog = true;
-                if (st.t <= b && st.active) {  // L1(b) not fully issued yet
-                    // nothing else can proceed: sleep in the barrier until the next
-                    // chunk is handed over (no issue slots taken from this SMSP)
-                    if (!prog) mbar_try(mb + MB_XFULL + (int)(g % kRing), (g / kRing) & 1u, 20000u);
-                    continue;
-                }
-                const int sl = (int)(b & 1);
-                const uint32_t S = tbase + (uint32_t)(sl * SLOT_COLS);
-                const uint32_t ph = (uint32_t)((b >> 1) & 1);
-                if (!d2ok && mbar_test(mb + MB_D2FREE, (uint32_t)((b - 1) & 1))) d2ok = true;
-                while (d2ok && c2 < 13 && mbar_test(mb + MB_A2R + 13 * sl + c2, ph)) {
-                    tc::fence_after();
-                    tc::mma_tf32_ts(tbase + TD2, S + 8 * c2, bd(W2H, c2, K2), id2, c2 > 0 ? 1u : 0u);
-                    if (c2 == 0) TRACE(2, b);
-                    tc::mma_tf32_ts(tbase + TD2, S + 8 * c2, bd(W2L, c2, K2), id2, 1u);
-                    tc::mma_tf32_ts(tbase + TD2, S + A2LO + 8 * c2, bd(W2H, c2, K2), id2, 1u);
-                    ++n_l2;
-                    prog = true;
-                    if (++c2 == 13) {
-                        tc::commit(mb + MB_D2F + sl);
-                        TRACE(3, b);
-                        ++b;
-                        c2 = 0;
-                        d2ok = false;
-                        break;
+            unsigned long long n_k = 0;  // k-steps issued (evidence counters)
+            if (warp == MMA_WARP) {
+                uint32_t g = 0;  // ring chunks consumed
+                for (int64_t t = 0; t < my_tiles; ++t) {
+                    const int sl = (int)(t & 1);
+                    if (t >= 2) mbar_wait(mb + MB_D2F + sl, (uint32_t)(((t >> 1) - 1) & 1));
+                    const uint32_t D = tbase + (uint32_t)(sl * SLOT_COLS);
+                    uint32_t mask = 0u;
+                    for (int c = 0; c < 17; ++c) {
+                        const int b = (int)(g % kRing);
+                        if (c > 0 && !((mask >> c) & 1u)) continue;
+                        mbar_wait(mb + MB_XFULL + b, (g / kRing) & 1u);
+                        tc::fence_after();
+                        if (c == 0) {
+                            mask = misc[sl];  // published before the tile's first chunk
+                            TRACE(0, t);
+                        }
+                        const uint32_t xa = s0 + (uint32_t)(S_RING + b * kChunkF) * 4;
+                        const uint64_t ah = tc::sdesc(xa, 128, 256),
+                                       al = tc::sdesc(xa + TT * 8 * 4, 128, 256);
+                        tc::mma_tf32_ss(D, ah, bd(W1H, c, K1), id1, c == 0 ? 0u : 1u);
+                        tc::mma_tf32_ss(D, ah, bd(W1L, c, K1), id1, 1u);
+                        tc::mma_tf32_ss(D, al, bd(W1H, c, K1), id1, 1u);
+                        tc::commit(mb + MB_XEMPTY + b);
+                        ++g;
+                        ++n_k;
                     }
+                    tc::commit(mb + MB_D1F + sl);
+                    TRACE(1, t);
                 }
-                if (!prog) {
-                    // sleep in the barrier of the next layer-2 event; briefly when a
-                    // layer-1 chunk of the next tile may arrive first
-                    const uint32_t ns = st.active ? kMmaSleepNs : 20000u;
-                    if (!d2ok)
-                        mbar_try(mb + MB_D2FREE, (uint32_t)((b - 1) & 1), ns);
-                    else if (b < my_tiles)
-                        mbar_try(mb + MB_A2R + 13 * (int)(b & 1) + c2, (uint32_t)((b >> 1) & 1), ns);
+                if (J.counters) {
+                    atomicAdd(J.counters + 0, n_k);
+                    atomicAdd(J.counters + 2, (unsigned long long)my_tiles);
                 }
-            }
-            if (J.counters) {
-                atomicAdd(J.counters + 0, n_l1);
-                atomicAdd(J.counters + 1, n_l2);
-                atomicAdd(J.counters + 2, (unsigned long long)my_tiles);
+            } else {
+                for (int64_t t = 0; t < my_tiles; ++t) {
+                    const int sl = (int)(t & 1);
+                    const uint32_t S = tbase + (uint32_t)(sl * SLOT_COLS);
+                    const uint32_t ph = (uint32_t)((t >> 1) & 1);
+                    // D2 is free once the previous tile's epilogue has read it
+                    if (t >= 1) mbar_wait(mb + MB_D2FREE, (uint32_t)((t - 1) & 1));
+                    for (int c2 = 0; c2 < 13; ++c2) {
+                        mbar_wait(mb + MB_A2R + 13 * sl + c2, ph);
+                        tc::fence_after();
+                        tc::mma_tf32_ts(tbase + TD2, S + 8 * c2, bd(W2H, c2, K2), id2, c2 > 0 ? 1u : 0u);
+                        if (c2 == 0) TRACE(2, t);
+                        tc::mma_tf32_ts(tbase + TD2, S + 8 * c2, bd(W2L, c2, K2), id2, 1u);
+                        tc::mma_tf32_ts(tbase + TD2, S + A2LO + 8 * c2, bd(W2H, c2, K2), id2, 1u);
+                        ++n_k;
+                    }
+                    tc::commit(mb + MB_D2F + sl);
+                    TRACE(3, t);
+                }
+                if (J.counters) atomicAdd(J.counters + 1, n_k);
             }
         }
         __syncwarp();
@@ -706,6 +679,21 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
                 };
                 if (!uns) {
                     if (staged) {
+#ifdef DSO_TC_PA8
+#pragma unroll 1
+                        for (int e0 = 0; e0 < ce; e0 += 8) {
+                            uint32_t en[4], en2[4];
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) {
+                                const uint32_t v = s_row[e0 + u < ce ? e0 + u : 0];
+                                const uint32_t v2 = s_row[e0 + 4 + u < ce ? e0 + 4 + u : 0];
+                                en[u] = e0 + u < ce ? v : 127u;
+                                en2[u] = e0 + 4 + u < ce ? v2 : 127u;
+                            }
+                            group(en, e0);
+                            group(en2, e0 + 4);
+                        }
+#else
 #pragma unroll 1
                         for (int e0 = 0; e0 < ce; e0 += 4) {
                             uint32_t en[4];
@@ -716,6 +704,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
                             }
                             group(en, e0);
                         }
+#endif
                     } else {
                         const uint32_t* gp = J.entries + E.first;
 #pragma unroll 1
@@ -876,13 +865,17 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
                 const bool w64 = __any_sync(0xffffffffu, E.cnt > 32);
                 // pass B, branch-free: positions beyond n_c read a valid word (position 0)
                 // and their stores are predicated off
+#ifndef DSO_TC_PBW
+#define DSO_TC_PBW 4
+#endif
                 auto take = [&](auto stg, auto wide, uint64_t& rem, int n_c, int nmax, uint32_t bufa) {
+                    constexpr int WD = DSO_TC_PBW;  // entries per step
 #pragma unroll 1
-                    for (int i0 = 0; i0 < nmax; i0 += 4) {
-                        uint32_t en[4];
-                        bool on[4];
+                    for (int i0 = 0; i0 < nmax; i0 += WD) {
+                        uint32_t en[WD];
+                        bool on[WD];
 #pragma unroll
-                        for (int u = 0; u < 4; ++u) {
+                        for (int u = 0; u < WD; ++u) {
                             on[u] = i0 + u < n_c;
                             int e;
                             if constexpr (decltype(wide)::value) {
@@ -901,7 +894,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
                                 en[u] = __ldg(J.entries + g_first + e);
                         }
 #pragma unroll
-                        for (int u = 0; u < 4; ++u) {
+                        for (int u = 0; u < WD; ++u) {
                             const int slot = (int)(en[u] & 127u);
                             float t = tf0, r = rr0;
                             t = slot >= DSO_INSTR_SLOTS ? tf1 : t;
