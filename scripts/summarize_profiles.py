@@ -138,14 +138,15 @@ if os.path.exists(lc):
         for k, (c, t) in sorted(agg.items(), key=lambda x: -x[1][1]):
             f.write(f"{c}\t{t / 1e6:.3f}\t{k}\n")
     shutil.copy(lc, os.path.join(dst, "launches.csv"))
-for name in ("bench", "bench_c2", "bench_c4", "bench_c5", "bench_ffma", "bench_dense"):
+for name in ("bench", "bench_ref", "bench_c2", "bench_c4", "bench_c5", "bench_ffma", "bench_dense"):
     p = os.path.join(src, name + ".log")
     if os.path.exists(p):
-        line = open(p).readline().strip()
-        if line.startswith("{"):
-            open(os.path.join(dst, name + ".json"), "w").write(line + "\n")
-for extra in ("pytest_gpu.log", "memcheck.log", "smoke.log", "nvidia-smi.txt", "tc_phase.txt",
-              "phase_timing.txt"):
+        for line in open(p):
+            if line.startswith("{"):
+                open(os.path.join(dst, name + ".json"), "w").write(line.strip() + "\n")
+                break
+for extra in ("pytest_gpu.log", "memcheck.log", "racecheck.log", "synccheck.log", "smoke.log",
+              "nvidia-smi.txt", "nproc.txt", "tc_phase.txt", "phase_timing.txt"):
     p = os.path.join(src, extra)
     if os.path.exists(p):
         shutil.copy(p, os.path.join(dst, extra))
