@@ -455,14 +455,17 @@ __device__ __forceinline__ bool issue_tile_loads(float* act, uint64_t* mbar,
     return true;
 }
 
+// Blocks in mbarrier.try_wait until the phase with the given parity completes; the
+// explicit suspend-time hint (an upper bound: the thread resumes at completion)
+// keeps a waiting warp from re-issuing the test every few hundred cycles.
 __device__ __forceinline__ void mbar_wait(uint64_t* mbar, uint32_t parity) {
     const uint32_t bar = smem_u32(mbar);
     uint32_t done = 0;
     while (!done) {
         asm volatile(
-            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3; selp.u32 %0, 1, 0, p; }"
             : "=r"(done)
-            : "r"(bar), "r"(parity)
+            : "r"(bar), "r"(parity), "r"(1000000u)
             : "memory");
     }
 }
