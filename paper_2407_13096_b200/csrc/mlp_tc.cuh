@@ -58,6 +58,9 @@ constexpr int MMA_WARP = 4 * MMA_WG;
 #define DSO_MMA_SLEEP_NS 256
 #endif
 constexpr unsigned kMmaSleepNs = DSO_MMA_SLEEP_NS;  // MMA issuer: barrier sleep while two event streams are open
+#ifndef DSO_TC_SWEEP_UNR
+#define DSO_TC_SWEEP_UNR 4  // independent sweep groups per step in the epilogue
+#endif
 #ifndef DSO_EPI1_BATCH
 #define DSO_EPI1_BATCH 4
 #endif
@@ -1036,7 +1039,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
 #ifdef DSO_TCV_NOSWEEP
             const Best r{P.pr[0], P.pr[1], (int)(P.pr[2] > 1.f)};
 #else
-            const Best r = sweep_dispatch<4>(p, s_core, s_mem, s_pair, J, 0, J.nc);
+            const Best r = sweep_dispatch<DSO_TC_SWEEP_UNR>(p, s_core, s_mem, s_pair, J, 0, J.nc);
 #endif
 #pragma unroll
             for (int d = 0; d < 4; ++d) write_result(J, P.k, d, r, P.cl, P.pr, p, s_core, s_mem);
