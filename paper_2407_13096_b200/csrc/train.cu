@@ -21,6 +21,7 @@
 #include <math.h>
 
 #include <algorithm>
+#include <type_traits>
 
 #include "common.cuh"
 #include "tc.cuh"
@@ -774,14 +775,11 @@ __global__ void __launch_bounds__(twg::kThreadsWG, 1)
                 }
             }
         };
-        float4 nxt[PER_T];
-        if (stages > 0) load(0, nxt);
-        for (int it = 0; it < stages; ++it) {
+        // stage `it` of the split / store; its loads were issued two stages earlier into
+        // the register set of its parity (fixed registers per parity: a rotation through
+        // moves would wait on the newest loads at every step)
+        auto store = [&](int it, const float4 (&cur)[PER_T]) {
             const int b = it & 1;
-            float4 cur[PER_T];
-#pragma unroll
-            for (int i = 0; i < PER_T; ++i) cur[i] = nxt[i];
-            if (it + 1 < stages) load(it + 1, nxt);
             if (it >= 2) mb_wait(mb + 2 + b, (uint32_t)(((it >> 1) - 1) & 1));
             float* hi = sm + b * STAGE;
             float* lo = hi + HALF;
@@ -798,6 +796,17 @@ __global__ void __launch_bounds__(twg::kThreadsWG, 1)
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __syncwarp();
             if (lane == 0) mb_arrive(mb + b);
+        };
+        float4 va[PER_T], vb[PER_T];
+        if (stages > 0) load(0, va);
+        if (stages > 1) load(1, vb);
+        for (int it = 0; it < stages; it += 2) {
+            store(it, va);
+            if (it + 2 < stages) load(it + 2, va);
+            if (it + 1 < stages) {
+                store(it + 1, vb);
+                if (it + 3 < stages) load(it + 3, vb);
+            }
         }
     } else if (lane == 0) {
         // ---- MMA issuer ----------------------------------------------------------
@@ -830,6 +839,9 @@ __global__ void __launch_bounds__(twg::kThreadsWG, 1)
     }
     __syncwarp();
     // ---- accumulators -> this CTA's partial gradient (master layout) ------------
+    // per layer: TMEM (lane = output neuron) -> a [128][NPAD + 1] transpose buffer in the
+    // now idle stage memory -> global in master order (row-major W[n][k], then the
+    // biases), consecutive threads on consecutive addresses
     if (warp < 4) {
         float* out = partial + (int64_t)blockIdx.x * kMasterFloats;
         const int row = 32 * warp + lane;  // output neuron
@@ -837,8 +849,10 @@ __global__ void __launch_bounds__(twg::kThreadsWG, 1)
             mb_wait(mb + 4, 0);
             tc::fence_after();
         }
-#pragma unroll 1
-        for (int l = 0; l < 4; ++l) {
+        float* tr = sm;
+        auto layer = [&](auto lc) {
+            constexpr int l = decltype(lc)::value;
+            constexpr int P = NPAD(l) + 1, NI = NIN(l), NO = NOUT(l);
             for (int c0 = 0; c0 < NPAD(l); c0 += 8) {
                 float v[8];
                 if (stages > 0) {
@@ -848,16 +862,18 @@ __global__ void __launch_bounds__(twg::kThreadsWG, 1)
 #pragma unroll
                     for (int j = 0; j < 8; ++j) v[j] = 0.f;
                 }
-                if (row < NOUT(l)) {
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                        const int k = c0 + j;
-                        if (k < NIN(l)) out[MWL(l) + row * NIN(l) + k] = v[j];
-                        else if (k == NIN(l)) out[MBL(l) + row] = v[j];
-                    }
-                }
+                for (int j = 0; j < 8; ++j) tr[row * P + c0 + j] = v[j];
             }
-        }
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            for (int j = row; j < NO * NI; j += 128) out[MWL(l) + j] = tr[(j / NI) * P + j % NI];
+            for (int n = row; n < NO; n += 128) out[MBL(l) + n] = tr[n * P + NI];
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+        };
+        layer(std::integral_constant<int, 0>{});
+        layer(std::integral_constant<int, 1>{});
+        layer(std::integral_constant<int, 2>{});
+        layer(std::integral_constant<int, 3>{});
     }
     tc::fence_before();
     __syncthreads();
