@@ -205,6 +205,7 @@ int32_t dso_ctx_destroy(dso_ctx* ctx) {
     cudaFree(c.dp_grad);
     cudaFree(c.dp_dbl);
     cudaFree(c.gen_scratch);
+    cudaFree(c.dcsr_scratch);
     cudaFree(c.model.gstats);
     for (auto& s : c.aux)
         if (s) cudaStreamDestroy(s);
@@ -278,6 +279,10 @@ int32_t dso_set_option(dso_ctx* ctx, const char* key, int64_t value) {
     }
     if (std::string(key) == "fast_sweep") {
         ctx->c.fast_sweep = value != 0;
+        return kOk;
+    }
+    if (std::string(key) == "dense_csr") {
+        ctx->c.dense_csr = value != 0;
         return kOk;
     }
     if (std::string(key) == "train_tc") {
@@ -765,6 +770,14 @@ int32_t dso_pipeline(dso_ctx* ctx, const uint32_t* counts, const float* dcgm, in
     Ctx& c = ctx->c;
     const float K = (float)((1.0 - eta) * pmax);
     if (!(flags & DSO_HOST)) {
+        // auto engine: the dense counts go through the CSR form to the tensor-core pipeline
+        if (c.dense_csr && c.mlp_engine == 2 && tc_csr_eligible(c)) {
+            bool done = false;
+            DSO_CUDA(ctx, launch_pipeline_dense_via_csr(c, counts, dcgm, n, ld, (float)eta, K,
+                                                        params, clamped, idx, cost, energy, time,
+                                                        &done));
+            if (done) return kOk;
+        }
         DSO_CUDA(ctx, launch_pipeline(c, counts, dcgm, n, ld, (float)eta, K, params, clamped,
                                       idx, cost, energy, time, ld));
         return kOk;

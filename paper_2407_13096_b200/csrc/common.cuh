@@ -152,6 +152,10 @@ struct Ctx {
     // the generic-chain pipeline's staging (mlp_gen.cu)
     void* gen_scratch = nullptr;
     size_t gen_scratch_bytes = 0;
+    // dense counts -> CSR for the tensor-core pipeline (dense_csr.cu)
+    bool dense_csr = true;          // dso_set_option("dense_csr")
+    void* dcsr_scratch = nullptr;
+    size_t dcsr_bytes = 0;
 };
 
 }  // namespace dso_b200
@@ -210,6 +214,17 @@ cudaError_t launch_train_apply(Ctx& c, const float* grad, float lr_scale, bool r
 // n samples, without launching: makes the next gradients capturable
 cudaError_t train_prepare(Ctx& c, int64_t n);
 cudaError_t launch_repack(Ctx& c);
+// true when the tensor-core engine would run the CSR pipeline for the context's
+// model and domain (mlp.cu)
+bool tc_csr_eligible(const Ctx& c);
+// dso_pipeline on device buffers through the CSR form (dense_csr.cu): the dense
+// counts are compacted to slot-sorted CSR rows on the device and the tensor-core
+// CSR pipeline runs on them.  *done = false (nothing launched) when a count does
+// not fit the CSR field (>= 2^25).
+cudaError_t launch_pipeline_dense_via_csr(Ctx& c, const uint32_t* counts, const float* dcgm,
+                                          int64_t n, int64_t ld, float eta, float K,
+                                          float* params, uint8_t* clamped, int32_t* idx,
+                                          float* cost, float* energy, float* time, bool* done);
 // generic-chain engine and 64-bit-count features (mlp_gen.cu)
 GenNet gen_net_of(const ModelDev& md);
 cudaError_t launch_gen_forward(Ctx& c, const float* x, int64_t n, int64_t ld, float* raw,

@@ -1446,6 +1446,14 @@ cudaError_t launch_pipeline(Ctx& cx, const uint32_t* counts, const float* dcgm, 
     return launch_ws<MODE_DENSE>(cx, J);
 }
 
+bool tc_csr_eligible(const Ctx& cx) {
+    if (cx.model.generic) return false;
+    Job J{};
+    J.nc = cx.dom.nc;
+    J.nm = cx.dom.nm;
+    return tc_eligible<MODE_CSR>(cx, J);
+}
+
 cudaError_t launch_pipeline_csr(Ctx& cx, const uint64_t* row_ptr, const uint32_t* entries,
                                 uint64_t ent_base, const float* dcgm, int64_t n, int64_t ld,
                                 float eta, float K, float* params, uint8_t* clamped, int32_t* idx,

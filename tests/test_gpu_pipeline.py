@@ -238,6 +238,49 @@ def test_pipeline_csr_long_sorted_rows(ctx, port):
             np.testing.assert_array_equal(a[f].cpu().numpy(), b[f].cpu().numpy())
 
 
+def test_pipeline_dense_via_csr(ctx, port):
+    """Auto engine, dense counts on the device: compacted to CSR and run on the
+    tensor-core CSR pipeline — equal to pipeline_csr on the same kernels bit for bit
+    (synthetic stream with a ragged tail, random rows over all 126 slots); a count
+    >= 2^25 (outside the CSR field) falls back to the dense kernels."""
+    dom = config_domain("c3")
+    ctx.set_domain(dom)
+    ctx.set_model(stats_model(port))
+    ctx.set_option("mlp_engine", 2)
+    try:
+        n = 20_000 + 37
+        d = ctx.gen_synthetic(n, root=43, params=False)
+        s = ctx.gen_synthetic_csr(n, root=43)
+        a = ctx.pipeline(d["counts"], d["dcgm"], 0.8, want_params=True)
+        b = ctx.pipeline_csr(s["row_ptr"], s["entries"], s["dcgm"], 0.8, want_params=True)
+        for f in ("idx", "cost", "energy", "time", "params", "clamped"):
+            np.testing.assert_array_equal(a[f].cpu().numpy(), b[f].cpu().numpy())
+        rng = np.random.default_rng(21)
+        m = 5000 + 3
+        counts = np.zeros((m, 126), np.uint32)
+        for k in range(m):
+            nnz = int(rng.integers(0, 60))
+            counts[k, rng.choice(126, size=nnz, replace=False)] = rng.integers(1, 1 << 20, size=nnz)
+        dcgm = torch.from_numpy(np.ascontiguousarray(rng.uniform(0, 1, (8, m)).astype(np.float32))).cuda()
+        ct = torch.from_numpy(np.ascontiguousarray(counts.T).view(np.int32)).cuda()
+        a = ctx.pipeline(ct, dcgm, 0.5, want_params=True)
+        rp, ent = csr_from_dense(counts)
+        b = ctx.pipeline_csr(torch.from_numpy(rp).cuda(), torch.from_numpy(ent.view(np.int32)).cuda(),
+                             dcgm, 0.5, want_params=True)
+        for f in ("idx", "cost", "energy", "time", "params", "clamped"):
+            np.testing.assert_array_equal(a[f].cpu().numpy(), b[f].cpu().numpy())
+        counts[7, 3] = 1 << 26  # outside the CSR count field
+        ct = torch.from_numpy(np.ascontiguousarray(counts.T).view(np.int32)).cuda()
+        a = ctx.pipeline(ct, dcgm, 0.5, want_params=True)
+        ctx.set_option("dense_csr", 0)
+        b = ctx.pipeline(ct, dcgm, 0.5, want_params=True)
+        for f in ("idx", "cost", "energy", "time", "params", "clamped"):
+            np.testing.assert_array_equal(a[f].cpu().numpy(), b[f].cpu().numpy())
+    finally:
+        ctx.set_option("dense_csr", 1)
+        ctx.set_option("mlp_engine", 2)
+
+
 def test_pipeline_csr_host_large(ctx, port):
     dom = config_domain("c3")
     ctx.set_domain(dom)
