@@ -346,7 +346,9 @@ def measure_pipeline(ctx, name, args, rank, world, tm, peak, steps, warmup, csr=
     else:
         gen = ctx.gen_synthetic(n, root=ROOT_SEED, first=rank * n, params=False)
         dcgm = gen["dcgm"]
-        nnz = DSO_COUNT_ROWS
+        # the algorithmic layer-1 work counts the listed (non-zero) categories, whatever
+        # the input format
+        nnz = float((gen["counts"] != 0).sum().item()) / n
     out = ctx.alloc_pipeline_out(n)
     if csr:
         step = lambda i: ctx.pipeline_csr(gen["row_ptr"], gen["entries"], dcgm, cfg["eta"], out=out)  # noqa: E731
@@ -413,7 +415,8 @@ def measure_pipeline(ctx, name, args, rank, world, tm, peak, steps, warmup, csr=
            "kernels_per_gpu": n, "grid": f"{cfg['nc']}x{cfg['nm']}", "engine": engine,
            "roofline": roofline, "gpu_launches": launches,
            "input": ("sparse per-kernel PTX count lists (%g non-zeros/kernel) + DCGM" % nnz
-                     if csr else "dense [126][n] PTX counts + DCGM")}
+                     if csr else "dense [126][n] PTX counts (%g non-zeros/kernel) + DCGM; auto "
+                     "engine: compacted to CSR on the device, tensor-core CSR pipeline" % nnz)}
     if with_e2e:
         res["e2e"] = measure_e2e(ctx, gen, dcgm, cfg, n, csr, steps, tm, world, units)
     return res, gen
