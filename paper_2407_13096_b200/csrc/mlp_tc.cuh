@@ -58,13 +58,21 @@ constexpr int MMA_WARP = 4 * MMA_WG;
 #define DSO_MMA_SLEEP_NS 256
 #endif
 constexpr unsigned kMmaSleepNs = DSO_MMA_SLEEP_NS;  // MMA issuer: barrier sleep while two event streams are open
+#ifndef DSO_L3_UNROLL
+#define DSO_L3_UNROLL 50
+#endif
+constexpr int kL3Unroll = DSO_L3_UNROLL;  // layer-3 input neurons per unrolled step
 #ifndef DSO_TC_SWEEP_UNR
 #define DSO_TC_SWEEP_UNR 4  // independent sweep groups per step in the epilogue
 #endif
 #ifndef DSO_EPI1_BATCH
 #define DSO_EPI1_BATCH 4
 #endif
-constexpr int kEpi1Batch = DSO_EPI1_BATCH;  // layer-1 epilogue chunks per TMEM load/store wait
+constexpr int kEpi1Batch = DSO_EPI1_BATCH;
+#ifndef DSO_EPI1_UNROLL
+#define DSO_EPI1_UNROLL 1
+#endif
+constexpr int kEpi1Unroll = DSO_EPI1_UNROLL;  // layer-1 epilogue batches per unrolled step  // layer-1 epilogue chunks per TMEM load/store wait
 // Registers (setmaxnreg): launched at 128 per thread; the MMA warpgroup (the MMA
 // warp and three idle warps) releases down to 56, producers grow to 168 and the
 // epilogue groups to 144 (128*168 + 256*144 + 128*56 = 64K).
@@ -1058,7 +1066,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
                 // wait, activations split and stored as A2, one store wait, then the
                 // batch's chunks are signalled (tcgen05 load / store latencies paid once
                 // per batch instead of once per chunk)
-#pragma unroll 1
+#pragma unroll kEpi1Unroll
                 for (int c0 = 0; c0 < 13; c0 += kEpi1Batch) {
                     float v[kEpi1Batch][8];
 #pragma unroll
@@ -1141,7 +1149,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
                 float2 a3[14];
 #pragma unroll
                 for (int u = 0; u < 14; ++u) a3[u] = make_float2(0.f, 0.f);
-#pragma unroll 5
+#pragma unroll kL3Unroll
                 for (int kk = 0; kk < H2; ++kk) {
                     const float4* wr = reinterpret_cast<const float4*>(sm + W3T + kk * 28);
                     const float2 x2 = make_float2(h2[kk], h2[kk]);

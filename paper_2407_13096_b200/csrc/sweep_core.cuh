@@ -333,6 +333,12 @@ __device__ __forceinline__ float group_min(const KParams& p, const float4* __res
 
 // Exact sweep of core levels [i_lo, i_hi) (non-empty) x all memory levels:
 // identical result to sweep_levels<NM>(..., i_lo, i_hi, ...).
+constexpr int DSO_SWEEP_STEP_UNROLL_C =
+#ifdef DSO_SWEEP_STEP_UNROLL
+    DSO_SWEEP_STEP_UNROLL;
+#else
+    1;
+#endif
 template <int NM, int UNR = 4>
 __device__ __forceinline__ Best sweep_best(const KParams& p, const float4* __restrict__ s_core,
                                            const float2* __restrict__ s_mem, int nm_rt, int i_lo,
@@ -355,7 +361,10 @@ __device__ __forceinline__ Best sweep_best(const KParams& p, const float4* __res
             // UNR independent groups per step: their loads and min trees overlap
             // (a single group is a ~80-cycle dependency chain); folded in order
             if (s_pair && !(i_lo & 1)) {  // groups start on even levels: paired level terms
-#pragma unroll 1
+#ifndef DSO_SWEEP_STEP_UNROLL
+#define DSO_SWEEP_STEP_UNROLL 1
+#endif
+#pragma unroll DSO_SWEEP_STEP_UNROLL_C
                 for (; i + UNR * GL <= i_hi; i += UNR * GL) {
                     float m[UNR];
 #pragma unroll
