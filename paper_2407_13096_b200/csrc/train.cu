@@ -66,6 +66,19 @@ constexpr int kMasterFloats = MB4 + 7;  // 20007
 
 __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
 
+// loop unrolling of the forward / backward layers (build knobs)
+#ifndef DSO_TRAIN_DENSE_UNROLL
+#define DSO_TRAIN_DENSE_UNROLL 4
+#endif
+#ifndef DSO_TRAIN_L1_UNROLL
+#define DSO_TRAIN_L1_UNROLL 4
+#endif
+#ifndef DSO_TRAIN_BACK_UNROLL
+#define DSO_TRAIN_BACK_UNROLL 8
+#endif
+constexpr int kDenseUnroll = DSO_TRAIN_DENSE_UNROLL, kL1Unroll = DSO_TRAIN_L1_UNROLL,
+              kBackUnroll = DSO_TRAIN_BACK_UNROLL;
+
 // The weight image [0, A0S) of the training kernel's shared memory — forward
 // packings per layer, transposed copies for the delta recursion, biases, zero
 // padding — built from the master weights once per update (train_pack_kernel)
@@ -154,7 +167,7 @@ __device__ __forceinline__ void dense(const float* sm, int woff, int boff, int i
     };
     Op A, B;
     load(A, 0);
-#pragma unroll 1
+#pragma unroll kDenseUnroll
     for (int k = 0; k + 1 < K; k += 2) {
         load(B, k + 1);
         math(A);
@@ -212,7 +225,7 @@ __device__ __forceinline__ void dense_l1(float* sm) {
     };
     Op A, B;
     load(A, 0);
-#pragma unroll 1
+#pragma unroll kL1Unroll
     for (int k = 0; k < 132; k += 4) {  // 134 = 33 double stages + one trailing pair
         load(B, k + 2);
         math(A);
@@ -246,7 +259,7 @@ __device__ __forceinline__ void backprop(const float* sm, int toff, int din_off,
     for (int t = 0; t < TK; ++t) res[t] = f2(0.f, 0.f);
     // weights W[n][TK*kg + t] are contiguous in the transposed copy (warp-uniform
     // broadcast loads, TKP/4 LDS.128 per n)
-#pragma unroll 2
+#pragma unroll kBackUnroll
     for (int n = 0; n < NIN; ++n) {
         const float2 d = d2[n * RS2 + mp];
         const float4* w4 = reinterpret_cast<const float4*>(sm + toff + (n * 8 + kg) * TKP);
