@@ -77,7 +77,13 @@ constexpr int kEpi1Unroll = DSO_EPI1_UNROLL;  // layer-1 epilogue batches per un
 // warp and three idle warps) releases down to 56, producers grow to 168 and the
 // epilogue groups to 144 (128*168 + 256*144 + 128*56 = 64K).
 constexpr int kRegLaunch = 128;  // ptxas allocation at launch (checked by launch_tc)
-constexpr int kRegProd = 168, kRegEpi = 144, kRegMma = 56;
+#ifndef DSO_REG_PROD
+#define DSO_REG_PROD 168
+#endif
+#ifndef DSO_REG_EPI
+#define DSO_REG_EPI 144
+#endif
+constexpr int kRegProd = DSO_REG_PROD, kRegEpi = DSO_REG_EPI, kRegMma = 56;
 static_assert(128 * (kRegLaunch - kRegMma) >= 128 * (kRegProd - kRegLaunch) + 256 * (kRegEpi - kRegLaunch),
               "setmaxnreg: increases must be covered by releases");
 constexpr int N1 = 112, K1 = 136, N2 = 64, K2 = 104;
