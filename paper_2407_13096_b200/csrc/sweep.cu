@@ -33,6 +33,10 @@ constexpr int kBlock = 256;
 #ifndef DSO_ETA_CH
 #define DSO_ETA_CH 26
 #endif
+#ifndef DSO_ETA_GROUP_UNROLL
+#define DSO_ETA_GROUP_UNROLL 1
+#endif
+constexpr int kEtaGroupUnroll = DSO_ETA_GROUP_UNROLL;  // eta-sweep groups per unrolled step
 
 __device__ __forceinline__ bool params_invalid(float p0, float kp, float g, float c, float t0,
                                                float a, float b) {
@@ -331,7 +335,7 @@ __global__ void __launch_bounds__(128) eta_sweep_fast_kernel(
                 }
             };
             int i = 0;
-#pragma unroll 1
+#pragma unroll kEtaGroupUnroll
             for (; i + GL <= nc; i += GL) group(i, std::false_type{});
             if (i < nc) group(i, std::true_type{});
         }

@@ -821,6 +821,10 @@ __global__ void __launch_bounds__(twg::kThreadsWG, 1)
                 if (it + 3 < stages) load(it + 3, vb);
             }
         }
+        // every loader's stage writes are ordered before the read-out below reuses the
+        // stage memory as its transpose buffer (the mbarrier / commit chain orders them
+        // too, but this makes it explicit to every tool)
+        asm volatile("bar.sync 2, %0;" ::"n"(kLoadWarps * 32) : "memory");
     } else if (lane == 0) {
         // ---- MMA issuer ----------------------------------------------------------
         const uint32_t s0 = tc::smem_addr(sm);
