@@ -86,7 +86,10 @@ int32_t dso_get_counters(dso_ctx* ctx, uint64_t* out, int32_t n, int32_t reset);
 /* Tuning / verification switches (no reference counterpart; results never
  * depend on them).  key "fast_sweep": 1 (default) lets the FP32 sweeps use the
  * group-minimum argmin (bit-identical, see sweep_core.cuh), 0 forces the
- * pair-by-pair lexicographic scan.  key "dense_csr": 1 (default) lets
+ * pair-by-pair lexicographic scan.  key "eta_prune": 1 (default) lets
+ * dso_eta_sweep on an ascending-frequency domain with 2-4 memory levels sweep
+ * only the nc + nm candidate pairs no other pair can beat (bit-identical, see
+ * sweep.cu), 0 sweeps all pairs.  key "dense_csr": 1 (default) lets
  * dso_pipeline on device buffers with the auto engine compact the dense counts
  * to CSR on the device and run the tensor-core CSR pipeline (one host sync per
  * call), 0 keeps the FMA-pipe dense kernel.  key "train_tc": 1 (default) computes the

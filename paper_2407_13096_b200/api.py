@@ -147,7 +147,8 @@ class Context:
 
     def set_option(self, key: str, value: int) -> None:
         """dso_set_option: verification/tuning switches: "fast_sweep" (0/1, exact
-        group-minimum sweep), "mlp_engine" (0 = FMA-pipe predictor kernel; 1 =
+        group-minimum sweep), "eta_prune" (0/1, eta sweep over the candidate
+        pairs only), "dense_csr", "train_tc", "mlp_engine" (0 = FMA-pipe predictor kernel; 1 =
         tcgen05 3xTF32 kernel for predict and the fused pipelines; 2 = auto, the
         default: tensor cores for predict and the CSR pipeline, FMA pipe for dense)."""
         self._raise(self._lib.dso_set_option(self._h, key.encode(), int(value)))

@@ -281,6 +281,10 @@ int32_t dso_set_option(dso_ctx* ctx, const char* key, int64_t value) {
         ctx->c.fast_sweep = value != 0;
         return kOk;
     }
+    if (std::string(key) == "eta_prune") {
+        ctx->c.eta_prune = value != 0;
+        return kOk;
+    }
     if (std::string(key) == "dense_csr") {
         ctx->c.dense_csr = value != 0;
         return kOk;
@@ -357,6 +361,13 @@ int32_t dso_set_domain(dso_ctx* ctx, const double* core, int32_t nc, const doubl
         fast = fast && mem2[j].x >= 0.f && mem2[j].x <= 1e6f && mem2[j].y >= 0.f &&
                mem2[j].y <= 1e3f;
     c.dom.fast_ok = fast;
+    bool sorted = true;
+    for (int i = 1; i < nc; ++i)
+        sorted = sorted && core4[i].x >= core4[i - 1].x && core4[i].y >= core4[i - 1].y &&
+                 core4[i].z <= core4[i - 1].z;
+    for (int j = 1; j < nm; ++j)
+        sorted = sorted && mem2[j].x >= mem2[j - 1].x && mem2[j].y <= mem2[j - 1].y;
+    c.dom.sorted_ok = sorted;
     c.has_domain = true;
     return kOk;
 }
@@ -744,9 +755,13 @@ int32_t dso_eta_sweep(dso_ctx* ctx, const float* params, int64_t n, int64_t ld,
     }
     DSO_CUDA(ctx, cudaMemcpyAsync(c.eta_dev, ek.data(), sizeof(float2) * n_eta,
                                   cudaMemcpyHostToDevice, c.stream));
-    bool fast = true;
-    for (int e = 0; e < n_eta; ++e) fast = fast && fast_sweep_ok(c, ek[e].y);
-    DSO_CUDA(ctx, launch_eta_sweep(c, params, n, ld, c.eta_dev, n_eta, idx, cost, ld_out, fast));
+    bool fast = true, k_nonneg = true;
+    for (int e = 0; e < n_eta; ++e) {
+        fast = fast && fast_sweep_ok(c, ek[e].y);
+        k_nonneg = k_nonneg && ek[e].x >= 0.f && ek[e].y >= 0.f;
+    }
+    DSO_CUDA(ctx, launch_eta_sweep(c, params, n, ld, c.eta_dev, n_eta, idx, cost, ld_out, fast,
+                                   fast && k_nonneg && c.eta_prune && c.dom.sorted_ok));
     return kOk;
 }
 
@@ -898,7 +913,10 @@ int32_t dso_pipeline_csr(dso_ctx* ctx, const uint64_t* row_ptr, const uint32_t* 
         return kOk;
     }
     // ---- host buffers: chunked, double-buffered H2D / compute / D2H ----------------
-    const int64_t CH = std::min<int64_t>(n, (int64_t)1 << 21);
+#ifndef DSO_HOST_CSR_CHUNK_LOG2
+#define DSO_HOST_CSR_CHUNK_LOG2 20
+#endif
+    const int64_t CH = std::min<int64_t>(n, (int64_t)1 << DSO_HOST_CSR_CHUNK_LOG2);
     uint64_t max_ent = 0;
     for (int64_t off = 0; off < n; off += CH) {
         const int64_t m = std::min(CH, n - off);

@@ -67,6 +67,10 @@ struct DomainDev {
     // the f32 tables are within the bounds under which the fast exact sweep's
     // costs stay finite (sweep_core.cuh sweep_best)
     bool fast_ok;
+    // vc and vc^2 fc non-decreasing and 1/fc non-increasing along the core
+    // levels, fm non-decreasing and 1/fm non-increasing along the memory levels
+    // (ascending frequency lists): the eta sweep's candidate pruning applies
+    bool sorted_ok;
 };
 
 // Device model: transposed, zero-padded weights for the FP32 MLP kernels.
@@ -134,6 +138,7 @@ struct Ctx {
     cudaEvent_t ev[8] = {};
     int num_sms = 148;
     bool fast_sweep = true;         // dso_set_option("fast_sweep")
+    bool eta_prune = true;          // dso_set_option("eta_prune"): pruned eta sweep
     bool train_tc = true;           // dso_set_option("train_tc"): weight gradients on tcgen05
     int mlp_engine = 2;             // dso_set_option("mlp_engine"): 0 FMA pipe, 1 tensor cores,
                                     // 2 auto (tensor cores for predict / CSR, FMA pipe for dense)
@@ -176,7 +181,7 @@ cudaError_t launch_sweep_f64(Ctx& c, const double* params, int64_t n, double eta
                              int32_t* kstatus);
 cudaError_t launch_eta_sweep(Ctx& c, const float* params, int64_t n, int64_t ld,
                              const float2* etaK_dev, int n_eta, int32_t* idx, float* cost,
-                             int64_t ld_out, bool fast);
+                             int64_t ld_out, bool fast, bool prune);
 cudaError_t launch_optimal_config(Ctx& c, const double* params, int64_t n, double eta,
                                   double K, int32_t* idx, double* cost, double* energy,
                                   double* time, int64_t* candidates, uint8_t* fallback,

@@ -36,6 +36,12 @@ constexpr int kBlock = 256;
 #ifndef DSO_ETA_GROUP_UNROLL
 #define DSO_ETA_GROUP_UNROLL 1
 #endif
+#ifndef DSO_ETA_PRUNE_MINB
+#define DSO_ETA_PRUNE_MINB 3
+#endif
+#ifndef DSO_ETA_PRUNE_CH
+#define DSO_ETA_PRUNE_CH 26
+#endif
 constexpr int kEtaGroupUnroll = DSO_ETA_GROUP_UNROLL;  // eta-sweep groups per unrolled step
 
 __device__ __forceinline__ bool params_invalid(float p0, float kp, float g, float c, float t0,
@@ -354,6 +360,291 @@ __global__ void __launch_bounds__(128) eta_sweep_fast_kernel(
     }
 }
 
+// ---- Pruned exact eta sweep (NM = 2..4) ------------------------------------
+//
+// Preconditions (host: DomainDev::sorted_ok, every eta >= 0 and K >= 0; device:
+// params_fast): along the core levels vc and vc^2 fc are non-decreasing and
+// 1/fc non-increasing, along the memory levels fm is non-decreasing and 1/fm
+// non-increasing.  With params >= 0 (validate(params)) every rounded quantity
+// is then monotone: Pc_i and TB_i = t0 + b/fc_i along i (up / down), G_j = g fm_j
+// and TA_j = t0 + a/fm_j along j (up / down), and C = (eta P + K) T, E = P T are
+// non-decreasing in P and T (round-to-nearest is monotone; all operands >= 0).
+//
+// Every pair (i, j) has T = max(TA_j, TB_i), so it lies in
+//   J_i = { j : TA_j <= TB_i }  (T = TB_i; a suffix of the memory levels) or
+//   S_j = { i : TB_i <= TA_j }  (T = TA_j; a suffix of the core levels).
+// Inside J_i the first member j0(i) has the least P and the same T as the others,
+// hence C and E no larger, and it comes first in visit order: no other member of
+// J_i can be strictly better than it (better(), optimizer.cpp:27-32), so none can
+// be the scan's answer.  Likewise inside S_j for its first member i0(j).  The
+// scan's answer is therefore among the candidates
+//   (i, j0(i)) for every level i with J_i non-empty, and (i0(j), j) for every j
+// with S_j non-empty: at most nc + NM points instead of nc * NM (132 of 512 on
+// the 128 x 4 grids).  Over the candidates the group-minimum scheme of
+// sweep_best runs unchanged (groups of 8 level candidates plus one group of the
+// NM knee candidates; a minimum reached by two groups -> exact full rescan), and
+// the winning group's candidates are replayed with the sequential rule: each
+// eta's (idx, cost) equals dso_sweep's bit for bit.  A missing candidate is a
+// NaN slot (FMNMX drops it; it never compares equal or smaller).
+constexpr int kPruneL = 8;  // level candidates per group
+
+// Candidates of the 8 levels i .. i+7 (clamped to nc-1: a repeated candidate is
+// the same pair, so neither the group minimum nor the replay changes).
+template <int NM, bool PAIRED>
+__device__ __forceinline__ void prune_level_cands(const KParams& p,
+                                                  const float4* __restrict__ s_core,
+                                                  const float4* __restrict__ s_pair, int i,
+                                                  int nc, const float* G, const float* TA,
+                                                  float2* P2, float2* T2, int* js) {
+    float pc[kPruneL], tb[kPruneL];
+    if constexpr (PAIRED) {  // i even, i + 8 <= nc
+#pragma unroll
+        for (int l2 = 0; l2 < kPruneL / 2; ++l2) {
+            const int q = (i >> 1) + l2;
+            const float4 v = s_pair[2 * q], r = s_pair[2 * q + 1];
+            const float2 pc2 = ffma2(make_float2(p.c, p.c), make_float2(v.z, v.w),
+                                     ffma2(make_float2(p.kp, p.kp), make_float2(v.x, v.y),
+                                           make_float2(p.p0, p.p0)));
+            pc[2 * l2] = pc2.x;
+            pc[2 * l2 + 1] = pc2.y;
+            tb[2 * l2] = __fadd_rn(p.t0, __fmul_rn(p.b, r.x));
+            tb[2 * l2 + 1] = __fadd_rn(p.t0, __fmul_rn(p.b, r.y));
+        }
+    } else {
+#pragma unroll
+        for (int l = 0; l < kPruneL; ++l) {
+            const float4 t = s_core[min(i + l, nc - 1)];
+            pc[l] = pc_f32(p.p0, p.kp, p.c, t);
+            tb[l] = __fadd_rn(p.t0, __fmul_rn(p.b, t.z));
+        }
+    }
+    float P[kPruneL];
+#pragma unroll
+    for (int l = 0; l < kPruneL; ++l) {
+        float gs = __int_as_float(0x7fffffff);  // J_i empty -> NaN slot
+        int j0 = NM;
+#pragma unroll
+        for (int j = NM - 1; j >= 0; --j) {
+            const bool cb = TA[j] <= tb[l];
+            gs = cb ? G[j] : gs;
+            j0 = cb ? j : j0;
+        }
+        P[l] = __fadd_rn(pc[l], gs);
+        js[l] = j0;
+    }
+#pragma unroll
+    for (int q = 0; q < kPruneL / 2; ++q) {
+        P2[q] = make_float2(P[2 * q], P[2 * q + 1]);
+        T2[q] = make_float2(tb[2 * q], tb[2 * q + 1]);
+    }
+}
+
+__device__ __forceinline__ float prune_min8(const float2* P2, const float2* T2, float eta,
+                                            float K) {
+    float c[8];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const float2 C = fmul2(ffma2(make_float2(eta, eta), P2[q], make_float2(K, K)), T2[q]);
+        c[2 * q] = C.x;
+        c[2 * q + 1] = C.y;
+    }
+    return fminf(fmin3(c[0], c[1], c[2]), fmin3(c[3], c[4], fmin3(c[5], c[6], c[7])));
+}
+
+__device__ __forceinline__ float prune_min4(const float2* P2, const float2* T2, float eta,
+                                            float K) {
+    float c[4];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+        const float2 C = fmul2(ffma2(make_float2(eta, eta), P2[q], make_float2(K, K)), T2[q]);
+        c[2 * q] = C.x;
+        c[2 * q + 1] = C.y;
+    }
+    return fminf(fmin3(c[0], c[1], c[2]), c[3]);
+}
+
+// Sequential rule over candidate slots in visit order (strictly better wins).
+__device__ __forceinline__ void prune_upd(float P, float T, float eta, float K, int id,
+                                          float& rc, float& re, int& ri) {
+    const float C = cost_f32(eta, K, P, T);
+    const float E = __fmul_rn(P, T);
+    const bool better = (C < rc) | ((C == rc) & (E < re));
+    rc = better ? C : rc;
+    re = better ? E : re;
+    ri = better ? id : ri;
+}
+
+// Exact replay of one group's candidates (out of line: one copy of the code
+// for all unrolled etas keeps the kernel inside the instruction cache).
+// Arguments by value (registers): G / TA are re-formed from the tables and the
+// knee levels arrive packed 16 bits each.
+template <int NM>
+__device__ __noinline__ int2 prune_replay(const KParams p, const float4* __restrict__ s_core,
+                                          const float2* __restrict__ s_mem, int g, int ng,
+                                          int nc, uint64_t i0p, float eta, float K) {
+    float G[NM], TA[NM];
+#pragma unroll
+    for (int j = 0; j < NM; ++j) {
+        G[j] = __fmul_rn(p.g, s_mem[j].x);
+        TA[j] = __fadd_rn(p.t0, __fmul_rn(p.a, s_mem[j].y));
+    }
+    float rc = __int_as_float(0x7f800000), re = rc;
+    int ri = -1;
+    if (g == ng) {
+#pragma unroll
+        for (int j = 0; j < NM; ++j) {
+            const int i0 = (int)((i0p >> (16 * j)) & 0xffffu);
+            const float pc = pc_f32(p.p0, p.kp, p.c, s_core[min(i0, nc - 1)]);
+            const float P = i0 < nc ? __fadd_rn(pc, G[j]) : __int_as_float(0x7fffffff);
+            prune_upd(P, TA[j], eta, K, i0 * NM + j, rc, re, ri);
+        }
+    } else {
+        float2 P2[4], T2[4];
+        int js[kPruneL];
+        prune_level_cands<NM, false>(p, s_core, nullptr, g * kPruneL, nc, G, TA, P2, T2, js);
+#pragma unroll
+        for (int l = 0; l < kPruneL; ++l) {
+            const float P = l & 1 ? P2[l >> 1].y : P2[l >> 1].x;
+            const float T = l & 1 ? T2[l >> 1].y : T2[l >> 1].x;
+            prune_upd(P, T, eta, K, min(g * kPruneL + l, nc - 1) * NM + js[l], rc, re, ri);
+        }
+    }
+    return make_int2(ri, __float_as_int(rc));
+}
+
+template <int CH, int NM>
+__global__ void __launch_bounds__(128, DSO_ETA_PRUNE_MINB) eta_sweep_pruned_kernel(
+    const float* __restrict__ params, int64_t n, int64_t ld, const float4* __restrict__ core4,
+    int nc, const float2* __restrict__ mem2, const float2* __restrict__ etaK, int n_eta,
+    int32_t* __restrict__ idx, float* __restrict__ cost, int64_t ld_out) {
+    static_assert(CH <= 64 && NM >= 2 && NM <= 4, "tie bits / memory levels");
+    using TieT = std::conditional_t<(CH > 32), uint64_t, uint32_t>;
+    __shared__ float4 s_core[kMaxCore];
+    __shared__ float4 s_pair[kMaxCore + 2];
+    __shared__ float2 s_mem[NM];
+    for (int i = threadIdx.x; i < nc; i += blockDim.x) s_core[i] = core4[i];
+    if (threadIdx.x < NM) s_mem[threadIdx.x] = mem2[threadIdx.x];
+    build_pairs(s_pair, core4, nc);
+    __syncthreads();
+    const int e0 = blockIdx.y * CH;
+    float ev[CH], Kv[CH];
+#pragma unroll
+    for (int e = 0; e < CH; ++e) {
+        const int ee = e0 + e < n_eta ? e0 + e : n_eta - 1;
+        ev[e] = etaK[ee].x;
+        Kv[e] = etaK[ee].y;
+    }
+    const int ng_full = nc / kPruneL;  // paired groups; a tail group covers the rest
+    const int ng = (nc + kPruneL - 1) / kPruneL;
+    const int top = 1 << (31 - __clz(nc));
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride) {
+        KParams p;
+        p.p0 = __ldg(params + k);
+        p.kp = __ldg(params + ld + k);
+        p.g = __ldg(params + 2 * ld + k);
+        p.c = __ldg(params + 3 * ld + k);
+        p.t0 = __ldg(params + 4 * ld + k);
+        p.a = __ldg(params + 5 * ld + k);
+        p.b = __ldg(params + 6 * ld + k);
+        if (params_invalid(p.p0, p.kp, p.g, p.c, p.t0, p.a, p.b)) {
+#pragma unroll
+            for (int e = 0; e < CH; ++e)
+                if (e0 + e < n_eta) {
+                    idx[(int64_t)(e0 + e) * ld_out + k] = -1;
+                    if (cost) cost[(int64_t)(e0 + e) * ld_out + k] = __int_as_float(0x7fc00000);
+                }
+            continue;
+        }
+        const bool fast = params_fast(p);
+        float G[NM], TA[NM];
+#pragma unroll
+        for (int j = 0; j < NM; ++j) {
+            G[j] = __fmul_rn(p.g, s_mem[j].x);
+            TA[j] = __fadd_rn(p.t0, __fmul_rn(p.a, s_mem[j].y));
+        }
+        // knee candidates (i0(j), j): i0(j) = #{ i : TB_i > TA_j } (a prefix)
+        uint64_t i0p = 0;
+        float2 KP2[2], KT2[2];
+        {
+            float kp_[4], kt_[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                kp_[j] = __int_as_float(0x7fffffff);
+                kt_[j] = 1.f;
+            }
+#pragma unroll
+            for (int j = 0; j < NM; ++j) {
+                int pos = 0;
+                for (int s = top; s > 0; s >>= 1)
+                    if (pos + s <= nc &&
+                        __fadd_rn(p.t0, __fmul_rn(p.b, s_core[pos + s - 1].z)) > TA[j])
+                        pos += s;
+                i0p |= (uint64_t)pos << (16 * j);
+                const float pc = pc_f32(p.p0, p.kp, p.c, s_core[min(pos, nc - 1)]);
+                kp_[j] = pos < nc ? __fadd_rn(pc, G[j]) : __int_as_float(0x7fffffff);
+                kt_[j] = TA[j];
+            }
+            KP2[0] = make_float2(kp_[0], kp_[1]);
+            KP2[1] = make_float2(kp_[2], kp_[3]);
+            KT2[0] = make_float2(kt_[0], kt_[1]);
+            KT2[1] = make_float2(kt_[2], kt_[3]);
+        }
+        float bc[CH];
+        int bg[CH];
+        TieT ties = fast ? TieT(0) : ~TieT(0);
+        if (fast) {
+#pragma unroll
+            for (int e = 0; e < CH; ++e) {
+                bc[e] = fminf(prune_min4(KP2, KT2, ev[e], Kv[e]), __int_as_float(0x7f800000));
+                bg[e] = ng;  // the knee group
+            }
+            auto group = [&](int g, auto paired) {
+                float2 P2[4], T2[4];
+                int js[kPruneL];
+                prune_level_cands<NM, decltype(paired)::value>(p, s_core, s_pair, g * kPruneL,
+                                                               nc, G, TA, P2, T2, js);
+#pragma unroll
+                for (int e = 0; e < CH; ++e) {
+                    const float m = prune_min8(P2, T2, ev[e], Kv[e]);
+                    ties |= m == bc[e] ? TieT(1) << e : TieT(0);
+                    bg[e] = m < bc[e] ? g : bg[e];
+                    bc[e] = fminf(m, bc[e]);
+                }
+            };
+            int g = 0;
+#pragma unroll 1
+            for (; g < ng_full; ++g) group(g, std::true_type{});
+            if (g < ng) group(g, std::false_type{});
+        } else {
+#pragma unroll
+            for (int e = 0; e < CH; ++e) {
+                bc[e] = 0.f;
+                bg[e] = 0;
+            }
+        }
+#pragma unroll
+        for (int e = 0; e < CH; ++e) {
+            if (e0 + e < n_eta) {
+                int bi;
+                float bcost;
+                if ((ties >> e) & TieT(1)) {
+                    const Best b = replay_levels<NM>(p, s_core, s_mem, 0, nc, ev[e], Kv[e]);
+                    bi = b.i;
+                    bcost = b.c;
+                } else {
+                    const int2 r = prune_replay<NM>(p, s_core, s_mem, bg[e], ng, nc, i0p,
+                                                    ev[e], Kv[e]);
+                    bi = r.x;
+                    bcost = __int_as_float(r.y);
+                }
+                idx[(int64_t)(e0 + e) * ld_out + k] = bi;
+                if (cost) cost[(int64_t)(e0 + e) * ld_out + k] = bcost;
+            }
+        }
+    }
+}
+
 }  // namespace
 
 cudaError_t launch_sweep_f32(Ctx& cx, const float* params, int64_t n, int64_t ld, float eta,
@@ -393,9 +684,26 @@ cudaError_t launch_sweep_f64(Ctx& cx, const double* params, int64_t n, double et
 
 cudaError_t launch_eta_sweep(Ctx& cx, const float* params, int64_t n, int64_t ld,
                              const float2* etaK_dev, int n_eta, int32_t* idx, float* cost,
-                             int64_t ld_out, bool fast) {
+                             int64_t ld_out, bool fast, bool prune) {
     if (n <= 0 || n_eta <= 0) return cudaSuccess;
     const DomainDev& d = cx.dom;
+    if (prune && d.nm >= 2 && d.nm <= 4) {
+        constexpr int CH = DSO_ETA_PRUNE_CH;
+        const int chunks = (n_eta + CH - 1) / CH;
+        const int gx = grid_for(n, 128, cx.num_sms, 16);
+        dim3 grid(gx, chunks);
+#define DSO_ETA_PRUNED(NMV)                                                                 \
+    eta_sweep_pruned_kernel<CH, NMV><<<grid, 128, 0, cx.stream>>>(                          \
+        params, n, ld, d.core4, d.nc, d.mem2, etaK_dev, n_eta, idx, cost, ld_out)
+        switch (d.nm) {
+            case 2: DSO_ETA_PRUNED(2); break;
+            case 3: DSO_ETA_PRUNED(3); break;
+            default: DSO_ETA_PRUNED(4); break;
+        }
+#undef DSO_ETA_PRUNED
+        ++cx.launches;
+        return cudaGetLastError();
+    }
     if (fast && d.nm >= 1 && d.nm <= 4) {
         // chunks of up to 26 etas (101 -> 4 chunks of 26, 3 padding slots)
         constexpr int CH = DSO_ETA_CH;

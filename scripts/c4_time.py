@@ -18,8 +18,10 @@ p = ctx.gen_synthetic(n, root=0xD50B203, counts=False, dcgm=False)["params"]
 idx_o = torch.empty((101, n), dtype=torch.int32, device="cuda")
 cost_o = torch.empty((101, n), dtype=torch.float32, device="cuda")
 ea = np.ascontiguousarray(np.arange(101) / 100.0)
-ts = []
-for _ in range(6):
+for prune in (1, 0):
+  ctx.set_option("eta_prune", prune)
+  ts = []
+  for _ in range(6):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     ctx._raise(ctx._lib.dso_eta_sweep(ctx._h, _ptr(p), n, n, ea.ctypes.data_as(C.POINTER(C.c_double)),
@@ -27,4 +29,8 @@ for _ in range(6):
     e1.record()
     torch.cuda.synchronize()
     ts.append(e0.elapsed_time(e1))
-print("C4 eta sweep ms:", [round(t, 2) for t in ts])
+  if prune:
+    ref_idx, ref_cost = idx_o.clone(), cost_o.clone()
+  else:
+    print("pruned == unpruned:", bool(torch.equal(ref_idx, idx_o)), bool(torch.equal(ref_cost.view(torch.int32), cost_o.view(torch.int32))))
+  print("C4 eta sweep prune=%d ms:" % prune, [round(t, 2) for t in ts])

@@ -227,6 +227,51 @@ def test_fast_eta_sweep_bit_identical(ctx, golden_sweep, name):
         np.testing.assert_array_equal(ia[e], r["idx"].cpu().numpy())
 
 
+def _eta_runs(ctx, p, etas, opts):
+    out = []
+    try:
+        for fast, prune in opts:
+            ctx.set_option("fast_sweep", fast)
+            ctx.set_option("eta_prune", prune)
+            i, c = (x.cpu().numpy() for x in ctx.eta_sweep(p, etas))
+            out.append((i, c.view(np.uint32)))
+    finally:
+        ctx.set_option("fast_sweep", 1)
+        ctx.set_option("eta_prune", 1)
+    return out
+
+
+@pytest.mark.parametrize("dom", ["c4", "nm2", "nm3", "tail", "close"])
+def test_pruned_eta_sweep_bit_identical(ctx, dom):
+    """The pruned eta sweep (candidate set of nc + nm points, sweep.cu) equals the
+    unpruned group-minimum sweep and the pair-by-pair scan bit for bit (domains
+    are strictly increasing by validate(DvfsDomain); "close" has levels whose f32
+    tables are equal), with tie-built, huge, non-finite and invalid params among
+    realistic ones."""
+    base = config_domain("c4")
+    core, mem, dev = base.core_freqs_mhz, base.mem_freqs_mhz, base.dev
+    if dom == "close":                   # adjacent levels whose f32 tables coincide
+        core = np.sort(np.concatenate([core[:60], core[:60] * (1 + 1e-9)]))
+        mem = np.array([mem[0], mem[0] * (1 + 1e-9), mem[2]])
+    elif dom == "nm2":
+        mem = mem[:2].copy()
+    elif dom == "nm3":
+        core, mem = core[::3].copy(), mem[:3].copy()
+    elif dom == "tail":                  # nc not a multiple of the 8-level group
+        core = core[:77].copy()
+    ctx.set_domain(DvfsDomain(core, mem, dev))
+    rng = np.random.default_rng(21)
+    gen = ctx.gen_synthetic(6_000, root=0xD50B204, counts=False, dcgm=False)
+    params = np.concatenate([gen["params"].cpu().numpy().T.astype(np.float64),
+                             _tie_params(rng, 6_000)])
+    p = soa(params)
+    etas = np.concatenate([np.arange(101) / 100.0, [0.0, 1.0, 0.55]])
+    runs = _eta_runs(ctx, p, etas, [(1, 1), (1, 0), (0, 0)])
+    for i, c in runs[1:]:
+        np.testing.assert_array_equal(runs[0][0], i)
+        np.testing.assert_array_equal(runs[0][1], c)
+
+
 def test_set_option_errors(ctx):
     with pytest.raises(DsoError) as e:
         ctx.set_option("no_such_option", 1)
