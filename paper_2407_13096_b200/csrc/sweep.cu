@@ -463,54 +463,24 @@ __device__ __forceinline__ float prune_min4(const float2* P2, const float2* T2, 
     return fminf(fmin3(c[0], c[1], c[2]), c[3]);
 }
 
-// Sequential rule over candidate slots in visit order (strictly better wins).
-__device__ __forceinline__ void prune_upd(float P, float T, float eta, float K, int id,
-                                          float& rc, float& re, int& ri) {
-    const float C = cost_f32(eta, K, P, T);
-    const float E = __fmul_rn(P, T);
-    const bool better = (C < rc) | ((C == rc) & (E < re));
-    rc = better ? C : rc;
-    re = better ? E : re;
-    ri = better ? id : ri;
+// First slot (visit order) of the exact lexicographic winner among n slots
+// whose minimum cost m is known: the least energy among the slots costing m,
+// the first such slot on equal energies (better(), optimizer.cpp:27-32).
+template <int N>
+__device__ __forceinline__ int prune_pick(const float* C, const float* E, float m) {
+    float e[N];
+#pragma unroll
+    for (int l = 0; l < N; ++l) e[l] = C[l] == m ? E[l] : __int_as_float(0x7f800000);
+    float emin = e[0];
+#pragma unroll
+    for (int l = 1; l < N; ++l) emin = fminf(emin, e[l]);
+    int pos = N - 1;
+#pragma unroll
+    for (int l = N - 2; l >= 0; --l) pos = e[l] == emin ? l : pos;
+    return pos;
 }
 
-// Exact replay of one group's candidates (out of line: one copy of the code
-// for all unrolled etas keeps the kernel inside the instruction cache).
-// Arguments by value (registers): G / TA are re-formed from the tables and the
-// knee levels arrive packed 16 bits each.
-template <int NM>
-__device__ __noinline__ int2 prune_replay(const KParams p, const float4* __restrict__ s_core,
-                                          const float2* __restrict__ s_mem, int g, int ng,
-                                          int nc, uint64_t i0p, float eta, float K) {
-    float G[NM], TA[NM];
-#pragma unroll
-    for (int j = 0; j < NM; ++j) {
-        G[j] = __fmul_rn(p.g, s_mem[j].x);
-        TA[j] = __fadd_rn(p.t0, __fmul_rn(p.a, s_mem[j].y));
-    }
-    float rc = __int_as_float(0x7f800000), re = rc;
-    int ri = -1;
-    if (g == ng) {
-#pragma unroll
-        for (int j = 0; j < NM; ++j) {
-            const int i0 = (int)((i0p >> (16 * j)) & 0xffffu);
-            const float pc = pc_f32(p.p0, p.kp, p.c, s_core[min(i0, nc - 1)]);
-            const float P = i0 < nc ? __fadd_rn(pc, G[j]) : __int_as_float(0x7fffffff);
-            prune_upd(P, TA[j], eta, K, i0 * NM + j, rc, re, ri);
-        }
-    } else {
-        float2 P2[4], T2[4];
-        int js[kPruneL];
-        prune_level_cands<NM, false>(p, s_core, nullptr, g * kPruneL, nc, G, TA, P2, T2, js);
-#pragma unroll
-        for (int l = 0; l < kPruneL; ++l) {
-            const float P = l & 1 ? P2[l >> 1].y : P2[l >> 1].x;
-            const float T = l & 1 ? T2[l >> 1].y : T2[l >> 1].x;
-            prune_upd(P, T, eta, K, min(g * kPruneL + l, nc - 1) * NM + js[l], rc, re, ri);
-        }
-    }
-    return make_int2(ri, __float_as_int(rc));
-}
+constexpr int kPruneMaxCore = 256;  // pruned kernel: nc <= 256 (per-thread js cache)
 
 template <int CH, int NM>
 __global__ void __launch_bounds__(128, DSO_ETA_PRUNE_MINB) eta_sweep_pruned_kernel(
@@ -519,26 +489,33 @@ __global__ void __launch_bounds__(128, DSO_ETA_PRUNE_MINB) eta_sweep_pruned_kern
     int32_t* __restrict__ idx, float* __restrict__ cost, int64_t ld_out) {
     static_assert(CH <= 64 && NM >= 2 && NM <= 4, "tie bits / memory levels");
     using TieT = std::conditional_t<(CH > 32), uint64_t, uint32_t>;
-    __shared__ float4 s_core[kMaxCore];
-    __shared__ float4 s_pair[kMaxCore + 2];
+    __shared__ float4 s_core[kPruneMaxCore];
+    __shared__ float4 s_pair[kPruneMaxCore + 2];
     __shared__ float2 s_mem[NM];
-    for (int i = threadIdx.x; i < nc; i += blockDim.x) s_core[i] = core4[i];
-    if (threadIdx.x < NM) s_mem[threadIdx.x] = mem2[threadIdx.x];
+    __shared__ float2 s_ek[CH];
+    // per thread: the 2-bit j0 of every level candidate (one 16-bit word per
+    // group), each eta's winning group, and G_j — read back by the replay
+    __shared__ uint16_t s_js[kPruneMaxCore / kPruneL][128];
+    __shared__ uint8_t s_bg[CH][128];
+    __shared__ float s_G[NM][128];
+    const int tid = threadIdx.x;
+    for (int i = tid; i < nc; i += blockDim.x) s_core[i] = core4[i];
+    if (tid < NM) s_mem[tid] = mem2[tid];
     build_pairs(s_pair, core4, nc);
-    __syncthreads();
     const int e0 = blockIdx.y * CH;
+    for (int e = tid; e < CH; e += blockDim.x) s_ek[e] = etaK[e0 + e < n_eta ? e0 + e : n_eta - 1];
+    __syncthreads();
     float ev[CH], Kv[CH];
 #pragma unroll
     for (int e = 0; e < CH; ++e) {
-        const int ee = e0 + e < n_eta ? e0 + e : n_eta - 1;
-        ev[e] = etaK[ee].x;
-        Kv[e] = etaK[ee].y;
+        ev[e] = s_ek[e].x;
+        Kv[e] = s_ek[e].y;
     }
     const int ng_full = nc / kPruneL;  // paired groups; a tail group covers the rest
     const int ng = (nc + kPruneL - 1) / kPruneL;
     const int top = 1 << (31 - __clz(nc));
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride) {
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + tid; k < n; k += stride) {
         KParams p;
         p.p0 = __ldg(params + k);
         p.kp = __ldg(params + ld + k);
@@ -562,9 +539,10 @@ __global__ void __launch_bounds__(128, DSO_ETA_PRUNE_MINB) eta_sweep_pruned_kern
         for (int j = 0; j < NM; ++j) {
             G[j] = __fmul_rn(p.g, s_mem[j].x);
             TA[j] = __fadd_rn(p.t0, __fmul_rn(p.a, s_mem[j].y));
+            s_G[j][tid] = G[j];
         }
         // knee candidates (i0(j), j): i0(j) = #{ i : TB_i > TA_j } (a prefix)
-        uint64_t i0p = 0;
+        int i0[4];
         float2 KP2[2], KT2[2];
         {
             float kp_[4], kt_[4];
@@ -572,6 +550,7 @@ __global__ void __launch_bounds__(128, DSO_ETA_PRUNE_MINB) eta_sweep_pruned_kern
             for (int j = 0; j < 4; ++j) {
                 kp_[j] = __int_as_float(0x7fffffff);
                 kt_[j] = 1.f;
+                i0[j] = 0;
             }
 #pragma unroll
             for (int j = 0; j < NM; ++j) {
@@ -580,7 +559,7 @@ __global__ void __launch_bounds__(128, DSO_ETA_PRUNE_MINB) eta_sweep_pruned_kern
                     if (pos + s <= nc &&
                         __fadd_rn(p.t0, __fmul_rn(p.b, s_core[pos + s - 1].z)) > TA[j])
                         pos += s;
-                i0p |= (uint64_t)pos << (16 * j);
+                i0[j] = pos;
                 const float pc = pc_f32(p.p0, p.kp, p.c, s_core[min(pos, nc - 1)]);
                 kp_[j] = pos < nc ? __fadd_rn(pc, G[j]) : __int_as_float(0x7fffffff);
                 kt_[j] = TA[j];
@@ -590,10 +569,10 @@ __global__ void __launch_bounds__(128, DSO_ETA_PRUNE_MINB) eta_sweep_pruned_kern
             KT2[0] = make_float2(kt_[0], kt_[1]);
             KT2[1] = make_float2(kt_[2], kt_[3]);
         }
-        float bc[CH];
-        int bg[CH];
         TieT ties = fast ? TieT(0) : ~TieT(0);
         if (fast) {
+            float bc[CH];
+            int bg[CH];
 #pragma unroll
             for (int e = 0; e < CH; ++e) {
                 bc[e] = fminf(prune_min4(KP2, KT2, ev[e], Kv[e]), __int_as_float(0x7f800000));
@@ -604,6 +583,10 @@ __global__ void __launch_bounds__(128, DSO_ETA_PRUNE_MINB) eta_sweep_pruned_kern
                 int js[kPruneL];
                 prune_level_cands<NM, decltype(paired)::value>(p, s_core, s_pair, g * kPruneL,
                                                                nc, G, TA, P2, T2, js);
+                uint32_t w = 0;
+#pragma unroll
+                for (int l = 0; l < kPruneL; ++l) w |= (uint32_t)(js[l] & 3) << (2 * l);
+                s_js[g][tid] = (uint16_t)w;
 #pragma unroll
                 for (int e = 0; e < CH; ++e) {
                     const float m = prune_min8(P2, T2, ev[e], Kv[e]);
@@ -616,31 +599,64 @@ __global__ void __launch_bounds__(128, DSO_ETA_PRUNE_MINB) eta_sweep_pruned_kern
 #pragma unroll 1
             for (; g < ng_full; ++g) group(g, std::true_type{});
             if (g < ng) group(g, std::false_type{});
-        } else {
 #pragma unroll
-            for (int e = 0; e < CH; ++e) {
-                bc[e] = 0.f;
-                bg[e] = 0;
-            }
+            for (int e = 0; e < CH; ++e) s_bg[e][tid] = (uint8_t)bg[e];
         }
+        // replay, one eta per iteration (rolled: one copy of the code)
+        const float ta_last = TA[NM - 1];
+#pragma unroll 1
+        for (int e = 0; e < CH && e0 + e < n_eta; ++e) {
+            const float eta = s_ek[e].x, K = s_ek[e].y;
+            int bi;
+            float bcost;
+            if ((ties >> e) & TieT(1)) {
+                const Best b = replay_levels<NM>(p, s_core, s_mem, 0, nc, eta, K);
+                bi = b.i;
+                bcost = b.c;
+            } else {
+                const int g = s_bg[e][tid];
+                if (g == ng) {
+                    float C[4], E[4];
 #pragma unroll
-        for (int e = 0; e < CH; ++e) {
-            if (e0 + e < n_eta) {
-                int bi;
-                float bcost;
-                if ((ties >> e) & TieT(1)) {
-                    const Best b = replay_levels<NM>(p, s_core, s_mem, 0, nc, ev[e], Kv[e]);
-                    bi = b.i;
-                    bcost = b.c;
+                    for (int q = 0; q < 2; ++q) {
+                        const float2 c2 = fmul2(
+                            ffma2(make_float2(eta, eta), KP2[q], make_float2(K, K)), KT2[q]);
+                        const float2 e2 = fmul2(KP2[q], KT2[q]);
+                        C[2 * q] = c2.x;
+                        C[2 * q + 1] = c2.y;
+                        E[2 * q] = e2.x;
+                        E[2 * q + 1] = e2.y;
+                    }
+                    const float m = fminf(fmin3(C[0], C[1], C[2]), C[3]);
+                    const int pos = prune_pick<4>(C, E, m);
+                    int ip = i0[0];
+#pragma unroll
+                    for (int j = 1; j < 4; ++j) ip = pos == j ? i0[j] : ip;
+                    bi = ip * NM + pos;
+                    bcost = m;
                 } else {
-                    const int2 r = prune_replay<NM>(p, s_core, s_mem, bg[e], ng, nc, i0p,
-                                                    ev[e], Kv[e]);
-                    bi = r.x;
-                    bcost = __int_as_float(r.y);
+                    const uint32_t w = s_js[g][tid];
+                    const int ib = g * kPruneL;
+                    float C[kPruneL], E[kPruneL];
+#pragma unroll
+                    for (int l = 0; l < kPruneL; ++l) {
+                        const float4 t = s_core[min(ib + l, nc - 1)];
+                        const float pc = pc_f32(p.p0, p.kp, p.c, t);
+                        const float tb = __fadd_rn(p.t0, __fmul_rn(p.b, t.z));
+                        const float gj = s_G[(w >> (2 * l)) & 3][tid];
+                        const float P = ta_last > tb ? __int_as_float(0x7fffffff)
+                                                     : __fadd_rn(pc, gj);
+                        C[l] = cost_f32(eta, K, P, tb);
+                        E[l] = __fmul_rn(P, tb);
+                    }
+                    const float m = fminf(fmin3(C[0], C[1], C[2]), fmin3(C[3], C[4], fmin3(C[5], C[6], C[7])));
+                    const int pos = prune_pick<kPruneL>(C, E, m);
+                    bi = min(ib + pos, nc - 1) * NM + (int)((w >> (2 * pos)) & 3);
+                    bcost = m;
                 }
-                idx[(int64_t)(e0 + e) * ld_out + k] = bi;
-                if (cost) cost[(int64_t)(e0 + e) * ld_out + k] = bcost;
             }
+            idx[(int64_t)(e0 + e) * ld_out + k] = bi;
+            if (cost) cost[(int64_t)(e0 + e) * ld_out + k] = bcost;
         }
     }
 }
@@ -687,7 +703,7 @@ cudaError_t launch_eta_sweep(Ctx& cx, const float* params, int64_t n, int64_t ld
                              int64_t ld_out, bool fast, bool prune) {
     if (n <= 0 || n_eta <= 0) return cudaSuccess;
     const DomainDev& d = cx.dom;
-    if (prune && d.nm >= 2 && d.nm <= 4) {
+    if (prune && d.nm >= 2 && d.nm <= 4 && d.nc <= kPruneMaxCore) {
         constexpr int CH = DSO_ETA_PRUNE_CH;
         const int chunks = (n_eta + CH - 1) / CH;
         const int gx = grid_for(n, 128, cx.num_sms, 16);
