@@ -311,10 +311,59 @@ __device__ __forceinline__ void write_rows(const float* sm, int off, int R, floa
 // deltas D1 | D2 | D3 | D4 then activations A1 | A2 | A3.
 constexpr int SD1 = 0, SD2 = 100, SD3 = 150, SD4 = 175, SA1 = 182, SA2 = 282, SA3 = 332;
 constexpr int kScratchRows = 357;
+constexpr int kScratchAlloc = 528;  // floats per sample: the stage images (>= kScratchRows)
+
+// Stage images for the tensor-core weight gradient (train_tc): per 16-sample
+// stage one contiguous block holding that stage's operands exactly as
+// train_wgrad_tc_kernel's shared memory holds them (SWIZZLE_NONE K-major core
+// matrices, 8 rows x 4 samples per 128 bytes): deltas D1..D4 (the A operands,
+// rows padded to 8 with zeros) then x, A1, A2, A3 (the B operands, each followed
+// by its row of ones for the bias column and zero rows up to a multiple of 8).
+// The kernel then moves a stage with eight bulk copies instead of 491 scattered
+// 64-byte row segments.
+namespace wimg {
+constexpr int KS = 16;
+// segment s: 0..3 = D1..D4 (A_0..A_3), 4..7 = x, A1, A2, A3 (B_0..B_3)
+__host__ __device__ constexpr int ROWS(int s) {
+    return s == 0 ? 104 : s == 1 ? 56 : s == 2 ? 32 : s == 3 ? 8 : s == 4 ? 136 : s == 5 ? 104 : s == 6 ? 56 : 32;
+}
+// (closed form, not recursive: it must fold to a constant in device code)
+__host__ __device__ constexpr int OFF(int s) {
+    return KS * (s <= 0 ? 0 : s == 1 ? 104 : s == 2 ? 160 : s == 3 ? 192 : s == 4 ? 200
+                 : s == 5 ? 336 : s == 6 ? 440 : s == 7 ? 496 : 528);
+}
+constexpr int FLOATS = OFF(8);  // 8448 floats = 33,792 bytes per stage
+static_assert(FLOATS == 528 * KS && OFF(5) == OFF(4) + ROWS(4) * KS && OFF(8) == OFF(7) + ROWS(7) * KS,
+              "image size");
+}  // namespace wimg
+
+// Rows [0, R) of one 64-sample tile (smem [R][RS]) -> segment `seg` of the four
+// stage images of the tile; rows [R, R8) are the ones row (bias, `ones`) and zeros.
+// A warp writes one contiguous 512-byte block (8 rows x 4 sample quads of one
+// stage); lane -> (row r & 7, quad (lane / 8 + r) & 3), so a quarter-warp's reads
+// hit 4 distinct bank groups (2-way at most with the 256-byte row stride).
+__device__ __forceinline__ void write_img(const float* sm, int off, int R, bool ones, int seg,
+                                          float* __restrict__ img, int64_t tile) {
+    const int R8 = wimg::ROWS(seg), G = R8 / 8;
+    float* base = img + tile * 4 * wimg::FLOATS + wimg::OFF(seg);
+    const int lane = threadIdx.x & 31, rl = lane & 7, k4 = ((lane >> 3) + rl) & 3;
+    for (int wi = threadIdx.x >> 5; wi < 4 * G; wi += kThreads / 32) {
+        const int st = wi / G, g = wi - st * G, r = g * 8 + rl;
+        float4 v;
+        if (r < R) {
+            v = *reinterpret_cast<const float4*>(sm + off + r * RS + st * 16 + 4 * k4);
+        } else {
+            const float f = (ones && r == R) ? 1.f : 0.f;
+            v = make_float4(f, f, f, f);
+        }
+        reinterpret_cast<float4*>(base + st * wimg::FLOATS)[(g * 4 + k4) * 8 + rl] = v;
+    }
+}
 
 // Forward (forward_trace) and the backward deltas (analytic_gradients' delta
 // recursion) of 64-sample tiles; activations and deltas go to the scratch rows
 // for train_wgrad_kernel, the per-CTA loss sum to loss_partial.
+template <bool IMG>
 __global__ void __launch_bounds__(kThreads, 1)
     train_fb_kernel(const float* __restrict__ master, const float* __restrict__ x,
                     const float* __restrict__ y, int64_t n, int64_t ld,
@@ -377,6 +426,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncthreads();
         // ---- forward (forward_trace) -------------------------------------------------
         dense_l1(sm);
+        if constexpr (IMG) write_img(sm, A0S, 134, true, 4, scr, tile);  // before the prefetch
         __syncthreads();
         const int64_t next = tile + gridDim.x;
         prefetched = next < tiles && xvec && full_tile(next);
@@ -387,9 +437,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncthreads();
         dense<25, 1, 1, false>(sm, W4S, B4S, A3S, OS);
         __syncthreads();
-        write_rows(sm, A1S, 100, scr + SA1 * lds, lds, t0);
-        write_rows(sm, A2S, 50, scr + SA2 * lds, lds, t0);
-        write_rows(sm, A3S, 25, scr + SA3 * lds, lds, t0);
+        if constexpr (IMG) {
+            write_img(sm, A1S, 100, true, 5, scr, tile);
+            write_img(sm, A2S, 50, true, 6, scr, tile);
+            write_img(sm, A3S, 25, true, 7, scr, tile);
+        } else {
+            write_rows(sm, A1S, 100, scr + SA1 * lds, lds, t0);
+            write_rows(sm, A2S, 50, scr + SA2 * lds, lds, t0);
+            write_rows(sm, A3S, 25, scr + SA3 * lds, lds, t0);
+        }
         // ---- residual and loss: delta4 = out - y (dead samples 0) -----------------
         if (tid < TM) {
             float l = 0.f;
@@ -402,26 +458,26 @@ __global__ void __launch_bounds__(kThreads, 1)
             loss += 0.5 * (double)l;
         }
         __syncthreads();
-        write_rows(sm, OS, 7, scr + SD4 * lds, lds, t0);
+        if constexpr (IMG) write_img(sm, OS, 7, false, 3, scr, tile); else write_rows(sm, OS, 7, scr + SD4 * lds, lds, t0);
         // ---- d3 = (W4^T d4) .* a3(1-a3), d2, d1 likewise ------------------------------
         float2 r3[4];
         backprop<25, 4, 7, 4>(sm, T4S, OS, A3S, r3);
         __syncthreads();
         store_delta<25, 4>(sm, A3S, r3);
         __syncthreads();
-        write_rows(sm, A3S, 25, scr + SD3 * lds, lds, t0);
+        if constexpr (IMG) write_img(sm, A3S, 25, false, 2, scr, tile); else write_rows(sm, A3S, 25, scr + SD3 * lds, lds, t0);
         float2 r2[7];
         backprop<50, 7, 25, 8>(sm, T3S, A3S, A2S, r2);
         __syncthreads();
         store_delta<50, 7>(sm, A2S, r2);
         __syncthreads();
-        write_rows(sm, A2S, 50, scr + SD2 * lds, lds, t0);
+        if constexpr (IMG) write_img(sm, A2S, 50, false, 1, scr, tile); else write_rows(sm, A2S, 50, scr + SD2 * lds, lds, t0);
         float2 r1[13];
         backprop<100, 13, 50, 16>(sm, T2S, A2S, A1S, r1);
         __syncthreads();
         store_delta<100, 13>(sm, A1S, r1);
         __syncthreads();
-        write_rows(sm, A1S, 100, scr + SD1 * lds, lds, t0);
+        if constexpr (IMG) write_img(sm, A1S, 100, false, 0, scr, tile); else write_rows(sm, A1S, 100, scr + SD1 * lds, lds, t0);
         __syncthreads();
     }
     // loss: block reduce of the 64 per-sample-thread partials
@@ -449,6 +505,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 // the current chunk's math (register double-buffering).
 constexpr int WG_THREADS = 384;
 constexpr int WG_CHUNK = 32;
+#ifndef DSO_TWG_INFLIGHT
+#define DSO_TWG_INFLIGHT 2
+#endif
 // Record layout: every operand row block of 8 (one thread tile's n or k block)
 // is stored with a 12-float stride, so the 16-byte chunks of consecutive blocks
 // fall in different bank groups (a warp's 17 k blocks read in 3 wavefronts).
@@ -654,7 +713,7 @@ __global__ void __launch_bounds__(WG_THREADS, 1)
 // and four warps read the accumulators out at the end.
 namespace twg {
 constexpr int KS = 16;                      // samples per stage
-constexpr int kLoadWarps = 16, kThreadsWG = (kLoadWarps + 1) * 32;
+constexpr int kLoadWarps = 16, kThreadsWG = (kLoadWarps + 2) * 32;  // + MMA warp + copy warp
 __host__ __device__ constexpr int NOUT(int l) { return l == 0 ? 100 : l == 1 ? 50 : l == 2 ? 25 : 7; }
 __host__ __device__ constexpr int NIN(int l) { return l == 0 ? 134 : l == 1 ? 100 : l == 2 ? 50 : 25; }
 // MMA N per layer (multiple of 16, > NIN for the ones row) and D's TMEM column
@@ -666,8 +725,8 @@ __host__ __device__ constexpr int BREG(int l) { return BOFF + TCOL(l) * KS; }
 constexpr int HALF = BOFF + 352 * KS;         // floats of one hi (or lo) part
 constexpr int STAGE = 2 * HALF;               // hi + lo
 constexpr int SMEM_FLOATS = 2 * STAGE + 16;   // two stages + barriers
-constexpr int ROWS = 491;                     // operand rows loaded per stage
-constexpr int ITEMS = ROWS * (KS / 4);        // float4 items per stage
+constexpr int ITEMS = wimg::FLOATS / 4;       // float4 items per stage image
+static_assert(KS == wimg::KS, "stage image and MMA stage agree");
 constexpr int PER_T = (ITEMS + kLoadWarps * 32 - 1) / (kLoadWarps * 32);
 // master offsets of layer l's weights / biases
 __host__ __device__ constexpr int MWL(int l) { return l == 0 ? MW1 : l == 1 ? MW2 : l == 2 ? MW3 : MW4; }
@@ -676,27 +735,6 @@ __host__ __device__ constexpr int MBL(int l) { return l == 0 ? MB1 : l == 1 ? MB
 // element (r, k) of an [R][KS] K-major core-matrix operand
 __host__ __device__ constexpr int cm_off(int r, int k) {
     return ((r >> 3) * (KS / 4) + (k >> 2)) * 32 + (r & 7) * 4 + (k & 3);
-}
-// operand row r (0..490) of a stage -> (smem float offset of its row in the hi part,
-// global source row, from x?)
-__device__ __forceinline__ void row_map(int r, int& base, int& src, bool& from_x) {
-    from_x = false;
-    if (r < 134) { base = BREG(0) + cm_off(r, 0); src = r; from_x = true; return; }
-    r -= 134;
-    if (r < 100) { base = AOFF + 0 * 128 * KS + cm_off(r, 0); src = SD1 + r; return; }
-    r -= 100;
-    if (r < 100) { base = BREG(1) + cm_off(r, 0); src = SA1 + r; return; }
-    r -= 100;
-    if (r < 50) { base = AOFF + 1 * 128 * KS + cm_off(r, 0); src = SD2 + r; return; }
-    r -= 50;
-    if (r < 50) { base = BREG(2) + cm_off(r, 0); src = SA2 + r; return; }
-    r -= 50;
-    if (r < 25) { base = AOFF + 2 * 128 * KS + cm_off(r, 0); src = SD3 + r; return; }
-    r -= 25;
-    if (r < 25) { base = BREG(3) + cm_off(r, 0); src = SA3 + r; return; }
-    r -= 25;
-    base = AOFF + 3 * 128 * KS + cm_off(r, 0);  // r < 7
-    src = SD4 + r;
 }
 __device__ __forceinline__ void mb_init(uint64_t* b, int count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(tc::smem_addr(b)), "r"(count)
@@ -715,15 +753,25 @@ __device__ __forceinline__ void mb_wait(uint64_t* b, uint32_t parity) {
             : "r"(tc::smem_addr(b)), "r"(parity), "r"(100000u)
             : "memory");
 }
+// the same without a suspend-time hint (the bulk-copy barriers: polled)
+__device__ __forceinline__ void mb_wait_spin(uint64_t* b, uint32_t parity) {
+    uint32_t done = 0;
+    while (!done)
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+            : "=r"(done)
+            : "r"(tc::smem_addr(b)), "r"(parity)
+            : "memory");
+}
 }  // namespace twg
 
 __global__ void __launch_bounds__(twg::kThreadsWG, 1)
-    train_wgrad_tc_kernel(const float* __restrict__ x, int64_t ld, const float* __restrict__ act,
-                          int64_t lds, int64_t n, int64_t per, float* __restrict__ partial) {
+    train_wgrad_tc_kernel(const float* __restrict__ img, int64_t n, int64_t per,
+                          float* __restrict__ partial) {
     using namespace twg;
     extern __shared__ __align__(16) float sm[];
     uint64_t* mb = reinterpret_cast<uint64_t*>(sm + 2 * STAGE);  // FULL[2] EMPTY[2] DONE
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(sm + 2 * STAGE + 10);
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(sm + 2 * STAGE + 14);  // FULL[2] EMPTY[2] DONE LOADED[2]
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int64_t s_lo = (int64_t)blockIdx.x * per, s_hi = min(n, s_lo + per);
     const int stages = s_hi > s_lo ? (int)((s_hi - s_lo + KS - 1) / KS) : 0;
@@ -741,6 +789,8 @@ __global__ void __launch_bounds__(twg::kThreadsWG, 1)
             mb_init(mb + 2 + i, 1);           // EMPTY (MMA commit)
         }
         mb_init(mb + 4, 1);                   // DONE
+        mb_init(mb + 5, 1);                   // LOADED[2] (bulk copies, expect_tx)
+        mb_init(mb + 6, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == kLoadWarps) tc::tmem_alloc<512>(tslot);
@@ -751,55 +801,30 @@ __global__ void __launch_bounds__(twg::kThreadsWG, 1)
     const uint32_t tbase = *tslot;
 
     if (warp < kLoadWarps) {
-        // ---- loaders: each thread's float4 items (row, sample quad) are fixed ----
-        const bool vec = ((ld | lds) & 3) == 0 && ((reinterpret_cast<uintptr_t>(x) |
-                                                    reinterpret_cast<uintptr_t>(act)) & 15) == 0 &&
-                         (s_lo & 3) == 0;
+        // ---- loaders: wait for a stage's bulk copies, then split every float of the
+        // stage image in place into its tf32 hi part and write the lo part --------
         int soff[PER_T];
-        const float* gsrc[PER_T];
-        int qd[PER_T];
 #pragma unroll
         for (int i = 0; i < PER_T; ++i) {
-            const int it = tid + i * kLoadWarps * 32;
-            const int r = it < ITEMS ? it / (KS / 4) : 0;
-            qd[i] = it < ITEMS ? it % (KS / 4) : -1;
-            int base, src;
-            bool fx;
-            row_map(r, base, src, fx);
-            soff[i] = base + qd[i] * 32;  // sample quad q: core matrix k4 = q
-            gsrc[i] = fx ? x + (int64_t)src * ld : act + (int64_t)src * lds;
-        }
-        // a stage's loads are issued one stage ahead (registers), so their latency
-        // overlaps the current stage's split / store and the wait for its buffer
-        auto load = [&](int it, float4 (&v)[PER_T]) {
-            const int64_t s0 = s_lo + (int64_t)it * KS;
+            const int j = tid + i * kLoadWarps * 32;  // float4 of the stage image
+            soff[i] = -1;
+            if (j < wimg::FLOATS / 4) {
+                int sg = 0;
 #pragma unroll
-            for (int i = 0; i < PER_T; ++i) {
-                v[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-                if (qd[i] < 0) continue;
-                const int64_t s = s0 + 4 * qd[i];
-                if (vec && s + 3 < s_hi) {
-                    v[i] = __ldg(reinterpret_cast<const float4*>(gsrc[i] + s));
-                } else {
-                    v[i].x = s < s_hi ? __ldg(gsrc[i] + s) : 0.f;
-                    v[i].y = s + 1 < s_hi ? __ldg(gsrc[i] + s + 1) : 0.f;
-                    v[i].z = s + 2 < s_hi ? __ldg(gsrc[i] + s + 2) : 0.f;
-                    v[i].w = s + 3 < s_hi ? __ldg(gsrc[i] + s + 3) : 0.f;
-                }
+                for (int t = 1; t < 8; ++t) sg = 4 * j >= wimg::OFF(t) ? t : sg;
+                const int base = sg < 4 ? AOFF + sg * 128 * KS : BREG(sg - 4);
+                soff[i] = base + 4 * j - wimg::OFF(sg);
             }
-        };
-        // stage `it` of the split / store; its loads were issued two stages earlier into
-        // the register set of its parity (fixed registers per parity: a rotation through
-        // moves would wait on the newest loads at every step)
-        auto store = [&](int it, const float4 (&cur)[PER_T]) {
+        }
+        for (int it = 0; it < stages; ++it) {
             const int b = it & 1;
-            if (it >= 2) mb_wait(mb + 2 + b, (uint32_t)(((it >> 1) - 1) & 1));
+            mb_wait_spin(mb + 5 + b, (uint32_t)((it >> 1) & 1));
             float* hi = sm + b * STAGE;
             float* lo = hi + HALF;
 #pragma unroll
             for (int i = 0; i < PER_T; ++i) {
-                if (qd[i] < 0) continue;
-                const float4 v = cur[i];
+                if (soff[i] < 0) continue;
+                const float4 v = *reinterpret_cast<const float4*>(hi + soff[i]);
                 const float4 h = make_float4(tc::tf32_hi_finite(v.x), tc::tf32_hi_finite(v.y),
                                              tc::tf32_hi_finite(v.z), tc::tf32_hi_finite(v.w));
                 *reinterpret_cast<float4*>(hi + soff[i]) = h;
@@ -809,22 +834,36 @@ __global__ void __launch_bounds__(twg::kThreadsWG, 1)
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __syncwarp();
             if (lane == 0) mb_arrive(mb + b);
-        };
-        float4 va[PER_T], vb[PER_T];
-        if (stages > 0) load(0, va);
-        if (stages > 1) load(1, vb);
-        for (int it = 0; it < stages; it += 2) {
-            store(it, va);
-            if (it + 2 < stages) load(it + 2, va);
-            if (it + 1 < stages) {
-                store(it + 1, vb);
-                if (it + 3 < stages) load(it + 3, vb);
-            }
         }
         // every loader's stage writes are ordered before the read-out below reuses the
-        // stage memory as its transpose buffer (the mbarrier / commit chain orders them
-        // too, but this makes it explicit to every tool)
+        // stage memory as its transpose buffer
         asm volatile("bar.sync 2, %0;" ::"n"(kLoadWarps * 32) : "memory");
+    } else if (warp == kLoadWarps + 1) {
+        // ---- copy warp: a stage image -> the hi buffer once the MMAs of the stage
+        // two back have released it --------------------------------------------------
+        if (lane == 0) {
+            const int64_t st0 = s_lo / KS;
+            for (int it = 0; it < stages; ++it) {
+                const int b = it & 1;
+                if (it >= 2) mb_wait(mb + 2 + b, (uint32_t)(((it >> 1) - 1) & 1));
+                const uint32_t bar = tc::smem_addr(mb + 5 + b);
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                             "r"((uint32_t)(wimg::FLOATS * 4))
+                             : "memory");
+                const float* src = img + (st0 + it) * wimg::FLOATS;
+                float* hi = sm + b * STAGE;
+#pragma unroll
+                for (int sg = 0; sg < 8; ++sg) {
+                    const int base = sg < 4 ? AOFF + sg * 128 * KS : BREG(sg - 4);
+                    asm volatile(
+                        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                            tc::smem_addr(hi + base)),
+                        "l"(src + wimg::OFF(sg)), "r"((uint32_t)(wimg::ROWS(sg) * KS * 4)), "r"(bar)
+                        : "memory");
+                }
+            }
+        }
     } else if (lane == 0) {
         // ---- MMA issuer ----------------------------------------------------------
         const uint32_t s0 = tc::smem_addr(sm);
@@ -978,7 +1017,7 @@ cudaError_t train_prepare(Ctx& cx, int64_t n) {
     const int parts = cx.num_sms;
     const int64_t lds = ((n + TM - 1) / TM) * TM;
     const size_t need = (size_t)parts * kMasterFloats * sizeof(float) + (size_t)parts * sizeof(double) +
-                        (size_t)kScratchRows * (size_t)(lds > 0 ? lds : TM) * sizeof(float) + 256;
+                        (size_t)kScratchAlloc * (size_t)(lds > 0 ? lds : TM) * sizeof(float) + 256;
     if (cx.train_scratch_bytes < need) {
         cudaFree(cx.train_scratch);
         cx.train_scratch = nullptr;
@@ -992,8 +1031,11 @@ cudaError_t train_prepare(Ctx& cx, int64_t n) {
         if (e != cudaSuccess) return e;
         cx.model.train_dirty = true;
     }
-    cudaError_t e = ensure_smem_attr((const void*)train_fb_kernel, cx.device,
+    cudaError_t e = ensure_smem_attr((const void*)train_fb_kernel<false>, cx.device,
                                      (int)((size_t)kSmemFloats * sizeof(float)));
+    if (e != cudaSuccess) return e;
+    e = ensure_smem_attr((const void*)train_fb_kernel<true>, cx.device,
+                         (int)((size_t)kSmemFloats * sizeof(float)));
     if (e != cudaSuccess) return e;
     return ensure_smem_attr((const void*)train_wgrad_kernel, cx.device,
                             (int)((size_t)2 * WG_CHUNK * WG_REC * sizeof(float)));
@@ -1006,7 +1048,8 @@ cudaError_t launch_train_grad(Ctx& cx, const float* x, const float* y, int64_t n
     const int64_t lds = ((n + TM - 1) / TM) * TM;  // scratch row length (whole tiles)
     const size_t part_b = (size_t)parts * kMasterFloats * sizeof(float);
     const size_t loss_b = (size_t)parts * sizeof(double);
-    const size_t act_b = (size_t)kScratchRows * (size_t)(lds > 0 ? lds : TM) * sizeof(float);
+    // row scratch [357][lds] (FMA-pipe weight gradient) or the stage images (tcgen05)
+    const size_t act_b = (size_t)kScratchAlloc * (size_t)(lds > 0 ? lds : TM) * sizeof(float);
     const size_t need = part_b + loss_b + act_b + 256;
     if (cx.train_scratch_bytes < need) {
         cudaFree(cx.train_scratch);
@@ -1022,7 +1065,9 @@ cudaError_t launch_train_grad(Ctx& cx, const float* x, const float* y, int64_t n
     const size_t smem = (size_t)kSmemFloats * sizeof(float);
     const size_t smem_wg = (size_t)2 * WG_CHUNK * WG_REC * sizeof(float);
     {
-        cudaError_t e = ensure_smem_attr((const void*)train_fb_kernel, cx.device, (int)smem);
+        cudaError_t e = ensure_smem_attr(cx.train_tc ? (const void*)train_fb_kernel<true>
+                                                     : (const void*)train_fb_kernel<false>,
+                                         cx.device, (int)smem);
         if (e != cudaSuccess) return e;
         e = ensure_smem_attr((const void*)train_wgrad_kernel, cx.device, (int)smem_wg);
         if (e != cudaSuccess) return e;
@@ -1043,8 +1088,12 @@ cudaError_t launch_train_grad(Ctx& cx, const float* x, const float* y, int64_t n
         ++cx.launches;
         cx.model.train_dirty = false;
     }
-    train_fb_kernel<<<fb_parts, kThreads, smem, cx.stream>>>(cx.model.w_train, x, y, n, ld, act,
-                                                             lds, lp);
+    if (cx.train_tc)
+        train_fb_kernel<true><<<fb_parts, kThreads, smem, cx.stream>>>(cx.model.w_train, x, y, n,
+                                                                       ld, act, lds, lp);
+    else
+        train_fb_kernel<false><<<fb_parts, kThreads, smem, cx.stream>>>(cx.model.w_train, x, y, n,
+                                                                        ld, act, lds, lp);
     const int64_t chunks = (n + WG_CHUNK - 1) / WG_CHUNK;
     const int wg_parts = (int)std::max<int64_t>(1, std::min<int64_t>(parts, chunks));
     int64_t per = (n + wg_parts - 1) / wg_parts;
@@ -1054,8 +1103,8 @@ cudaError_t launch_train_grad(Ctx& cx, const float* x, const float* y, int64_t n
         const size_t smem_tc = (size_t)twg::SMEM_FLOATS * sizeof(float);
         cudaError_t e = ensure_smem_attr((const void*)train_wgrad_tc_kernel, cx.device, (int)smem_tc);
         if (e != cudaSuccess) return e;
-        train_wgrad_tc_kernel<<<wg_parts, twg::kThreadsWG, smem_tc, cx.stream>>>(x, ld, act, lds, n,
-                                                                             per, partial);
+        train_wgrad_tc_kernel<<<wg_parts, twg::kThreadsWG, smem_tc, cx.stream>>>(act, n, per,
+                                                                             partial);
     } else {
         train_wgrad_kernel<<<wg_parts, WG_THREADS, smem_wg, cx.stream>>>(x, ld, act, lds, n, per,
                                                                          partial);
