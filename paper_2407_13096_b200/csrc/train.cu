@@ -505,9 +505,6 @@ __global__ void __launch_bounds__(kThreads, 1)
 // the current chunk's math (register double-buffering).
 constexpr int WG_THREADS = 384;
 constexpr int WG_CHUNK = 32;
-#ifndef DSO_TWG_INFLIGHT
-#define DSO_TWG_INFLIGHT 2
-#endif
 // Record layout: every operand row block of 8 (one thread tile's n or k block)
 // is stored with a 12-float stride, so the 16-byte chunks of consecutive blocks
 // fall in different bank groups (a warp's 17 k blocks read in 3 wavefronts).
@@ -707,10 +704,11 @@ __global__ void __launch_bounds__(WG_THREADS, 1)
 // inputs (rows = input features, zero-padded to N_l = 144 / 112 / 64 / 32, plus
 // one row of ones whose column gives the bias gradient sum_s delta_l[n][s]).
 // 3xTF32 (hi.hi + hi.lo + lo.hi, FP32 accumulation in TMEM: 352 columns) keeps
-// the FP32 result.  Eight loader warps read a stage's 491 operand rows from the
-// scratch rows train_fb_kernel wrote (and x), split them hi/lo into the SWIZZLE_NONE
-// K-major core-matrix layout (two stage buffers), one thread issues the MMAs,
-// and four warps read the accumulators out at the end.
+// the FP32 result.  A copy warp moves a stage's image (written by
+// train_fb_kernel<true> already in the SWIZZLE_NONE K-major core-matrix layout)
+// into the stage's hi buffer with eight bulk copies; sixteen loader warps split
+// it in place into hi and lo (two stage buffers), one thread issues the MMAs, and
+// four warps read the accumulators out at the end.
 namespace twg {
 constexpr int KS = 16;                      // samples per stage
 constexpr int kLoadWarps = 16, kThreadsWG = (kLoadWarps + 2) * 32;  // + MMA warp + copy warp
