@@ -29,7 +29,7 @@ done
     -o $OUT/prof_pipeline python bench.py --steps 1 --warmup 1 --kernels 2097152 --no-e2e --no-cpu --no-stages --no-extra > $OUT/ncu_full.log 2>&1; echo "rc=$?" >> $OUT/ncu_full.log )
 ( $K 900 ncu --set full --clock-control none --import-source on -k regex:ws_kernel -s 1 -c 1 \
     -o $OUT/prof_pipeline_ffma python bench.py --engine ffma --steps 1 --warmup 1 --kernels 2097152 --no-e2e --no-cpu --no-stages --no-extra > $OUT/ncu_full_ffma.log 2>&1; echo "rc=$?" >> $OUT/ncu_full_ffma.log )
-( $K 600 ncu --set full --clock-control none -k regex:eta_sweep_fast -s 1 -c 1 \
+( $K 600 ncu --set full --clock-control none -k regex:eta_sweep_pruned -s 1 -c 1 \
     -o $OUT/prof_eta python bench.py --config c4 --steps 1 --warmup 1 --kernels 1048576 --no-cpu > $OUT/ncu_eta.log 2>&1; echo "rc=$?" >> $OUT/ncu_eta.log )
 ( $K 600 ncu --set full --clock-control none -k regex:"train_fb|train_wgrad" -s 2 -c 2 \
     -o $OUT/prof_train python bench.py --config c5 --steps 1 --warmup 1 --no-cpu > $OUT/ncu_train.log 2>&1; echo "rc=$?" >> $OUT/ncu_train.log )
