@@ -245,6 +245,79 @@ __device__ __forceinline__ void dense_l1(float* sm) {
     }
 }
 
+// Layer 2 (100 -> 50) with layer 1's register tile (4 samples x 7 neurons per
+// thread, a quarter of the shared-memory loads per FFMA2 of dense<>): eight groups
+// of 7 neurons x 16 sample quads cover 128 threads, so the two halves of the CTA
+// each take half of K; the upper half leaves its partial sums in the output rows,
+// the lower half adds them, the bias and the sigmoid.
+__device__ __forceinline__ void dense_l2_split(float* sm) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int sq = lane & 15, g = (warp & 3) * 2 + (lane >> 4), half = warp >> 2;
+    constexpr int RS4 = RS / 4;
+    const int k0 = half * 50;
+    const float4* a4 = reinterpret_cast<const float4*>(sm + A1S) + sq;
+    const float4* w4 = reinterpret_cast<const float4*>(sm + W2S) + g * 2;  // 16 float4 per k
+    float2 acc0[7], acc1[7];
+#pragma unroll
+    for (int t = 0; t < 7; ++t) acc0[t] = acc1[t] = f2(0.f, 0.f);
+    struct Op {
+        float4 a[2], w0[2], w1[2];
+    };
+    auto load = [&](Op& o, int k) {
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            o.a[u] = a4[(k + u) * RS4];
+            o.w0[u] = w4[(k + u) * 16];
+            o.w1[u] = w4[(k + u) * 16 + 1];
+        }
+    };
+    auto math = [&](const Op& o) {
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const float w[7] = {o.w0[u].x, o.w0[u].y, o.w0[u].z, o.w0[u].w,
+                                o.w1[u].x, o.w1[u].y, o.w1[u].z};
+            const float2 a01 = f2(o.a[u].x, o.a[u].y), a23 = f2(o.a[u].z, o.a[u].w);
+#pragma unroll
+            for (int t = 0; t < 7; ++t) {
+                acc0[t] = ffma2(a01, f2(w[t], w[t]), acc0[t]);
+                acc1[t] = ffma2(a23, f2(w[t], w[t]), acc1[t]);
+            }
+        }
+    };
+    Op A, B;
+    load(A, k0);
+#pragma unroll kL1Unroll
+    for (int k = k0; k < k0 + 48; k += 4) {  // 50 = 12 double stages + one trailing pair
+        load(B, k + 2);
+        math(A);
+        load(A, k + 4);
+        math(B);
+    }
+    math(A);  // k0 + 48, k0 + 49
+    float4* out4 = reinterpret_cast<float4*>(sm + A2S) + sq;
+    if (half == 1) {
+#pragma unroll
+        for (int t = 0; t < 7; ++t)
+            if (7 * g + t < 50)
+                out4[(7 * g + t) * RS4] = make_float4(acc0[t].x, acc0[t].y, acc1[t].x, acc1[t].y);
+    }
+    __syncthreads();
+    if (half == 0) {
+#pragma unroll
+        for (int t = 0; t < 7; ++t) {
+            const int n = 7 * g + t;
+            if (n < 50) {
+                const float4 q = out4[n * RS4];
+                const float bb = sm[B2S + n];
+                out4[n * RS4] = make_float4(sigmoidf_fast(acc0[t].x + q.x + bb),
+                                            sigmoidf_fast(acc0[t].y + q.y + bb),
+                                            sigmoidf_fast(acc1[t].x + q.z + bb),
+                                            sigmoidf_fast(acc1[t].y + q.w + bb));
+            }
+        }
+    }
+}
+
 // delta_l[k][m] = (sum_n W[n][k] delta_{l+1}[n][m]) * a_l[k][m] (1 - a_l[k][m]),
 // thread = (sample pair, group of TK consecutive k); weights read as scalar
 // broadcasts from the packed [K][8][TNP] layout of layer l.  Returns values in
@@ -431,7 +504,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int64_t next = tile + gridDim.x;
         prefetched = next < tiles && xvec && full_tile(next);
         if (prefetched) prefetch_x(next);
+#ifndef DSO_TRAIN_L2_DENSE
+        dense_l2_split(sm);
+#else
         dense<100, 7, 8, true>(sm, W2S, B2S, A1S, A2S);
+#endif
         __syncthreads();
         dense<50, 4, 4, true>(sm, W3S, B3S, A2S, A3S);
         __syncthreads();
