@@ -34,17 +34,35 @@ __global__ void __launch_bounds__(kBlk) dense_nnz_kernel(const uint32_t* __restr
     if (big) *wide = 1;
 }
 
+// Entries of a block of 256 kernels are contiguous in the output: they are
+// gathered in shared memory (thread = kernel, at its row's offset) and written out
+// coalesced — direct per-kernel writes would leave 4-byte pieces of 32 kernels'
+// rows per store instruction (partial sectors).  A block with more than kStage
+// entries writes directly.
+constexpr int kStage = 8192;
 __global__ void __launch_bounds__(kBlk) dense_fill_kernel(const uint32_t* __restrict__ counts,
                                                           int64_t n, int64_t ld,
                                                           const uint64_t* __restrict__ row_ptr,
                                                           uint32_t* __restrict__ entries) {
-    const int64_t k = (int64_t)blockIdx.x * kBlk + threadIdx.x;
-    if (k >= n) return;
-    uint64_t p = row_ptr[k];
+    __shared__ uint32_t s_ent[kStage];
+    const int64_t k0 = (int64_t)blockIdx.x * kBlk, k = k0 + threadIdx.x;
+    const int64_t k1 = k0 + kBlk < n ? k0 + kBlk : n;
+    const uint64_t b0 = row_ptr[k0], b1 = row_ptr[k1];
+    const bool staged = b1 - b0 <= (uint64_t)kStage;
+    if (k < n) {
+        const uint64_t p0 = row_ptr[k];
+        uint32_t* dst = staged ? s_ent : entries + p0;
+        int p = staged ? (int)(p0 - b0) : 0;
 #pragma unroll 14
-    for (int r = 0; r < DSO_COUNT_ROWS; ++r) {
-        const uint32_t v = __ldg(counts + (int64_t)r * ld + k);
-        if (v) entries[p++] = (v << 7) | (uint32_t)r;
+        for (int r = 0; r < DSO_COUNT_ROWS; ++r) {
+            const uint32_t v = __ldg(counts + (int64_t)r * ld + k);
+            if (v) dst[p++] = (v << 7) | (uint32_t)r;
+        }
+    }
+    if (staged) {
+        __syncthreads();
+        const int tot = (int)(b1 - b0);
+        for (int i = threadIdx.x; i < tot; i += kBlk) entries[b0 + i] = s_ent[i];
     }
 }
 
