@@ -1,10 +1,11 @@
 // dense_csr.cu — dense [126][ld] PTX counts -> slot-sorted CSR rows on the device, so
 // dso_pipeline's dense input runs on the tensor-core CSR pipeline (mlp_tc.cuh)
-// instead of the FMA-pipe kernel: one pass counts each kernel's non-zero slots,
-// a device scan turns the counts into row_ptr, a second pass writes the entries
-// ((count << 7) | slot, increasing slot).  Both passes read the counts coalesced
-// (thread = kernel, a row of 32 consecutive kernels per warp load).
-#include <cub/device/device_scan.cuh>
+// instead of the FMA-pipe kernel.  One pass over the counts (thread = kernel, a row
+// of 32 consecutive kernels per warp load): per block of 256 kernels a block scan
+// of the non-zero counts plus a decoupled look-back gives row_ptr, and the entries
+// ((count << 7) | slot, increasing slot) are gathered in shared memory and written
+// out coalesced.
+#include <cub/block/block_scan.cuh>
 
 #include "common.cuh"
 
@@ -13,56 +14,100 @@ namespace {
 
 constexpr int kBlk = 256;
 
-__global__ void __launch_bounds__(kBlk) dense_nnz_kernel(const uint32_t* __restrict__ counts,
-                                                         int64_t n, int64_t ld,
-                                                         uint64_t* __restrict__ nnz,
-                                                         int* __restrict__ wide) {
-    const int64_t k = (int64_t)blockIdx.x * kBlk + threadIdx.x;
-    if (k > n) return;
-    if (k == n) {  // the scan's last element: row_ptr[n] = total
-        nnz[n] = 0;
-        return;
-    }
-    uint32_t c = 0, big = 0;
-#pragma unroll 14
-    for (int r = 0; r < DSO_COUNT_ROWS; ++r) {
-        const uint32_t v = __ldg(counts + (int64_t)r * ld + k);
-        c += v != 0u;
-        big |= v >> 25;
-    }
-    nnz[k] = c;
-    if (big) *wide = 1;
-}
+constexpr int kStage = 8192;  // entries of a block gathered in shared memory
 
-// Entries of a block of 256 kernels are contiguous in the output: they are
-// gathered in shared memory (thread = kernel, at its row's offset) and written out
-// coalesced — direct per-kernel writes would leave 4-byte pieces of 32 kernels'
-// rows per store instruction (partial sectors).  A block with more than kStage
-// entries writes directly.
-constexpr int kStage = 8192;
-__global__ void __launch_bounds__(kBlk) dense_fill_kernel(const uint32_t* __restrict__ counts,
-                                                          int64_t n, int64_t ld,
-                                                          const uint64_t* __restrict__ row_ptr,
-                                                          uint32_t* __restrict__ entries) {
-    __shared__ uint32_t s_ent[kStage];
-    const int64_t k0 = (int64_t)blockIdx.x * kBlk, k = k0 + threadIdx.x;
-    const int64_t k1 = k0 + kBlk < n ? k0 + kBlk : n;
-    const uint64_t b0 = row_ptr[k0], b1 = row_ptr[k1];
-    const bool staged = b1 - b0 <= (uint64_t)kStage;
+// One pass (the default): per block of 256 kernels the counts are read once; each
+// kernel's first kPer entries wait in shared memory while a block scan and a
+// decoupled look-back over the preceding blocks (dynamic block order, so every
+// predecessor is running or done) give the block's offset; then row_ptr and the
+// entries are written (a kernel with more than kPer non-zeros re-reads its
+// column).  status[b]: bits 62-63 = 1 (block aggregate) or 2 (inclusive prefix).
+constexpr int kPer = 24;
+constexpr uint64_t kAgg = 1ull << 62, kPre = 2ull << 62, kVal = (1ull << 62) - 1;
+__global__ void __launch_bounds__(kBlk) dense_csr_fused_kernel(
+    const uint32_t* __restrict__ counts, int64_t n, int64_t ld, uint64_t* __restrict__ row_ptr,
+    uint32_t* __restrict__ entries, uint64_t cap, unsigned long long* __restrict__ status,
+    unsigned int* __restrict__ ticket, int* __restrict__ flags) {
+    using Scan = cub::BlockScan<uint32_t, kBlk>;
+    __shared__ typename Scan::TempStorage s_scan;
+    // s_tmp[j][thread] (pass A) and the block's gathered entries share one buffer
+    __shared__ uint32_t s_buf[kStage];
+    static_assert(kPer * kBlk <= kStage, "staging");
+    auto s_tmp = reinterpret_cast<uint32_t(*)[kBlk]>(s_buf);
+    __shared__ uint64_t s_prefix;
+    __shared__ unsigned int s_bid;
+    const int tid = threadIdx.x;
+    if (tid == 0) s_bid = atomicAdd(ticket, 1u);
+    __syncthreads();
+    const unsigned int bid = s_bid;
+    const int64_t k = (int64_t)bid * kBlk + tid;
+    uint32_t c = 0, big = 0;
     if (k < n) {
-        const uint64_t p0 = row_ptr[k];
-        uint32_t* dst = staged ? s_ent : entries + p0;
-        int p = staged ? (int)(p0 - b0) : 0;
 #pragma unroll 14
         for (int r = 0; r < DSO_COUNT_ROWS; ++r) {
             const uint32_t v = __ldg(counts + (int64_t)r * ld + k);
-            if (v) dst[p++] = (v << 7) | (uint32_t)r;
+            if (v) {
+                if (c < kPer) s_tmp[c][tid] = (v << 7) | (uint32_t)r;
+                ++c;
+            }
+            big |= v >> 25;
+        }
+    }
+    uint32_t excl, agg;
+    Scan(s_scan).ExclusiveSum(c, excl, agg);
+    const int any_big = __syncthreads_or(big != 0u);
+    if (tid == 0) {
+        if (any_big) atomicOr(flags, 1);
+        uint64_t prefix = 0;
+        if (bid == 0) {
+            __threadfence();
+            atomicExch(status, (unsigned long long)(kPre | agg));
+        } else {
+            atomicExch(status + bid, (unsigned long long)(kAgg | agg));
+            for (int64_t j = (int64_t)bid - 1; j >= 0; --j) {
+                uint64_t st;
+                do {
+                    st = atomicAdd(status + j, 0ull);
+                } while ((st >> 62) == 0);
+                prefix += st & kVal;
+                if ((st >> 62) == 2) break;
+            }
+            __threadfence();
+            atomicExch(status + bid, (unsigned long long)(kPre | (prefix + agg)));
+        }
+        s_prefix = prefix;
+    }
+    __syncthreads();
+    const uint64_t base = s_prefix;
+    if (k < n) row_ptr[k] = base + excl;
+    if (k == n - 1) row_ptr[n] = base + excl + c;
+    if (any_big) return;  // the caller runs the dense kernels
+    if (base + agg > cap) {  // the entry buffer is too small: the caller regrows and reruns
+        if (tid == 0) atomicOr(flags, 2);
+        return;
+    }
+    const bool staged = agg <= (uint32_t)kStage;  // block-uniform
+    uint32_t e[kPer];
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) e[j] = (uint32_t)j < c ? s_tmp[j][tid] : 0u;
+    __syncthreads();  // s_tmp is overwritten by the gathered entries below
+    if (k < n) {
+        uint32_t* dst = staged ? s_buf + excl : entries + base + excl;
+        if (c <= (uint32_t)kPer) {
+#pragma unroll
+            for (int j = 0; j < kPer; ++j)
+                if ((uint32_t)j < c) dst[j] = e[j];
+        } else {
+            uint32_t p = 0;
+            for (int r = 0; r < DSO_COUNT_ROWS; ++r) {
+                const uint32_t v = __ldg(counts + (int64_t)r * ld + k);
+                if (v) dst[p++] = (v << 7) | (uint32_t)r;
+            }
         }
     }
     if (staged) {
         __syncthreads();
-        const int tot = (int)(b1 - b0);
-        for (int i = threadIdx.x; i < tot; i += kBlk) entries[b0 + i] = s_ent[i];
+        for (uint32_t i = tid; i < agg; i += kBlk) entries[base + i] = s_buf[i];
     }
 }
 
@@ -77,18 +122,13 @@ cudaError_t launch_pipeline_dense_via_csr(Ctx& cx, const uint32_t* counts, const
         *done = true;
         return cudaSuccess;
     }
-    size_t scan_b = 0;
-    cudaError_t e = cub::DeviceScan::ExclusiveSum(nullptr, scan_b, (uint64_t*)nullptr,
-                                                  (uint64_t*)nullptr, (int64_t)(n + 1), cx.stream);
-    if (e != cudaSuccess) return e;
-    // [nnz (n+1) | row_ptr (n+1) | wide flag | scan temp | entries (grown after the scan)]
+    const int64_t nb = (n + kBlk - 1) / kBlk;
+    // [row_ptr (n+1) | status (nb) | ticket, flags | entries]
     auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
-    const size_t o_rp = al((size_t)(n + 1) * 8), o_flag = o_rp + al((size_t)(n + 1) * 8),
-                 o_tmp = o_flag + 256, o_ent = o_tmp + al(scan_b);
-    bool moved = false;  // set when grow() replaced the allocation
+    const size_t o_st = al((size_t)(n + 1) * 8), o_fl = o_st + al((size_t)nb * 8),
+                 o_ent = o_fl + 256;
     auto grow = [&](size_t need) -> cudaError_t {
         if (cx.dcsr_bytes >= need) return cudaSuccess;
-        moved = true;
         cudaError_t r = cudaStreamSynchronize(cx.stream);
         if (r != cudaSuccess) return r;
         cudaFree(cx.dcsr_scratch);
@@ -99,52 +139,39 @@ cudaError_t launch_pipeline_dense_via_csr(Ctx& cx, const uint32_t* counts, const
         cx.dcsr_bytes = need;
         return cudaSuccess;
     };
-    if ((e = grow(o_ent + (size_t)n * 4 * 32)) != cudaSuccess) return e;  // room for ~32 per kernel
-    char* base = (char*)cx.dcsr_scratch;
-    uint64_t* nnz = (uint64_t*)base;
-    uint64_t* rp = (uint64_t*)(base + o_rp);
-    int* wide = (int*)(base + o_flag);
-    if ((e = cudaMemsetAsync(wide, 0, sizeof(int), cx.stream)) != cudaSuccess) return e;
-    const unsigned blocks = (unsigned)((n + 1 + kBlk - 1) / kBlk);
-    dense_nnz_kernel<<<blocks, kBlk, 0, cx.stream>>>(counts, n, ld, nnz, wide);
-    ++cx.launches;
-    if ((e = cub::DeviceScan::ExclusiveSum(base + o_tmp, scan_b, nnz, rp, (int64_t)(n + 1),
-                                           cx.stream)) != cudaSuccess)
-        return e;
-    ++cx.launches;
-    // the total (row_ptr[n]) and the field check decide the entry buffer / the path
-    struct {
-        uint64_t total;
-        int wide;
-    } h{};
-    if ((e = cudaMemcpyAsync(&h.total, rp + n, 8, cudaMemcpyDeviceToHost, cx.stream)) != cudaSuccess ||
-        (e = cudaMemcpyAsync(&h.wide, wide, 4, cudaMemcpyDeviceToHost, cx.stream)) != cudaSuccess ||
-        (e = cudaStreamSynchronize(cx.stream)) != cudaSuccess)
-        return e;
-    if (h.wide) return cudaSuccess;  // a count >= 2^25: the caller runs the dense kernels
-    moved = false;
-    if ((e = grow(o_ent + (size_t)(h.total + 4) * 4)) != cudaSuccess) return e;
-    base = (char*)cx.dcsr_scratch;
-    nnz = (uint64_t*)base;
-    rp = (uint64_t*)(base + o_rp);
-    wide = (int*)(base + o_flag);
-    if (moved) {
-        // the buffer was regrown: row_ptr lived in the old allocation, recompute it
-        if ((e = cudaMemsetAsync(wide, 0, sizeof(int), cx.stream)) != cudaSuccess) return e;
-        dense_nnz_kernel<<<blocks, kBlk, 0, cx.stream>>>(counts, n, ld, nnz, wide);
-        if ((e = cub::DeviceScan::ExclusiveSum(base + o_tmp, scan_b, nnz, rp, (int64_t)(n + 1),
-                                               cx.stream)) != cudaSuccess)
+    cudaError_t e = grow(o_ent + (size_t)n * 4 * 32);  // room for ~32 entries per kernel
+    if (e != cudaSuccess) return e;
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        char* base = (char*)cx.dcsr_scratch;
+        uint64_t* rp = (uint64_t*)base;
+        unsigned long long* status = (unsigned long long*)(base + o_st);
+        unsigned int* ticket = (unsigned int*)(base + o_fl);
+        int* flags = (int*)(base + o_fl + 16);
+        uint32_t* ent = (uint32_t*)(base + o_ent);
+        const uint64_t cap = (uint64_t)((cx.dcsr_bytes - o_ent) / 4);
+        if ((e = cudaMemsetAsync(base + o_st, 0, o_ent - o_st, cx.stream)) != cudaSuccess) return e;
+        dense_csr_fused_kernel<<<(unsigned)nb, kBlk, 0, cx.stream>>>(counts, n, ld, rp, ent, cap,
+                                                                       status, ticket, flags);
+        ++cx.launches;
+        // the field check and the entry count decide the path / the buffer
+        struct {
+            uint64_t total;
+            int flags;
+        } h{};
+        if ((e = cudaMemcpyAsync(&h.total, rp + n, 8, cudaMemcpyDeviceToHost, cx.stream)) != cudaSuccess ||
+            (e = cudaMemcpyAsync(&h.flags, flags, 4, cudaMemcpyDeviceToHost, cx.stream)) != cudaSuccess ||
+            (e = cudaStreamSynchronize(cx.stream)) != cudaSuccess)
             return e;
-        cx.launches += 2;
+        if (h.flags & 1) return cudaSuccess;  // a count >= 2^25: the caller runs the dense kernels
+        if (h.flags & 2) {                    // more entries than the buffer holds: regrow, rerun
+            if ((e = grow(o_ent + (size_t)(h.total + 4) * 4)) != cudaSuccess) return e;
+            continue;
+        }
+        *done = true;
+        return launch_pipeline_csr(cx, rp, ent, 0, dcgm, n, ld, eta, K, params, clamped, idx,
+                                   cost, energy, time, ld);
     }
-    uint32_t* ent = (uint32_t*)(base + o_ent);
-    dense_fill_kernel<<<(unsigned)((n + kBlk - 1) / kBlk), kBlk, 0, cx.stream>>>(counts, n, ld, rp,
-                                                                                 ent);
-    ++cx.launches;
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    *done = true;
-    return launch_pipeline_csr(cx, rp, ent, 0, dcgm, n, ld, eta, K, params, clamped, idx, cost,
-                               energy, time, ld);
+    return cudaErrorUnknown;  // unreachable: the second pass has room for every entry
 }
 
 }  // namespace dso_b200
