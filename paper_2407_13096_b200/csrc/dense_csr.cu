@@ -14,6 +14,9 @@ namespace {
 
 constexpr int kBlk = 256;
 
+#ifndef DSO_DCSR_MINB
+#define DSO_DCSR_MINB 6
+#endif
 constexpr int kStage = 8192;  // entries of a block gathered in shared memory
 
 // One pass (the default): per block of 256 kernels the counts are read once; each
@@ -24,7 +27,7 @@ constexpr int kStage = 8192;  // entries of a block gathered in shared memory
 // column).  status[b]: bits 62-63 = 1 (block aggregate) or 2 (inclusive prefix).
 constexpr int kPer = 24;
 constexpr uint64_t kAgg = 1ull << 62, kPre = 2ull << 62, kVal = (1ull << 62) - 1;
-__global__ void __launch_bounds__(kBlk) dense_csr_fused_kernel(
+__global__ void __launch_bounds__(kBlk, DSO_DCSR_MINB) dense_csr_fused_kernel(
     const uint32_t* __restrict__ counts, int64_t n, int64_t ld, uint64_t* __restrict__ row_ptr,
     uint32_t* __restrict__ entries, uint64_t cap, unsigned long long* __restrict__ status,
     unsigned int* __restrict__ ticket, int* __restrict__ flags) {
