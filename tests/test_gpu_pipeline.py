@@ -449,3 +449,38 @@ def test_pipeline_csr_realistic_mix_vs_oracle(ctx, port):
                      0.8, want_params=True)
     for f in ("idx", "cost", "energy", "time", "params", "clamped"):
         np.testing.assert_array_equal(a[f].cpu().numpy(), out[f].cpu().numpy())
+
+
+def test_dense_csr_regrow_and_many_blocks(port):
+    """The one-pass dense -> CSR compaction on a fresh context: rows denser than
+    the first entry-buffer guess (~32 per kernel) make it regrow and rerun, and
+    a 300k-kernel stream spans ~1,200 look-back blocks; both equal pipeline_csr
+    on the same kernels bit for bit."""
+    from paper_2407_13096_b200.api import Context
+    c = Context(0)
+    try:
+        c.set_domain(config_domain("c3"))
+        c.set_model(stats_model(port))
+        rng = np.random.default_rng(5)
+        m = 3000 + 11
+        counts = np.zeros((m, 126), np.uint32)
+        for k in range(m):
+            nnz = int(rng.integers(90, 127))
+            counts[k, rng.choice(126, size=nnz, replace=False)] = rng.integers(1, 1 << 24, size=nnz)
+        dcgm = torch.from_numpy(np.ascontiguousarray(rng.uniform(0, 1, (8, m)).astype(np.float32))).cuda()
+        ct = torch.from_numpy(np.ascontiguousarray(counts.T).view(np.int32)).cuda()
+        a = c.pipeline(ct, dcgm, 0.3, want_params=True)
+        rp, ent = csr_from_dense(counts)
+        b = c.pipeline_csr(torch.from_numpy(rp).cuda(), torch.from_numpy(ent.view(np.int32)).cuda(),
+                           dcgm, 0.3, want_params=True)
+        for f in ("idx", "cost", "energy", "time", "params", "clamped"):
+            np.testing.assert_array_equal(a[f].cpu().numpy(), b[f].cpu().numpy())
+        n = 300_000 + 5
+        d = c.gen_synthetic(n, root=77, params=False)
+        s = c.gen_synthetic_csr(n, root=77)
+        a = c.pipeline(d["counts"], d["dcgm"], 0.8, want_params=True)
+        b = c.pipeline_csr(s["row_ptr"], s["entries"], s["dcgm"], 0.8, want_params=True)
+        for f in ("idx", "cost", "params"):
+            np.testing.assert_array_equal(a[f].cpu().numpy(), b[f].cpu().numpy())
+    finally:
+        c.close()
