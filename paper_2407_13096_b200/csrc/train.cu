@@ -799,7 +799,10 @@ constexpr int AOFF = 0, BOFF = 4 * 128 * KS;
 __host__ __device__ constexpr int BREG(int l) { return BOFF + TCOL(l) * KS; }
 constexpr int HALF = BOFF + 352 * KS;         // floats of one hi (or lo) part
 constexpr int STAGE = 2 * HALF;               // hi + lo
-constexpr int SMEM_FLOATS = 2 * STAGE + 16;   // two stages + barriers
+constexpr int NRAW = 3;                       // raw landing buffers (stage images)
+constexpr int RAW = STAGE;                    // float offset of raw buffer 0
+constexpr int MBF = RAW + NRAW * wimg::FLOATS;  // barriers
+constexpr int SMEM_FLOATS = MBF + 32;         // one hi/lo stage + 3 raw images + barriers
 constexpr int ITEMS = wimg::FLOATS / 4;       // float4 items per stage image
 static_assert(KS == wimg::KS, "stage image and MMA stage agree");
 constexpr int PER_T = (ITEMS + kLoadWarps * 32 - 1) / (kLoadWarps * 32);
@@ -845,27 +848,23 @@ __global__ void __launch_bounds__(twg::kThreadsWG, 1)
                           float* __restrict__ partial) {
     using namespace twg;
     extern __shared__ __align__(16) float sm[];
-    uint64_t* mb = reinterpret_cast<uint64_t*>(sm + 2 * STAGE);  // FULL[2] EMPTY[2] DONE
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(sm + 2 * STAGE + 14);  // FULL[2] EMPTY[2] DONE LOADED[2]
+    // barriers: FULL, EMPTY (MMA commit), DONE, LOADED[3] (bulk copies), RFREE[3]
+    uint64_t* mb = reinterpret_cast<uint64_t*>(sm + MBF);
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(sm + MBF + 20);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int64_t s_lo = (int64_t)blockIdx.x * per, s_hi = min(n, s_lo + per);
     const int stages = s_hi > s_lo ? (int)((s_hi - s_lo + KS - 1) / KS) : 0;
-    // zero both stages (padding rows stay zero), then the ones rows (bias columns)
-    for (int i = tid; i < 2 * STAGE / 4; i += kThreadsWG)
+    // zero the hi/lo stage (padding rows stay zero; the images carry the ones rows)
+    for (int i = tid; i < STAGE / 4; i += kThreadsWG)
         reinterpret_cast<float4*>(sm)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-    __syncthreads();
-    for (int i = tid; i < 2 * 4 * KS; i += kThreadsWG) {
-        const int st = i / (4 * KS), l = (i / KS) & 3, k = i % KS;
-        sm[st * STAGE + BREG(l) + cm_off(NIN(l), k)] = 1.0f;  // hi = 1, lo = 0
-    }
     if (tid == 0) {
-        for (int i = 0; i < 2; ++i) {
-            mb_init(mb + i, kLoadWarps);      // FULL
-            mb_init(mb + 2 + i, 1);           // EMPTY (MMA commit)
+        mb_init(mb + 0, kLoadWarps);  // FULL
+        mb_init(mb + 1, 1);           // EMPTY
+        mb_init(mb + 2, 1);           // DONE
+        for (int i = 0; i < NRAW; ++i) {
+            mb_init(mb + 3 + i, 1);            // LOADED[i] (expect_tx)
+            mb_init(mb + 6 + i, kLoadWarps);   // RFREE[i]
         }
-        mb_init(mb + 4, 1);                   // DONE
-        mb_init(mb + 5, 1);                   // LOADED[2] (bulk copies, expect_tx)
-        mb_init(mb + 6, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == kLoadWarps) tc::tmem_alloc<512>(tslot);
@@ -876,8 +875,8 @@ __global__ void __launch_bounds__(twg::kThreadsWG, 1)
     const uint32_t tbase = *tslot;
 
     if (warp < kLoadWarps) {
-        // ---- loaders: wait for a stage's bulk copies, then split every float of the
-        // stage image in place into its tf32 hi part and write the lo part --------
+        // ---- loaders: raw stage image -> the hi/lo stage (once the MMAs of the
+        // previous stage are done with it), then the raw buffer is free again ------
         int soff[PER_T];
 #pragma unroll
         for (int i = 0; i < PER_T; ++i) {
@@ -891,82 +890,82 @@ __global__ void __launch_bounds__(twg::kThreadsWG, 1)
                 soff[i] = base + 4 * j - wimg::OFF(sg);
             }
         }
+        float* hi = sm;
+        float* lo = sm + HALF;
         for (int it = 0; it < stages; ++it) {
-            const int b = it & 1;
-            mb_wait_spin(mb + 5 + b, (uint32_t)((it >> 1) & 1));
-            float* hi = sm + b * STAGE;
-            float* lo = hi + HALF;
+            const int rb = it % NRAW;
+            mb_wait_spin(mb + 3 + rb, (uint32_t)((it / NRAW) & 1));
+            const float* raw = sm + RAW + rb * wimg::FLOATS;
+            float4 v[PER_T];
+#pragma unroll
+            for (int i = 0; i < PER_T; ++i)
+                if (soff[i] >= 0)
+                    v[i] = reinterpret_cast<const float4*>(raw)[tid + i * kLoadWarps * 32];
+            __syncwarp();
+            if (lane == 0) mb_arrive(mb + 6 + rb);  // raw buffer consumed
+            if (it > 0) mb_wait_spin(mb + 1, (uint32_t)((it - 1) & 1));  // MMAs of it-1 done
 #pragma unroll
             for (int i = 0; i < PER_T; ++i) {
                 if (soff[i] < 0) continue;
-                const float4 v = *reinterpret_cast<const float4*>(hi + soff[i]);
-                const float4 h = make_float4(tc::tf32_hi_finite(v.x), tc::tf32_hi_finite(v.y),
-                                             tc::tf32_hi_finite(v.z), tc::tf32_hi_finite(v.w));
+                const float4 h = make_float4(tc::tf32_hi_finite(v[i].x), tc::tf32_hi_finite(v[i].y),
+                                             tc::tf32_hi_finite(v[i].z), tc::tf32_hi_finite(v[i].w));
                 *reinterpret_cast<float4*>(hi + soff[i]) = h;
                 *reinterpret_cast<float4*>(lo + soff[i]) =
-                    make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
+                    make_float4(v[i].x - h.x, v[i].y - h.y, v[i].z - h.z, v[i].w - h.w);
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __syncwarp();
-            if (lane == 0) mb_arrive(mb + b);
+            if (lane == 0) mb_arrive(mb + 0);
         }
         // every loader's stage writes are ordered before the read-out below reuses the
         // stage memory as its transpose buffer
         asm volatile("bar.sync 2, %0;" ::"n"(kLoadWarps * 32) : "memory");
     } else if (warp == kLoadWarps + 1) {
-        // ---- copy warp: a stage image -> the hi buffer once the MMAs of the stage
-        // two back have released it --------------------------------------------------
+        // ---- copy warp: stage images into the raw buffers, NRAW stages ahead ------
         if (lane == 0) {
             const int64_t st0 = s_lo / KS;
             for (int it = 0; it < stages; ++it) {
-                const int b = it & 1;
-                if (it >= 2) mb_wait(mb + 2 + b, (uint32_t)(((it >> 1) - 1) & 1));
-                const uint32_t bar = tc::smem_addr(mb + 5 + b);
+                const int rb = it % NRAW;
+                if (it >= NRAW) mb_wait(mb + 6 + rb, (uint32_t)(((it / NRAW) - 1) & 1));
+                const uint32_t bar = tc::smem_addr(mb + 3 + rb);
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
                              "r"((uint32_t)(wimg::FLOATS * 4))
                              : "memory");
-                const float* src = img + (st0 + it) * wimg::FLOATS;
-                float* hi = sm + b * STAGE;
-#pragma unroll
-                for (int sg = 0; sg < 8; ++sg) {
-                    const int base = sg < 4 ? AOFF + sg * 128 * KS : BREG(sg - 4);
-                    asm volatile(
-                        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                            tc::smem_addr(hi + base)),
-                        "l"(src + wimg::OFF(sg)), "r"((uint32_t)(wimg::ROWS(sg) * KS * 4)), "r"(bar)
-                        : "memory");
-                }
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                        tc::smem_addr(sm + RAW + rb * wimg::FLOATS)),
+                    "l"(img + (st0 + it) * wimg::FLOATS), "r"((uint32_t)(wimg::FLOATS * 4)), "r"(bar)
+                    : "memory");
             }
         }
     } else if (lane == 0) {
         // ---- MMA issuer ----------------------------------------------------------
         const uint32_t s0 = tc::smem_addr(sm);
+        // the hi/lo stage is fixed: every operand descriptor is a base descriptor plus a
+        // compile-time offset in its 16-byte address field (no carry: smem < 256 KB)
+        const uint64_t dh = tc::sdesc(s0, 128, (KS / 4) * 128),
+                       dl = tc::sdesc(s0 + HALF * 4, 128, (KS / 4) * 128);
         for (int it = 0; it < stages; ++it) {
-            const int b = it & 1;
-            mb_wait(mb + b, (uint32_t)((it >> 1) & 1));
+            mb_wait_spin(mb + 0, (uint32_t)(it & 1));
             tc::fence_after();
-            const uint32_t hi = s0 + (uint32_t)(b * STAGE) * 4, lo = hi + HALF * 4;
 #pragma unroll
             for (int l = 0; l < 4; ++l) {
                 const uint32_t id = tc::idesc_tf32(128, NPAD(l));
                 const uint32_t d = tbase + (uint32_t)TCOL(l);
 #pragma unroll
                 for (int kk = 0; kk < KS / 8; ++kk) {
-                    const uint32_t ao = (uint32_t)(AOFF + l * 128 * KS) * 4 + kk * 256,
-                                   bo = (uint32_t)BREG(l) * 4 + kk * 256;
-                    const uint64_t ah = tc::sdesc(hi + ao, 128, (KS / 4) * 128),
-                                   al = tc::sdesc(lo + ao, 128, (KS / 4) * 128),
-                                   bh = tc::sdesc(hi + bo, 128, (KS / 4) * 128),
-                                   bl = tc::sdesc(lo + bo, 128, (KS / 4) * 128);
+                    const uint64_t ao = (uint64_t)(((AOFF + l * 128 * KS) * 4 + kk * 256) >> 4),
+                                   bo = (uint64_t)((BREG(l) * 4 + kk * 256) >> 4);
+                    const uint64_t ah = dh + ao, al = dl + ao, bh = dh + bo, bl = dl + bo;
                     tc::mma_tf32_ss(d, ah, bh, id, (it > 0 || kk > 0) ? 1u : 0u);
                     tc::mma_tf32_ss(d, ah, bl, id, 1u);
                     tc::mma_tf32_ss(d, al, bh, id, 1u);
                 }
             }
-            tc::commit(mb + 2 + b);
+            tc::commit(mb + 1);  // EMPTY: the hi/lo stage may be rewritten
         }
-        tc::commit(mb + 4);
+        tc::commit(mb + 2);      // DONE
     }
     __syncwarp();
     // ---- accumulators -> this CTA's partial gradient (master layout) ------------
@@ -977,7 +976,7 @@ __global__ void __launch_bounds__(twg::kThreadsWG, 1)
         float* out = partial + (int64_t)blockIdx.x * kMasterFloats;
         const int row = 32 * warp + lane;  // output neuron
         if (stages > 0) {
-            mb_wait(mb + 4, 0);
+            mb_wait(mb + 2, 0);
             tc::fence_after();
         }
         float* tr = sm;
