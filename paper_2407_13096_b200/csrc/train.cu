@@ -384,51 +384,49 @@ __device__ __forceinline__ void write_rows(const float* sm, int off, int R, floa
 // deltas D1 | D2 | D3 | D4 then activations A1 | A2 | A3.
 constexpr int SD1 = 0, SD2 = 100, SD3 = 150, SD4 = 175, SA1 = 182, SA2 = 282, SA3 = 332;
 constexpr int kScratchRows = 357;
-constexpr int kScratchAlloc = 528;  // floats per sample: the stage images (>= kScratchRows)
+constexpr int kScratchAlloc = 504;  // floats per sample: the stage images (>= kScratchRows)
 
 // Stage images for the tensor-core weight gradient (train_tc): per 16-sample
 // stage one contiguous block holding that stage's operands exactly as
 // train_wgrad_tc_kernel's shared memory holds them (SWIZZLE_NONE K-major core
-// matrices, 8 rows x 4 samples per 128 bytes): deltas D1..D4 (the A operands,
-// rows padded to 8 with zeros) then x, A1, A2, A3 (the B operands, each followed
-// by its row of ones for the bias column and zero rows up to a multiple of 8).
-// The kernel then moves a stage with eight bulk copies instead of 491 scattered
-// 64-byte row segments.
+// matrices, 8 rows x 4 samples per 128 bytes).  Layers 2-4 share one MMA chain:
+// their deltas are stacked into one A operand (rows d2 0-49 | d3 50-74 | d4 75-81)
+// and their inputs into one B operand (rows a1 0-99 | a2 100-149 | a3 150-174 |
+// ones 175), so D = A B^T holds the three weight gradients as diagonal blocks and
+// the bias gradients in the ones column (the off-diagonal blocks are not used).
+// Segments: 0 = d1 (A of layer 1, 104 rows), 1 = stacked deltas (88 rows),
+// 2 = x + ones row (136 rows), 3 = stacked inputs + ones row (176 rows).
+// The kernel moves a stage with one bulk copy.
 namespace wimg {
 constexpr int KS = 16;
-// segment s: 0..3 = D1..D4 (A_0..A_3), 4..7 = x, A1, A2, A3 (B_0..B_3)
 __host__ __device__ constexpr int ROWS(int s) {
-    return s == 0 ? 104 : s == 1 ? 56 : s == 2 ? 32 : s == 3 ? 8 : s == 4 ? 136 : s == 5 ? 104 : s == 6 ? 56 : 32;
+    return s == 0 ? 104 : s == 1 ? 88 : s == 2 ? 136 : 176;
 }
 // (closed form, not recursive: it must fold to a constant in device code)
 __host__ __device__ constexpr int OFF(int s) {
-    return KS * (s <= 0 ? 0 : s == 1 ? 104 : s == 2 ? 160 : s == 3 ? 192 : s == 4 ? 200
-                 : s == 5 ? 336 : s == 6 ? 440 : s == 7 ? 496 : 528);
+    return KS * (s <= 0 ? 0 : s == 1 ? 104 : s == 2 ? 192 : s == 3 ? 328 : 504);
 }
-constexpr int FLOATS = OFF(8);  // 8448 floats = 33,792 bytes per stage
-static_assert(FLOATS == 528 * KS && OFF(5) == OFF(4) + ROWS(4) * KS && OFF(8) == OFF(7) + ROWS(7) * KS,
-              "image size");
+constexpr int FLOATS = OFF(4);  // 8064 floats = 32,256 bytes per stage
+static_assert(OFF(4) == OFF(3) + ROWS(3) * KS && OFF(3) == OFF(2) + ROWS(2) * KS &&
+                  OFF(2) == OFF(1) + ROWS(1) * KS, "image size");
 }  // namespace wimg
 
-// Rows [0, R) of one 64-sample tile (smem [R][RS]) -> segment `seg` of the four
-// stage images of the tile; rows [R, R8) are the ones row (bias, `ones`) and zeros.
-// A warp writes one contiguous 512-byte block (8 rows x 4 sample quads of one
-// stage); lane -> (row r & 7, quad (lane / 8 + r) & 3), so a quarter-warp's reads
-// hit 4 distinct bank groups (2-way at most with the 256-byte row stride).
-__device__ __forceinline__ void write_img(const float* sm, int off, int R, bool ones, int seg,
-                                          float* __restrict__ img, int64_t tile) {
-    const int R8 = wimg::ROWS(seg), G = R8 / 8;
+// Rows [lo, hi) of segment `seg` in the four stage images of one 64-sample tile:
+// row r takes smem row r - lo of [..][RS] at `off` (off < 0: the constant `fill`).
+// A warp writes one 512-byte block (8 rows x 4 sample quads of one stage) at a time;
+// lane -> (row r & 7, quad (lane / 8 + r) & 3), so a quarter-warp's reads hit 4
+// distinct bank groups (2-way at most with the 256-byte row stride).
+__device__ __forceinline__ void write_img(const float* sm, int off, int lo, int hi, float fill,
+                                          int seg, float* __restrict__ img, int64_t tile) {
+    const int g0 = lo >> 3, G = ((hi + 7) >> 3) - g0;
     float* base = img + tile * 4 * wimg::FLOATS + wimg::OFF(seg);
     const int lane = threadIdx.x & 31, rl = lane & 7, k4 = ((lane >> 3) + rl) & 3;
     for (int wi = threadIdx.x >> 5; wi < 4 * G; wi += kThreads / 32) {
-        const int st = wi / G, g = wi - st * G, r = g * 8 + rl;
-        float4 v;
-        if (r < R) {
-            v = *reinterpret_cast<const float4*>(sm + off + r * RS + st * 16 + 4 * k4);
-        } else {
-            const float f = (ones && r == R) ? 1.f : 0.f;
-            v = make_float4(f, f, f, f);
-        }
+        const int st = wi / G, g = g0 + wi - st * G, r = g * 8 + rl;
+        if (r < lo || r >= hi) continue;
+        const float4 v = off >= 0
+                             ? *reinterpret_cast<const float4*>(sm + off + (r - lo) * RS + st * 16 + 4 * k4)
+                             : make_float4(fill, fill, fill, fill);
         reinterpret_cast<float4*>(base + st * wimg::FLOATS)[(g * 4 + k4) * 8 + rl] = v;
     }
 }
@@ -499,7 +497,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncthreads();
         // ---- forward (forward_trace) -------------------------------------------------
         dense_l1(sm);
-        if constexpr (IMG) write_img(sm, A0S, 134, true, 4, scr, tile);  // before the prefetch
+        if constexpr (IMG) {  // x + ones row + zero row, before the prefetch overwrites A0
+            write_img(sm, A0S, 0, 134, 0.f, 2, scr, tile);
+            write_img(sm, -1, 134, 135, 1.f, 2, scr, tile);
+            write_img(sm, -1, 135, 136, 0.f, 2, scr, tile);
+        }
         __syncthreads();
         const int64_t next = tile + gridDim.x;
         prefetched = next < tiles && xvec && full_tile(next);
@@ -515,9 +517,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         dense<25, 1, 1, false>(sm, W4S, B4S, A3S, OS);
         __syncthreads();
         if constexpr (IMG) {
-            write_img(sm, A1S, 100, true, 5, scr, tile);
-            write_img(sm, A2S, 50, true, 6, scr, tile);
-            write_img(sm, A3S, 25, true, 7, scr, tile);
+            write_img(sm, A1S, 0, 100, 0.f, 3, scr, tile);
+            write_img(sm, A2S, 100, 150, 0.f, 3, scr, tile);
+            write_img(sm, A3S, 150, 175, 0.f, 3, scr, tile);
+            write_img(sm, -1, 175, 176, 1.f, 3, scr, tile);
         } else {
             write_rows(sm, A1S, 100, scr + SA1 * lds, lds, t0);
             write_rows(sm, A2S, 50, scr + SA2 * lds, lds, t0);
@@ -535,26 +538,26 @@ __global__ void __launch_bounds__(kThreads, 1)
             loss += 0.5 * (double)l;
         }
         __syncthreads();
-        if constexpr (IMG) write_img(sm, OS, 7, false, 3, scr, tile); else write_rows(sm, OS, 7, scr + SD4 * lds, lds, t0);
+        if constexpr (IMG) { write_img(sm, OS, 75, 82, 0.f, 1, scr, tile); write_img(sm, -1, 82, 88, 0.f, 1, scr, tile); } else write_rows(sm, OS, 7, scr + SD4 * lds, lds, t0);
         // ---- d3 = (W4^T d4) .* a3(1-a3), d2, d1 likewise ------------------------------
         float2 r3[4];
         backprop<25, 4, 7, 4>(sm, T4S, OS, A3S, r3);
         __syncthreads();
         store_delta<25, 4>(sm, A3S, r3);
         __syncthreads();
-        if constexpr (IMG) write_img(sm, A3S, 25, false, 2, scr, tile); else write_rows(sm, A3S, 25, scr + SD3 * lds, lds, t0);
+        if constexpr (IMG) write_img(sm, A3S, 50, 75, 0.f, 1, scr, tile); else write_rows(sm, A3S, 25, scr + SD3 * lds, lds, t0);
         float2 r2[7];
         backprop<50, 7, 25, 8>(sm, T3S, A3S, A2S, r2);
         __syncthreads();
         store_delta<50, 7>(sm, A2S, r2);
         __syncthreads();
-        if constexpr (IMG) write_img(sm, A2S, 50, false, 1, scr, tile); else write_rows(sm, A2S, 50, scr + SD2 * lds, lds, t0);
+        if constexpr (IMG) write_img(sm, A2S, 0, 50, 0.f, 1, scr, tile); else write_rows(sm, A2S, 50, scr + SD2 * lds, lds, t0);
         float2 r1[13];
         backprop<100, 13, 50, 16>(sm, T2S, A2S, A1S, r1);
         __syncthreads();
         store_delta<100, 13>(sm, A1S, r1);
         __syncthreads();
-        if constexpr (IMG) write_img(sm, A1S, 100, false, 0, scr, tile); else write_rows(sm, A1S, 100, scr + SD1 * lds, lds, t0);
+        if constexpr (IMG) { write_img(sm, A1S, 0, 100, 0.f, 0, scr, tile); write_img(sm, -1, 100, 104, 0.f, 0, scr, tile); } else write_rows(sm, A1S, 100, scr + SD1 * lds, lds, t0);
         __syncthreads();
     }
     // loss: block reduce of the 64 per-sample-thread partials
@@ -789,15 +792,18 @@ __global__ void __launch_bounds__(WG_THREADS, 1)
 namespace twg {
 constexpr int KS = 16;                      // samples per stage
 constexpr int kLoadWarps = 16, kThreadsWG = (kLoadWarps + 2) * 32;  // + MMA warp + copy warp
-__host__ __device__ constexpr int NOUT(int l) { return l == 0 ? 100 : l == 1 ? 50 : l == 2 ? 25 : 7; }
-__host__ __device__ constexpr int NIN(int l) { return l == 0 ? 134 : l == 1 ? 100 : l == 2 ? 50 : 25; }
-// MMA N per layer (multiple of 16, > NIN for the ones row) and D's TMEM column
-__host__ __device__ constexpr int NPAD(int l) { return l == 0 ? 144 : l == 1 ? 112 : l == 2 ? 64 : 32; }
-__host__ __device__ constexpr int TCOL(int l) { return l == 0 ? 0 : l == 1 ? 144 : l == 2 ? 256 : 320; }
-// stage layout (floats): A_l [128][KS] at 2048 l, then B_1..B_4; hi part, then lo part
-constexpr int AOFF = 0, BOFF = 4 * 128 * KS;
-__host__ __device__ constexpr int BREG(int l) { return BOFF + TCOL(l) * KS; }
-constexpr int HALF = BOFF + 352 * KS;         // floats of one hi (or lo) part
+// two MMA chains: c = 0 is layer 1 (A = d1, B = x + ones), c = 1 the stacked
+// layers 2-4 (A = d2|d3|d4, B = a1|a2|a3 + ones); N (multiple of 16, ones row
+// included) and D's TMEM column per chain
+__host__ __device__ constexpr int NPADC(int c) { return c == 0 ? 144 : 176; }
+__host__ __device__ constexpr int TCOLC(int c) { return c == 0 ? 0 : 144; }
+// stage layout (floats): A_c [128][KS] at 2048 c, then B_0, B_1; hi part, then lo part
+constexpr int BOFF = 2 * 128 * KS;
+__host__ __device__ constexpr int AOFFC(int c) { return c * 128 * KS; }
+__host__ __device__ constexpr int BREG(int c) { return BOFF + TCOLC(c) * KS; }
+// shared-memory base of image segment s (wimg: d1, stacked deltas, x, stacked inputs)
+__host__ __device__ constexpr int SEGBASE(int s) { return s < 2 ? AOFFC(s) : BREG(s - 2); }
+constexpr int HALF = BOFF + 320 * KS;         // floats of one hi (or lo) part
 constexpr int STAGE = 2 * HALF;               // hi + lo
 constexpr int NRAW = 3;                       // raw landing buffers (stage images)
 constexpr int RAW = STAGE;                    // float offset of raw buffer 0
@@ -806,9 +812,6 @@ constexpr int SMEM_FLOATS = MBF + 32;         // one hi/lo stage + 3 raw images 
 constexpr int ITEMS = wimg::FLOATS / 4;       // float4 items per stage image
 static_assert(KS == wimg::KS, "stage image and MMA stage agree");
 constexpr int PER_T = (ITEMS + kLoadWarps * 32 - 1) / (kLoadWarps * 32);
-// master offsets of layer l's weights / biases
-__host__ __device__ constexpr int MWL(int l) { return l == 0 ? MW1 : l == 1 ? MW2 : l == 2 ? MW3 : MW4; }
-__host__ __device__ constexpr int MBL(int l) { return l == 0 ? MB1 : l == 1 ? MB2 : l == 2 ? MB3 : MB4; }
 
 // element (r, k) of an [R][KS] K-major core-matrix operand
 __host__ __device__ constexpr int cm_off(int r, int k) {
@@ -885,9 +888,8 @@ __global__ void __launch_bounds__(twg::kThreadsWG, 1)
             if (j < wimg::FLOATS / 4) {
                 int sg = 0;
 #pragma unroll
-                for (int t = 1; t < 8; ++t) sg = 4 * j >= wimg::OFF(t) ? t : sg;
-                const int base = sg < 4 ? AOFF + sg * 128 * KS : BREG(sg - 4);
-                soff[i] = base + 4 * j - wimg::OFF(sg);
+                for (int t = 1; t < 4; ++t) sg = 4 * j >= wimg::OFF(t) ? t : sg;
+                soff[i] = SEGBASE(sg) + 4 * j - wimg::OFF(sg);
             }
         }
         float* hi = sm;
@@ -950,12 +952,12 @@ __global__ void __launch_bounds__(twg::kThreadsWG, 1)
             mb_wait_spin(mb + 0, (uint32_t)(it & 1));
             tc::fence_after();
 #pragma unroll
-            for (int l = 0; l < 4; ++l) {
-                const uint32_t id = tc::idesc_tf32(128, NPAD(l));
-                const uint32_t d = tbase + (uint32_t)TCOL(l);
+            for (int l = 0; l < 2; ++l) {
+                const uint32_t id = tc::idesc_tf32(128, NPADC(l));
+                const uint32_t d = tbase + (uint32_t)TCOLC(l);
 #pragma unroll
                 for (int kk = 0; kk < KS / 8; ++kk) {
-                    const uint64_t ao = (uint64_t)(((AOFF + l * 128 * KS) * 4 + kk * 256) >> 4),
+                    const uint64_t ao = (uint64_t)((AOFFC(l) * 4 + kk * 256) >> 4),
                                    bo = (uint64_t)((BREG(l) * 4 + kk * 256) >> 4);
                     const uint64_t ah = dh + ao, al = dl + ao, bh = dh + bo, bl = dl + bo;
                     tc::mma_tf32_ss(d, ah, bh, id, (it > 0 || kk > 0) ? 1u : 0u);
@@ -979,14 +981,15 @@ __global__ void __launch_bounds__(twg::kThreadsWG, 1)
             mb_wait(mb + 2, 0);
             tc::fence_after();
         }
-        float* tr = sm;
-        auto layer = [&](auto lc) {
-            constexpr int l = decltype(lc)::value;
-            constexpr int P = NPAD(l) + 1, NI = NIN(l), NO = NOUT(l);
-            for (int c0 = 0; c0 < NPAD(l); c0 += 8) {
+        float* tr = sm;  // the stage and raw buffers are idle now
+        // chain c: TMEM columns -> tr[128][NPADC + 1] -> the diagonal blocks in master order
+        auto chain = [&](auto cc) {
+            constexpr int c = decltype(cc)::value;
+            constexpr int P = NPADC(c) + 1;
+            for (int c0 = 0; c0 < NPADC(c); c0 += 8) {
                 float v[8];
                 if (stages > 0) {
-                    tc::ld8(tbase + ((uint32_t)(32 * warp) << 16) + (uint32_t)(TCOL(l) + c0), v);
+                    tc::ld8(tbase + ((uint32_t)(32 * warp) << 16) + (uint32_t)(TCOLC(c) + c0), v);
                     tc::wait_ld();
                 } else {
 #pragma unroll
@@ -996,14 +999,22 @@ __global__ void __launch_bounds__(twg::kThreadsWG, 1)
                 for (int j = 0; j < 8; ++j) tr[row * P + c0 + j] = v[j];
             }
             asm volatile("bar.sync 1, 128;" ::: "memory");
-            for (int j = row; j < NO * NI; j += 128) out[MWL(l) + j] = tr[(j / NI) * P + j % NI];
-            for (int n = row; n < NO; n += 128) out[MBL(l) + n] = tr[n * P + NI];
+            // block (rows r0.., columns k0..) of NO x NI, bias in column `bc`
+            auto block = [&](int mw, int mb, int NO, int NI, int r0, int k0, int bc) {
+                for (int j = row; j < NO * NI; j += 128) out[mw + j] = tr[(r0 + j / NI) * P + k0 + j % NI];
+                for (int m = row; m < NO; m += 128) out[mb + m] = tr[(r0 + m) * P + bc];
+            };
+            if constexpr (c == 0) {
+                block(MW1, MB1, 100, 134, 0, 0, 134);
+            } else {
+                block(MW2, MB2, 50, 100, 0, 0, 175);
+                block(MW3, MB3, 25, 50, 50, 100, 175);
+                block(MW4, MB4, 7, 25, 75, 150, 175);
+            }
             asm volatile("bar.sync 1, 128;" ::: "memory");
         };
-        layer(std::integral_constant<int, 0>{});
-        layer(std::integral_constant<int, 1>{});
-        layer(std::integral_constant<int, 2>{});
-        layer(std::integral_constant<int, 3>{});
+        chain(std::integral_constant<int, 0>{});
+        chain(std::integral_constant<int, 1>{});
     }
     tc::fence_before();
     __syncthreads();
