@@ -928,7 +928,7 @@ __global__ void __launch_bounds__(twg::kThreadsWG, 1)
             const int64_t st0 = s_lo / KS;
             for (int it = 0; it < stages; ++it) {
                 const int rb = it % NRAW;
-                if (it >= NRAW) mb_wait(mb + 6 + rb, (uint32_t)(((it / NRAW) - 1) & 1));
+                if (it >= NRAW) mb_wait_spin(mb + 6 + rb, (uint32_t)(((it / NRAW) - 1) & 1));
                 const uint32_t bar = tc::smem_addr(mb + 3 + rb);
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
