@@ -1022,23 +1022,34 @@ __global__ void __launch_bounds__(twg::kThreadsWG, 1)
     if (warp == kLoadWarps) tc::tmem_dealloc<512>(tbase);
 }
 
-__global__ void reduce_partials(const float* __restrict__ partial, int parts,
-                                const double* __restrict__ loss_partial, int loss_parts,
-                                float* __restrict__ grad, double* __restrict__ loss_sum) {
-    // 8 lanes per output: lane j sums parts j, j+8, ... in order, then a fixed
-    // butterfly combines them — deterministic, and 8x the loads in flight
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    const int e = t >> 3, j = t & 7;
+__global__ void __launch_bounds__(256) reduce_partials(const float* __restrict__ partial, int parts,
+                                                    const double* __restrict__ loss_partial,
+                                                    int loss_parts, float* __restrict__ grad,
+                                                    double* __restrict__ loss_sum) {
+    // block = 32 consecutive outputs x 8 slices (warp j sums parts j, j+8, ... in
+    // order; lanes read 128 contiguous bytes per part), then a fixed combination
+    // ((s0+s4)+(s2+s6)) + ((s1+s5)+(s3+s7)) — deterministic
+    __shared__ double red[8][32];
+    const int lane = threadIdx.x & 31, j = threadIdx.x >> 5;
+    const int e = blockIdx.x * 32 + lane;
     double s = 0.0;
-    if (e < kMasterFloats)
+    if (e < kMasterFloats) {
+#pragma unroll 4
         for (int c = j; c < parts; c += 8) s += partial[(int64_t)c * kMasterFloats + e];
-#pragma unroll
-    for (int o = 4; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (e < kMasterFloats && j == 0) grad[e] = (float)s;
-    if (t == 0) {
+    }
+    red[j][lane] = s;
+    __syncthreads();
+    if (j == 0 && e < kMasterFloats) {
+        const double a = (red[0][lane] + red[4][lane]) + (red[2][lane] + red[6][lane]);
+        const double b = (red[1][lane] + red[5][lane]) + (red[3][lane] + red[7][lane]);
+        grad[e] = (float)(a + b);
+    }
+    if (blockIdx.x == 0 && j == 0) {  // loss: lane l sums parts l, l+32, ..., fixed butterfly
         double l = 0.0;
-        for (int c = 0; c < loss_parts; ++c) l += loss_partial[c];
-        *loss_sum = l;
+        for (int c = lane; c < loss_parts; c += 32) l += loss_partial[c];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
+        if (lane == 0) *loss_sum = l;
     }
 }
 
@@ -1194,7 +1205,7 @@ cudaError_t launch_train_grad(Ctx& cx, const float* x, const float* y, int64_t n
         train_wgrad_kernel<<<wg_parts, WG_THREADS, smem_wg, cx.stream>>>(x, ld, act, lds, n, per,
                                                                          partial);
     }
-    reduce_partials<<<(kMasterFloats * 8 + 255) / 256, 256, 0, cx.stream>>>(partial, wg_parts, lp,
+    reduce_partials<<<(kMasterFloats + 31) / 32, 256, 0, cx.stream>>>(partial, wg_parts, lp,
                                                                         fb_parts, grad,
                                                                         loss_sum_dev);
     cx.launches += 3;
