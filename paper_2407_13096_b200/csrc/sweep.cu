@@ -637,20 +637,28 @@ __global__ void __launch_bounds__(128, DSO_ETA_PRUNE_MINB) eta_sweep_pruned_kern
                 } else {
                     const uint32_t w = s_js[g][tid];
                     const int ib = g * kPruneL;
-                    float C[kPruneL], E[kPruneL];
+                    float C[kPruneL], P[kPruneL], T[kPruneL];
 #pragma unroll
                     for (int l = 0; l < kPruneL; ++l) {
                         const float4 t = s_core[min(ib + l, nc - 1)];
                         const float pc = pc_f32(p.p0, p.kp, p.c, t);
-                        const float tb = __fadd_rn(p.t0, __fmul_rn(p.b, t.z));
+                        T[l] = __fadd_rn(p.t0, __fmul_rn(p.b, t.z));
                         const float gj = s_G[(w >> (2 * l)) & 3][tid];
-                        const float P = ta_last > tb ? __int_as_float(0x7fffffff)
-                                                     : __fadd_rn(pc, gj);
-                        C[l] = cost_f32(eta, K, P, tb);
-                        E[l] = __fmul_rn(P, tb);
+                        P[l] = ta_last > T[l] ? __int_as_float(0x7fffffff) : __fadd_rn(pc, gj);
+                        C[l] = cost_f32(eta, K, P[l], T[l]);
                     }
                     const float m = fminf(fmin3(C[0], C[1], C[2]), fmin3(C[3], C[4], fmin3(C[5], C[6], C[7])));
-                    const int pos = prune_pick<kPruneL>(C, E, m);
+                    // usually one slot attains m; energies only when several do
+                    uint32_t eq = 0;
+#pragma unroll
+                    for (int l = 0; l < kPruneL; ++l) eq |= C[l] == m ? 1u << l : 0u;
+                    int pos = __ffs(eq) - 1;
+                    if (eq & (eq - 1)) {
+                        float E[kPruneL];
+#pragma unroll
+                        for (int l = 0; l < kPruneL; ++l) E[l] = __fmul_rn(P[l], T[l]);
+                        pos = prune_pick<kPruneL>(C, E, m);
+                    }
                     bi = min(ib + pos, nc - 1) * NM + (int)((w >> (2 * pos)) & 3);
                     bcost = m;
                 }
