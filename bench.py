@@ -443,10 +443,36 @@ def measure_e2e(ctx, gen, dcgm, cfg, n, csr, steps, tm, world, units):
     for _ in range(k):
         run(hout)
     el = tm.max_over_ranks((time.perf_counter() - t0) / k)
+    probe = pcie_probe(hent if csr else hc)
     return {"value": units * world / el, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(n * 16), "ms_per_step": el * 1e3, "steps": k,
+            "h2d_gbs": h2d / el / 1e9, "link": probe,
+            "link_frac": (h2d / el / 1e9) / probe["h2d_gbs"] if probe.get("h2d_gbs") else None,
             "timing": "host wall clock around synchronous C-ABI calls (dso_pipeline%s with "
                       "DSO_HOST, pinned buffers), max over ranks" % ("_csr" if csr else "")}
+
+
+def pcie_probe(host_buf):
+    """The box's host->device copy bandwidth: plain cudaMemcpy of the same pinned
+    buffer (the PCIe placement varies between boxes; e2e is judged against it)."""
+    import torch
+    try:
+        src = host_buf.view(-1)[: min(host_buf.numel(), 1 << 28)]
+        dst = torch.empty(src.shape, dtype=src.dtype, device="cuda")
+        dst.copy_(src, non_blocking=True)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(3):
+            dst.copy_(src, non_blocking=True)
+        b.record()
+        torch.cuda.synchronize()
+        nbytes = src.numel() * src.element_size()
+        gbs = 3 * nbytes / (a.elapsed_time(b) * 1e-3) / 1e9
+        del dst
+        return {"h2d_gbs": gbs, "bytes": nbytes, "method": "3 x torch copy_ of the pinned entry buffer, CUDA events"}
+    except Exception as e:  # noqa: BLE001
+        return {"error": str(e)[:120]}
 
 
 def measure_eta(ctx, args, rank, world, tm, peak, steps, warmup):
