@@ -122,7 +122,11 @@ __host__ __device__ inline int tc_pos(int slot) {  // slot -> position on the K 
     return 24 + slot - below;
 }
 // shared memory (floats)
-constexpr int kRing = 2;                     // X chunk buffers
+#ifndef DSO_TC_RING
+#define DSO_TC_RING 2
+#endif
+constexpr int kRing = DSO_TC_RING;           // X chunk buffers
+static_assert(kRing <= 3, "ring barriers: MB_XFULL / MB_XEMPTY hold 3 each");
 constexpr int kChunkF = 2 * TT * 8;          // hi [128][8] + lo [128][8] (core-matrix layout)
 constexpr int S_STATS = kModel;              // mean[8] std[8]
 constexpr int S_RING = S_STATS + 16;

@@ -22,7 +22,7 @@ ctx = Context(0)
 ctx.set_option("mlp_engine", 1)
 n = 1 << 22
 for mode in os.environ.get("TC_PHASE_MODES", "pipeline_csr,predict,pipeline").split(","):
-    ctx.set_domain(config_domain("c3"))
+    ctx.set_domain(config_domain(os.environ.get("TC_PHASE_DOMAIN", "c3")))
     m = init_mlp(seed=424242)
     m.target_mean = np.array([60, 10, 0.01, 0.004, 0.15, 200, 200.0])
     m.target_std = np.array([15, 3, 0.005, 0.001, 0.07, 100, 100.0])
