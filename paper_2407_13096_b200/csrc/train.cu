@@ -384,7 +384,8 @@ __device__ __forceinline__ void write_rows(const float* sm, int off, int R, floa
 // deltas D1 | D2 | D3 | D4 then activations A1 | A2 | A3.
 constexpr int SD1 = 0, SD2 = 100, SD3 = 150, SD4 = 175, SA1 = 182, SA2 = 282, SA3 = 332;
 constexpr int kScratchRows = 357;
-constexpr int kScratchAlloc = 504;  // floats per sample: the stage images (>= kScratchRows)
+constexpr int kScratchAlloc = 504;  // floats per sample: the stage images
+static_assert(kScratchAlloc >= kScratchRows, "the scratch holds either layout");
 
 // Stage images for the tensor-core weight gradient (train_tc): per 16-sample
 // stage one contiguous block holding that stage's operands exactly as
@@ -813,10 +814,6 @@ constexpr int ITEMS = wimg::FLOATS / 4;       // float4 items per stage image
 static_assert(KS == wimg::KS, "stage image and MMA stage agree");
 constexpr int PER_T = (ITEMS + kLoadWarps * 32 - 1) / (kLoadWarps * 32);
 
-// element (r, k) of an [R][KS] K-major core-matrix operand
-__host__ __device__ constexpr int cm_off(int r, int k) {
-    return ((r >> 3) * (KS / 4) + (k >> 2)) * 32 + (r & 7) * 4 + (k & 3);
-}
 __device__ __forceinline__ void mb_init(uint64_t* b, int count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(tc::smem_addr(b)), "r"(count)
                  : "memory");
