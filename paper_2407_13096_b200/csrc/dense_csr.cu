@@ -26,6 +26,14 @@ constexpr int kStage = 8192;  // entries of a block gathered in shared memory
 // entries are written (a kernel with more than kPer non-zeros re-reads its
 // column).  status[b]: bits 62-63 = 1 (block aggregate) or 2 (inclusive prefix).
 constexpr int kPer = 24;
+__device__ __forceinline__ uint64_t ld_acquire(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release(unsigned long long* p, uint64_t v) {
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"((unsigned long long)v) : "memory");
+}
 constexpr uint64_t kAgg = 1ull << 62, kPre = 2ull << 62, kVal = (1ull << 62) - 1;
 __global__ void __launch_bounds__(kBlk, DSO_DCSR_MINB) dense_csr_fused_kernel(
     const uint32_t* __restrict__ counts, int64_t n, int64_t ld, uint64_t* __restrict__ row_ptr,
@@ -59,26 +67,32 @@ __global__ void __launch_bounds__(kBlk, DSO_DCSR_MINB) dense_csr_fused_kernel(
     uint32_t excl, agg;
     Scan(s_scan).ExclusiveSum(c, excl, agg);
     const int any_big = __syncthreads_or(big != 0u);
-    if (tid == 0) {
-        if (any_big) atomicOr(flags, 1);
-        uint64_t prefix = 0;
-        if (bid == 0) {
-            __threadfence();
-            atomicExch(status, (unsigned long long)(kPre | agg));
-        } else {
-            atomicExch(status + bid, (unsigned long long)(kAgg | agg));
-            for (int64_t j = (int64_t)bid - 1; j >= 0; --j) {
-                uint64_t st;
-                do {
-                    st = atomicAdd(status + j, 0ull);
-                } while ((st >> 62) == 0);
-                prefix += st & kVal;
-                if ((st >> 62) == 2) break;
-            }
-            __threadfence();
-            atomicExch(status + bid, (unsigned long long)(kPre | (prefix + agg)));
+    if (tid < 32) {
+        // decoupled look-back, one warp: lane l inspects block bid - 1 - l; a step
+        // covers 32 predecessors (the nearest inclusive prefix plus the aggregates
+        // of the blocks after it)
+        const int lane = tid;
+        if (lane == 0) {
+            if (any_big) atomicOr(flags, 1);
+            st_release(status + bid, (bid == 0 ? kPre : kAgg) | agg);
         }
-        s_prefix = prefix;
+        uint64_t prefix = 0;
+        if (bid > 0) {
+            for (int64_t j = (int64_t)bid - 1 - lane;; j -= 32) {
+                uint64_t st = j >= 0 ? ld_acquire(status + j) : kPre;
+                while (__any_sync(0xffffffffu, (st >> 62) == 0))
+                    if ((st >> 62) == 0) st = ld_acquire(status + j);
+                const uint32_t pre = __ballot_sync(0xffffffffu, (st >> 62) == 2);
+                const int first = pre ? __ffs(pre) - 1 : 31;
+                uint64_t v = lane <= first ? (st & kVal) : 0;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                prefix += v;
+                if (pre) break;
+            }
+            if (lane == 0) st_release(status + bid, kPre | (prefix + agg));
+        }
+        if (lane == 0) s_prefix = prefix;
     }
     __syncthreads();
     const uint64_t base = s_prefix;
