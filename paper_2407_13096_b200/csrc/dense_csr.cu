@@ -12,12 +12,15 @@
 namespace dso_b200 {
 namespace {
 
-constexpr int kBlk = 256;
+#ifndef DSO_DCSR_BLK
+#define DSO_DCSR_BLK 256
+#endif
+constexpr int kBlk = DSO_DCSR_BLK;
 
 #ifndef DSO_DCSR_MINB
 #define DSO_DCSR_MINB 6
 #endif
-constexpr int kStage = 8192;  // entries of a block gathered in shared memory
+constexpr int kStage = 32 * kBlk;  // entries of a block gathered in shared memory
 
 // One pass (the default): per block of 256 kernels the counts are read once; each
 // kernel's first kPer entries wait in shared memory while a block scan and a
