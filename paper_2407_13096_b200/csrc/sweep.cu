@@ -37,10 +37,10 @@ constexpr int kBlock = 256;
 #define DSO_ETA_GROUP_UNROLL 1
 #endif
 #ifndef DSO_ETA_PRUNE_MINB
-#define DSO_ETA_PRUNE_MINB 3
+#define DSO_ETA_PRUNE_MINB 4
 #endif
 #ifndef DSO_ETA_PRUNE_CH
-#define DSO_ETA_PRUNE_CH 26
+#define DSO_ETA_PRUNE_CH 34
 #endif
 constexpr int kEtaGroupUnroll = DSO_ETA_GROUP_UNROLL;  // eta-sweep groups per unrolled step
 
