@@ -441,6 +441,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const float* __restrict__ y, int64_t n, int64_t ld,
                     float* __restrict__ scr, int64_t lds, double* __restrict__ loss_partial) {
     extern __shared__ __align__(16) float sm[];
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // programmatic dependent launch
     stage_weights(sm, master);
     __syncthreads();
     const int tid = threadIdx.x;
@@ -873,6 +874,9 @@ __global__ void __launch_bounds__(twg::kThreadsWG, 1)
     __syncthreads();
     tc::fence_after();
     const uint32_t tbase = *tslot;
+    // launched as a programmatic dependent of the forward kernel: the prologue above
+    // overlaps its tail; the stage images are read only after it has completed
+    asm volatile("griddepcontrol.wait;" ::: "memory");
 
     if (warp < kLoadWarps) {
         // ---- loaders: raw stage image -> the hi/lo stage (once the MMAs of the
@@ -1027,6 +1031,7 @@ __global__ void __launch_bounds__(256) reduce_partials(const float* __restrict__
     // order; lanes read 128 contiguous bytes per part), then a fixed combination
     // ((s0+s4)+(s2+s6)) + ((s1+s5)+(s3+s7)) — deterministic
     __shared__ double red[8][32];
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // programmatic dependent launch
     const int lane = threadIdx.x & 31, j = threadIdx.x >> 5;
     const int e = blockIdx.x * 32 + lane;
     double s = 0.0;
@@ -1051,6 +1056,7 @@ __global__ void __launch_bounds__(256) reduce_partials(const float* __restrict__
 }
 
 __global__ void sgd_apply(float* __restrict__ master, const float* __restrict__ grad, float s) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // programmatic dependent launch
     const int e = blockIdx.x * blockDim.x + threadIdx.x;
     if (e < kMasterFloats) master[e] = fmaf(-s, grad[e], master[e]);
 }
@@ -1060,6 +1066,7 @@ __global__ void sgd_apply(float* __restrict__ master, const float* __restrict__ 
 // repack; the image's zero padding is never touched.
 __global__ void sgd_apply_pack(float* __restrict__ master, const float* __restrict__ grad,
                                float s, float* __restrict__ img) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // programmatic dependent launch
     const int e = blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= kMasterFloats) return;
     const float w = fmaf(-s, grad[e], master[e]);
@@ -1134,6 +1141,25 @@ cudaError_t train_prepare(Ctx& cx, int64_t n) {
                             (int)((size_t)2 * WG_CHUNK * WG_REC * sizeof(float)));
 }
 
+// Launch as a programmatic dependent of the previous kernel in the stream: its CTAs
+// may start while the previous grid drains; the kernel calls griddepcontrol.wait
+// before it reads that grid's outputs.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t stream, Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, ((KArgs)args)...);
+}
+
 cudaError_t launch_train_grad(Ctx& cx, const float* x, const float* y, int64_t n, int64_t ld,
                               float* grad, double* loss_sum_dev) {
     if (cx.model.generic) return launch_gen_grad(cx, x, y, n, ld, grad, loss_sum_dev);
@@ -1181,12 +1207,12 @@ cudaError_t launch_train_grad(Ctx& cx, const float* x, const float* y, int64_t n
         ++cx.launches;
         cx.model.train_dirty = false;
     }
-    if (cx.train_tc)
-        train_fb_kernel<true><<<fb_parts, kThreads, smem, cx.stream>>>(cx.model.w_train, x, y, n,
-                                                                       ld, act, lds, lp);
-    else
-        train_fb_kernel<false><<<fb_parts, kThreads, smem, cx.stream>>>(cx.model.w_train, x, y, n,
-                                                                        ld, act, lds, lp);
+    {
+        cudaError_t e = launch_pdl(cx.train_tc ? train_fb_kernel<true> : train_fb_kernel<false>,
+                                   dim3(fb_parts), dim3(kThreads), smem, cx.stream,
+                                   (const float*)cx.model.w_train, x, y, n, ld, act, lds, lp);
+        if (e != cudaSuccess) return e;
+    }
     const int64_t chunks = (n + WG_CHUNK - 1) / WG_CHUNK;
     const int wg_parts = (int)std::max<int64_t>(1, std::min<int64_t>(parts, chunks));
     int64_t per = (n + wg_parts - 1) / wg_parts;
@@ -1196,15 +1222,19 @@ cudaError_t launch_train_grad(Ctx& cx, const float* x, const float* y, int64_t n
         const size_t smem_tc = (size_t)twg::SMEM_FLOATS * sizeof(float);
         cudaError_t e = ensure_smem_attr((const void*)train_wgrad_tc_kernel, cx.device, (int)smem_tc);
         if (e != cudaSuccess) return e;
-        train_wgrad_tc_kernel<<<wg_parts, twg::kThreadsWG, smem_tc, cx.stream>>>(act, n, per,
-                                                                             partial);
+        e = launch_pdl(train_wgrad_tc_kernel, dim3(wg_parts), dim3(twg::kThreadsWG), smem_tc,
+                       cx.stream, (const float*)act, n, per, partial);
+        if (e != cudaSuccess) return e;
     } else {
         train_wgrad_kernel<<<wg_parts, WG_THREADS, smem_wg, cx.stream>>>(x, ld, act, lds, n, per,
                                                                          partial);
     }
-    reduce_partials<<<(kMasterFloats + 31) / 32, 256, 0, cx.stream>>>(partial, wg_parts, lp,
-                                                                        fb_parts, grad,
-                                                                        loss_sum_dev);
+    {
+        cudaError_t e = launch_pdl(reduce_partials, dim3((kMasterFloats + 31) / 32), dim3(256), 0,
+                                   cx.stream, (const float*)partial, wg_parts, (const double*)lp,
+                                   fb_parts, grad, loss_sum_dev);
+        if (e != cudaSuccess) return e;
+    }
     cx.launches += 3;
     return cudaGetLastError();
 }
@@ -1214,12 +1244,14 @@ cudaError_t launch_train_apply(Ctx& cx, const float* grad, float lr_scale, bool 
     if (cx.model.w_train && !cx.model.train_dirty) {
         // update master and the training image together (no repack before the
         // next gradient)
-        sgd_apply_pack<<<(kMasterFloats + 255) / 256, 256, 0, cx.stream>>>(
-            cx.model.w_master, grad, lr_scale, cx.model.w_train);
+        cudaError_t e = launch_pdl(sgd_apply_pack, dim3((kMasterFloats + 255) / 256), dim3(256), 0,
+                                   cx.stream, cx.model.w_master, grad, lr_scale, cx.model.w_train);
+        if (e != cudaSuccess) return e;
     } else {
         cx.model.train_dirty = true;
-        sgd_apply<<<(kMasterFloats + 255) / 256, 256, 0, cx.stream>>>(cx.model.w_master, grad,
-                                                                      lr_scale);
+        cudaError_t e = launch_pdl(sgd_apply, dim3((kMasterFloats + 255) / 256), dim3(256), 0,
+                                   cx.stream, cx.model.w_master, grad, lr_scale);
+        if (e != cudaSuccess) return e;
     }
     ++cx.launches;
     cudaError_t e = cudaGetLastError();
